@@ -1,0 +1,152 @@
+/*
+ * vortex_b200.h — C-ABI of the B200-native retrieval stage (exact inner-product
+ * top-k over a sharded index + ColBERT/PreFLMR MaxSim re-scoring).
+ *
+ * This is the boundary a Vortex deployment binds instead of the simulated
+ * search stage. The reference plugs operators in as
+ *     using ComponentFn = std::function<std::vector<Payload>(const std::vector<Payload>&)>;
+ *     Runtime::register_component(model_id, fn)            (proj/include/vortex/runtime.hpp:179, :202-211)
+ * and today the search stage ("modelD", proj/assets/pipeline.json:7) is only a
+ * profiled latency (proj/include/vortex/executor.hpp:172-182, profiles.csv:17-22).
+ * The C++ adapter in include/vortex_b200_component.hpp wraps these entry points
+ * into exactly that ComponentFn; see INTEGRATION.md for the reference-side
+ * binding.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no exceptions cross this ABI.  Every call
+ *    returns a vx_status; vx_last_error() returns a thread-local message.
+ *  - Host-buffer entry points (vx_search, vx_maxsim, vx_search_rescore) own the
+ *    H2D/D2H copies (through pinned staging) and return when results are on the
+ *    host.  *_dev variants take device pointers and a cudaStream_t (as void*;
+ *    NULL = the handle's own stream) and are asynchronous.
+ *  - Output of a top-k: ids int64 [B][k] and scores float [B][k], ordered by
+ *    score descending, then id ascending.  Missing entries (k > N) are id -1,
+ *    score -INF.
+ *  - Sharded mode (n_shards > 1): one handle per rank/GPU owns rows
+ *    [floor(N*g/G), floor(N*(g+1)/G)).  Rank 0 is the operator: its search
+ *    call broadcasts the batch to the other ranks over NCCL, every rank scans
+ *    its shard and rescoring its local top-k, and the k x G candidates are
+ *    gathered to rank 0 and merged.  Ranks != 0 sit in vx_shard_serve().
+ *  - The library never falls back to the CPU.  If no usable sm_100 device is
+ *    present, vx_index_create fails with VX_ERR_CUDA.
+ */
+#ifndef VORTEX_B200_H_
+#define VORTEX_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VX_ABI_VERSION 1
+
+typedef enum vx_status {
+  VX_OK = 0,
+  VX_ERR_INVALID = 1,     /* bad argument / shape (reference: errc::bad_config) */
+  VX_ERR_CUDA = 2,        /* CUDA runtime / launch failure */
+  VX_ERR_OOM = 3,         /* device allocation failed (reference: errc::out_of_memory) */
+  VX_ERR_NCCL = 4,        /* collective failure */
+  VX_ERR_STATE = 5,       /* call not valid in this handle state (reference: errc::bad_transition) */
+  VX_ERR_UNSUPPORTED = 6  /* shape outside the compiled kernel envelope */
+} vx_status;
+
+typedef struct vx_index vx_index;
+
+/* Scan algorithm selection (vx_set_option VX_OPT_SCAN). */
+enum { VX_SCAN_AUTO = 0, VX_SCAN_F32 = 1, VX_SCAN_TC = 2 };
+/* Options. */
+enum {
+  VX_OPT_SCAN = 1,        /* one of VX_SCAN_* */
+  VX_OPT_GRID = 2,        /* CTAs for the scan (0 = auto: one per SM) */
+  VX_OPT_GRAPHS = 3       /* 1 = replay pre-captured CUDA graphs per batch bucket */
+};
+
+typedef struct vx_index_desc {
+  int64_t n_docs;      /* global document count N (1 <= N < 2^32) */
+  int32_t dim;         /* embedding dimension D (multiple of 32, <= 4096) */
+  int32_t device;      /* CUDA device ordinal used by this handle */
+  int32_t n_shards;    /* G: number of index shards (ranks); 1 = whole index */
+  int32_t shard;       /* g: this handle's shard, 0 <= g < G */
+  int32_t tok_per_doc; /* Nd: late-interaction tokens per document (0 = no token store) */
+  int32_t tok_dim;     /* d: token dimension (multiple of 64 when Nd > 0) */
+  int64_t tok_blocks;  /* T: token-store blocks; document id uses block (id mod T) */
+  int32_t max_batch;   /* largest batch B accepted (workspace sizing) */
+  int32_t max_k;       /* largest k accepted (<= 256) */
+  int32_t max_qtok;    /* largest Nq accepted (<= 128) */
+  int32_t reserved;
+} vx_index_desc;
+
+typedef struct vx_stats {
+  uint64_t kernel_launches;   /* kernels this handle launched since creation / last reset */
+  uint64_t batches;           /* search/maxsim batches served */
+  uint64_t queries;           /* queries served */
+  uint64_t graph_replays;     /* CUDA graph launches */
+  uint64_t cert_fallbacks;    /* queries re-scanned exactly after a failed TC certificate */
+  float last_scan_ms;         /* device time of the last scan kernel (CUDA events) */
+  float last_step_ms;         /* device time of the last whole stage */
+  double scan_ms_total;       /* sum of scan device times sampled by vx_sync */
+  double step_ms_total;       /* sum of stage device times sampled by vx_sync */
+  uint64_t timed_batches;     /* batches whose times were sampled (one per vx_sync) */
+} vx_stats;
+
+int32_t vx_abi_version(void);
+const char* vx_last_error(void);
+
+vx_status vx_index_create(const vx_index_desc* desc, vx_index** out);
+vx_status vx_index_destroy(vx_index* h);
+/* Rows owned by this handle: [*row0, *row0 + *n_local). */
+vx_status vx_index_shard_range(const vx_index* h, int64_t* row0, int64_t* n_local);
+vx_status vx_set_option(vx_index* h, int32_t option, int64_t value);
+vx_status vx_get_stats(const vx_index* h, vx_stats* out);
+vx_status vx_reset_stats(vx_index* h);
+
+/* Fill this shard's rows with the synthetic generator of vx_synth.h (seed). */
+vx_status vx_index_synth(vx_index* h, uint64_t seed);
+/* Upload rows [row0, row0+n) (global ids, must lie inside this shard), fp32 row-major. */
+vx_status vx_index_upload(vx_index* h, const float* rows, int64_t row0, int64_t n);
+/* Copy rows [row0, row0+n) (global ids inside this shard) back to the host. */
+vx_status vx_index_download(const vx_index* h, float* rows, int64_t row0, int64_t n);
+/* Fill the token store with the generator (bf16 of the unit rows, seed). */
+vx_status vx_tokens_synth(vx_index* h, uint64_t seed);
+/* Upload token blocks [blk0, blk0+n): bf16 bits, [n][Nd][d]. */
+vx_status vx_tokens_upload(vx_index* h, const uint16_t* tokens_bf16, int64_t blk0, int64_t n);
+vx_status vx_tokens_download(const vx_index* h, uint16_t* tokens_bf16, int64_t blk0, int64_t n);
+
+/* Exact inner-product top-k of B queries (fp32 [B][D]).  Host buffers. */
+vx_status vx_search(vx_index* h, const float* queries, int32_t B, int32_t k, int64_t* ids,
+                    float* scores);
+/* MaxSim of B queries' tokens (fp32 [B][Nq][d], rounded to bf16) against C
+ * candidate ids per query ([B][C], -1 = skip -> -INF).  Host buffers. */
+vx_status vx_maxsim(vx_index* h, const float* qtok, int32_t B, int32_t nq,
+                    const int64_t* cand, int32_t C, float* out);
+/* The fused stage: top-k by inner product, MaxSim of those k, results ordered
+ * by MaxSim descending (ties: id ascending).  ip/maxsim are [B][k]. */
+vx_status vx_search_rescore(vx_index* h, const float* queries, const float* qtok, int32_t B,
+                            int32_t nq, int32_t k, int64_t* ids, float* ip, float* maxsim);
+
+/* Device-pointer variants (inputs already resident in HBM; asynchronous on stream). */
+vx_status vx_search_dev(vx_index* h, const float* d_queries, int32_t B, int32_t k,
+                        int64_t* d_ids, float* d_scores, void* stream);
+vx_status vx_maxsim_dev(vx_index* h, const float* d_qtok, int32_t B, int32_t nq,
+                        const int64_t* d_cand, int32_t C, float* d_out, void* stream);
+vx_status vx_search_rescore_dev(vx_index* h, const float* d_queries, const float* d_qtok,
+                                int32_t B, int32_t nq, int32_t k, int64_t* d_ids, float* d_ip,
+                                float* d_maxsim, void* stream);
+/* Wait for the handle's work; samples the last batch's scan/stage device times. */
+vx_status vx_sync(vx_index* h);
+
+/* Multi-GPU (one process per GPU).  Rank 0 creates the id, the host plumbing
+ * (torch.distributed / MPI / a file) distributes the 128 bytes, every rank
+ * calls vx_comm_init.  Ranks != 0 then call vx_shard_serve(), which returns
+ * after rank 0 calls vx_shard_stop(). */
+vx_status vx_comm_unique_id(uint8_t out_id[128]);
+vx_status vx_comm_init(vx_index* h, const uint8_t id[128], int32_t nranks, int32_t rank);
+vx_status vx_shard_serve(vx_index* h);
+vx_status vx_shard_stop(vx_index* h);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VORTEX_B200_H_ */

@@ -1,0 +1,302 @@
+// scan_f32.cu — K1: exact fp32 inner-product scan of an index shard fused with a
+// per-CTA top-k (the score matrix never reaches HBM).
+//
+// Replaces the simulated search time of the reference (SimExecutor::execute_batch,
+// proj/include/vortex/executor.hpp:172-182, modelD profile rows
+// proj/assets/profiles.csv:17-22) with the real computation the stage performs.
+//
+// Data path (HBM-streaming, one CTA per SM, persistent):
+//   docs  [n_local][D] fp32 row-major in HBM
+//     --TMA 2-D, box {32 floats, 128 rows} x TD/128, SWIZZLE_128B, L2 evict_first-->
+//   smem ring of NS stages (each TD rows x 128 B)
+//     --conflict-free LDS.128 (the 128B swizzle spreads 8 consecutive rows over
+//       all 32 banks)-->  registers: each thread owns RD docs x RQ queries
+//   queries [BQ][D+4] fp32 resident in smem (padded rows: QL distinct query rows
+//   per LDS.128 land in distinct banks)
+// Arithmetic: every (doc, query) dot product is ONE in-order fmaf chain over the
+// dimension, t = 0..D-1 — the same order as the oracle's VXO_F32 mode, so scores
+// are bit-identical to the CPU reference.
+// Top-k: per tile, scores go to smem; one warp per query filters them against a
+// running threshold (the kcap-th best key so far) into a candidate buffer and
+// compacts it with an in-smem bitonic sort when it could overflow.  At the end
+// each CTA writes its kcap best keys per query; K3 (topk.cu) merges the CTAs.
+// Keys: (order-preserving score bits << 32) | ~local_id, one u64 compare =
+// "score desc, id asc".
+#include <cuda_runtime.h>
+
+#include "vx_internal.cuh"
+#include "vx_ptx.cuh"
+
+namespace vx {
+
+constexpr int kComputeWarps = 8;
+constexpr int kScanThreads = (kComputeWarps + 1) * 32;  // + 1 TMA producer warp
+constexpr int kSmemLimit = 227 * 1024;
+
+template <int RQ, int QL, int RD>
+struct ScanCfg {
+  static constexpr int BQ = RQ * QL;            // queries per launch
+  static constexpr int DL = 32 / QL;            // doc lanes per warp
+  static constexpr int TD = kComputeWarps * DL * RD;  // docs per tile
+  static constexpr int kStageBytes = TD * 128;
+};
+
+struct ScanLayout {
+  size_t ring, qs, sc, cand, thr, cnt, bars, total;
+};
+
+__host__ __device__ static ScanLayout scan_layout(int BQ, int TD, int D, int cap, int ns) {
+  ScanLayout L;
+  size_t off = 0;
+  L.ring = off;  // 1024-aligned by the kernel (base rounded up)
+  off += (size_t)ns * TD * 128;
+  L.qs = off;
+  off += (size_t)BQ * (D + 4) * 4;
+  L.sc = off;
+  off += (size_t)BQ * TD * 4;
+  off = (off + 15) & ~(size_t)15;
+  L.cand = off;
+  off += (size_t)BQ * cap * 8;
+  L.thr = off;
+  off += (size_t)BQ * 8;
+  L.cnt = off;
+  off += (size_t)BQ * 4;
+  off = (off + 7) & ~(size_t)7;
+  L.bars = off;
+  off += (size_t)ns * 2 * 8;
+  L.total = off + 1024;  // slack for aligning the ring base
+  return L;
+}
+
+template <int RQ, int QL, int RD>
+__global__ void __launch_bounds__(kScanThreads, 1)
+    scan_f32_kernel(const __grid_constant__ CUtensorMap tmap, const ScanF32Args a) {
+  using C = ScanCfg<RQ, QL, RD>;
+  constexpr int BQ = C::BQ, DL = C::DL, TD = C::TD;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  const int D = a.D, QS = a.D + 4, ns = a.ns, cap = a.cap, kcap = a.kcap;
+  const ScanLayout L = scan_layout(BQ, TD, D, cap, ns);
+  uint8_t* ring = smem + L.ring;
+  float* q_s = reinterpret_cast<float*>(smem + L.qs);
+  float* sc_s = reinterpret_cast<float*>(smem + L.sc);
+  uint64_t* cand = reinterpret_cast<uint64_t*>(smem + L.cand);
+  uint64_t* thr_s = reinterpret_cast<uint64_t*>(smem + L.thr);
+  int* cnt_s = reinterpret_cast<int*>(smem + L.cnt);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
+  uint64_t* empty = full + ns;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nch = D >> 5;
+  const uint32_t n_local = a.n_local;
+  const int ntiles = (int)((n_local + TD - 1) / TD);
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmap);
+    for (int s = 0; s < ns; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kComputeWarps);
+    }
+    fence_barrier_init();
+  }
+  for (int i = threadIdx.x; i < BQ * D; i += blockDim.x) {
+    int qi = i / D, t = i - qi * D;
+    q_s[qi * QS + t] = (qi < a.B) ? a.q[(size_t)qi * D + t] : 0.0f;
+  }
+  for (int i = threadIdx.x; i < BQ; i += blockDim.x) {
+    thr_s[i] = 0ull;
+    cnt_s[i] = 0;
+  }
+  __syncthreads();
+
+  if (warp == kComputeWarps) {
+    // ---------------- TMA producer (one elected lane)
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      int s = 0;
+      uint32_t ph = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (int c = 0; c < nch; ++c) {
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], C::kStageBytes);
+#pragma unroll
+          for (int h = 0; h < TD; h += 128)
+            tma_load_2d(ring + (size_t)s * C::kStageBytes + h * 128, &tmap, &full[s], c * 32,
+                        tile * TD + h, pol);
+          if (++s == ns) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- compute warps
+  const int dl = lane / QL, qlid = lane % QL;
+  int s = 0;
+  uint32_t ph = 0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    float acc[RD][RQ];
+#pragma unroll
+    for (int j = 0; j < RD; ++j)
+#pragma unroll
+      for (int i = 0; i < RQ; ++i) acc[j][i] = 0.0f;
+
+    for (int c = 0; c < nch; ++c) {
+      mbar_wait(&full[s], ph);
+      const uint8_t* st = ring + (size_t)s * C::kStageBytes;
+      const float* qc = q_s + c * 32;
+#pragma unroll
+      for (int c4 = 0; c4 < 8; ++c4) {
+        float4 dv[RD];
+#pragma unroll
+        for (int j = 0; j < RD; ++j) {
+          const int r = warp * (DL * RD) + j * DL + dl;
+          dv[j] = *reinterpret_cast<const float4*>(st + r * 128 + ((c4 ^ (r & 7)) << 4));
+        }
+#pragma unroll
+        for (int i = 0; i < RQ; ++i) {
+          const int qi = i * QL + qlid;
+          const float4 qv = *reinterpret_cast<const float4*>(qc + qi * QS + c4 * 4);
+#pragma unroll
+          for (int j = 0; j < RD; ++j) {
+            acc[j][i] = fmaf(dv[j].x, qv.x, acc[j][i]);
+            acc[j][i] = fmaf(dv[j].y, qv.y, acc[j][i]);
+            acc[j][i] = fmaf(dv[j].z, qv.z, acc[j][i]);
+            acc[j][i] = fmaf(dv[j].w, qv.w, acc[j][i]);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == ns) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+
+    // scores of this tile -> smem (previous tile's selection must be done)
+    named_bar_sync(1, kComputeWarps * 32);
+#pragma unroll
+    for (int j = 0; j < RD; ++j) {
+      const int r = warp * (DL * RD) + j * DL + dl;
+#pragma unroll
+      for (int i = 0; i < RQ; ++i) sc_s[(i * QL + qlid) * TD + r] = acc[j][i];
+    }
+    named_bar_sync(1, kComputeWarps * 32);
+
+    // selection: one warp per query
+    for (int qi = warp; qi < a.B; qi += kComputeWarps) {
+      uint64_t* cb = cand + (size_t)qi * cap;
+      int cnt = cnt_s[qi];
+      uint64_t thr = thr_s[qi];
+      const float* sq = sc_s + qi * TD;
+      for (int base = 0; base < TD; base += 32) {
+        const uint32_t doc = (uint32_t)tile * TD + base + lane;
+        const uint64_t key = (doc < n_local) ? vx_make_key(sq[base + lane], doc) : 0ull;
+        bool pass = key > thr;
+        unsigned m = __ballot_sync(0xffffffffu, pass);
+        if (m == 0) continue;
+        int n = __popc(m);
+        if (cnt + n > cap) {
+          for (int i = cnt + lane; i < cap; i += 32) cb[i] = 0ull;
+          __syncwarp();
+          warp_bitonic_desc(cb, cap);
+          cnt = min(cnt, kcap);
+          thr = cnt >= kcap ? cb[kcap - 1] : 0ull;
+          pass = key > thr;
+          m = __ballot_sync(0xffffffffu, pass);
+          n = __popc(m);
+        }
+        if (pass) cb[cnt + __popc(m & ((1u << lane) - 1u))] = key;
+        cnt += n;
+        __syncwarp();
+      }
+      if (lane == 0) {
+        cnt_s[qi] = cnt;
+        thr_s[qi] = thr;
+      }
+      __syncwarp();
+    }
+  }
+
+  // final per-CTA lists
+  named_bar_sync(1, kComputeWarps * 32);
+  for (int qi = warp; qi < a.B; qi += kComputeWarps) {
+    uint64_t* cb = cand + (size_t)qi * cap;
+    const int cnt = cnt_s[qi];
+    for (int i = cnt + lane; i < cap; i += 32) cb[i] = 0ull;
+    __syncwarp();
+    warp_bitonic_desc(cb, cap);
+    uint64_t* out = a.part + ((size_t)qi * gridDim.x + blockIdx.x) * kcap;
+    for (int i = lane; i < kcap; i += 32) out[i] = cb[i];
+  }
+}
+
+// ---------------------------------------------------------------- host side
+
+#define VX_SCAN_CONFIGS(X) \
+  X(1, 1, 1, 1)            \
+  X(2, 1, 2, 1)            \
+  X(4, 2, 2, 1)            \
+  X(8, 4, 2, 1)            \
+  X(16, 4, 4, 2)           \
+  X(32, 8, 4, 2)
+
+int scan_f32_bucket(int B) {
+  if (B <= 1) return 1;
+  if (B <= 2) return 2;
+  if (B <= 4) return 4;
+  if (B <= 8) return 8;
+  if (B <= 16) return 16;
+  return 32;
+}
+
+int scan_f32_tile_docs(int bucket) {
+#define X(BK, RQ, QL, RD) \
+  if (bucket == BK) return ScanCfg<RQ, QL, RD>::TD;
+  VX_SCAN_CONFIGS(X)
+#undef X
+  return 0;
+}
+
+size_t scan_f32_smem(int bucket, int D, int kcap, int* ns_out, int* cap_out) {
+  int TD = scan_f32_tile_docs(bucket);
+  if (!TD) return 0;
+  int cap = 2 * kcap > kcap + 32 ? 2 * kcap : kcap + 32;
+  // cap must be a power of two for the bitonic sort
+  int p2 = 1;
+  while (p2 < cap) p2 <<= 1;
+  cap = p2;
+  int ns = 8;
+  while (ns >= 2) {
+    ScanLayout L = scan_layout(bucket, TD, D, cap, ns);
+    if (L.total <= (size_t)kSmemLimit && (size_t)ns * TD * 128 <= 160 * 1024) {
+      *ns_out = ns;
+      *cap_out = cap;
+      return L.total;
+    }
+    --ns;
+  }
+  return 0;
+}
+
+cudaError_t launch_scan_f32(int bucket, const CUtensorMap* tmap, const ScanF32Args& a, int grid,
+                            size_t smem, cudaStream_t st) {
+#define X(BK, RQ, QL, RD)                                                                      \
+  if (bucket == BK) {                                                                          \
+    auto kfn = scan_f32_kernel<RQ, QL, RD>;                                                    \
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                                         (int)smem);                                           \
+    if (e != cudaSuccess) return e;                                                            \
+    kfn<<<grid, kScanThreads, smem, st>>>(*tmap, a);                                           \
+    return cudaGetLastError();                                                                 \
+  }
+  VX_SCAN_CONFIGS(X)
+#undef X
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace vx

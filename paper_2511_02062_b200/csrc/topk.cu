@@ -1,0 +1,184 @@
+// topk.cu — K3: merge of per-CTA (or per-shard) candidate key lists into the
+// final per-query top-k, and the MaxSim re-ordering of the stage output.
+//
+// One CTA per query.  MSB-first radix select over the u64 keys (8-bit digits,
+// histogram in smem) narrows to the bin holding the k-th key — usually 2-3 passes
+// over the M = P*kcap candidates, which are L2-resident — then one collection
+// pass gathers exactly k keys and a block bitonic sort orders them
+// (score desc, id asc; the key encodes both, vx_synth.h vx_make_key).
+// Padding keys (0) rank below every real key and come out as id -1 / -INF.
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "vx_internal.cuh"
+#include "vx_ptx.cuh"
+
+namespace vx {
+
+constexpr int kMergeThreads = 512;
+constexpr int kMaxK = 256;
+
+__device__ __forceinline__ void block_bitonic_desc(uint64_t* buf, int n) {
+  for (int size = 2; size <= n; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < (n >> 1); i += blockDim.x) {
+        int lo = 2 * i - (i & (stride - 1));
+        int hi = lo + stride;
+        bool desc = (lo & size) == 0;
+        uint64_t a = buf[lo], b = buf[hi];
+        if ((a < b) == desc) {
+          buf[lo] = b;
+          buf[hi] = a;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kMergeThreads)
+    merge_topk_kernel(const uint64_t* __restrict__ in, int M, int k, int64_t id_base,
+                      uint64_t* __restrict__ out_keys, int64_t* __restrict__ out_ids,
+                      float* __restrict__ out_scores) {
+  __shared__ uint32_t hist[256];
+  __shared__ uint64_t s_prefix, s_mask;
+  __shared__ int s_kk, s_done, s_above, s_eq;
+  __shared__ uint64_t sel[kMaxK];
+  const uint64_t* L = in + (size_t)blockIdx.x * M;
+
+  uint64_t prefix = 0, mask = 0;
+  int kk = k;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < M; i += blockDim.x) {
+      uint64_t key = L[i];
+      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int above = 0, d = 255;
+      for (; d > 0; --d) {
+        if (above + (int)hist[d] >= kk) break;
+        above += hist[d];
+      }
+      s_prefix = prefix | ((uint64_t)d << shift);
+      s_mask = mask | (0xFFull << shift);
+      s_kk = kk - above;
+      s_done = ((int)hist[d] == kk - above);
+    }
+    __syncthreads();
+    prefix = s_prefix;
+    mask = s_mask;
+    kk = s_kk;
+    if (s_done) break;
+    __syncthreads();
+  }
+  int kp = 16;
+  while (kp < k) kp <<= 1;
+  for (int i = threadIdx.x; i < kp; i += blockDim.x) sel[i] = 0ull;
+  if (threadIdx.x == 0) {
+    s_above = 0;
+    s_eq = 0;
+  }
+  __syncthreads();
+  const int n_above = k - kk;
+  for (int i = threadIdx.x; i < M; i += blockDim.x) {
+    uint64_t key = L[i];
+    uint64_t m = key & mask;
+    if (m > prefix) {
+      int slot = atomicAdd(&s_above, 1);
+      sel[slot] = key;
+    } else if (m == prefix) {
+      int slot = atomicAdd(&s_eq, 1);
+      if (slot < kk) sel[n_above + slot] = key;
+    }
+  }
+  __syncthreads();
+  block_bitonic_desc(sel, kp);
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    uint64_t key = sel[i];
+    size_t o = (size_t)blockIdx.x * k + i;
+    if (key == 0ull) {
+      if (out_keys) out_keys[o] = 0ull;
+      if (out_ids) out_ids[o] = -1;
+      if (out_scores) out_scores[o] = -INFINITY;
+    } else {
+      int64_t gid = (int64_t)vx_key_id(key) + id_base;
+      if (out_keys)
+        out_keys[o] = (key & 0xFFFFFFFF00000000ull) | (uint64_t)(0xFFFFFFFFu - (uint32_t)gid);
+      if (out_ids) out_ids[o] = gid;
+      if (out_scores) out_scores[o] = vx_key_score(key);
+    }
+  }
+}
+
+cudaError_t launch_merge_topk(const uint64_t* in, int B, int M, int k, int64_t id_base,
+                              uint64_t* out_keys, int64_t* out_ids, float* out_scores,
+                              cudaStream_t st) {
+  if (k < 1 || k > kMaxK || M < k) return cudaErrorInvalidValue;
+  merge_topk_kernel<<<B, kMergeThreads, 0, st>>>(in, M, k, id_base, out_keys, out_ids,
+                                                 out_scores);
+  return cudaGetLastError();
+}
+
+// Stage output order: MaxSim descending, then id ascending.  k <= 256, one CTA per query.
+__global__ void __launch_bounds__(256)
+    order_by_kernel(const float* __restrict__ ms, const int64_t* __restrict__ ids,
+                    const float* __restrict__ ip, int k, int64_t* __restrict__ out_ids,
+                    float* __restrict__ out_ip, float* __restrict__ out_ms) {
+  __shared__ uint64_t buf[kMaxK];
+  __shared__ float s_ip[kMaxK], s_ms[kMaxK];
+  __shared__ int64_t s_id[kMaxK];
+  int kp = 16;
+  while (kp < k) kp <<= 1;
+  const size_t base = (size_t)blockIdx.x * k;
+  for (int i = threadIdx.x; i < kp; i += blockDim.x) {
+    uint64_t key = 0ull;
+    if (i < k) {
+      int64_t id = ids[base + i];
+      s_ip[i] = ip[base + i];
+      s_ms[i] = ms[base + i];
+      s_id[i] = id;
+      // position i is carried in the low bits; ties on MaxSim resolve by id
+      // because the IP top-k list is id-unique and we rank (ms desc, id asc).
+      if (id >= 0) {
+        uint32_t ord = vx_order_f32(ms[base + i]);
+        key = ((uint64_t)ord << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)id);
+      }
+    }
+    buf[i] = key;
+  }
+  __syncthreads();
+  block_bitonic_desc(buf, kp);
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    uint64_t key = buf[i];
+    if (key == 0ull) {
+      out_ids[base + i] = -1;
+      out_ip[base + i] = -INFINITY;
+      out_ms[base + i] = -INFINITY;
+      continue;
+    }
+    uint32_t id32 = 0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFu);
+    // find the source slot (k <= 256: linear scan of smem)
+    int src = 0;
+    for (int j = 0; j < k; ++j)
+      if (s_id[j] >= 0 && (uint32_t)s_id[j] == id32) {
+        src = j;
+        break;
+      }
+    out_ids[base + i] = s_id[src];
+    out_ip[base + i] = s_ip[src];
+    out_ms[base + i] = s_ms[src];
+  }
+}
+
+cudaError_t launch_order_by(const float* key_score, const int64_t* ids, const float* ip, int B,
+                            int k, int64_t* out_ids, float* out_ip, float* out_ms,
+                            cudaStream_t st) {
+  if (k < 1 || k > kMaxK) return cudaErrorInvalidValue;
+  order_by_kernel<<<B, 256, 0, st>>>(key_score, ids, ip, k, out_ids, out_ip, out_ms);
+  return cudaGetLastError();
+}
+
+}  // namespace vx

@@ -1,0 +1,793 @@
+// vx_api.cu — the C-ABI (include/vortex_b200.h): index handles, device memory,
+// streams, the per-batch stage pipeline and the NCCL shard exchange.
+//
+// The stage a deployment registers as the search operator (reference:
+// ComponentFn, proj/include/vortex/runtime.hpp:179; invoked by
+// Runtime::complete_batch, runtime.hpp:656-672) runs, per batch of B queries:
+//   [H2D queries]  -> K1 scan + per-CTA top-k  -> K3 merge (local top-k)
+//   -> K4 MaxSim of the local top-k -> [NCCL gather k x G to rank 0 -> merge]
+//   -> order by MaxSim -> [D2H]
+// Shard mode mirrors the reference's key->shard placement (kvs.hpp:160-175):
+// contiguous document ranges, a document's row and its token block on one GPU.
+// No CPU fallback: every entry point fails loudly without a usable device.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+#include <stdarg.h>
+#include <stdlib.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/vortex_b200.h"
+#include "vx_internal.cuh"
+
+// ---------------------------------------------------------------- NCCL (loaded lazily)
+// NCCL is dlopen'ed on first use instead of linked: a host process (e.g. PyTorch) may
+// already carry its own libnccl.so.2, and two copies under one soname break each other.
+// Order: an already-loaded libnccl.so.2, $VX_NCCL_LIB, then the system library.
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*CommDestroy)(ncclComm_t);
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                            cudaStream_t);
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*GroupStart)();
+  ncclResult_t (*GroupEnd)();
+  const char* (*GetErrorString)(ncclResult_t);
+  bool ok = false;
+};
+
+static NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    const char* env = getenv("VX_NCCL_LIB");
+    if (!h && env && *env) h = dlopen(env, RTLD_NOW | RTLD_LOCAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!h) return;
+#define SYM(field, name) api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, name))
+    SYM(GetUniqueId, "ncclGetUniqueId");
+    SYM(CommInitRank, "ncclCommInitRank");
+    SYM(CommDestroy, "ncclCommDestroy");
+    SYM(Broadcast, "ncclBroadcast");
+    SYM(Send, "ncclSend");
+    SYM(Recv, "ncclRecv");
+    SYM(GroupStart, "ncclGroupStart");
+    SYM(GroupEnd, "ncclGroupEnd");
+    SYM(GetErrorString, "ncclGetErrorString");
+#undef SYM
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Broadcast &&
+             api.Send && api.Recv && api.GroupStart && api.GroupEnd && api.GetErrorString;
+  });
+  return api;
+}
+
+// ---------------------------------------------------------------- errors
+static thread_local std::string g_err;
+
+static vx_status fail(vx_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define CU_TRY(expr)                                                                     \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess)                                                               \
+      return fail(_e == cudaErrorMemoryAllocation ? VX_ERR_OOM : VX_ERR_CUDA, "%s: %s (%s:%d)", \
+                  #expr, cudaGetErrorString(_e), __FILE__, __LINE__);                    \
+  } while (0)
+
+#define NCCL_TRY(expr)                                                                    \
+  do {                                                                                    \
+    ncclResult_t _r = (expr);                                                             \
+    if (_r != ncclSuccess)                                                                \
+      return fail(VX_ERR_NCCL, "%s: %s (%s:%d)", #expr, nccl().GetErrorString(_r), __FILE__, \
+                  __LINE__);                                                              \
+  } while (0)
+
+#define VX_TRY(expr)                 \
+  do {                               \
+    vx_status _s = (expr);           \
+    if (_s != VX_OK) return _s;      \
+  } while (0)
+
+// ---------------------------------------------------------------- tensor maps
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                    CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  });
+  return fn;
+}
+
+// 2-D row-major matrix [rows][cols] of `elem` bytes, box {box_cols, box_rows}, 128B swizzle.
+static vx_status make_tmap_2d(CUtensorMap* m, const void* base, CUtensorMapDataType dt,
+                              int elem, uint64_t rows, uint64_t cols, uint32_t box_cols,
+                              uint32_t box_rows) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return fail(VX_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * (uint64_t)elem};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(VX_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return VX_OK;
+}
+
+// ---------------------------------------------------------------- handle
+struct ShardRec {  // one gathered candidate of the shard exchange
+  uint64_t key;    // (ip order bits, ~global id)
+  float ms;
+  float pad;
+};
+
+struct vx_index {
+  vx_index_desc desc{};
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  int64_t row0 = 0, n_local = 0;
+  float* docs = nullptr;
+  uint16_t* tokens = nullptr;
+  CUtensorMap tmap_docs{};
+  // options
+  int scan_algo = VX_SCAN_AUTO;
+  int grid = 0;
+  // workspace
+  float* d_q = nullptr;          // [maxB][D]
+  float* d_qtok = nullptr;       // [maxB][maxNq][d]
+  uint64_t* d_part = nullptr;    // [maxB][grid][256]
+  uint64_t* d_keys = nullptr;    // [maxB][maxK]
+  int64_t* d_ids = nullptr;      // [maxB][maxK]
+  float* d_ip = nullptr;         // [maxB][maxK]
+  float* d_ms = nullptr;         // [maxB][maxK]
+  int64_t* d_out_ids = nullptr;  // [maxB][maxK]
+  float* d_out_ip = nullptr;
+  float* d_out_ms = nullptr;
+  ShardRec* d_send = nullptr;    // [maxB][maxK]
+  ShardRec* d_recv = nullptr;    // [G][maxB][maxK]  (rank 0)
+  int32_t* d_hdr = nullptr;      // [4]
+  // pinned host staging
+  void* h_stage = nullptr;
+  size_t h_stage_bytes = 0;
+  int32_t* h_hdr = nullptr;
+  // comm
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  // stats
+  vx_stats st{};
+  cudaEvent_t ev[4] = {};
+  bool timing_pending = false;
+};
+
+static void count_launch(vx_index* h, int n = 1) { h->st.kernel_launches += n; }
+
+extern "C" int32_t vx_abi_version(void) { return VX_ABI_VERSION; }
+extern "C" const char* vx_last_error(void) { return g_err.c_str(); }
+
+static int next_pow2(int x) {
+  int p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+static int kcap_of(int k) { return std::max(16, next_pow2(k)); }
+
+extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
+  if (!d || !out) return fail(VX_ERR_INVALID, "null argument");
+  *out = nullptr;
+  if (d->n_docs < 1 || d->n_docs >= (int64_t)0xFFFFFFFFll)
+    return fail(VX_ERR_INVALID, "n_docs must be in [1, 2^32-1)");
+  if (d->dim < 32 || d->dim > 4096 || d->dim % 32)
+    return fail(VX_ERR_INVALID, "dim must be a multiple of 32 in [32, 4096]");
+  if (d->n_shards < 1 || d->shard < 0 || d->shard >= d->n_shards)
+    return fail(VX_ERR_INVALID, "bad shard %d of %d", d->shard, d->n_shards);
+  if (d->max_batch < 1 || d->max_k < 1 || d->max_k > 256)
+    return fail(VX_ERR_INVALID, "max_batch >= 1 and 1 <= max_k <= 256 required");
+  if (d->tok_per_doc < 0 || (d->tok_per_doc > 0 && (d->tok_dim < 16 || d->tok_dim % 16 ||
+                                                    d->tok_blocks < 1 || d->max_qtok < 1 ||
+                                                    d->max_qtok > 128)))
+    return fail(VX_ERR_INVALID, "bad token-store shape");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(VX_ERR_CUDA, "no CUDA device visible (the B200 path has no CPU fallback)");
+  if (d->device < 0 || d->device >= ndev) return fail(VX_ERR_INVALID, "device %d", d->device);
+  cudaDeviceProp prop;
+  CU_TRY(cudaGetDeviceProperties(&prop, d->device));
+  if (prop.major != 10)
+    return fail(VX_ERR_CUDA, "device %d is sm_%d%d; this build targets sm_100a", d->device,
+                prop.major, prop.minor);
+  vx_index* h = new vx_index();
+  h->desc = *d;
+  h->device = d->device;
+  h->num_sms = prop.multiProcessorCount;
+  h->row0 = (d->n_docs * d->shard) / d->n_shards;
+  h->n_local = (d->n_docs * (d->shard + 1)) / d->n_shards - h->row0;
+  vx_status s = VX_OK;
+  auto cleanup = [&](vx_status e) {
+    vx_index_destroy(h);
+    return e;
+  };
+  if (cudaSetDevice(h->device) != cudaSuccess) return cleanup(fail(VX_ERR_CUDA, "cudaSetDevice"));
+  if (h->n_local < 1) return cleanup(fail(VX_ERR_INVALID, "empty shard"));
+#define ALLOC(ptr, bytes)                                                              \
+  do {                                                                                 \
+    cudaError_t _e = cudaMalloc((void**)&(ptr), (bytes));                              \
+    if (_e != cudaSuccess)                                                             \
+      return cleanup(fail(VX_ERR_OOM, "cudaMalloc %zu bytes: %s", (size_t)(bytes),       \
+                          cudaGetErrorString(_e)));                                    \
+  } while (0)
+  const size_t D = d->dim, B = d->max_batch, K = d->max_k;
+  ALLOC(h->docs, (size_t)h->n_local * D * 4);
+  if (d->tok_per_doc > 0)
+    ALLOC(h->tokens, (size_t)d->tok_blocks * d->tok_per_doc * d->tok_dim * 2);
+  h->grid = h->num_sms;
+  ALLOC(h->d_q, B * D * 4);
+  if (d->tok_per_doc > 0) ALLOC(h->d_qtok, B * d->max_qtok * d->tok_dim * 4);
+  ALLOC(h->d_part, B * (size_t)h->grid * 256 * 8);
+  ALLOC(h->d_keys, B * K * 8);
+  ALLOC(h->d_ids, B * K * 8);
+  ALLOC(h->d_ip, B * K * 4);
+  ALLOC(h->d_ms, B * K * 4);
+  ALLOC(h->d_out_ids, B * K * 8);
+  ALLOC(h->d_out_ip, B * K * 4);
+  ALLOC(h->d_out_ms, B * K * 4);
+  ALLOC(h->d_send, B * K * sizeof(ShardRec));
+  if (d->n_shards > 1 && d->shard == 0)
+    ALLOC(h->d_recv, (size_t)d->n_shards * B * K * sizeof(ShardRec));
+  ALLOC(h->d_hdr, 16);
+#undef ALLOC
+  if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess)
+    return cleanup(fail(VX_ERR_CUDA, "stream create"));
+  for (auto& e : h->ev)
+    if (cudaEventCreate(&e) != cudaSuccess) return cleanup(fail(VX_ERR_CUDA, "event create"));
+  h->h_stage_bytes = B * D * 4 + (d->tok_per_doc > 0 ? B * d->max_qtok * d->tok_dim * 4 : 0) +
+                     B * K * 16 + 64;
+  if (cudaMallocHost(&h->h_stage, h->h_stage_bytes) != cudaSuccess)
+    return cleanup(fail(VX_ERR_OOM, "pinned staging"));
+  if (cudaMallocHost((void**)&h->h_hdr, 16) != cudaSuccess)
+    return cleanup(fail(VX_ERR_OOM, "pinned header"));
+  s = make_tmap_2d(&h->tmap_docs, h->docs, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                   (uint64_t)h->n_local, D, 32, 128);
+  if (s != VX_OK) return cleanup(s);
+  *out = h;
+  return VX_OK;
+}
+
+extern "C" vx_status vx_index_destroy(vx_index* h) {
+  if (!h) return VX_OK;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->comm) nccl().CommDestroy(h->comm);
+  void* ptrs[] = {h->docs,  h->tokens,    h->d_q,      h->d_qtok,    h->d_part, h->d_keys,
+                  h->d_ids, h->d_ip,      h->d_ms,     h->d_out_ids, h->d_out_ip,
+                  h->d_out_ms, h->d_send, h->d_recv, h->d_hdr};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (h->h_stage) cudaFreeHost(h->h_stage);
+  if (h->h_hdr) cudaFreeHost(h->h_hdr);
+  for (auto& e : h->ev)
+    if (e) cudaEventDestroy(e);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+  return VX_OK;
+}
+
+extern "C" vx_status vx_index_shard_range(const vx_index* h, int64_t* row0, int64_t* n_local) {
+  if (!h) return fail(VX_ERR_INVALID, "null handle");
+  if (row0) *row0 = h->row0;
+  if (n_local) *n_local = h->n_local;
+  return VX_OK;
+}
+
+extern "C" vx_status vx_set_option(vx_index* h, int32_t option, int64_t value) {
+  if (!h) return fail(VX_ERR_INVALID, "null handle");
+  switch (option) {
+    case VX_OPT_SCAN:
+      if (value != VX_SCAN_AUTO && value != VX_SCAN_F32 && value != VX_SCAN_TC)
+        return fail(VX_ERR_INVALID, "scan algorithm %lld", (long long)value);
+      if (value == VX_SCAN_TC) return fail(VX_ERR_UNSUPPORTED, "tensor-core scan not built yet");
+      h->scan_algo = (int)value;
+      return VX_OK;
+    case VX_OPT_GRID:
+      if (value < 0 || value > h->num_sms) return fail(VX_ERR_INVALID, "grid %lld", (long long)value);
+      h->grid = value == 0 ? h->num_sms : (int)value;
+      return VX_OK;
+    case VX_OPT_GRAPHS:
+      return value == 0 ? VX_OK : fail(VX_ERR_UNSUPPORTED, "graphs not built yet");
+    default:
+      return fail(VX_ERR_INVALID, "unknown option %d", option);
+  }
+}
+
+extern "C" vx_status vx_get_stats(const vx_index* h, vx_stats* out) {
+  if (!h || !out) return fail(VX_ERR_INVALID, "null argument");
+  *out = h->st;
+  return VX_OK;
+}
+extern "C" vx_status vx_reset_stats(vx_index* h) {
+  if (!h) return fail(VX_ERR_INVALID, "null handle");
+  h->st = vx_stats{};
+  return VX_OK;
+}
+
+extern "C" vx_status vx_index_synth(vx_index* h, uint64_t seed) {
+  if (!h) return fail(VX_ERR_INVALID, "null handle");
+  CU_TRY(cudaSetDevice(h->device));
+  CU_TRY(vx::launch_synth_rows(h->docs, seed, h->row0, h->n_local, h->desc.dim, h->stream));
+  count_launch(h);
+  CU_TRY(cudaStreamSynchronize(h->stream));
+  return VX_OK;
+}
+
+extern "C" vx_status vx_index_upload(vx_index* h, const float* rows, int64_t row0, int64_t n) {
+  if (!h || (!rows && n > 0)) return fail(VX_ERR_INVALID, "null argument");
+  if (row0 < h->row0 || n < 0 || row0 + n > h->row0 + h->n_local)
+    return fail(VX_ERR_INVALID, "rows [%lld,%lld) outside shard [%lld,%lld)", (long long)row0,
+                (long long)(row0 + n), (long long)h->row0, (long long)(h->row0 + h->n_local));
+  CU_TRY(cudaSetDevice(h->device));
+  CU_TRY(cudaMemcpyAsync(h->docs + (row0 - h->row0) * h->desc.dim, rows,
+                         (size_t)n * h->desc.dim * 4, cudaMemcpyHostToDevice, h->stream));
+  CU_TRY(cudaStreamSynchronize(h->stream));
+  return VX_OK;
+}
+
+extern "C" vx_status vx_index_download(const vx_index* h, float* rows, int64_t row0, int64_t n) {
+  if (!h || (!rows && n > 0)) return fail(VX_ERR_INVALID, "null argument");
+  if (row0 < h->row0 || n < 0 || row0 + n > h->row0 + h->n_local)
+    return fail(VX_ERR_INVALID, "rows outside shard");
+  CU_TRY(cudaSetDevice(h->device));
+  CU_TRY(cudaMemcpyAsync(rows, h->docs + (row0 - h->row0) * h->desc.dim,
+                         (size_t)n * h->desc.dim * 4, cudaMemcpyDeviceToHost, h->stream));
+  CU_TRY(cudaStreamSynchronize(h->stream));
+  return VX_OK;
+}
+
+extern "C" vx_status vx_tokens_download(const vx_index* h, uint16_t* tok, int64_t blk0, int64_t n) {
+  if (!h || (!tok && n > 0)) return fail(VX_ERR_INVALID, "null argument");
+  if (!h->tokens) return fail(VX_ERR_STATE, "index has no token store");
+  if (blk0 < 0 || n < 0 || blk0 + n > h->desc.tok_blocks)
+    return fail(VX_ERR_INVALID, "token blocks out of range");
+  const size_t blk = (size_t)h->desc.tok_per_doc * h->desc.tok_dim;
+  CU_TRY(cudaSetDevice(h->device));
+  CU_TRY(cudaMemcpyAsync(tok, h->tokens + blk0 * blk, n * blk * 2, cudaMemcpyDeviceToHost,
+                         h->stream));
+  CU_TRY(cudaStreamSynchronize(h->stream));
+  return VX_OK;
+}
+
+extern "C" vx_status vx_tokens_synth(vx_index* h, uint64_t seed) {
+  if (!h) return fail(VX_ERR_INVALID, "null handle");
+  if (!h->tokens) return fail(VX_ERR_STATE, "index has no token store");
+  CU_TRY(cudaSetDevice(h->device));
+  CU_TRY(vx::launch_synth_tokens(h->tokens, seed, 0, h->desc.tok_blocks, h->desc.tok_per_doc,
+                                 h->desc.tok_dim, h->stream));
+  count_launch(h);
+  CU_TRY(cudaStreamSynchronize(h->stream));
+  return VX_OK;
+}
+
+extern "C" vx_status vx_tokens_upload(vx_index* h, const uint16_t* tok, int64_t blk0, int64_t n) {
+  if (!h || (!tok && n > 0)) return fail(VX_ERR_INVALID, "null argument");
+  if (!h->tokens) return fail(VX_ERR_STATE, "index has no token store");
+  if (blk0 < 0 || n < 0 || blk0 + n > h->desc.tok_blocks)
+    return fail(VX_ERR_INVALID, "token blocks out of range");
+  const size_t blk = (size_t)h->desc.tok_per_doc * h->desc.tok_dim;
+  CU_TRY(cudaSetDevice(h->device));
+  CU_TRY(cudaMemcpyAsync(h->tokens + blk0 * blk, tok, n * blk * 2, cudaMemcpyHostToDevice,
+                         h->stream));
+  CU_TRY(cudaStreamSynchronize(h->stream));
+  return VX_OK;
+}
+
+// ---------------------------------------------------------------- pipeline pieces
+
+static cudaStream_t pick_stream(vx_index* h, void* s) {
+  return s ? reinterpret_cast<cudaStream_t>(s) : h->stream;
+}
+
+static vx_status check_batch(vx_index* h, int32_t B, int32_t k) {
+  if (B < 1 || B > h->desc.max_batch)
+    return fail(VX_ERR_INVALID, "batch %d outside [1, %d]", B, h->desc.max_batch);
+  if (k < 1 || k > h->desc.max_k) return fail(VX_ERR_INVALID, "k %d outside [1, %d]", k, h->desc.max_k);
+  return VX_OK;
+}
+
+// local scan + merge: d_q [B][D] -> keys (global ids) / ids / scores [B][k]
+static vx_status local_topk(vx_index* h, const float* d_q, int B, int k, uint64_t* keys,
+                            int64_t* ids, float* scores, cudaStream_t st) {
+  const int D = h->desc.dim;
+  const int kcap = kcap_of(k);
+  const int grid = h->grid;
+  // queries per launch: the largest bucket whose smem plan fits (big k / big D shrink it)
+  int gmax = 32, ns0 = 0, cap0 = 0;
+  while (gmax > 1 && !vx::scan_f32_smem(gmax, D, kcap, &ns0, &cap0)) gmax >>= 1;
+  for (int g0 = 0; g0 < B; g0 += gmax) {
+    const int Bg = std::min(gmax, B - g0);
+    const int bucket = vx::scan_f32_bucket(Bg);
+    int ns = 0, cap = 0;
+    size_t smem = vx::scan_f32_smem(bucket, D, kcap, &ns, &cap);
+    if (!smem) return fail(VX_ERR_UNSUPPORTED, "scan config (B=%d, D=%d, k=%d) exceeds smem", Bg, D, k);
+    vx::ScanF32Args a;
+    a.q = d_q + (size_t)g0 * D;
+    a.B = Bg;
+    a.D = D;
+    a.n_local = (uint32_t)h->n_local;
+    a.kcap = kcap;
+    a.cap = cap;
+    a.ns = ns;
+    a.part = h->d_part + (size_t)g0 * grid * kcap;
+    if (g0 == 0) CU_TRY(cudaEventRecord(h->ev[0], st));
+    CU_TRY(vx::launch_scan_f32(bucket, &h->tmap_docs, a, grid, smem, st));
+    count_launch(h);
+  }
+  CU_TRY(cudaEventRecord(h->ev[1], st));
+  CU_TRY(vx::launch_merge_topk(h->d_part, B, grid * kcap, k, h->row0, keys, ids, scores, st));
+  count_launch(h);
+  return VX_OK;
+}
+
+static vx_status run_maxsim(vx_index* h, const float* d_qtok, int B, int nq, const int64_t* d_cand,
+                            int C, float* d_out, cudaStream_t st) {
+  if (!h->tokens) return fail(VX_ERR_STATE, "index has no token store");
+  if (nq < 1 || nq > h->desc.max_qtok) return fail(VX_ERR_INVALID, "nq %d", nq);
+  vx::MaxSimArgs a;
+  a.qtok = d_qtok;
+  a.cand = d_cand;
+  a.table = h->tokens;
+  a.T = h->desc.tok_blocks;
+  a.B = B;
+  a.nq = nq;
+  a.C = C;
+  a.Nd = h->desc.tok_per_doc;
+  a.d = h->desc.tok_dim;
+  a.out = d_out;
+  CU_TRY(vx::launch_maxsim(a, st));
+  count_launch(h);
+  return VX_OK;
+}
+
+// ---------------------------------------------------------------- shard exchange
+enum { OP_STOP = 0, OP_SEARCH = 1, OP_RESCORE = 2 };
+
+__global__ void pack_shard_kernel(const uint64_t* keys, const float* ms, int n, ShardRec* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    ShardRec r;
+    r.key = keys[i];
+    r.ms = ms ? ms[i] : 0.0f;
+    r.pad = 0.0f;
+    out[i] = r;
+  }
+}
+
+// recv [G][B][k] -> keys [B][G*k] (reusing d_part) for the merge
+__global__ void transpose_shard_kernel(const ShardRec* recv, int G, int B, int k, uint64_t* keys) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int total = G * B * k;
+  if (i < total) {
+    int g = i / (B * k), r = i - g * B * k, b = r / k, j = r - b * k;
+    keys[(size_t)b * G * k + g * k + j] = recv[i].key;
+  }
+}
+
+// After the global merge: recover each winner's MaxSim from the gathered records.
+__global__ void lookup_ms_kernel(const ShardRec* recv, int G, int B, int k, const uint64_t* win,
+                                 float* ms_out) {
+  int b = blockIdx.x;
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    uint64_t key = win[(size_t)b * k + j];
+    float v = -INFINITY;
+    if (key)
+      for (int g = 0; g < G; ++g) {
+        const ShardRec* r = recv + ((size_t)g * B + b) * k;
+        for (int t = 0; t < k; ++t)
+          if (r[t].key == key) v = r[t].ms;
+      }
+    ms_out[(size_t)b * k + j] = v;
+  }
+}
+
+// Worker and root share this: given queries (and tokens) on device, compute the
+// local candidates and, for G > 1, exchange and merge at rank 0.
+static vx_status stage_core(vx_index* h, int op, const float* d_q, const float* d_qtok, int B,
+                            int nq, int k, int64_t* d_ids, float* d_ip, float* d_ms,
+                            cudaStream_t st) {
+  const bool rescore = (op == OP_RESCORE);
+  VX_TRY(local_topk(h, d_q, B, k, h->d_keys, h->d_ids, h->d_ip, st));
+  if (rescore) VX_TRY(run_maxsim(h, d_qtok, B, nq, h->d_ids, k, h->d_ms, st));
+  const int n = B * k;
+  if (h->nranks == 1) {
+    if (rescore) {
+      CU_TRY(vx::launch_order_by(h->d_ms, h->d_ids, h->d_ip, B, k, d_ids, d_ip, d_ms, st));
+      count_launch(h);
+    } else {
+      CU_TRY(cudaMemcpyAsync(d_ids, h->d_ids, (size_t)n * 8, cudaMemcpyDeviceToDevice, st));
+      CU_TRY(cudaMemcpyAsync(d_ip, h->d_ip, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+    }
+    return VX_OK;
+  }
+  // ---- G > 1: gather k x G records to rank 0
+  pack_shard_kernel<<<(n + 255) / 256, 256, 0, st>>>(h->d_keys, rescore ? h->d_ms : nullptr, n,
+                                                     h->d_send);
+  count_launch(h);
+  CU_TRY(cudaGetLastError());
+  const size_t bytes = (size_t)n * sizeof(ShardRec);
+  NCCL_TRY(nccl().GroupStart());
+  if (h->rank == 0) {
+    for (int r = 0; r < h->nranks; ++r) {
+      if (r == 0)
+        CU_TRY(cudaMemcpyAsync(h->d_recv, h->d_send, bytes, cudaMemcpyDeviceToDevice, st));
+      else
+        NCCL_TRY(nccl().Recv(reinterpret_cast<uint8_t*>(h->d_recv) + (size_t)r * bytes, bytes,
+                          ncclUint8, r, h->comm, st));
+    }
+  } else {
+    NCCL_TRY(nccl().Send(h->d_send, bytes, ncclUint8, 0, h->comm, st));
+  }
+  NCCL_TRY(nccl().GroupEnd());
+  if (h->rank != 0) return VX_OK;
+  const int G = h->nranks;
+  transpose_shard_kernel<<<(G * n + 255) / 256, 256, 0, st>>>(h->d_recv, G, B, k, h->d_part);
+  count_launch(h);
+  // keys already carry global ids: id_base 0
+  CU_TRY(vx::launch_merge_topk(h->d_part, B, G * k, k, 0, h->d_keys, h->d_ids, h->d_ip, st));
+  count_launch(h);
+  if (rescore) {
+    lookup_ms_kernel<<<B, 128, 0, st>>>(h->d_recv, G, B, k, h->d_keys, h->d_ms);
+    count_launch(h);
+    CU_TRY(vx::launch_order_by(h->d_ms, h->d_ids, h->d_ip, B, k, d_ids, d_ip, d_ms, st));
+    count_launch(h);
+  } else {
+    CU_TRY(cudaMemcpyAsync(d_ids, h->d_ids, (size_t)n * 8, cudaMemcpyDeviceToDevice, st));
+    CU_TRY(cudaMemcpyAsync(d_ip, h->d_ip, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+  }
+  return VX_OK;
+}
+
+// Rank 0 entry: announce the batch to the shards, then run the core.
+static vx_status stage_root(vx_index* h, int op, const float* d_q, const float* d_qtok, int B,
+                            int nq, int k, int64_t* d_ids, float* d_ip, float* d_ms,
+                            cudaStream_t st) {
+  if (h->nranks > 1) {
+    if (h->rank != 0) return fail(VX_ERR_STATE, "only rank 0 issues searches; call vx_shard_serve");
+    h->h_hdr[0] = op;
+    h->h_hdr[1] = B;
+    h->h_hdr[2] = k;
+    h->h_hdr[3] = nq;
+    CU_TRY(cudaMemcpyAsync(h->d_hdr, h->h_hdr, 16, cudaMemcpyHostToDevice, st));
+    NCCL_TRY(nccl().Broadcast(h->d_hdr, h->d_hdr, 4, ncclInt32, 0, h->comm, st));
+    NCCL_TRY(nccl().GroupStart());
+    NCCL_TRY(nccl().Broadcast(d_q, h->d_q, (size_t)B * h->desc.dim, ncclFloat32, 0, h->comm, st));
+    if (op == OP_RESCORE)
+      NCCL_TRY(nccl().Broadcast(d_qtok, h->d_qtok, (size_t)B * nq * h->desc.tok_dim, ncclFloat32, 0,
+                             h->comm, st));
+    NCCL_TRY(nccl().GroupEnd());
+  }
+  CU_TRY(cudaEventRecord(h->ev[2], st));
+  VX_TRY(stage_core(h, op, d_q, d_qtok, B, nq, k, d_ids, d_ip, d_ms, st));
+  CU_TRY(cudaEventRecord(h->ev[3], st));
+  h->timing_pending = true;
+  h->st.batches += 1;
+  h->st.queries += B;
+  return VX_OK;
+}
+
+extern "C" vx_status vx_search_dev(vx_index* h, const float* d_q, int32_t B, int32_t k,
+                                   int64_t* d_ids, float* d_scores, void* stream) {
+  if (!h || !d_q || !d_ids || !d_scores) return fail(VX_ERR_INVALID, "null argument");
+  VX_TRY(check_batch(h, B, k));
+  CU_TRY(cudaSetDevice(h->device));
+  return stage_root(h, OP_SEARCH, d_q, nullptr, B, 0, k, d_ids, d_scores, nullptr,
+                    pick_stream(h, stream));
+}
+
+extern "C" vx_status vx_search_rescore_dev(vx_index* h, const float* d_q, const float* d_qtok,
+                                           int32_t B, int32_t nq, int32_t k, int64_t* d_ids,
+                                           float* d_ip, float* d_ms, void* stream) {
+  if (!h || !d_q || !d_qtok || !d_ids || !d_ip || !d_ms) return fail(VX_ERR_INVALID, "null argument");
+  VX_TRY(check_batch(h, B, k));
+  if (!h->tokens) return fail(VX_ERR_STATE, "index has no token store");
+  if (nq < 1 || nq > h->desc.max_qtok) return fail(VX_ERR_INVALID, "nq %d", nq);
+  CU_TRY(cudaSetDevice(h->device));
+  return stage_root(h, OP_RESCORE, d_q, d_qtok, B, nq, k, d_ids, d_ip, d_ms,
+                    pick_stream(h, stream));
+}
+
+extern "C" vx_status vx_maxsim_dev(vx_index* h, const float* d_qtok, int32_t B, int32_t nq,
+                                   const int64_t* d_cand, int32_t C, float* d_out, void* stream) {
+  if (!h || !d_qtok || !d_cand || !d_out) return fail(VX_ERR_INVALID, "null argument");
+  if (B < 1 || B > h->desc.max_batch || C < 1) return fail(VX_ERR_INVALID, "B %d C %d", B, C);
+  CU_TRY(cudaSetDevice(h->device));
+  return run_maxsim(h, d_qtok, B, nq, d_cand, C, d_out, pick_stream(h, stream));
+}
+
+extern "C" vx_status vx_sync(vx_index* h) {
+  if (!h) return fail(VX_ERR_INVALID, "null handle");
+  CU_TRY(cudaSetDevice(h->device));
+  CU_TRY(cudaStreamSynchronize(h->stream));
+  if (h->timing_pending) {
+    CU_TRY(cudaEventSynchronize(h->ev[3]));
+    float a = 0, b = 0;
+    if (cudaEventElapsedTime(&a, h->ev[0], h->ev[1]) == cudaSuccess &&
+        cudaEventElapsedTime(&b, h->ev[2], h->ev[3]) == cudaSuccess) {
+      h->st.last_scan_ms = a;
+      h->st.last_step_ms = b;
+      h->st.scan_ms_total += a;
+      h->st.step_ms_total += b;
+      h->st.timed_batches += 1;
+    }
+    h->timing_pending = false;
+  }
+  cudaGetLastError();
+  return VX_OK;
+}
+
+// ---------------------------------------------------------------- host-buffer API
+extern "C" vx_status vx_search(vx_index* h, const float* q, int32_t B, int32_t k, int64_t* ids,
+                               float* scores) {
+  if (!h || !q || !ids || !scores) return fail(VX_ERR_INVALID, "null argument");
+  VX_TRY(check_batch(h, B, k));
+  CU_TRY(cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  const size_t qb = (size_t)B * h->desc.dim * 4;
+  uint8_t* stage = static_cast<uint8_t*>(h->h_stage);
+  memcpy(stage, q, qb);
+  CU_TRY(cudaMemcpyAsync(h->d_q, stage, qb, cudaMemcpyHostToDevice, st));
+  VX_TRY(stage_root(h, OP_SEARCH, h->d_q, nullptr, B, 0, k, h->d_out_ids, h->d_out_ip, nullptr, st));
+  int64_t* hid = reinterpret_cast<int64_t*>(stage);
+  float* hsc = reinterpret_cast<float*>(stage + (size_t)B * k * 8);
+  CU_TRY(cudaMemcpyAsync(hid, h->d_out_ids, (size_t)B * k * 8, cudaMemcpyDeviceToHost, st));
+  CU_TRY(cudaMemcpyAsync(hsc, h->d_out_ip, (size_t)B * k * 4, cudaMemcpyDeviceToHost, st));
+  VX_TRY(vx_sync(h));
+  memcpy(ids, hid, (size_t)B * k * 8);
+  memcpy(scores, hsc, (size_t)B * k * 4);
+  return VX_OK;
+}
+
+extern "C" vx_status vx_maxsim(vx_index* h, const float* qtok, int32_t B, int32_t nq,
+                               const int64_t* cand, int32_t C, float* out) {
+  if (!h || !qtok || !cand || !out) return fail(VX_ERR_INVALID, "null argument");
+  if (!h->tokens) return fail(VX_ERR_STATE, "index has no token store");
+  if (B < 1 || B > h->desc.max_batch || C < 1 || C > h->desc.max_k)
+    return fail(VX_ERR_INVALID, "B %d / C %d outside [1,%d] / [1,%d]", B, C, h->desc.max_batch,
+                h->desc.max_k);
+  if (nq < 1 || nq > h->desc.max_qtok) return fail(VX_ERR_INVALID, "nq %d", nq);
+  CU_TRY(cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  const size_t tb = (size_t)B * nq * h->desc.tok_dim * 4, cb = (size_t)B * C * 8;
+  uint8_t* stage = static_cast<uint8_t*>(h->h_stage);
+  memcpy(stage, qtok, tb);
+  CU_TRY(cudaMemcpyAsync(h->d_qtok, stage, tb, cudaMemcpyHostToDevice, st));
+  memcpy(stage + tb, cand, cb);
+  CU_TRY(cudaMemcpyAsync(h->d_out_ids, stage + tb, cb, cudaMemcpyHostToDevice, st));
+  VX_TRY(run_maxsim(h, h->d_qtok, B, nq, h->d_out_ids, C, h->d_out_ms, st));
+  CU_TRY(cudaMemcpyAsync(stage, h->d_out_ms, (size_t)B * C * 4, cudaMemcpyDeviceToHost, st));
+  VX_TRY(vx_sync(h));
+  memcpy(out, stage, (size_t)B * C * 4);
+  return VX_OK;
+}
+
+extern "C" vx_status vx_search_rescore(vx_index* h, const float* q, const float* qtok, int32_t B,
+                                       int32_t nq, int32_t k, int64_t* ids, float* ip,
+                                       float* ms) {
+  if (!h || !q || !qtok || !ids || !ip || !ms) return fail(VX_ERR_INVALID, "null argument");
+  VX_TRY(check_batch(h, B, k));
+  if (!h->tokens) return fail(VX_ERR_STATE, "index has no token store");
+  if (nq < 1 || nq > h->desc.max_qtok) return fail(VX_ERR_INVALID, "nq %d", nq);
+  CU_TRY(cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  const size_t qb = (size_t)B * h->desc.dim * 4, tb = (size_t)B * nq * h->desc.tok_dim * 4;
+  uint8_t* stage = static_cast<uint8_t*>(h->h_stage);
+  memcpy(stage, q, qb);
+  memcpy(stage + qb, qtok, tb);
+  CU_TRY(cudaMemcpyAsync(h->d_q, stage, qb, cudaMemcpyHostToDevice, st));
+  CU_TRY(cudaMemcpyAsync(h->d_qtok, stage + qb, tb, cudaMemcpyHostToDevice, st));
+  VX_TRY(stage_root(h, OP_RESCORE, h->d_q, h->d_qtok, B, nq, k, h->d_out_ids, h->d_out_ip,
+                    h->d_out_ms, st));
+  const size_t n = (size_t)B * k;
+  CU_TRY(cudaMemcpyAsync(stage, h->d_out_ids, n * 8, cudaMemcpyDeviceToHost, st));
+  CU_TRY(cudaMemcpyAsync(stage + n * 8, h->d_out_ip, n * 4, cudaMemcpyDeviceToHost, st));
+  CU_TRY(cudaMemcpyAsync(stage + n * 12, h->d_out_ms, n * 4, cudaMemcpyDeviceToHost, st));
+  VX_TRY(vx_sync(h));
+  memcpy(ids, stage, n * 8);
+  memcpy(ip, stage + n * 8, n * 4);
+  memcpy(ms, stage + n * 12, n * 4);
+  return VX_OK;
+}
+
+// ---------------------------------------------------------------- comm
+extern "C" vx_status vx_comm_unique_id(uint8_t out_id[128]) {
+  if (!out_id) return fail(VX_ERR_INVALID, "null argument");
+  if (!nccl().ok) return fail(VX_ERR_NCCL, "libnccl.so.2 not loadable (set VX_NCCL_LIB)");
+  ncclUniqueId id;
+  NCCL_TRY(nccl().GetUniqueId(&id));
+  static_assert(sizeof(ncclUniqueId) == 128, "nccl id size");
+  memcpy(out_id, &id, 128);
+  return VX_OK;
+}
+
+extern "C" vx_status vx_comm_init(vx_index* h, const uint8_t id[128], int32_t nranks,
+                                  int32_t rank) {
+  if (!h || !id) return fail(VX_ERR_INVALID, "null argument");
+  if (nranks != h->desc.n_shards || rank != h->desc.shard)
+    return fail(VX_ERR_INVALID, "comm (%d of %d) must match shard (%d of %d)", rank, nranks,
+                h->desc.shard, h->desc.n_shards);
+  if (h->comm) return fail(VX_ERR_STATE, "comm already initialised");
+  if (!nccl().ok) return fail(VX_ERR_NCCL, "libnccl.so.2 not loadable (set VX_NCCL_LIB)");
+  CU_TRY(cudaSetDevice(h->device));
+  ncclUniqueId uid;
+  memcpy(&uid, id, 128);
+  NCCL_TRY(nccl().CommInitRank(&h->comm, nranks, uid, rank));
+  h->nranks = nranks;
+  h->rank = rank;
+  return VX_OK;
+}
+
+extern "C" vx_status vx_shard_serve(vx_index* h) {
+  if (!h) return fail(VX_ERR_INVALID, "null handle");
+  if (!h->comm || h->rank == 0) return fail(VX_ERR_STATE, "vx_shard_serve is for ranks != 0");
+  CU_TRY(cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  for (;;) {
+    NCCL_TRY(nccl().Broadcast(h->d_hdr, h->d_hdr, 4, ncclInt32, 0, h->comm, st));
+    CU_TRY(cudaMemcpyAsync(h->h_hdr, h->d_hdr, 16, cudaMemcpyDeviceToHost, st));
+    CU_TRY(cudaStreamSynchronize(st));
+    const int op = h->h_hdr[0], B = h->h_hdr[1], k = h->h_hdr[2], nq = h->h_hdr[3];
+    if (op == OP_STOP) return VX_OK;
+    if (B < 1 || B > h->desc.max_batch || k < 1 || k > h->desc.max_k)
+      return fail(VX_ERR_STATE, "bad batch header %d/%d/%d", op, B, k);
+    NCCL_TRY(nccl().GroupStart());
+    NCCL_TRY(nccl().Broadcast(h->d_q, h->d_q, (size_t)B * h->desc.dim, ncclFloat32, 0, h->comm, st));
+    if (op == OP_RESCORE)
+      NCCL_TRY(nccl().Broadcast(h->d_qtok, h->d_qtok, (size_t)B * nq * h->desc.tok_dim, ncclFloat32,
+                             0, h->comm, st));
+    NCCL_TRY(nccl().GroupEnd());
+    VX_TRY(stage_core(h, op, h->d_q, h->d_qtok, B, nq, k, h->d_out_ids, h->d_out_ip, h->d_out_ms,
+                      st));
+    h->st.batches += 1;
+    h->st.queries += B;
+  }
+}
+
+extern "C" vx_status vx_shard_stop(vx_index* h) {
+  if (!h) return fail(VX_ERR_INVALID, "null handle");
+  if (!h->comm || h->rank != 0) return fail(VX_ERR_STATE, "vx_shard_stop is for rank 0");
+  CU_TRY(cudaSetDevice(h->device));
+  h->h_hdr[0] = OP_STOP;
+  h->h_hdr[1] = h->h_hdr[2] = h->h_hdr[3] = 0;
+  CU_TRY(cudaMemcpyAsync(h->d_hdr, h->h_hdr, 16, cudaMemcpyHostToDevice, h->stream));
+  NCCL_TRY(nccl().Broadcast(h->d_hdr, h->d_hdr, 4, ncclInt32, 0, h->comm, h->stream));
+  CU_TRY(cudaStreamSynchronize(h->stream));
+  return VX_OK;
+}

@@ -1,0 +1,61 @@
+// vx_internal.cuh — shared declarations between the kernels and the C-ABI layer.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/vx_synth.h"
+
+namespace vx {
+
+// -------- exact fp32 scan (K1): scan_f32.cu
+struct ScanF32Args {
+  const float* q;      // [B][D] device, fp32
+  int32_t B;           // queries in this launch (<= the config's BQ)
+  int32_t D;           // dimension (multiple of 32)
+  uint32_t n_local;    // rows in the shard
+  int32_t kcap;        // per-CTA list length (power of 2, >= k, 16..256)
+  int32_t cap;         // candidate buffer per query
+  int32_t ns;          // pipeline stages
+  uint64_t* part;      // [B][gridDim.x][kcap] keys (score desc, local id asc)
+};
+
+// Returns the queries-per-launch bucket the f32 scan uses for a batch of B.
+int scan_f32_bucket(int B);
+// Dynamic smem bytes for (bucket, D, kcap); 0 if it does not fit.
+size_t scan_f32_smem(int bucket, int D, int kcap, int* ns_out, int* cap_out);
+cudaError_t launch_scan_f32(int bucket, const CUtensorMap* tmap, const ScanF32Args& a, int grid,
+                            size_t smem, cudaStream_t st);
+int scan_f32_tile_docs(int bucket);
+
+// -------- top-k merge (K3): topk.cu
+// For each query q: select the k largest keys among in[q][0..M), write them
+// descending to out_keys[q][k] (re-keyed with id + id_base), ids (-1 for empty) and scores.
+cudaError_t launch_merge_topk(const uint64_t* in, int B, int M, int k, int64_t id_base,
+                              uint64_t* out_keys, int64_t* out_ids, float* out_scores,
+                              cudaStream_t st);
+// Order k candidates per query by a float score descending (ties id asc) and
+// permute the companion arrays: used to order by MaxSim after the IP top-k.
+cudaError_t launch_order_by(const float* key_score, const int64_t* ids, const float* ip, int B,
+                            int k, int64_t* out_ids, float* out_ip, float* out_ms,
+                            cudaStream_t st);
+
+// -------- synthetic fill: synth.cu
+cudaError_t launch_synth_rows(float* out, uint64_t seed, int64_t row0, int64_t n, int D,
+                              cudaStream_t st);
+cudaError_t launch_synth_tokens(uint16_t* out, uint64_t seed, int64_t blk0, int64_t nblk, int Nd,
+                                int d, cudaStream_t st);
+
+// -------- MaxSim (K4): maxsim.cu
+struct MaxSimArgs {
+  const float* qtok;     // [B][nq][d] fp32 (rounded to bf16 in-kernel)
+  const int64_t* cand;   // [B][C] global doc ids, -1 = skip
+  const uint16_t* table; // [T][Nd][d] bf16 bits
+  int64_t T;
+  int32_t B, nq, C, Nd, d;
+  float* out;            // [B][C]
+};
+cudaError_t launch_maxsim(const MaxSimArgs& a, cudaStream_t st);
+
+}  // namespace vx

@@ -1,0 +1,194 @@
+"""Parity of the CUDA path (through the C-ABI) with the CPU oracle.  Runs on a B200.
+
+Bar (BASELINE.json north_star):
+  * exact scan: ids AND scores bit-identical to the oracle's VXO_F32 mode (same in-order
+    fmaf chain per dot product, same (score desc, id asc) order); vs the fp64 truth, any id
+    difference must be a tie within TIE_TOL and scores within 1e-4 relative;
+  * MaxSim (bf16 tokens, fp32 accumulate): CUDA-core kernel bit-identical to VXO_F32; vs the
+    fp64 truth of the same bf16 inputs within MS_RTOL (stated bf16-path tolerance).
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TIE_TOL = 1e-6     # |s64(a) - s64(b)| under which two docs count as tied (fp32 noise ~1e-8)
+SCORE_RTOL = 1e-4  # north-star bound for fp32-accumulated scores
+MS_RTOL = 1e-5     # bf16-input MaxSim, fp32 accumulation vs fp64 of the same inputs
+
+
+@pytest.fixture(scope="module")
+def vx(vxlib):
+    import paper_2511_02062_b200 as vx
+    return vx
+
+
+def ties_ok(ids_gpu, ids_ref, s64_lookup, kth_score):
+    """ids may differ only where the differing docs are tied (fp64) with the k-th score."""
+    a, b = set(ids_gpu.tolist()), set(ids_ref.tolist())
+    for d in a ^ b:
+        if abs(s64_lookup(d) - kth_score) > TIE_TOL:
+            return False
+    return True
+
+
+def test_device_synth_bit_exact(vx, oracle):
+    with vx.Index(5000, 768, tok_per_doc=16, tok_dim=64, tok_blocks=9) as idx:
+        idx.synth(42)
+        idx.tokens_synth(45)
+        got = idx.download(0, 5000)
+        want = oracle.synth_rows(42, 0, 5000, 768)
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+        assert np.array_equal(idx.tokens_download(0, 9), oracle.synth_tokens(45, 0, 9, 16, 64))
+
+
+@pytest.mark.parametrize("N,D,B,k", [
+    (1000, 64, 1, 1), (1000, 64, 5, 7), (4097, 128, 3, 10), (3000, 768, 4, 10),
+    (100_000, 768, 16, 10), (20_000, 1024, 8, 100), (12_345, 768, 32, 100),
+    (50_000, 256, 17, 128), (30_000, 768, 33, 256), (9_999, 768, 2, 64), (7, 32, 6, 5)])
+def test_scan_bit_identical_to_oracle_f32(vx, oracle, N, D, B, k):
+    X = oracle.synth_rows(42, 0, N, D)
+    Q = oracle.synth_rows(43, 0, B, D)
+    with vx.Index(N, D, max_batch=max(B, 1), max_k=max(k, 1)) as idx:
+        idx.synth(42)
+        ids, sc = idx.search(Q, k)
+    rid, rsc = oracle.flat_topk(X, Q, k, mode=1)
+    assert np.array_equal(ids, rid)
+    valid = rid >= 0
+    assert np.array_equal(sc[valid], rsc[valid].astype(np.float32))
+    assert np.isneginf(sc[~valid]).all()
+    # against the fp64 truth: ties within tolerance, scores within 1e-4 relative
+    tid, tsc = oracle.flat_topk(X, Q, k, mode=0)
+    for b in range(B):
+        s64 = lambda d, b=b: float(np.dot(X[d].astype(np.float64), Q[b].astype(np.float64)))
+        kth = tsc[b][min(k, N) - 1]
+        assert ties_ok(ids[b][ids[b] >= 0], tid[b][tid[b] >= 0], s64, kth)
+    v = tid >= 0
+    np.testing.assert_allclose(sc[v], tsc[v], rtol=SCORE_RTOL, atol=1e-7)
+
+
+def test_known_answer_ties(vx, golden):
+    g = golden("kat_ties")
+    X = np.zeros((6, 32), np.float32)
+    X[:, :2] = g["X"]
+    Q = np.zeros((2, 32), np.float32)
+    Q[:, :2] = g["Q"]
+    with vx.Index(6, 32, max_batch=2, max_k=4) as idx:
+        idx.upload(X)
+        ids, sc = idx.search(Q, 4)
+    assert ids.tolist() == g["ids"].tolist()
+    assert np.array_equal(sc, g["scores"].astype(np.float32))
+
+
+def test_golden_fixture_ids(vx, oracle, golden):
+    for name in ("ip_small", "ip_768", "ip_k100"):
+        g = golden(name)
+        N, D, B, k = (int(g[x]) for x in ("N", "D", "B", "k"))
+        with vx.Index(N, D, max_batch=B, max_k=k) as idx:
+            idx.synth(42)
+            ids, sc = idx.search(oracle.synth_rows(43, 0, B, D), k)
+        assert np.array_equal(ids, g["ids"]), name
+        np.testing.assert_allclose(sc, g["scores"], rtol=SCORE_RTOL)
+
+
+def test_edge_cases(vx, oracle):
+    # k > N pads with -1/-INF; duplicate rows tie and resolve by id; zero query -> all ties
+    X = oracle.synth_rows(42, 0, 40, 64)
+    X[10] = X[3]
+    X[20] = X[3]
+    with vx.Index(40, 64, max_batch=4, max_k=64) as idx:
+        idx.upload(X)
+        ids, sc = idx.search(np.stack([X[3], np.zeros(64, np.float32)]), 50)
+    assert ids[0, :3].tolist() == [3, 10, 20]
+    assert (ids[:, 40:] == -1).all() and np.isneginf(sc[:, 40:]).all()
+    assert ids[1, :40].tolist() == list(range(40))
+
+
+def test_scan_rejects_bad_shapes(vx):
+    with vx.Index(100, 64, max_batch=4, max_k=8) as idx:
+        idx.synth(1)
+        with pytest.raises(vx.VxError):
+            idx.search(np.zeros((5, 64), np.float32), 4)
+        with pytest.raises(vx.VxError):
+            idx.search(np.zeros((1, 64), np.float32), 9)
+
+
+def test_maxsim_matches_oracle(vx, oracle, golden):
+    g = golden("maxsim_small")
+    T, Nd, d = g["table"].shape
+    with vx.Index(100, 32, tok_per_doc=Nd, tok_dim=d, tok_blocks=T, max_batch=4, max_k=8,
+                  max_qtok=8) as idx:
+        idx.tokens_upload(g["table"])
+        out = idx.maxsim(g["qtok"], g["cand"])
+    fin = np.isfinite(g["ms"])
+    np.testing.assert_allclose(out[fin], g["ms"][fin], rtol=MS_RTOL)
+    assert np.isneginf(out[~fin]).all()
+    ref32 = oracle.maxsim(g["qtok"], g["cand"], g["table"], mode=1)
+    assert np.array_equal(out[fin], ref32[fin].astype(np.float32))
+
+
+@pytest.mark.parametrize("B,C", [(1, 100), (8, 100), (64, 100)])
+def test_maxsim_preflmr_shape(vx, oracle, B, C):
+    # PreFLMR config: 32 query tokens x 100 candidates x 128 doc tokens, dim 128
+    T, Nd, d, nq = 257, 128, 128, 32
+    rng = np.random.default_rng(B)
+    cand = np.stack([rng.choice(10_000_000, C, replace=False) for _ in range(B)]).astype(np.int64)
+    qtok = oracle.synth_rows(44, 0, B * nq, d).reshape(B, nq, d)
+    with vx.Index(1000, 32, tok_per_doc=Nd, tok_dim=d, tok_blocks=T, max_batch=B, max_k=C,
+                  max_qtok=nq) as idx:
+        idx.tokens_synth(45)
+        out = idx.maxsim(qtok, cand)
+    table = oracle.synth_tokens(45, 0, T, Nd, d)
+    ref = oracle.maxsim(qtok, cand, table, mode=0)
+    np.testing.assert_allclose(out, ref, rtol=MS_RTOL)
+
+
+def test_search_rescore_matches_oracle(vx, oracle):
+    N, D, B, k, T, Nd, d, nq = 20_000, 768, 5, 100, 97, 128, 128, 32
+    X = oracle.synth_rows(42, 0, N, D)
+    Q = oracle.synth_rows(43, 0, B, D)
+    qtok = oracle.synth_rows(44, 0, B * nq, d).reshape(B, nq, d)
+    table = oracle.synth_tokens(45, 0, T, Nd, d)
+    with vx.Index(N, D, tok_per_doc=Nd, tok_dim=d, tok_blocks=T, max_batch=B, max_k=k,
+                  max_qtok=nq) as idx:
+        idx.synth(42)
+        idx.tokens_synth(45)
+        ids, ip, ms = idx.search_rescore(Q, qtok, k)
+    rid, rip, rms = oracle.search_rescore(X, Q, qtok, table, k, mode=1)
+    for b in range(B):
+        assert sorted(ids[b].tolist()) == sorted(rid[b].tolist())
+        lut = {i: (p, m) for i, p, m in zip(rid[b].tolist(), rip[b].tolist(), rms[b].tolist())}
+        for i, p, m in zip(ids[b].tolist(), ip[b].tolist(), ms[b].tolist()):
+            assert np.float32(lut[i][0]) == np.float32(p)
+            assert abs(lut[i][1] - m) <= MS_RTOL * abs(lut[i][1])
+        assert all(ms[b][j] >= ms[b][j + 1] for j in range(k - 1))
+
+
+def test_component_payload_path(vx, oracle):
+    N, D, k, T, Nd, d, nq = 5000, 768, 10, 31, 128, 128, 32
+    Q = oracle.synth_rows(43, 0, 3, D)
+    qtok = oracle.synth_rows(44, 0, 3 * nq, d).reshape(3, nq, d)
+    with vx.Index(N, D, tok_per_doc=Nd, tok_dim=d, tok_blocks=T, max_batch=4, max_k=k,
+                  max_qtok=nq) as idx:
+        idx.synth(42)
+        idx.tokens_synth(45)
+        reg = vx.Registry()
+        reg.register_component("modelD", vx.SearchComponent(idx, k))
+        outs = reg.invoke("modelD", [vx.encode_query(Q[i], qtok[i]) for i in range(3)])
+        ids, ip, ms = idx.search_rescore(Q, qtok, k)
+    assert len(outs) == 3
+    for i, p in enumerate(outs):
+        r = vx.decode_result(p)
+        assert r["id"].tolist() == ids[i].tolist()
+        assert np.array_equal(r["ms"], ms[i])
+
+
+def test_stats_count_launches(vx):
+    with vx.Index(10_000, 128, max_batch=4, max_k=10) as idx:
+        idx.synth(1)
+        idx.reset_stats()
+        idx.search(np.ones((4, 128), np.float32), 10)
+        st = idx.stats()
+    assert st["kernel_launches"] >= 2 and st["batches"] == 1 and st["queries"] == 4
