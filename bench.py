@@ -45,7 +45,7 @@ def peaks() -> dict:
 def parse() -> argparse.Namespace:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n-docs", type=int, default=10_000_000)
@@ -66,7 +66,8 @@ def parse() -> argparse.Namespace:
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks/throttle reasons sampled every 100 ms during the timed region
+    (written to a file: a pipe would hold the lines in nvidia-smi's stdio buffer)."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -74,38 +75,43 @@ class ClockSampler:
 
     def __init__(self, device: int):
         self.device, self.rows, self.proc = device, [], None
+        self.path = Path(f"/tmp/vx_clocks_{os.getpid()}_{device}.csv")
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            threading.Thread(target=self._read, daemon=True).start()
+                 "--format=csv,noheader,nounits", "-lms", "100", "-f", str(self.path)],
+                stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+            time.sleep(0.15)
         except FileNotFoundError:
             self.proc = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
-
     def __exit__(self, *exc):
         if self.proc:
+            time.sleep(0.15)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=2)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
+            if self.path.exists():
+                self.rows = [[x.strip() for x in ln.split(",")]
+                             for ln in self.path.read_text().splitlines() if ln.strip()]
+                self.path.unlink()
 
     def summary(self) -> dict:
-        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        ok = [r for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        sm = [float(r[1]) for r in ok]
+        mx = [float(r[2]) for r in ok]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows if len(r) >= 9
-                          for i in range(4) if r[5 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(sm)}
+        reasons = sorted({names[i] for r in ok for i in range(4) if r[5 + i].lower() == "active"})
+        out = {"sm_mhz": statistics.median(sm) if sm else None,
+               "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(sm)}
+        if not ok and self.rows:
+            out["raw"] = ",".join(self.rows[0])[:200]
+        return out
 
 
 # ----------------------------------------------------------------------------- CPU legs
@@ -180,7 +186,8 @@ def run_ours(args) -> None:
         idx.comm_init(uid[0], world, rank)
 
     dev = torch.device("cuda", local)
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(dev)  # a real stream: the library launches on it, events see it
+    torch.cuda.set_stream(stream)
     sp = stream.cuda_stream
     from paper_2511_02062_b200 import synth
 

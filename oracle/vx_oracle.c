@@ -263,14 +263,14 @@ int vxo_maxsim(const float* qtok, int32_t B, int32_t nq, int32_t dim, const int6
 }
 
 int vxo_search_rescore(const float* X, int64_t n, int32_t dim, const float* Q, const float* qtok,
-                       int32_t B, int32_t nq, int32_t k, const uint16_t* table, int64_t T,
+                       int32_t B, int32_t nq, int32_t tdim, int32_t k, const uint16_t* table, int64_t T,
                        int32_t Nd, int32_t mode, int32_t threads, int64_t* ids, double* ip,
                        double* ms) {
   int64_t* tid = (int64_t*)malloc(sizeof(int64_t) * (size_t)B * k);
   double* tsc = (double*)malloc(sizeof(double) * (size_t)B * k);
   double* tms = (double*)malloc(sizeof(double) * (size_t)B * k);
   int rc = vxo_flat_topk(X, n, dim, 0, Q, B, k, mode, threads, tid, tsc);
-  if (rc == 0) rc = vxo_maxsim(qtok, B, nq, dim, tid, k, table, T, Nd, mode, threads, tms);
+  if (rc == 0) rc = vxo_maxsim(qtok, B, nq, tdim, tid, k, table, T, Nd, mode, threads, tms);
   if (rc == 0) {
     vxo_ent* L = (vxo_ent*)malloc(sizeof(vxo_ent) * (size_t)k);
     for (int32_t b = 0; b < B; ++b) {

@@ -67,7 +67,7 @@ int vxo_maxsim(const float* qtok, int32_t B, int32_t nq, int32_t dim, const int6
 /* The fused stage: IP top-k, MaxSim of those k, re-ordered by MaxSim desc (ties
  * id asc).  ids/ip/ms [B][k]. */
 int vxo_search_rescore(const float* X, int64_t n, int32_t dim, const float* Q, const float* qtok,
-                       int32_t B, int32_t nq, int32_t k, const uint16_t* table, int64_t T,
+                       int32_t B, int32_t nq, int32_t tdim, int32_t k, const uint16_t* table, int64_t T,
                        int32_t Nd, int32_t mode, int32_t threads, int64_t* ids, double* ip,
                        double* ms);
 

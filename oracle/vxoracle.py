@@ -39,7 +39,7 @@ def lib():
         L.vxo_dot.restype = C.c_double
         L.vxo_flat_topk.argtypes = [fp, i64, i32, i64, fp, i32, i32, i32, i32, lp, dp]
         L.vxo_maxsim.argtypes = [fp, i32, i32, i32, lp, i32, hp, i64, i32, i32, i32, dp]
-        L.vxo_search_rescore.argtypes = [fp, i64, i32, fp, fp, i32, i32, i32, hp, i64, i32, i32,
+        L.vxo_search_rescore.argtypes = [fp, i64, i32, fp, fp, i32, i32, i32, i32, hp, i64, i32, i32,
                                          i32, lp, dp, dp]
         L.vxo_percentile.argtypes = [dp, i64, C.c_double]
         L.vxo_percentile.restype = C.c_double
@@ -102,7 +102,7 @@ def search_rescore(X, Q, qtok, table, k, mode=F64, threads=0):
     ip = np.empty((B, k), np.float64)
     ms = np.empty((B, k), np.float64)
     rc = lib().vxo_search_rescore(_p(X, C.c_float), X.shape[0], X.shape[1], _p(Q, C.c_float),
-                                  _p(qtok, C.c_float), B, nq, k, _p(table, C.c_uint16),
+                                  _p(qtok, C.c_float), B, nq, d, k, _p(table, C.c_uint16),
                                   table.shape[0], table.shape[1], mode, threads,
                                   _p(ids, C.c_int64), _p(ip, C.c_double), _p(ms, C.c_double))
     assert rc == 0
