@@ -1,0 +1,383 @@
+// scan_tc.cu — K2: tensor-core (tcgen05, kind::tf32) coarse scan of an index shard with a
+// fused per-CTA top-16 per query, followed by K2b: exact fp32 re-ranking of the merged
+// coarse top-k' with a correctness certificate.
+//
+// Why: the exact fp32 CUDA-core scan (scan_f32.cu) is shared-memory-bandwidth bound at
+// B >= 16 (ncu, profiles/r01); the tensor pipe does the B x N x D contraction ~30x faster,
+// so the scan stays HBM-bound up to B ~ 256.  TF32 products are not exact, so the tensor
+// pass only SELECTS candidates; every reported score is recomputed exactly (in-order fmaf
+// chain, bit-identical to the oracle) and a certificate proves that no document outside
+// the candidate set can enter the exact top-k (else the query is re-scanned exactly).
+//
+// K2 layout (one CTA per SM, persistent over 128-document tiles):
+//   A = queries   [QT x 128 rows][32 fp32 per K-chunk]  (TMA, SWIZZLE_128B, L2 evict_last)
+//   B = documents [128 rows][32 fp32 per K-chunk]        (TMA, SWIZZLE_128B, L2 evict_first)
+//   D = scores in TMEM: lane = query, column = document (fp32), NBUF accumulator buffers
+//   warp 0: TMA producer; warp 1: TMEM allocator + single-thread MMA issuer;
+//   warps 2..: epilogue — thread = one query: tcgen05.ld its 128 scores of the tile and
+//   keep its 16 best (score desc, id asc) in registers (branch-free insertion).
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "vx_internal.cuh"
+#include "vx_ptx.cuh"
+
+namespace vx {
+
+constexpr int kTcTD = 128;            // documents per tile (MMA N)
+constexpr int kTcKC = 16;             // per-CTA list length per query
+constexpr int kTcStageUnit = 16384;   // one 128-row x 128-byte operand tile
+
+template <int QT>
+struct TcCfg {
+  static constexpr int EG = QT == 1 ? 1 : 2;               // epilogue warp groups
+  static constexpr int kThreads = (2 + 4 * EG) * 32;
+  static constexpr int NBUF = 2;                            // accumulator buffers
+  static constexpr int kTmemCols = NBUF * QT * kTcTD;       // 256 or 512
+  static constexpr int kStageBytes = (QT + 1) * kTcStageUnit;
+  static constexpr int QPT = QT / EG;                       // query tiles per epilogue thread
+};
+
+__device__ __forceinline__ void insert_desc16(uint64_t (&L)[kTcKC], uint64_t key) {
+#pragma unroll
+  for (int j = 0; j < kTcKC; ++j) {
+    const uint64_t a = L[j];
+    L[j] = a > key ? a : key;
+    key = a > key ? key : a;
+  }
+}
+
+template <int QT>
+__global__ void __launch_bounds__(TcCfg<QT>::kThreads, 1)
+    scan_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tx,
+                   const ScanTcArgs a) {
+  using C = TcCfg<QT>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  const int ns = a.ns;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)ns * C::kStageBytes);
+  uint64_t* empty = full + ns;
+  uint64_t* tfull = empty + ns;
+  uint64_t* tempty = tfull + C::NBUF;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + C::NBUF);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nch = a.D >> 5;
+  const uint32_t n_local = a.n_local;
+  const int ntiles = (int)((n_local + kTcTD - 1) / kTcTD);
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tq);
+    tma_prefetch_desc(&tx);
+    for (int s = 0; s < ns; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < C::NBUF; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4 * C::EG);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, C::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const uint64_t pol_x = policy_evict_first();
+      const uint64_t pol_q = policy_evict_last();
+      const uint32_t bytes = (uint32_t)(QT * a.a_rows * 128 + kTcTD * 128);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (int c = 0; c < nch; ++c) {
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], bytes);
+          uint8_t* st = smem + (size_t)s * C::kStageBytes;
+#pragma unroll
+          for (int qt = 0; qt < QT; ++qt)
+            tma_load_2d(st + qt * kTcStageUnit, &tq, &full[s], c * 32, qt * 128, pol_q);
+          tma_load_2d(st + QT * kTcStageUnit, &tx, &full[s], c * 32, tile * kTcTD, pol_x);
+          if (++s == ns) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer (one thread)
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc(2u /*TF32*/, 128u, (uint32_t)kTcTD);
+      int s = 0;
+      uint32_t ph = 0;
+      int buf = 0;
+      uint32_t bph = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        mbar_wait(&tempty[buf], bph ^ 1);
+        tc_fence_after();
+        for (int c = 0; c < nch; ++c) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t st = smem_u32(smem + (size_t)s * C::kStageBytes);
+#pragma unroll
+          for (int qt = 0; qt < QT; ++qt) {
+            const uint32_t d = tmem_base + (uint32_t)((buf * QT + qt) * kTcTD);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const uint64_t ad = umma_desc_sw128(st + qt * kTcStageUnit + j * 32);
+              const uint64_t bd = umma_desc_sw128(st + QT * kTcStageUnit + j * 32);
+              mma_tf32_ss(d, ad, bd, idesc, (c | j) != 0 ? 1u : 0u);
+            }
+          }
+          mma_commit(&empty[s]);
+          if (++s == ns) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        mma_commit(&tfull[buf]);
+        if (++buf == C::NBUF) {
+          buf = 0;
+          bph ^= 1;
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue: thread = query
+    const int e = warp - 2;
+    const int g = e >> 2;                 // epilogue group
+    const int quad = warp & 3;            // TMEM lane quadrant this warp may access
+    const int m = quad * 32 + lane;       // query row within a 128-query tile
+    uint64_t L[C::QPT][kTcKC];
+#pragma unroll
+    for (int t = 0; t < C::QPT; ++t)
+#pragma unroll
+      for (int j = 0; j < kTcKC; ++j) L[t][j] = 0ull;
+    int buf = 0;
+    uint32_t bph = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      mbar_wait(&tfull[buf], bph);
+      tc_fence_after();
+#pragma unroll
+      for (int t = 0; t < C::QPT; ++t) {
+        const int qt = g + t * C::EG;
+        const int q = qt * 128 + m;
+        const uint32_t col = tmem_base + (uint32_t)((buf * QT + qt) * kTcTD) +
+                             ((uint32_t)(quad * 32) << 16);
+#pragma unroll
+        for (int cc = 0; cc < kTcTD / 32; ++cc) {
+          uint32_t r[32];
+          tmem_ld32(col + cc * 32, r);
+          tmem_ld_wait();
+          if (q < a.B) {
+            float thr = vx_key_score(L[t][kTcKC - 1]);
+            if (L[t][kTcKC - 1] == 0ull) thr = -INFINITY;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float sc = __uint_as_float(r[i]);
+              if (sc >= thr) {
+                const uint32_t doc = (uint32_t)tile * kTcTD + cc * 32 + i;
+                const uint64_t key = vx_make_key(sc, doc);
+                if (doc < n_local && key > L[t][kTcKC - 1]) {
+                  insert_desc16(L[t], key);
+                  thr = vx_key_score(L[t][kTcKC - 1]);
+                  if (L[t][kTcKC - 1] == 0ull) thr = -INFINITY;
+                }
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);
+      if (++buf == C::NBUF) {
+        buf = 0;
+        bph ^= 1;
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < C::QPT; ++t) {
+      const int q = (g + t * C::EG) * 128 + m;
+      if (q < a.B) {
+        uint64_t* out = a.part + ((size_t)q * gridDim.x + blockIdx.x) * kTcKC;
+#pragma unroll
+        for (int j = 0; j < kTcKC; ++j) out[j] = L[t][j];
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, C::kTmemCols);
+  }
+}
+
+// ------------------------------------------------------------------- K2b: exact re-rank
+// One CTA per query.  cand: the merged coarse top-k' keys (score desc); part: the per-CTA
+// lists of K2 (certificate 1); docs/queries fp32.  Writes the exact top-k and flags[b] = 1
+// when the certificate fails (the caller re-scans that query with the exact kernel).
+__global__ void __launch_bounds__(256)
+    rerank_kernel(const float* __restrict__ docs, const float* __restrict__ qv, int D,
+                  const uint64_t* __restrict__ cand, int kp, const uint64_t* __restrict__ part,
+                  int grid, int k, int64_t row0, const float* __restrict__ xnorm_max,
+                  uint64_t* __restrict__ out_keys, int64_t* __restrict__ out_ids,
+                  float* __restrict__ out_scores, int* __restrict__ flags) {
+  extern __shared__ float rsm[];
+  float* qs = rsm;                                             // [D]
+  uint64_t* keys = reinterpret_cast<uint64_t*>(rsm + ((D + 1) & ~1));  // [kp]
+  __shared__ float s_red[32];
+  __shared__ int s_fail;
+  const int b = blockIdx.x;
+  const float* q = qv + (size_t)b * D;
+  float ss = 0.0f;
+  for (int t = threadIdx.x; t < D; t += blockDim.x) {
+    float v = q[t];
+    qs[t] = v;
+    ss = fmaf(v, v, ss);
+  }
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = ss;
+  if (threadIdx.x == 0) s_fail = 0;
+  __syncthreads();
+  const uint64_t* cb = cand + (size_t)b * kp;
+  const uint64_t tprime = cb[kp - 1];  // coarse k'-th key (0: fewer than k' candidates)
+  for (int t = threadIdx.x; t < kp; t += blockDim.x) {
+    const uint64_t ck = cb[t];
+    uint64_t ek = 0ull;
+    if (ck) {
+      const uint32_t id = vx_key_id(ck);
+      const float4* x = reinterpret_cast<const float4*>(docs + (size_t)id * D);
+      float acc = 0.0f;
+      for (int c = 0; c < (D >> 2); ++c) {
+        const float4 xv = __ldg(x + c);
+        acc = fmaf(xv.x, qs[4 * c + 0], acc);
+        acc = fmaf(xv.y, qs[4 * c + 1], acc);
+        acc = fmaf(xv.z, qs[4 * c + 2], acc);
+        acc = fmaf(xv.w, qs[4 * c + 3], acc);
+      }
+      ek = vx_make_key(acc, id);
+    }
+    keys[t] = ek;
+  }
+  // certificate 1: no CTA that truncated its list (16 kept) had its 16th key inside the top-k'
+  for (int t = threadIdx.x; t < grid; t += blockDim.x) {
+    const uint64_t last = part[((size_t)b * grid + t) * kTcKC + (kTcKC - 1)];
+    if (last != 0ull && (tprime == 0ull || last >= tprime)) s_fail = 1;
+  }
+  __syncthreads();
+  // block bitonic sort of the exact keys (kp is a power of two)
+  for (int size = 2; size <= kp; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < (kp >> 1); i += blockDim.x) {
+        int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+        bool desc = (lo & size) == 0;
+        uint64_t x0 = keys[lo], x1 = keys[hi];
+        if ((x0 < x1) == desc) {
+          keys[lo] = x1;
+          keys[hi] = x0;
+        }
+      }
+      __syncthreads();
+    }
+  if (threadIdx.x == 0 && tprime != 0ull) {
+    // certificate 2: every document outside the candidates has coarse score <= s(T'), so
+    // exact score <= s(T') + E; the exact k-th must beat that bound strictly.
+    float qn = 0.0f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) qn += s_red[w];
+    const float E = (0.001953125f + 0.000244140625f) * sqrtf(qn) * 1.0001f * xnorm_max[0] + 1e-30f;
+    const uint64_t ek = keys[k - 1];
+    if (ek == 0ull || !(vx_key_score(ek) > vx_key_score(tprime) + E)) s_fail = 1;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    const uint64_t key = keys[i];
+    const size_t o = (size_t)b * k + i;
+    if (key == 0ull) {
+      out_keys[o] = 0ull;
+      out_ids[o] = -1;
+      out_scores[o] = -INFINITY;
+    } else {
+      const int64_t gid = (int64_t)vx_key_id(key) + row0;
+      out_keys[o] = (key & 0xFFFFFFFF00000000ull) | (uint64_t)(0xFFFFFFFFu - (uint32_t)gid);
+      out_ids[o] = gid;
+      out_scores[o] = vx_key_score(key);
+    }
+  }
+  if (threadIdx.x == 0) flags[b] = s_fail;
+}
+
+// max row L2 norm of the shard (for the certificate's error bound)
+__global__ void row_norm_max_kernel(const float* __restrict__ docs, int64_t n, int D,
+                                    unsigned int* __restrict__ out_bits) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  float best = 0.0f;
+  for (int64_t r = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); r < n;
+       r += (int64_t)gridDim.x * wpb) {
+    const float* x = docs + r * D;
+    float ss = 0.0f;
+    for (int c = lane; c < D; c += 32) ss = fmaf(x[c], x[c], ss);
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    best = fmaxf(best, sqrtf(ss));
+  }
+  if (lane == 0) atomicMax(out_bits, __float_as_uint(best * 1.00001f));
+}
+
+// ------------------------------------------------------------------- host side
+size_t scan_tc_smem(int QT, int* ns_out) {
+  const int stage = (QT + 1) * kTcStageUnit;
+  int ns = QT == 1 ? 6 : 4;
+  *ns_out = ns;
+  return (size_t)ns * stage + (size_t)(2 * ns + 4) * 8 + 16 + 1024;
+}
+
+cudaError_t launch_scan_tc(int QT, const CUtensorMap* tq, const CUtensorMap* tx,
+                           const ScanTcArgs& a, int grid, size_t smem, cudaStream_t st) {
+  if (QT == 1) {
+    auto kfn = scan_tc_kernel<1>;
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kfn<<<grid, TcCfg<1>::kThreads, smem, st>>>(*tq, *tx, a);
+    return cudaGetLastError();
+  }
+  if (QT == 2) {
+    auto kfn = scan_tc_kernel<2>;
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kfn<<<grid, TcCfg<2>::kThreads, smem, st>>>(*tq, *tx, a);
+    return cudaGetLastError();
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64_t* cand, int B,
+                          int kp, const uint64_t* part, int grid, int k, int64_t row0,
+                          const float* xnorm_max, uint64_t* out_keys, int64_t* out_ids,
+                          float* out_scores, int* flags, cudaStream_t st) {
+  size_t smem = (size_t)((D + 1) & ~1) * 4 + (size_t)kp * 8;
+  cudaError_t e = cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  rerank_kernel<<<B, 256, smem, st>>>(docs, q, D, cand, kp, part, grid, k, row0, xnorm_max,
+                                      out_keys, out_ids, out_scores, flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_row_norm_max(const float* docs, int64_t n, int D, unsigned int* out_bits,
+                                cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out_bits, 0, 4, st);
+  if (e != cudaSuccess) return e;
+  int64_t blocks = (n + 7) / 8;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  row_norm_max_kernel<<<(int)(blocks < 1 ? 1 : blocks), 256, 0, st>>>(docs, n, D, out_bits);
+  return cudaGetLastError();
+}
+
+}  // namespace vx

@@ -178,10 +178,15 @@ struct vx_index {
   ShardRec* d_send = nullptr;    // [maxB][maxK]
   ShardRec* d_recv = nullptr;    // [G][maxB][maxK]  (rank 0)
   int32_t* d_hdr = nullptr;      // [4]
+  uint64_t* d_ckeys = nullptr;   // [maxB][256] merged coarse keys (TC path)
+  int* d_flags = nullptr;        // [maxB] certificate failures (TC path)
+  unsigned int* d_xnorm = nullptr;  // max row norm of the shard (float bits)
+  float* d_fq = nullptr;         // [maxB][D] queries gathered for the exact fallback
   // pinned host staging
   void* h_stage = nullptr;
   size_t h_stage_bytes = 0;
   int32_t* h_hdr = nullptr;
+  int* h_flags = nullptr;
   // comm
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
@@ -266,6 +271,10 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
   if (d->n_shards > 1 && d->shard == 0)
     ALLOC(h->d_recv, (size_t)d->n_shards * B * K * sizeof(ShardRec));
   ALLOC(h->d_hdr, 16);
+  ALLOC(h->d_ckeys, B * 256 * 8);
+  ALLOC(h->d_flags, B * 4);
+  ALLOC(h->d_xnorm, 4);
+  ALLOC(h->d_fq, B * D * 4);
 #undef ALLOC
   if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess)
     return cleanup(fail(VX_ERR_CUDA, "stream create"));
@@ -277,6 +286,9 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
     return cleanup(fail(VX_ERR_OOM, "pinned staging"));
   if (cudaMallocHost((void**)&h->h_hdr, 16) != cudaSuccess)
     return cleanup(fail(VX_ERR_OOM, "pinned header"));
+  if (cudaMallocHost((void**)&h->h_flags, B * 4) != cudaSuccess)
+    return cleanup(fail(VX_ERR_OOM, "pinned flags"));
+  if (cudaMemset(h->d_xnorm, 0, 4) != cudaSuccess) return cleanup(fail(VX_ERR_CUDA, "memset"));
   s = make_tmap_2d(&h->tmap_docs, h->docs, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
                    (uint64_t)h->n_local, D, 32, 128);
   if (s != VX_OK) return cleanup(s);
@@ -291,11 +303,13 @@ extern "C" vx_status vx_index_destroy(vx_index* h) {
   if (h->comm) nccl().CommDestroy(h->comm);
   void* ptrs[] = {h->docs,  h->tokens,    h->d_q,      h->d_qtok,    h->d_part, h->d_keys,
                   h->d_ids, h->d_ip,      h->d_ms,     h->d_out_ids, h->d_out_ip,
-                  h->d_out_ms, h->d_send, h->d_recv, h->d_hdr};
+                  h->d_out_ms, h->d_send, h->d_recv, h->d_hdr, h->d_ckeys, h->d_flags,
+                  h->d_xnorm, h->d_fq};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->h_stage) cudaFreeHost(h->h_stage);
   if (h->h_hdr) cudaFreeHost(h->h_hdr);
+  if (h->h_flags) cudaFreeHost(h->h_flags);
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
   if (h->stream) cudaStreamDestroy(h->stream);
@@ -316,7 +330,6 @@ extern "C" vx_status vx_set_option(vx_index* h, int32_t option, int64_t value) {
     case VX_OPT_SCAN:
       if (value != VX_SCAN_AUTO && value != VX_SCAN_F32 && value != VX_SCAN_TC)
         return fail(VX_ERR_INVALID, "scan algorithm %lld", (long long)value);
-      if (value == VX_SCAN_TC) return fail(VX_ERR_UNSUPPORTED, "tensor-core scan not built yet");
       h->scan_algo = (int)value;
       return VX_OK;
     case VX_OPT_GRID:
@@ -346,6 +359,8 @@ extern "C" vx_status vx_index_synth(vx_index* h, uint64_t seed) {
   CU_TRY(cudaSetDevice(h->device));
   CU_TRY(vx::launch_synth_rows(h->docs, seed, h->row0, h->n_local, h->desc.dim, h->stream));
   count_launch(h);
+  CU_TRY(vx::launch_row_norm_max(h->docs, h->n_local, h->desc.dim, h->d_xnorm, h->stream));
+  count_launch(h);
   CU_TRY(cudaStreamSynchronize(h->stream));
   return VX_OK;
 }
@@ -358,6 +373,9 @@ extern "C" vx_status vx_index_upload(vx_index* h, const float* rows, int64_t row
   CU_TRY(cudaSetDevice(h->device));
   CU_TRY(cudaMemcpyAsync(h->docs + (row0 - h->row0) * h->desc.dim, rows,
                          (size_t)n * h->desc.dim * 4, cudaMemcpyHostToDevice, h->stream));
+  // the TC certificate needs an upper bound on the row norms: recompute over the shard
+  CU_TRY(vx::launch_row_norm_max(h->docs, h->n_local, h->desc.dim, h->d_xnorm, h->stream));
+  count_launch(h);
   CU_TRY(cudaStreamSynchronize(h->stream));
   return VX_OK;
 }
@@ -423,9 +441,9 @@ static vx_status check_batch(vx_index* h, int32_t B, int32_t k) {
   return VX_OK;
 }
 
-// local scan + merge: d_q [B][D] -> keys (global ids) / ids / scores [B][k]
-static vx_status local_topk(vx_index* h, const float* d_q, int B, int k, uint64_t* keys,
-                            int64_t* ids, float* scores, cudaStream_t st) {
+// Exact path: K1 scan + merge: d_q [B][D] -> keys (global ids) / ids / scores [B][k]
+static vx_status local_topk_f32(vx_index* h, const float* d_q, int B, int k, uint64_t* keys,
+                                int64_t* ids, float* scores, cudaStream_t st) {
   const int D = h->desc.dim;
   const int kcap = kcap_of(k);
   const int grid = h->grid;
@@ -455,6 +473,86 @@ static vx_status local_topk(vx_index* h, const float* d_q, int B, int k, uint64_
   CU_TRY(vx::launch_merge_topk(h->d_part, B, grid * kcap, k, h->row0, keys, ids, scores, st));
   count_launch(h);
   return VX_OK;
+}
+
+// candidates the TC pass hands to the exact re-rank
+static int kprime_of(int k) { return std::min(256, std::max(64, 4 * next_pow2(k))); }
+
+static bool tc_eligible(const vx_index* h, int B, int k) {
+  (void)h;
+  (void)B;
+  return k <= 128;
+}
+
+// Tensor-core path: K2 coarse scan (top-16 per CTA) -> K3 merge to top-k' -> K2b exact
+// re-rank + certificate -> exact re-scan of any query whose certificate failed.
+static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint64_t* keys,
+                               int64_t* ids, float* scores, cudaStream_t st) {
+  const int D = h->desc.dim;
+  const int grid = h->grid;
+  const int kp = kprime_of(k);
+  CU_TRY(cudaEventRecord(h->ev[0], st));
+  for (int g0 = 0; g0 < B; g0 += 256) {
+    const int Bg = std::min(256, B - g0);
+    const int QT = Bg <= 128 ? 1 : 2;
+    const int a_rows = QT == 1 ? ((Bg + 7) & ~7) : 128;
+    CUtensorMap tq;
+    VX_TRY(make_tmap_2d(&tq, d_q + (size_t)g0 * D, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                        (uint64_t)Bg, D, 32, (uint32_t)a_rows));
+    int ns = 0;
+    const size_t smem = vx::scan_tc_smem(QT, &ns);
+    vx::ScanTcArgs a;
+    a.n_local = (uint32_t)h->n_local;
+    a.D = D;
+    a.B = Bg;
+    a.ns = ns;
+    a.a_rows = a_rows;
+    a.part = h->d_part + (size_t)g0 * grid * vx::kTcListLen;
+    CU_TRY(vx::launch_scan_tc(QT, &tq, &h->tmap_docs, a, grid, smem, st));
+    count_launch(h);
+  }
+  CU_TRY(cudaEventRecord(h->ev[1], st));
+  CU_TRY(vx::launch_merge_topk(h->d_part, B, grid * vx::kTcListLen, kp, 0, h->d_ckeys, nullptr,
+                               nullptr, st));
+  count_launch(h);
+  CU_TRY(vx::launch_rerank(h->docs, d_q, D, h->d_ckeys, B, kp, h->d_part, grid, k, h->row0,
+                           reinterpret_cast<const float*>(h->d_xnorm), keys, ids, scores,
+                           h->d_flags, st));
+  count_launch(h);
+  // certificate failures: re-scan those queries exactly (expected ~never on real data)
+  CU_TRY(cudaMemcpyAsync(h->h_flags, h->d_flags, (size_t)B * 4, cudaMemcpyDeviceToHost, st));
+  CU_TRY(cudaStreamSynchronize(st));
+  std::vector<int> bad;
+  for (int b = 0; b < B; ++b)
+    if (h->h_flags[b]) bad.push_back(b);
+  if (bad.empty()) return VX_OK;
+  h->st.cert_fallbacks += bad.size();
+  for (size_t i = 0; i < bad.size(); ++i)
+    CU_TRY(cudaMemcpyAsync(h->d_fq + i * D, d_q + (size_t)bad[i] * D, (size_t)D * 4,
+                           cudaMemcpyDeviceToDevice, st));
+  const int nb = (int)bad.size();
+  uint64_t* fk = h->d_ckeys;  // reuse: [nb][k] (k <= 256)
+  int64_t* fi = h->d_out_ids;
+  float* fs = h->d_out_ms;
+  VX_TRY(local_topk_f32(h, h->d_fq, nb, k, fk, fi, fs, st));
+  for (int i = 0; i < nb; ++i) {
+    const size_t o = (size_t)bad[i] * k, s = (size_t)i * k;
+    CU_TRY(cudaMemcpyAsync(keys + o, fk + s, (size_t)k * 8, cudaMemcpyDeviceToDevice, st));
+    CU_TRY(cudaMemcpyAsync(ids + o, fi + s, (size_t)k * 8, cudaMemcpyDeviceToDevice, st));
+    CU_TRY(cudaMemcpyAsync(scores + o, fs + s, (size_t)k * 4, cudaMemcpyDeviceToDevice, st));
+  }
+  return VX_OK;
+}
+
+static vx_status local_topk(vx_index* h, const float* d_q, int B, int k, uint64_t* keys,
+                            int64_t* ids, float* scores, cudaStream_t st) {
+  const bool tc = h->scan_algo == VX_SCAN_TC ||
+                  (h->scan_algo == VX_SCAN_AUTO && tc_eligible(h, B, k) && B > 4);
+  if (tc) {
+    if (!tc_eligible(h, B, k)) return fail(VX_ERR_UNSUPPORTED, "tensor-core scan needs k <= 128");
+    return local_topk_tc(h, d_q, B, k, keys, ids, scores, st);
+  }
+  return local_topk_f32(h, d_q, B, k, keys, ids, scores, st);
 }
 
 static vx_status run_maxsim(vx_index* h, const float* d_qtok, int B, int nq, const int64_t* d_cand,

@@ -29,6 +29,26 @@ cudaError_t launch_scan_f32(int bucket, const CUtensorMap* tmap, const ScanF32Ar
                             size_t smem, cudaStream_t st);
 int scan_f32_tile_docs(int bucket);
 
+// -------- tensor-core coarse scan (K2) + exact re-rank (K2b): scan_tc.cu
+struct ScanTcArgs {
+  uint32_t n_local;  // rows in the shard
+  int32_t D;         // dimension (multiple of 32)
+  int32_t B;         // queries in this launch (<= QT*128)
+  int32_t ns;        // pipeline stages
+  int32_t a_rows;    // TMA box rows of the query map (multiple of 8, <= 128)
+  uint64_t* part;    // [B][gridDim.x][16] coarse keys
+};
+constexpr int kTcListLen = 16;
+size_t scan_tc_smem(int QT, int* ns_out);
+cudaError_t launch_scan_tc(int QT, const CUtensorMap* tq, const CUtensorMap* tx,
+                           const ScanTcArgs& a, int grid, size_t smem, cudaStream_t st);
+cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64_t* cand, int B,
+                          int kp, const uint64_t* part, int grid, int k, int64_t row0,
+                          const float* xnorm_max, uint64_t* out_keys, int64_t* out_ids,
+                          float* out_scores, int* flags, cudaStream_t st);
+cudaError_t launch_row_norm_max(const float* docs, int64_t n, int D, unsigned int* out_bits,
+                                cudaStream_t st);
+
 // -------- top-k merge (K3): topk.cu
 // For each query q: select the k largest keys among in[q][0..M), write them
 // descending to out_keys[q][k] (re-keyed with id + id_base), ids (-1 for empty) and scores.

@@ -192,3 +192,41 @@ def test_stats_count_launches(vx):
         idx.search(np.ones((4, 128), np.float32), 10)
         st = idx.stats()
     assert st["kernel_launches"] >= 2 and st["batches"] == 1 and st["queries"] == 4
+
+
+# ------------------------------------------------------------------ tensor-core scan (K2)
+@pytest.mark.parametrize("N,D,B,k", [
+    (100_000, 768, 16, 10), (50_000, 768, 1, 1), (20_000, 1024, 8, 100), (12_345, 768, 32, 100),
+    (30_000, 768, 128, 128), (40_000, 256, 129, 10), (25_000, 768, 256, 100), (9_000, 128, 300, 64),
+    (4097, 64, 5, 7), (1000, 32, 3, 5)])
+def test_tc_scan_bit_identical_to_oracle_f32(vx, oracle, N, D, B, k):
+    X = oracle.synth_rows(42, 0, N, D)
+    Q = oracle.synth_rows(43, 0, B, D)
+    with vx.Index(N, D, max_batch=B, max_k=k) as idx:
+        idx.synth(42)
+        idx.set_option(vx.VX_OPT_SCAN, vx.VX_SCAN_TC)
+        ids, sc = idx.search(Q, k)
+        fallbacks = idx.stats()["cert_fallbacks"]
+    rid, rsc = oracle.flat_topk(X, Q, k, mode=1)
+    assert np.array_equal(ids, rid)
+    v = rid >= 0
+    assert np.array_equal(sc[v], rsc[v].astype(np.float32))
+    if N >= 10_000:
+        assert fallbacks == 0
+
+
+def test_tc_certificate_forces_exact_fallback(vx, oracle):
+    # 600 identical rows + noise rows: coarse scores tie massively, the certificate cannot
+    # separate the k-th from the candidate boundary -> exact re-scan, still exact results
+    N, D, B, k = 3000, 128, 4, 10
+    X = oracle.synth_rows(42, 0, N, D)
+    X[:600] = X[0]
+    Q = np.stack([X[0], X[0], oracle.synth_rows(43, 0, 1, D)[0], X[5]])
+    with vx.Index(N, D, max_batch=B, max_k=k) as idx:
+        idx.upload(X)
+        idx.set_option(vx.VX_OPT_SCAN, vx.VX_SCAN_TC)
+        ids, sc = idx.search(Q, k)
+        st = idx.stats()
+    rid, rsc = oracle.flat_topk(X, Q, k, mode=1)
+    assert np.array_equal(ids, rid)
+    assert st["cert_fallbacks"] >= 2
