@@ -53,6 +53,7 @@ def test_scan_bit_identical_to_oracle_f32(vx, oracle, N, D, B, k):
     Q = oracle.synth_rows(43, 0, B, D)
     with vx.Index(N, D, max_batch=max(B, 1), max_k=max(k, 1)) as idx:
         idx.synth(42)
+        idx.set_option(vx.VX_OPT_SCAN, vx.VX_SCAN_F32)
         ids, sc = idx.search(Q, k)
     rid, rsc = oracle.flat_topk(X, Q, k, mode=1)
     assert np.array_equal(ids, rid)
