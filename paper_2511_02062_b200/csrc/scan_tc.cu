@@ -38,13 +38,27 @@ struct TcCfg {
   static constexpr int QPT = QT / EG;                       // query tiles per epilogue thread
 };
 
-__device__ __forceinline__ void insert_desc16(uint64_t (&L)[kTcKC], uint64_t key) {
-#pragma unroll
-  for (int j = 0; j < kTcKC; ++j) {
-    const uint64_t a = L[j];
-    L[j] = a > key ? a : key;
-    key = a > key ? key : a;
+// Insert a candidate into one query's descending list (smem, stride `ld` between entries)
+// and return the new admission threshold.  Out of line on purpose: the caller tests 128
+// scores per tile inline, and an inlined insertion per score would blow the I-cache
+// (measured: 4x slower epilogue).
+__device__ __noinline__ float tc_list_insert(uint64_t* L, int ld, float sc, uint32_t doc,
+                                             uint32_t n_local) {
+  const uint64_t last = L[(kTcKC - 1) * ld];
+  if (doc < n_local) {
+    uint64_t key = vx_make_key(sc, doc);
+    if (key > last) {
+      for (int j = 0; j < kTcKC; ++j) {
+        const uint64_t a = L[j * ld];
+        if (key > a) {
+          L[j * ld] = key;
+          key = a;
+        }
+      }
+    }
   }
+  const uint64_t nl = L[(kTcKC - 1) * ld];
+  return nl == 0ull ? -INFINITY : vx_key_score(nl);
 }
 
 template <int QT>
@@ -55,7 +69,9 @@ __global__ void __launch_bounds__(TcCfg<QT>::kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   const int ns = a.ns;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)ns * C::kStageBytes);
+  // per-query candidate lists: [QT*128 queries][16] keys, entry j of query q at [j][q]
+  uint64_t* lists = reinterpret_cast<uint64_t*>(smem + (size_t)ns * C::kStageBytes);
+  uint64_t* full = lists + (size_t)QT * 128 * kTcKC;
   uint64_t* empty = full + ns;
   uint64_t* tfull = empty + ns;
   uint64_t* tempty = tfull + C::NBUF;
@@ -153,11 +169,14 @@ __global__ void __launch_bounds__(TcCfg<QT>::kThreads, 1)
     const int g = e >> 2;                 // epilogue group
     const int quad = warp & 3;            // TMEM lane quadrant this warp may access
     const int m = quad * 32 + lane;       // query row within a 128-query tile
-    uint64_t L[C::QPT][kTcKC];
+    constexpr int LD = QT * 128;          // list stride (entries of one query are LD apart)
+    float thr[C::QPT];
 #pragma unroll
-    for (int t = 0; t < C::QPT; ++t)
-#pragma unroll
-      for (int j = 0; j < kTcKC; ++j) L[t][j] = 0ull;
+    for (int t = 0; t < C::QPT; ++t) {
+      const int qt = g + t * C::EG;
+      for (int j = 0; j < kTcKC; ++j) lists[j * LD + qt * 128 + m] = 0ull;
+      thr[t] = -INFINITY;
+    }
     int buf = 0;
     uint32_t bph = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -167,28 +186,20 @@ __global__ void __launch_bounds__(TcCfg<QT>::kThreads, 1)
       for (int t = 0; t < C::QPT; ++t) {
         const int qt = g + t * C::EG;
         const int q = qt * 128 + m;
+        uint64_t* L = lists + qt * 128 + m;
         const uint32_t col = tmem_base + (uint32_t)((buf * QT + qt) * kTcTD) +
                              ((uint32_t)(quad * 32) << 16);
-#pragma unroll
+#pragma unroll 1
         for (int cc = 0; cc < kTcTD / 32; ++cc) {
           uint32_t r[32];
           tmem_ld32(col + cc * 32, r);
           tmem_ld_wait();
           if (q < a.B) {
-            float thr = vx_key_score(L[t][kTcKC - 1]);
-            if (L[t][kTcKC - 1] == 0ull) thr = -INFINITY;
+            const uint32_t doc0 = (uint32_t)tile * kTcTD + cc * 32;
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               const float sc = __uint_as_float(r[i]);
-              if (sc >= thr) {
-                const uint32_t doc = (uint32_t)tile * kTcTD + cc * 32 + i;
-                const uint64_t key = vx_make_key(sc, doc);
-                if (doc < n_local && key > L[t][kTcKC - 1]) {
-                  insert_desc16(L[t], key);
-                  thr = vx_key_score(L[t][kTcKC - 1]);
-                  if (L[t][kTcKC - 1] == 0ull) thr = -INFINITY;
-                }
-              }
+              if (sc >= thr[t]) thr[t] = tc_list_insert(L, LD, sc, doc0 + i, n_local);
             }
           }
         }
@@ -203,11 +214,11 @@ __global__ void __launch_bounds__(TcCfg<QT>::kThreads, 1)
     }
 #pragma unroll
     for (int t = 0; t < C::QPT; ++t) {
-      const int q = (g + t * C::EG) * 128 + m;
+      const int qt = g + t * C::EG;
+      const int q = qt * 128 + m;
       if (q < a.B) {
         uint64_t* out = a.part + ((size_t)q * gridDim.x + blockIdx.x) * kTcKC;
-#pragma unroll
-        for (int j = 0; j < kTcKC; ++j) out[j] = L[t][j];
+        for (int j = 0; j < kTcKC; ++j) out[j] = lists[j * LD + qt * 128 + m];
       }
     }
   }
@@ -335,7 +346,7 @@ size_t scan_tc_smem(int QT, int* ns_out) {
   const int stage = (QT + 1) * kTcStageUnit;
   int ns = QT == 1 ? 6 : 4;
   *ns_out = ns;
-  return (size_t)ns * stage + (size_t)(2 * ns + 4) * 8 + 16 + 1024;
+  return (size_t)ns * stage + (size_t)QT * 128 * kTcKC * 8 + (size_t)(2 * ns + 4) * 8 + 16 + 1024;
 }
 
 cudaError_t launch_scan_tc(int QT, const CUtensorMap* tq, const CUtensorMap* tx,
