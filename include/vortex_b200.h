@@ -59,8 +59,11 @@ enum { VX_SCAN_AUTO = 0, VX_SCAN_F32 = 1, VX_SCAN_TC = 2 };
 enum {
   VX_OPT_SCAN = 1,        /* one of VX_SCAN_* */
   VX_OPT_GRID = 2,        /* CTAs for the scan (0 = auto: one per SM) */
-  VX_OPT_GRAPHS = 3       /* 1 = replay pre-captured CUDA graphs per batch bucket */
+  VX_OPT_GRAPHS = 3,      /* 1 = replay pre-captured CUDA graphs per batch bucket */
+  VX_OPT_MAXSIM = 4       /* one of VX_MAXSIM_* */
 };
+/* MaxSim kernel selection (vx_set_option VX_OPT_MAXSIM). */
+enum { VX_MAXSIM_AUTO = 0, VX_MAXSIM_CC = 1, VX_MAXSIM_TC = 2 };
 
 typedef struct vx_index_desc {
   int64_t n_docs;      /* global document count N (1 <= N < 2^32) */

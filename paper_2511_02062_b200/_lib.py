@@ -17,7 +17,8 @@ VX_OK = 0
 STATUS = {0: "VX_OK", 1: "VX_ERR_INVALID", 2: "VX_ERR_CUDA", 3: "VX_ERR_OOM", 4: "VX_ERR_NCCL",
           5: "VX_ERR_STATE", 6: "VX_ERR_UNSUPPORTED"}
 VX_SCAN_AUTO, VX_SCAN_F32, VX_SCAN_TC = 0, 1, 2
-VX_OPT_SCAN, VX_OPT_GRID, VX_OPT_GRAPHS = 1, 2, 3
+VX_OPT_SCAN, VX_OPT_GRID, VX_OPT_GRAPHS, VX_OPT_MAXSIM = 1, 2, 3, 4
+VX_MAXSIM_AUTO, VX_MAXSIM_CC, VX_MAXSIM_TC = 0, 1, 2
 
 
 class VxError(RuntimeError):

@@ -1,0 +1,225 @@
+// maxsim_tc.cu — K4: fused tensor-core MaxSim (tcgen05 kind::f16, bf16 in / fp32 accumulate)
+//   score(q, d) = sum_{i<Nq} max_{j<Nd} <q_i, d_j>          (ColBERT late interaction)
+//
+// One CTA per (query, chunk of its candidates); 2 CTAs per SM.
+//   A = the query's tokens, bf16, M = 128 rows (rows >= Nq are zero), resident in smem for
+//       the whole chunk (written once by the CTA, SWIZZLE_128B, K-major);
+//   B = one candidate's doc-token block [Nd rows][d] bf16, TMA-streamed from the token store
+//       (block = id mod T), NS-stage ring;
+//   D = TMEM accumulator [query token (lane)][doc token (column)], double-buffered.
+// Epilogue (4 warps): thread = query token; tcgen05.ld its Nd scores, row max in registers,
+// warp-sum over query tokens, cross-warp sum in smem -> one fp32 score per candidate.  The
+// token x token matrix never leaves the SM.
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "vx_internal.cuh"
+#include "vx_ptx.cuh"
+
+namespace vx {
+
+constexpr int kMsStages = 2;
+constexpr int kMsThreads = 6 * 32;  // producer, MMA, 4 epilogue warps
+
+template <int ND, int DK>
+struct MsCfg {
+  static constexpr int kATile = 128 * 128;                 // one K-block of A: 128 rows x 128 B
+  static constexpr int kABytes = DK * kATile;
+  static constexpr int kStageBytes = DK * ND * 128;        // one candidate block
+  static constexpr int kTmemCols = 2 * ND;                 // double-buffered accumulator
+  static constexpr size_t kSmem = (size_t)kABytes + (size_t)kMsStages * kStageBytes +
+                                  (2 * kMsStages + 4) * 8 + 2 * 4 * 4 + 16 + 1024;
+};
+
+template <int ND, int DK>
+__global__ void __launch_bounds__(kMsThreads, 2)
+    maxsim_tc_kernel(const __grid_constant__ CUtensorMap tt, const MaxSimArgs a, int chunk,
+                     int cpq) {
+  using C = MsCfg<ND, DK>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + (size_t)kMsStages * C::kStageBytes);
+  uint64_t* empty = full + kMsStages;
+  uint64_t* tfull = empty + kMsStages;
+  uint64_t* tempty = tfull + 2;
+  float* partial = reinterpret_cast<float*>(tempty + 2);  // [2 bufs][4 quads]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(partial + 8);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x / cpq;
+  const int c0 = (blockIdx.x % cpq) * chunk;
+  const int c1 = min(a.C, c0 + chunk);
+  const int nq = a.nq;
+  const int64_t* cand = a.cand + (size_t)b * a.C;
+
+  // A tile: query tokens -> bf16 (RNE), SWIZZLE_128B K-major; rows >= nq are zero
+  {
+    const float* qt = a.qtok + (size_t)b * nq * a.d;
+    const int chunks16 = DK * 128 * 8;  // 16-byte chunks in the A tile
+    for (int i = threadIdx.x; i < chunks16; i += blockDim.x) {
+      const int kb = i / (128 * 8), rem = i % (128 * 8), r = rem >> 3, ch = rem & 7;
+      uint32_t w[4] = {0, 0, 0, 0};
+      if (r < nq) {
+        const float* src = qt + (size_t)r * a.d + kb * 64 + ch * 8;
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          w[e] = (uint32_t)vx_f32_to_bf16_bits(src[2 * e]) |
+                 ((uint32_t)vx_f32_to_bf16_bits(src[2 * e + 1]) << 16);
+      }
+      uint4* dst = reinterpret_cast<uint4*>(sA + kb * C::kATile + r * 128 + ((ch ^ (r & 7)) << 4));
+      *dst = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tt);
+    for (int s = 0; s < kMsStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+    }
+    fence_barrier_init();
+  }
+  fence_proxy_async();  // generic-proxy smem writes (A tile) -> visible to the tensor core
+  if (warp == 1) tmem_alloc(tmem_slot, C::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      int s = 0;
+      uint32_t ph = 0;
+      for (int c = c0; c < c1; ++c) {
+        const int64_t id = cand[c];
+        const int64_t blk = id < 0 ? 0 : id % a.T;
+        mbar_wait(&empty[s], ph ^ 1);
+        mbar_expect_tx(&full[s], C::kStageBytes);
+#pragma unroll
+        for (int kb = 0; kb < DK; ++kb)
+          tma_load_2d(sB + (size_t)s * C::kStageBytes + kb * ND * 128, &tt, &full[s], kb * 64,
+                      (int32_t)(blk * a.Nd), pol);
+        if (++s == kMsStages) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc(1u /*BF16*/, 128u, (uint32_t)ND);
+      int s = 0, buf = 0;
+      uint32_t ph = 0, bph = 0;
+      for (int c = c0; c < c1; ++c) {
+        mbar_wait(&tempty[buf], bph ^ 1);
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        const uint32_t aa = smem_u32(sA);
+        const uint32_t bb = smem_u32(sB + (size_t)s * C::kStageBytes);
+#pragma unroll
+        for (int kb = 0; kb < DK; ++kb)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            mma_f16_ss(tmem_base + (uint32_t)(buf * ND),
+                       umma_desc_sw128(aa + kb * C::kATile + j * 32),
+                       umma_desc_sw128(bb + kb * ND * 128 + j * 32), idesc,
+                       (kb | j) != 0 ? 1u : 0u);
+        mma_commit(&empty[s]);
+        mma_commit(&tfull[buf]);
+        if (++s == kMsStages) {
+          s = 0;
+          ph ^= 1;
+        }
+        if (++buf == 2) {
+          buf = 0;
+          bph ^= 1;
+        }
+      }
+    }
+  } else {
+    const int quad = warp & 3;
+    const bool active = quad * 32 < nq;  // warp-uniform: does this lane quadrant hold tokens?
+    int buf = 0;
+    uint32_t bph = 0;
+    for (int c = c0; c < c1; ++c) {
+      mbar_wait(&tfull[buf], bph);
+      tc_fence_after();
+      float mx = -INFINITY;
+      if (active) {
+        const uint32_t col = tmem_base + (uint32_t)(buf * ND) + ((uint32_t)(quad * 32) << 16);
+#pragma unroll
+        for (int cc = 0; cc < ND / 32; ++cc) {
+          uint32_t r[32];
+          tmem_ld32(col + cc * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(r[i]));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);
+      float v = (active && quad * 32 + lane < nq) ? mx : 0.0f;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) partial[buf * 4 + quad] = v;
+      named_bar_sync(1, 128);
+      if (warp == 2 && lane == 0) {
+        const float total = partial[buf * 4 + 0] + partial[buf * 4 + 1] + partial[buf * 4 + 2] +
+                            partial[buf * 4 + 3];
+        a.out[(size_t)b * a.C + c] = cand[c] < 0 ? -INFINITY : total;
+      }
+      if (++buf == 2) {
+        buf = 0;
+        bph ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, C::kTmemCols);
+  }
+}
+
+template <int ND, int DK>
+static cudaError_t launch_ms(const CUtensorMap* tt, const MaxSimArgs& a, cudaStream_t st) {
+  using C = MsCfg<ND, DK>;
+  auto kfn = maxsim_tc_kernel<ND, DK>;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
+  if (e != cudaSuccess) return e;
+  // enough CTAs to cover 2 per SM, at least 2 candidates per CTA (pipeline)
+  const long pairs = (long)a.B * a.C;
+  int chunk = (int)((pairs + 2 * 148 - 1) / (2 * 148));
+  chunk = chunk < 2 ? 2 : (chunk > 64 ? 64 : chunk);
+  const int cpq = (a.C + chunk - 1) / chunk;
+  kfn<<<a.B * cpq, kMsThreads, C::kSmem, st>>>(*tt, a, chunk, cpq);
+  return cudaGetLastError();
+}
+
+bool maxsim_tc_supported(int nq, int Nd, int d) {
+  return nq >= 1 && nq <= 128 && (Nd == 64 || Nd == 128 || Nd == 256) && (d == 64 || d == 128);
+}
+
+cudaError_t launch_maxsim_tc(const CUtensorMap* tt, const MaxSimArgs& a, cudaStream_t st) {
+  if (a.B <= 0 || a.C <= 0) return cudaSuccess;
+  if (a.d == 128) {
+    if (a.Nd == 128) return launch_ms<128, 2>(tt, a, st);
+    if (a.Nd == 64) return launch_ms<64, 2>(tt, a, st);
+    if (a.Nd == 256) return launch_ms<256, 2>(tt, a, st);
+  } else if (a.d == 64) {
+    if (a.Nd == 128) return launch_ms<128, 1>(tt, a, st);
+    if (a.Nd == 64) return launch_ms<64, 1>(tt, a, st);
+    if (a.Nd == 256) return launch_ms<256, 1>(tt, a, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace vx

@@ -161,8 +161,10 @@ struct vx_index {
   float* docs = nullptr;
   uint16_t* tokens = nullptr;
   CUtensorMap tmap_docs{};
+  CUtensorMap tmap_tok{};
   // options
   int scan_algo = VX_SCAN_AUTO;
+  int maxsim_algo = VX_MAXSIM_AUTO;
   int grid = 0;
   // workspace
   float* d_q = nullptr;          // [maxB][D]
@@ -289,6 +291,12 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
   if (cudaMallocHost((void**)&h->h_flags, B * 4) != cudaSuccess)
     return cleanup(fail(VX_ERR_OOM, "pinned flags"));
   if (cudaMemset(h->d_xnorm, 0, 4) != cudaSuccess) return cleanup(fail(VX_ERR_CUDA, "memset"));
+  if (h->tokens) {
+    s = make_tmap_2d(&h->tmap_tok, h->tokens, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                     (uint64_t)d->tok_blocks * d->tok_per_doc, (uint64_t)d->tok_dim, 64,
+                     (uint32_t)std::min(d->tok_per_doc, 256));
+    if (s != VX_OK) return cleanup(s);
+  }
   s = make_tmap_2d(&h->tmap_docs, h->docs, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
                    (uint64_t)h->n_local, D, 32, 128);
   if (s != VX_OK) return cleanup(s);
@@ -335,6 +343,14 @@ extern "C" vx_status vx_set_option(vx_index* h, int32_t option, int64_t value) {
     case VX_OPT_GRID:
       if (value < 0 || value > h->num_sms) return fail(VX_ERR_INVALID, "grid %lld", (long long)value);
       h->grid = value == 0 ? h->num_sms : (int)value;
+      return VX_OK;
+    case VX_OPT_MAXSIM:
+      if (value != VX_MAXSIM_AUTO && value != VX_MAXSIM_CC && value != VX_MAXSIM_TC)
+        return fail(VX_ERR_INVALID, "maxsim algorithm %lld", (long long)value);
+      if (value == VX_MAXSIM_TC && h->tokens &&
+          !vx::maxsim_tc_supported(h->desc.max_qtok, h->desc.tok_per_doc, h->desc.tok_dim))
+        return fail(VX_ERR_UNSUPPORTED, "tensor-core MaxSim needs Nd in {64,128,256}, d in {64,128}");
+      h->maxsim_algo = (int)value;
       return VX_OK;
     case VX_OPT_GRAPHS:
       return value == 0 ? VX_OK : fail(VX_ERR_UNSUPPORTED, "graphs not built yet");
@@ -570,7 +586,14 @@ static vx_status run_maxsim(vx_index* h, const float* d_qtok, int B, int nq, con
   a.Nd = h->desc.tok_per_doc;
   a.d = h->desc.tok_dim;
   a.out = d_out;
-  CU_TRY(vx::launch_maxsim(a, st));
+  const bool tc = h->maxsim_algo != VX_MAXSIM_CC &&
+                  vx::maxsim_tc_supported(nq, a.Nd, a.d);
+  if (h->maxsim_algo == VX_MAXSIM_TC && !tc)
+    return fail(VX_ERR_UNSUPPORTED, "tensor-core MaxSim unsupported for nq=%d Nd=%d d=%d", nq, a.Nd, a.d);
+  if (tc)
+    CU_TRY(vx::launch_maxsim_tc(&h->tmap_tok, a, st));
+  else
+    CU_TRY(vx::launch_maxsim(a, st));
   count_launch(h);
   return VX_OK;
 }

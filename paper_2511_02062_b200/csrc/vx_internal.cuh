@@ -77,5 +77,7 @@ struct MaxSimArgs {
   float* out;            // [B][C]
 };
 cudaError_t launch_maxsim(const MaxSimArgs& a, cudaStream_t st);
+bool maxsim_tc_supported(int nq, int Nd, int d);
+cudaError_t launch_maxsim_tc(const CUtensorMap* tt, const MaxSimArgs& a, cudaStream_t st);
 
 }  // namespace vx
