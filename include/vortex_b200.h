@@ -139,6 +139,28 @@ vx_status vx_search_rescore_dev(vx_index* h, const float* d_queries, const float
 /* Wait for the handle's work; samples the last batch's scan/stage device times. */
 vx_status vx_sync(vx_index* h);
 
+/* ---- Opportunistic, SLO-bounded batcher (reference: Runtime::maybe_dispatch,
+ * proj/include/vortex/runtime.hpp:617-654: when the member is idle, dispatch the
+ * min(|queue|, cap) oldest queries, never wait to fill).
+ *
+ * vx_batcher_simulate: replay on a virtual clock with a piecewise-linear latency profile
+ * L(b) (knots, profile.hpp:90-109); no GPU.  arrivals_us sorted ascending.  Per query:
+ * batch index, dispatch and completion time (us).  Completion = dispatch +
+ * trunc(L(b)*1000) us, as SimExecutor::execute_batch (executor.hpp:172-182). */
+vx_status vx_batcher_simulate(const uint64_t* arrivals_us, int64_t n, int32_t cap,
+                              const int32_t* knot_batch, const double* knot_ms, int32_t n_knots,
+                              int64_t* batch_of, uint64_t* dispatch_us, uint64_t* complete_us,
+                              int64_t* n_batches);
+/* vx_serve_trace: live mode — replays the arrival trace in wall-clock time through the
+ * same batcher onto this handle's GPU stage (one batch in flight; each dispatched batch
+ * is copied host->device, searched (and re-scored when qtok != NULL), and its results
+ * copied back before the batch completes).  queries [n][D], qtok [n][nq][d] or NULL.
+ * latency_us[i] = completion - planned arrival (bench.hpp:222).  ids [n][k] optional. */
+vx_status vx_serve_trace(vx_index* h, const uint64_t* arrivals_us, int64_t n, int32_t cap,
+                         const float* queries, const float* qtok, int32_t nq, int32_t k,
+                         int64_t* ids, double* latency_us, int64_t* batch_of,
+                         int64_t* n_batches);
+
 /* Multi-GPU (one process per GPU).  Rank 0 creates the id, the host plumbing
  * (torch.distributed / MPI / a file) distributes the 128 bytes, every rank
  * calls vx_comm_init.  Ranks != 0 then call vx_shard_serve(), which returns

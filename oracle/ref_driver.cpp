@@ -1,0 +1,182 @@
+// ref_driver.cpp — drives the REFERENCE's own runtime (header-only C++20 under
+// /root/reference/proj/include, compiled where it lies by oracle/Makefile into oracle/_ref/).
+// TEST INFRASTRUCTURE: the checker for the batcher and the drop-in boundary.
+//
+//   vortex_ref_driver batcher <arrivals.txt> <cap> <b:ms,b:ms,...>
+//       One-stage pipeline ("D" / modelD, stage max_batch = cap) on the reference
+//       SimExecutor with the given profile knots.  Registers a recording ComponentFn and
+//       prints, per query (input order): "<index> <batch> <dispatch_us> <complete_us>",
+//       times relative to the first instant after the warm model load.
+//       (runtime.hpp:617-672, executor.hpp:172-182, profile.hpp:90-109)
+//
+//   vortex_ref_driver operator <N> <D> <k> <B> <nq> <T>
+//       Registers the B200 stage (include/vortex_b200_component.hpp over
+//       libvortex_b200.so) as "modelD" in the reference Runtime and pushes B synthetic
+//       queries (vx_synth.h seeds 43/44) through the reference batcher with cap 4
+//       (pipeline.json:7).  Prints one line per query: "<index> <id> <id> ..." (needs a GPU).
+#include <cstdio>
+#include <cstdlib>
+#include <fstream>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "vortex/runtime.hpp"
+
+#ifdef VX_WITH_B200
+#include <cmath>
+
+#include "vortex_b200_component.hpp"
+#include "vx_synth.h"
+#endif
+
+using namespace vortex;
+
+static std::vector<std::pair<int, double>> parse_knots(const std::string& s) {
+  std::vector<std::pair<int, double>> out;
+  for (const auto& tok : split(s, ',')) {
+    auto kv = split(tok, ':');
+    out.emplace_back(std::stoi(kv.at(0)), std::stod(kv.at(1)));
+  }
+  return out;
+}
+
+struct World {
+  sim::EventLoop loop;
+  kvs::HandlerRegistry handlers;
+  kvs::Store store{loop, handlers};
+  exec::ProfileTable prof;
+  std::unique_ptr<exec::SimExecutor> ex;
+  std::unique_ptr<runtime::Runtime> rt;
+  std::map<std::string, std::vector<exec::Instance*>> pools;
+  runtime::PipelineSpec spec;
+
+  World(int cap, const std::vector<std::pair<int, double>>& knots) {
+    for (auto [b, ms] : knots) prof.add("modelD", 24, exec::ProfileEntry{b, ms, 1000.0 * b / ms, 1});
+    ex = std::make_unique<exec::SimExecutor>(loop, prof);
+    rt = std::make_unique<runtime::Runtime>(loop, store, handlers, *ex);
+    int node = ex->add_node(24);
+    ex->partition_node(node, exec::MIGLayout{{24}});
+    pools["modelD"] = {&ex->instance(node, 0)};
+    spec.name = "search";
+    spec.stages = {{"D", "modelD", cap, {}, {}}};
+    spec.ingress = "D";
+    spec.egress = "D";
+  }
+};
+
+static int run_batcher(int argc, char** argv) {
+  if (argc < 5) return 2;
+  std::ifstream in(argv[2]);
+  std::vector<sim::micros> arr;
+  for (unsigned long long t; in >> t;) arr.push_back(t);
+  const int cap = std::atoi(argv[3]);
+  World w(cap, parse_knots(argv[4]));
+  std::vector<std::vector<int>> batches;
+  w.rt->register_component("modelD", [&](const std::vector<Payload>& inputs) {
+    std::vector<int> b;
+    for (const auto& p : inputs) b.push_back(std::stoi(payload_str(p)));
+    batches.push_back(b);
+    return inputs;  // output i <-> input i
+  });
+  w.rt->load_pipeline(w.spec, w.pools);  // warm start: runs the model load to completion
+  const sim::micros t0 = w.loop.now();
+  std::map<std::uint64_t, int> qid_of;
+  for (size_t i = 0; i < arr.size(); ++i)
+    w.loop.at(t0 + arr[i], [&, i] {
+      qid_of[w.rt->ingress_submit("search", make_payload(std::to_string(i)))] = (int)i;
+    });
+  w.loop.run_all();
+  std::vector<int> batch_of(arr.size(), -1);
+  for (size_t b = 0; b < batches.size(); ++b)
+    for (int i : batches[b]) batch_of[i] = (int)b;
+  for (const auto& [qid, i] : qid_of) {
+    const auto& rec = w.rt->record("search", qid);
+    const auto& tr = rec.stages.at("D");
+    std::printf("%d %d %llu %llu\n", i, batch_of[i], (unsigned long long)(tr.dispatch - t0),
+                (unsigned long long)(rec.egress_ts - t0));
+  }
+  return 0;
+}
+
+#ifdef VX_WITH_B200
+static std::vector<float> synth_row(uint64_t seed, uint64_t row, int dim) {
+  std::vector<int32_t> v(dim);
+  int64_t ss = 0;
+  for (int c = 0; c < dim; ++c) {
+    v[c] = vx_synth_int(seed, row, c);
+    ss += (int64_t)v[c] * v[c];
+  }
+  std::vector<float> out(dim);
+  for (int c = 0; c < dim; ++c) out[c] = vx_synth_finish(v[c], ss);
+  return out;
+}
+
+static int run_operator(int argc, char** argv) {
+  if (argc < 8) return 2;
+  const int64_t N = std::atoll(argv[2]);
+  const int D = std::atoi(argv[3]), k = std::atoi(argv[4]), B = std::atoi(argv[5]);
+  const int nq = std::atoi(argv[6]);
+  const int64_t T = std::atoll(argv[7]);
+  const int Nd = 128, td = 128;
+  vx_index_desc d{};
+  d.n_docs = N;
+  d.dim = D;
+  d.n_shards = 1;
+  d.tok_per_doc = nq ? Nd : 0;
+  d.tok_dim = nq ? td : 0;
+  d.tok_blocks = nq ? T : 0;
+  d.max_batch = 4;
+  d.max_k = k;
+  d.max_qtok = nq;
+  vx_index* h = nullptr;
+  if (vx_index_create(&d, &h) != VX_OK || vx_index_synth(h, 42) != VX_OK ||
+      (nq && vx_tokens_synth(h, 45) != VX_OK)) {
+    std::fprintf(stderr, "vx: %s\n", vx_last_error());
+    return 3;
+  }
+  World w(4, {{1, 125}, {4, 400}});  // modelD profile rows, profiles.csv:17-22; cap 4
+  w.rt->register_component("modelD", vortex_b200::make_search_component(h, D, k));
+  w.rt->load_pipeline(w.spec, w.pools);
+  std::vector<std::uint64_t> qids;
+  for (int i = 0; i < B; ++i) {
+    auto q = synth_row(43, i, D);
+    std::vector<float> tok;
+    for (int j = 0; j < nq; ++j) {
+      auto r = synth_row(44, (uint64_t)i * nq + j, td);
+      tok.insert(tok.end(), r.begin(), r.end());
+    }
+    qids.push_back(w.rt->ingress_submit(
+        "search", vortex_b200::encode_query(q.data(), D, nq ? tok.data() : nullptr, nq, td)));
+  }
+  w.loop.run_all();
+  for (int i = 0; i < B; ++i) {
+    const auto& rec = w.rt->record("search", qids[i]);
+    auto res = vortex_b200::decode_result(rec.outputs.at("D"));
+    std::printf("%d batch=%d", i, rec.stages.at("D").batch);
+    for (const auto& r : res) std::printf(" %lld:%.9g:%.9g", (long long)r.id, r.ip, r.ms);
+    std::printf("\n");
+  }
+  vx_index_destroy(h);
+  return 0;
+}
+#endif
+
+int main(int argc, char** argv) {
+  if (argc < 2) {
+    std::fprintf(stderr, "usage: %s batcher|operator ...\n", argv[0]);
+    return 2;
+  }
+  std::string mode = argv[1];
+  try {
+    if (mode == "batcher") return run_batcher(argc, argv);
+#ifdef VX_WITH_B200
+    if (mode == "operator") return run_operator(argc, argv);
+#endif
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "error: %s\n", e.what());
+    return 1;
+  }
+  std::fprintf(stderr, "unknown mode %s\n", mode.c_str());
+  return 2;
+}

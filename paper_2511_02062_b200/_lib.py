@@ -71,6 +71,10 @@ SIGNATURES = {
     "vx_maxsim_dev": [P, P, I32, I32, P, I32, P, P],
     "vx_search_rescore_dev": [P, P, P, I32, I32, I32, P, P, P, P],
     "vx_sync": [P],
+    "vx_batcher_simulate": [C.POINTER(U64), I64, I32, C.POINTER(I32), C.POINTER(C.c_double), I32,
+                            LP, C.POINTER(U64), C.POINTER(U64), C.POINTER(I64)],
+    "vx_serve_trace": [P, C.POINTER(U64), I64, I32, FP, FP, I32, I32, LP,
+                       C.POINTER(C.c_double), LP, C.POINTER(I64)],
     "vx_comm_unique_id": [C.POINTER(C.c_uint8)],
     "vx_comm_init": [P, C.POINTER(C.c_uint8), I32, I32],
     "vx_shard_serve": [P],

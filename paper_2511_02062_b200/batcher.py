@@ -1,0 +1,102 @@
+"""Opportunistic, SLO-bounded batcher (reference: Runtime::maybe_dispatch,
+proj/include/vortex/runtime.hpp:617-654) — Python face of the native implementation in
+csrc/vx_batcher.{hpp,cu} (virtual clock) and vx_serve_trace (wall clock, live GPU).
+
+Also: the open-loop arrival trace (bench.hpp:54-67 semantics), nearest-rank percentiles
+(bench.hpp:69-76), SLO miss rate (bench.hpp:78-83), the SLO-bounded cap (largest profiled
+batch whose latency fits the budget; planner.hpp:91-102) and measured profile rows in the
+reference's CSV schema (profile.hpp:24: model_id,instance_size_gb,batch_size,latency_ms,
+throughput_qps,memory_gb).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import numpy as np
+
+from . import _lib
+from ._lib import FP, LP, check
+
+
+def poisson_arrivals(rate_qps: float, count: int, seed: int = 42, start_us: int = 0) -> np.ndarray:
+    """Open-loop Poisson arrivals in integer microseconds: t += Exp(rate) gaps, rounded to
+    the nearest microsecond (bench.hpp:54-67).  numpy's generator, not mt19937_64: the trace
+    is seeded and reproducible but not the reference's exact draw."""
+    rng = np.random.default_rng(seed)
+    gaps = rng.exponential(1e6 / rate_qps, size=count)
+    return np.rint(start_us + np.cumsum(gaps)).astype(np.uint64)
+
+
+def constant_arrivals(rate_qps: float, count: int, start_us: int = 0) -> np.ndarray:
+    return np.rint(start_us + np.arange(count) * (1e6 / rate_qps)).astype(np.uint64)
+
+
+def percentile(values, p: float) -> float:
+    """Nearest rank: the ceil(p/100*n)-th smallest (bench.hpp:69-76)."""
+    v = np.sort(np.asarray(values, np.float64))
+    if v.size == 0:
+        raise ValueError("percentile of empty sample")
+    rank = min(max(math.ceil(p / 100.0 * v.size), 1), v.size)
+    return float(v[rank - 1])
+
+
+def slo_miss_rate(latencies_us, target_us: float) -> float:
+    v = np.asarray(latencies_us, np.float64)
+    if v.size == 0:
+        raise ValueError("miss rate of empty sample")
+    return float((v > target_us).mean())
+
+
+def slo_cap(profile: dict[int, float], slo_ms: float, stage_max_batch: int | None = None) -> int:
+    """Largest profiled batch whose latency fits the SLO budget (and the stage cap)."""
+    ok = [b for b, ms in profile.items() if ms <= slo_ms and (stage_max_batch is None or b <= stage_max_batch)]
+    return max(ok) if ok else 1
+
+
+def profile_rows(model_id: str, size_gb: float, profile: dict[int, float], memory_gb: float) -> str:
+    out = "model_id,instance_size_gb,batch_size,latency_ms,throughput_qps,memory_gb\n"
+    for b in sorted(profile):
+        ms = profile[b]
+        out += f"{model_id},{size_gb:g},{b},{ms:.6f},{1000.0 * b / ms:.3f},{memory_gb:.3f}\n"
+    return out
+
+
+def simulate(arrivals_us, cap: int, knots: dict[int, float]):
+    """Virtual-clock replay (native).  Returns (batch_of, dispatch_us, complete_us)."""
+    lib = _lib.load()
+    a = np.ascontiguousarray(arrivals_us, np.uint64)
+    n = a.shape[0]
+    kb = np.array(sorted(knots), np.int32)
+    km = np.array([knots[b] for b in sorted(knots)], np.float64)
+    bo = np.empty(n, np.int64)
+    du = np.empty(n, np.uint64)
+    cu = np.empty(n, np.uint64)
+    nb = C.c_int64()
+    U64P = C.POINTER(C.c_uint64)
+    check(lib.vx_batcher_simulate(a.ctypes.data_as(U64P), n, cap, kb.ctypes.data_as(C.POINTER(C.c_int32)),
+                                  km.ctypes.data_as(C.POINTER(C.c_double)), kb.shape[0],
+                                  bo.ctypes.data_as(LP), du.ctypes.data_as(U64P),
+                                  cu.ctypes.data_as(U64P), C.byref(nb)))
+    return bo, du, cu
+
+
+def serve_trace(index, arrivals_us, cap: int, queries: np.ndarray, qtok: np.ndarray | None, k: int,
+                want_ids: bool = False):
+    """Live mode on the GPU: returns (latency_us, batch_of, ids or None)."""
+    a = np.ascontiguousarray(arrivals_us, np.uint64)
+    n = a.shape[0]
+    q = np.ascontiguousarray(queries, np.float32)
+    t = None if qtok is None else np.ascontiguousarray(qtok, np.float32)
+    lat = np.empty(n, np.float64)
+    bo = np.empty(n, np.int64)
+    ids = np.empty((n, k), np.int64) if want_ids else None
+    nb = C.c_int64()
+    U64P = C.POINTER(C.c_uint64)
+    check(index.lib.vx_serve_trace(index.handle, a.ctypes.data_as(U64P), n, cap, q.ctypes.data_as(FP),
+                                   None if t is None else t.ctypes.data_as(FP),
+                                   0 if t is None else t.shape[1], k,
+                                   None if ids is None else ids.ctypes.data_as(LP),
+                                   lat.ctypes.data_as(C.POINTER(C.c_double)), bo.ctypes.data_as(LP),
+                                   C.byref(nb)))
+    return lat, bo, ids

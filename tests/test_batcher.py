@@ -1,0 +1,100 @@
+"""The product batcher (csrc/vx_batcher.{hpp,cu}, virtual clock) against the REFERENCE
+runtime's own decisions: committed fixtures produced by oracle/_ref (tests/golden/
+make_batcher_golden.py) and, when the reference is mounted, fresh random traces run through
+the reference binary.  Plus the reference's own batching test (test_runtime.cpp:246-268) and
+the bench helpers (bench.hpp:54-83).  CPU only."""
+from __future__ import annotations
+
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+DRIVER = ROOT / "oracle" / "_ref" / "vortex_ref_driver"
+
+
+@pytest.fixture(scope="module")
+def bat(vxlib):
+    from paper_2511_02062_b200 import batcher
+    return batcher
+
+
+def fixtures():
+    return json.loads((ROOT / "tests" / "golden" / "batcher_ref.json").read_text())
+
+
+@pytest.mark.parametrize("case", fixtures(), ids=lambda c: c["name"])
+def test_matches_reference_runtime_fixtures(bat, case):
+    knots = {int(k): v for k, v in case["knots"].items()}
+    b, d, c = bat.simulate(case["arrivals_us"], case["cap"], knots)
+    assert b.tolist() == case["batch"]
+    assert d.tolist() == case["dispatch_us"]
+    assert c.tolist() == case["complete_us"]
+
+
+def test_reference_opportunistic_batching_semantics(bat):
+    # test_runtime.cpp:246-268: first arrival alone; 5 queued while busy -> one batch of 5;
+    # 20 queued at once never exceed the cap of 8
+    arr = [0] * 6
+    b, _, _ = bat.simulate(arr, 8, {1: 10.0, 8: 40.0})
+    sizes = np.bincount(b)
+    assert sizes.tolist() == [1, 5]
+    b, _, _ = bat.simulate([0] * 21, 8, {1: 10.0, 8: 40.0})
+    assert np.bincount(b).max() <= 8 and np.bincount(b)[0] == 1
+
+
+def test_fifo_order_and_conservation(bat):
+    rng = np.random.default_rng(3)
+    arr = np.sort(rng.integers(0, 1_000_000, 2000)).astype(np.uint64)
+    b, d, c = bat.simulate(arr, 32, {1: 2.0, 32: 9.0})
+    assert (np.diff(b) >= 0).all()              # FIFO: batches consume the queue in order
+    assert (d >= arr).all() and (c > d).all()   # dispatched after arrival, done after dispatch
+    assert len(np.unique(b)) == b.max() + 1     # every batch index used
+
+
+@pytest.mark.skipif(not DRIVER.exists(), reason="oracle/_ref not built (needs /root/reference)")
+@pytest.mark.parametrize("seed", range(6))
+def test_random_traces_against_reference_binary(bat, seed):
+    import sys
+    sys.path.insert(0, str(ROOT / "tests" / "golden"))
+    from make_batcher_golden import run_reference
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 700))
+    rate = float(rng.choice([10.0, 200.0, 5000.0, 50000.0]))
+    arr = np.rint(np.cumsum(rng.exponential(1e6 / rate, n))).astype(np.int64)
+    if seed % 2:
+        arr[rng.integers(0, n, n // 3)] = arr[0]  # duplicate timestamps
+        arr = np.sort(arr)
+    cap = int(rng.integers(1, 300))
+    kb = np.unique(rng.integers(1, 400, int(rng.integers(1, 5))))
+    knots = {int(b): float(0.5 + b * rng.uniform(0.01, 2.0)) for b in kb}
+    ms = np.cumsum([knots[b] for b in sorted(knots)])  # monotone latencies
+    knots = {b: float(m) for b, m in zip(sorted(knots), ms)}
+    rb, rd, rc = run_reference(arr.tolist(), cap, knots)
+    b, d, c = bat.simulate(arr, cap, knots)
+    assert b.tolist() == rb and d.tolist() == rd and c.tolist() == rc
+
+
+def test_bench_helpers(bat):
+    # bench.hpp:69-83 semantics
+    assert bat.percentile(list(range(1, 101)), 95) == 95.0
+    assert bat.percentile([3, 1, 2], 50) == 2.0
+    assert bat.slo_miss_rate([100, 300, 200, 201], 200) == 0.5
+    a = bat.constant_arrivals(10, 5, start_us=1000)
+    assert a.tolist() == [1000, 101000, 201000, 301000, 401000]  # test_bench.cpp:108-113
+    p = bat.poisson_arrivals(100, 10000, seed=42)
+    gap = (int(p[-1]) - int(p[0])) / (len(p) - 1)
+    assert abs(gap - 10000.0) < 500.0                            # test_bench.cpp:115-125
+    assert (bat.poisson_arrivals(100, 50, seed=42) == bat.poisson_arrivals(100, 50, seed=42)).all()
+
+
+def test_slo_cap_and_profile_rows(bat):
+    prof = {1: 4.8, 16: 5.1, 64: 5.8, 128: 6.1, 256: 8.7}
+    assert bat.slo_cap(prof, 6.0) == 64
+    assert bat.slo_cap(prof, 200.0) == 256
+    assert bat.slo_cap(prof, 200.0, stage_max_batch=4) == 1
+    rows = bat.profile_rows("modelD", 180, prof, 40.0).splitlines()
+    assert rows[0] == "model_id,instance_size_gb,batch_size,latency_ms,throughput_qps,memory_gb"
+    assert rows[2].startswith("modelD,180,16,5.1")

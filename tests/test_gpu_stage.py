@@ -1,0 +1,88 @@
+"""The stage behind the reference's own runtime, and the live batcher, on a B200.
+
+* test_reference_runtime_drives_b200_operator: oracle/_ref/vortex_ref_operator is the
+  REFERENCE Runtime (proj/include/vortex/runtime.hpp, compiled where it lies) with the B200
+  stage registered as its `modelD` ComponentFn (include/vortex_b200_component.hpp).  The
+  reference batcher forms the batches (cap 4, pipeline.json:7); results must equal the
+  oracle's.
+* test_live_batcher_*: vx_serve_trace replays an open-loop trace in wall-clock time through
+  the opportunistic batcher onto the GPU.
+"""
+from __future__ import annotations
+
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+OPERATOR = ROOT / "oracle" / "_ref" / "vortex_ref_operator"
+
+
+@pytest.fixture(scope="module")
+def vx(vxlib):
+    import paper_2511_02062_b200 as vx
+    return vx
+
+
+@pytest.mark.skipif(not OPERATOR.exists(), reason="oracle/_ref/vortex_ref_operator not built")
+def test_reference_runtime_drives_b200_operator(vx, oracle):
+    N, D, k, B, nq, T = 20_000, 768, 10, 7, 32, 97
+    out = subprocess.run([str(OPERATOR), "operator", str(N), str(D), str(k), str(B), str(nq), str(T)],
+                         check=True, capture_output=True, text=True, timeout=300).stdout
+    rows = [ln.split() for ln in out.strip().splitlines()]
+    assert len(rows) == B
+    # reference batcher with cap 4, all 7 submitted at one instant: 1, then 4, then 2
+    assert [r[1] for r in rows] == ["batch=1"] + ["batch=4"] * 4 + ["batch=2"] * 2
+    X = oracle.synth_rows(42, 0, N, D)
+    Q = oracle.synth_rows(43, 0, B, D)
+    qt = oracle.synth_rows(44, 0, B * nq, 128).reshape(B, nq, 128)
+    table = oracle.synth_tokens(45, 0, T, 128, 128)
+    rid, rip, rms = oracle.search_rescore(X, Q, qt, table, k, mode=1)
+    for i, r in enumerate(rows):
+        recs = [tuple(x.split(":")) for x in r[2:]]
+        ids = [int(a) for a, _, _ in recs]
+        assert sorted(ids) == sorted(rid[i].tolist())
+        lut = dict(zip(rid[i].tolist(), rip[i].tolist()))
+        for a, p, m in recs:
+            assert np.float32(lut[int(a)]) == np.float32(float(p))
+
+
+def test_live_batcher_results_and_policy(vx, oracle):
+    from paper_2511_02062_b200 import batcher, synth
+    N, D, k, n, cap = 200_000, 768, 10, 600, 32
+    arr = batcher.poisson_arrivals(20_000.0, n, seed=7)
+    Q = synth.rows(43, 0, n, D)
+    with vx.Index(N, D, max_batch=cap, max_k=k) as idx:
+        idx.synth(42)
+        lat, bo, ids = batcher.serve_trace(idx, arr, cap, Q, None, k, want_ids=True)
+        ref_ids, _ = idx.search(Q[:cap], k)
+    sizes = np.bincount(bo)
+    assert sizes.max() <= cap and sizes.sum() == n
+    assert (np.diff(bo) >= 0).all()  # FIFO
+    assert (lat > 0).all()
+    assert np.array_equal(ids[:cap][bo[:cap] == bo[0]], ref_ids[bo[:cap] == bo[0]])
+    X = oracle.synth_rows(42, 0, N, D)
+    sel = np.arange(0, n, 37)
+    rid, _ = oracle.flat_topk(X, Q[sel], k, mode=1)
+    assert np.array_equal(ids[sel], rid)
+    p99 = batcher.percentile(lat, 99)
+    assert p99 < 1e6  # sanity: sub-second tail at 20k qps offered on a 200K index
+
+
+def test_live_batcher_with_rescore(vx):
+    from paper_2511_02062_b200 import batcher, synth
+    N, D, k, n, cap, nq = 100_000, 768, 100, 200, 16, 32
+    arr = batcher.constant_arrivals(5000.0, n)
+    Q = synth.rows(43, 0, n, D)
+    qt = synth.query_tokens(n, nq, 128)
+    with vx.Index(N, D, tok_per_doc=128, tok_dim=128, tok_blocks=512, max_batch=cap, max_k=k,
+                  max_qtok=nq) as idx:
+        idx.synth(42)
+        idx.tokens_synth(45)
+        lat, bo, ids = batcher.serve_trace(idx, arr, cap, Q, qt, k, want_ids=True)
+        want, _, _ = idx.search_rescore(Q[:5], qt[:5], k)
+    assert np.array_equal(ids[:5], want)
+    assert np.bincount(bo).max() <= cap

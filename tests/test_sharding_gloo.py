@@ -1,0 +1,78 @@
+"""N > 1 host logic on CPU with gloo, world_size 2 (the GPU exchange uses NCCL).
+
+What is tested is the sharded algorithm the stage runs across GPUs (vx_api.cu stage_core):
+contiguous shard ranges [floor(N*g/G), floor(N*(g+1)/G)) (the affinity-group analog of
+kvs.hpp:160-175), a per-shard exact top-k, a gather of k x G candidates to rank 0 and a
+merge on (score desc, id asc).  Exactness: every global top-k member is in its owner's
+local top-k, so rank 0's merge equals the single-index oracle.
+"""
+from __future__ import annotations
+
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def shard_range(N: int, G: int, g: int) -> tuple[int, int]:
+    r0 = (N * g) // G
+    return r0, (N * (g + 1)) // G - r0
+
+
+def _worker(rank: int, world: int, port: int, q) -> None:
+    import torch.distributed as dist
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import vxoracle as o
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    N, D, B, k = 30_001, 64, 5, 17
+    r0, n = shard_range(N, world, rank)
+    X = o.synth_rows(42, r0, n, D)
+    Q = o.synth_rows(43, 0, B, D)
+    ids, sc = o.flat_topk(X, Q, k, mode=1, id_base=r0, threads=2)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, (ids, sc))
+    if rank == 0:
+        allid = np.concatenate([g[0] for g in gathered], axis=1)
+        allsc = np.concatenate([g[1] for g in gathered], axis=1)
+        merged = np.empty((B, k), np.int64)
+        for b in range(B):
+            order = np.lexsort((allid[b], -allsc[b]))[:k]
+            merged[b] = allid[b][order]
+        Xf = o.synth_rows(42, 0, N, D)
+        want, _ = o.flat_topk(Xf, Q, k, mode=1, threads=2)
+        q.put(bool(np.array_equal(merged, want)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_shard_ranges_partition():
+    for N in (1, 7, 10_000_000, 2**31 + 5):
+        for G in (1, 2, 3, 4, 8):
+            if N < G:
+                continue
+            spans = [shard_range(N, G, g) for g in range(G)]
+            assert spans[0][0] == 0
+            assert all(a[0] + a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            assert spans[-1][0] + spans[-1][1] == N
+            assert max(s[1] for s in spans) - min(s[1] for s in spans) <= 1
+
+
+def test_two_rank_gloo_gather_merge_equals_global(oracle):
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + os.getpid() % 1000
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    ok = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert ok
