@@ -50,7 +50,7 @@ def parse() -> argparse.Namespace:
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n-docs", type=int, default=10_000_000)
     ap.add_argument("--dim", type=int, default=768)
-    ap.add_argument("--batch", type=int, default=16)
+    ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--k", type=int, default=100)
     ap.add_argument("--nq", type=int, default=32)
     ap.add_argument("--tok-per-doc", type=int, default=128)
@@ -284,7 +284,7 @@ def run_ours(args) -> None:
     n_local = idx.n_local
     scan_bytes = n_local * D * 4 + B * D * 4 + B * k * 12  # per-launch algorithmic bytes
     achieved = scan_bytes / (scan_ms / 1e3) / 1e9
-    tc = args.scan == "tc" or (args.scan == "auto" and B > 4 and k <= 128)
+    tc = args.scan == "tc" or (args.scan == "auto" and k <= 128)
     kernel_name = "scan_tc_kernel (K2, tcgen05 tf32 + fused top-k)" if tc else "scan_f32_kernel (K1)"
     cpu = None
     if not args.no_cpu_baseline:

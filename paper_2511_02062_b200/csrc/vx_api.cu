@@ -566,7 +566,7 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
 static vx_status local_topk(vx_index* h, const float* d_q, int B, int k, uint64_t* keys,
                             int64_t* ids, float* scores, cudaStream_t st) {
   const bool tc = h->scan_algo == VX_SCAN_TC ||
-                  (h->scan_algo == VX_SCAN_AUTO && tc_eligible(h, B, k) && B > 4);
+                  (h->scan_algo == VX_SCAN_AUTO && tc_eligible(h, B, k));
   if (tc) {
     if (!tc_eligible(h, B, k)) return fail(VX_ERR_UNSUPPORTED, "tensor-core scan needs k <= 128");
     return local_topk_tc(h, d_q, B, k, keys, ids, scores, st);
