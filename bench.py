@@ -58,6 +58,8 @@ def parse() -> argparse.Namespace:
     ap.add_argument("--tok-blocks", type=int, default=1 << 18)
     ap.add_argument("--slo-ms", type=float, default=200.0)
     ap.add_argument("--scan", choices=["auto", "f32", "tc"], default="auto")
+    ap.add_argument("--coarse", choices=["auto", "tf32", "bf16"], default="auto",
+                    help="operand format of the tensor-core candidate scan (exact fp32 re-rank either way)")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -176,6 +178,8 @@ def run_ours(args) -> None:
     idx = vx.Index(args.n_docs, D, device=local, n_shards=world, shard=rank,
                    tok_per_doc=args.tok_per_doc, tok_dim=td, tok_blocks=args.tok_blocks,
                    max_batch=B, max_k=k, max_qtok=nq)
+    if args.coarse != "auto":
+        idx.set_option(vx.VX_OPT_COARSE, {"tf32": vx.VX_COARSE_TF32, "bf16": vx.VX_COARSE_BF16}[args.coarse])
     if args.scan != "auto":
         idx.set_option(vx.VX_OPT_SCAN, {"f32": vx.VX_SCAN_F32, "tc": vx.VX_SCAN_TC}[args.scan])
     idx.synth(42)
@@ -282,10 +286,14 @@ def run_ours(args) -> None:
     pk = peaks()
     scan_ms = st["scan_ms_total"] / max(1, st["timed_batches"])
     n_local = idx.n_local
-    scan_bytes = n_local * D * 4 + B * D * 4 + B * k * 12  # per-launch algorithmic bytes
-    achieved = scan_bytes / (scan_ms / 1e3) / 1e9
     tc = args.scan == "tc" or (args.scan == "auto" and k <= 128)
-    kernel_name = "scan_tc_kernel (K2, tcgen05 tf32 + fused top-k)" if tc else "scan_f32_kernel (K1)"
+    bf16 = tc and args.coarse != "tf32"
+    elem = 2 if bf16 else 4  # the scan reads the bf16 shadow (bf16 coarse) or the fp32 rows
+    # SURVEY §8(d) per-launch algorithmic bytes: the index rows the scan streams + queries + results
+    scan_bytes = n_local * D * elem + B * D * elem + B * k * 12
+    achieved = scan_bytes / (scan_ms / 1e3) / 1e9
+    kernel_name = ((f"scan_tc_kernel (K2, tcgen05 {'kind::f16 on the bf16 shadow' if bf16 else 'kind::tf32'}"
+                    " + fused top-k; exact fp32 re-rank)") if tc else "scan_f32_kernel (K1)")
     cpu = None
     if not args.no_cpu_baseline:
         rows, reps = cpu_sample_rows(args)
@@ -301,7 +309,8 @@ def run_ours(args) -> None:
                                f"MaxSim rescore ({nq}x{args.tok_per_doc}x{td} bf16), batch {B}",
                    "n_docs": args.n_docs, "dim": D, "batch": B, "k": k, "shards": world,
                    "tok_blocks": args.tok_blocks, "l2": "index (GB) >> 126 MB L2: every step streams from HBM",
-                   "scan": args.scan},
+                   "scan": args.scan, "coarse": ("bf16" if bf16 else "tf32") if tc else None,
+                   "exactness": "ids+scores bit-identical to the fp32 oracle (certified re-rank)"},
         "roofline": {"bound": "hbm", "kernel": kernel_name, "achieved": achieved,
                      "peak": pk["hbm_gbs"], "peak_src": pk["src"], "unit": "GB/s",
                      "frac": achieved / pk["hbm_gbs"], "frac_of_8tbs": achieved / 8000.0,

@@ -60,8 +60,15 @@ enum {
   VX_OPT_SCAN = 1,        /* one of VX_SCAN_* */
   VX_OPT_GRID = 2,        /* CTAs for the scan (0 = auto: one per SM) */
   VX_OPT_GRAPHS = 3,      /* 1 = replay pre-captured CUDA graphs per batch bucket */
-  VX_OPT_MAXSIM = 4       /* one of VX_MAXSIM_* */
+  VX_OPT_MAXSIM = 4,      /* one of VX_MAXSIM_* */
+  VX_OPT_COARSE = 5       /* one of VX_COARSE_*: operand format of the tensor-core scan */
 };
+/* Coarse (candidate-selecting) tensor-core scan format.  Either way every reported score is
+ * recomputed exactly in fp32 and certified.  BF16 reads a bf16 shadow
+ * of the index (half the HBM bytes, 2x the tensor rate); TF32 reads the fp32 rows. */
+enum { VX_COARSE_AUTO = 0, VX_COARSE_TF32 = 1, VX_COARSE_BF16 = 2 };
+/* vx_index_desc.flags */
+enum { VX_FLAG_NO_BF16_SHADOW = 1 /* do not keep the bf16 copy of the index (saves N*D*2 B) */ };
 /* MaxSim kernel selection (vx_set_option VX_OPT_MAXSIM). */
 enum { VX_MAXSIM_AUTO = 0, VX_MAXSIM_CC = 1, VX_MAXSIM_TC = 2 };
 
@@ -77,7 +84,7 @@ typedef struct vx_index_desc {
   int32_t max_batch;   /* largest batch B accepted (workspace sizing) */
   int32_t max_k;       /* largest k accepted (<= 256) */
   int32_t max_qtok;    /* largest Nq accepted (<= 128) */
-  int32_t reserved;
+  int32_t flags;       /* VX_FLAG_* */
 } vx_index_desc;
 
 typedef struct vx_stats {

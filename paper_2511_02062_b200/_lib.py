@@ -19,6 +19,9 @@ STATUS = {0: "VX_OK", 1: "VX_ERR_INVALID", 2: "VX_ERR_CUDA", 3: "VX_ERR_OOM", 4:
 VX_SCAN_AUTO, VX_SCAN_F32, VX_SCAN_TC = 0, 1, 2
 VX_OPT_SCAN, VX_OPT_GRID, VX_OPT_GRAPHS, VX_OPT_MAXSIM = 1, 2, 3, 4
 VX_MAXSIM_AUTO, VX_MAXSIM_CC, VX_MAXSIM_TC = 0, 1, 2
+VX_OPT_COARSE = 5
+VX_COARSE_AUTO, VX_COARSE_TF32, VX_COARSE_BF16 = 0, 1, 2
+VX_FLAG_NO_BF16_SHADOW = 1
 
 
 class VxError(RuntimeError):
@@ -33,7 +36,7 @@ class IndexDesc(C.Structure):
     _fields_ = [("n_docs", C.c_int64), ("dim", C.c_int32), ("device", C.c_int32),
                 ("n_shards", C.c_int32), ("shard", C.c_int32), ("tok_per_doc", C.c_int32),
                 ("tok_dim", C.c_int32), ("tok_blocks", C.c_int64), ("max_batch", C.c_int32),
-                ("max_k", C.c_int32), ("max_qtok", C.c_int32), ("reserved", C.c_int32)]
+                ("max_k", C.c_int32), ("max_qtok", C.c_int32), ("flags", C.c_int32)]
 
 
 class Stats(C.Structure):

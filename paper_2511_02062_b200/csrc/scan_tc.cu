@@ -78,7 +78,9 @@ __global__ void __launch_bounds__(TcCfg<QT>::kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + C::NBUF);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nch = a.D >> 5;
+  // K-chunk = one 128-byte swizzle atom: 32 fp32 (kind::tf32) or 64 bf16 (kind::f16)
+  const int cw = a.fmt == 2 ? 32 : 64;
+  const int nch = a.D / cw;
   const uint32_t n_local = a.n_local;
   const int ntiles = (int)((n_local + kTcTD - 1) / kTcTD);
 
@@ -116,8 +118,8 @@ __global__ void __launch_bounds__(TcCfg<QT>::kThreads, 1)
           uint8_t* st = smem + (size_t)s * C::kStageBytes;
 #pragma unroll
           for (int qt = 0; qt < QT; ++qt)
-            tma_load_2d(st + qt * kTcStageUnit, &tq, &full[s], c * 32, qt * 128, pol_q);
-          tma_load_2d(st + QT * kTcStageUnit, &tx, &full[s], c * 32, tile * kTcTD, pol_x);
+            tma_load_2d(st + qt * kTcStageUnit, &tq, &full[s], c * cw, qt * 128, pol_q);
+          tma_load_2d(st + QT * kTcStageUnit, &tx, &full[s], c * cw, tile * kTcTD, pol_x);
           if (++s == ns) {
             s = 0;
             ph ^= 1;
@@ -128,7 +130,7 @@ __global__ void __launch_bounds__(TcCfg<QT>::kThreads, 1)
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer (one thread)
     if (lane == 0) {
-      constexpr uint32_t idesc = make_idesc(2u /*TF32*/, 128u, (uint32_t)kTcTD);
+      const uint32_t idesc = make_idesc((uint32_t)a.fmt /*2 TF32, 1 BF16*/, 128u, (uint32_t)kTcTD);
       int s = 0;
       uint32_t ph = 0;
       int buf = 0;
@@ -147,7 +149,10 @@ __global__ void __launch_bounds__(TcCfg<QT>::kThreads, 1)
             for (int j = 0; j < 4; ++j) {
               const uint64_t ad = umma_desc_sw128(st + qt * kTcStageUnit + j * 32);
               const uint64_t bd = umma_desc_sw128(st + QT * kTcStageUnit + j * 32);
-              mma_tf32_ss(d, ad, bd, idesc, (c | j) != 0 ? 1u : 0u);
+              if (a.fmt == 2)
+                mma_tf32_ss(d, ad, bd, idesc, (c | j) != 0 ? 1u : 0u);
+              else
+                mma_f16_ss(d, ad, bd, idesc, (c | j) != 0 ? 1u : 0u);
             }
           }
           mma_commit(&empty[s]);
@@ -238,6 +243,7 @@ __global__ void __launch_bounds__(256)
     rerank_kernel(const float* __restrict__ docs, const float* __restrict__ qv, int D,
                   const uint64_t* __restrict__ cand, int kp, const uint64_t* __restrict__ part,
                   int grid, int k, int64_t row0, const float* __restrict__ xnorm_max,
+                  float err_coef,
                   uint64_t* __restrict__ out_keys, int64_t* __restrict__ out_ids,
                   float* __restrict__ out_scores, int* __restrict__ flags) {
   extern __shared__ float rsm[];
@@ -302,7 +308,7 @@ __global__ void __launch_bounds__(256)
     // exact score <= s(T') + E; the exact k-th must beat that bound strictly.
     float qn = 0.0f;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) qn += s_red[w];
-    const float E = (0.001953125f + 0.000244140625f) * sqrtf(qn) * 1.0001f * xnorm_max[0] + 1e-30f;
+    const float E = err_coef * sqrtf(qn) * 1.0001f * xnorm_max[0] + 1e-30f;
     const uint64_t ek = keys[k - 1];
     if (ek == 0ull || !(vx_key_score(ek) > vx_key_score(tprime) + E)) s_fail = 1;
   }
@@ -370,14 +376,14 @@ cudaError_t launch_scan_tc(int QT, const CUtensorMap* tq, const CUtensorMap* tx,
 
 cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64_t* cand, int B,
                           int kp, const uint64_t* part, int grid, int k, int64_t row0,
-                          const float* xnorm_max, uint64_t* out_keys, int64_t* out_ids,
-                          float* out_scores, int* flags, cudaStream_t st) {
+                          const float* xnorm_max, float err_coef, uint64_t* out_keys,
+                          int64_t* out_ids, float* out_scores, int* flags, cudaStream_t st) {
   size_t smem = (size_t)((D + 1) & ~1) * 4 + (size_t)kp * 8;
   cudaError_t e = cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
   rerank_kernel<<<B, 256, smem, st>>>(docs, q, D, cand, kp, part, grid, k, row0, xnorm_max,
-                                      out_keys, out_ids, out_scores, flags);
+                                      err_coef, out_keys, out_ids, out_scores, flags);
   return cudaGetLastError();
 }
 

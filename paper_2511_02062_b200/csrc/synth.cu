@@ -46,6 +46,32 @@ cudaError_t launch_synth_rows(float* out, uint64_t seed, int64_t row0, int64_t n
   return cudaGetLastError();
 }
 
+// fp32 -> bf16 (RNE on the bit pattern, vx_synth.h): the coarse-scan shadow of the index
+// and the per-batch query copy.  8 elements per thread (two 16-byte loads, one 16-byte store).
+__global__ void to_bf16_kernel(const float4* __restrict__ in, uint4* __restrict__ out, int64_t n8) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 a = in[2 * i], b = in[2 * i + 1];
+    uint4 o;
+    o.x = vx_f32_to_bf16_bits(a.x) | ((uint32_t)vx_f32_to_bf16_bits(a.y) << 16);
+    o.y = vx_f32_to_bf16_bits(a.z) | ((uint32_t)vx_f32_to_bf16_bits(a.w) << 16);
+    o.z = vx_f32_to_bf16_bits(b.x) | ((uint32_t)vx_f32_to_bf16_bits(b.y) << 16);
+    o.w = vx_f32_to_bf16_bits(b.z) | ((uint32_t)vx_f32_to_bf16_bits(b.w) << 16);
+    out[i] = o;
+  }
+}
+
+cudaError_t launch_to_bf16(const float* in, uint16_t* out, int64_t n, cudaStream_t st) {
+  if (n % 8) return cudaErrorInvalidValue;  // callers pass rows of D (multiple of 32)
+  const int64_t n8 = n / 8;
+  int64_t blocks = (n8 + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  to_bf16_kernel<<<(int)blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(in),
+                                              reinterpret_cast<uint4*>(out), n8);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_synth_tokens(uint16_t* out, uint64_t seed, int64_t blk0, int64_t nblk, int Nd,
                                 int d, cudaStream_t st) {
   int64_t rows = nblk * Nd;

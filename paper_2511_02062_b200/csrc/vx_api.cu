@@ -165,6 +165,10 @@ struct vx_index {
   uint16_t* tokens = nullptr;
   CUtensorMap tmap_docs{};
   CUtensorMap tmap_tok{};
+  uint16_t* docs16 = nullptr;    // bf16 shadow of the shard (coarse scan), may be null
+  CUtensorMap tmap_docs16{};
+  uint16_t* d_q16 = nullptr;     // [maxB][D] bf16 queries for the bf16 coarse scan
+  int coarse = VX_COARSE_AUTO;
   // options
   int scan_algo = VX_SCAN_AUTO;
   int maxsim_algo = VX_MAXSIM_AUTO;
@@ -280,6 +284,10 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
   ALLOC(h->d_flags, B * 4);
   ALLOC(h->d_xnorm, 4);
   ALLOC(h->d_fq, B * D * 4);
+  if (!(d->flags & VX_FLAG_NO_BF16_SHADOW)) {
+    ALLOC(h->docs16, (size_t)h->n_local * D * 2);
+    ALLOC(h->d_q16, B * D * 2);
+  }
 #undef ALLOC
   if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess)
     return cleanup(fail(VX_ERR_CUDA, "stream create"));
@@ -303,6 +311,11 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
   s = make_tmap_2d(&h->tmap_docs, h->docs, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
                    (uint64_t)h->n_local, D, 32, 128);
   if (s != VX_OK) return cleanup(s);
+  if (h->docs16) {
+    s = make_tmap_2d(&h->tmap_docs16, h->docs16, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                     (uint64_t)h->n_local, D, 64, 128);
+    if (s != VX_OK) return cleanup(s);
+  }
   *out = h;
   return VX_OK;
 }
@@ -315,7 +328,7 @@ extern "C" vx_status vx_index_destroy(vx_index* h) {
   void* ptrs[] = {h->docs,  h->tokens,    h->d_q,      h->d_qtok,    h->d_part, h->d_keys,
                   h->d_ids, h->d_ip,      h->d_ms,     h->d_out_ids, h->d_out_ip,
                   h->d_out_ms, h->d_send, h->d_recv, h->d_hdr, h->d_ckeys, h->d_flags,
-                  h->d_xnorm, h->d_fq};
+                  h->d_xnorm, h->d_fq, h->docs16, h->d_q16};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->h_stage) cudaFreeHost(h->h_stage);
@@ -346,6 +359,13 @@ extern "C" vx_status vx_set_option(vx_index* h, int32_t option, int64_t value) {
     case VX_OPT_GRID:
       if (value < 0 || value > h->num_sms) return fail(VX_ERR_INVALID, "grid %lld", (long long)value);
       h->grid = value == 0 ? h->num_sms : (int)value;
+      return VX_OK;
+    case VX_OPT_COARSE:
+      if (value != VX_COARSE_AUTO && value != VX_COARSE_TF32 && value != VX_COARSE_BF16)
+        return fail(VX_ERR_INVALID, "coarse format %lld", (long long)value);
+      if (value == VX_COARSE_BF16 && !h->docs16)
+        return fail(VX_ERR_STATE, "index created with VX_FLAG_NO_BF16_SHADOW");
+      h->coarse = (int)value;
       return VX_OK;
     case VX_OPT_MAXSIM:
       if (value != VX_MAXSIM_AUTO && value != VX_MAXSIM_CC && value != VX_MAXSIM_TC)
@@ -380,6 +400,10 @@ extern "C" vx_status vx_index_synth(vx_index* h, uint64_t seed) {
   count_launch(h);
   CU_TRY(vx::launch_row_norm_max(h->docs, h->n_local, h->desc.dim, h->d_xnorm, h->stream));
   count_launch(h);
+  if (h->docs16) {
+    CU_TRY(vx::launch_to_bf16(h->docs, h->docs16, h->n_local * h->desc.dim, h->stream));
+    count_launch(h);
+  }
   CU_TRY(cudaStreamSynchronize(h->stream));
   return VX_OK;
 }
@@ -395,6 +419,11 @@ extern "C" vx_status vx_index_upload(vx_index* h, const float* rows, int64_t row
   // the TC certificate needs an upper bound on the row norms: recompute over the shard
   CU_TRY(vx::launch_row_norm_max(h->docs, h->n_local, h->desc.dim, h->d_xnorm, h->stream));
   count_launch(h);
+  if (h->docs16 && n > 0) {
+    const size_t off = (size_t)(row0 - h->row0) * h->desc.dim;
+    CU_TRY(vx::launch_to_bf16(h->docs + off, h->docs16 + off, n * h->desc.dim, h->stream));
+    count_launch(h);
+  }
   CU_TRY(cudaStreamSynchronize(h->stream));
   return VX_OK;
 }
@@ -510,14 +539,23 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
   const int D = h->desc.dim;
   const int grid = h->grid;
   const int kp = kprime_of(k);
+  const bool bf16 = h->docs16 && h->coarse != VX_COARSE_TF32;
   CU_TRY(cudaEventRecord(h->ev[0], st));
+  if (bf16) {
+    CU_TRY(vx::launch_to_bf16(d_q, h->d_q16, (int64_t)B * D, st));
+    count_launch(h);
+  }
   for (int g0 = 0; g0 < B; g0 += 256) {
     const int Bg = std::min(256, B - g0);
     const int QT = Bg <= 128 ? 1 : 2;
     const int a_rows = QT == 1 ? ((Bg + 7) & ~7) : 128;
     CUtensorMap tq;
-    VX_TRY(make_tmap_2d(&tq, d_q + (size_t)g0 * D, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
-                        (uint64_t)Bg, D, 32, (uint32_t)a_rows));
+    if (bf16)
+      VX_TRY(make_tmap_2d(&tq, h->d_q16 + (size_t)g0 * D, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                          (uint64_t)Bg, D, 64, (uint32_t)a_rows));
+    else
+      VX_TRY(make_tmap_2d(&tq, d_q + (size_t)g0 * D, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                          (uint64_t)Bg, D, 32, (uint32_t)a_rows));
     int ns = 0;
     const size_t smem = vx::scan_tc_smem(QT, &ns);
     vx::ScanTcArgs a;
@@ -526,8 +564,9 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
     a.B = Bg;
     a.ns = ns;
     a.a_rows = a_rows;
+    a.fmt = bf16 ? 1 : 2;
     a.part = h->d_part + (size_t)g0 * grid * vx::kTcListLen;
-    CU_TRY(vx::launch_scan_tc(QT, &tq, &h->tmap_docs, a, grid, smem, st));
+    CU_TRY(vx::launch_scan_tc(QT, &tq, bf16 ? &h->tmap_docs16 : &h->tmap_docs, a, grid, smem, st));
     count_launch(h);
   }
   CU_TRY(cudaEventRecord(h->ev[1], st));
@@ -535,7 +574,8 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
                                nullptr, st));
   count_launch(h);
   CU_TRY(vx::launch_rerank(h->docs, d_q, D, h->d_ckeys, B, kp, h->d_part, grid, k, h->row0,
-                           reinterpret_cast<const float*>(h->d_xnorm), keys, ids, scores,
+                           reinterpret_cast<const float*>(h->d_xnorm),
+                           bf16 ? vx::kErrCoefBF16 : vx::kErrCoefTF32, keys, ids, scores,
                            h->d_flags, st));
   count_launch(h);
   // certificate failures: re-scan those queries exactly (expected ~never on real data)

@@ -36,16 +36,23 @@ struct ScanTcArgs {
   int32_t B;         // queries in this launch (<= QT*128)
   int32_t ns;        // pipeline stages
   int32_t a_rows;    // TMA box rows of the query map (multiple of 8, <= 128)
+  int32_t fmt;       // operand format: 2 = fp32 read as TF32 (kind::tf32), 1 = bf16 (kind::f16)
   uint64_t* part;    // [B][gridDim.x][16] coarse keys
 };
+// coarse-score error bound coefficients E = coef * ||q|| * max||x|| (see scan_tc.cu):
+// TF32 truncates both operands to 10 mantissa bits (<= 2^-10 each); bf16 rounds both to
+// 8 bits (<= 2^-9 each); + 2^-12 of slack for fp32 accumulation inside the tensor core.
+constexpr float kErrCoefTF32 = 0.001953125f + 0.000244140625f;
+constexpr float kErrCoefBF16 = 0.00390625f + 0.000244140625f;
+cudaError_t launch_to_bf16(const float* in, uint16_t* out, int64_t n, cudaStream_t st);
 constexpr int kTcListLen = 16;
 size_t scan_tc_smem(int QT, int* ns_out);
 cudaError_t launch_scan_tc(int QT, const CUtensorMap* tq, const CUtensorMap* tx,
                            const ScanTcArgs& a, int grid, size_t smem, cudaStream_t st);
 cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64_t* cand, int B,
                           int kp, const uint64_t* part, int grid, int k, int64_t row0,
-                          const float* xnorm_max, uint64_t* out_keys, int64_t* out_ids,
-                          float* out_scores, int* flags, cudaStream_t st);
+                          const float* xnorm_max, float err_coef, uint64_t* out_keys,
+                          int64_t* out_ids, float* out_scores, int* flags, cudaStream_t st);
 cudaError_t launch_row_norm_max(const float* docs, int64_t n, int D, unsigned int* out_bits,
                                 cudaStream_t st);
 

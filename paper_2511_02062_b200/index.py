@@ -25,12 +25,12 @@ class Index:
 
     def __init__(self, n_docs: int, dim: int, *, device: int = 0, n_shards: int = 1, shard: int = 0,
                  tok_per_doc: int = 0, tok_dim: int = 128, tok_blocks: int = 1,
-                 max_batch: int = 64, max_k: int = 128, max_qtok: int = 32):
+                 max_batch: int = 64, max_k: int = 128, max_qtok: int = 32, flags: int = 0):
         self.lib = _lib.load()
         d = IndexDesc(n_docs=n_docs, dim=dim, device=device, n_shards=n_shards, shard=shard,
                       tok_per_doc=tok_per_doc, tok_dim=tok_dim if tok_per_doc else 0,
                       tok_blocks=tok_blocks if tok_per_doc else 0, max_batch=max_batch,
-                      max_k=max_k, max_qtok=max_qtok if tok_per_doc else 0, reserved=0)
+                      max_k=max_k, max_qtok=max_qtok if tok_per_doc else 0, flags=flags)
         self.desc = d
         self._h = C.c_void_p()
         check(self.lib.vx_index_create(C.byref(d), C.byref(self._h)))

@@ -1,0 +1,63 @@
+"""Both coarse formats of the tensor-core scan (TF32 on the fp32 rows, bf16 on the shadow)
+return the oracle's exact answer: ids AND scores bit-identical to VXO_F32, because the coarse
+pass only selects candidates and the certificate proves nothing outside them can enter the
+top-k (else the query is re-scanned exactly).  Runs on a B200."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def vx(vxlib):
+    import paper_2511_02062_b200 as vx
+    return vx
+
+
+@pytest.mark.parametrize("coarse", ["tf32", "bf16"])
+@pytest.mark.parametrize("N,D,B,k", [
+    (100_000, 768, 16, 10), (50_000, 768, 1, 100), (20_000, 1024, 64, 100), (30_000, 768, 200, 128),
+    (12_345, 128, 7, 5), (4_000, 64, 300, 64)])
+def test_coarse_formats_exact(vx, oracle, coarse, N, D, B, k):
+    X = oracle.synth_rows(42, 0, N, D)
+    Q = oracle.synth_rows(43, 0, B, D)
+    with vx.Index(N, D, max_batch=B, max_k=k) as idx:
+        idx.synth(42)
+        idx.set_option(vx.VX_OPT_SCAN, vx.VX_SCAN_TC)
+        idx.set_option(vx.VX_OPT_COARSE, {"tf32": vx.VX_COARSE_TF32, "bf16": vx.VX_COARSE_BF16}[coarse])
+        ids, sc = idx.search(Q, k)
+        fb = idx.stats()["cert_fallbacks"]
+    rid, rsc = oracle.flat_topk(X, Q, k, mode=1)
+    assert np.array_equal(ids, rid)
+    v = rid >= 0
+    assert np.array_equal(sc[v], rsc[v].astype(np.float32))
+    if N >= 20_000:
+        assert fb == 0, f"{fb} certificate fallbacks"
+
+
+def test_no_shadow_flag(vx, oracle):
+    N, D, B, k = 10_000, 256, 4, 10
+    with vx.Index(N, D, max_batch=B, max_k=k, flags=vx.VX_FLAG_NO_BF16_SHADOW) as idx:
+        idx.synth(42)
+        with pytest.raises(vx.VxError):
+            idx.set_option(vx.VX_OPT_COARSE, vx.VX_COARSE_BF16)
+        ids, _ = idx.search(oracle.synth_rows(43, 0, B, D), k)
+    rid, _ = oracle.flat_topk(oracle.synth_rows(42, 0, N, D), oracle.synth_rows(43, 0, B, D), k, mode=1)
+    assert np.array_equal(ids, rid)
+
+
+def test_upload_refreshes_shadow(vx, oracle):
+    # rows uploaded in two pieces; the bf16 shadow must follow every upload
+    N, D, B, k = 6_000, 128, 5, 10
+    X = oracle.synth_rows(7, 0, N, D)
+    Q = oracle.synth_rows(8, 0, B, D)
+    with vx.Index(N, D, max_batch=B, max_k=k) as idx:
+        idx.synth(1)
+        idx.upload(X[:3000], 0)
+        idx.upload(X[3000:], 3000)
+        idx.set_option(vx.VX_OPT_COARSE, vx.VX_COARSE_BF16)
+        ids, sc = idx.search(Q, k)
+    rid, rsc = oracle.flat_topk(X, Q, k, mode=1)
+    assert np.array_equal(ids, rid)
