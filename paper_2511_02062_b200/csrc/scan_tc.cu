@@ -24,18 +24,19 @@
 
 namespace vx {
 
-constexpr int kTcTD = 128;            // documents per tile (MMA N)
 constexpr int kTcKC = 16;             // per-CTA list length per query
 constexpr int kTcStageUnit = 16384;   // one 128-row x 128-byte operand tile
 
-template <int QT>
+// QT: 128-query tiles per launch (A operands); TD: documents per tile (MMA N, 128 or 256).
+// A bigger TD re-streams the query tiles from L2 half as often per document byte.
+template <int QT, int TD>
 struct TcCfg {
-  static constexpr int EG = QT == 1 ? 1 : 2;               // epilogue warp groups
+  static constexpr int EG = QT == 1 ? 1 : 2;                       // epilogue warp groups
   static constexpr int kThreads = (2 + 4 * EG) * 32;
-  static constexpr int NBUF = 2;                            // accumulator buffers
-  static constexpr int kTmemCols = NBUF * QT * kTcTD;       // 256 or 512
-  static constexpr int kStageBytes = (QT + 1) * kTcStageUnit;
-  static constexpr int QPT = QT / EG;                       // query tiles per epilogue thread
+  static constexpr int NBUF = (2 * QT * TD <= 512) ? 2 : 1;         // accumulator buffers
+  static constexpr int kTmemCols = NBUF * QT * TD;                  // 256 or 512
+  static constexpr int kStageBytes = QT * kTcStageUnit + TD * 128;
+  static constexpr int QPT = QT / EG;                               // query tiles per epilogue thread
 };
 
 // Insert a candidate into one query's descending list (smem, stride `ld` between entries)
@@ -61,11 +62,11 @@ __device__ __noinline__ float tc_list_insert(uint64_t* L, int ld, float sc, uint
   return nl == 0ull ? -INFINITY : vx_key_score(nl);
 }
 
-template <int QT>
-__global__ void __launch_bounds__(TcCfg<QT>::kThreads, 1)
+template <int QT, int TD>
+__global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
     scan_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tx,
                    const ScanTcArgs a) {
-  using C = TcCfg<QT>;
+  using C = TcCfg<QT, TD>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   const int ns = a.ns;
@@ -82,7 +83,7 @@ __global__ void __launch_bounds__(TcCfg<QT>::kThreads, 1)
   const int cw = a.fmt == 2 ? 32 : 64;
   const int nch = a.D / cw;
   const uint32_t n_local = a.n_local;
-  const int ntiles = (int)((n_local + kTcTD - 1) / kTcTD);
+  const int ntiles = (int)((n_local + TD - 1) / TD);
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tq);
@@ -108,7 +109,7 @@ __global__ void __launch_bounds__(TcCfg<QT>::kThreads, 1)
     if (lane == 0) {
       const uint64_t pol_x = policy_evict_first();
       const uint64_t pol_q = policy_evict_last();
-      const uint32_t bytes = (uint32_t)(QT * a.a_rows * 128 + kTcTD * 128);
+      const uint32_t bytes = (uint32_t)(QT * a.a_rows * 128 + TD * 128);
       int s = 0;
       uint32_t ph = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -119,7 +120,10 @@ __global__ void __launch_bounds__(TcCfg<QT>::kThreads, 1)
 #pragma unroll
           for (int qt = 0; qt < QT; ++qt)
             tma_load_2d(st + qt * kTcStageUnit, &tq, &full[s], c * cw, qt * 128, pol_q);
-          tma_load_2d(st + QT * kTcStageUnit, &tx, &full[s], c * cw, tile * kTcTD, pol_x);
+#pragma unroll
+          for (int h = 0; h < TD; h += 128)  // the document map's box is 128 rows
+            tma_load_2d(st + QT * kTcStageUnit + h * 128, &tx, &full[s], c * cw, tile * TD + h,
+                        pol_x);
           if (++s == ns) {
             s = 0;
             ph ^= 1;
@@ -130,7 +134,7 @@ __global__ void __launch_bounds__(TcCfg<QT>::kThreads, 1)
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer (one thread)
     if (lane == 0) {
-      const uint32_t idesc = make_idesc((uint32_t)a.fmt /*2 TF32, 1 BF16*/, 128u, (uint32_t)kTcTD);
+      const uint32_t idesc = make_idesc((uint32_t)a.fmt /*2 TF32, 1 BF16*/, 128u, (uint32_t)TD);
       int s = 0;
       uint32_t ph = 0;
       int buf = 0;
@@ -144,7 +148,7 @@ __global__ void __launch_bounds__(TcCfg<QT>::kThreads, 1)
           const uint32_t st = smem_u32(smem + (size_t)s * C::kStageBytes);
 #pragma unroll
           for (int qt = 0; qt < QT; ++qt) {
-            const uint32_t d = tmem_base + (uint32_t)((buf * QT + qt) * kTcTD);
+            const uint32_t d = tmem_base + (uint32_t)((buf * QT + qt) * TD);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               const uint64_t ad = umma_desc_sw128(st + qt * kTcStageUnit + j * 32);
@@ -192,15 +196,15 @@ __global__ void __launch_bounds__(TcCfg<QT>::kThreads, 1)
         const int qt = g + t * C::EG;
         const int q = qt * 128 + m;
         uint64_t* L = lists + qt * 128 + m;
-        const uint32_t col = tmem_base + (uint32_t)((buf * QT + qt) * kTcTD) +
+        const uint32_t col = tmem_base + (uint32_t)((buf * QT + qt) * TD) +
                              ((uint32_t)(quad * 32) << 16);
 #pragma unroll 1
-        for (int cc = 0; cc < kTcTD / 32; ++cc) {
+        for (int cc = 0; cc < TD / 32; ++cc) {
           uint32_t r[32];
           tmem_ld32(col + cc * 32, r);
           tmem_ld_wait();
           if (q < a.B) {
-            const uint32_t doc0 = (uint32_t)tile * kTcTD + cc * 32;
+            const uint32_t doc0 = (uint32_t)tile * TD + cc * 32;
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               const float sc = __uint_as_float(r[i]);
@@ -348,29 +352,31 @@ __global__ void row_norm_max_kernel(const float* __restrict__ docs, int64_t n, i
 }
 
 // ------------------------------------------------------------------- host side
-size_t scan_tc_smem(int QT, int* ns_out) {
-  const int stage = (QT + 1) * kTcStageUnit;
-  int ns = QT == 1 ? 6 : 4;
+size_t scan_tc_smem(int QT, int TD, int* ns_out) {
+  const int stage = QT * kTcStageUnit + TD * 128;
+  const size_t fixed = (size_t)QT * 128 * kTcKC * 8 + 16 + 1024;
+  int ns = 6;
+  while (ns > 2 && (size_t)ns * stage + fixed + (2 * ns + 4) * 8 > 227 * 1024) --ns;
   *ns_out = ns;
-  return (size_t)ns * stage + (size_t)QT * 128 * kTcKC * 8 + (size_t)(2 * ns + 4) * 8 + 16 + 1024;
+  return (size_t)ns * stage + fixed + (size_t)(2 * ns + 4) * 8;
 }
 
-cudaError_t launch_scan_tc(int QT, const CUtensorMap* tq, const CUtensorMap* tx,
+template <int QT, int TD>
+static cudaError_t launch_tc(const CUtensorMap* tq, const CUtensorMap* tx, const ScanTcArgs& a,
+                             int grid, size_t smem, cudaStream_t st) {
+  auto kfn = scan_tc_kernel<QT, TD>;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kfn<<<grid, TcCfg<QT, TD>::kThreads, smem, st>>>(*tq, *tx, a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scan_tc(int QT, int TD, const CUtensorMap* tq, const CUtensorMap* tx,
                            const ScanTcArgs& a, int grid, size_t smem, cudaStream_t st) {
-  if (QT == 1) {
-    auto kfn = scan_tc_kernel<1>;
-    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    kfn<<<grid, TcCfg<1>::kThreads, smem, st>>>(*tq, *tx, a);
-    return cudaGetLastError();
-  }
-  if (QT == 2) {
-    auto kfn = scan_tc_kernel<2>;
-    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    kfn<<<grid, TcCfg<2>::kThreads, smem, st>>>(*tq, *tx, a);
-    return cudaGetLastError();
-  }
+  if (QT == 1 && TD == 128) return launch_tc<1, 128>(tq, tx, a, grid, smem, st);
+  if (QT == 1 && TD == 256) return launch_tc<1, 256>(tq, tx, a, grid, smem, st);
+  if (QT == 2 && TD == 128) return launch_tc<2, 128>(tq, tx, a, grid, smem, st);
+  if (QT == 2 && TD == 256) return launch_tc<2, 256>(tq, tx, a, grid, smem, st);
   return cudaErrorInvalidValue;
 }
 

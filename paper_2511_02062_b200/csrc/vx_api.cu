@@ -169,6 +169,7 @@ struct vx_index {
   CUtensorMap tmap_docs16{};
   uint16_t* d_q16 = nullptr;     // [maxB][D] bf16 queries for the bf16 coarse scan
   int coarse = VX_COARSE_AUTO;
+  int scan_tile = 0;             // documents per tensor-core tile (0 = auto)
   // options
   int scan_algo = VX_SCAN_AUTO;
   int maxsim_algo = VX_MAXSIM_AUTO;
@@ -359,6 +360,11 @@ extern "C" vx_status vx_set_option(vx_index* h, int32_t option, int64_t value) {
     case VX_OPT_GRID:
       if (value < 0 || value > h->num_sms) return fail(VX_ERR_INVALID, "grid %lld", (long long)value);
       h->grid = value == 0 ? h->num_sms : (int)value;
+      return VX_OK;
+    case VX_OPT_SCAN_TILE:
+      if (value != 0 && value != 128 && value != 256)
+        return fail(VX_ERR_INVALID, "scan tile %lld (0, 128 or 256)", (long long)value);
+      h->scan_tile = (int)value;
       return VX_OK;
     case VX_OPT_COARSE:
       if (value != VX_COARSE_AUTO && value != VX_COARSE_TF32 && value != VX_COARSE_BF16)
@@ -557,7 +563,8 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
       VX_TRY(make_tmap_2d(&tq, d_q + (size_t)g0 * D, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
                           (uint64_t)Bg, D, 32, (uint32_t)a_rows));
     int ns = 0;
-    const size_t smem = vx::scan_tc_smem(QT, &ns);
+    const int TD = h->scan_tile ? h->scan_tile : 256;
+    const size_t smem = vx::scan_tc_smem(QT, TD, &ns);
     vx::ScanTcArgs a;
     a.n_local = (uint32_t)h->n_local;
     a.D = D;
@@ -566,7 +573,8 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
     a.a_rows = a_rows;
     a.fmt = bf16 ? 1 : 2;
     a.part = h->d_part + (size_t)g0 * grid * vx::kTcListLen;
-    CU_TRY(vx::launch_scan_tc(QT, &tq, bf16 ? &h->tmap_docs16 : &h->tmap_docs, a, grid, smem, st));
+    CU_TRY(vx::launch_scan_tc(QT, TD, &tq, bf16 ? &h->tmap_docs16 : &h->tmap_docs, a, grid, smem,
+                              st));
     count_launch(h);
   }
   CU_TRY(cudaEventRecord(h->ev[1], st));

@@ -46,8 +46,8 @@ constexpr float kErrCoefTF32 = 0.001953125f + 0.000244140625f;
 constexpr float kErrCoefBF16 = 0.00390625f + 0.000244140625f;
 cudaError_t launch_to_bf16(const float* in, uint16_t* out, int64_t n, cudaStream_t st);
 constexpr int kTcListLen = 16;
-size_t scan_tc_smem(int QT, int* ns_out);
-cudaError_t launch_scan_tc(int QT, const CUtensorMap* tq, const CUtensorMap* tx,
+size_t scan_tc_smem(int QT, int TD, int* ns_out);
+cudaError_t launch_scan_tc(int QT, int TD, const CUtensorMap* tq, const CUtensorMap* tx,
                            const ScanTcArgs& a, int grid, size_t smem, cudaStream_t st);
 cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64_t* cand, int B,
                           int kp, const uint64_t* part, int grid, int k, int64_t row0,
