@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
           uint32_t r[32];
           tmem_ld32(col + cc * 32, r);
           tmem_ld_wait();
-          if (q < a.B) {
+          if (q < a.B && !a.dbg_no_select) {
             const uint32_t doc0 = (uint32_t)tile * TD + cc * 32;
 #pragma unroll
             for (int i = 0; i < 32; ++i) {

@@ -563,8 +563,8 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
       VX_TRY(make_tmap_2d(&tq, d_q + (size_t)g0 * D, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
                           (uint64_t)Bg, D, 32, (uint32_t)a_rows));
     int ns = 0;
-    const int TD = h->scan_tile ? h->scan_tile : 256;
-    const size_t smem = vx::scan_tc_smem(QT, TD, &ns);
+    const int TD = h->scan_tile ? h->scan_tile : (QT == 1 ? 256 : 128);
+    size_t smem = vx::scan_tc_smem(QT, TD, &ns);
     vx::ScanTcArgs a;
     a.n_local = (uint32_t)h->n_local;
     a.D = D;
@@ -572,6 +572,15 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
     a.ns = ns;
     a.a_rows = a_rows;
     a.fmt = bf16 ? 1 : 2;
+    a.dbg_no_select = 0;
+    if (const char* e = getenv("VX_DEBUG_TC_STAGES")) {  // timing experiments only
+      const int want = atoi(e);
+      if (want >= 2 && want < ns) {
+        smem -= (size_t)(ns - want) * (QT * 16384 + TD * 128 + 16);
+        a.ns = ns = want;
+      }
+    }
+    if (getenv("VX_DEBUG_TC_NOSELECT")) a.dbg_no_select = 1;
     a.part = h->d_part + (size_t)g0 * grid * vx::kTcListLen;
     CU_TRY(vx::launch_scan_tc(QT, TD, &tq, bf16 ? &h->tmap_docs16 : &h->tmap_docs, a, grid, smem,
                               st));

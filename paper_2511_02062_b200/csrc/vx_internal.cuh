@@ -37,6 +37,7 @@ struct ScanTcArgs {
   int32_t ns;        // pipeline stages
   int32_t a_rows;    // TMA box rows of the query map (multiple of 8, <= 128)
   int32_t fmt;       // operand format: 2 = fp32 read as TF32 (kind::tf32), 1 = bf16 (kind::f16)
+  int32_t dbg_no_select;  // timing experiments only (VX_DEBUG_TC_NOSELECT): skip the top-k
   uint64_t* part;    // [B][gridDim.x][16] coarse keys
 };
 // coarse-score error bound coefficients E = coef * ||q|| * max||x|| (see scan_tc.cu):
