@@ -39,29 +39,6 @@ struct TcCfg {
   static constexpr int QPT = QT / EG;                               // query tiles per epilogue thread
 };
 
-// Insert a candidate into one query's descending list (smem, stride `ld` between entries)
-// and return the new admission threshold.  Out of line on purpose: the caller tests 128
-// scores per tile inline, and an inlined insertion per score would blow the I-cache
-// (measured: 4x slower epilogue).
-__device__ __noinline__ float tc_list_insert(uint64_t* L, int ld, float sc, uint32_t doc,
-                                             uint32_t n_local) {
-  const uint64_t last = L[(kTcKC - 1) * ld];
-  if (doc < n_local) {
-    uint64_t key = vx_make_key(sc, doc);
-    if (key > last) {
-      for (int j = 0; j < kTcKC; ++j) {
-        const uint64_t a = L[j * ld];
-        if (key > a) {
-          L[j * ld] = key;
-          key = a;
-        }
-      }
-    }
-  }
-  const uint64_t nl = L[(kTcKC - 1) * ld];
-  return nl == 0ull ? -INFINITY : vx_key_score(nl);
-}
-
 template <int QT, int TD>
 __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
     scan_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tx,
@@ -178,14 +155,21 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
     const int g = e >> 2;                 // epilogue group
     const int quad = warp & 3;            // TMEM lane quadrant this warp may access
     const int m = quad * 32 + lane;       // query row within a 128-query tile
-    constexpr int LD = QT * 128;          // list stride (entries of one query are LD apart)
+    // Selection.  Fast path: one max over the 32 scores of a column chunk against the
+    // query's admission threshold (the 16th best key so far); only when it passes are the
+    // passing positions enumerated (bit mask) and inserted into the register-resident
+    // descending list with an unrolled compare-exchange network.  The scores of a passing
+    // chunk are parked in smem so the enumeration can index them.
+    constexpr int NEPI = 4 * C::EG * 32;
+    float* scratch = reinterpret_cast<float*>(lists) + (e * 32 + lane);  // [32][NEPI]
+    uint64_t L[C::QPT][kTcKC];
+#pragma unroll
+    for (int t = 0; t < C::QPT; ++t)
+#pragma unroll
+      for (int j = 0; j < kTcKC; ++j) L[t][j] = 0ull;
     float thr[C::QPT];
 #pragma unroll
-    for (int t = 0; t < C::QPT; ++t) {
-      const int qt = g + t * C::EG;
-      for (int j = 0; j < kTcKC; ++j) lists[j * LD + qt * 128 + m] = 0ull;
-      thr[t] = -INFINITY;
-    }
+    for (int t = 0; t < C::QPT; ++t) thr[t] = -INFINITY;
     int buf = 0;
     uint32_t bph = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -195,7 +179,6 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
       for (int t = 0; t < C::QPT; ++t) {
         const int qt = g + t * C::EG;
         const int q = qt * 128 + m;
-        uint64_t* L = lists + qt * 128 + m;
         const uint32_t col = tmem_base + (uint32_t)((buf * QT + qt) * TD) +
                              ((uint32_t)(quad * 32) << 16);
 #pragma unroll 1
@@ -203,13 +186,33 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
           uint32_t r[32];
           tmem_ld32(col + cc * 32, r);
           tmem_ld_wait();
-          if (q < a.B && !a.dbg_no_select) {
-            const uint32_t doc0 = (uint32_t)tile * TD + cc * 32;
+          if (q >= a.B || a.dbg_no_select) continue;
+          float mx = __uint_as_float(r[0]);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const float sc = __uint_as_float(r[i]);
-              if (sc >= thr[t]) thr[t] = tc_list_insert(L, LD, sc, doc0 + i, n_local);
+          for (int i = 1; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(r[i]));
+          if (mx < thr[t]) continue;  // common case after the first tiles
+          uint32_t mask = 0;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float sc = __uint_as_float(r[i]);
+            mask |= (sc >= thr[t] ? 1u : 0u) << i;
+            scratch[i * NEPI] = sc;
+          }
+          const uint32_t doc0 = (uint32_t)tile * TD + cc * 32;
+          while (mask) {
+            const int i = __ffs(mask) - 1;
+            mask &= mask - 1;
+            const uint32_t doc = doc0 + i;
+            if (doc >= n_local) break;  // positions are increasing: the rest are padding
+            uint64_t key = vx_make_key(scratch[i * NEPI], doc);
+            if (key <= L[t][kTcKC - 1]) continue;
+#pragma unroll
+            for (int j = 0; j < kTcKC; ++j) {  // insertion into the sorted list
+              const uint64_t a0 = L[t][j];
+              L[t][j] = a0 > key ? a0 : key;
+              key = a0 > key ? key : a0;
             }
+            thr[t] = L[t][kTcKC - 1] == 0ull ? -INFINITY : vx_key_score(L[t][kTcKC - 1]);
           }
         }
       }
@@ -227,7 +230,8 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
       const int q = qt * 128 + m;
       if (q < a.B) {
         uint64_t* out = a.part + ((size_t)q * gridDim.x + blockIdx.x) * kTcKC;
-        for (int j = 0; j < kTcKC; ++j) out[j] = lists[j * LD + qt * 128 + m];
+#pragma unroll
+        for (int j = 0; j < kTcKC; ++j) out[j] = L[t][j];
       }
     }
   }
