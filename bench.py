@@ -50,7 +50,7 @@ def parse() -> argparse.Namespace:
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n-docs", type=int, default=10_000_000)
     ap.add_argument("--dim", type=int, default=768)
-    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--batch", type=int, default=128)
     ap.add_argument("--k", type=int, default=100)
     ap.add_argument("--nq", type=int, default=32)
     ap.add_argument("--tok-per-doc", type=int, default=128)

@@ -563,7 +563,9 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
       VX_TRY(make_tmap_2d(&tq, d_q + (size_t)g0 * D, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
                           (uint64_t)Bg, D, 32, (uint32_t)a_rows));
     int ns = 0;
-    const int TD = h->scan_tile ? h->scan_tile : (QT == 1 ? 256 : 128);
+    // 256-document tiles halve the per-document query re-streaming from L2 (measured: B=128
+    // bf16 2.31 ms vs 3.78 ms with 128; B=256 3.9 ms vs 4.36 ms) — profiles/r01/
+    const int TD = h->scan_tile ? h->scan_tile : 256;
     size_t smem = vx::scan_tc_smem(QT, TD, &ns);
     vx::ScanTcArgs a;
     a.n_local = (uint32_t)h->n_local;
