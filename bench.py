@@ -62,6 +62,8 @@ def parse() -> argparse.Namespace:
                     help="operand format of the tensor-core candidate scan (exact fp32 re-rank either way)")
     ap.add_argument("--tile", type=int, default=0, choices=[0, 128, 256],
                     help="documents per tensor-core scan tile (0 = library default)")
+    ap.add_argument("--graphs", type=int, default=1, choices=[0, 1],
+                    help="replay one captured CUDA graph per batch shape (single GPU)")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -180,6 +182,8 @@ def run_ours(args) -> None:
     idx = vx.Index(args.n_docs, D, device=local, n_shards=world, shard=rank,
                    tok_per_doc=args.tok_per_doc, tok_dim=td, tok_blocks=args.tok_blocks,
                    max_batch=B, max_k=k, max_qtok=nq)
+    if args.graphs:
+        idx.set_option(vx.VX_OPT_GRAPHS, 1)
     if args.tile:
         idx.set_option(vx.VX_OPT_SCAN_TILE, args.tile)
     if args.coarse != "auto":

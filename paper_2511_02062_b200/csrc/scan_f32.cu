@@ -90,6 +90,13 @@ __global__ void __launch_bounds__(kScanThreads, 1)
   const int nch = D >> 5;
   const uint32_t n_local = a.n_local;
   const int ntiles = (int)((n_local + TD - 1) / TD);
+  // queries in this launch: static, or read on device (exact re-scan of the queries whose
+  // tensor-core certificate failed; the count is only known on the GPU)
+  int nB = a.B;
+  if (a.d_count) {
+    nB = min(nB, *a.d_count - a.g0);
+    if (nB <= 0) return;
+  }
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmap);
@@ -101,7 +108,7 @@ __global__ void __launch_bounds__(kScanThreads, 1)
   }
   for (int i = threadIdx.x; i < BQ * D; i += blockDim.x) {
     int qi = i / D, t = i - qi * D;
-    q_s[qi * QS + t] = (qi < a.B) ? a.q[(size_t)qi * D + t] : 0.0f;
+    q_s[qi * QS + t] = (qi < nB) ? a.q[(size_t)qi * D + t] : 0.0f;
   }
   for (int i = threadIdx.x; i < BQ; i += blockDim.x) {
     thr_s[i] = 0ull;
@@ -188,7 +195,7 @@ __global__ void __launch_bounds__(kScanThreads, 1)
     named_bar_sync(1, kComputeWarps * 32);
 
     // selection: one warp per query
-    for (int qi = warp; qi < a.B; qi += kComputeWarps) {
+    for (int qi = warp; qi < nB; qi += kComputeWarps) {
       uint64_t* cb = cand + (size_t)qi * cap;
       int cnt = cnt_s[qi];
       uint64_t thr = thr_s[qi];
@@ -224,7 +231,7 @@ __global__ void __launch_bounds__(kScanThreads, 1)
 
   // final per-CTA lists
   named_bar_sync(1, kComputeWarps * 32);
-  for (int qi = warp; qi < a.B; qi += kComputeWarps) {
+  for (int qi = warp; qi < nB; qi += kComputeWarps) {
     uint64_t* cb = cand + (size_t)qi * cap;
     const int cnt = cnt_s[qi];
     for (int i = cnt + lane; i < cap; i += 32) cb[i] = 0ull;

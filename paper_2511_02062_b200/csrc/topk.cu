@@ -39,7 +39,8 @@ __device__ __forceinline__ void block_bitonic_desc(uint64_t* buf, int n) {
 __global__ void __launch_bounds__(kMergeThreads)
     merge_topk_kernel(const uint64_t* __restrict__ in, int M, int k, int64_t id_base,
                       uint64_t* __restrict__ out_keys, int64_t* __restrict__ out_ids,
-                      float* __restrict__ out_scores) {
+                      float* __restrict__ out_scores, const int* __restrict__ d_count) {
+  if (d_count && (int)blockIdx.x >= *d_count) return;  // device-sized batch (cert fallback)
   __shared__ uint32_t hist[256];
   __shared__ uint64_t s_prefix, s_mask;
   __shared__ int s_kk, s_done, s_above, s_eq;
@@ -115,10 +116,10 @@ __global__ void __launch_bounds__(kMergeThreads)
 
 cudaError_t launch_merge_topk(const uint64_t* in, int B, int M, int k, int64_t id_base,
                               uint64_t* out_keys, int64_t* out_ids, float* out_scores,
-                              cudaStream_t st) {
+                              cudaStream_t st, const int* d_count) {
   if (k < 1 || k > kMaxK || M < k) return cudaErrorInvalidValue;
   merge_topk_kernel<<<B, kMergeThreads, 0, st>>>(in, M, k, id_base, out_keys, out_ids,
-                                                 out_scores);
+                                                 out_scores, d_count);
   return cudaGetLastError();
 }
 
@@ -178,6 +179,63 @@ cudaError_t launch_order_by(const float* key_score, const int64_t* ids, const fl
                             cudaStream_t st) {
   if (k < 1 || k > kMaxK) return cudaErrorInvalidValue;
   order_by_kernel<<<B, 256, 0, st>>>(key_score, ids, ip, k, out_ids, out_ip, out_ms);
+  return cudaGetLastError();
+}
+
+}  // namespace vx
+
+namespace vx {
+
+// ---- device-side handling of tensor-core certificate failures (no host round trip, so the
+// whole stage can live in one CUDA graph)
+__global__ void cert_compact_kernel(const int* __restrict__ flags, int B,
+                                    const float* __restrict__ q, int D, int* __restrict__ fidx,
+                                    int* __restrict__ fcount, float* __restrict__ fq) {
+  __shared__ int s_idx[1024];
+  __shared__ int s_n;
+  if (threadIdx.x == 0) {
+    int n = 0;
+    for (int b = 0; b < B; ++b)
+      if (flags[b]) s_idx[n++] = b;  // ascending query order
+    s_n = n;
+    fcount[0] = n;   // this batch
+    fcount[1] += n;  // running total (vx_stats.cert_fallbacks)
+  }
+  __syncthreads();
+  const int n = s_n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) fidx[i] = s_idx[i];
+  for (int i = threadIdx.x; i < n * D; i += blockDim.x) {
+    const int r = i / D;
+    fq[i] = q[(size_t)s_idx[r] * D + (i - r * D)];
+  }
+}
+
+__global__ void cert_scatter_kernel(const int* __restrict__ fidx, const int* __restrict__ fcount,
+                                    int k, const uint64_t* __restrict__ fkeys,
+                                    const int64_t* __restrict__ fids, const float* __restrict__ fsc,
+                                    uint64_t* __restrict__ keys, int64_t* __restrict__ ids,
+                                    float* __restrict__ scores) {
+  const int i = blockIdx.x;
+  if (i >= *fcount) return;
+  const size_t dst = (size_t)fidx[i] * k, src = (size_t)i * k;
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    keys[dst + j] = fkeys[src + j];
+    ids[dst + j] = fids[src + j];
+    scores[dst + j] = fsc[src + j];
+  }
+}
+
+cudaError_t launch_cert_compact(const int* flags, int B, const float* q, int D, int* fidx,
+                                int* fcount, float* fq, cudaStream_t st) {
+  if (B > 1024) return cudaErrorInvalidValue;
+  cert_compact_kernel<<<1, 512, 0, st>>>(flags, B, q, D, fidx, fcount, fq);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cert_scatter(const int* fidx, const int* fcount, int B, int k,
+                                const uint64_t* fkeys, const int64_t* fids, const float* fsc,
+                                uint64_t* keys, int64_t* ids, float* scores, cudaStream_t st) {
+  cert_scatter_kernel<<<B, 128, 0, st>>>(fidx, fcount, k, fkeys, fids, fsc, keys, ids, scores);
   return cudaGetLastError();
 }
 

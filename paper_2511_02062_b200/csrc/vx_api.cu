@@ -23,6 +23,7 @@
 #include <atomic>
 #include <chrono>
 #include <thread>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -192,6 +193,8 @@ struct vx_index {
   int* d_flags = nullptr;        // [maxB] certificate failures (TC path)
   unsigned int* d_xnorm = nullptr;  // max row norm of the shard (float bits)
   float* d_fq = nullptr;         // [maxB][D] queries gathered for the exact fallback
+  int* d_fidx = nullptr;         // [maxB] flagged query indices
+  int* d_fcount = nullptr;       // [2] flagged count of the last batch, running total
   // pinned host staging
   void* h_stage = nullptr;
   size_t h_stage_bytes = 0;
@@ -204,6 +207,13 @@ struct vx_index {
   vx_stats st{};
   cudaEvent_t ev[4] = {};
   bool timing_pending = false;
+  // CUDA graphs per (op, B, k, nq)
+  struct GraphEntry {
+    cudaGraphExec_t exec;
+    int launches;
+  };
+  bool use_graphs = false;
+  std::map<uint64_t, GraphEntry> graphs;
 };
 
 static void count_launch(vx_index* h, int n = 1) { h->st.kernel_launches += n; }
@@ -285,6 +295,8 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
   ALLOC(h->d_flags, B * 4);
   ALLOC(h->d_xnorm, 4);
   ALLOC(h->d_fq, B * D * 4);
+  ALLOC(h->d_fidx, B * 4);
+  ALLOC(h->d_fcount, 16);
   if (!(d->flags & VX_FLAG_NO_BF16_SHADOW)) {
     ALLOC(h->docs16, (size_t)h->n_local * D * 2);
     ALLOC(h->d_q16, B * D * 2);
@@ -302,7 +314,8 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
     return cleanup(fail(VX_ERR_OOM, "pinned header"));
   if (cudaMallocHost((void**)&h->h_flags, B * 4) != cudaSuccess)
     return cleanup(fail(VX_ERR_OOM, "pinned flags"));
-  if (cudaMemset(h->d_xnorm, 0, 4) != cudaSuccess) return cleanup(fail(VX_ERR_CUDA, "memset"));
+  if (cudaMemset(h->d_xnorm, 0, 4) != cudaSuccess || cudaMemset(h->d_fcount, 0, 16) != cudaSuccess)
+    return cleanup(fail(VX_ERR_CUDA, "memset"));
   if (h->tokens) {
     s = make_tmap_2d(&h->tmap_tok, h->tokens, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                      (uint64_t)d->tok_blocks * d->tok_per_doc, (uint64_t)d->tok_dim, 64,
@@ -326,10 +339,11 @@ extern "C" vx_status vx_index_destroy(vx_index* h) {
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   if (h->comm) nccl().CommDestroy(h->comm);
+  for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second.exec);
   void* ptrs[] = {h->docs,  h->tokens,    h->d_q,      h->d_qtok,    h->d_part, h->d_keys,
                   h->d_ids, h->d_ip,      h->d_ms,     h->d_out_ids, h->d_out_ip,
                   h->d_out_ms, h->d_send, h->d_recv, h->d_hdr, h->d_ckeys, h->d_flags,
-                  h->d_xnorm, h->d_fq, h->docs16, h->d_q16};
+                  h->d_xnorm, h->d_fq, h->docs16, h->d_q16, h->d_fidx, h->d_fcount};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->h_stage) cudaFreeHost(h->h_stage);
@@ -382,7 +396,9 @@ extern "C" vx_status vx_set_option(vx_index* h, int32_t option, int64_t value) {
       h->maxsim_algo = (int)value;
       return VX_OK;
     case VX_OPT_GRAPHS:
-      return value == 0 ? VX_OK : fail(VX_ERR_UNSUPPORTED, "graphs not built yet");
+      if (value != 0 && value != 1) return fail(VX_ERR_INVALID, "graphs %lld", (long long)value);
+      h->use_graphs = value == 1;
+      return VX_OK;
     default:
       return fail(VX_ERR_INVALID, "unknown option %d", option);
   }
@@ -395,6 +411,9 @@ extern "C" vx_status vx_get_stats(const vx_index* h, vx_stats* out) {
 }
 extern "C" vx_status vx_reset_stats(vx_index* h) {
   if (!h) return fail(VX_ERR_INVALID, "null handle");
+  CU_TRY(cudaSetDevice(h->device));
+  CU_TRY(cudaStreamSynchronize(h->stream));
+  CU_TRY(cudaMemset(h->d_fcount, 0, 16));
   h->st = vx_stats{};
   return VX_OK;
 }
@@ -497,7 +516,8 @@ static vx_status check_batch(vx_index* h, int32_t B, int32_t k) {
 
 // Exact path: K1 scan + merge: d_q [B][D] -> keys (global ids) / ids / scores [B][k]
 static vx_status local_topk_f32(vx_index* h, const float* d_q, int B, int k, uint64_t* keys,
-                                int64_t* ids, float* scores, cudaStream_t st) {
+                                int64_t* ids, float* scores, cudaStream_t st,
+                                const int* d_count = nullptr) {
   const int D = h->desc.dim;
   const int kcap = kcap_of(k);
   const int grid = h->grid;
@@ -519,12 +539,15 @@ static vx_status local_topk_f32(vx_index* h, const float* d_q, int B, int k, uin
     a.cap = cap;
     a.ns = ns;
     a.part = h->d_part + (size_t)g0 * grid * kcap;
-    if (g0 == 0) CU_TRY(cudaEventRecord(h->ev[0], st));
+    a.d_count = d_count;
+    a.g0 = g0;
+    if (g0 == 0 && !d_count) CU_TRY(cudaEventRecord(h->ev[0], st));
     CU_TRY(vx::launch_scan_f32(bucket, &h->tmap_docs, a, grid, smem, st));
     count_launch(h);
   }
-  CU_TRY(cudaEventRecord(h->ev[1], st));
-  CU_TRY(vx::launch_merge_topk(h->d_part, B, grid * kcap, k, h->row0, keys, ids, scores, st));
+  if (!d_count) CU_TRY(cudaEventRecord(h->ev[1], st));
+  CU_TRY(vx::launch_merge_topk(h->d_part, B, grid * kcap, k, h->row0, keys, ids, scores, st,
+                               d_count));
   count_launch(h);
   return VX_OK;
 }
@@ -597,28 +620,18 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
                            bf16 ? vx::kErrCoefBF16 : vx::kErrCoefTF32, keys, ids, scores,
                            h->d_flags, st));
   count_launch(h);
-  // certificate failures: re-scan those queries exactly (expected ~never on real data)
-  CU_TRY(cudaMemcpyAsync(h->h_flags, h->d_flags, (size_t)B * 4, cudaMemcpyDeviceToHost, st));
-  CU_TRY(cudaStreamSynchronize(st));
-  std::vector<int> bad;
-  for (int b = 0; b < B; ++b)
-    if (h->h_flags[b]) bad.push_back(b);
-  if (bad.empty()) return VX_OK;
-  h->st.cert_fallbacks += bad.size();
-  for (size_t i = 0; i < bad.size(); ++i)
-    CU_TRY(cudaMemcpyAsync(h->d_fq + i * D, d_q + (size_t)bad[i] * D, (size_t)D * 4,
-                           cudaMemcpyDeviceToDevice, st));
-  const int nb = (int)bad.size();
-  uint64_t* fk = h->d_ckeys;  // reuse: [nb][k] (k <= 256)
+  // certificate failures: re-scan those queries exactly (expected ~never on real data).
+  // Entirely on device — compact the flagged queries, exact scan sized by the device count
+  // (launches with a zero count exit at once), scatter back — so no host round trip and
+  // the stage stays capturable in one CUDA graph.
+  CU_TRY(vx::launch_cert_compact(h->d_flags, B, d_q, D, h->d_fidx, h->d_fcount, h->d_fq, st));
+  count_launch(h);
+  uint64_t* fk = h->d_ckeys;  // reuse: [B][k] (k <= 256)
   int64_t* fi = h->d_out_ids;
   float* fs = h->d_out_ms;
-  VX_TRY(local_topk_f32(h, h->d_fq, nb, k, fk, fi, fs, st));
-  for (int i = 0; i < nb; ++i) {
-    const size_t o = (size_t)bad[i] * k, s = (size_t)i * k;
-    CU_TRY(cudaMemcpyAsync(keys + o, fk + s, (size_t)k * 8, cudaMemcpyDeviceToDevice, st));
-    CU_TRY(cudaMemcpyAsync(ids + o, fi + s, (size_t)k * 8, cudaMemcpyDeviceToDevice, st));
-    CU_TRY(cudaMemcpyAsync(scores + o, fs + s, (size_t)k * 4, cudaMemcpyDeviceToDevice, st));
-  }
+  VX_TRY(local_topk_f32(h, h->d_fq, B, k, fk, fi, fs, st, h->d_fcount));
+  CU_TRY(vx::launch_cert_scatter(h->d_fidx, h->d_fcount, B, k, fk, fi, fs, keys, ids, scores, st));
+  count_launch(h);
   return VX_OK;
 }
 
@@ -759,6 +772,65 @@ static vx_status stage_core(vx_index* h, int op, const float* d_q, const float* 
 }
 
 // Rank 0 entry: announce the batch to the shards, then run the core.
+// CUDA-graph mode (VX_OPT_GRAPHS, single GPU): the whole stage for one (op, B, k, nq) is
+// captured once and replayed — one launch per batch instead of ~8, no host work between the
+// kernels (the batcher hands each batch to the graph of its size, north star (e)).  The graph
+// reads the handle's fixed input buffers and writes its fixed output buffers; user pointers
+// are copied in/out around the replay.  The first batch of a shape runs eagerly (it also
+// sets the kernels' smem attributes) and captures the graph for the next ones.
+static vx_status stage_graph(vx_index* h, int op, const float* d_q, const float* d_qtok, int B,
+                             int nq, int k, int64_t* d_ids, float* d_ip, float* d_ms,
+                             cudaStream_t st) {
+  const size_t D = h->desc.dim, td = h->desc.tok_dim;
+  if (d_q != h->d_q)
+    CU_TRY(cudaMemcpyAsync(h->d_q, d_q, (size_t)B * D * 4, cudaMemcpyDeviceToDevice, st));
+  if (op == OP_RESCORE && d_qtok != h->d_qtok)
+    CU_TRY(cudaMemcpyAsync(h->d_qtok, d_qtok, (size_t)B * nq * td * 4, cudaMemcpyDeviceToDevice,
+                           st));
+  const uint64_t key = ((uint64_t)op << 48) | ((uint64_t)B << 24) | ((uint64_t)k << 12) | (uint64_t)nq;
+  auto it = h->graphs.find(key);
+  if (it == h->graphs.end()) {
+    CU_TRY(cudaEventRecord(h->ev[2], st));
+    VX_TRY(stage_core(h, op, h->d_q, h->d_qtok, B, nq, k, h->d_out_ids, h->d_out_ip, h->d_out_ms, st));
+    CU_TRY(cudaEventRecord(h->ev[3], st));
+    // capture on the handle's stream (after the eager run completes: capture records, it
+    // does not execute)
+    CU_TRY(cudaStreamSynchronize(st));
+    const uint64_t before = h->st.kernel_launches;
+    CU_TRY(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    cudaEventRecord(h->ev[2], h->stream);
+    vx_status s = stage_core(h, op, h->d_q, h->d_qtok, B, nq, k, h->d_out_ids, h->d_out_ip,
+                             h->d_out_ms, h->stream);
+    cudaEventRecord(h->ev[3], h->stream);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+    const int launches = (int)(h->st.kernel_launches - before);
+    h->st.kernel_launches = before;
+    if (s != VX_OK) {
+      if (g) cudaGraphDestroy(g);
+      return s;
+    }
+    if (e != cudaSuccess) return fail(VX_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
+    cudaGraphExec_t ex = nullptr;
+    e = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(VX_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
+    h->graphs[key] = {ex, launches};
+  } else {
+    CU_TRY(cudaGraphLaunch(it->second.exec, st));
+    h->st.kernel_launches += it->second.launches;
+    h->st.graph_replays += 1;
+  }
+  const size_t n = (size_t)B * k;
+  if (d_ids != h->d_out_ids)
+    CU_TRY(cudaMemcpyAsync(d_ids, h->d_out_ids, n * 8, cudaMemcpyDeviceToDevice, st));
+  if (d_ip != h->d_out_ip)
+    CU_TRY(cudaMemcpyAsync(d_ip, h->d_out_ip, n * 4, cudaMemcpyDeviceToDevice, st));
+  if (op == OP_RESCORE && d_ms != h->d_out_ms)
+    CU_TRY(cudaMemcpyAsync(d_ms, h->d_out_ms, n * 4, cudaMemcpyDeviceToDevice, st));
+  return VX_OK;
+}
+
 static vx_status stage_root(vx_index* h, int op, const float* d_q, const float* d_qtok, int B,
                             int nq, int k, int64_t* d_ids, float* d_ip, float* d_ms,
                             cudaStream_t st) {
@@ -777,9 +849,13 @@ static vx_status stage_root(vx_index* h, int op, const float* d_q, const float* 
                              h->comm, st));
     NCCL_TRY(nccl().GroupEnd());
   }
-  CU_TRY(cudaEventRecord(h->ev[2], st));
-  VX_TRY(stage_core(h, op, d_q, d_qtok, B, nq, k, d_ids, d_ip, d_ms, st));
-  CU_TRY(cudaEventRecord(h->ev[3], st));
+  if (h->use_graphs && h->nranks == 1) {
+    VX_TRY(stage_graph(h, op, d_q, d_qtok, B, nq, k, d_ids, d_ip, d_ms, st));
+  } else {
+    CU_TRY(cudaEventRecord(h->ev[2], st));
+    VX_TRY(stage_core(h, op, d_q, d_qtok, B, nq, k, d_ids, d_ip, d_ms, st));
+    CU_TRY(cudaEventRecord(h->ev[3], st));
+  }
   h->timing_pending = true;
   h->st.batches += 1;
   h->st.queries += B;
@@ -831,6 +907,9 @@ extern "C" vx_status vx_sync(vx_index* h) {
       h->st.timed_batches += 1;
     }
     h->timing_pending = false;
+    int fc[2] = {0, 0};  // certificate fallbacks counted on device
+    CU_TRY(cudaMemcpy(fc, h->d_fcount, 8, cudaMemcpyDeviceToHost));
+    h->st.cert_fallbacks = (uint64_t)fc[1];
   }
   cudaGetLastError();
   return VX_OK;

@@ -19,6 +19,8 @@ struct ScanF32Args {
   int32_t cap;         // candidate buffer per query
   int32_t ns;          // pipeline stages
   uint64_t* part;      // [B][gridDim.x][kcap] keys (score desc, local id asc)
+  const int* d_count;  // optional: queries actually present = min(B, *d_count - g0) (device)
+  int32_t g0;
 };
 
 // Returns the queries-per-launch bucket the f32 scan uses for a batch of B.
@@ -62,7 +64,14 @@ cudaError_t launch_row_norm_max(const float* docs, int64_t n, int D, unsigned in
 // descending to out_keys[q][k] (re-keyed with id + id_base), ids (-1 for empty) and scores.
 cudaError_t launch_merge_topk(const uint64_t* in, int B, int M, int k, int64_t id_base,
                               uint64_t* out_keys, int64_t* out_ids, float* out_scores,
-                              cudaStream_t st);
+                              cudaStream_t st, const int* d_count = nullptr);
+// Certificate failures (flags[B]) -> compacted list fidx/fcount and the flagged query rows
+// gathered into fq; after the exact re-scan, scatter its [fcount][k] results back.
+cudaError_t launch_cert_compact(const int* flags, int B, const float* q, int D, int* fidx,
+                                int* fcount, float* fq, cudaStream_t st);
+cudaError_t launch_cert_scatter(const int* fidx, const int* fcount, int B, int k,
+                                const uint64_t* fkeys, const int64_t* fids, const float* fsc,
+                                uint64_t* keys, int64_t* ids, float* scores, cudaStream_t st);
 // Order k candidates per query by a float score descending (ties id asc) and
 // permute the companion arrays: used to order by MaxSim after the IP top-k.
 cudaError_t launch_order_by(const float* key_score, const int64_t* ids, const float* ip, int B,

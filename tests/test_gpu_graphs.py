@@ -1,0 +1,74 @@
+"""CUDA-graph mode (VX_OPT_GRAPHS): one captured graph per (op, B, k, nq) replayed for every
+batch of that shape; results identical to the eager path, including the device-side exact
+re-scan of certificate failures.  Runs on a B200."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def vx(vxlib):
+    import paper_2511_02062_b200 as vx
+    return vx
+
+
+def test_graph_replay_matches_eager(vx, oracle):
+    from paper_2511_02062_b200 import synth
+    N, D, k, nq = 50_000, 768, 100, 32
+    with vx.Index(N, D, tok_per_doc=128, tok_dim=128, tok_blocks=300, max_batch=64, max_k=k,
+                  max_qtok=nq) as idx:
+        idx.synth(42)
+        idx.tokens_synth(45)
+        want = {}
+        for B in (1, 7, 64):
+            Q = synth.rows(43, 1000 * B, B, D)
+            qt = synth.query_tokens(B, nq, 128, seed=44 + B)
+            want[B] = (Q, qt, idx.search_rescore(Q, qt, k))
+        idx.set_option(vx.VX_OPT_GRAPHS, 1)
+        idx.reset_stats()
+        for rep in range(3):
+            for B in (1, 7, 64):
+                Q, qt, (ids, ip, ms) = want[B]
+                gids, gip, gms = idx.search_rescore(Q, qt, k)
+                assert np.array_equal(gids, ids) and np.array_equal(gip, ip) and np.array_equal(gms, ms)
+        st = idx.stats()
+    assert st["graph_replays"] == 6  # first batch of each shape runs eagerly and captures
+    assert st["batches"] == 9
+
+
+def test_graph_mode_device_pointers(vx):
+    import torch
+    from paper_2511_02062_b200 import synth
+    N, D, k, B = 30_000, 768, 10, 16
+    with vx.Index(N, D, max_batch=B, max_k=k) as idx:
+        idx.synth(42)
+        Q = synth.rows(43, 0, B, D)
+        ref, _ = idx.search(Q, k)
+        idx.set_option(vx.VX_OPT_GRAPHS, 1)
+        q = torch.from_numpy(Q).cuda()
+        ids = torch.empty((B, k), dtype=torch.int64, device="cuda")
+        sc = torch.empty((B, k), dtype=torch.float32, device="cuda")
+        s = torch.cuda.Stream()
+        for _ in range(4):
+            ids.zero_()
+            idx.search_dev(q, ids, sc, k, stream=s.cuda_stream)
+            s.synchronize()
+            assert np.array_equal(ids.cpu().numpy(), ref)
+
+
+def test_graph_with_certificate_fallback(vx, oracle):
+    N, D, B, k = 3000, 128, 4, 10
+    X = oracle.synth_rows(42, 0, N, D)
+    X[:600] = X[0]
+    Q = np.stack([X[0], X[0], oracle.synth_rows(43, 0, 1, D)[0], X[5]])
+    with vx.Index(N, D, max_batch=B, max_k=k) as idx:
+        idx.upload(X)
+        idx.set_option(vx.VX_OPT_GRAPHS, 1)
+        for _ in range(3):
+            ids, sc = idx.search(Q, k)
+            rid, _ = oracle.flat_topk(X, Q, k, mode=1)
+            assert np.array_equal(ids, rid)
+        assert idx.stats()["cert_fallbacks"] >= 6
