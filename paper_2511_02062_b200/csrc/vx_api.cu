@@ -205,7 +205,10 @@ struct vx_index {
   int nranks = 1, rank = 0;
   // stats
   vx_stats st{};
-  cudaEvent_t ev[4] = {};
+  cudaEvent_t ev[4] = {};        // eager-path timing events: scan begin/end, stage begin/end
+  cudaEvent_t gev[4] = {};       // the same, recorded by captured graph nodes
+  cudaEvent_t* tev = ev;         // events the code being issued records into
+  cudaEvent_t* last_tev = ev;    // events of the last issued batch (read by vx_sync)
   bool timing_pending = false;
   // CUDA graphs per (op, B, k, nq)
   struct GraphEntry {
@@ -306,6 +309,8 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
     return cleanup(fail(VX_ERR_CUDA, "stream create"));
   for (auto& e : h->ev)
     if (cudaEventCreate(&e) != cudaSuccess) return cleanup(fail(VX_ERR_CUDA, "event create"));
+  for (auto& e : h->gev)
+    if (cudaEventCreate(&e) != cudaSuccess) return cleanup(fail(VX_ERR_CUDA, "event create"));
   h->h_stage_bytes = B * D * 4 + (d->tok_per_doc > 0 ? B * d->max_qtok * d->tok_dim * 4 : 0) +
                      B * K * 16 + 64;
   if (cudaMallocHost(&h->h_stage, h->h_stage_bytes) != cudaSuccess)
@@ -350,6 +355,8 @@ extern "C" vx_status vx_index_destroy(vx_index* h) {
   if (h->h_hdr) cudaFreeHost(h->h_hdr);
   if (h->h_flags) cudaFreeHost(h->h_flags);
   for (auto& e : h->ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : h->gev)
     if (e) cudaEventDestroy(e);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
@@ -541,11 +548,11 @@ static vx_status local_topk_f32(vx_index* h, const float* d_q, int B, int k, uin
     a.part = h->d_part + (size_t)g0 * grid * kcap;
     a.d_count = d_count;
     a.g0 = g0;
-    if (g0 == 0 && !d_count) CU_TRY(cudaEventRecord(h->ev[0], st));
+    if (g0 == 0 && !d_count) CU_TRY(cudaEventRecord(h->tev[0], st));
     CU_TRY(vx::launch_scan_f32(bucket, &h->tmap_docs, a, grid, smem, st));
     count_launch(h);
   }
-  if (!d_count) CU_TRY(cudaEventRecord(h->ev[1], st));
+  if (!d_count) CU_TRY(cudaEventRecord(h->tev[1], st));
   CU_TRY(vx::launch_merge_topk(h->d_part, B, grid * kcap, k, h->row0, keys, ids, scores, st,
                                d_count));
   count_launch(h);
@@ -569,7 +576,7 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
   const int grid = h->grid;
   const int kp = kprime_of(k);
   const bool bf16 = h->docs16 && h->coarse != VX_COARSE_TF32;
-  CU_TRY(cudaEventRecord(h->ev[0], st));
+  CU_TRY(cudaEventRecord(h->tev[0], st));
   if (bf16) {
     CU_TRY(vx::launch_to_bf16(d_q, h->d_q16, (int64_t)B * D, st));
     count_launch(h);
@@ -611,7 +618,7 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
                               st));
     count_launch(h);
   }
-  CU_TRY(cudaEventRecord(h->ev[1], st));
+  CU_TRY(cudaEventRecord(h->tev[1], st));
   CU_TRY(vx::launch_merge_topk(h->d_part, B, grid * vx::kTcListLen, kp, 0, h->d_ckeys, nullptr,
                                nullptr, st));
   count_launch(h);
@@ -790,20 +797,23 @@ static vx_status stage_graph(vx_index* h, int op, const float* d_q, const float*
   const uint64_t key = ((uint64_t)op << 48) | ((uint64_t)B << 24) | ((uint64_t)k << 12) | (uint64_t)nq;
   auto it = h->graphs.find(key);
   if (it == h->graphs.end()) {
-    CU_TRY(cudaEventRecord(h->ev[2], st));
+    CU_TRY(cudaEventRecord(h->tev[2], st));
     VX_TRY(stage_core(h, op, h->d_q, h->d_qtok, B, nq, k, h->d_out_ids, h->d_out_ip, h->d_out_ms, st));
-    CU_TRY(cudaEventRecord(h->ev[3], st));
+    CU_TRY(cudaEventRecord(h->tev[3], st));
     // capture on the handle's stream (after the eager run completes: capture records, it
     // does not execute)
     CU_TRY(cudaStreamSynchronize(st));
     const uint64_t before = h->st.kernel_launches;
+    h->last_tev = h->ev;  // this call's timing: the eager run
+    h->tev = h->gev;      // the graph records its own events
     CU_TRY(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-    cudaEventRecord(h->ev[2], h->stream);
+    cudaEventRecord(h->tev[2], h->stream);
     vx_status s = stage_core(h, op, h->d_q, h->d_qtok, B, nq, k, h->d_out_ids, h->d_out_ip,
                              h->d_out_ms, h->stream);
-    cudaEventRecord(h->ev[3], h->stream);
+    cudaEventRecord(h->tev[3], h->stream);
     cudaGraph_t g = nullptr;
     cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+    h->tev = h->ev;
     const int launches = (int)(h->st.kernel_launches - before);
     h->st.kernel_launches = before;
     if (s != VX_OK) {
@@ -820,6 +830,7 @@ static vx_status stage_graph(vx_index* h, int op, const float* d_q, const float*
     CU_TRY(cudaGraphLaunch(it->second.exec, st));
     h->st.kernel_launches += it->second.launches;
     h->st.graph_replays += 1;
+    h->last_tev = h->gev;
   }
   const size_t n = (size_t)B * k;
   if (d_ids != h->d_out_ids)
@@ -852,9 +863,10 @@ static vx_status stage_root(vx_index* h, int op, const float* d_q, const float* 
   if (h->use_graphs && h->nranks == 1) {
     VX_TRY(stage_graph(h, op, d_q, d_qtok, B, nq, k, d_ids, d_ip, d_ms, st));
   } else {
-    CU_TRY(cudaEventRecord(h->ev[2], st));
+    CU_TRY(cudaEventRecord(h->tev[2], st));
     VX_TRY(stage_core(h, op, d_q, d_qtok, B, nq, k, d_ids, d_ip, d_ms, st));
-    CU_TRY(cudaEventRecord(h->ev[3], st));
+    CU_TRY(cudaEventRecord(h->tev[3], st));
+    h->last_tev = h->ev;
   }
   h->timing_pending = true;
   h->st.batches += 1;
@@ -896,10 +908,11 @@ extern "C" vx_status vx_sync(vx_index* h) {
   CU_TRY(cudaSetDevice(h->device));
   CU_TRY(cudaStreamSynchronize(h->stream));
   if (h->timing_pending) {
-    CU_TRY(cudaEventSynchronize(h->ev[3]));
+    cudaEvent_t* E = h->last_tev;
+    CU_TRY(cudaEventSynchronize(E[3]));
     float a = 0, b = 0;
-    if (cudaEventElapsedTime(&a, h->ev[0], h->ev[1]) == cudaSuccess &&
-        cudaEventElapsedTime(&b, h->ev[2], h->ev[3]) == cudaSuccess) {
+    if (cudaEventElapsedTime(&a, E[0], E[1]) == cudaSuccess &&
+        cudaEventElapsedTime(&b, E[2], E[3]) == cudaSuccess) {
       h->st.last_scan_ms = a;
       h->st.last_step_ms = b;
       h->st.scan_ms_total += a;
