@@ -221,6 +221,13 @@ struct vx_index {
 
 static void count_launch(vx_index* h, int n = 1) { h->st.kernel_launches += n; }
 
+// Timing events: inside a stream capture they must be EXTERNAL event nodes, or the graph only
+// uses them for internal ordering and never records them for the host to read.
+static cudaError_t record_ev(vx_index* h, cudaEvent_t e, cudaStream_t st) {
+  return cudaEventRecordWithFlags(e, st,
+                                  h->tev == h->gev ? cudaEventRecordExternal : cudaEventRecordDefault);
+}
+
 extern "C" int32_t vx_abi_version(void) { return VX_ABI_VERSION; }
 extern "C" const char* vx_last_error(void) { return g_err.c_str(); }
 
@@ -548,11 +555,11 @@ static vx_status local_topk_f32(vx_index* h, const float* d_q, int B, int k, uin
     a.part = h->d_part + (size_t)g0 * grid * kcap;
     a.d_count = d_count;
     a.g0 = g0;
-    if (g0 == 0 && !d_count) CU_TRY(cudaEventRecord(h->tev[0], st));
+    if (g0 == 0 && !d_count) CU_TRY(record_ev(h, h->tev[0], st));
     CU_TRY(vx::launch_scan_f32(bucket, &h->tmap_docs, a, grid, smem, st));
     count_launch(h);
   }
-  if (!d_count) CU_TRY(cudaEventRecord(h->tev[1], st));
+  if (!d_count) CU_TRY(record_ev(h, h->tev[1], st));
   CU_TRY(vx::launch_merge_topk(h->d_part, B, grid * kcap, k, h->row0, keys, ids, scores, st,
                                d_count));
   count_launch(h);
@@ -576,7 +583,7 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
   const int grid = h->grid;
   const int kp = kprime_of(k);
   const bool bf16 = h->docs16 && h->coarse != VX_COARSE_TF32;
-  CU_TRY(cudaEventRecord(h->tev[0], st));
+  CU_TRY(record_ev(h, h->tev[0], st));
   if (bf16) {
     CU_TRY(vx::launch_to_bf16(d_q, h->d_q16, (int64_t)B * D, st));
     count_launch(h);
@@ -618,7 +625,7 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
                               st));
     count_launch(h);
   }
-  CU_TRY(cudaEventRecord(h->tev[1], st));
+  CU_TRY(record_ev(h, h->tev[1], st));
   CU_TRY(vx::launch_merge_topk(h->d_part, B, grid * vx::kTcListLen, kp, 0, h->d_ckeys, nullptr,
                                nullptr, st));
   count_launch(h);
@@ -797,9 +804,9 @@ static vx_status stage_graph(vx_index* h, int op, const float* d_q, const float*
   const uint64_t key = ((uint64_t)op << 48) | ((uint64_t)B << 24) | ((uint64_t)k << 12) | (uint64_t)nq;
   auto it = h->graphs.find(key);
   if (it == h->graphs.end()) {
-    CU_TRY(cudaEventRecord(h->tev[2], st));
+    CU_TRY(record_ev(h, h->tev[2], st));
     VX_TRY(stage_core(h, op, h->d_q, h->d_qtok, B, nq, k, h->d_out_ids, h->d_out_ip, h->d_out_ms, st));
-    CU_TRY(cudaEventRecord(h->tev[3], st));
+    CU_TRY(record_ev(h, h->tev[3], st));
     // capture on the handle's stream (after the eager run completes: capture records, it
     // does not execute)
     CU_TRY(cudaStreamSynchronize(st));
@@ -807,10 +814,10 @@ static vx_status stage_graph(vx_index* h, int op, const float* d_q, const float*
     h->last_tev = h->ev;  // this call's timing: the eager run
     h->tev = h->gev;      // the graph records its own events
     CU_TRY(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-    cudaEventRecord(h->tev[2], h->stream);
+    record_ev(h, h->tev[2], h->stream);
     vx_status s = stage_core(h, op, h->d_q, h->d_qtok, B, nq, k, h->d_out_ids, h->d_out_ip,
                              h->d_out_ms, h->stream);
-    cudaEventRecord(h->tev[3], h->stream);
+    record_ev(h, h->tev[3], h->stream);
     cudaGraph_t g = nullptr;
     cudaError_t e = cudaStreamEndCapture(h->stream, &g);
     h->tev = h->ev;
@@ -863,9 +870,9 @@ static vx_status stage_root(vx_index* h, int op, const float* d_q, const float* 
   if (h->use_graphs && h->nranks == 1) {
     VX_TRY(stage_graph(h, op, d_q, d_qtok, B, nq, k, d_ids, d_ip, d_ms, st));
   } else {
-    CU_TRY(cudaEventRecord(h->tev[2], st));
+    CU_TRY(record_ev(h, h->tev[2], st));
     VX_TRY(stage_core(h, op, d_q, d_qtok, B, nq, k, d_ids, d_ip, d_ms, st));
-    CU_TRY(cudaEventRecord(h->tev[3], st));
+    CU_TRY(record_ev(h, h->tev[3], st));
     h->last_tev = h->ev;
   }
   h->timing_pending = true;
