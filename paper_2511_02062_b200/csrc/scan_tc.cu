@@ -280,12 +280,20 @@ __global__ void __launch_bounds__(256)
       const uint32_t id = vx_key_id(ck);
       const float4* x = reinterpret_cast<const float4*>(docs + (size_t)id * D);
       float acc = 0.0f;
-      for (int c = 0; c < (D >> 2); ++c) {
-        const float4 xv = __ldg(x + c);
-        acc = fmaf(xv.x, qs[4 * c + 0], acc);
-        acc = fmaf(xv.y, qs[4 * c + 1], acc);
-        acc = fmaf(xv.z, qs[4 * c + 2], acc);
-        acc = fmaf(xv.w, qs[4 * c + 3], acc);
+      // 8 independent 16-byte loads in flight per thread (the gather is latency-bound:
+      // one load at a time made this kernel 5x slower), then the in-order fmaf chain.
+      for (int c0 = 0; c0 < (D >> 2); c0 += 8) {
+        float4 xv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) xv[u] = __ldg(x + c0 + u);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int c = c0 + u;
+          acc = fmaf(xv[u].x, qs[4 * c + 0], acc);
+          acc = fmaf(xv[u].y, qs[4 * c + 1], acc);
+          acc = fmaf(xv[u].z, qs[4 * c + 2], acc);
+          acc = fmaf(xv[u].w, qs[4 * c + 3], acc);
+        }
       }
       ek = vx_make_key(acc, id);
     }
