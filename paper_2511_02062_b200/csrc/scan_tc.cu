@@ -280,20 +280,28 @@ __global__ void __launch_bounds__(256)
       const uint32_t id = vx_key_id(ck);
       const float4* x = reinterpret_cast<const float4*>(docs + (size_t)id * D);
       float acc = 0.0f;
-      // 8 independent 16-byte loads in flight per thread (the gather is latency-bound:
-      // one load at a time made this kernel 5x slower), then the in-order fmaf chain.
-      for (int c0 = 0; c0 < (D >> 2); c0 += 8) {
-        float4 xv[8];
+      // The gather is latency-bound (one 3 KB row per thread, an in-order fmaf chain that
+      // cannot be split): software-pipelined, 8 16-byte loads of the next block are in
+      // flight while the current block's 32 FMAs run.
+      const int nc = D >> 2;  // float4 per row (multiple of 8)
+      float4 cur[8], nxt[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) xv[u] = __ldg(x + c0 + u);
+      for (int u = 0; u < 8; ++u) cur[u] = __ldg(x + u);
+      for (int c0 = 0; c0 < nc; c0 += 8) {
+        if (c0 + 8 < nc) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) nxt[u] = __ldg(x + c0 + 8 + u);
+        }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int c = c0 + u;
-          acc = fmaf(xv[u].x, qs[4 * c + 0], acc);
-          acc = fmaf(xv[u].y, qs[4 * c + 1], acc);
-          acc = fmaf(xv[u].z, qs[4 * c + 2], acc);
-          acc = fmaf(xv[u].w, qs[4 * c + 3], acc);
+          acc = fmaf(cur[u].x, qs[4 * c + 0], acc);
+          acc = fmaf(cur[u].y, qs[4 * c + 1], acc);
+          acc = fmaf(cur[u].z, qs[4 * c + 2], acc);
+          acc = fmaf(cur[u].w, qs[4 * c + 3], acc);
         }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) cur[u] = nxt[u];
       }
       ek = vx_make_key(acc, id);
     }
