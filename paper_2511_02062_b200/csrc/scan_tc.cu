@@ -253,12 +253,14 @@ __global__ void __launch_bounds__(256)
                   int grid, int k, int64_t row0, const float* __restrict__ xnorm_max,
                   float err_coef,
                   uint64_t* __restrict__ out_keys, int64_t* __restrict__ out_ids,
-                  float* __restrict__ out_scores, int* __restrict__ flags) {
-  extern __shared__ float rsm[];
+                  float* __restrict__ out_scores, int* __restrict__ flags, int rows_per_round) {
+  extern __shared__ __align__(16) float rsm[];
   float* qs = rsm;                                             // [D]
-  uint64_t* keys = reinterpret_cast<uint64_t*>(rsm + ((D + 1) & ~1));  // [kp]
+  uint64_t* keys = reinterpret_cast<uint64_t*>(rsm + ((D + 3) & ~3));  // [kp]
+  float* rowbuf = reinterpret_cast<float*>(keys + kp);         // [R][D+4] staged rows
   __shared__ float s_red[32];
   __shared__ int s_fail;
+  __shared__ __align__(8) uint64_t s_bar;
   const int b = blockIdx.x;
   const float* q = qv + (size_t)b * D;
   float ss = 0.0f;
@@ -273,39 +275,46 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   const uint64_t* cb = cand + (size_t)b * kp;
   const uint64_t tprime = cb[kp - 1];  // coarse k'-th key (0: fewer than k' candidates)
-  for (int t = threadIdx.x; t < kp; t += blockDim.x) {
-    const uint64_t ck = cb[t];
-    uint64_t ek = 0ull;
-    if (ck) {
-      const uint32_t id = vx_key_id(ck);
-      const float4* x = reinterpret_cast<const float4*>(docs + (size_t)id * D);
-      float acc = 0.0f;
-      // The gather is latency-bound (one 3 KB row per thread, an in-order fmaf chain that
-      // cannot be split): software-pipelined, 8 16-byte loads of the next block are in
-      // flight while the current block's 32 FMAs run.
-      const int nc = D >> 2;  // float4 per row (multiple of 8)
-      float4 cur[8], nxt[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) cur[u] = __ldg(x + u);
-      for (int c0 = 0; c0 < nc; c0 += 8) {
-        if (c0 + 8 < nc) {
-#pragma unroll
-          for (int u = 0; u < 8; ++u) nxt[u] = __ldg(x + c0 + 8 + u);
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int c = c0 + u;
-          acc = fmaf(cur[u].x, qs[4 * c + 0], acc);
-          acc = fmaf(cur[u].y, qs[4 * c + 1], acc);
-          acc = fmaf(cur[u].z, qs[4 * c + 2], acc);
-          acc = fmaf(cur[u].w, qs[4 * c + 3], acc);
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) cur[u] = nxt[u];
-      }
-      ek = vx_make_key(acc, id);
+  // The candidate rows are random 3 KB gathers from HBM (DRAM-page unfriendly); per-thread
+  // loads left too few bytes in flight (measured 85 us at B=128).  Instead each round stages
+  // R rows into smem with one TMA bulk copy per row (R x 3 KB in flight per SM), then R
+  // threads run the in-order fmaf chains from smem (row stride D+4 floats: the LDS.128 of
+  // 8 consecutive lanes hit distinct banks).
+  const int R = rows_per_round, RS = D + 4;
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar, (uint32_t)R);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  for (int r0 = 0, round = 0; r0 < kp; r0 += R, ++round) {
+    const int t = threadIdx.x;
+    const int idx = r0 + t;
+    uint64_t ck = 0ull;
+    if (t < R) {
+      ck = idx < kp ? cb[idx] : 0ull;
+      const uint32_t bytes = ck ? (uint32_t)D * 4u : 0u;
+      mbar_expect_tx(&s_bar, bytes);  // every staging thread arrives once (count R)
+      if (ck)
+        bulk_load(rowbuf + (size_t)t * RS, docs + (size_t)vx_key_id(ck) * D, bytes, &s_bar);
     }
-    keys[t] = ek;
+    mbar_wait(&s_bar, (uint32_t)(round & 1));
+    if (t < R && idx < kp) {
+      uint64_t ek = 0ull;
+      if (ck) {
+        const float4* x = reinterpret_cast<const float4*>(rowbuf + (size_t)t * RS);
+        float acc = 0.0f;
+        for (int c = 0; c < (D >> 2); ++c) {
+          const float4 xv = x[c];
+          acc = fmaf(xv.x, qs[4 * c + 0], acc);
+          acc = fmaf(xv.y, qs[4 * c + 1], acc);
+          acc = fmaf(xv.z, qs[4 * c + 2], acc);
+          acc = fmaf(xv.w, qs[4 * c + 3], acc);
+        }
+        ek = vx_make_key(acc, vx_key_id(ck));
+      }
+      keys[idx] = ek;
+    }
+    __syncthreads();  // the buffer is reused by the next round's bulk copies
   }
   // certificate 1: no CTA that truncated its list (16 kept) had its 16th key inside the top-k'
   for (int t = threadIdx.x; t < grid; t += blockDim.x) {
@@ -404,12 +413,16 @@ cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64
                           int kp, const uint64_t* part, int grid, int k, int64_t row0,
                           const float* xnorm_max, float err_coef, uint64_t* out_keys,
                           int64_t* out_ids, float* out_scores, int* flags, cudaStream_t st) {
-  size_t smem = (size_t)((D + 1) & ~1) * 4 + (size_t)kp * 8;
+  const size_t base = (size_t)((D + 3) & ~3) * 4 + (size_t)kp * 8;
+  const size_t row = (size_t)(D + 4) * 4;
+  int R = (int)((220 * 1024 - base) / row);
+  R = R > 64 ? 64 : (R < 1 ? 1 : R);
+  const size_t smem = base + (size_t)R * row;
   cudaError_t e = cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
   rerank_kernel<<<B, 256, smem, st>>>(docs, q, D, cand, kp, part, grid, k, row0, xnorm_max,
-                                      err_coef, out_keys, out_ids, out_scores, flags);
+                                      err_coef, out_keys, out_ids, out_scores, flags, R);
   return cudaGetLastError();
 }
 
