@@ -325,6 +325,9 @@ def run_ours(args) -> None:
                      "scan_ms": scan_ms, "traffic": None},
         "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": int(st["kernel_launches"]),
+        "root_phases_ms": ({"broadcast": st["phase_ms"][0], "local_stage": st["phase_ms"][1],
+                            "gather": st["phase_ms"][2], "merge": st["phase_ms"][3]}
+                           if world > 1 else None),
         "clocks": result["clocks"],
     }
     print(json.dumps(out), flush=True)

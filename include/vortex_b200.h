@@ -99,6 +99,8 @@ typedef struct vx_stats {
   double scan_ms_total;       /* sum of scan device times sampled by vx_sync */
   double step_ms_total;       /* sum of stage device times sampled by vx_sync */
   uint64_t timed_batches;     /* batches whose times were sampled (one per vx_sync) */
+  float phase_ms[4];          /* sharded rank 0, last batch: broadcast, local stage,
+                                 gather of the k x G candidates, final merge + order */
 } vx_stats;
 
 int32_t vx_abi_version(void);

@@ -44,7 +44,7 @@ class Stats(C.Structure):
                 ("graph_replays", C.c_uint64), ("cert_fallbacks", C.c_uint64),
                 ("last_scan_ms", C.c_float), ("last_step_ms", C.c_float),
                 ("scan_ms_total", C.c_double), ("step_ms_total", C.c_double),
-                ("timed_batches", C.c_uint64)]
+                ("timed_batches", C.c_uint64), ("phase_ms", C.c_float * 4)]
 
 
 P = C.c_void_p

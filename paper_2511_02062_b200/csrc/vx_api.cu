@@ -209,6 +209,8 @@ struct vx_index {
   cudaEvent_t gev[4] = {};       // the same, recorded by captured graph nodes
   cudaEvent_t* tev = ev;         // events the code being issued records into
   cudaEvent_t* last_tev = ev;    // events of the last issued batch (read by vx_sync)
+  cudaEvent_t pev[5] = {};       // sharded rank 0 phases: start, bcast done, local done,
+  bool phases_pending = false;   //   gather done, end
   bool timing_pending = false;
   // CUDA graphs per (op, B, k, nq)
   struct GraphEntry {
@@ -318,6 +320,8 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
     if (cudaEventCreate(&e) != cudaSuccess) return cleanup(fail(VX_ERR_CUDA, "event create"));
   for (auto& e : h->gev)
     if (cudaEventCreate(&e) != cudaSuccess) return cleanup(fail(VX_ERR_CUDA, "event create"));
+  for (auto& e : h->pev)
+    if (cudaEventCreate(&e) != cudaSuccess) return cleanup(fail(VX_ERR_CUDA, "event create"));
   h->h_stage_bytes = B * D * 4 + (d->tok_per_doc > 0 ? B * d->max_qtok * d->tok_dim * 4 : 0) +
                      B * K * 16 + 64;
   if (cudaMallocHost(&h->h_stage, h->h_stage_bytes) != cudaSuccess)
@@ -364,6 +368,8 @@ extern "C" vx_status vx_index_destroy(vx_index* h) {
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : h->gev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : h->pev)
     if (e) cudaEventDestroy(e);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
@@ -752,6 +758,7 @@ static vx_status stage_core(vx_index* h, int op, const float* d_q, const float* 
                                                      h->d_send);
   count_launch(h);
   CU_TRY(cudaGetLastError());
+  if (h->rank == 0) CU_TRY(cudaEventRecord(h->pev[2], st));
   const size_t bytes = (size_t)n * sizeof(ShardRec);
   NCCL_TRY(nccl().GroupStart());
   if (h->rank == 0) {
@@ -767,6 +774,7 @@ static vx_status stage_core(vx_index* h, int op, const float* d_q, const float* 
   }
   NCCL_TRY(nccl().GroupEnd());
   if (h->rank != 0) return VX_OK;
+  CU_TRY(cudaEventRecord(h->pev[3], st));
   const int G = h->nranks;
   transpose_shard_kernel<<<(G * n + 255) / 256, 256, 0, st>>>(h->d_recv, G, B, k, h->d_part);
   count_launch(h);
@@ -782,6 +790,8 @@ static vx_status stage_core(vx_index* h, int op, const float* d_q, const float* 
     CU_TRY(cudaMemcpyAsync(d_ids, h->d_ids, (size_t)n * 8, cudaMemcpyDeviceToDevice, st));
     CU_TRY(cudaMemcpyAsync(d_ip, h->d_ip, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
   }
+  CU_TRY(cudaEventRecord(h->pev[4], st));
+  h->phases_pending = true;
   return VX_OK;
 }
 
@@ -858,6 +868,7 @@ static vx_status stage_root(vx_index* h, int op, const float* d_q, const float* 
     h->h_hdr[1] = B;
     h->h_hdr[2] = k;
     h->h_hdr[3] = nq;
+    CU_TRY(cudaEventRecord(h->pev[0], st));
     CU_TRY(cudaMemcpyAsync(h->d_hdr, h->h_hdr, 16, cudaMemcpyHostToDevice, st));
     NCCL_TRY(nccl().Broadcast(h->d_hdr, h->d_hdr, 4, ncclInt32, 0, h->comm, st));
     NCCL_TRY(nccl().GroupStart());
@@ -866,6 +877,7 @@ static vx_status stage_root(vx_index* h, int op, const float* d_q, const float* 
       NCCL_TRY(nccl().Broadcast(d_qtok, h->d_qtok, (size_t)B * nq * h->desc.tok_dim, ncclFloat32, 0,
                              h->comm, st));
     NCCL_TRY(nccl().GroupEnd());
+    CU_TRY(cudaEventRecord(h->pev[1], st));
   }
   if (h->use_graphs && h->nranks == 1) {
     VX_TRY(stage_graph(h, op, d_q, d_qtok, B, nq, k, d_ids, d_ip, d_ms, st));
@@ -927,6 +939,14 @@ extern "C" vx_status vx_sync(vx_index* h) {
       h->st.timed_batches += 1;
     }
     h->timing_pending = false;
+    if (h->phases_pending) {
+      for (int i = 0; i < 4; ++i) {
+        float ms = 0;
+        if (cudaEventElapsedTime(&ms, h->pev[i], h->pev[i + 1]) == cudaSuccess)
+          h->st.phase_ms[i] = ms;
+      }
+      h->phases_pending = false;
+    }
     int fc[2] = {0, 0};  // certificate fallbacks counted on device
     CU_TRY(cudaMemcpy(fc, h->d_fcount, 8, cudaMemcpyDeviceToHost));
     h->st.cert_fallbacks = (uint64_t)fc[1];

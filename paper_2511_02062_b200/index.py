@@ -70,7 +70,9 @@ class Index:
     def stats(self) -> dict:
         s = Stats()
         check(self.lib.vx_get_stats(self._h, C.byref(s)))
-        return {f: getattr(s, f) for f, _ in Stats._fields_}
+        out = {f: getattr(s, f) for f, _ in Stats._fields_}
+        out["phase_ms"] = list(s.phase_ms)
+        return out
 
     def reset_stats(self) -> None:
         check(self.lib.vx_reset_stats(self._h))
