@@ -717,7 +717,9 @@ __global__ void transpose_shard_kernel(const ShardRec* recv, int G, int B, int k
   }
 }
 
-// After the global merge: recover each winner's MaxSim from the gathered records.
+// After the global merge: recover each winner's MaxSim from the gathered records.  Every
+// shard's list is sorted by key descending (it is that shard's merged top-k), so a binary
+// search per shard finds the record (keys are unique).
 __global__ void lookup_ms_kernel(const ShardRec* recv, int G, int B, int k, const uint64_t* win,
                                  float* ms_out) {
   int b = blockIdx.x;
@@ -727,8 +729,17 @@ __global__ void lookup_ms_kernel(const ShardRec* recv, int G, int B, int k, cons
     if (key)
       for (int g = 0; g < G; ++g) {
         const ShardRec* r = recv + ((size_t)g * B + b) * k;
-        for (int t = 0; t < k; ++t)
-          if (r[t].key == key) v = r[t].ms;
+        int lo = 0, hi = k - 1;
+        while (lo <= hi) {
+          const int mid = (lo + hi) >> 1;
+          const uint64_t km = r[mid].key;
+          if (km == key) {
+            v = r[mid].ms;
+            break;
+          }
+          if (km > key) lo = mid + 1;
+          else hi = mid - 1;
+        }
       }
     ms_out[(size_t)b * k + j] = v;
   }
