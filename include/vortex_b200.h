@@ -62,7 +62,8 @@ enum {
   VX_OPT_GRAPHS = 3,      /* 1 = replay pre-captured CUDA graphs per batch bucket */
   VX_OPT_MAXSIM = 4,      /* one of VX_MAXSIM_* */
   VX_OPT_COARSE = 5,      /* one of VX_COARSE_*: operand format of the tensor-core scan */
-  VX_OPT_SCAN_TILE = 6    /* documents per tensor-core scan tile: 0 (auto), 128 or 256 */
+  VX_OPT_SCAN_TILE = 6,   /* documents per tensor-core scan tile: 0 (auto), 128 or 256 */
+  VX_OPT_SCAN_PAIRS = 7   /* 1 (default): CTA-pair (cta_group::2) scan for 128 < B <= 256 */
 };
 /* Coarse (candidate-selecting) tensor-core scan format.  Either way every reported score is
  * recomputed exactly in fp32 and certified.  BF16 reads a bf16 shadow

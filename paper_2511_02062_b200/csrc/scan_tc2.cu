@@ -1,0 +1,221 @@
+// scan_tc2.cu — K2 for 128 < B <= 256: the coarse tensor-core scan on CTA PAIRS
+// (tcgen05.mma.cta_group::2, cluster of 2 on one TPC).
+//
+// One pair owns a 256-query x 256-document tile: CTA r stages queries [128r, 128r+128) (A)
+// and documents [256t + 128r, +128) (B) of every K-chunk in ITS smem; the leader issues
+// M=256 x N=256 MMAs that read both CTAs' smem; each CTA's TMEM receives its 128 query rows
+// x all 256 documents.  Compared with one CTA holding both query tiles (scan_tc.cu QT=2):
+// every SM streams half the query bytes per document byte and the accumulators are double
+// buffered (2 x 256 TMEM columns per CTA).
+//
+// Pipeline / synchronisation (CUTLASS-style 2-SM UMMA pipeline, written out):
+//   full[s]   leader-only, count 1: leader producer arrive.expect_tx(both CTAs' bytes); both
+//             CTAs' TMA (.cta_group::2) complete_tx on the leader's barrier.
+//   empty[s]  both CTAs, count 1: leader's tcgen05.commit multicast to both.
+//   tfull[b]  both CTAs, count 1: leader's commit multicast after the tile's last chunk.
+//   tempty[b] leader-only, count 8: the 4 epilogue warps of each CTA arrive (peer: remotely).
+// Epilogue = scan_tc.cu's (thread = query, max-of-32 filter, register-resident 16-list).
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "vx_internal.cuh"
+#include "vx_ptx.cuh"
+
+namespace vx {
+
+constexpr int kP2TD = 256;            // documents per pair tile (MMA N)
+constexpr int kP2KC = 16;             // per-pair list length per query
+constexpr int kP2Unit = 16384;        // 128 rows x 128 B
+constexpr int kP2Stage = 2 * kP2Unit; // per CTA: A (128 queries) + B (its 128 documents)
+constexpr int kP2Threads = 6 * 32;
+constexpr int kP2Cols = 2 * kP2TD;    // two accumulator buffers
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
+    scan_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tx,
+                    const ScanTcArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  const int ns = a.ns;
+  float* scratch_base = reinterpret_cast<float*>(smem + (size_t)ns * kP2Stage);  // [32][128]
+  uint64_t* full = reinterpret_cast<uint64_t*>(scratch_base + 32 * 128);
+  uint64_t* empty = full + ns;
+  uint64_t* tfull = empty + ns;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int cw = a.fmt == 2 ? 32 : 64;
+  const int nch = a.D / cw;
+  const uint32_t n_local = a.n_local;
+  const int ntiles = (int)((n_local + kP2TD - 1) / kP2TD);
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tq);
+    tma_prefetch_desc(&tx);
+    for (int s = 0; s < ns; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 8);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_pair(tmem_slot, kP2Cols);
+  tc_fence_before();
+  cluster_sync();  // barrier inits + TMEM allocation visible pair-wide
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer (both CTAs)
+    if (lane == 0) {
+      const uint64_t pol_x = policy_evict_first();
+      const uint64_t pol_q = policy_evict_last();
+      const uint32_t bytes_pair = 2u * (uint32_t)(128 * 128 + 128 * 128);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int tile = pair; tile < ntiles; tile += npairs) {
+        for (int c = 0; c < nch; ++c) {
+          mbar_wait(&empty[s], ph ^ 1);
+          const uint32_t fb = mapa_shared(smem_u32(&full[s]), 0);
+          if (leader) mbar_expect_tx(&full[s], bytes_pair);
+          uint8_t* st = smem + (size_t)s * kP2Stage;
+          tma_load_2d_pair(st, &tq, fb, c * cw, (int)rank * 128, pol_q);
+          tma_load_2d_pair(st + kP2Unit, &tx, fb, c * cw, tile * kP2TD + (int)rank * 128, pol_x);
+          if (++s == ns) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer (leader, one thread)
+    if (leader && lane == 0) {
+      const uint32_t idesc = make_idesc((uint32_t)a.fmt, 256u, (uint32_t)kP2TD);
+      const uint32_t tf32 = a.fmt == 2 ? 1u : 0u;
+      int s = 0, buf = 0;
+      uint32_t ph = 0, bph = 0;
+      for (int tile = pair; tile < ntiles; tile += npairs) {
+        mbar_wait(&tempty[buf], bph ^ 1);
+        tc_fence_after();
+        for (int c = 0; c < nch; ++c) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t st = smem_u32(smem + (size_t)s * kP2Stage);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            mma_pair(tf32, tmem_base + (uint32_t)(buf * kP2TD), umma_desc_sw128(st + j * 32),
+                     umma_desc_sw128(st + kP2Unit + j * 32), idesc, (c | j) != 0 ? 1u : 0u);
+          mma_commit_pair(&empty[s], 0x3);
+          if (++s == ns) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        mma_commit_pair(&tfull[buf], 0x3);
+        if (++buf == 2) {
+          buf = 0;
+          bph ^= 1;
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue (both CTAs): thread = query
+    const int e = warp - 2;
+    const int quad = warp & 3;
+    const int m = quad * 32 + lane;            // row of this CTA's 128 queries
+    const int q = (int)rank * 128 + m;         // query within the launch
+    float* scratch = scratch_base + (e * 32 + lane);  // [32][128]
+    const uint32_t te_leader = mapa_shared(smem_u32(&tempty[0]), 0);
+    uint64_t L[kP2KC];
+#pragma unroll
+    for (int j = 0; j < kP2KC; ++j) L[j] = 0ull;
+    float thr = -INFINITY;
+    int buf = 0;
+    uint32_t bph = 0;
+    for (int tile = pair; tile < ntiles; tile += npairs) {
+      mbar_wait(&tfull[buf], bph);
+      tc_fence_after();
+      const uint32_t col = tmem_base + (uint32_t)(buf * kP2TD) + ((uint32_t)(quad * 32) << 16);
+#pragma unroll 1
+      for (int cc = 0; cc < kP2TD / 32; ++cc) {
+        uint32_t r[32];
+        tmem_ld32(col + cc * 32, r);
+        tmem_ld_wait();
+        if (q >= a.B || a.dbg_no_select) continue;
+        float mx = __uint_as_float(r[0]);
+#pragma unroll
+        for (int i = 1; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(r[i]));
+        if (mx < thr) continue;
+        uint32_t mask = 0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float sc = __uint_as_float(r[i]);
+          mask |= (sc >= thr ? 1u : 0u) << i;
+          scratch[i * 128] = sc;
+        }
+        // columns [0,128) are the leader's documents, [128,256) the peer's
+        const uint32_t doc0 = (uint32_t)tile * kP2TD + cc * 32;
+        while (mask) {
+          const int i = __ffs(mask) - 1;
+          mask &= mask - 1;
+          const uint32_t doc = doc0 + i;
+          if (doc >= n_local) break;
+          uint64_t key = vx_make_key(scratch[i * 128], doc);
+          if (key <= L[kP2KC - 1]) continue;
+#pragma unroll
+          for (int j = 0; j < kP2KC; ++j) {
+            const uint64_t a0 = L[j];
+            L[j] = a0 > key ? a0 : key;
+            key = a0 > key ? key : a0;
+          }
+          thr = L[kP2KC - 1] == 0ull ? -INFINITY : vx_key_score(L[kP2KC - 1]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(te_leader + (uint32_t)(buf * 8));
+      if (++buf == 2) {
+        buf = 0;
+        bph ^= 1;
+      }
+    }
+    if (q < a.B) {
+      uint64_t* out = a.part + ((size_t)q * npairs + pair) * kP2KC;
+#pragma unroll
+      for (int j = 0; j < kP2KC; ++j) out[j] = L[j];
+    }
+  }
+  tc_fence_before();
+  cluster_sync();  // both CTAs done with TMEM and with each other's barriers
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, kP2Cols);
+  }
+}
+
+size_t scan_tc2_smem(int* ns_out) {
+  const size_t fixed = 32 * 128 * 4 + 16 + 1024;
+  int ns = 6;
+  while (ns > 2 && (size_t)ns * kP2Stage + fixed + (2 * ns + 4) * 8 > 227 * 1024) --ns;
+  *ns_out = ns;
+  return (size_t)ns * kP2Stage + fixed + (size_t)(2 * ns + 4) * 8;
+}
+
+cudaError_t launch_scan_tc2(const CUtensorMap* tq, const CUtensorMap* tx, const ScanTcArgs& a,
+                            int grid, size_t smem, cudaStream_t st) {
+  if (grid < 2 || (grid & 1)) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(scan_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  scan_tc2_kernel<<<grid, kP2Threads, smem, st>>>(*tq, *tx, a);
+  return cudaGetLastError();
+}
+
+}  // namespace vx

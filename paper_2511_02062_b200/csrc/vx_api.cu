@@ -171,6 +171,7 @@ struct vx_index {
   uint16_t* d_q16 = nullptr;     // [maxB][D] bf16 queries for the bf16 coarse scan
   int coarse = VX_COARSE_AUTO;
   int scan_tile = 0;             // documents per tensor-core tile (0 = auto)
+  bool use_pairs = true;         // CTA-pair scan for 128 < B <= 256 (VX_OPT_SCAN_PAIRS)
   // options
   int scan_algo = VX_SCAN_AUTO;
   int maxsim_algo = VX_MAXSIM_AUTO;
@@ -394,6 +395,10 @@ extern "C" vx_status vx_set_option(vx_index* h, int32_t option, int64_t value) {
     case VX_OPT_GRID:
       if (value < 0 || value > h->num_sms) return fail(VX_ERR_INVALID, "grid %lld", (long long)value);
       h->grid = value == 0 ? h->num_sms : (int)value;
+      return VX_OK;
+    case VX_OPT_SCAN_PAIRS:
+      if (value != 0 && value != 1) return fail(VX_ERR_INVALID, "pairs %lld", (long long)value);
+      h->use_pairs = value == 1;
       return VX_OK;
     case VX_OPT_SCAN_TILE:
       if (value != 0 && value != 128 && value != 256)
@@ -627,19 +632,34 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
     }
     if (getenv("VX_DEBUG_TC_NOSELECT")) a.dbg_no_select = 1;
     a.part = h->d_part + (size_t)g0 * grid * vx::kTcListLen;
-    CU_TRY(vx::launch_scan_tc(QT, TD, &tq, bf16 ? &h->tmap_docs16 : &h->tmap_docs, a, grid, smem,
-                              st));
+    if (Bg > 128 && h->use_pairs && grid % 2 == 0) {
+      // 128 < B <= 256: CTA pairs (cta_group::2), one 256x256 tile per pair
+      int ns2 = 0;
+      const size_t smem2 = vx::scan_tc2_smem(&ns2);
+      a.ns = ns2;
+      a.a_rows = 128;
+      CU_TRY(vx::launch_scan_tc2(&tq, bf16 ? &h->tmap_docs16 : &h->tmap_docs, a, grid, smem2, st));
+    } else {
+      CU_TRY(vx::launch_scan_tc(QT, TD, &tq, bf16 ? &h->tmap_docs16 : &h->tmap_docs, a, grid,
+                                smem, st));
+    }
     count_launch(h);
   }
   CU_TRY(record_ev(h, h->tev[1], st));
-  CU_TRY(vx::launch_merge_topk(h->d_part, B, grid * vx::kTcListLen, kp, 0, h->d_ckeys, nullptr,
-                               nullptr, st));
-  count_launch(h);
-  CU_TRY(vx::launch_rerank(h->docs, d_q, D, h->d_ckeys, B, kp, h->d_part, grid, k, h->row0,
-                           reinterpret_cast<const float*>(h->d_xnorm),
-                           bf16 ? vx::kErrCoefBF16 : vx::kErrCoefTF32, keys, ids, scores,
-                           h->d_flags, st));
-  count_launch(h);
+  // per query group: merge its lists (P per query) to the coarse top-k', exact re-rank
+  for (int g0 = 0; g0 < B; g0 += 256) {
+    const int Bg = std::min(256, B - g0);
+    const int P = (Bg > 128 && h->use_pairs && grid % 2 == 0) ? grid / 2 : grid;
+    const uint64_t* part = h->d_part + (size_t)g0 * grid * vx::kTcListLen;
+    uint64_t* ck = h->d_ckeys + (size_t)g0 * kp;
+    CU_TRY(vx::launch_merge_topk(part, Bg, P * vx::kTcListLen, kp, 0, ck, nullptr, nullptr, st));
+    count_launch(h);
+    CU_TRY(vx::launch_rerank(h->docs, d_q + (size_t)g0 * D, D, ck, Bg, kp, part, P, k, h->row0,
+                             reinterpret_cast<const float*>(h->d_xnorm),
+                             bf16 ? vx::kErrCoefBF16 : vx::kErrCoefTF32, keys + (size_t)g0 * k,
+                             ids + (size_t)g0 * k, scores + (size_t)g0 * k, h->d_flags + g0, st));
+    count_launch(h);
+  }
   // certificate failures: re-scan those queries exactly (expected ~never on real data).
   // Entirely on device — compact the flagged queries, exact scan sized by the device count
   // (launches with a zero count exit at once), scatter back — so no host round trip and
