@@ -62,7 +62,7 @@ def parse() -> argparse.Namespace:
                     help="operand format of the tensor-core candidate scan (exact fp32 re-rank either way)")
     ap.add_argument("--tile", type=int, default=0, choices=[0, 128, 256],
                     help="documents per tensor-core scan tile (0 = library default)")
-    ap.add_argument("--pairs", type=int, default=1, choices=[0, 1],
+    ap.add_argument("--pairs", type=int, default=-1, choices=[-1, 0, 1, 2],
                     help="CTA-pair (cta_group::2) scan for 128 < batch <= 256")
     ap.add_argument("--graphs", type=int, default=1, choices=[0, 1],
                     help="replay one captured CUDA graph per batch shape (single GPU)")
@@ -188,8 +188,8 @@ def run_ours(args) -> None:
         idx.set_option(vx.VX_OPT_GRAPHS, 1)
     if args.tile:
         idx.set_option(vx.VX_OPT_SCAN_TILE, args.tile)
-    if not args.pairs:
-        idx.set_option(vx.VX_OPT_SCAN_PAIRS, 0)
+    if args.pairs >= 0:
+        idx.set_option(vx.VX_OPT_SCAN_PAIRS, args.pairs)
     if args.coarse != "auto":
         idx.set_option(vx.VX_OPT_COARSE, {"tf32": vx.VX_COARSE_TF32, "bf16": vx.VX_COARSE_BF16}[args.coarse])
     if args.scan != "auto":

@@ -1,19 +1,22 @@
 // scan_tc2.cu — K2 for 128 < B <= 256: the coarse tensor-core scan on CTA PAIRS
 // (tcgen05.mma.cta_group::2, cluster of 2 on one TPC).
 //
-// One pair owns a 256-query x 256-document tile: CTA r stages queries [128r, 128r+128) (A)
-// and documents [256t + 128r, +128) (B) of every K-chunk in ITS smem; the leader issues
-// M=256 x N=256 MMAs that read both CTAs' smem; each CTA's TMEM receives its 128 query rows
-// x all 256 documents.  Compared with one CTA holding both query tiles (scan_tc.cu QT=2):
-// every SM streams half the query bytes per document byte and the accumulators are double
-// buffered (2 x 256 TMEM columns per CTA).
+// One pair owns a 256-query x (256*H)-document tile.  CTA r stages queries [128r, 128r+128)
+// (A) and, for each half h < H, documents [tile*256H + 256h + 128r, +128) (B rows
+// [128h, 128h+128)) of every K-chunk in ITS smem.  Per k-step the leader issues H MMAs of
+// M=256 x N=256, MMA h reading B rows [128h, +128) of both CTAs -> TMEM columns [256h, +256)
+// = documents [256h, 256h+256) of the tile (contiguous).  Each CTA's TMEM receives its 128
+// query rows.
+//   H = 1: 256-doc tiles, two accumulator buffers (epilogue overlaps the next tile).
+//   H = 2: 512-doc tiles, one buffer; each SM streams its 128 queries once per 256 of its
+//          documents — half the L2->SM query traffic of H = 1 (the limiter at B = 256).
 //
-// Pipeline / synchronisation (CUTLASS-style 2-SM UMMA pipeline, written out):
+// Pipeline / synchronisation (a 2-SM UMMA pipeline, written out):
 //   full[s]   leader-only, count 1: leader producer arrive.expect_tx(both CTAs' bytes); both
 //             CTAs' TMA (.cta_group::2) complete_tx on the leader's barrier.
-//   empty[s]  both CTAs, count 1: leader's tcgen05.commit multicast to both.
-//   tfull[b]  both CTAs, count 1: leader's commit multicast after the tile's last chunk.
-//   tempty[b] leader-only, count 8: the 4 epilogue warps of each CTA arrive (peer: remotely).
+//   empty[s]  both CTAs, count 1: the leader's tcgen05.commit multicast to both.
+//   tfull[b]  both CTAs, count 1: commit multicast after the tile's last chunk.
+//   tempty[b] leader-only, count 8: the 4 epilogue warps of each CTA (the peer remotely).
 // Epilogue = scan_tc.cu's (thread = query, max-of-32 filter, register-resident 16-list).
 #include <cuda_runtime.h>
 #include <math.h>
@@ -23,20 +26,28 @@
 
 namespace vx {
 
-constexpr int kP2TD = 256;            // documents per pair tile (MMA N)
 constexpr int kP2KC = 16;             // per-pair list length per query
 constexpr int kP2Unit = 16384;        // 128 rows x 128 B
-constexpr int kP2Stage = 2 * kP2Unit; // per CTA: A (128 queries) + B (its 128 documents)
 constexpr int kP2Threads = 6 * 32;
-constexpr int kP2Cols = 2 * kP2TD;    // two accumulator buffers
 
+template <int H>
+struct P2Cfg {
+  static constexpr int TD = 256 * H;                 // documents per pair tile
+  static constexpr int kStage = kP2Unit * (1 + H);   // per CTA: A + H B-blocks
+  static constexpr int NBUF = 2 / H;
+  static constexpr int kCols = 512;                  // NBUF * TD
+};
+
+template <int H>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
     scan_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tx,
                     const ScanTcArgs a) {
+  using C = P2Cfg<H>;
+  constexpr int TD = C::TD;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   const int ns = a.ns;
-  float* scratch_base = reinterpret_cast<float*>(smem + (size_t)ns * kP2Stage);  // [32][128]
+  float* scratch_base = reinterpret_cast<float*>(smem + (size_t)ns * C::kStage);  // [32][128]
   uint64_t* full = reinterpret_cast<uint64_t*>(scratch_base + 32 * 128);
   uint64_t* empty = full + ns;
   uint64_t* tfull = empty + ns;
@@ -50,7 +61,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
   const int cw = a.fmt == 2 ? 32 : 64;
   const int nch = a.D / cw;
   const uint32_t n_local = a.n_local;
-  const int ntiles = (int)((n_local + kP2TD - 1) / kP2TD);
+  const int ntiles = (int)((n_local + TD - 1) / TD);
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tq);
@@ -65,7 +76,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc_pair(tmem_slot, kP2Cols);
+  if (warp == 1) tmem_alloc_pair(tmem_slot, C::kCols);
   tc_fence_before();
   cluster_sync();  // barrier inits + TMEM allocation visible pair-wide
   tc_fence_after();
@@ -76,7 +87,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
     if (lane == 0) {
       const uint64_t pol_x = policy_evict_first();
       const uint64_t pol_q = policy_evict_last();
-      const uint32_t bytes_pair = 2u * (uint32_t)(128 * 128 + 128 * 128);
+      const uint32_t bytes_pair = 2u * (uint32_t)C::kStage;
       int s = 0;
       uint32_t ph = 0;
       for (int tile = pair; tile < ntiles; tile += npairs) {
@@ -84,9 +95,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
           mbar_wait(&empty[s], ph ^ 1);
           const uint32_t fb = mapa_shared(smem_u32(&full[s]), 0);
           if (leader) mbar_expect_tx(&full[s], bytes_pair);
-          uint8_t* st = smem + (size_t)s * kP2Stage;
+          uint8_t* st = smem + (size_t)s * C::kStage;
           tma_load_2d_pair(st, &tq, fb, c * cw, (int)rank * 128, pol_q);
-          tma_load_2d_pair(st + kP2Unit, &tx, fb, c * cw, tile * kP2TD + (int)rank * 128, pol_x);
+#pragma unroll
+          for (int h = 0; h < H; ++h)
+            tma_load_2d_pair(st + kP2Unit * (1 + h), &tx, fb, c * cw,
+                             tile * TD + h * 256 + (int)rank * 128, pol_x);
           if (++s == ns) {
             s = 0;
             ph ^= 1;
@@ -97,7 +111,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer (leader, one thread)
     if (leader && lane == 0) {
-      const uint32_t idesc = make_idesc((uint32_t)a.fmt, 256u, (uint32_t)kP2TD);
+      const uint32_t idesc = make_idesc((uint32_t)a.fmt, 256u, 256u);
       const uint32_t tf32 = a.fmt == 2 ? 1u : 0u;
       int s = 0, buf = 0;
       uint32_t ph = 0, bph = 0;
@@ -107,11 +121,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
         for (int c = 0; c < nch; ++c) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
-          const uint32_t st = smem_u32(smem + (size_t)s * kP2Stage);
+          const uint32_t st = smem_u32(smem + (size_t)s * C::kStage);
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            mma_pair(tf32, tmem_base + (uint32_t)(buf * kP2TD), umma_desc_sw128(st + j * 32),
-                     umma_desc_sw128(st + kP2Unit + j * 32), idesc, (c | j) != 0 ? 1u : 0u);
+          for (int h = 0; h < H; ++h)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              mma_pair(tf32, tmem_base + (uint32_t)(buf * TD + h * 256), umma_desc_sw128(st + j * 32),
+                       umma_desc_sw128(st + kP2Unit * (1 + h) + j * 32), idesc,
+                       (c | j) != 0 ? 1u : 0u);
           mma_commit_pair(&empty[s], 0x3);
           if (++s == ns) {
             s = 0;
@@ -119,7 +136,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
           }
         }
         mma_commit_pair(&tfull[buf], 0x3);
-        if (++buf == 2) {
+        if (++buf == C::NBUF) {
           buf = 0;
           bph ^= 1;
         }
@@ -142,9 +159,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
     for (int tile = pair; tile < ntiles; tile += npairs) {
       mbar_wait(&tfull[buf], bph);
       tc_fence_after();
-      const uint32_t col = tmem_base + (uint32_t)(buf * kP2TD) + ((uint32_t)(quad * 32) << 16);
+      const uint32_t col = tmem_base + (uint32_t)(buf * TD) + ((uint32_t)(quad * 32) << 16);
 #pragma unroll 1
-      for (int cc = 0; cc < kP2TD / 32; ++cc) {
+      for (int cc = 0; cc < TD / 32; ++cc) {
         uint32_t r[32];
         tmem_ld32(col + cc * 32, r);
         tmem_ld_wait();
@@ -160,8 +177,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
           mask |= (sc >= thr ? 1u : 0u) << i;
           scratch[i * 128] = sc;
         }
-        // columns [0,128) are the leader's documents, [128,256) the peer's
-        const uint32_t doc0 = (uint32_t)tile * kP2TD + cc * 32;
+        const uint32_t doc0 = (uint32_t)tile * TD + cc * 32;  // columns map to docs 1:1
         while (mask) {
           const int i = __ffs(mask) - 1;
           mask &= mask - 1;
@@ -181,7 +197,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(te_leader + (uint32_t)(buf * 8));
-      if (++buf == 2) {
+      if (++buf == C::NBUF) {
         buf = 0;
         bph ^= 1;
       }
@@ -196,25 +212,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
   cluster_sync();  // both CTAs done with TMEM and with each other's barriers
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc_pair(tmem_base, kP2Cols);
+    tmem_dealloc_pair(tmem_base, C::kCols);
   }
 }
 
-size_t scan_tc2_smem(int* ns_out) {
+size_t scan_tc2_smem(int H, int* ns_out) {
+  const size_t stage = (size_t)kP2Unit * (1 + H);
   const size_t fixed = 32 * 128 * 4 + 16 + 1024;
   int ns = 6;
-  while (ns > 2 && (size_t)ns * kP2Stage + fixed + (2 * ns + 4) * 8 > 227 * 1024) --ns;
+  while (ns > 2 && (size_t)ns * stage + fixed + (2 * ns + 4) * 8 > 227 * 1024) --ns;
   *ns_out = ns;
-  return (size_t)ns * kP2Stage + fixed + (size_t)(2 * ns + 4) * 8;
+  return (size_t)ns * stage + fixed + (size_t)(2 * ns + 4) * 8;
 }
 
-cudaError_t launch_scan_tc2(const CUtensorMap* tq, const CUtensorMap* tx, const ScanTcArgs& a,
-                            int grid, size_t smem, cudaStream_t st) {
+cudaError_t launch_scan_tc2(int H, const CUtensorMap* tq, const CUtensorMap* tx,
+                            const ScanTcArgs& a, int grid, size_t smem, cudaStream_t st) {
   if (grid < 2 || (grid & 1)) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(scan_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  auto kfn = H == 2 ? scan_tc2_kernel<2> : scan_tc2_kernel<1>;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  scan_tc2_kernel<<<grid, kP2Threads, smem, st>>>(*tq, *tx, a);
+  kfn<<<grid, kP2Threads, smem, st>>>(*tq, *tx, a);
   return cudaGetLastError();
 }
 

@@ -171,7 +171,8 @@ struct vx_index {
   uint16_t* d_q16 = nullptr;     // [maxB][D] bf16 queries for the bf16 coarse scan
   int coarse = VX_COARSE_AUTO;
   int scan_tile = 0;             // documents per tensor-core tile (0 = auto)
-  bool use_pairs = true;         // CTA-pair scan for 128 < B <= 256 (VX_OPT_SCAN_PAIRS)
+  int use_pairs = 2;             // CTA-pair scan for 128 < B <= 256: 0 off, 1/2 = 256-doc
+                                 // halves per pair tile (VX_OPT_SCAN_PAIRS)
   // options
   int scan_algo = VX_SCAN_AUTO;
   int maxsim_algo = VX_MAXSIM_AUTO;
@@ -397,8 +398,8 @@ extern "C" vx_status vx_set_option(vx_index* h, int32_t option, int64_t value) {
       h->grid = value == 0 ? h->num_sms : (int)value;
       return VX_OK;
     case VX_OPT_SCAN_PAIRS:
-      if (value != 0 && value != 1) return fail(VX_ERR_INVALID, "pairs %lld", (long long)value);
-      h->use_pairs = value == 1;
+      if (value < 0 || value > 2) return fail(VX_ERR_INVALID, "pairs %lld", (long long)value);
+      h->use_pairs = (int)value;
       return VX_OK;
     case VX_OPT_SCAN_TILE:
       if (value != 0 && value != 128 && value != 256)
@@ -635,10 +636,11 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
     if (Bg > 128 && h->use_pairs && grid % 2 == 0) {
       // 128 < B <= 256: CTA pairs (cta_group::2), one 256x256 tile per pair
       int ns2 = 0;
-      const size_t smem2 = vx::scan_tc2_smem(&ns2);
+      const size_t smem2 = vx::scan_tc2_smem(h->use_pairs, &ns2);
       a.ns = ns2;
       a.a_rows = 128;
-      CU_TRY(vx::launch_scan_tc2(&tq, bf16 ? &h->tmap_docs16 : &h->tmap_docs, a, grid, smem2, st));
+      CU_TRY(vx::launch_scan_tc2(h->use_pairs, &tq, bf16 ? &h->tmap_docs16 : &h->tmap_docs, a,
+                                 grid, smem2, st));
     } else {
       CU_TRY(vx::launch_scan_tc(QT, TD, &tq, bf16 ? &h->tmap_docs16 : &h->tmap_docs, a, grid,
                                 smem, st));

@@ -53,9 +53,10 @@ size_t scan_tc_smem(int QT, int TD, int* ns_out);
 cudaError_t launch_scan_tc(int QT, int TD, const CUtensorMap* tq, const CUtensorMap* tx,
                            const ScanTcArgs& a, int grid, size_t smem, cudaStream_t st);
 // CTA-pair variant for 128 < B <= 256 (scan_tc2.cu); grid must be even; lists per pair.
-size_t scan_tc2_smem(int* ns_out);
-cudaError_t launch_scan_tc2(const CUtensorMap* tq, const CUtensorMap* tx, const ScanTcArgs& a,
-                            int grid, size_t smem, cudaStream_t st);
+// H = 256-document halves per pair tile (1: 256-doc tiles, double-buffered; 2: 512-doc tiles)
+size_t scan_tc2_smem(int H, int* ns_out);
+cudaError_t launch_scan_tc2(int H, const CUtensorMap* tq, const CUtensorMap* tx,
+                            const ScanTcArgs& a, int grid, size_t smem, cudaStream_t st);
 cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64_t* cand, int B,
                           int kp, const uint64_t* part, int grid, int k, int64_t row0,
                           const float* xnorm_max, float err_coef, uint64_t* out_keys,
