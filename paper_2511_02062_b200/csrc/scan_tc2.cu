@@ -28,12 +28,16 @@ namespace vx {
 
 constexpr int kP2KC = 16;             // per-pair list length per query
 constexpr int kP2Unit = 16384;        // 128 rows x 128 B
-constexpr int kP2Threads = 6 * 32;
+constexpr int kP2Threads = 7 * 32;  // B producer, MMA, 4 epilogue warps, A producer
+constexpr int kP2NA = 4;             // query (A) stages: L2-resident, short latency
 
+// Separate rings for A (queries, from L2) and B (documents, from HBM): the document ring
+// gets all the remaining smem, so each SM keeps ~128 KB of HBM reads in flight (a shared
+// ring of A+B stages held half of that and left the pair scan latency-bound).
 template <int H>
 struct P2Cfg {
   static constexpr int TD = 256 * H;                 // documents per pair tile
-  static constexpr int kStage = kP2Unit * (1 + H);   // per CTA: A + H B-blocks
+  static constexpr int kBStage = kP2Unit * H;        // per CTA: H B-blocks
   static constexpr int NBUF = 2 / H;
   static constexpr int kCols = 512;                  // NBUF * TD
 };
@@ -46,11 +50,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
   constexpr int TD = C::TD;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-  const int ns = a.ns;
-  float* scratch_base = reinterpret_cast<float*>(smem + (size_t)ns * C::kStage);  // [32][128]
-  uint64_t* full = reinterpret_cast<uint64_t*>(scratch_base + 32 * 128);
-  uint64_t* empty = full + ns;
-  uint64_t* tfull = empty + ns;
+  const int nb = a.ns;  // document stages
+  uint8_t* ringA = smem;
+  uint8_t* ringB = smem + (size_t)kP2NA * kP2Unit;
+  float* scratch_base = reinterpret_cast<float*>(ringB + (size_t)nb * C::kBStage);  // [32][128]
+  uint64_t* fullA = reinterpret_cast<uint64_t*>(scratch_base + 32 * 128);
+  uint64_t* emptyA = fullA + kP2NA;
+  uint64_t* fullB = emptyA + kP2NA;
+  uint64_t* emptyB = fullB + nb;
+  uint64_t* tfull = emptyB + nb;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -66,9 +74,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tq);
     tma_prefetch_desc(&tx);
-    for (int s = 0; s < ns; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+    for (int i = 0; i < kP2NA; ++i) {
+      mbar_init(&fullA[i], 1);
+      mbar_init(&emptyA[i], 1);
+    }
+    for (int i = 0; i < nb; ++i) {
+      mbar_init(&fullB[i], 1);
+      mbar_init(&emptyB[i], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
@@ -82,26 +94,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0) {
-    // ------------------------------------------------ TMA producer (both CTAs)
+  if (warp == 0 || warp == 6) {
+    // ------------------------------------------------ TMA producers (both CTAs):
+    // warp 0 streams document blocks, warp 6 query blocks, each with its own ring
     if (lane == 0) {
-      const uint64_t pol_x = policy_evict_first();
-      const uint64_t pol_q = policy_evict_last();
-      const uint32_t bytes_pair = 2u * (uint32_t)C::kStage;
+      const bool docs = warp == 0;
+      const uint64_t pol = docs ? policy_evict_first() : policy_evict_last();
+      const int nst = docs ? nb : kP2NA;
+      uint64_t* fullR = docs ? fullB : fullA;
+      uint64_t* emptyR = docs ? emptyB : emptyA;
+      uint8_t* ring = docs ? ringB : ringA;
+      const int sbytes = docs ? C::kBStage : kP2Unit;
+      const uint32_t bytes_pair = 2u * (uint32_t)sbytes;
       int s = 0;
       uint32_t ph = 0;
       for (int tile = pair; tile < ntiles; tile += npairs) {
         for (int c = 0; c < nch; ++c) {
-          mbar_wait(&empty[s], ph ^ 1);
-          const uint32_t fb = mapa_shared(smem_u32(&full[s]), 0);
-          if (leader) mbar_expect_tx(&full[s], bytes_pair);
-          uint8_t* st = smem + (size_t)s * C::kStage;
-          tma_load_2d_pair(st, &tq, fb, c * cw, (int)rank * 128, pol_q);
+          mbar_wait(&emptyR[s], ph ^ 1);
+          const uint32_t fb = mapa_shared(smem_u32(&fullR[s]), 0);
+          if (leader) mbar_expect_tx(&fullR[s], bytes_pair);
+          uint8_t* st = ring + (size_t)s * sbytes;
+          if (docs) {
 #pragma unroll
-          for (int h = 0; h < H; ++h)
-            tma_load_2d_pair(st + kP2Unit * (1 + h), &tx, fb, c * cw,
-                             tile * TD + h * 256 + (int)rank * 128, pol_x);
-          if (++s == ns) {
+            for (int h = 0; h < H; ++h)
+              tma_load_2d_pair(st + kP2Unit * h, &tx, fb, c * cw,
+                               tile * TD + h * 256 + (int)rank * 128, pol);
+          } else {
+            tma_load_2d_pair(st, &tq, fb, c * cw, (int)rank * 128, pol);
+          }
+          if (++s == nst) {
             s = 0;
             ph ^= 1;
           }
@@ -113,26 +134,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
     if (leader && lane == 0) {
       const uint32_t idesc = make_idesc((uint32_t)a.fmt, 256u, 256u);
       const uint32_t tf32 = a.fmt == 2 ? 1u : 0u;
-      int s = 0, buf = 0;
-      uint32_t ph = 0, bph = 0;
+      int sa = 0, sb = 0, buf = 0;
+      uint32_t pa = 0, pb = 0, bph = 0;
       for (int tile = pair; tile < ntiles; tile += npairs) {
         mbar_wait(&tempty[buf], bph ^ 1);
         tc_fence_after();
         for (int c = 0; c < nch; ++c) {
-          mbar_wait(&full[s], ph);
+          mbar_wait(&fullA[sa], pa);
+          mbar_wait(&fullB[sb], pb);
           tc_fence_after();
-          const uint32_t st = smem_u32(smem + (size_t)s * C::kStage);
+          const uint32_t sta = smem_u32(ringA + (size_t)sa * kP2Unit);
+          const uint32_t stb = smem_u32(ringB + (size_t)sb * C::kBStage);
 #pragma unroll
           for (int h = 0; h < H; ++h)
 #pragma unroll
             for (int j = 0; j < 4; ++j)
-              mma_pair(tf32, tmem_base + (uint32_t)(buf * TD + h * 256), umma_desc_sw128(st + j * 32),
-                       umma_desc_sw128(st + kP2Unit * (1 + h) + j * 32), idesc,
-                       (c | j) != 0 ? 1u : 0u);
-          mma_commit_pair(&empty[s], 0x3);
-          if (++s == ns) {
-            s = 0;
-            ph ^= 1;
+              mma_pair(tf32, tmem_base + (uint32_t)(buf * TD + h * 256),
+                       umma_desc_sw128(sta + j * 32), umma_desc_sw128(stb + kP2Unit * h + j * 32),
+                       idesc, (c | j) != 0 ? 1u : 0u);
+          mma_commit_pair(&emptyA[sa], 0x3);
+          mma_commit_pair(&emptyB[sb], 0x3);
+          if (++sa == kP2NA) {
+            sa = 0;
+            pa ^= 1;
+          }
+          if (++sb == nb) {
+            sb = 0;
+            pb ^= 1;
           }
         }
         mma_commit_pair(&tfull[buf], 0x3);
@@ -217,12 +245,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
 }
 
 size_t scan_tc2_smem(int H, int* ns_out) {
-  const size_t stage = (size_t)kP2Unit * (1 + H);
-  const size_t fixed = 32 * 128 * 4 + 16 + 1024;
-  int ns = 6;
-  while (ns > 2 && (size_t)ns * stage + fixed + (2 * ns + 4) * 8 > 227 * 1024) --ns;
-  *ns_out = ns;
-  return (size_t)ns * stage + fixed + (size_t)(2 * ns + 4) * 8;
+  const size_t stage = (size_t)kP2Unit * H;
+  const size_t fixed = (size_t)kP2NA * kP2Unit + 32 * 128 * 4 + (2 * kP2NA + 4) * 8 + 16 + 1024;
+  int nb = 8;
+  while (nb > 2 && (size_t)nb * stage + fixed + 2 * nb * 8 > 227 * 1024) --nb;
+  *ns_out = nb;
+  return (size_t)nb * stage + fixed + (size_t)(2 * nb) * 8;
 }
 
 cudaError_t launch_scan_tc2(int H, const CUtensorMap* tq, const CUtensorMap* tx,

@@ -171,7 +171,7 @@ struct vx_index {
   uint16_t* d_q16 = nullptr;     // [maxB][D] bf16 queries for the bf16 coarse scan
   int coarse = VX_COARSE_AUTO;
   int scan_tile = 0;             // documents per tensor-core tile (0 = auto)
-  int use_pairs = 2;             // CTA-pair scan for 128 < B <= 256: 0 off, 1/2 = 256-doc
+  int use_pairs = 1;             // CTA-pair scan for 128 < B <= 256: 0 off, 1/2 = 256-doc
                                  // halves per pair tile (VX_OPT_SCAN_PAIRS)
   // options
   int scan_algo = VX_SCAN_AUTO;
