@@ -110,6 +110,14 @@ __global__ void __launch_bounds__(kMsThreads, 2)
           ph ^= 1;
         }
       }
+      // producer tail: every async commit-arrive on our barriers has landed before exit
+      for (int i = 0; i < kMsStages; ++i) {
+        mbar_wait(&empty[s], ph ^ 1);
+        if (++s == kMsStages) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
     }
   } else if (warp == 1) {
     if (lane == 0) {

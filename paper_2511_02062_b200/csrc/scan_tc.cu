@@ -107,6 +107,16 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
           }
         }
       }
+      // Producer tail: wait until the MMA's commits have released every stage, so no async
+      // mbarrier arrive can land in this CTA's smem after it exits (it would corrupt the
+      // next kernel resident on the SM).
+      for (int i = 0; i < ns; ++i) {
+        mbar_wait(&empty[s], ph ^ 1);
+        if (++s == ns) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer (one thread)

@@ -128,6 +128,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
           }
         }
       }
+      // Producer tail: the leader's multicast commits to our empty barriers must all have
+      // landed before this CTA exits (a late arrive would hit the next kernel's smem).
+      for (int i = 0; i < nst; ++i) {
+        mbar_wait(&emptyR[s], ph ^ 1);
+        if (++s == nst) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer (leader, one thread)
