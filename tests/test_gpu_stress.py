@@ -19,7 +19,7 @@ def test_alternating_shapes_stay_exact(vxlib, oracle):
     want = {B: oracle.flat_topk(X, Qs[B], k, mode=1)[0] for B in shapes}
     qt = synth.query_tokens(16, nq, 128)
     cand = np.arange(16 * 20, dtype=np.int64).reshape(16, 20) * 997 % N
-    with vx.Index(N, D, tok_per_doc=128, tok_dim=128, tok_blocks=64, max_batch=256, max_k=k,
+    with vx.Index(N, D, tok_per_doc=128, tok_dim=128, tok_blocks=64, max_batch=256, max_k=20,
                   max_qtok=nq) as idx:
         idx.synth(42)
         idx.tokens_synth(45)
