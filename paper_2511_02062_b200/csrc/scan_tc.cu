@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
           uint32_t r[32];
           tmem_ld32(col + cc * 32, r);
           tmem_ld_wait();
-          if (q >= a.B || a.dbg_no_select) continue;
+          if (q >= a.B || (a.dbg_no_select & 1)) continue;
           float mx = __uint_as_float(r[0]);
 #pragma unroll
           for (int i = 1; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(r[i]));

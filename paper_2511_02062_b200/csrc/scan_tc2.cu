@@ -112,9 +112,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
         for (int c = 0; c < nch; ++c) {
           mbar_wait(&emptyR[s], ph ^ 1);
           const uint32_t fb = mapa_shared(smem_u32(&fullR[s]), 0);
-          if (leader) mbar_expect_tx(&fullR[s], bytes_pair);
+          // timing experiments (dbg bits 2/4): after the first pass over the ring, stop
+          // streaming documents / queries and let the MMA reuse the staged data
+          const bool skip = (a.dbg_no_select & (docs ? 2 : 4)) && (tile != pair);
+          if (leader) mbar_expect_tx(&fullR[s], skip ? 0u : bytes_pair);
           uint8_t* st = ring + (size_t)s * sbytes;
-          if (docs) {
+          if (skip) {
+          } else if (docs) {
 #pragma unroll
             for (int h = 0; h < H; ++h)
               tma_load_2d_pair(st + kP2Unit * h, &tx, fb, c * cw,
@@ -202,7 +206,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
         uint32_t r[32];
         tmem_ld32(col + cc * 32, r);
         tmem_ld_wait();
-        if (q >= a.B || a.dbg_no_select) continue;
+        if (q >= a.B || (a.dbg_no_select & 1)) continue;
         float mx = __uint_as_float(r[0]);
 #pragma unroll
         for (int i = 1; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(r[i]));

@@ -631,7 +631,7 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
         a.ns = ns = want;
       }
     }
-    if (getenv("VX_DEBUG_TC_NOSELECT")) a.dbg_no_select = 1;
+    if (const char* e = getenv("VX_DEBUG_TC_NOSELECT")) a.dbg_no_select = atoi(e);  // bit mask
     a.part = h->d_part + (size_t)g0 * grid * vx::kTcListLen;
     if (Bg > 128 && h->use_pairs && grid % 2 == 0) {
       // 128 < B <= 256: CTA pairs (cta_group::2), one 256x256 tile per pair
