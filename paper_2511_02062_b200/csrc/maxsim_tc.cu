@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(kMsThreads, 2)
   float* partial = reinterpret_cast<float*>(tempty + 2);  // [2 bufs][4 quads]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(partial + 8);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = warp_idx_uniform(), lane = threadIdx.x & 31;
   const int b = blockIdx.x / cpq;
   const int c0 = (blockIdx.x % cpq) * chunk;
   const int c1 = min(a.C, c0 + chunk);
@@ -120,34 +120,38 @@ __global__ void __launch_bounds__(kMsThreads, 2)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = make_idesc(1u /*BF16*/, 128u, (uint32_t)ND);
-      int s = 0, buf = 0;
-      uint32_t ph = 0, bph = 0;
-      for (int c = c0; c < c1; ++c) {
-        mbar_wait(&tempty[buf], bph ^ 1);
-        mbar_wait(&full[s], ph);
-        tc_fence_after();
-        const uint32_t aa = smem_u32(sA);
-        const uint32_t bb = smem_u32(sB + (size_t)s * C::kStageBytes);
+    // whole warp walks the pipeline, one elected lane issues (uniform-datapath descriptors)
+    constexpr uint32_t idesc = make_idesc(1u /*BF16*/, 128u, (uint32_t)ND);
+    const uint64_t da = umma_desc_sw128(smem_u32(sA));
+    const uint64_t db0 = umma_desc_sw128(smem_u32(sB));
+    int s = 0, buf = 0;
+    uint32_t ph = 0, bph = 0;
+    for (int c = c0; c < c1; ++c) {
+      mbar_wait(&tempty[buf], bph ^ 1);
+      mbar_wait(&full[s], ph);
+      tc_fence_after();
+      __syncwarp();
+      if (elect_one()) {
+        const uint64_t db = db0 + (uint64_t)(s * (C::kStageBytes >> 4));
 #pragma unroll
         for (int kb = 0; kb < DK; ++kb)
 #pragma unroll
           for (int j = 0; j < 4; ++j)
             mma_f16_ss(tmem_base + (uint32_t)(buf * ND),
-                       umma_desc_sw128(aa + kb * C::kATile + j * 32),
-                       umma_desc_sw128(bb + kb * ND * 128 + j * 32), idesc,
+                       da + (uint64_t)(kb * (C::kATile >> 4) + 2 * j),
+                       db + (uint64_t)(kb * (ND * 128 >> 4) + 2 * j), idesc,
                        (kb | j) != 0 ? 1u : 0u);
         mma_commit(&empty[s]);
         mma_commit(&tfull[buf]);
-        if (++s == kMsStages) {
-          s = 0;
-          ph ^= 1;
-        }
-        if (++buf == 2) {
-          buf = 0;
-          bph ^= 1;
-        }
+      }
+      __syncwarp();
+      if (++s == kMsStages) {
+        s = 0;
+        ph ^= 1;
+      }
+      if (++buf == 2) {
+        buf = 0;
+        bph ^= 1;
       }
     }
   } else {

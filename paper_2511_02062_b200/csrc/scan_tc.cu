@@ -39,7 +39,7 @@ struct TcCfg {
   static constexpr int QPT = QT / EG;                               // query tiles per epilogue thread
 };
 
-template <int QT, int TD>
+template <int QT, int TD, bool TF32>
 __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
     scan_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tx,
                    const ScanTcArgs a) {
@@ -55,9 +55,9 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
   uint64_t* tempty = tfull + C::NBUF;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + C::NBUF);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = warp_idx_uniform(), lane = threadIdx.x & 31;
   // K-chunk = one 128-byte swizzle atom: 32 fp32 (kind::tf32) or 64 bf16 (kind::f16)
-  const int cw = a.fmt == 2 ? 32 : 64;
+  constexpr int cw = TF32 ? 32 : 64;
   const int nch = a.D / cw;
   const uint32_t n_local = a.n_local;
   const int ntiles = (int)((n_local + TD - 1) / TD);
@@ -119,44 +119,45 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer (one thread)
-    if (lane == 0) {
-      const uint32_t idesc = make_idesc((uint32_t)a.fmt /*2 TF32, 1 BF16*/, 128u, (uint32_t)TD);
-      int s = 0;
-      uint32_t ph = 0;
-      int buf = 0;
-      uint32_t bph = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        mbar_wait(&tempty[buf], bph ^ 1);
+    // ------------------------------------------------ MMA issuer (whole warp, one elected
+    // lane issues; loop state warp-uniform -> uniform-datapath descriptors, see scan_tc2.cu)
+    constexpr uint32_t idesc = make_idesc(TF32 ? 2u : 1u, 128u, (uint32_t)TD);
+    const uint64_t d0 = umma_desc_sw128(smem_u32(smem));
+    int s = 0;
+    uint32_t ph = 0;
+    int buf = 0;
+    uint32_t bph = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      mbar_wait(&tempty[buf], bph ^ 1);
+      tc_fence_after();
+      for (int c = 0; c < nch; ++c) {
+        mbar_wait(&full[s], ph);
         tc_fence_after();
-        for (int c = 0; c < nch; ++c) {
-          mbar_wait(&full[s], ph);
-          tc_fence_after();
-          const uint32_t st = smem_u32(smem + (size_t)s * C::kStageBytes);
+        __syncwarp();
+        if (elect_one()) {
+          const uint64_t ds = d0 + (uint64_t)(s * (C::kStageBytes >> 4));  // start addr >> 4
 #pragma unroll
           for (int qt = 0; qt < QT; ++qt) {
             const uint32_t d = tmem_base + (uint32_t)((buf * QT + qt) * TD);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const uint64_t ad = umma_desc_sw128(st + qt * kTcStageUnit + j * 32);
-              const uint64_t bd = umma_desc_sw128(st + QT * kTcStageUnit + j * 32);
-              if (a.fmt == 2)
-                mma_tf32_ss(d, ad, bd, idesc, (c | j) != 0 ? 1u : 0u);
-              else
-                mma_f16_ss(d, ad, bd, idesc, (c | j) != 0 ? 1u : 0u);
-            }
+            for (int j = 0; j < 4; ++j)
+              mma_ss<TF32>(d, ds + (uint64_t)(qt * (kTcStageUnit >> 4) + 2 * j),
+                           ds + (uint64_t)(QT * (kTcStageUnit >> 4) + 2 * j), idesc,
+                           (c | j) != 0 ? 1u : 0u);
           }
           mma_commit(&empty[s]);
-          if (++s == ns) {
-            s = 0;
-            ph ^= 1;
-          }
         }
-        mma_commit(&tfull[buf]);
-        if (++buf == C::NBUF) {
-          buf = 0;
-          bph ^= 1;
+        __syncwarp();
+        if (++s == ns) {
+          s = 0;
+          ph ^= 1;
         }
+      }
+      if (elect_one()) mma_commit(&tfull[buf]);
+      __syncwarp();
+      if (++buf == C::NBUF) {
+        buf = 0;
+        bph ^= 1;
       }
     }
   } else {
@@ -403,7 +404,7 @@ size_t scan_tc_smem(int QT, int TD, int* ns_out) {
 template <int QT, int TD>
 static cudaError_t launch_tc(const CUtensorMap* tq, const CUtensorMap* tx, const ScanTcArgs& a,
                              int grid, size_t smem, cudaStream_t st) {
-  auto kfn = scan_tc_kernel<QT, TD>;
+  auto kfn = a.fmt == 2 ? scan_tc_kernel<QT, TD, true> : scan_tc_kernel<QT, TD, false>;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   kfn<<<grid, TcCfg<QT, TD>::kThreads, smem, st>>>(*tq, *tx, a);

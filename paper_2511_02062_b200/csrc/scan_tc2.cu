@@ -42,7 +42,7 @@ struct P2Cfg {
   static constexpr int kCols = 512;                  // NBUF * TD
 };
 
-template <int H>
+template <int H, bool TF32>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
     scan_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tx,
                     const ScanTcArgs a) {
@@ -62,11 +62,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = warp_idx_uniform(), lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-  const int cw = a.fmt == 2 ? 32 : 64;
+  constexpr int cw = TF32 ? 32 : 64;
   const int nch = a.D / cw;
   const uint32_t n_local = a.n_local;
   const int ntiles = (int)((n_local + TD - 1) / TD);
@@ -97,7 +97,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
   if (warp == 0 || warp == 6) {
     // ------------------------------------------------ TMA producers (both CTAs):
     // warp 0 streams document blocks, warp 6 query blocks, each with its own ring
-    if (lane == 0) {
+    // whole warp walks the ring (warp-uniform state), one elected lane issues the copies
+    {
       const bool docs = warp == 0;
       const uint64_t pol = docs ? policy_evict_first() : policy_evict_last();
       const int nst = docs ? nb : kP2NA;
@@ -106,26 +107,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
       uint8_t* ring = docs ? ringB : ringA;
       const int sbytes = docs ? C::kBStage : kP2Unit;
       const uint32_t bytes_pair = 2u * (uint32_t)sbytes;
+      const uint32_t fb0 = mapa_shared(smem_u32(fullR), 0);  // the leader's full barriers
       int s = 0;
       uint32_t ph = 0;
       for (int tile = pair; tile < ntiles; tile += npairs) {
         for (int c = 0; c < nch; ++c) {
           mbar_wait(&emptyR[s], ph ^ 1);
-          const uint32_t fb = mapa_shared(smem_u32(&fullR[s]), 0);
           // timing experiments (dbg bits 2/4): after the first pass over the ring, stop
           // streaming documents / queries and let the MMA reuse the staged data
           const bool skip = (a.dbg_no_select & (docs ? 2 : 4)) && (tile != pair);
-          if (leader) mbar_expect_tx(&fullR[s], skip ? 0u : bytes_pair);
-          uint8_t* st = ring + (size_t)s * sbytes;
-          if (skip) {
-          } else if (docs) {
+          __syncwarp();
+          if (elect_one()) {
+            const uint32_t fb = fb0 + (uint32_t)(s * 8);
+            if (leader) mbar_expect_tx(&fullR[s], skip ? 0u : bytes_pair);
+            uint8_t* st = ring + (size_t)s * sbytes;
+            if (skip) {
+            } else if (docs) {
 #pragma unroll
-            for (int h = 0; h < H; ++h)
-              tma_load_2d_pair(st + kP2Unit * h, &tx, fb, c * cw,
-                               tile * TD + h * 256 + (int)rank * 128, pol);
-          } else {
-            tma_load_2d_pair(st, &tq, fb, c * cw, (int)rank * 128, pol);
+              for (int h = 0; h < H; ++h)
+                tma_load_2d_pair(st + kP2Unit * h, &tx, fb, c * cw,
+                                 tile * TD + h * 256 + (int)rank * 128, pol);
+            } else {
+              tma_load_2d_pair(st, &tq, fb, c * cw, (int)rank * 128, pol);
+            }
           }
+          __syncwarp();
           if (++s == nst) {
             s = 0;
             ph ^= 1;
@@ -143,10 +149,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer (leader, one thread)
-    if (leader && lane == 0) {
-      const uint32_t idesc = make_idesc((uint32_t)a.fmt, 256u, 256u);
-      const uint32_t tf32 = a.fmt == 2 ? 1u : 0u;
+    // ------------------------------------------------ MMA issuer (leader CTA, whole warp)
+    // The warp walks the pipeline together (all lanes wait on the barriers) and one elected
+    // lane issues: loop state stays warp-uniform, so descriptors live in uniform registers
+    // and each MMA is a single UTCHMMA — a single-thread loop paid R2UR waterfalls per
+    // MMA and could not keep up with a 2-SM M=256 x N=256 MMA (128 cycles each).
+    if (leader) {
+      constexpr uint32_t idesc = make_idesc(TF32 ? 2u : 1u, 256u, 256u);
+      const uint64_t da0 = umma_desc_sw128(smem_u32(ringA));
+      const uint64_t db0 = umma_desc_sw128(smem_u32(ringB));
       int sa = 0, sb = 0, buf = 0;
       uint32_t pa = 0, pb = 0, bph = 0;
       for (int tile = pair; tile < ntiles; tile += npairs) {
@@ -156,17 +167,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
           mbar_wait(&fullA[sa], pa);
           mbar_wait(&fullB[sb], pb);
           tc_fence_after();
-          const uint32_t sta = smem_u32(ringA + (size_t)sa * kP2Unit);
-          const uint32_t stb = smem_u32(ringB + (size_t)sb * C::kBStage);
+          __syncwarp();
+          if (elect_one()) {
+            // descriptor start address is addr >> 4: stage / K-step offsets add directly
+            const uint64_t da = da0 + (uint64_t)(sa * (kP2Unit >> 4));
+            const uint64_t db = db0 + (uint64_t)(sb * (C::kBStage >> 4));
 #pragma unroll
-          for (int h = 0; h < H; ++h)
+            for (int h = 0; h < H; ++h)
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-              mma_pair(tf32, tmem_base + (uint32_t)(buf * TD + h * 256),
-                       umma_desc_sw128(sta + j * 32), umma_desc_sw128(stb + kP2Unit * h + j * 32),
-                       idesc, (c | j) != 0 ? 1u : 0u);
-          mma_commit_pair(&emptyA[sa], 0x3);
-          mma_commit_pair(&emptyB[sb], 0x3);
+              for (int j = 0; j < 4; ++j)
+                mma_pair_k<TF32>(tmem_base + (uint32_t)(buf * TD + h * 256), da + 2 * j,
+                                 db + (uint64_t)(h * (kP2Unit >> 4) + 2 * j), idesc,
+                                 (c | j) != 0 ? 1u : 0u);
+            mma_commit_pair(&emptyA[sa], 0x3);
+            mma_commit_pair(&emptyB[sb], 0x3);
+          }
+          __syncwarp();
           if (++sa == kP2NA) {
             sa = 0;
             pa ^= 1;
@@ -176,7 +192,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
             pb ^= 1;
           }
         }
-        mma_commit_pair(&tfull[buf], 0x3);
+        if (elect_one()) mma_commit_pair(&tfull[buf], 0x3);
+        __syncwarp();
         if (++buf == C::NBUF) {
           buf = 0;
           bph ^= 1;
@@ -269,7 +286,9 @@ size_t scan_tc2_smem(int H, int* ns_out) {
 cudaError_t launch_scan_tc2(int H, const CUtensorMap* tq, const CUtensorMap* tx,
                             const ScanTcArgs& a, int grid, size_t smem, cudaStream_t st) {
   if (grid < 2 || (grid & 1)) return cudaErrorInvalidValue;
-  auto kfn = H == 2 ? scan_tc2_kernel<2> : scan_tc2_kernel<1>;
+  const bool tf32 = a.fmt == 2;
+  auto kfn = H == 2 ? (tf32 ? scan_tc2_kernel<2, true> : scan_tc2_kernel<2, false>)
+                    : (tf32 ? scan_tc2_kernel<1, true> : scan_tc2_kernel<1, false>);
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   kfn<<<grid, kP2Threads, smem, st>>>(*tq, *tx, a);

@@ -248,6 +248,24 @@ VX_DEV void mma_pair(uint32_t kind_tf32, uint32_t d_tmem, uint64_t adesc, uint64
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// Compile-time operand kind (no per-MMA runtime select in the issue loop).
+template <bool TF32>
+VX_DEV void mma_ss(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                   uint32_t accumulate) {
+  if constexpr (TF32)
+    mma_tf32_ss(d_tmem, adesc, bdesc, idesc, accumulate);
+  else
+    mma_f16_ss(d_tmem, adesc, bdesc, idesc, accumulate);
+}
+template <bool TF32>
+VX_DEV void mma_pair_k(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                       uint32_t accumulate) {
+  mma_pair(TF32 ? 1u : 0u, d_tmem, adesc, bdesc, idesc, accumulate);
+}
+// Warp index the compiler can prove warp-uniform (so role branches and the MMA issue loop
+// live on the uniform datapath instead of per-thread registers + R2UR waterfalls).
+VX_DEV int warp_idx_uniform() { return __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0); }
+
 // Commit the leader's MMAs to the mbarrier at the same offset in every CTA of `mask`.
 VX_DEV void mma_commit_pair(uint64_t* bar, uint16_t mask) {
   asm volatile(
