@@ -150,6 +150,17 @@ vx_status vx_search_rescore_dev(vx_index* h, const float* d_queries, const float
 /* Wait for the handle's work; samples the last batch's scan/stage device times. */
 vx_status vx_sync(vx_index* h);
 
+/* Model-load step ("index preload", reference: exec::Executor::load_model,
+ * proj/include/vortex/executor.hpp:129-149, and preload_one, elasticity.hpp:221-232):
+ * with graphs enabled on a single-GPU handle, run and capture the stage graph of every
+ * batch size 1..b_max for (op, k, nq) so that no batch the runtime dispatches later pays a
+ * capture.  op: VX_PREPARE_SEARCH or VX_PREPARE_RESCORE.  Uses the handle's own
+ * input buffers (filled with generator rows).  No-op (VX_OK) without graphs or with
+ * nranks > 1. */
+#define VX_PREPARE_SEARCH 1
+#define VX_PREPARE_RESCORE 2
+vx_status vx_prepare(vx_index* h, int32_t op, int32_t k, int32_t nq, int32_t b_max);
+
 /* ---- Opportunistic, SLO-bounded batcher (reference: Runtime::maybe_dispatch,
  * proj/include/vortex/runtime.hpp:617-654: when the member is idle, dispatch the
  * min(|queue|, cap) oldest queries, never wait to fill).

@@ -22,6 +22,7 @@ VX_MAXSIM_AUTO, VX_MAXSIM_CC, VX_MAXSIM_TC = 0, 1, 2
 VX_OPT_COARSE, VX_OPT_SCAN_TILE, VX_OPT_SCAN_PAIRS = 5, 6, 7
 VX_COARSE_AUTO, VX_COARSE_TF32, VX_COARSE_BF16 = 0, 1, 2
 VX_FLAG_NO_BF16_SHADOW = 1
+VX_PREPARE_SEARCH, VX_PREPARE_RESCORE = 1, 2
 
 
 class VxError(RuntimeError):
@@ -74,6 +75,7 @@ SIGNATURES = {
     "vx_maxsim_dev": [P, P, I32, I32, P, I32, P, P],
     "vx_search_rescore_dev": [P, P, P, I32, I32, I32, P, P, P, P],
     "vx_sync": [P],
+    "vx_prepare": [P, I32, I32, I32, I32],
     "vx_batcher_simulate": [C.POINTER(U64), I64, I32, C.POINTER(I32), C.POINTER(C.c_double), I32,
                             LP, C.POINTER(U64), C.POINTER(U64), C.POINTER(I64)],
     "vx_serve_trace": [P, C.POINTER(U64), I64, I32, FP, FP, I32, I32, LP,

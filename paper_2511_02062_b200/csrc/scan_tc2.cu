@@ -172,6 +172,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
             // descriptor start address is addr >> 4: stage / K-step offsets add directly
             const uint64_t da = da0 + (uint64_t)(sa * (kP2Unit >> 4));
             const uint64_t db = db0 + (uint64_t)(sb * (C::kBStage >> 4));
+            // dbg bit 8 (timing experiments): stream + commit without issuing the MMAs
+            if (!(a.dbg_no_select & 8) || tile == pair)
 #pragma unroll
             for (int h = 0; h < H; ++h)
 #pragma unroll

@@ -955,6 +955,34 @@ extern "C" vx_status vx_maxsim_dev(vx_index* h, const float* d_qtok, int32_t B, 
   return run_maxsim(h, d_qtok, B, nq, d_cand, C, d_out, pick_stream(h, stream));
 }
 
+extern "C" vx_status vx_prepare(vx_index* h, int32_t op, int32_t k, int32_t nq, int32_t b_max) {
+  if (!h) return fail(VX_ERR_INVALID, "null handle");
+  if (op != VX_PREPARE_SEARCH && op != VX_PREPARE_RESCORE) return fail(VX_ERR_INVALID, "op %d", op);
+  VX_TRY(check_batch(h, b_max, k));
+  const bool rescore = op == VX_PREPARE_RESCORE;
+  if (rescore && (!h->tokens || nq < 1 || nq > h->desc.max_qtok))
+    return fail(VX_ERR_INVALID, "rescore needs a token store and 1 <= nq <= max_qtok");
+  if (!h->use_graphs || h->nranks > 1) return VX_OK;
+  CU_TRY(cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  // realistic inputs (generator rows), so every eager run takes the certified fast path
+  CU_TRY(vx::launch_synth_rows(h->d_q, 0x5eedull, 0, b_max, h->desc.dim, st));
+  if (rescore)
+    CU_TRY(vx::launch_synth_rows(h->d_qtok, 0x5eed1ull, 0, (int64_t)b_max * nq, h->desc.tok_dim, st));
+  const vx_stats saved = h->st;
+  for (int B = 1; B <= b_max; ++B) {
+    const uint64_t key = ((uint64_t)(rescore ? OP_RESCORE : OP_SEARCH) << 48) | ((uint64_t)B << 24) |
+                         ((uint64_t)k << 12) | (uint64_t)(rescore ? nq : 0);
+    if (h->graphs.count(key)) continue;
+    VX_TRY(stage_graph(h, rescore ? OP_RESCORE : OP_SEARCH, h->d_q, h->d_qtok, B,
+                       rescore ? nq : 0, k, h->d_out_ids, h->d_out_ip, h->d_out_ms, st));
+  }
+  CU_TRY(cudaStreamSynchronize(st));
+  h->st = saved;  // preload work is not serving work
+  h->timing_pending = false;
+  return VX_OK;
+}
+
 extern "C" vx_status vx_sync(vx_index* h) {
   if (!h) return fail(VX_ERR_INVALID, "null handle");
   CU_TRY(cudaSetDevice(h->device));

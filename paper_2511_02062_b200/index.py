@@ -155,6 +155,12 @@ class Index:
     def sync(self) -> None:
         check(self.lib.vx_sync(self._h))
 
+    def prepare(self, k: int, b_max: int | None = None, nq: int = 0) -> None:
+        """Model load: capture the stage graph of every batch size 1..b_max (nq > 0: the
+        fused search+rescore stage, else search) before serving."""
+        op = _lib.VX_PREPARE_RESCORE if nq else _lib.VX_PREPARE_SEARCH
+        check(self.lib.vx_prepare(self._h, op, k, nq, b_max or self.max_batch))
+
     # -- multi-GPU -----------------------------------------------------------------------------
     @staticmethod
     def comm_unique_id() -> bytes:

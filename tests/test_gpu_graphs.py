@@ -72,3 +72,26 @@ def test_graph_with_certificate_fallback(vx, oracle):
             rid, _ = oracle.flat_topk(X, Q, k, mode=1)
             assert np.array_equal(ids, rid)
         assert idx.stats()["cert_fallbacks"] >= 6
+
+
+def test_prepare_precaptures_every_batch_size(vx, oracle):
+    """vx_prepare (model load): after it, every batch size replays a graph on its first call
+    and the results are the oracle's."""
+    from paper_2511_02062_b200 import synth
+    N, D, k, nq, bmax = 40_000, 256, 10, 8, 12
+    X = oracle.synth_rows(42, 0, N, D)
+    with vx.Index(N, D, tok_per_doc=64, tok_dim=64, tok_blocks=100, max_batch=bmax, max_k=k,
+                  max_qtok=nq) as idx:
+        idx.synth(42)
+        idx.tokens_synth(45)
+        idx.set_option(vx.VX_OPT_GRAPHS, 1)
+        idx.prepare(k, bmax)            # search graphs for B = 1..12
+        idx.prepare(k, bmax, nq=nq)     # fused-stage graphs
+        assert idx.stats()["batches"] == 0  # preload work is not serving work
+        for B in (1, 5, 12):
+            Q = synth.rows(43, 100 * B, B, D)
+            ids, _ = idx.search(Q, k)
+            assert np.array_equal(ids, oracle.flat_topk(X, Q, k, mode=1)[0])
+            idx.search_rescore(Q, synth.query_tokens(B, nq, 64, seed=50 + B), k)
+        st = idx.stats()
+    assert st["graph_replays"] == 6 and st["batches"] == 6
