@@ -521,7 +521,8 @@ def run_ours(args) -> None:
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": int(st["kernel_launches"]),
         "root_phases_ms": ({"broadcast": st["phase_ms"][0], "local_stage": st["phase_ms"][1],
-                            "gather": st["phase_ms"][2], "merge": st["phase_ms"][3]}
+                            "gather_merge": st["phase_ms"][2],
+                            "rescore_phase2": st["phase_ms"][3]}
                            if sharded else None),
         "clocks": result["clocks"],
     }

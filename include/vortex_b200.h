@@ -101,7 +101,8 @@ typedef struct vx_stats {
   double step_ms_total;       /* sum of stage device times sampled by vx_sync */
   uint64_t timed_batches;     /* batches whose times were sampled (one per vx_sync) */
   float phase_ms[4];          /* sharded rank 0, last batch: broadcast, local stage,
-                                 gather of the k x G candidates, final merge + order */
+                                 gather of the k x G keys + global merge, phase 2 (winner
+                                 broadcast, owner MaxSim, max-reduce, order) */
 } vx_stats;
 
 int32_t vx_abi_version(void);

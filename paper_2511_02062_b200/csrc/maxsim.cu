@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(kMsThreads)
   float* best = d_s + Nd * DS;            // [nq]
   float* wm = best + nq;                  // [warps][nq] per-warp running max
   const int64_t id = a.cand[(size_t)b * a.C + c];
-  if (id < 0) {
+  if (id < 0 || id < a.id_lo || id >= a.id_hi) {  // no candidate / another shard's
     if (threadIdx.x == 0) a.out[(size_t)b * a.C + c] = -INFINITY;
     return;
   }

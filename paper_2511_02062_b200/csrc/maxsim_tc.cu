@@ -53,6 +53,12 @@ __global__ void __launch_bounds__(kMsThreads, 2)
   const int c1 = min(a.C, c0 + chunk);
   const int nq = a.nq;
   const int64_t* cand = a.cand + (size_t)b * a.C;
+  // candidates another shard owns (or none, id < 0) are skipped by every role: no loads,
+  // no MMA, the epilogue writes -INF; the ring advances only over owned candidates
+  auto owned = [&](int c) {
+    const int64_t id = cand[c];
+    return id >= 0 && id >= a.id_lo && id < a.id_hi;
+  };
 
   // A tile: query tokens -> bf16 (RNE), SWIZZLE_128B K-major; rows >= nq are zero
   {
@@ -97,8 +103,8 @@ __global__ void __launch_bounds__(kMsThreads, 2)
       int s = 0;
       uint32_t ph = 0;
       for (int c = c0; c < c1; ++c) {
-        const int64_t id = cand[c];
-        const int64_t blk = id < 0 ? 0 : id % a.T;
+        if (!owned(c)) continue;
+        const int64_t blk = cand[c] % a.T;
         mbar_wait(&empty[s], ph ^ 1);
         mbar_expect_tx(&full[s], C::kStageBytes);
 #pragma unroll
@@ -127,6 +133,7 @@ __global__ void __launch_bounds__(kMsThreads, 2)
     int s = 0, buf = 0;
     uint32_t ph = 0, bph = 0;
     for (int c = c0; c < c1; ++c) {
+      if (!owned(c)) continue;
       mbar_wait(&tempty[buf], bph ^ 1);
       mbar_wait(&full[s], ph);
       tc_fence_after();
@@ -160,6 +167,10 @@ __global__ void __launch_bounds__(kMsThreads, 2)
     int buf = 0;
     uint32_t bph = 0;
     for (int c = c0; c < c1; ++c) {
+      if (!owned(c)) {
+        if (warp == 2 && lane == 0) a.out[(size_t)b * a.C + c] = -INFINITY;
+        continue;
+      }
       mbar_wait(&tfull[buf], bph);
       tc_fence_after();
       float mx = -INFINITY;
@@ -185,7 +196,7 @@ __global__ void __launch_bounds__(kMsThreads, 2)
       if (warp == 2 && lane == 0) {
         const float total = partial[buf * 4 + 0] + partial[buf * 4 + 1] + partial[buf * 4 + 2] +
                             partial[buf * 4 + 3];
-        a.out[(size_t)b * a.C + c] = cand[c] < 0 ? -INFINITY : total;
+        a.out[(size_t)b * a.C + c] = total;
       }
       if (++buf == 2) {
         buf = 0;

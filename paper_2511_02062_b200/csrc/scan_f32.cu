@@ -91,12 +91,15 @@ __global__ void __launch_bounds__(kScanThreads, 1)
   const uint32_t n_local = a.n_local;
   const int ntiles = (int)((n_local + TD - 1) / TD);
   // queries in this launch: static, or read on device (exact re-scan of the queries whose
-  // tensor-core certificate failed; the count is only known on the GPU)
-  int nB = a.B;
+  // tensor-core certificate failed; the count is only known on the GPU).  A device-count
+  // launch covers ALL of them in query groups of BQ, looping on the device (one launch
+  // instead of one per group: with no failures it exits at once).
+  int nBtot = a.B;
   if (a.d_count) {
-    nB = min(nB, *a.d_count - a.g0);
-    if (nB <= 0) return;
+    nBtot = min(nBtot, *a.d_count - a.g0);
+    if (nBtot <= 0) return;
   }
+  const int ngroups = (nBtot + BQ - 1) / BQ;
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmap);
@@ -106,14 +109,6 @@ __global__ void __launch_bounds__(kScanThreads, 1)
     }
     fence_barrier_init();
   }
-  for (int i = threadIdx.x; i < BQ * D; i += blockDim.x) {
-    int qi = i / D, t = i - qi * D;
-    q_s[qi * QS + t] = (qi < nB) ? a.q[(size_t)qi * D + t] : 0.0f;
-  }
-  for (int i = threadIdx.x; i < BQ; i += blockDim.x) {
-    thr_s[i] = 0ull;
-    cnt_s[i] = 0;
-  }
   __syncthreads();
 
   if (warp == kComputeWarps) {
@@ -122,28 +117,42 @@ __global__ void __launch_bounds__(kScanThreads, 1)
       const uint64_t pol = policy_evict_first();
       int s = 0;
       uint32_t ph = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        for (int c = 0; c < nch; ++c) {
-          mbar_wait(&empty[s], ph ^ 1);
-          mbar_expect_tx(&full[s], C::kStageBytes);
+      for (int grp = 0; grp < ngroups; ++grp)
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+          for (int c = 0; c < nch; ++c) {
+            mbar_wait(&empty[s], ph ^ 1);
+            mbar_expect_tx(&full[s], C::kStageBytes);
 #pragma unroll
-          for (int h = 0; h < TD; h += 128)
-            tma_load_2d(ring + (size_t)s * C::kStageBytes + h * 128, &tmap, &full[s], c * 32,
-                        tile * TD + h, pol);
-          if (++s == ns) {
-            s = 0;
-            ph ^= 1;
+            for (int h = 0; h < TD; h += 128)
+              tma_load_2d(ring + (size_t)s * C::kStageBytes + h * 128, &tmap, &full[s], c * 32,
+                          tile * TD + h, pol);
+            if (++s == ns) {
+              s = 0;
+              ph ^= 1;
+            }
           }
         }
-      }
     }
     return;
   }
 
   // ---------------- compute warps
+  constexpr int kCT = kComputeWarps * 32;
   const int dl = lane / QL, qlid = lane % QL;
   int s = 0;
   uint32_t ph = 0;
+  for (int grp = 0; grp < ngroups; ++grp) {
+  const int gq = grp * BQ;
+  const int nB = min(BQ, nBtot - gq);
+  for (int i = threadIdx.x; i < BQ * D; i += kCT) {
+    int qi = i / D, t = i - qi * D;
+    q_s[qi * QS + t] = (qi < nB) ? a.q[(size_t)(gq + qi) * D + t] : 0.0f;
+  }
+  for (int i = threadIdx.x; i < BQ; i += kCT) {
+    thr_s[i] = 0ull;
+    cnt_s[i] = 0;
+  }
+  named_bar_sync(1, kCT);
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     float acc[RD][RQ];
 #pragma unroll
@@ -185,14 +194,14 @@ __global__ void __launch_bounds__(kScanThreads, 1)
     }
 
     // scores of this tile -> smem (previous tile's selection must be done)
-    named_bar_sync(1, kComputeWarps * 32);
+    named_bar_sync(1, kCT);
 #pragma unroll
     for (int j = 0; j < RD; ++j) {
       const int r = warp * (DL * RD) + j * DL + dl;
 #pragma unroll
       for (int i = 0; i < RQ; ++i) sc_s[(i * QL + qlid) * TD + r] = acc[j][i];
     }
-    named_bar_sync(1, kComputeWarps * 32);
+    named_bar_sync(1, kCT);
 
     // selection: one warp per query
     for (int qi = warp; qi < nB; qi += kComputeWarps) {
@@ -229,16 +238,18 @@ __global__ void __launch_bounds__(kScanThreads, 1)
     }
   }
 
-  // final per-CTA lists
-  named_bar_sync(1, kComputeWarps * 32);
+  // final per-CTA lists of this query group
+  named_bar_sync(1, kCT);
   for (int qi = warp; qi < nB; qi += kComputeWarps) {
     uint64_t* cb = cand + (size_t)qi * cap;
     const int cnt = cnt_s[qi];
     for (int i = cnt + lane; i < cap; i += 32) cb[i] = 0ull;
     __syncwarp();
     warp_bitonic_desc(cb, cap);
-    uint64_t* out = a.part + ((size_t)qi * gridDim.x + blockIdx.x) * kcap;
+    uint64_t* out = a.part + ((size_t)(gq + qi) * gridDim.x + blockIdx.x) * kcap;
     for (int i = lane; i < kcap; i += 32) out[i] = cb[i];
+  }
+  named_bar_sync(1, kCT);  // the next group reuses q_s / cand / thr / cnt
   }
 }
 

@@ -42,6 +42,8 @@ struct NcclApi {
   ncclResult_t (*CommDestroy)(ncclComm_t);
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
                             cudaStream_t);
+  ncclResult_t (*Reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
+                         cudaStream_t);
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
   ncclResult_t (*GroupStart)();
@@ -64,6 +66,7 @@ static NcclApi& nccl() {
     SYM(CommInitRank, "ncclCommInitRank");
     SYM(CommDestroy, "ncclCommDestroy");
     SYM(Broadcast, "ncclBroadcast");
+    SYM(Reduce, "ncclReduce");
     SYM(Send, "ncclSend");
     SYM(Recv, "ncclRecv");
     SYM(GroupStart, "ncclGroupStart");
@@ -150,11 +153,6 @@ static vx_status make_tmap_2d(CUtensorMap* m, const void* base, CUtensorMapDataT
 }
 
 // ---------------------------------------------------------------- handle
-struct ShardRec {  // one gathered candidate of the shard exchange
-  uint64_t key;    // (ip order bits, ~global id)
-  float ms;
-  float pad;
-};
 
 struct vx_index {
   vx_index_desc desc{};
@@ -188,8 +186,8 @@ struct vx_index {
   int64_t* d_out_ids = nullptr;  // [maxB][maxK]
   float* d_out_ip = nullptr;
   float* d_out_ms = nullptr;
-  ShardRec* d_send = nullptr;    // [maxB][maxK]
-  ShardRec* d_recv = nullptr;    // [G][maxB][maxK]  (rank 0)
+  void* d_send = nullptr;        // [maxB][maxK] x 8 B scratch (rank 0: the reduced MaxSim)
+  void* d_recv = nullptr;        // [G][maxB][maxK] gathered keys (rank 0)
   int32_t* d_hdr = nullptr;      // [4]
   uint64_t* d_ckeys = nullptr;   // [maxB][256] merged coarse keys (TC path)
   int* d_flags = nullptr;        // [maxB] certificate failures (TC path)
@@ -301,9 +299,9 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
   ALLOC(h->d_out_ids, B * K * 8);
   ALLOC(h->d_out_ip, B * K * 4);
   ALLOC(h->d_out_ms, B * K * 4);
-  ALLOC(h->d_send, B * K * sizeof(ShardRec));
+  ALLOC(h->d_send, B * K * 8);
   if (d->n_shards > 1 && d->shard == 0)
-    ALLOC(h->d_recv, (size_t)d->n_shards * B * K * sizeof(ShardRec));
+    ALLOC(h->d_recv, (size_t)d->n_shards * B * K * 8);
   ALLOC(h->d_hdr, 16);
   ALLOC(h->d_ckeys, B * 256 * 8);
   ALLOC(h->d_flags, B * 4);
@@ -550,9 +548,12 @@ static vx_status local_topk_f32(vx_index* h, const float* d_q, int B, int k, uin
   // queries per launch: the largest bucket whose smem plan fits (big k / big D shrink it)
   int gmax = 32, ns0 = 0, cap0 = 0;
   while (gmax > 1 && !vx::scan_f32_smem(gmax, D, kcap, &ns0, &cap0)) gmax >>= 1;
-  for (int g0 = 0; g0 < B; g0 += gmax) {
-    const int Bg = std::min(gmax, B - g0);
-    const int bucket = vx::scan_f32_bucket(Bg);
+  // device-count launch (certificate fallback): ONE launch loops over the query groups on
+  // the device, sized by the count; host-sized batches launch one kernel per group
+  const int step = d_count ? B : gmax;
+  for (int g0 = 0; g0 < B; g0 += step) {
+    const int Bg = std::min(step, B - g0);
+    const int bucket = d_count ? gmax : vx::scan_f32_bucket(Bg);
     int ns = 0, cap = 0;
     size_t smem = vx::scan_f32_smem(bucket, D, kcap, &ns, &cap);
     if (!smem) return fail(VX_ERR_UNSUPPORTED, "scan config (B=%d, D=%d, k=%d) exceeds smem", Bg, D, k);
@@ -689,7 +690,8 @@ static vx_status local_topk(vx_index* h, const float* d_q, int B, int k, uint64_
 }
 
 static vx_status run_maxsim(vx_index* h, const float* d_qtok, int B, int nq, const int64_t* d_cand,
-                            int C, float* d_out, cudaStream_t st) {
+                            int C, float* d_out, cudaStream_t st, int64_t id_lo = 0,
+                            int64_t id_hi = INT64_MAX) {
   if (!h->tokens) return fail(VX_ERR_STATE, "index has no token store");
   if (nq < 1 || nq > h->desc.max_qtok) return fail(VX_ERR_INVALID, "nq %d", nq);
   vx::MaxSimArgs a;
@@ -703,6 +705,8 @@ static vx_status run_maxsim(vx_index* h, const float* d_qtok, int B, int nq, con
   a.Nd = h->desc.tok_per_doc;
   a.d = h->desc.tok_dim;
   a.out = d_out;
+  a.id_lo = id_lo;
+  a.id_hi = id_hi;
   const bool tc = h->maxsim_algo != VX_MAXSIM_CC &&
                   vx::maxsim_tc_supported(nq, a.Nd, a.d);
   if (h->maxsim_algo == VX_MAXSIM_TC && !tc)
@@ -718,66 +722,34 @@ static vx_status run_maxsim(vx_index* h, const float* d_qtok, int B, int nq, con
 // ---------------------------------------------------------------- shard exchange
 enum { OP_STOP = 0, OP_SEARCH = 1, OP_RESCORE = 2 };
 
-__global__ void pack_shard_kernel(const uint64_t* keys, const float* ms, int n, ShardRec* out) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) {
-    ShardRec r;
-    r.key = keys[i];
-    r.ms = ms ? ms[i] : 0.0f;
-    r.pad = 0.0f;
-    out[i] = r;
-  }
-}
-
-// recv [G][B][k] -> keys [B][G*k] (reusing d_part) for the merge
-__global__ void transpose_shard_kernel(const ShardRec* recv, int G, int B, int k, uint64_t* keys) {
+// recv [G][B][k] keys -> [B][G*k] (reusing d_part) for the merge
+__global__ void transpose_shard_kernel(const uint64_t* recv, int G, int B, int k, uint64_t* keys) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   int total = G * B * k;
   if (i < total) {
     int g = i / (B * k), r = i - g * B * k, b = r / k, j = r - b * k;
-    keys[(size_t)b * G * k + g * k + j] = recv[i].key;
+    keys[(size_t)b * G * k + g * k + j] = recv[i];
   }
 }
 
-// After the global merge: recover each winner's MaxSim from the gathered records.  Every
-// shard's list is sorted by key descending (it is that shard's merged top-k), so a binary
-// search per shard finds the record (keys are unique).
-__global__ void lookup_ms_kernel(const ShardRec* recv, int G, int B, int k, const uint64_t* win,
-                                 float* ms_out) {
-  int b = blockIdx.x;
-  for (int j = threadIdx.x; j < k; j += blockDim.x) {
-    uint64_t key = win[(size_t)b * k + j];
-    float v = -INFINITY;
-    if (key)
-      for (int g = 0; g < G; ++g) {
-        const ShardRec* r = recv + ((size_t)g * B + b) * k;
-        int lo = 0, hi = k - 1;
-        while (lo <= hi) {
-          const int mid = (lo + hi) >> 1;
-          const uint64_t km = r[mid].key;
-          if (km == key) {
-            v = r[mid].ms;
-            break;
-          }
-          if (km > key) lo = mid + 1;
-          else hi = mid - 1;
-        }
-      }
-    ms_out[(size_t)b * k + j] = v;
-  }
-}
-
-// Worker and root share this: given queries (and tokens) on device, compute the
-// local candidates and, for G > 1, exchange and merge at rank 0.
+// Worker and root share this: given queries (and tokens) on device, compute the local
+// candidates and, for G > 1, run the two-phase shard exchange:
+//   phase 1: every shard's certified local top-k keys -> rank 0 (grouped send/recv, 8 B per
+//            candidate: a key carries the exact fp32 score and the global id), merge to the
+//            global top-k by inner product;
+//   phase 2 (rescore): rank 0 broadcasts the B x k global winners, each shard computes
+//            MaxSim only for the winners it owns (others -INF, no token loads), and an
+//            NCCL max-reduce to rank 0 assembles the scores.  Every shard does 1/G of the
+//            MaxSim work (rescoring all local top-k would cost each shard the full B x k).
 static vx_status stage_core(vx_index* h, int op, const float* d_q, const float* d_qtok, int B,
                             int nq, int k, int64_t* d_ids, float* d_ip, float* d_ms,
                             cudaStream_t st) {
   const bool rescore = (op == OP_RESCORE);
   VX_TRY(local_topk(h, d_q, B, k, h->d_keys, h->d_ids, h->d_ip, st));
-  if (rescore) VX_TRY(run_maxsim(h, d_qtok, B, nq, h->d_ids, k, h->d_ms, st));
   const int n = B * k;
   if (h->nranks == 1) {
     if (rescore) {
+      VX_TRY(run_maxsim(h, d_qtok, B, nq, h->d_ids, k, h->d_ms, st));
       CU_TRY(vx::launch_order_by(h->d_ms, h->d_ids, h->d_ip, B, k, d_ids, d_ip, d_ms, st));
       count_launch(h);
     } else {
@@ -786,43 +758,50 @@ static vx_status stage_core(vx_index* h, int op, const float* d_q, const float* 
     }
     return VX_OK;
   }
-  // ---- G > 1: gather k x G records to rank 0
-  pack_shard_kernel<<<(n + 255) / 256, 256, 0, st>>>(h->d_keys, rescore ? h->d_ms : nullptr, n,
-                                                     h->d_send);
-  count_launch(h);
-  CU_TRY(cudaGetLastError());
-  if (h->rank == 0) CU_TRY(cudaEventRecord(h->pev[2], st));
-  const size_t bytes = (size_t)n * sizeof(ShardRec);
+  // ---- phase 1: gather the local top-k keys to rank 0, merge
+  const bool root = h->rank == 0;
+  if (root) CU_TRY(cudaEventRecord(h->pev[2], st));
+  const size_t bytes = (size_t)n * 8;
+  uint64_t* recv = reinterpret_cast<uint64_t*>(h->d_recv);
   NCCL_TRY(nccl().GroupStart());
-  if (h->rank == 0) {
+  if (root) {
     for (int r = 0; r < h->nranks; ++r) {
       if (r == 0)
-        CU_TRY(cudaMemcpyAsync(h->d_recv, h->d_send, bytes, cudaMemcpyDeviceToDevice, st));
+        CU_TRY(cudaMemcpyAsync(recv, h->d_keys, bytes, cudaMemcpyDeviceToDevice, st));
       else
-        NCCL_TRY(nccl().Recv(reinterpret_cast<uint8_t*>(h->d_recv) + (size_t)r * bytes, bytes,
-                          ncclUint8, r, h->comm, st));
+        NCCL_TRY(nccl().Recv(recv + (size_t)r * n, bytes, ncclUint8, r, h->comm, st));
     }
   } else {
-    NCCL_TRY(nccl().Send(h->d_send, bytes, ncclUint8, 0, h->comm, st));
+    NCCL_TRY(nccl().Send(h->d_keys, bytes, ncclUint8, 0, h->comm, st));
   }
   NCCL_TRY(nccl().GroupEnd());
-  if (h->rank != 0) return VX_OK;
-  CU_TRY(cudaEventRecord(h->pev[3], st));
-  const int G = h->nranks;
-  transpose_shard_kernel<<<(G * n + 255) / 256, 256, 0, st>>>(h->d_recv, G, B, k, h->d_part);
-  count_launch(h);
-  // keys already carry global ids: id_base 0
-  CU_TRY(vx::launch_merge_topk(h->d_part, B, G * k, k, 0, h->d_keys, h->d_ids, h->d_ip, st));
-  count_launch(h);
-  if (rescore) {
-    lookup_ms_kernel<<<B, 128, 0, st>>>(h->d_recv, G, B, k, h->d_keys, h->d_ms);
+  if (root) {
+    const int G = h->nranks;
+    transpose_shard_kernel<<<(G * n + 255) / 256, 256, 0, st>>>(recv, G, B, k, h->d_part);
     count_launch(h);
-    CU_TRY(vx::launch_order_by(h->d_ms, h->d_ids, h->d_ip, B, k, d_ids, d_ip, d_ms, st));
+    CU_TRY(cudaGetLastError());
+    // keys already carry global ids: id_base 0
+    CU_TRY(vx::launch_merge_topk(h->d_part, B, G * k, k, 0, h->d_keys, h->d_ids, h->d_ip, st));
     count_launch(h);
-  } else {
-    CU_TRY(cudaMemcpyAsync(d_ids, h->d_ids, (size_t)n * 8, cudaMemcpyDeviceToDevice, st));
-    CU_TRY(cudaMemcpyAsync(d_ip, h->d_ip, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+    CU_TRY(cudaEventRecord(h->pev[3], st));
   }
+  if (!rescore) {
+    if (root) {
+      CU_TRY(cudaMemcpyAsync(d_ids, h->d_ids, (size_t)n * 8, cudaMemcpyDeviceToDevice, st));
+      CU_TRY(cudaMemcpyAsync(d_ip, h->d_ip, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+      CU_TRY(cudaEventRecord(h->pev[4], st));
+      h->phases_pending = true;
+    }
+    return VX_OK;
+  }
+  // ---- phase 2: MaxSim of the global winners, each on its owner shard
+  NCCL_TRY(nccl().Broadcast(h->d_ids, h->d_ids, (size_t)n, ncclInt64, 0, h->comm, st));
+  VX_TRY(run_maxsim(h, d_qtok, B, nq, h->d_ids, k, h->d_ms, st, h->row0, h->row0 + h->n_local));
+  float* ms_all = reinterpret_cast<float*>(h->d_send);  // [B][k] on rank 0
+  NCCL_TRY(nccl().Reduce(h->d_ms, ms_all, (size_t)n, ncclFloat32, ncclMax, 0, h->comm, st));
+  if (!root) return VX_OK;
+  CU_TRY(vx::launch_order_by(ms_all, h->d_ids, h->d_ip, B, k, d_ids, d_ip, d_ms, st));
+  count_launch(h);
   CU_TRY(cudaEventRecord(h->pev[4], st));
   h->phases_pending = true;
   return VX_OK;

@@ -97,6 +97,7 @@ struct MaxSimArgs {
   int64_t T;
   int32_t B, nq, C, Nd, d;
   float* out;            // [B][C]
+  int64_t id_lo = 0, id_hi = INT64_MAX;  // ids outside [lo, hi) (another shard's) -> -INF, no loads
 };
 cudaError_t launch_maxsim(const MaxSimArgs& a, cudaStream_t st);
 bool maxsim_tc_supported(int nq, int Nd, int d);

@@ -216,6 +216,28 @@ def test_tc_scan_bit_identical_to_oracle_f32(vx, oracle, N, D, B, k):
         assert fallbacks == 0
 
 
+@pytest.mark.parametrize("B,k", [(40, 100), (70, 20)])
+def test_tc_certificate_fallback_many_queries(vx, oracle, B, k):
+    # most queries fail the certificate: the exact re-scan runs as ONE device-count launch
+    # looping over several query groups on the device
+    N, D = 3000, 128
+    X = oracle.synth_rows(42, 0, N, D)
+    X[:600] = X[0]
+    Q = np.stack([X[0] if i % 7 else oracle.synth_rows(43, i, 1, D)[0] for i in range(B)])
+    with vx.Index(N, D, max_batch=B, max_k=k) as idx:
+        idx.upload(X)
+        idx.set_option(vx.VX_OPT_SCAN, vx.VX_SCAN_TC)
+        for graphs in (0, 1, 1):
+            idx.set_option(vx.VX_OPT_GRAPHS, graphs)
+            ids, sc = idx.search(Q, k)
+            rid, rsc = oracle.flat_topk(X, Q, k, mode=1)
+            assert np.array_equal(ids, rid)
+            v = rid >= 0
+            assert np.array_equal(sc[v], rsc[v].astype(np.float32))
+        st = idx.stats()
+    assert st["cert_fallbacks"] >= B // 2
+
+
 def test_tc_certificate_forces_exact_fallback(vx, oracle):
     # 600 identical rows + noise rows: coarse scores tie massively, the certificate cannot
     # separate the k-th from the candidate boundary -> exact re-scan, still exact results

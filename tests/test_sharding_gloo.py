@@ -3,8 +3,11 @@
 What is tested is the sharded algorithm the stage runs across GPUs (vx_api.cu stage_core):
 contiguous shard ranges [floor(N*g/G), floor(N*(g+1)/G)) (the affinity-group analog of
 kvs.hpp:160-175), a per-shard exact top-k, a gather of k x G candidates to rank 0 and a
-merge on (score desc, id asc).  Exactness: every global top-k member is in its owner's
-local top-k, so rank 0's merge equals the single-index oracle.
+merge on (score desc, id asc) [phase 1]; then rank 0 broadcasts the global winners, each
+shard computes MaxSim only for the winners it owns (-inf elsewhere) and a max-reduce to
+rank 0 assembles the scores [phase 2].  Exactness: every global top-k member is in its
+owner's local top-k, so rank 0's merge equals the single-index oracle, and every winner
+has exactly one owner, so the max-reduce equals the single-index MaxSim.
 """
 from __future__ import annotations
 
@@ -24,6 +27,7 @@ def shard_range(N: int, G: int, g: int) -> tuple[int, int]:
 
 
 def _worker(rank: int, world: int, port: int, q) -> None:
+    import torch
     import torch.distributed as dist
     sys.path.insert(0, str(ROOT / "oracle"))
     import vxoracle as o
@@ -37,16 +41,27 @@ def _worker(rank: int, world: int, port: int, q) -> None:
     ids, sc = o.flat_topk(X, Q, k, mode=1, id_base=r0, threads=2)
     gathered = [None] * world
     dist.all_gather_object(gathered, (ids, sc))
+    merged = np.zeros((B, k), np.int64)
     if rank == 0:
         allid = np.concatenate([g[0] for g in gathered], axis=1)
         allsc = np.concatenate([g[1] for g in gathered], axis=1)
-        merged = np.empty((B, k), np.int64)
         for b in range(B):
             order = np.lexsort((allid[b], -allsc[b]))[:k]
             merged[b] = allid[b][order]
+    # phase 2: broadcast the winners, MaxSim on the owner, max-reduce to rank 0
+    win = torch.from_numpy(merged)
+    dist.broadcast(win, src=0)
+    win = win.numpy()
+    qtok = o.synth_rows(44, 0, B * 4, 32).reshape(B, 4, 32)
+    table = o.synth_tokens(45, 0, 23, 8, 32)
+    owned = np.where((win >= r0) & (win < r0 + n), win, -1)
+    ms = torch.from_numpy(o.maxsim(qtok, owned, table, mode=1))
+    dist.reduce(ms, dst=0, op=dist.ReduceOp.MAX)
+    if rank == 0:
         Xf = o.synth_rows(42, 0, N, D)
         want, _ = o.flat_topk(Xf, Q, k, mode=1, threads=2)
-        q.put(bool(np.array_equal(merged, want)))
+        want_ms = o.maxsim(qtok, want, table, mode=1)
+        q.put(bool(np.array_equal(merged, want)) and bool(np.array_equal(ms.numpy(), want_ms)))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -63,7 +78,7 @@ def test_shard_ranges_partition():
             assert max(s[1] for s in spans) - min(s[1] for s in spans) <= 1
 
 
-def test_two_rank_gloo_gather_merge_equals_global(oracle):
+def test_two_rank_gloo_two_phase_exchange_equals_global(oracle):
     import multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
