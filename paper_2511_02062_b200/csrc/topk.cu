@@ -15,7 +15,7 @@
 
 namespace vx {
 
-constexpr int kMergeThreads = 512;
+constexpr int kMergeThreads = 256;
 constexpr int kMaxK = 256;
 
 __device__ __forceinline__ void block_bitonic_desc(uint64_t* buf, int n) {
@@ -46,27 +46,71 @@ __global__ void __launch_bounds__(kMergeThreads)
   __shared__ int s_kk, s_done, s_above, s_eq;
   __shared__ uint64_t sel[kMaxK];
   const uint64_t* L = in + (size_t)blockIdx.x * M;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
   uint64_t prefix = 0, mask = 0;
   int kk = k;
   for (int shift = 56; shift >= 0; shift -= 8) {
     for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
     __syncthreads();
-    for (int i = threadIdx.x; i < M; i += blockDim.x) {
-      uint64_t key = L[i];
-      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+    // histogram of the next digit over the keys still matching the prefix; lanes with the
+    // same digit aggregate first (top digits are shared by most keys: one atomic per warp)
+    for (int i0 = 0; i0 < M; i0 += blockDim.x) {
+      const int i = i0 + (int)threadIdx.x;
+      const uint64_t key = i < M ? L[i] : 0ull;
+      const bool live = i < M && (key & mask) == prefix;
+      const unsigned act = __ballot_sync(0xffffffffu, live);
+      if (live) {
+        const uint32_t dg = (uint32_t)(key >> shift) & 255u;
+        const unsigned same = __match_any_sync(act, dg);
+        if (lane == __ffs(same) - 1) atomicAdd(&hist[dg], (uint32_t)__popc(same));
+      }
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      int above = 0, d = 255;
-      for (; d > 0; --d) {
-        if (above + (int)hist[d] >= kk) break;
-        above += hist[d];
+    if (warp == 0) {
+      // bins from the top: lane l owns digits 255-8l .. 248-8l; find the digit d holding
+      // the kk-th key (descending) with a suffix scan over the lanes
+      uint32_t c[8];
+      uint32_t tot = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        c[j] = hist[255 - 8 * lane - j];
+        tot += c[j];
       }
-      s_prefix = prefix | ((uint64_t)d << shift);
-      s_mask = mask | (0xFFull << shift);
-      s_kk = kk - above;
-      s_done = ((int)hist[d] == kk - above);
+      uint32_t incl = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const uint32_t excl = incl - tot;  // keys in higher digits than this lane's
+      const bool mine = excl < (uint32_t)kk && incl >= (uint32_t)kk;
+      const unsigned who = __ballot_sync(0xffffffffu, mine);
+      if (who == 0) {
+        // fewer than kk keys match at all: every one of them is selected; digit 0 (lane 31,
+        // j = 7) becomes the "equal" bin, the other digits count as above it
+        if (lane == 31) {
+          s_prefix = prefix;
+          s_mask = mask | (0xFFull << shift);
+          s_kk = kk - (int)(incl - c[7]);
+          s_done = 1;
+        }
+      } else if (lane == __ffs(who) - 1) {
+        uint32_t above = excl;
+        int d = 255 - 8 * lane;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (above + c[j] >= (uint32_t)kk) {
+            d = 255 - 8 * lane - j;
+            s_kk = kk - (int)above;
+            s_done = (c[j] == (uint32_t)kk - above);
+            break;
+          }
+          above += c[j];
+        }
+        s_prefix = prefix | ((uint64_t)d << shift);
+        s_mask = mask | (0xFFull << shift);
+      }
     }
     __syncthreads();
     prefix = s_prefix;
@@ -188,25 +232,49 @@ namespace vx {
 
 // ---- device-side handling of tensor-core certificate failures (no host round trip, so the
 // whole stage can live in one CUDA graph)
-__global__ void cert_compact_kernel(const int* __restrict__ flags, int B,
-                                    const float* __restrict__ q, int D, int* __restrict__ fidx,
-                                    int* __restrict__ fcount, float* __restrict__ fq) {
-  __shared__ int s_idx[1024];
-  __shared__ int s_n;
+__global__ void __launch_bounds__(1024)
+    cert_compact_kernel(const int* __restrict__ flags, int B, const float* __restrict__ q, int D,
+                        int* __restrict__ fidx, int* __restrict__ fcount, float* __restrict__ fq) {
+  // stream compaction of the flagged queries (ascending order), 1024 flags per round:
+  // warp ballots + a prefix over the 32 warp counts
+  __shared__ int s_warp[32];
+  __shared__ int s_base;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_base = 0;
+  __syncthreads();
+  for (int b0 = 0; b0 < B; b0 += 1024) {
+    const int b = b0 + (int)threadIdx.x;
+    const bool f = b < B && flags[b] != 0;
+    const unsigned m = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) s_warp[warp] = __popc(m);
+    __syncthreads();
+    if (warp == 0) {
+      const int c = s_warp[lane];
+      int x = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      s_warp[lane] = x - c;  // exclusive prefix
+    }
+    __syncthreads();
+    const int base = s_base;
+    if (f) fidx[base + s_warp[warp] + __popc(m & ((1u << lane) - 1u))] = b;
+    __syncthreads();
+    if (threadIdx.x == 1023) s_base = base + s_warp[31] + __popc(m);
+    __syncthreads();
+  }
+  const int n = s_base;
   if (threadIdx.x == 0) {
-    int n = 0;
-    for (int b = 0; b < B; ++b)
-      if (flags[b]) s_idx[n++] = b;  // ascending query order
-    s_n = n;
     fcount[0] = n;   // this batch
     fcount[1] += n;  // running total (vx_stats.cert_fallbacks)
   }
+  __threadfence_block();
   __syncthreads();
-  const int n = s_n;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) fidx[i] = s_idx[i];
   for (int i = threadIdx.x; i < n * D; i += blockDim.x) {
     const int r = i / D;
-    fq[i] = q[(size_t)s_idx[r] * D + (i - r * D)];
+    fq[i] = q[(size_t)fidx[r] * D + (i - r * D)];
   }
 }
 
@@ -227,8 +295,7 @@ __global__ void cert_scatter_kernel(const int* __restrict__ fidx, const int* __r
 
 cudaError_t launch_cert_compact(const int* flags, int B, const float* q, int D, int* fidx,
                                 int* fcount, float* fq, cudaStream_t st) {
-  if (B > 1024) return cudaErrorInvalidValue;
-  cert_compact_kernel<<<1, 512, 0, st>>>(flags, B, q, D, fidx, fcount, fq);
+  cert_compact_kernel<<<1, 1024, 0, st>>>(flags, B, q, D, fidx, fcount, fq);
   return cudaGetLastError();
 }
 
