@@ -127,7 +127,7 @@ def parse() -> argparse.Namespace:
     ap.add_argument("--tile", type=int, default=0, choices=[0, 128, 256],
                     help="documents per tensor-core scan tile (0 = library default)")
     ap.add_argument("--pairs", type=int, default=-1, choices=[-1, 0, 1, 2],
-                    help="CTA-pair (cta_group::2) scan for 128 < batch <= 256")
+                    help="CTA-pair (cta_group::2) scan for batch > 128 (2: 512 queries per pass)")
     ap.add_argument("--graphs", type=int, default=1, choices=[0, 1],
                     help="replay one captured CUDA graph per batch shape (single GPU)")
     ap.add_argument("--trace-s", type=float, default=0.5,

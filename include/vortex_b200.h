@@ -63,7 +63,9 @@ enum {
   VX_OPT_MAXSIM = 4,      /* one of VX_MAXSIM_* */
   VX_OPT_COARSE = 5,      /* one of VX_COARSE_*: operand format of the tensor-core scan */
   VX_OPT_SCAN_TILE = 6,   /* documents per tensor-core scan tile: 0 (auto), 128 or 256 */
-  VX_OPT_SCAN_PAIRS = 7   /* 1 (default): CTA-pair (cta_group::2) scan for 128 < B <= 256 */
+  VX_OPT_SCAN_PAIRS = 7   /* 1 (default): CTA-pair (cta_group::2) scan for B > 128, 256 queries
+                             per pass over the index; 2: 512 queries per pass (two accumulator
+                             groups, one TMEM buffer); 0: single-CTA kernels */
 };
 /* Coarse (candidate-selecting) tensor-core scan format.  Either way every reported score is
  * recomputed exactly in fp32 and certified.  BF16 reads a bf16 shadow

@@ -1,23 +1,27 @@
-// scan_tc2.cu — K2 for 128 < B <= 256: the coarse tensor-core scan on CTA PAIRS
-// (tcgen05.mma.cta_group::2, cluster of 2 on one TPC).
+// scan_tc2.cu — K2 for B > 128: the coarse tensor-core scan on CTA PAIRS
+// (tcgen05.mma.cta_group::2, cluster of 2 on one TPC), 256 x QG queries per pass.
 //
-// One pair owns a 256-query x (256*H)-document tile.  CTA r stages queries [128r, 128r+128)
-// (A) and, for each half h < H, documents [tile*256H + 256h + 128r, +128) (B rows
-// [128h, 128h+128)) of every K-chunk in ITS smem.  Per k-step the leader issues H MMAs of
-// M=256 x N=256, MMA h reading B rows [128h, +128) of both CTAs -> TMEM columns [256h, +256)
-// = documents [256h, 256h+256) of the tile (contiguous).  Each CTA's TMEM receives its 128
-// query rows.
-//   H = 1: 256-doc tiles, two accumulator buffers (epilogue overlaps the next tile).
-//   H = 2: 512-doc tiles, one buffer; each SM streams its 128 queries once per 256 of its
-//          documents — half the L2->SM query traffic of H = 1 (the limiter at B = 256).
+// One pair owns a 256-document tile and QG query groups of 256.  CTA r stages, per K-chunk,
+// the 128 query rows [256g + 128r, +128) of every group g (A) and documents
+// [tile*256 + 128r, +128) (B) in ITS smem.  Per k-step the leader issues QG MMAs of
+// M=256 x N=256 — MMA g reads group g's A rows of both CTAs and the B rows of both CTAs —
+// into TMEM columns [(buf*QG + g)*256, +256) = documents of the tile (contiguous).  Each
+// CTA's TMEM receives its 128 query rows.
+//   QG = 1 (128 < B <= 256): two accumulator buffers, the epilogue overlaps the next tile.
+//   QG = 2 (256 < B <= 512): the 512 TMEM columns hold one buffer for both groups; every
+//          document byte read from HBM feeds 512 queries (half the HBM traffic per query of
+//          QG = 1, which at B = 256 already shares the pass with the tensor-pipe limit).
 //
 // Pipeline / synchronisation (a 2-SM UMMA pipeline, written out):
 //   full[s]   leader-only, count 1: leader producer arrive.expect_tx(both CTAs' bytes); both
 //             CTAs' TMA (.cta_group::2) complete_tx on the leader's barrier.
 //   empty[s]  both CTAs, count 1: the leader's tcgen05.commit multicast to both.
 //   tfull[b]  both CTAs, count 1: commit multicast after the tile's last chunk.
-//   tempty[b] leader-only, count 8: the 4 epilogue warps of each CTA (the peer remotely).
-// Epilogue = scan_tc.cu's (thread = query, max-of-32 filter, register-resident 16-list).
+//   tempty[b] leader-only, count 2 x 4QG: every epilogue warp of both CTAs (the peer remotely).
+// Warps: 0 document producer, 1 MMA issuer (+ TMEM allocator), 2 query producer,
+//        3 .. 3+4QG-1 epilogue (group g = warps 3+4g .. 6+4g; warp w reads TMEM lanes
+//        32*(w%4) .. +31).  Epilogue = scan_tc.cu's (thread = query, max-of-32 filter,
+//        register-resident 16-list).
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -28,35 +32,44 @@ namespace vx {
 
 constexpr int kP2KC = 16;             // per-pair list length per query
 constexpr int kP2Unit = 16384;        // 128 rows x 128 B
-constexpr int kP2Threads = 7 * 32;  // B producer, MMA, 4 epilogue warps, A producer
-constexpr int kP2NA = 4;             // query (A) stages: L2-resident, short latency
+constexpr int kP2SmemLimit = 227 * 1024;
 
-// Separate rings for A (queries, from L2) and B (documents, from HBM): the document ring
-// gets all the remaining smem, so each SM keeps ~128 KB of HBM reads in flight (a shared
-// ring of A+B stages held half of that and left the pair scan latency-bound).
-template <int H>
+template <int QG>
 struct P2Cfg {
-  static constexpr int TD = 256 * H;                 // documents per pair tile
-  static constexpr int kBStage = kP2Unit * H;        // per CTA: H B-blocks
-  static constexpr int NBUF = 2 / H;
-  static constexpr int kCols = 512;                  // NBUF * TD
+  static constexpr int TD = 256;                         // documents per pair tile
+  static constexpr int NBUF = 2 / QG;                    // accumulator buffers (512 columns)
+  static constexpr int kCols = 512;
+  static constexpr int kEpiWarps = 4 * QG;
+  static constexpr int kThreads = (3 + kEpiWarps) * 32;
+  static constexpr int kAStage = QG * kP2Unit;           // per CTA: QG query blocks
+  static constexpr int kNA = QG == 1 ? 4 : 3;            // query stages (L2-resident: short)
+  static constexpr int kScratch = kEpiWarps * 32 * 32 * 4;
 };
 
-template <int H, bool TF32>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
+// Separate rings for A (queries, from L2) and B (documents, from HBM): the document ring
+// gets the remaining smem, so each SM keeps ~100-128 KB of HBM reads in flight.
+template <int QG>
+static size_t p2_smem(int nb) {
+  using C = P2Cfg<QG>;
+  return (size_t)C::kNA * C::kAStage + (size_t)nb * kP2Unit + C::kScratch +
+         (size_t)(2 * C::kNA + 2 * nb + 4) * 8 + 16 + 1024;
+}
+
+template <int QG, bool TF32>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P2Cfg<QG>::kThreads, 1)
     scan_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tx,
                     const ScanTcArgs a) {
-  using C = P2Cfg<H>;
-  constexpr int TD = C::TD;
+  using C = P2Cfg<QG>;
+  constexpr int TD = C::TD, NA = C::kNA;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   const int nb = a.ns;  // document stages
   uint8_t* ringA = smem;
-  uint8_t* ringB = smem + (size_t)kP2NA * kP2Unit;
-  float* scratch_base = reinterpret_cast<float*>(ringB + (size_t)nb * C::kBStage);  // [32][128]
-  uint64_t* fullA = reinterpret_cast<uint64_t*>(scratch_base + 32 * 128);
-  uint64_t* emptyA = fullA + kP2NA;
-  uint64_t* fullB = emptyA + kP2NA;
+  uint8_t* ringB = smem + (size_t)NA * C::kAStage;
+  float* scratch_base = reinterpret_cast<float*>(ringB + (size_t)nb * kP2Unit);  // [32][32*EW]
+  uint64_t* fullA = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(scratch_base) + C::kScratch);
+  uint64_t* emptyA = fullA + NA;
+  uint64_t* fullB = emptyA + NA;
   uint64_t* emptyB = fullB + nb;
   uint64_t* tfull = emptyB + nb;
   uint64_t* tempty = tfull + 2;
@@ -74,7 +87,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tq);
     tma_prefetch_desc(&tx);
-    for (int i = 0; i < kP2NA; ++i) {
+    for (int i = 0; i < NA; ++i) {
       mbar_init(&fullA[i], 1);
       mbar_init(&emptyA[i], 1);
     }
@@ -84,7 +97,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 8);
+      mbar_init(&tempty[b], 2 * C::kEpiWarps);
     }
     fence_barrier_init();
   }
@@ -94,58 +107,55 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0 || warp == 6) {
+  if (warp == 0 || warp == 2) {
     // ------------------------------------------------ TMA producers (both CTAs):
-    // warp 0 streams document blocks, warp 6 query blocks, each with its own ring
+    // warp 0 streams document blocks, warp 2 query blocks, each with its own ring; the
     // whole warp walks the ring (warp-uniform state), one elected lane issues the copies
-    {
-      const bool docs = warp == 0;
-      const uint64_t pol = docs ? policy_evict_first() : policy_evict_last();
-      const int nst = docs ? nb : kP2NA;
-      uint64_t* fullR = docs ? fullB : fullA;
-      uint64_t* emptyR = docs ? emptyB : emptyA;
-      uint8_t* ring = docs ? ringB : ringA;
-      const int sbytes = docs ? C::kBStage : kP2Unit;
-      const uint32_t bytes_pair = 2u * (uint32_t)sbytes;
-      const uint32_t fb0 = mapa_shared(smem_u32(fullR), 0);  // the leader's full barriers
-      int s = 0;
-      uint32_t ph = 0;
-      for (int tile = pair; tile < ntiles; tile += npairs) {
-        for (int c = 0; c < nch; ++c) {
-          mbar_wait(&emptyR[s], ph ^ 1);
-          // timing experiments (dbg bits 2/4): after the first pass over the ring, stop
-          // streaming documents / queries and let the MMA reuse the staged data
-          const bool skip = (a.dbg_no_select & (docs ? 2 : 4)) && (tile != pair);
-          __syncwarp();
-          if (elect_one()) {
-            const uint32_t fb = fb0 + (uint32_t)(s * 8);
-            if (leader) mbar_expect_tx(&fullR[s], skip ? 0u : bytes_pair);
-            uint8_t* st = ring + (size_t)s * sbytes;
-            if (skip) {
-            } else if (docs) {
+    const bool docs = warp == 0;
+    const uint64_t pol = docs ? policy_evict_first() : policy_evict_last();
+    const int nst = docs ? nb : NA;
+    uint64_t* fullR = docs ? fullB : fullA;
+    uint64_t* emptyR = docs ? emptyB : emptyA;
+    uint8_t* ring = docs ? ringB : ringA;
+    const int sbytes = docs ? kP2Unit : C::kAStage;
+    const uint32_t bytes_pair = 2u * (uint32_t)sbytes;
+    const uint32_t fb0 = mapa_shared(smem_u32(fullR), 0);  // the leader's full barriers
+    int s = 0;
+    uint32_t ph = 0;
+    for (int tile = pair; tile < ntiles; tile += npairs) {
+      for (int c = 0; c < nch; ++c) {
+        mbar_wait(&emptyR[s], ph ^ 1);
+        // timing experiments (dbg bits 2/4): after the first pass over the ring, stop
+        // streaming documents / queries and let the MMA reuse the staged data
+        const bool skip = (a.dbg_no_select & (docs ? 2 : 4)) && (tile != pair);
+        __syncwarp();
+        if (elect_one()) {
+          const uint32_t fb = fb0 + (uint32_t)(s * 8);
+          if (leader) mbar_expect_tx(&fullR[s], skip ? 0u : bytes_pair);
+          uint8_t* st = ring + (size_t)s * sbytes;
+          if (skip) {
+          } else if (docs) {
+            tma_load_2d_pair(st, &tx, fb, c * cw, tile * TD + (int)rank * 128, pol);
+          } else {
 #pragma unroll
-              for (int h = 0; h < H; ++h)
-                tma_load_2d_pair(st + kP2Unit * h, &tx, fb, c * cw,
-                                 tile * TD + h * 256 + (int)rank * 128, pol);
-            } else {
-              tma_load_2d_pair(st, &tq, fb, c * cw, (int)rank * 128, pol);
-            }
-          }
-          __syncwarp();
-          if (++s == nst) {
-            s = 0;
-            ph ^= 1;
+            for (int g = 0; g < QG; ++g)
+              tma_load_2d_pair(st + g * kP2Unit, &tq, fb, c * cw, g * 256 + (int)rank * 128, pol);
           }
         }
-      }
-      // Producer tail: the leader's multicast commits to our empty barriers must all have
-      // landed before this CTA exits (a late arrive would hit the next kernel's smem).
-      for (int i = 0; i < nst; ++i) {
-        mbar_wait(&emptyR[s], ph ^ 1);
+        __syncwarp();
         if (++s == nst) {
           s = 0;
           ph ^= 1;
         }
+      }
+    }
+    // Producer tail: the leader's multicast commits to our empty barriers must all have
+    // landed before this CTA exits (a late arrive would hit the next kernel's smem).
+    for (int i = 0; i < nst; ++i) {
+      mbar_wait(&emptyR[s], ph ^ 1);
+      if (++s == nst) {
+        s = 0;
+        ph ^= 1;
       }
     }
   } else if (warp == 1) {
@@ -169,23 +179,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
           tc_fence_after();
           __syncwarp();
           if (elect_one()) {
-            // descriptor start address is addr >> 4: stage / K-step offsets add directly
-            const uint64_t da = da0 + (uint64_t)(sa * (kP2Unit >> 4));
-            const uint64_t db = db0 + (uint64_t)(sb * (C::kBStage >> 4));
+            // descriptor start address is addr >> 4: stage / group / K-step offsets add
+            const uint64_t da = da0 + (uint64_t)(sa * (C::kAStage >> 4));
+            const uint64_t db = db0 + (uint64_t)(sb * (kP2Unit >> 4));
             // dbg bit 8 (timing experiments): stream + commit without issuing the MMAs
             if (!(a.dbg_no_select & 8) || tile == pair)
 #pragma unroll
-            for (int h = 0; h < H; ++h)
-#pragma unroll
               for (int j = 0; j < 4; ++j)
-                mma_pair_k<TF32>(tmem_base + (uint32_t)(buf * TD + h * 256), da + 2 * j,
-                                 db + (uint64_t)(h * (kP2Unit >> 4) + 2 * j), idesc,
-                                 (c | j) != 0 ? 1u : 0u);
+#pragma unroll
+                for (int g = 0; g < QG; ++g)
+                  mma_pair_k<TF32>(tmem_base + (uint32_t)((buf * QG + g) * TD),
+                                   da + (uint64_t)(g * (kP2Unit >> 4) + 2 * j), db + 2 * j, idesc,
+                                   (c | j) != 0 ? 1u : 0u);
             mma_commit_pair(&emptyA[sa], 0x3);
             mma_commit_pair(&emptyB[sb], 0x3);
           }
           __syncwarp();
-          if (++sa == kP2NA) {
+          if (++sa == NA) {
             sa = 0;
             pa ^= 1;
           }
@@ -204,11 +214,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
     }
   } else {
     // ------------------------------------------------ epilogue (both CTAs): thread = query
-    const int e = warp - 2;
-    const int quad = warp & 3;
-    const int m = quad * 32 + lane;            // row of this CTA's 128 queries
-    const int q = (int)rank * 128 + m;         // query within the launch
-    float* scratch = scratch_base + (e * 32 + lane);  // [32][128]
+    const int e = warp - 3;                    // 0 .. 4QG-1
+    const int g = e >> 2;                      // query group
+    const int quad = warp & 3;                 // TMEM lane quadrant this warp may access
+    const int m = quad * 32 + lane;            // row of this CTA's 128 queries of group g
+    const int q = g * 256 + (int)rank * 128 + m;  // query within the launch
+    float* scratch = scratch_base + (e * 32 + lane);  // [32][32*EW]
+    constexpr int SS = C::kEpiWarps * 32;             // scratch row stride
     const uint32_t te_leader = mapa_shared(smem_u32(&tempty[0]), 0);
     uint64_t L[kP2KC];
 #pragma unroll
@@ -219,7 +231,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
     for (int tile = pair; tile < ntiles; tile += npairs) {
       mbar_wait(&tfull[buf], bph);
       tc_fence_after();
-      const uint32_t col = tmem_base + (uint32_t)(buf * TD) + ((uint32_t)(quad * 32) << 16);
+      const uint32_t col = tmem_base + (uint32_t)((buf * QG + g) * TD) + ((uint32_t)(quad * 32) << 16);
 #pragma unroll 1
       for (int cc = 0; cc < TD / 32; ++cc) {
         uint32_t r[32];
@@ -235,7 +247,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
         for (int i = 0; i < 32; ++i) {
           const float sc = __uint_as_float(r[i]);
           mask |= (sc >= thr ? 1u : 0u) << i;
-          scratch[i * 128] = sc;
+          scratch[i * SS] = sc;
         }
         const uint32_t doc0 = (uint32_t)tile * TD + cc * 32;  // columns map to docs 1:1
         while (mask) {
@@ -243,7 +255,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
           mask &= mask - 1;
           const uint32_t doc = doc0 + i;
           if (doc >= n_local) break;
-          uint64_t key = vx_make_key(scratch[i * 128], doc);
+          uint64_t key = vx_make_key(scratch[i * SS], doc);
           if (key <= L[kP2KC - 1]) continue;
 #pragma unroll
           for (int j = 0; j < kP2KC; ++j) {
@@ -276,24 +288,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
   }
 }
 
-size_t scan_tc2_smem(int H, int* ns_out) {
-  const size_t stage = (size_t)kP2Unit * H;
-  const size_t fixed = (size_t)kP2NA * kP2Unit + 32 * 128 * 4 + (2 * kP2NA + 4) * 8 + 16 + 1024;
+size_t scan_tc2_smem(int QG, int* ns_out) {
   int nb = 8;
-  while (nb > 2 && (size_t)nb * stage + fixed + 2 * nb * 8 > 227 * 1024) --nb;
+  auto sz = [&](int n) { return QG == 2 ? p2_smem<2>(n) : p2_smem<1>(n); };
+  while (nb > 2 && sz(nb) > (size_t)kP2SmemLimit) --nb;
   *ns_out = nb;
-  return (size_t)nb * stage + fixed + (size_t)(2 * nb) * 8;
+  return sz(nb);
 }
 
-cudaError_t launch_scan_tc2(int H, const CUtensorMap* tq, const CUtensorMap* tx,
+cudaError_t launch_scan_tc2(int QG, const CUtensorMap* tq, const CUtensorMap* tx,
                             const ScanTcArgs& a, int grid, size_t smem, cudaStream_t st) {
-  if (grid < 2 || (grid & 1)) return cudaErrorInvalidValue;
+  if (grid < 2 || (grid & 1) || (QG != 1 && QG != 2)) return cudaErrorInvalidValue;
   const bool tf32 = a.fmt == 2;
-  auto kfn = H == 2 ? (tf32 ? scan_tc2_kernel<2, true> : scan_tc2_kernel<2, false>)
-                    : (tf32 ? scan_tc2_kernel<1, true> : scan_tc2_kernel<1, false>);
+  auto kfn = QG == 2 ? (tf32 ? scan_tc2_kernel<2, true> : scan_tc2_kernel<2, false>)
+                     : (tf32 ? scan_tc2_kernel<1, true> : scan_tc2_kernel<1, false>);
+  const int threads = QG == 2 ? P2Cfg<2>::kThreads : P2Cfg<1>::kThreads;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kfn<<<grid, kP2Threads, smem, st>>>(*tq, *tx, a);
+  kfn<<<grid, threads, smem, st>>>(*tq, *tx, a);
   return cudaGetLastError();
 }
 

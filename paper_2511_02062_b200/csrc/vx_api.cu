@@ -169,8 +169,8 @@ struct vx_index {
   uint16_t* d_q16 = nullptr;     // [maxB][D] bf16 queries for the bf16 coarse scan
   int coarse = VX_COARSE_AUTO;
   int scan_tile = 0;             // documents per tensor-core tile (0 = auto)
-  int use_pairs = 1;             // CTA-pair scan for 128 < B <= 256: 0 off, 1/2 = 256-doc
-                                 // halves per pair tile (VX_OPT_SCAN_PAIRS)
+  int use_pairs = 1;             // CTA-pair scan for B > 128: 0 off, 1 on, 2 on + 512-query
+                                 // passes (VX_OPT_SCAN_PAIRS)
   // options
   int scan_algo = VX_SCAN_AUTO;
   int maxsim_algo = VX_MAXSIM_AUTO;
@@ -601,10 +601,17 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
     CU_TRY(vx::launch_to_bf16(d_q, h->d_q16, (int64_t)B * D, st));
     count_launch(h);
   }
-  for (int g0 = 0; g0 < B; g0 += 256) {
-    const int Bg = std::min(256, B - g0);
+  // queries per pass over the index: 256 (CTA pairs, or the single-CTA kernel's QT = 2 x
+  // 128); VX_OPT_SCAN_PAIRS = 2 feeds 512 queries per pass on CTA pairs (QG = 2: a single
+  // TMEM buffer for both groups, so the epilogue no longer overlaps the MMA — measured
+  // slower than two QG = 1 passes at 10M x 768, profiles/r01/README.md)
+  const bool pairs = h->use_pairs && grid % 2 == 0;
+  const int GS = (pairs && h->use_pairs == 2) ? 512 : 256;
+  for (int g0 = 0; g0 < B; g0 += GS) {
+    const int Bg = std::min(GS, B - g0);
+    const bool on_pairs = pairs && Bg > 128;
     const int QT = Bg <= 128 ? 1 : 2;
-    const int a_rows = QT == 1 ? ((Bg + 7) & ~7) : 128;
+    const int a_rows = on_pairs ? 128 : (QT == 1 ? ((Bg + 7) & ~7) : 128);
     CUtensorMap tq;
     if (bf16)
       VX_TRY(make_tmap_2d(&tq, h->d_q16 + (size_t)g0 * D, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
@@ -612,37 +619,37 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
     else
       VX_TRY(make_tmap_2d(&tq, d_q + (size_t)g0 * D, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
                           (uint64_t)Bg, D, 32, (uint32_t)a_rows));
-    int ns = 0;
-    // 256-document tiles halve the per-document query re-streaming from L2 (measured: B=128
-    // bf16 2.31 ms vs 3.78 ms with 128; B=256 3.9 ms vs 4.36 ms) — profiles/r01/
-    const int TD = h->scan_tile ? h->scan_tile : 256;
-    size_t smem = vx::scan_tc_smem(QT, TD, &ns);
     vx::ScanTcArgs a;
     a.n_local = (uint32_t)h->n_local;
     a.D = D;
     a.B = Bg;
-    a.ns = ns;
     a.a_rows = a_rows;
     a.fmt = bf16 ? 1 : 2;
     a.dbg_no_select = 0;
-    if (const char* e = getenv("VX_DEBUG_TC_STAGES")) {  // timing experiments only
-      const int want = atoi(e);
-      if (want >= 2 && want < ns) {
-        smem -= (size_t)(ns - want) * (QT * 16384 + TD * 128 + 16);
-        a.ns = ns = want;
-      }
-    }
     if (const char* e = getenv("VX_DEBUG_TC_NOSELECT")) a.dbg_no_select = atoi(e);  // bit mask
     a.part = h->d_part + (size_t)g0 * grid * vx::kTcListLen;
-    if (Bg > 128 && h->use_pairs && grid % 2 == 0) {
-      // 128 < B <= 256: CTA pairs (cta_group::2), one 256x256 tile per pair
+    if (on_pairs) {
+      // 128 < B: CTA pairs (cta_group::2), 256 documents x 256 QG queries per pair tile
+      const int QG = Bg > 256 ? 2 : 1;
       int ns2 = 0;
-      const size_t smem2 = vx::scan_tc2_smem(h->use_pairs, &ns2);
+      const size_t smem2 = vx::scan_tc2_smem(QG, &ns2);
       a.ns = ns2;
-      a.a_rows = 128;
-      CU_TRY(vx::launch_scan_tc2(h->use_pairs, &tq, bf16 ? &h->tmap_docs16 : &h->tmap_docs, a,
-                                 grid, smem2, st));
+      CU_TRY(vx::launch_scan_tc2(QG, &tq, bf16 ? &h->tmap_docs16 : &h->tmap_docs, a, grid,
+                                 smem2, st));
     } else {
+      // 256-document tiles halve the per-document query re-streaming from L2 (measured: B=128
+      // bf16 2.31 ms vs 3.78 ms with 128; B=256 3.9 ms vs 4.36 ms) — profiles/r01/
+      const int TD = h->scan_tile ? h->scan_tile : 256;
+      int ns = 0;
+      size_t smem = vx::scan_tc_smem(QT, TD, &ns);
+      if (const char* e = getenv("VX_DEBUG_TC_STAGES")) {  // timing experiments only
+        const int want = atoi(e);
+        if (want >= 2 && want < ns) {
+          smem -= (size_t)(ns - want) * (QT * 16384 + TD * 128 + 16);
+          ns = want;
+        }
+      }
+      a.ns = ns;
       CU_TRY(vx::launch_scan_tc(QT, TD, &tq, bf16 ? &h->tmap_docs16 : &h->tmap_docs, a, grid,
                                 smem, st));
     }
@@ -650,9 +657,9 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
   }
   CU_TRY(record_ev(h, h->tev[1], st));
   // per query group: merge its lists (P per query) to the coarse top-k', exact re-rank
-  for (int g0 = 0; g0 < B; g0 += 256) {
-    const int Bg = std::min(256, B - g0);
-    const int P = (Bg > 128 && h->use_pairs && grid % 2 == 0) ? grid / 2 : grid;
+  for (int g0 = 0; g0 < B; g0 += GS) {
+    const int Bg = std::min(GS, B - g0);
+    const int P = (pairs && Bg > 128) ? grid / 2 : grid;
     const uint64_t* part = h->d_part + (size_t)g0 * grid * vx::kTcListLen;
     uint64_t* ck = h->d_ckeys + (size_t)g0 * kp;
     CU_TRY(vx::launch_merge_topk(part, Bg, P * vx::kTcListLen, kp, 0, ck, nullptr, nullptr, st));

@@ -216,6 +216,29 @@ def test_tc_scan_bit_identical_to_oracle_f32(vx, oracle, N, D, B, k):
         assert fallbacks == 0
 
 
+@pytest.mark.parametrize("pairs", [1, 2])
+@pytest.mark.parametrize("coarse", ["bf16", "tf32"])
+@pytest.mark.parametrize("N,D,B,k", [(60_000, 768, 512, 100), (30_001, 256, 257, 10),
+                                     (20_000, 768, 700, 50), (10_000, 128, 1100, 16)])
+def test_tc_pairs_large_batch_bit_identical(vx, oracle, N, D, B, k, coarse, pairs):
+    # B > 256: several passes of the CTA-pair kernel (pairs=1: 256 queries per pass; pairs=2:
+    # 512 per pass, two accumulator groups); results are still the exact oracle's
+    X = oracle.synth_rows(42, 0, N, D)
+    Q = oracle.synth_rows(43, 0, B, D)
+    with vx.Index(N, D, max_batch=B, max_k=k) as idx:
+        idx.synth(42)
+        idx.set_option(vx.VX_OPT_SCAN, vx.VX_SCAN_TC)
+        idx.set_option(vx.VX_OPT_COARSE, vx.VX_COARSE_BF16 if coarse == "bf16" else vx.VX_COARSE_TF32)
+        idx.set_option(vx.VX_OPT_SCAN_PAIRS, pairs)
+        ids, sc = idx.search(Q, k)
+        fallbacks = idx.stats()["cert_fallbacks"]
+    rid, rsc = oracle.flat_topk(X, Q, k, mode=1)
+    assert np.array_equal(ids, rid)
+    v = rid >= 0
+    assert np.array_equal(sc[v], rsc[v].astype(np.float32))
+    assert fallbacks <= B // 50
+
+
 @pytest.mark.parametrize("B,k", [(40, 100), (70, 20)])
 def test_tc_certificate_fallback_many_queries(vx, oracle, B, k):
     # most queries fail the certificate: the exact re-scan runs as ONE device-count launch
