@@ -261,27 +261,39 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
 __global__ void __launch_bounds__(256)
     rerank_kernel(const float* __restrict__ docs, const float* __restrict__ qv, int D,
                   const uint64_t* __restrict__ cand, int kp, const uint64_t* __restrict__ part,
-                  int grid, int k, int64_t row0, const float* __restrict__ xnorm_max,
-                  float err_coef,
+                  int grid, int k, int64_t row0, const float* __restrict__ xstats,
+                  int coarse_bf16,
                   uint64_t* __restrict__ out_keys, int64_t* __restrict__ out_ids,
                   float* __restrict__ out_scores, int* __restrict__ flags, int rows_per_round) {
   extern __shared__ __align__(16) float rsm[];
   float* qs = rsm;                                             // [D]
   uint64_t* keys = reinterpret_cast<uint64_t*>(rsm + ((D + 3) & ~3));  // [kp]
   float* rowbuf = reinterpret_cast<float*>(keys + kp);         // [R][D+4] staged rows
-  __shared__ float s_red[32];
+  __shared__ float s_red[32], s_red16[32], s_redr[32];
   __shared__ int s_fail;
   __shared__ __align__(8) uint64_t s_bar;
   const int b = blockIdx.x;
   const float* q = qv + (size_t)b * D;
-  float ss = 0.0f;
+  // ||q||^2, ||bf16(q)||^2, ||q - bf16(q)||^2 (the certificate's error bound, below)
+  float ss = 0.0f, s16 = 0.0f, sr = 0.0f;
   for (int t = threadIdx.x; t < D; t += blockDim.x) {
-    float v = q[t];
+    const float v = q[t];
+    const float v16 = vx_bf16_bits_to_f32(vx_f32_to_bf16_bits(v));
     qs[t] = v;
     ss = fmaf(v, v, ss);
+    s16 = fmaf(v16, v16, s16);
+    sr = fmaf(v - v16, v - v16, sr);  // v - v16 is exact (Sterbenz)
   }
-  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = ss;
+  for (int o = 16; o > 0; o >>= 1) {
+    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    s16 += __shfl_xor_sync(0xffffffffu, s16, o);
+    sr += __shfl_xor_sync(0xffffffffu, sr, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s_red[threadIdx.x >> 5] = ss;
+    s_red16[threadIdx.x >> 5] = s16;
+    s_redr[threadIdx.x >> 5] = sr;
+  }
   if (threadIdx.x == 0) s_fail = 0;
   __syncthreads();
   const uint64_t* cb = cand + (size_t)b * kp;
@@ -349,10 +361,27 @@ __global__ void __launch_bounds__(256)
     }
   if (threadIdx.x == 0 && tprime != 0ull) {
     // certificate 2: every document outside the candidates has coarse score <= s(T'), so
-    // exact score <= s(T') + E; the exact k-th must beat that bound strictly.
-    float qn = 0.0f;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) qn += s_red[w];
-    const float E = err_coef * sqrtf(qn) * 1.0001f * xnorm_max[0] + 1e-30f;
+    // its exact score <= s(T') + E; the exact k-th must beat that bound strictly.
+    //   bf16 coarse: with q16 = bf16(q), rq = q - q16 (x16, rx likewise, per shard maxima
+    //   from row_stats_kernel), q.x - q16.x16 = q16.rx + rq.x16 + rq.rx, so by Cauchy-Schwarz
+    //   |q.x - q16.x16| <= |q16| max|rx| + |rq| max|x16| + |rq| max|rx|: a rigorous bound
+    //   from the actual rounding residuals (the worst case 2u|q||x| = 2^-7 |q||x| is ~2x
+    //   looser).  TF32 coarse: per-operand truncation <= 2^-10 -> 2^-9 |q| max|x|.
+    //   Both: + 2^-12 |q| max|x| for the fp32 accumulation of the tensor core and of the
+    //   exact in-order chain (each <= 768 * 2^-24 relative, 5x margin).
+    float qn = 0.0f, q16 = 0.0f, qr = 0.0f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      qn += s_red[w];
+      q16 += s_red16[w];
+      qr += s_redr[w];
+    }
+    qn = sqrtf(qn) * 1.0001f;
+    q16 = sqrtf(q16) * 1.0001f;
+    qr = sqrtf(qr) * 1.0001f;
+    const float xmax = fmaxf(xstats[0], xstats[1]);
+    const float E = (coarse_bf16 ? (q16 * xstats[2] + qr * xstats[1] + qr * xstats[2])
+                                 : kErrCoefTF32 * qn * xstats[0]) * 1.001f +
+                    0.000244140625f * fmaxf(qn, q16) * xmax + 1e-30f;
     const uint64_t ek = keys[k - 1];
     if (ek == 0ull || !(vx_key_score(ek) > vx_key_score(tprime) + E)) s_fail = 1;
   }
@@ -374,21 +403,38 @@ __global__ void __launch_bounds__(256)
   if (threadIdx.x == 0) flags[b] = s_fail;
 }
 
-// max row L2 norm of the shard (for the certificate's error bound)
-__global__ void row_norm_max_kernel(const float* __restrict__ docs, int64_t n, int D,
-                                    unsigned int* __restrict__ out_bits) {
+// Per-shard maxima for the certificate's error bound: [0] max |x|, [1] max |bf16(x)|,
+// [2] max |x - bf16(x)| over the shard's rows (float bits, atomicMax of non-negative floats).
+__global__ void row_stats_kernel(const float* __restrict__ docs, int64_t n, int D,
+                                 unsigned int* __restrict__ out_bits) {
   const int lane = threadIdx.x & 31;
   const int64_t wpb = blockDim.x >> 5;
-  float best = 0.0f;
+  float b0 = 0.0f, b1 = 0.0f, b2 = 0.0f;
   for (int64_t r = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); r < n;
        r += (int64_t)gridDim.x * wpb) {
     const float* x = docs + r * D;
-    float ss = 0.0f;
-    for (int c = lane; c < D; c += 32) ss = fmaf(x[c], x[c], ss);
-    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    best = fmaxf(best, sqrtf(ss));
+    float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f;
+    for (int c = lane; c < D; c += 32) {
+      const float v = x[c];
+      const float v16 = vx_bf16_bits_to_f32(vx_f32_to_bf16_bits(v));
+      s0 = fmaf(v, v, s0);
+      s1 = fmaf(v16, v16, s1);
+      s2 = fmaf(v - v16, v - v16, s2);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    b0 = fmaxf(b0, sqrtf(s0));
+    b1 = fmaxf(b1, sqrtf(s1));
+    b2 = fmaxf(b2, sqrtf(s2));
   }
-  if (lane == 0) atomicMax(out_bits, __float_as_uint(best * 1.00001f));
+  if (lane == 0) {
+    atomicMax(&out_bits[0], __float_as_uint(b0 * 1.00001f));
+    atomicMax(&out_bits[1], __float_as_uint(b1 * 1.00001f));
+    atomicMax(&out_bits[2], __float_as_uint(b2 * 1.00001f));
+  }
 }
 
 // ------------------------------------------------------------------- host side
@@ -422,7 +468,7 @@ cudaError_t launch_scan_tc(int QT, int TD, const CUtensorMap* tq, const CUtensor
 
 cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64_t* cand, int B,
                           int kp, const uint64_t* part, int grid, int k, int64_t row0,
-                          const float* xnorm_max, float err_coef, uint64_t* out_keys,
+                          const float* xstats, int coarse_bf16, uint64_t* out_keys,
                           int64_t* out_ids, float* out_scores, int* flags, cudaStream_t st) {
   const size_t base = (size_t)((D + 3) & ~3) * 4 + (size_t)kp * 8;
   const size_t row = (size_t)(D + 4) * 4;
@@ -432,18 +478,18 @@ cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64
   cudaError_t e = cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  rerank_kernel<<<B, 256, smem, st>>>(docs, q, D, cand, kp, part, grid, k, row0, xnorm_max,
-                                      err_coef, out_keys, out_ids, out_scores, flags, R);
+  rerank_kernel<<<B, 256, smem, st>>>(docs, q, D, cand, kp, part, grid, k, row0, xstats,
+                                      coarse_bf16, out_keys, out_ids, out_scores, flags, R);
   return cudaGetLastError();
 }
 
-cudaError_t launch_row_norm_max(const float* docs, int64_t n, int D, unsigned int* out_bits,
-                                cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(out_bits, 0, 4, st);
+cudaError_t launch_row_stats(const float* docs, int64_t n, int D, unsigned int* out_bits,
+                             cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out_bits, 0, 12, st);
   if (e != cudaSuccess) return e;
   int64_t blocks = (n + 7) / 8;
   if (blocks > 148 * 32) blocks = 148 * 32;
-  row_norm_max_kernel<<<(int)(blocks < 1 ? 1 : blocks), 256, 0, st>>>(docs, n, D, out_bits);
+  row_stats_kernel<<<(int)(blocks < 1 ? 1 : blocks), 256, 0, st>>>(docs, n, D, out_bits);
   return cudaGetLastError();
 }
 

@@ -191,7 +191,7 @@ struct vx_index {
   int32_t* d_hdr = nullptr;      // [4]
   uint64_t* d_ckeys = nullptr;   // [maxB][256] merged coarse keys (TC path)
   int* d_flags = nullptr;        // [maxB] certificate failures (TC path)
-  unsigned int* d_xnorm = nullptr;  // max row norm of the shard (float bits)
+  unsigned int* d_xnorm = nullptr;  // [3] row-norm maxima of the shard (float bits, row_stats)
   float* d_fq = nullptr;         // [maxB][D] queries gathered for the exact fallback
   int* d_fidx = nullptr;         // [maxB] flagged query indices
   int* d_fcount = nullptr;       // [2] flagged count of the last batch, running total
@@ -305,7 +305,7 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
   ALLOC(h->d_hdr, 16);
   ALLOC(h->d_ckeys, B * 256 * 8);
   ALLOC(h->d_flags, B * 4);
-  ALLOC(h->d_xnorm, 4);
+  ALLOC(h->d_xnorm, 16);
   ALLOC(h->d_fq, B * D * 4);
   ALLOC(h->d_fidx, B * 4);
   ALLOC(h->d_fcount, 16);
@@ -330,7 +330,7 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
     return cleanup(fail(VX_ERR_OOM, "pinned header"));
   if (cudaMallocHost((void**)&h->h_flags, B * 4) != cudaSuccess)
     return cleanup(fail(VX_ERR_OOM, "pinned flags"));
-  if (cudaMemset(h->d_xnorm, 0, 4) != cudaSuccess || cudaMemset(h->d_fcount, 0, 16) != cudaSuccess)
+  if (cudaMemset(h->d_xnorm, 0, 16) != cudaSuccess || cudaMemset(h->d_fcount, 0, 16) != cudaSuccess)
     return cleanup(fail(VX_ERR_CUDA, "memset"));
   if (h->tokens) {
     s = make_tmap_2d(&h->tmap_tok, h->tokens, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
@@ -447,7 +447,7 @@ extern "C" vx_status vx_index_synth(vx_index* h, uint64_t seed) {
   CU_TRY(cudaSetDevice(h->device));
   CU_TRY(vx::launch_synth_rows(h->docs, seed, h->row0, h->n_local, h->desc.dim, h->stream));
   count_launch(h);
-  CU_TRY(vx::launch_row_norm_max(h->docs, h->n_local, h->desc.dim, h->d_xnorm, h->stream));
+  CU_TRY(vx::launch_row_stats(h->docs, h->n_local, h->desc.dim, h->d_xnorm, h->stream));
   count_launch(h);
   if (h->docs16) {
     CU_TRY(vx::launch_to_bf16(h->docs, h->docs16, h->n_local * h->desc.dim, h->stream));
@@ -466,7 +466,7 @@ extern "C" vx_status vx_index_upload(vx_index* h, const float* rows, int64_t row
   CU_TRY(cudaMemcpyAsync(h->docs + (row0 - h->row0) * h->desc.dim, rows,
                          (size_t)n * h->desc.dim * 4, cudaMemcpyHostToDevice, h->stream));
   // the TC certificate needs an upper bound on the row norms: recompute over the shard
-  CU_TRY(vx::launch_row_norm_max(h->docs, h->n_local, h->desc.dim, h->d_xnorm, h->stream));
+  CU_TRY(vx::launch_row_stats(h->docs, h->n_local, h->desc.dim, h->d_xnorm, h->stream));
   count_launch(h);
   if (h->docs16 && n > 0) {
     const size_t off = (size_t)(row0 - h->row0) * h->desc.dim;
@@ -665,8 +665,8 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
     CU_TRY(vx::launch_merge_topk(part, Bg, P * vx::kTcListLen, kp, 0, ck, nullptr, nullptr, st));
     count_launch(h);
     CU_TRY(vx::launch_rerank(h->docs, d_q + (size_t)g0 * D, D, ck, Bg, kp, part, P, k, h->row0,
-                             reinterpret_cast<const float*>(h->d_xnorm),
-                             bf16 ? vx::kErrCoefBF16 : vx::kErrCoefTF32, keys + (size_t)g0 * k,
+                             reinterpret_cast<const float*>(h->d_xnorm), bf16 ? 1 : 0,
+                             keys + (size_t)g0 * k,
                              ids + (size_t)g0 * k, scores + (size_t)g0 * k, h->d_flags + g0, st));
     count_launch(h);
   }

@@ -42,11 +42,10 @@ struct ScanTcArgs {
   int32_t dbg_no_select;  // timing experiments only (VX_DEBUG_TC_NOSELECT): skip the top-k
   uint64_t* part;    // [B][gridDim.x][16] coarse keys
 };
-// coarse-score error bound coefficients E = coef * ||q|| * max||x|| (see scan_tc.cu):
-// TF32 truncates both operands to 10 mantissa bits (<= 2^-10 each); bf16 rounds both to
-// 8 bits (<= 2^-9 each); + 2^-12 of slack for fp32 accumulation inside the tensor core.
-constexpr float kErrCoefTF32 = 0.001953125f + 0.000244140625f;
-constexpr float kErrCoefBF16 = 0.00390625f + 0.000244140625f;
+// TF32 coarse-score error bound coefficient E = coef * ||q|| * max||x||: the tensor core
+// truncates both operands to 10 mantissa bits (<= 2^-10 each).  The bf16 bound is computed
+// from the actual rounding residuals (rerank_kernel in scan_tc.cu).
+constexpr float kErrCoefTF32 = 0.001953125f;
 cudaError_t launch_to_bf16(const float* in, uint16_t* out, int64_t n, cudaStream_t st);
 constexpr int kTcListLen = 16;
 size_t scan_tc_smem(int QT, int TD, int* ns_out);
@@ -59,10 +58,11 @@ cudaError_t launch_scan_tc2(int H, const CUtensorMap* tq, const CUtensorMap* tx,
                             const ScanTcArgs& a, int grid, size_t smem, cudaStream_t st);
 cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64_t* cand, int B,
                           int kp, const uint64_t* part, int grid, int k, int64_t row0,
-                          const float* xnorm_max, float err_coef, uint64_t* out_keys,
+                          const float* xstats, int coarse_bf16, uint64_t* out_keys,
                           int64_t* out_ids, float* out_scores, int* flags, cudaStream_t st);
-cudaError_t launch_row_norm_max(const float* docs, int64_t n, int D, unsigned int* out_bits,
-                                cudaStream_t st);
+// per-shard maxima [max|x|, max|bf16(x)|, max|x - bf16(x)|] (3 floats as uint bits)
+cudaError_t launch_row_stats(const float* docs, int64_t n, int D, unsigned int* out_bits,
+                             cudaStream_t st);
 
 // -------- top-k merge (K3): topk.cu
 // For each query q: select the k largest keys among in[q][0..M), write them
