@@ -520,7 +520,7 @@ def run_ours(args) -> None:
         "dtype": "f32", "data": "synthetic", "config": cfg,
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": int(st["kernel_launches"]),
-        "cert_fallbacks": int(st["cert_fallbacks"]),
+        "cert_fallbacks": int(st["cert_fallbacks"]), "cert_level2": int(st["cert_level2"]),
         "root_phases_ms": ({"broadcast": st["phase_ms"][0], "local_stage": st["phase_ms"][1],
                             "gather_merge": st["phase_ms"][2],
                             "rescore_phase2": st["phase_ms"][3]}

@@ -65,7 +65,9 @@ enum {
   VX_OPT_SCAN_TILE = 6,   /* documents per tensor-core scan tile: 0 (auto), 128 or 256 */
   VX_OPT_SCAN_PAIRS = 7   /* 1 (default): CTA-pair (cta_group::2) scan for B > 128, 256 queries
                              per pass over the index; 2: 512 queries per pass (two accumulator
-                             groups, one TMEM buffer); 0: single-CTA kernels */
+                             groups, one TMEM buffer); 0: single-CTA kernels */,
+  VX_OPT_KPRIME = 8       /* tensor-core candidate set k' re-ranked exactly: 0 (auto:
+                             4 next_pow2(k) in [64, 256]) or a power of two in [16, 512] */
 };
 /* Coarse (candidate-selecting) tensor-core scan format.  Either way every reported score is
  * recomputed exactly in fp32 and certified.  BF16 reads a bf16 shadow
@@ -96,7 +98,8 @@ typedef struct vx_stats {
   uint64_t batches;           /* search/maxsim batches served */
   uint64_t queries;           /* queries served */
   uint64_t graph_replays;     /* CUDA graph launches */
-  uint64_t cert_fallbacks;    /* queries re-scanned exactly after a failed TC certificate */
+  uint64_t cert_fallbacks;    /* queries re-scanned exactly after both TC certificate levels
+                                 failed */
   float last_scan_ms;         /* device time of the last scan kernel (CUDA events) */
   float last_step_ms;         /* device time of the last whole stage */
   double scan_ms_total;       /* sum of scan device times sampled by vx_sync */
@@ -105,6 +108,8 @@ typedef struct vx_stats {
   float phase_ms[4];          /* sharded rank 0, last batch: broadcast, local stage,
                                  gather of the k x G keys + global merge, phase 2 (winner
                                  broadcast, owner MaxSim, max-reduce, order) */
+  uint64_t cert_level2;       /* queries whose k'-candidate certificate failed and that went
+                                 to the wide re-rank over the full per-CTA lists */
 } vx_stats;
 
 int32_t vx_abi_version(void);

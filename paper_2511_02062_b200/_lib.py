@@ -19,7 +19,7 @@ STATUS = {0: "VX_OK", 1: "VX_ERR_INVALID", 2: "VX_ERR_CUDA", 3: "VX_ERR_OOM", 4:
 VX_SCAN_AUTO, VX_SCAN_F32, VX_SCAN_TC = 0, 1, 2
 VX_OPT_SCAN, VX_OPT_GRID, VX_OPT_GRAPHS, VX_OPT_MAXSIM = 1, 2, 3, 4
 VX_MAXSIM_AUTO, VX_MAXSIM_CC, VX_MAXSIM_TC = 0, 1, 2
-VX_OPT_COARSE, VX_OPT_SCAN_TILE, VX_OPT_SCAN_PAIRS = 5, 6, 7
+VX_OPT_COARSE, VX_OPT_SCAN_TILE, VX_OPT_SCAN_PAIRS, VX_OPT_KPRIME = 5, 6, 7, 8
 VX_COARSE_AUTO, VX_COARSE_TF32, VX_COARSE_BF16 = 0, 1, 2
 VX_FLAG_NO_BF16_SHADOW = 1
 VX_PREPARE_SEARCH, VX_PREPARE_RESCORE = 1, 2
@@ -45,7 +45,8 @@ class Stats(C.Structure):
                 ("graph_replays", C.c_uint64), ("cert_fallbacks", C.c_uint64),
                 ("last_scan_ms", C.c_float), ("last_step_ms", C.c_float),
                 ("scan_ms_total", C.c_double), ("step_ms_total", C.c_double),
-                ("timed_batches", C.c_uint64), ("phase_ms", C.c_float * 4)]
+                ("timed_batches", C.c_uint64), ("phase_ms", C.c_float * 4),
+                ("cert_level2", C.c_uint64)]
 
 
 P = C.c_void_p

@@ -254,6 +254,16 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
   }
 }
 
+// Certificate-2 error bound E for one query (see rerank_kernel): qn = |q|, q16 = |bf16(q)|,
+// qr = |q - bf16(q)| (each already inflated for fp32 rounding), xstats = shard maxima.
+__device__ __forceinline__ float cert_err_bound(int coarse_bf16, float qn, float q16, float qr,
+                                                const float* __restrict__ xstats) {
+  const float xmax = fmaxf(xstats[0], xstats[1]);
+  return (coarse_bf16 ? (q16 * xstats[2] + qr * xstats[1] + qr * xstats[2])
+                      : kErrCoefTF32 * qn * xstats[0]) * 1.001f +
+         0.000244140625f * fmaxf(qn, q16) * xmax + 1e-30f;
+}
+
 // ------------------------------------------------------------------- K2b: exact re-rank
 // One CTA per query.  cand: the merged coarse top-k' keys (score desc); part: the per-CTA
 // lists of K2 (certificate 1); docs/queries fp32.  Writes the exact top-k and flags[b] = 1
@@ -378,10 +388,7 @@ __global__ void __launch_bounds__(256)
     qn = sqrtf(qn) * 1.0001f;
     q16 = sqrtf(q16) * 1.0001f;
     qr = sqrtf(qr) * 1.0001f;
-    const float xmax = fmaxf(xstats[0], xstats[1]);
-    const float E = (coarse_bf16 ? (q16 * xstats[2] + qr * xstats[1] + qr * xstats[2])
-                                 : kErrCoefTF32 * qn * xstats[0]) * 1.001f +
-                    0.000244140625f * fmaxf(qn, q16) * xmax + 1e-30f;
+    const float E = cert_err_bound(coarse_bf16, qn, q16, qr, xstats);
     const uint64_t ek = keys[k - 1];
     if (ek == 0ull || !(vx_key_score(ek) > vx_key_score(tprime) + E)) s_fail = 1;
   }
@@ -401,6 +408,139 @@ __global__ void __launch_bounds__(256)
     }
   }
   if (threadIdx.x == 0) flags[b] = s_fail;
+}
+
+// ------------------------------------------------------------------- K2c: wide re-rank
+// Second certificate level for the (rare) queries whose k'-candidate certificate failed:
+// the per-CTA (per-pair) lists hold more than the k' candidates.  With T'' = the largest
+// 16th key among FULL lists (the deepest truncation point), every document whose coarse key
+// is >= T'' is in some list (a document outside its list has key < that list's 16th key <=
+// T''), so re-ranking all list entries >= T'' exactly (up to P x 16 rows) and checking
+// exact k-th > coarse(T'') + E certifies the query without touching the index again.  T''
+// sits ~5-7x deeper than the k'-th candidate, so the gap almost always clears E; queries
+// that still fail go on to the exact re-scan.  One CTA per compacted failing query.
+__global__ void __launch_bounds__(256)
+    rerank_wide_kernel(const float* __restrict__ docs, const float* __restrict__ fq, int D,
+                       const int* __restrict__ fidx, const int* __restrict__ fcount,
+                       const uint64_t* __restrict__ part_all, int B, int GS, int P_pairs,
+                       int P_single, int k, int64_t row0, const float* __restrict__ xstats,
+                       int coarse_bf16, uint64_t* __restrict__ out_keys,
+                       int64_t* __restrict__ out_ids, float* __restrict__ out_scores,
+                       int* __restrict__ flags) {
+  extern __shared__ __align__(16) float wsm[];
+  const int i = blockIdx.x;
+  if (i >= *fcount) return;
+  const int b = fidx[i];
+  const int g0 = (b / GS) * GS, Bg = min(GS, B - g0);
+  const int P = (P_pairs > 0 && Bg > 128) ? P_pairs : P_single;
+  const int M = P * kTcKC;
+  const uint64_t* lists = part_all + (size_t)g0 * (size_t)P_single * kTcKC + (size_t)(b - g0) * M;
+  int np2 = 16;
+  while (np2 < M) np2 <<= 1;
+  float* qs = wsm;                                                      // [D]
+  uint64_t* keys = reinterpret_cast<uint64_t*>(wsm + ((D + 3) & ~3));   // [np2]
+  __shared__ float s_r0[8], s_r1[8], s_r2[8];
+  __shared__ unsigned long long s_t2;
+  __shared__ int s_n;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float* q = fq + (size_t)i * D;
+  float ss = 0.0f, s16 = 0.0f, sr = 0.0f;
+  for (int t = threadIdx.x; t < D; t += blockDim.x) {
+    const float v = q[t];
+    const float v16 = vx_bf16_bits_to_f32(vx_f32_to_bf16_bits(v));
+    qs[t] = v;
+    ss = fmaf(v, v, ss);
+    s16 = fmaf(v16, v16, s16);
+    sr = fmaf(v - v16, v - v16, sr);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    s16 += __shfl_xor_sync(0xffffffffu, s16, o);
+    sr += __shfl_xor_sync(0xffffffffu, sr, o);
+  }
+  if (lane == 0) {
+    s_r0[warp] = ss;
+    s_r1[warp] = s16;
+    s_r2[warp] = sr;
+  }
+  if (threadIdx.x == 0) {
+    s_t2 = 0ull;
+    s_n = 0;
+  }
+  __syncthreads();
+  // T'' = max over full lists of their 16th key (0: no list was truncated)
+  for (int p = threadIdx.x; p < P; p += blockDim.x) {
+    const uint64_t last = lists[(size_t)p * kTcKC + (kTcKC - 1)];
+    if (last) atomicMax(&s_t2, (unsigned long long)last);
+  }
+  __syncthreads();
+  const uint64_t t2 = s_t2;
+  // candidates: list entries >= T'', re-scored exactly (in-order fmaf chain per row)
+  for (int j = threadIdx.x; j < M; j += blockDim.x) {
+    const uint64_t ck = lists[j];
+    if (ck == 0ull || ck < t2) continue;
+    const float4* x = reinterpret_cast<const float4*>(docs + (size_t)vx_key_id(ck) * D);
+    float acc = 0.0f;
+    for (int c = 0; c < (D >> 2); ++c) {
+      const float4 xv = __ldg(x + c);
+      acc = fmaf(xv.x, qs[4 * c + 0], acc);
+      acc = fmaf(xv.y, qs[4 * c + 1], acc);
+      acc = fmaf(xv.z, qs[4 * c + 2], acc);
+      acc = fmaf(xv.w, qs[4 * c + 3], acc);
+    }
+    keys[atomicAdd(&s_n, 1)] = vx_make_key(acc, vx_key_id(ck));
+  }
+  __syncthreads();
+  const int n = s_n;
+  for (int j = n + threadIdx.x; j < np2; j += blockDim.x) keys[j] = 0ull;
+  __syncthreads();
+  for (int size = 2; size <= np2; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < (np2 >> 1); t += blockDim.x) {
+        int lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
+        bool desc = (lo & size) == 0;
+        uint64_t x0 = keys[lo], x1 = keys[hi];
+        if ((x0 < x1) == desc) {
+          keys[lo] = x1;
+          keys[hi] = x0;
+        }
+      }
+      __syncthreads();
+    }
+  __shared__ int s_fail;
+  if (threadIdx.x == 0) {
+    int fail = 0;
+    if (t2 != 0ull) {
+      float qn = 0.0f, q16 = 0.0f, qr = 0.0f;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+        qn += s_r0[w];
+        q16 += s_r1[w];
+        qr += s_r2[w];
+      }
+      const float E = cert_err_bound(coarse_bf16, sqrtf(qn) * 1.0001f, sqrtf(q16) * 1.0001f,
+                                     sqrtf(qr) * 1.0001f, xstats);
+      const uint64_t ek = k <= n ? keys[k - 1] : 0ull;
+      fail = (ek == 0ull || !(vx_key_score(ek) > vx_key_score(t2) + E)) ? 1 : 0;
+    }
+    s_fail = fail;
+    flags[b] = fail;
+  }
+  __syncthreads();
+  if (s_fail) return;  // the exact re-scan writes this query
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    const uint64_t key = j < n ? keys[j] : 0ull;
+    const size_t o = (size_t)b * k + j;
+    if (key == 0ull) {
+      out_keys[o] = 0ull;
+      out_ids[o] = -1;
+      out_scores[o] = -INFINITY;
+    } else {
+      const int64_t gid = (int64_t)vx_key_id(key) + row0;
+      out_keys[o] = (key & 0xFFFFFFFF00000000ull) | (uint64_t)(0xFFFFFFFFu - (uint32_t)gid);
+      out_ids[o] = gid;
+      out_scores[o] = vx_key_score(key);
+    }
+  }
 }
 
 // Per-shard maxima for the certificate's error bound: [0] max |x|, [1] max |bf16(x)|,
@@ -438,6 +578,26 @@ __global__ void row_stats_kernel(const float* __restrict__ docs, int64_t n, int 
 }
 
 // ------------------------------------------------------------------- host side
+cudaError_t launch_rerank_wide(const float* docs, const float* fq, int D, const int* fidx,
+                               const int* fcount, const uint64_t* part_all, int B, int GS,
+                               int P_pairs, int P_single, int k, int64_t row0,
+                               const float* xstats, int coarse_bf16, uint64_t* out_keys,
+                               int64_t* out_ids, float* out_scores, int* flags,
+                               cudaStream_t st) {
+  const int M = P_single * kTcKC;
+  int np2 = 16;
+  while (np2 < M) np2 <<= 1;
+  const size_t smem = (size_t)((D + 3) & ~3) * 4 + (size_t)np2 * 8;
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(rerank_wide_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  rerank_wide_kernel<<<B, 256, smem, st>>>(docs, fq, D, fidx, fcount, part_all, B, GS, P_pairs,
+                                           P_single, k, row0, xstats, coarse_bf16, out_keys,
+                                           out_ids, out_scores, flags);
+  return cudaGetLastError();
+}
+
 size_t scan_tc_smem(int QT, int TD, int* ns_out) {
   const int stage = QT * kTcStageUnit + TD * 128;
   const size_t fixed = (size_t)QT * 128 * kTcKC * 8 + 16 + 1024;

@@ -16,7 +16,7 @@
 namespace vx {
 
 constexpr int kMergeThreads = 256;
-constexpr int kMaxK = 256;
+constexpr int kMaxK = 512;  // merge: k' up to 512 (the TC candidate set); order_by: k <= 256
 
 __device__ __forceinline__ void block_bitonic_desc(uint64_t* buf, int n) {
   for (int size = 2; size <= n; size <<= 1) {
@@ -172,9 +172,9 @@ __global__ void __launch_bounds__(256)
     order_by_kernel(const float* __restrict__ ms, const int64_t* __restrict__ ids,
                     const float* __restrict__ ip, int k, int64_t* __restrict__ out_ids,
                     float* __restrict__ out_ip, float* __restrict__ out_ms) {
-  __shared__ uint64_t buf[kMaxK];
-  __shared__ float s_ip[kMaxK], s_ms[kMaxK];
-  __shared__ int64_t s_id[kMaxK];
+  __shared__ uint64_t buf[256];
+  __shared__ float s_ip[256], s_ms[256];
+  __shared__ int64_t s_id[256];
   int kp = 16;
   while (kp < k) kp <<= 1;
   const size_t base = (size_t)blockIdx.x * k;
@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(256)
 cudaError_t launch_order_by(const float* key_score, const int64_t* ids, const float* ip, int B,
                             int k, int64_t* out_ids, float* out_ip, float* out_ms,
                             cudaStream_t st) {
-  if (k < 1 || k > kMaxK) return cudaErrorInvalidValue;
+  if (k < 1 || k > 256) return cudaErrorInvalidValue;
   order_by_kernel<<<B, 256, 0, st>>>(key_score, ids, ip, k, out_ids, out_ip, out_ms);
   return cudaGetLastError();
 }

@@ -169,6 +169,7 @@ struct vx_index {
   uint16_t* d_q16 = nullptr;     // [maxB][D] bf16 queries for the bf16 coarse scan
   int coarse = VX_COARSE_AUTO;
   int scan_tile = 0;             // documents per tensor-core tile (0 = auto)
+  int kprime = 0;                // TC candidate set size k' (0 = auto; VX_OPT_KPRIME)
   int use_pairs = 1;             // CTA-pair scan for B > 128: 0 off, 1 on, 2 on + 512-query
                                  // passes (VX_OPT_SCAN_PAIRS)
   // options
@@ -189,7 +190,7 @@ struct vx_index {
   void* d_send = nullptr;        // [maxB][maxK] x 8 B scratch (rank 0: the reduced MaxSim)
   void* d_recv = nullptr;        // [G][maxB][maxK] gathered keys (rank 0)
   int32_t* d_hdr = nullptr;      // [4]
-  uint64_t* d_ckeys = nullptr;   // [maxB][256] merged coarse keys (TC path)
+  uint64_t* d_ckeys = nullptr;   // [maxB][512] merged coarse keys (TC path)
   int* d_flags = nullptr;        // [maxB] certificate failures (TC path)
   unsigned int* d_xnorm = nullptr;  // [3] row-norm maxima of the shard (float bits, row_stats)
   float* d_fq = nullptr;         // [maxB][D] queries gathered for the exact fallback
@@ -303,13 +304,15 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
   if (d->n_shards > 1 && d->shard == 0)
     ALLOC(h->d_recv, (size_t)d->n_shards * B * K * 8);
   ALLOC(h->d_hdr, 16);
-  ALLOC(h->d_ckeys, B * 256 * 8);
+  ALLOC(h->d_ckeys, B * 512 * 8);
   ALLOC(h->d_flags, B * 4);
   ALLOC(h->d_xnorm, 16);
   ALLOC(h->d_fq, B * D * 4);
   ALLOC(h->d_fidx, B * 4);
   ALLOC(h->d_fcount, 16);
-  if (!(d->flags & VX_FLAG_NO_BF16_SHADOW)) {
+  // bf16 shadow for the coarse scan: K-chunks of 64 bf16 (one 128-byte swizzle atom), so
+  // D % 64 == 0; otherwise the coarse scan reads the fp32 rows as TF32 (32-wide chunks)
+  if (!(d->flags & VX_FLAG_NO_BF16_SHADOW) && D % 64 == 0) {
     ALLOC(h->docs16, (size_t)h->n_local * D * 2);
     ALLOC(h->d_q16, B * D * 2);
   }
@@ -394,6 +397,11 @@ extern "C" vx_status vx_set_option(vx_index* h, int32_t option, int64_t value) {
     case VX_OPT_GRID:
       if (value < 0 || value > h->num_sms) return fail(VX_ERR_INVALID, "grid %lld", (long long)value);
       h->grid = value == 0 ? h->num_sms : (int)value;
+      return VX_OK;
+    case VX_OPT_KPRIME:
+      if (value != 0 && (value < 16 || value > 512 || (value & (value - 1))))
+        return fail(VX_ERR_INVALID, "kprime %lld (0 or a power of two in [16, 512])", (long long)value);
+      h->kprime = (int)value;
       return VX_OK;
     case VX_OPT_SCAN_PAIRS:
       if (value < 0 || value > 2) return fail(VX_ERR_INVALID, "pairs %lld", (long long)value);
@@ -580,7 +588,14 @@ static vx_status local_topk_f32(vx_index* h, const float* d_q, int B, int k, uin
 }
 
 // candidates the TC pass hands to the exact re-rank
-static int kprime_of(int k) { return std::min(256, std::max(64, 4 * next_pow2(k))); }
+// k' = 4 next_pow2(k) in [64, 256] (VX_OPT_KPRIME overrides, up to 512).  256 is the
+// measured sweet spot for bf16 at k = 100: with 16-entry per-pair lists, k' = 512 fails
+// certificate 1 for ~13% of queries (a pair holding >= 16 of the top-512), k' = 256 for
+// ~0.03% (profiles/cert_rate.py, profiles/r01/cert_rate.jsonl).
+static int kprime_of(const vx_index* h, int k) {
+  if (h->kprime) return std::max(h->kprime, next_pow2(k));
+  return std::min(256, std::max(64, 4 * next_pow2(k)));
+}
 
 static bool tc_eligible(const vx_index* h, int B, int k) {
   (void)h;
@@ -594,8 +609,9 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
                                int64_t* ids, float* scores, cudaStream_t st) {
   const int D = h->desc.dim;
   const int grid = h->grid;
-  const int kp = kprime_of(k);
+  const int kp = kprime_of(h, k);
   const bool bf16 = h->docs16 && h->coarse != VX_COARSE_TF32;
+  if (D % (bf16 ? 64 : 32)) return fail(VX_ERR_UNSUPPORTED, "TC scan: D %d", D);
   CU_TRY(record_ev(h, h->tev[0], st));
   if (bf16) {
     CU_TRY(vx::launch_to_bf16(d_q, h->d_q16, (int64_t)B * D, st));
@@ -670,17 +686,28 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
                              ids + (size_t)g0 * k, scores + (size_t)g0 * k, h->d_flags + g0, st));
     count_launch(h);
   }
-  // certificate failures: re-scan those queries exactly (expected ~never on real data).
-  // Entirely on device — compact the flagged queries, exact scan sized by the device count
-  // (launches with a zero count exit at once), scatter back — so no host round trip and
-  // the stage stays capturable in one CUDA graph.
-  CU_TRY(vx::launch_cert_compact(h->d_flags, B, d_q, D, h->d_fidx, h->d_fcount, h->d_fq, st));
+  // Certificate failures, entirely on device (no host round trip: the stage stays
+  // capturable in one CUDA graph; every launch below exits at once when its count is 0):
+  //   level 2: compact the failing queries, re-rank all their list entries above the
+  //            deepest truncation point (rerank_wide_kernel) — no index access;
+  //   level 3: the queries that still fail are re-scanned exactly (K1 sized by the device
+  //            count) and scattered back.
+  int* cnt2 = h->d_fcount;      // [count, running total] of level-2 queries
+  int* cnt3 = h->d_fcount + 2;  // [count, running total] of exact re-scans
+  CU_TRY(vx::launch_cert_compact(h->d_flags, B, d_q, D, h->d_fidx, cnt2, h->d_fq, st));
+  count_launch(h);
+  CU_TRY(vx::launch_rerank_wide(h->docs, h->d_fq, D, h->d_fidx, cnt2, h->d_part, B, GS,
+                                pairs ? grid / 2 : 0, grid, k, h->row0,
+                                reinterpret_cast<const float*>(h->d_xnorm), bf16 ? 1 : 0, keys,
+                                ids, scores, h->d_flags, st));
+  count_launch(h);
+  CU_TRY(vx::launch_cert_compact(h->d_flags, B, d_q, D, h->d_fidx, cnt3, h->d_fq, st));
   count_launch(h);
   uint64_t* fk = h->d_ckeys;  // reuse: [B][k] (k <= 256)
   int64_t* fi = h->d_out_ids;
   float* fs = h->d_out_ms;
-  VX_TRY(local_topk_f32(h, h->d_fq, B, k, fk, fi, fs, st, h->d_fcount));
-  CU_TRY(vx::launch_cert_scatter(h->d_fidx, h->d_fcount, B, k, fk, fi, fs, keys, ids, scores, st));
+  VX_TRY(local_topk_f32(h, h->d_fq, B, k, fk, fi, fs, st, cnt3));
+  CU_TRY(vx::launch_cert_scatter(h->d_fidx, cnt3, B, k, fk, fi, fs, keys, ids, scores, st));
   count_launch(h);
   return VX_OK;
 }
@@ -994,9 +1021,10 @@ extern "C" vx_status vx_sync(vx_index* h) {
       }
       h->phases_pending = false;
     }
-    int fc[2] = {0, 0};  // certificate fallbacks counted on device
-    CU_TRY(cudaMemcpy(fc, h->d_fcount, 8, cudaMemcpyDeviceToHost));
-    h->st.cert_fallbacks = (uint64_t)fc[1];
+    int fc[4] = {0, 0, 0, 0};  // certificate levels counted on device
+    CU_TRY(cudaMemcpy(fc, h->d_fcount, 16, cudaMemcpyDeviceToHost));
+    h->st.cert_level2 = (uint64_t)fc[1];
+    h->st.cert_fallbacks = (uint64_t)fc[3];
   }
   cudaGetLastError();
   return VX_OK;

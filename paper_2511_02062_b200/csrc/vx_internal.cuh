@@ -60,6 +60,13 @@ cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64
                           int kp, const uint64_t* part, int grid, int k, int64_t row0,
                           const float* xstats, int coarse_bf16, uint64_t* out_keys,
                           int64_t* out_ids, float* out_scores, int* flags, cudaStream_t st);
+// second certificate level over the full per-CTA lists (compacted failing queries)
+cudaError_t launch_rerank_wide(const float* docs, const float* fq, int D, const int* fidx,
+                               const int* fcount, const uint64_t* part_all, int B, int GS,
+                               int P_pairs, int P_single, int k, int64_t row0,
+                               const float* xstats, int coarse_bf16, uint64_t* out_keys,
+                               int64_t* out_ids, float* out_scores, int* flags,
+                               cudaStream_t st);
 // per-shard maxima [max|x|, max|bf16(x)|, max|x - bf16(x)|] (3 floats as uint bits)
 cudaError_t launch_row_stats(const float* docs, int64_t n, int D, unsigned int* out_bits,
                              cudaStream_t st);

@@ -239,6 +239,28 @@ def test_tc_pairs_large_batch_bit_identical(vx, oracle, N, D, B, k, coarse, pair
     assert fallbacks <= B // 50
 
 
+@pytest.mark.parametrize("pairs", [0, 1])
+def test_tc_certificate_level2_wide_rerank(vx, oracle, pairs):
+    # k' = k = 16 candidates: the first certificate (exact k-th > coarse k'-th + E) fails for
+    # most queries; the wide re-rank over the full per-CTA lists (no index access) must
+    # rescue them, exactly
+    N, D, B, k = 100_000, 256, 200, 16
+    X = oracle.synth_rows(42, 0, N, D)
+    Q = oracle.synth_rows(43, 0, B, D)
+    with vx.Index(N, D, max_batch=B, max_k=k) as idx:
+        idx.synth(42)
+        idx.set_option(vx.VX_OPT_SCAN, vx.VX_SCAN_TC)
+        idx.set_option(vx.VX_OPT_SCAN_PAIRS, pairs)
+        idx.set_option(vx.VX_OPT_KPRIME, 16)
+        ids, sc = idx.search(Q, k)
+        st = idx.stats()
+    rid, rsc = oracle.flat_topk(X, Q, k, mode=1)
+    assert np.array_equal(ids, rid)
+    assert np.array_equal(sc, rsc.astype(np.float32))
+    assert st["cert_level2"] >= B // 4
+    assert st["cert_fallbacks"] <= st["cert_level2"] // 10
+
+
 @pytest.mark.parametrize("B,k", [(40, 100), (70, 20)])
 def test_tc_certificate_fallback_many_queries(vx, oracle, B, k):
     # most queries fail the certificate: the exact re-scan runs as ONE device-count launch
