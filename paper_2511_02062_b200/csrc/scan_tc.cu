@@ -18,6 +18,7 @@
 //   keep its 16 best (score desc, id asc) in registers (branch-free insertion).
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "vx_internal.cuh"
 #include "vx_ptx.cuh"
@@ -626,14 +627,19 @@ cudaError_t launch_scan_tc(int QT, int TD, const CUtensorMap* tq, const CUtensor
   return cudaErrorInvalidValue;
 }
 
+// rows per staging round: 32 rows (~100 KB of smem) lets two CTAs share an SM, so one
+// CTA's row gathers overlap the other's fmaf chains (R = 64 and one CTA per SM: 67 us per
+// 256 queries at k' = 256)
+static int kRerankRows = 32;
 cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64_t* cand, int B,
                           int kp, const uint64_t* part, int grid, int k, int64_t row0,
                           const float* xstats, int coarse_bf16, uint64_t* out_keys,
                           int64_t* out_ids, float* out_scores, int* flags, cudaStream_t st) {
   const size_t base = (size_t)((D + 3) & ~3) * 4 + (size_t)kp * 8;
   const size_t row = (size_t)(D + 4) * 4;
+  if (const char* e = getenv("VX_DEBUG_RERANK_ROWS")) kRerankRows = atoi(e);  // experiments
   int R = (int)((220 * 1024 - base) / row);
-  R = R > 64 ? 64 : (R < 1 ? 1 : R);
+  R = R > kRerankRows ? kRerankRows : (R < 1 ? 1 : R);
   const size_t smem = base + (size_t)R * row;
   cudaError_t e = cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);

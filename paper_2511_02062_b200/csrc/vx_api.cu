@@ -209,7 +209,11 @@ struct vx_index {
   cudaEvent_t ev[4] = {};        // eager-path timing events: scan begin/end, stage begin/end
   cudaEvent_t gev[4] = {};       // the same, recorded by captured graph nodes
   cudaEvent_t* tev = ev;         // events the code being issued records into
-  cudaEvent_t* last_tev = ev;    // events of the last issued batch (read by vx_sync)
+  cudaEvent_t* ev_start = ev;    // last batch: the array holding scan begin/end + stage begin
+  cudaEvent_t* ev_end = ev;      //   ... and the one holding the stage end (read by vx_sync)
+  cudaStream_t stream_last = nullptr;  // stream of the last batch's final part
+  cudaStream_t stream2 = nullptr;      // host API: query-token upload overlapping part 1
+  cudaEvent_t tok_ev = nullptr;
   cudaEvent_t pev[5] = {};       // sharded rank 0 phases: start, bcast done, local done,
   bool phases_pending = false;   //   gather done, end
   bool timing_pending = false;
@@ -317,7 +321,9 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
     ALLOC(h->d_q16, B * D * 2);
   }
 #undef ALLOC
-  if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess)
+  if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->tok_ev, cudaEventDisableTiming) != cudaSuccess)
     return cleanup(fail(VX_ERR_CUDA, "stream create"));
   for (auto& e : h->ev)
     if (cudaEventCreate(&e) != cudaSuccess) return cleanup(fail(VX_ERR_CUDA, "event create"));
@@ -374,6 +380,8 @@ extern "C" vx_status vx_index_destroy(vx_index* h) {
     if (e) cudaEventDestroy(e);
   for (auto& e : h->pev)
     if (e) cudaEventDestroy(e);
+  if (h->tok_ev) cudaEventDestroy(h->tok_ev);
+  if (h->stream2) cudaStreamDestroy(h->stream2);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
   return VX_OK;
@@ -766,33 +774,22 @@ __global__ void transpose_shard_kernel(const uint64_t* recv, int G, int B, int k
   }
 }
 
-// Worker and root share this: given queries (and tokens) on device, compute the local
-// candidates and, for G > 1, run the two-phase shard exchange:
-//   phase 1: every shard's certified local top-k keys -> rank 0 (grouped send/recv, 8 B per
-//            candidate: a key carries the exact fp32 score and the global id), merge to the
-//            global top-k by inner product;
-//   phase 2 (rescore): rank 0 broadcasts the B x k global winners, each shard computes
-//            MaxSim only for the winners it owns (others -INF, no token loads), and an
-//            NCCL max-reduce to rank 0 assembles the scores.  Every shard does 1/G of the
-//            MaxSim work (rescoring all local top-k would cost each shard the full B x k).
-static vx_status stage_core(vx_index* h, int op, const float* d_q, const float* d_qtok, int B,
-                            int nq, int k, int64_t* d_ids, float* d_ip, float* d_ms,
-                            cudaStream_t st) {
-  const bool rescore = (op == OP_RESCORE);
+// The stage in two parts, shared by rank 0 and the shard ranks:
+//   part 1 (core_topk): the certified local top-k by inner product into h->d_keys/d_ids/d_ip;
+//     G > 1, phase 1: every shard's local top-k KEYS -> rank 0 (grouped send/recv, 8 B per
+//     candidate: a key carries the exact fp32 score and the global id), rank 0 merges to
+//     the global top-k in the same buffers;
+//   part 2 (core_rescore): MaxSim of the top-k, output order (MaxSim desc, id asc).
+//     G > 1, phase 2: rank 0 broadcasts the query tokens and the B x k global winners, each
+//     shard computes MaxSim only for the winners it owns (others -INF, no token loads), an
+//     NCCL max-reduce to rank 0 assembles the scores.  Every shard does 1/G of the MaxSim
+//     work (rescoring each shard's whole local top-k would cost every GPU the full B x k).
+// The split lets the host API upload the query tokens while part 1 runs (they are only
+// read by part 2).
+static vx_status core_topk(vx_index* h, const float* d_q, int B, int k, cudaStream_t st) {
   VX_TRY(local_topk(h, d_q, B, k, h->d_keys, h->d_ids, h->d_ip, st));
+  if (h->nranks == 1) return VX_OK;
   const int n = B * k;
-  if (h->nranks == 1) {
-    if (rescore) {
-      VX_TRY(run_maxsim(h, d_qtok, B, nq, h->d_ids, k, h->d_ms, st));
-      CU_TRY(vx::launch_order_by(h->d_ms, h->d_ids, h->d_ip, B, k, d_ids, d_ip, d_ms, st));
-      count_launch(h);
-    } else {
-      CU_TRY(cudaMemcpyAsync(d_ids, h->d_ids, (size_t)n * 8, cudaMemcpyDeviceToDevice, st));
-      CU_TRY(cudaMemcpyAsync(d_ip, h->d_ip, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
-    }
-    return VX_OK;
-  }
-  // ---- phase 1: gather the local top-k keys to rank 0, merge
   const bool root = h->rank == 0;
   if (root) CU_TRY(cudaEventRecord(h->pev[2], st));
   const size_t bytes = (size_t)n * 8;
@@ -809,71 +806,86 @@ static vx_status stage_core(vx_index* h, int op, const float* d_q, const float* 
     NCCL_TRY(nccl().Send(h->d_keys, bytes, ncclUint8, 0, h->comm, st));
   }
   NCCL_TRY(nccl().GroupEnd());
-  if (root) {
-    const int G = h->nranks;
-    transpose_shard_kernel<<<(G * n + 255) / 256, 256, 0, st>>>(recv, G, B, k, h->d_part);
+  if (!root) return VX_OK;
+  const int G = h->nranks;
+  transpose_shard_kernel<<<(G * n + 255) / 256, 256, 0, st>>>(recv, G, B, k, h->d_part);
+  count_launch(h);
+  CU_TRY(cudaGetLastError());
+  // keys already carry global ids: id_base 0
+  CU_TRY(vx::launch_merge_topk(h->d_part, B, G * k, k, 0, h->d_keys, h->d_ids, h->d_ip, st));
+  count_launch(h);
+  CU_TRY(cudaEventRecord(h->pev[3], st));
+  return VX_OK;
+}
+
+// d_qtok: rank 0's query tokens (ignored on the shard ranks, which receive them)
+static vx_status core_rescore(vx_index* h, const float* d_qtok, int B, int nq, int k,
+                              int64_t* d_ids, float* d_ip, float* d_ms, cudaStream_t st) {
+  if (h->nranks == 1) {
+    VX_TRY(run_maxsim(h, d_qtok, B, nq, h->d_ids, k, h->d_ms, st));
+    CU_TRY(vx::launch_order_by(h->d_ms, h->d_ids, h->d_ip, B, k, d_ids, d_ip, d_ms, st));
     count_launch(h);
-    CU_TRY(cudaGetLastError());
-    // keys already carry global ids: id_base 0
-    CU_TRY(vx::launch_merge_topk(h->d_part, B, G * k, k, 0, h->d_keys, h->d_ids, h->d_ip, st));
-    count_launch(h);
-    CU_TRY(cudaEventRecord(h->pev[3], st));
-  }
-  if (!rescore) {
-    if (root) {
-      CU_TRY(cudaMemcpyAsync(d_ids, h->d_ids, (size_t)n * 8, cudaMemcpyDeviceToDevice, st));
-      CU_TRY(cudaMemcpyAsync(d_ip, h->d_ip, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
-      CU_TRY(cudaEventRecord(h->pev[4], st));
-      h->phases_pending = true;
-    }
     return VX_OK;
   }
-  // ---- phase 2: MaxSim of the global winners, each on its owner shard
+  const int n = B * k;
+  const bool root = h->rank == 0;
+  NCCL_TRY(nccl().GroupStart());
+  NCCL_TRY(nccl().Broadcast(root ? d_qtok : h->d_qtok, h->d_qtok,
+                            (size_t)B * nq * h->desc.tok_dim, ncclFloat32, 0, h->comm, st));
   NCCL_TRY(nccl().Broadcast(h->d_ids, h->d_ids, (size_t)n, ncclInt64, 0, h->comm, st));
-  VX_TRY(run_maxsim(h, d_qtok, B, nq, h->d_ids, k, h->d_ms, st, h->row0, h->row0 + h->n_local));
+  NCCL_TRY(nccl().GroupEnd());
+  VX_TRY(run_maxsim(h, h->d_qtok, B, nq, h->d_ids, k, h->d_ms, st, h->row0,
+                    h->row0 + h->n_local));
   float* ms_all = reinterpret_cast<float*>(h->d_send);  // [B][k] on rank 0
   NCCL_TRY(nccl().Reduce(h->d_ms, ms_all, (size_t)n, ncclFloat32, ncclMax, 0, h->comm, st));
   if (!root) return VX_OK;
   CU_TRY(vx::launch_order_by(ms_all, h->d_ids, h->d_ip, B, k, d_ids, d_ip, d_ms, st));
   count_launch(h);
-  CU_TRY(cudaEventRecord(h->pev[4], st));
-  h->phases_pending = true;
   return VX_OK;
 }
 
-// Rank 0 entry: announce the batch to the shards, then run the core.
-// CUDA-graph mode (VX_OPT_GRAPHS, single GPU): the whole stage for one (op, B, k, nq) is
-// captured once and replayed — one launch per batch instead of ~8, no host work between the
-// kernels (the batcher hands each batch to the graph of its size, north star (e)).  The graph
-// reads the handle's fixed input buffers and writes its fixed output buffers; user pointers
-// are copied in/out around the replay.  The first batch of a shape runs eagerly (it also
-// sets the kernels' smem attributes) and captures the graph for the next ones.
-static vx_status stage_graph(vx_index* h, int op, const float* d_q, const float* d_qtok, int B,
-                             int nq, int k, int64_t* d_ids, float* d_ip, float* d_ms,
-                             cudaStream_t st) {
-  const size_t D = h->desc.dim, td = h->desc.tok_dim;
-  if (d_q != h->d_q)
-    CU_TRY(cudaMemcpyAsync(h->d_q, d_q, (size_t)B * D * 4, cudaMemcpyDeviceToDevice, st));
-  if (op == OP_RESCORE && d_qtok != h->d_qtok)
-    CU_TRY(cudaMemcpyAsync(h->d_qtok, d_qtok, (size_t)B * nq * td * 4, cudaMemcpyDeviceToDevice,
-                           st));
-  const uint64_t key = ((uint64_t)op << 48) | ((uint64_t)B << 24) | ((uint64_t)k << 12) | (uint64_t)nq;
-  auto it = h->graphs.find(key);
-  if (it == h->graphs.end()) {
+// CUDA-graph mode (VX_OPT_GRAPHS, single GPU): each part for one (B, k[, nq]) is captured
+// once and replayed — one launch per part instead of ~12 kernels, no host work between the
+// kernels (the batcher hands each batch to the graphs of its size, north star (e)).  The
+// graphs read the handle's fixed input buffers and write its fixed output buffers; user
+// pointers are copied in/out around the replay.  The first batch of a shape runs the part
+// eagerly (it also sets the kernels' smem attributes) and captures it for the next ones.
+enum { PART_TOPK = 1, PART_RESCORE = 2 };
+
+static vx_status part_body(vx_index* h, int part, int B, int nq, int k, cudaStream_t st) {
+  if (part == PART_TOPK) {
     CU_TRY(record_ev(h, h->tev[2], st));
-    VX_TRY(stage_core(h, op, h->d_q, h->d_qtok, B, nq, k, h->d_out_ids, h->d_out_ip, h->d_out_ms, st));
-    CU_TRY(record_ev(h, h->tev[3], st));
-    // capture on the handle's stream (after the eager run completes: capture records, it
+    VX_TRY(core_topk(h, h->d_q, B, k, st));
+  } else {
+    VX_TRY(core_rescore(h, h->d_qtok, B, nq, k, h->d_out_ids, h->d_out_ip, h->d_out_ms, st));
+  }
+  CU_TRY(record_ev(h, h->tev[3], st));
+  return VX_OK;
+}
+
+static uint64_t part_key(int part, int B, int nq, int k) {
+  return ((uint64_t)part << 48) | ((uint64_t)B << 24) | ((uint64_t)k << 12) |
+         (uint64_t)(part == PART_RESCORE ? nq : 0);
+}
+
+static vx_status run_part(vx_index* h, int part, int B, int nq, int k, cudaStream_t st) {
+  const uint64_t key = part_key(part, B, nq, k);
+  cudaEvent_t* used;
+  auto it = h->graphs.find(key);
+  if (it != h->graphs.end()) {
+    CU_TRY(cudaGraphLaunch(it->second.exec, st));
+    h->st.kernel_launches += it->second.launches;
+    h->st.graph_replays += 1;
+    used = h->gev;
+  } else {
+    VX_TRY(part_body(h, part, B, nq, k, st));
+    // capture on the handle's stream after the eager run completes (capture records, it
     // does not execute)
     CU_TRY(cudaStreamSynchronize(st));
     const uint64_t before = h->st.kernel_launches;
-    h->last_tev = h->ev;  // this call's timing: the eager run
-    h->tev = h->gev;      // the graph records its own events
+    h->tev = h->gev;  // the graph records its own (external) events
     CU_TRY(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-    record_ev(h, h->tev[2], h->stream);
-    vx_status s = stage_core(h, op, h->d_q, h->d_qtok, B, nq, k, h->d_out_ids, h->d_out_ip,
-                             h->d_out_ms, h->stream);
-    record_ev(h, h->tev[3], h->stream);
+    vx_status s = part_body(h, part, B, nq, k, h->stream);
     cudaGraph_t g = nullptr;
     cudaError_t e = cudaStreamEndCapture(h->stream, &g);
     h->tev = h->ev;
@@ -889,25 +901,16 @@ static vx_status stage_graph(vx_index* h, int op, const float* d_q, const float*
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return fail(VX_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
     h->graphs[key] = {ex, launches};
-  } else {
-    CU_TRY(cudaGraphLaunch(it->second.exec, st));
-    h->st.kernel_launches += it->second.launches;
-    h->st.graph_replays += 1;
-    h->last_tev = h->gev;
+    used = h->ev;  // this call's timing: the eager run
   }
-  const size_t n = (size_t)B * k;
-  if (d_ids != h->d_out_ids)
-    CU_TRY(cudaMemcpyAsync(d_ids, h->d_out_ids, n * 8, cudaMemcpyDeviceToDevice, st));
-  if (d_ip != h->d_out_ip)
-    CU_TRY(cudaMemcpyAsync(d_ip, h->d_out_ip, n * 4, cudaMemcpyDeviceToDevice, st));
-  if (op == OP_RESCORE && d_ms != h->d_out_ms)
-    CU_TRY(cudaMemcpyAsync(d_ms, h->d_out_ms, n * 4, cudaMemcpyDeviceToDevice, st));
+  if (part == PART_TOPK) h->ev_start = used;
+  h->ev_end = used;
   return VX_OK;
 }
 
-static vx_status stage_root(vx_index* h, int op, const float* d_q, const float* d_qtok, int B,
-                            int nq, int k, int64_t* d_ids, float* d_ip, float* d_ms,
-                            cudaStream_t st) {
+// Rank 0 entry, part 1: announce the batch to the shards (header, queries), then top-k.
+static vx_status stage_begin(vx_index* h, int op, const float* d_q, int B, int nq, int k,
+                             cudaStream_t st) {
   if (h->nranks > 1) {
     if (h->rank != 0) return fail(VX_ERR_STATE, "only rank 0 issues searches; call vx_shard_serve");
     h->h_hdr[0] = op;
@@ -917,25 +920,66 @@ static vx_status stage_root(vx_index* h, int op, const float* d_q, const float* 
     CU_TRY(cudaEventRecord(h->pev[0], st));
     CU_TRY(cudaMemcpyAsync(h->d_hdr, h->h_hdr, 16, cudaMemcpyHostToDevice, st));
     NCCL_TRY(nccl().Broadcast(h->d_hdr, h->d_hdr, 4, ncclInt32, 0, h->comm, st));
-    NCCL_TRY(nccl().GroupStart());
     NCCL_TRY(nccl().Broadcast(d_q, h->d_q, (size_t)B * h->desc.dim, ncclFloat32, 0, h->comm, st));
-    if (op == OP_RESCORE)
-      NCCL_TRY(nccl().Broadcast(d_qtok, h->d_qtok, (size_t)B * nq * h->desc.tok_dim, ncclFloat32, 0,
-                             h->comm, st));
-    NCCL_TRY(nccl().GroupEnd());
     CU_TRY(cudaEventRecord(h->pev[1], st));
   }
   if (h->use_graphs && h->nranks == 1) {
-    VX_TRY(stage_graph(h, op, d_q, d_qtok, B, nq, k, d_ids, d_ip, d_ms, st));
+    if (d_q != h->d_q)
+      CU_TRY(cudaMemcpyAsync(h->d_q, d_q, (size_t)B * h->desc.dim * 4, cudaMemcpyDeviceToDevice,
+                             st));
+    VX_TRY(run_part(h, PART_TOPK, B, nq, k, st));
   } else {
     CU_TRY(record_ev(h, h->tev[2], st));
-    VX_TRY(stage_core(h, op, d_q, d_qtok, B, nq, k, d_ids, d_ip, d_ms, st));
+    VX_TRY(core_topk(h, d_q, B, k, st));
     CU_TRY(record_ev(h, h->tev[3], st));
-    h->last_tev = h->ev;
+    h->ev_start = h->ev_end = h->ev;
+  }
+  return VX_OK;
+}
+
+static void stage_done(vx_index* h, int B) {
+  if (h->nranks > 1 && h->rank == 0) {
+    cudaEventRecord(h->pev[4], h->stream_last);
+    h->phases_pending = true;
   }
   h->timing_pending = true;
   h->st.batches += 1;
   h->st.queries += B;
+}
+
+// part 2 of a search (no rescore): the top-k by inner product to the caller's buffers
+static vx_status stage_search_out(vx_index* h, int B, int k, int64_t* d_ids, float* d_ip,
+                                  cudaStream_t st) {
+  const size_t n = (size_t)B * k;
+  CU_TRY(cudaMemcpyAsync(d_ids, h->d_ids, n * 8, cudaMemcpyDeviceToDevice, st));
+  CU_TRY(cudaMemcpyAsync(d_ip, h->d_ip, n * 4, cudaMemcpyDeviceToDevice, st));
+  h->stream_last = st;
+  stage_done(h, B);
+  return VX_OK;
+}
+
+// part 2 of the fused stage: MaxSim rescore + order into the caller's buffers
+static vx_status stage_finish(vx_index* h, const float* d_qtok, int B, int nq, int k,
+                              int64_t* d_ids, float* d_ip, float* d_ms, cudaStream_t st) {
+  if (h->use_graphs && h->nranks == 1) {
+    if (d_qtok != h->d_qtok)
+      CU_TRY(cudaMemcpyAsync(h->d_qtok, d_qtok, (size_t)B * nq * h->desc.tok_dim * 4,
+                             cudaMemcpyDeviceToDevice, st));
+    VX_TRY(run_part(h, PART_RESCORE, B, nq, k, st));
+    const size_t n = (size_t)B * k;
+    if (d_ids != h->d_out_ids)
+      CU_TRY(cudaMemcpyAsync(d_ids, h->d_out_ids, n * 8, cudaMemcpyDeviceToDevice, st));
+    if (d_ip != h->d_out_ip)
+      CU_TRY(cudaMemcpyAsync(d_ip, h->d_out_ip, n * 4, cudaMemcpyDeviceToDevice, st));
+    if (d_ms != h->d_out_ms)
+      CU_TRY(cudaMemcpyAsync(d_ms, h->d_out_ms, n * 4, cudaMemcpyDeviceToDevice, st));
+  } else {
+    VX_TRY(core_rescore(h, d_qtok, B, nq, k, d_ids, d_ip, d_ms, st));
+    CU_TRY(record_ev(h, h->tev[3], st));
+    h->ev_end = h->ev;
+  }
+  h->stream_last = st;
+  stage_done(h, B);
   return VX_OK;
 }
 
@@ -944,8 +988,9 @@ extern "C" vx_status vx_search_dev(vx_index* h, const float* d_q, int32_t B, int
   if (!h || !d_q || !d_ids || !d_scores) return fail(VX_ERR_INVALID, "null argument");
   VX_TRY(check_batch(h, B, k));
   CU_TRY(cudaSetDevice(h->device));
-  return stage_root(h, OP_SEARCH, d_q, nullptr, B, 0, k, d_ids, d_scores, nullptr,
-                    pick_stream(h, stream));
+  cudaStream_t st = pick_stream(h, stream);
+  VX_TRY(stage_begin(h, OP_SEARCH, d_q, B, 0, k, st));
+  return stage_search_out(h, B, k, d_ids, d_scores, st);
 }
 
 extern "C" vx_status vx_search_rescore_dev(vx_index* h, const float* d_q, const float* d_qtok,
@@ -956,8 +1001,9 @@ extern "C" vx_status vx_search_rescore_dev(vx_index* h, const float* d_q, const 
   if (!h->tokens) return fail(VX_ERR_STATE, "index has no token store");
   if (nq < 1 || nq > h->desc.max_qtok) return fail(VX_ERR_INVALID, "nq %d", nq);
   CU_TRY(cudaSetDevice(h->device));
-  return stage_root(h, OP_RESCORE, d_q, d_qtok, B, nq, k, d_ids, d_ip, d_ms,
-                    pick_stream(h, stream));
+  cudaStream_t st = pick_stream(h, stream);
+  VX_TRY(stage_begin(h, OP_RESCORE, d_q, B, nq, k, st));
+  return stage_finish(h, d_qtok, B, nq, k, d_ids, d_ip, d_ms, st);
 }
 
 extern "C" vx_status vx_maxsim_dev(vx_index* h, const float* d_qtok, int32_t B, int32_t nq,
@@ -984,11 +1030,10 @@ extern "C" vx_status vx_prepare(vx_index* h, int32_t op, int32_t k, int32_t nq, 
     CU_TRY(vx::launch_synth_rows(h->d_qtok, 0x5eed1ull, 0, (int64_t)b_max * nq, h->desc.tok_dim, st));
   const vx_stats saved = h->st;
   for (int B = 1; B <= b_max; ++B) {
-    const uint64_t key = ((uint64_t)(rescore ? OP_RESCORE : OP_SEARCH) << 48) | ((uint64_t)B << 24) |
-                         ((uint64_t)k << 12) | (uint64_t)(rescore ? nq : 0);
-    if (h->graphs.count(key)) continue;
-    VX_TRY(stage_graph(h, rescore ? OP_RESCORE : OP_SEARCH, h->d_q, h->d_qtok, B,
-                       rescore ? nq : 0, k, h->d_out_ids, h->d_out_ip, h->d_out_ms, st));
+    if (!h->graphs.count(part_key(PART_TOPK, B, 0, k)))
+      VX_TRY(run_part(h, PART_TOPK, B, 0, k, st));
+    if (rescore && !h->graphs.count(part_key(PART_RESCORE, B, nq, k)))
+      VX_TRY(run_part(h, PART_RESCORE, B, nq, k, st));
   }
   CU_TRY(cudaStreamSynchronize(st));
   h->st = saved;  // preload work is not serving work
@@ -1001,11 +1046,12 @@ extern "C" vx_status vx_sync(vx_index* h) {
   CU_TRY(cudaSetDevice(h->device));
   CU_TRY(cudaStreamSynchronize(h->stream));
   if (h->timing_pending) {
-    cudaEvent_t* E = h->last_tev;
-    CU_TRY(cudaEventSynchronize(E[3]));
+    cudaEvent_t* E = h->ev_start;
+    cudaEvent_t* F = h->ev_end;
+    CU_TRY(cudaEventSynchronize(F[3]));
     float a = 0, b = 0;
     if (cudaEventElapsedTime(&a, E[0], E[1]) == cudaSuccess &&
-        cudaEventElapsedTime(&b, E[2], E[3]) == cudaSuccess) {
+        cudaEventElapsedTime(&b, E[2], F[3]) == cudaSuccess) {
       h->st.last_scan_ms = a;
       h->st.last_step_ms = b;
       h->st.scan_ms_total += a;
@@ -1041,7 +1087,8 @@ extern "C" vx_status vx_search(vx_index* h, const float* q, int32_t B, int32_t k
   uint8_t* stage = static_cast<uint8_t*>(h->h_stage);
   memcpy(stage, q, qb);
   CU_TRY(cudaMemcpyAsync(h->d_q, stage, qb, cudaMemcpyHostToDevice, st));
-  VX_TRY(stage_root(h, OP_SEARCH, h->d_q, nullptr, B, 0, k, h->d_out_ids, h->d_out_ip, nullptr, st));
+  VX_TRY(stage_begin(h, OP_SEARCH, h->d_q, B, 0, k, st));
+  VX_TRY(stage_search_out(h, B, k, h->d_out_ids, h->d_out_ip, st));
   int64_t* hid = reinterpret_cast<int64_t*>(stage);
   float* hsc = reinterpret_cast<float*>(stage + (size_t)B * k * 8);
   CU_TRY(cudaMemcpyAsync(hid, h->d_out_ids, (size_t)B * k * 8, cudaMemcpyDeviceToHost, st));
@@ -1087,11 +1134,14 @@ extern "C" vx_status vx_search_rescore(vx_index* h, const float* q, const float*
   const size_t qb = (size_t)B * h->desc.dim * 4, tb = (size_t)B * nq * h->desc.tok_dim * 4;
   uint8_t* stage = static_cast<uint8_t*>(h->h_stage);
   memcpy(stage, q, qb);
-  memcpy(stage + qb, qtok, tb);
   CU_TRY(cudaMemcpyAsync(h->d_q, stage, qb, cudaMemcpyHostToDevice, st));
-  CU_TRY(cudaMemcpyAsync(h->d_qtok, stage + qb, tb, cudaMemcpyHostToDevice, st));
-  VX_TRY(stage_root(h, OP_RESCORE, h->d_q, h->d_qtok, B, nq, k, h->d_out_ids, h->d_out_ip,
-                    h->d_out_ms, st));
+  VX_TRY(stage_begin(h, OP_RESCORE, h->d_q, B, nq, k, st));
+  // the query tokens are only read by part 2: stage + upload them while part 1 runs
+  memcpy(stage + qb, qtok, tb);
+  CU_TRY(cudaMemcpyAsync(h->d_qtok, stage + qb, tb, cudaMemcpyHostToDevice, h->stream2));
+  CU_TRY(cudaEventRecord(h->tok_ev, h->stream2));
+  CU_TRY(cudaStreamWaitEvent(st, h->tok_ev, 0));
+  VX_TRY(stage_finish(h, h->d_qtok, B, nq, k, h->d_out_ids, h->d_out_ip, h->d_out_ms, st));
   const size_t n = (size_t)B * k;
   CU_TRY(cudaMemcpyAsync(stage, h->d_out_ids, n * 8, cudaMemcpyDeviceToHost, st));
   CU_TRY(cudaMemcpyAsync(stage + n * 8, h->d_out_ip, n * 4, cudaMemcpyDeviceToHost, st));
@@ -1154,8 +1204,11 @@ extern "C" vx_status vx_serve_trace(vx_index* h, const uint64_t* arrivals_us, in
       for (int i = 0; i < B; ++i) memcpy(ts + i * tb, qtok + batch[i] * nq * td, tb);
       CU_TRY(cudaMemcpyAsync(h->d_qtok, ts, (size_t)B * tb, cudaMemcpyHostToDevice, st));
     }
-    VX_TRY(stage_root(h, rescore ? OP_RESCORE : OP_SEARCH, h->d_q, h->d_qtok, B, nq, k,
-                      h->d_out_ids, h->d_out_ip, h->d_out_ms, st));
+    VX_TRY(stage_begin(h, rescore ? OP_RESCORE : OP_SEARCH, h->d_q, B, nq, k, st));
+    if (rescore)
+      VX_TRY(stage_finish(h, h->d_qtok, B, nq, k, h->d_out_ids, h->d_out_ip, h->d_out_ms, st));
+    else
+      VX_TRY(stage_search_out(h, B, k, h->d_out_ids, h->d_out_ip, st));
     int64_t* hid = reinterpret_cast<int64_t*>(stage);
     CU_TRY(cudaMemcpyAsync(hid, h->d_out_ids, (size_t)B * k * 8, cudaMemcpyDeviceToHost, st));
     VX_TRY(vx_sync(h));
@@ -1214,14 +1267,12 @@ extern "C" vx_status vx_shard_serve(vx_index* h) {
     if (op == OP_STOP) return VX_OK;
     if (B < 1 || B > h->desc.max_batch || k < 1 || k > h->desc.max_k)
       return fail(VX_ERR_STATE, "bad batch header %d/%d/%d", op, B, k);
-    NCCL_TRY(nccl().GroupStart());
+    if (op == OP_RESCORE && (nq < 1 || nq > h->desc.max_qtok))
+      return fail(VX_ERR_STATE, "bad batch header nq %d", nq);
     NCCL_TRY(nccl().Broadcast(h->d_q, h->d_q, (size_t)B * h->desc.dim, ncclFloat32, 0, h->comm, st));
-    if (op == OP_RESCORE)
-      NCCL_TRY(nccl().Broadcast(h->d_qtok, h->d_qtok, (size_t)B * nq * h->desc.tok_dim, ncclFloat32,
-                             0, h->comm, st));
-    NCCL_TRY(nccl().GroupEnd());
-    VX_TRY(stage_core(h, op, h->d_q, h->d_qtok, B, nq, k, h->d_out_ids, h->d_out_ip, h->d_out_ms,
-                      st));
+    VX_TRY(core_topk(h, h->d_q, B, k, st));
+    if (op == OP_RESCORE)  // phase 2: receives the tokens + winners, MaxSim on owned winners
+      VX_TRY(core_rescore(h, nullptr, B, nq, k, h->d_out_ids, h->d_out_ip, h->d_out_ms, st));
     h->st.batches += 1;
     h->st.queries += B;
   }
