@@ -272,7 +272,7 @@ __device__ __forceinline__ float cert_err_bound(int coarse_bf16, float qn, float
 __global__ void __launch_bounds__(256)
     rerank_kernel(const float* __restrict__ docs, const float* __restrict__ qv, int D,
                   const uint64_t* __restrict__ cand, int kp, const uint64_t* __restrict__ part,
-                  int grid, int k, int64_t row0, const float* __restrict__ xstats,
+                  int grid, int ldlists, int k, int64_t row0, const float* __restrict__ xstats,
                   int coarse_bf16,
                   uint64_t* __restrict__ out_keys, int64_t* __restrict__ out_ids,
                   float* __restrict__ out_scores, int* __restrict__ flags, int rows_per_round) {
@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(256)
   }
   // certificate 1: no CTA that truncated its list (16 kept) had its 16th key inside the top-k'
   for (int t = threadIdx.x; t < grid; t += blockDim.x) {
-    const uint64_t last = part[((size_t)b * grid + t) * kTcKC + (kTcKC - 1)];
+    const uint64_t last = part[((size_t)b * ldlists + t) * kTcKC + (kTcKC - 1)];
     if (last != 0ull && (tprime == 0ull || last >= tprime)) s_fail = 1;
   }
   __syncthreads();
@@ -435,7 +435,8 @@ __global__ void __launch_bounds__(256)
   const int g0 = (b / GS) * GS, Bg = min(GS, B - g0);
   const int P = (P_pairs > 0 && Bg > 128) ? P_pairs : P_single;
   const int M = P * kTcKC;
-  const uint64_t* lists = part_all + (size_t)g0 * (size_t)P_single * kTcKC + (size_t)(b - g0) * M;
+  // every query's lists start at a stride of P_single lists (K2 / K2-pairs share it)
+  const uint64_t* lists = part_all + (size_t)b * P_single * kTcKC;
   int np2 = 16;
   while (np2 < M) np2 <<= 1;
   float* qs = wsm;                                                      // [D]
@@ -632,7 +633,8 @@ cudaError_t launch_scan_tc(int QT, int TD, const CUtensorMap* tq, const CUtensor
 // 256 queries at k' = 256)
 static int kRerankRows = 32;
 cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64_t* cand, int B,
-                          int kp, const uint64_t* part, int grid, int k, int64_t row0,
+                          int kp, const uint64_t* part, int grid, int ldlists, int k,
+                          int64_t row0,
                           const float* xstats, int coarse_bf16, uint64_t* out_keys,
                           int64_t* out_ids, float* out_scores, int* flags, cudaStream_t st) {
   const size_t base = (size_t)((D + 3) & ~3) * 4 + (size_t)kp * 8;
@@ -644,7 +646,7 @@ cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64
   cudaError_t e = cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  rerank_kernel<<<B, 256, smem, st>>>(docs, q, D, cand, kp, part, grid, k, row0, xstats,
+  rerank_kernel<<<B, 256, smem, st>>>(docs, q, D, cand, kp, part, grid, ldlists, k, row0, xstats,
                                       coarse_bf16, out_keys, out_ids, out_scores, flags, R);
   return cudaGetLastError();
 }

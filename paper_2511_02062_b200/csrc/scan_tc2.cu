@@ -275,7 +275,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P2Cfg<QG>::kThreads,
       }
     }
     if (q < a.B) {
-      uint64_t* out = a.part + ((size_t)q * npairs + pair) * kP2KC;
+      // per-query stride = gridDim.x lists (the single-CTA kernel's layout): every query
+      // group of a batch shares one layout, so one merge / re-rank launch covers the batch
+      uint64_t* out = a.part + ((size_t)q * gridDim.x + pair) * kP2KC;
 #pragma unroll
       for (int j = 0; j < kP2KC; ++j) out[j] = L[j];
     }

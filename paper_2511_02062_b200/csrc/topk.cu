@@ -37,7 +37,7 @@ __device__ __forceinline__ void block_bitonic_desc(uint64_t* buf, int n) {
 }
 
 __global__ void __launch_bounds__(kMergeThreads)
-    merge_topk_kernel(const uint64_t* __restrict__ in, int M, int k, int64_t id_base,
+    merge_topk_kernel(const uint64_t* __restrict__ in, int M, int64_t ldin, int k, int64_t id_base,
                       uint64_t* __restrict__ out_keys, int64_t* __restrict__ out_ids,
                       float* __restrict__ out_scores, const int* __restrict__ d_count) {
   if (d_count && (int)blockIdx.x >= *d_count) return;  // device-sized batch (cert fallback)
@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(kMergeThreads)
   __shared__ uint64_t s_prefix, s_mask;
   __shared__ int s_kk, s_done, s_above, s_eq;
   __shared__ uint64_t sel[kMaxK];
-  const uint64_t* L = in + (size_t)blockIdx.x * M;
+  const uint64_t* L = in + (size_t)blockIdx.x * ldin;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
   uint64_t prefix = 0, mask = 0;
@@ -160,10 +160,10 @@ __global__ void __launch_bounds__(kMergeThreads)
 
 cudaError_t launch_merge_topk(const uint64_t* in, int B, int M, int k, int64_t id_base,
                               uint64_t* out_keys, int64_t* out_ids, float* out_scores,
-                              cudaStream_t st, const int* d_count) {
+                              cudaStream_t st, const int* d_count, int64_t ldin) {
   if (k < 1 || k > kMaxK || M < k) return cudaErrorInvalidValue;
-  merge_topk_kernel<<<B, kMergeThreads, 0, st>>>(in, M, k, id_base, out_keys, out_ids,
-                                                 out_scores, d_count);
+  merge_topk_kernel<<<B, kMergeThreads, 0, st>>>(in, M, ldin > 0 ? ldin : M, k, id_base,
+                                                 out_keys, out_ids, out_scores, d_count);
   return cudaGetLastError();
 }
 

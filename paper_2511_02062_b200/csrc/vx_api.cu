@@ -680,19 +680,28 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
     count_launch(h);
   }
   CU_TRY(record_ev(h, h->tev[1], st));
-  // per query group: merge its lists (P per query) to the coarse top-k', exact re-rank
-  for (int g0 = 0; g0 < B; g0 += GS) {
-    const int Bg = std::min(GS, B - g0);
-    const int P = (pairs && Bg > 128) ? grid / 2 : grid;
-    const uint64_t* part = h->d_part + (size_t)g0 * grid * vx::kTcListLen;
-    uint64_t* ck = h->d_ckeys + (size_t)g0 * kp;
-    CU_TRY(vx::launch_merge_topk(part, Bg, P * vx::kTcListLen, kp, 0, ck, nullptr, nullptr, st));
+  // merge each query's lists (P per query, stride grid lists) to the coarse top-k', exact
+  // re-rank — one launch each per run of query groups with the same P (the whole batch
+  // when every group ran on CTA pairs), so the 2-per-SM re-rank CTAs pack full waves
+  const int ldp = grid * vx::kTcListLen;
+  for (int r0 = 0; r0 < B;) {
+    const int P = (pairs && std::min(GS, B - r0) > 128) ? grid / 2 : grid;
+    int r1 = r0;
+    while (r1 < B && ((pairs && std::min(GS, B - r1) > 128) ? grid / 2 : grid) == P) r1 += GS;
+    r1 = std::min(r1, B);
+    const int Bn = r1 - r0;
+    const uint64_t* part = h->d_part + (size_t)r0 * ldp;
+    uint64_t* ck = h->d_ckeys + (size_t)r0 * kp;
+    CU_TRY(vx::launch_merge_topk(part, Bn, P * vx::kTcListLen, kp, 0, ck, nullptr, nullptr, st,
+                                 nullptr, ldp));
     count_launch(h);
-    CU_TRY(vx::launch_rerank(h->docs, d_q + (size_t)g0 * D, D, ck, Bg, kp, part, P, k, h->row0,
+    CU_TRY(vx::launch_rerank(h->docs, d_q + (size_t)r0 * D, D, ck, Bn, kp, part, P, grid, k,
+                             h->row0,
                              reinterpret_cast<const float*>(h->d_xnorm), bf16 ? 1 : 0,
-                             keys + (size_t)g0 * k,
-                             ids + (size_t)g0 * k, scores + (size_t)g0 * k, h->d_flags + g0, st));
+                             keys + (size_t)r0 * k, ids + (size_t)r0 * k,
+                             scores + (size_t)r0 * k, h->d_flags + r0, st));
     count_launch(h);
+    r0 = r1;
   }
   // Certificate failures, entirely on device (no host round trip: the stage stays
   // capturable in one CUDA graph; every launch below exits at once when its count is 0):

@@ -57,7 +57,8 @@ size_t scan_tc2_smem(int H, int* ns_out);
 cudaError_t launch_scan_tc2(int H, const CUtensorMap* tq, const CUtensorMap* tx,
                             const ScanTcArgs& a, int grid, size_t smem, cudaStream_t st);
 cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64_t* cand, int B,
-                          int kp, const uint64_t* part, int grid, int k, int64_t row0,
+                          int kp, const uint64_t* part, int grid, int ldlists, int k,
+                          int64_t row0,
                           const float* xstats, int coarse_bf16, uint64_t* out_keys,
                           int64_t* out_ids, float* out_scores, int* flags, cudaStream_t st);
 // second certificate level over the full per-CTA lists (compacted failing queries)
@@ -74,9 +75,10 @@ cudaError_t launch_row_stats(const float* docs, int64_t n, int D, unsigned int* 
 // -------- top-k merge (K3): topk.cu
 // For each query q: select the k largest keys among in[q][0..M), write them
 // descending to out_keys[q][k] (re-keyed with id + id_base), ids (-1 for empty) and scores.
+// ldin: keys between consecutive queries' candidate lists (0: M, i.e. contiguous)
 cudaError_t launch_merge_topk(const uint64_t* in, int B, int M, int k, int64_t id_base,
                               uint64_t* out_keys, int64_t* out_ids, float* out_scores,
-                              cudaStream_t st, const int* d_count = nullptr);
+                              cudaStream_t st, const int* d_count = nullptr, int64_t ldin = 0);
 // Certificate failures (flags[B]) -> compacted list fidx/fcount and the flagged query rows
 // gathered into fq; after the exact re-scan, scatter its [fcount][k] results back.
 cudaError_t launch_cert_compact(const int* flags, int B, const float* q, int D, int* fidx,
