@@ -628,10 +628,11 @@ cudaError_t launch_scan_tc(int QT, int TD, const CUtensorMap* tq, const CUtensor
   return cudaErrorInvalidValue;
 }
 
-// rows per staging round: 32 rows (~100 KB of smem) lets two CTAs share an SM, so one
-// CTA's row gathers overlap the other's fmaf chains (R = 64 and one CTA per SM: 67 us per
-// 256 queries at k' = 256)
-static int kRerankRows = 32;
+// rows per staging round: 16 rows (~54 KB of smem) lets four CTAs share an SM, so the
+// CTAs' row gathers overlap each other's fmaf chains.  Measured at B = 1024, k' = 256
+// (one launch): R = 8/10/12/14/16/21/24/32: - / 255 / 222 / 201 / 179 / 221 / 251 / 208 us
+// (R = 64, one CTA per SM: 4 x 67 us)
+static int kRerankRows = 16;
 cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64_t* cand, int B,
                           int kp, const uint64_t* part, int grid, int ldlists, int k,
                           int64_t row0,
