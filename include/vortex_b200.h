@@ -181,6 +181,16 @@ vx_status vx_batcher_simulate(const uint64_t* arrivals_us, int64_t n, int32_t ca
                               const int32_t* knot_batch, const double* knot_ms, int32_t n_knots,
                               int64_t* batch_of, uint64_t* dispatch_us, uint64_t* complete_us,
                               int64_t* n_batches);
+/* Replica mode: `replicas` members of the stage, each batching as above, with the
+ * reference's routing in front (Runtime::pick_member, runtime.hpp:522-536: power of two
+ * choices on outstanding tags, ties to the lower index, draws from std::mt19937_64(seed) —
+ * the runtime's seed is 7, runtime.hpp:188).  Per query: instance, dispatch and
+ * completion time (us); n_batches counts batches over all instances. */
+vx_status vx_batcher_simulate_replicas(const uint64_t* arrivals_us, int64_t n, int32_t replicas,
+                                       int32_t cap, const int32_t* knot_batch,
+                                       const double* knot_ms, int32_t n_knots, uint64_t seed,
+                                       int32_t* instance_of, uint64_t* dispatch_us,
+                                       uint64_t* complete_us, int64_t* n_batches);
 /* vx_serve_trace: live mode — replays the arrival trace in wall-clock time through the
  * same batcher onto this handle's GPU stage (one batch in flight; each dispatched batch
  * is copied host->device, searched (and re-scored when qtok != NULL), and its results

@@ -9,6 +9,12 @@
 //       times relative to the first instant after the warm model load.
 //       (runtime.hpp:617-672, executor.hpp:172-182, profile.hpp:90-109)
 //
+//   vortex_ref_driver replicas <arrivals.txt> <cap> <b:ms,...> <R>
+//       The same stage with R members (R nodes, one instance each): the reference routes
+//       every query with Runtime::pick_member (power of two choices on outstanding tags,
+//       runtime.hpp:522-536, RNG seed RuntimeOptions::seed = 7) and each member batches on
+//       its own.  Prints per query: "<index> <instance> <dispatch_us> <complete_us>".
+//
 //   vortex_ref_driver operator <N> <D> <k> <B> <nq> <T>
 //       Registers the B200 stage (include/vortex_b200_component.hpp over
 //       libvortex_b200.so) as "modelD" in the reference Runtime and pushes B synthetic
@@ -51,13 +57,15 @@ struct World {
   std::map<std::string, std::vector<exec::Instance*>> pools;
   runtime::PipelineSpec spec;
 
-  World(int cap, const std::vector<std::pair<int, double>>& knots) {
+  World(int cap, const std::vector<std::pair<int, double>>& knots, int replicas = 1) {
     for (auto [b, ms] : knots) prof.add("modelD", 24, exec::ProfileEntry{b, ms, 1000.0 * b / ms, 1});
     ex = std::make_unique<exec::SimExecutor>(loop, prof);
     rt = std::make_unique<runtime::Runtime>(loop, store, handlers, *ex);
-    int node = ex->add_node(24);
-    ex->partition_node(node, exec::MIGLayout{{24}});
-    pools["modelD"] = {&ex->instance(node, 0)};
+    for (int r = 0; r < replicas; ++r) {
+      int node = ex->add_node(24);
+      ex->partition_node(node, exec::MIGLayout{{24}});
+      pools["modelD"].push_back(&ex->instance(node, 0));
+    }
     spec.name = "search";
     spec.stages = {{"D", "modelD", cap, {}, {}}};
     spec.ingress = "D";
@@ -94,6 +102,32 @@ static int run_batcher(int argc, char** argv) {
     const auto& rec = w.rt->record("search", qid);
     const auto& tr = rec.stages.at("D");
     std::printf("%d %d %llu %llu\n", i, batch_of[i], (unsigned long long)(tr.dispatch - t0),
+                (unsigned long long)(rec.egress_ts - t0));
+  }
+  return 0;
+}
+
+static int run_replicas(int argc, char** argv) {
+  if (argc < 6) return 2;
+  std::ifstream in(argv[2]);
+  std::vector<sim::micros> arr;
+  for (unsigned long long t; in >> t;) arr.push_back(t);
+  const int cap = std::atoi(argv[3]);
+  const int R = std::atoi(argv[5]);
+  World w(cap, parse_knots(argv[4]), R);
+  w.rt->register_component("modelD", [](const std::vector<Payload>& inputs) { return inputs; });
+  w.rt->load_pipeline(w.spec, w.pools);
+  const sim::micros t0 = w.loop.now();
+  std::map<std::uint64_t, int> qid_of;
+  for (size_t i = 0; i < arr.size(); ++i)
+    w.loop.at(t0 + arr[i], [&, i] {
+      qid_of[w.rt->ingress_submit("search", make_payload(std::to_string(i)))] = (int)i;
+    });
+  w.loop.run_all();
+  for (const auto& [qid, i] : qid_of) {
+    const auto& rec = w.rt->record("search", qid);
+    const auto& tr = rec.stages.at("D");
+    std::printf("%d %d %llu %llu\n", i, tr.instance, (unsigned long long)(tr.dispatch - t0),
                 (unsigned long long)(rec.egress_ts - t0));
   }
   return 0;
@@ -170,6 +204,7 @@ int main(int argc, char** argv) {
   std::string mode = argv[1];
   try {
     if (mode == "batcher") return run_batcher(argc, argv);
+    if (mode == "replicas") return run_replicas(argc, argv);
 #ifdef VX_WITH_B200
     if (mode == "operator") return run_operator(argc, argv);
 #endif

@@ -81,6 +81,29 @@ def simulate(arrivals_us, cap: int, knots: dict[int, float]):
     return bo, du, cu
 
 
+def simulate_replicas(arrivals_us, replicas: int, cap: int, knots: dict[int, float],
+                      seed: int = 7):
+    """Replica mode on the virtual clock: `replicas` members behind the reference's
+    power-of-two-choices router (runtime.hpp:522-536; seed 7 = RuntimeOptions::seed).
+    Returns (instance_of, dispatch_us, complete_us, n_batches)."""
+    lib = _lib.load()
+    a = np.ascontiguousarray(arrivals_us, np.uint64)
+    n = a.shape[0]
+    kb = np.array(sorted(knots), np.int32)
+    km = np.array([knots[b] for b in sorted(knots)], np.float64)
+    io = np.empty(n, np.int32)
+    du = np.empty(n, np.uint64)
+    cu = np.empty(n, np.uint64)
+    nb = C.c_int64()
+    U64P = C.POINTER(C.c_uint64)
+    check(lib.vx_batcher_simulate_replicas(
+        a.ctypes.data_as(U64P), n, replicas, cap, kb.ctypes.data_as(C.POINTER(C.c_int32)),
+        km.ctypes.data_as(C.POINTER(C.c_double)), kb.shape[0], seed,
+        io.ctypes.data_as(C.POINTER(C.c_int32)), du.ctypes.data_as(U64P), cu.ctypes.data_as(U64P),
+        C.byref(nb)))
+    return io, du, cu, nb.value
+
+
 def serve_trace(index, arrivals_us, cap: int, queries: np.ndarray, qtok: np.ndarray | None, k: int,
                 want_ids: bool = False):
     """Live mode on the GPU: returns (latency_us, batch_of, ids or None)."""

@@ -6,6 +6,7 @@
 //   instant run first (they were scheduled earlier, sim.hpp:19-24 FIFO tie order).
 #include <stdint.h>
 
+#include <random>
 #include <string>
 
 #include "../../include/vortex_b200.h"
@@ -52,6 +53,83 @@ extern "C" vx_status vx_batcher_simulate(const uint64_t* arrivals_us, int64_t n,
         if (complete_us) complete_us[q] = end;
       bat.complete();
       dispatch(end);
+    }
+  }
+  if (n_batches) *n_batches = nb;
+  return VX_OK;
+}
+
+// Replica mode: R members of one stage, each its own opportunistic batcher, and the
+// reference's routing in front of them (Runtime::pick_member, runtime.hpp:522-536):
+// power-of-two-choices on `outstanding` (tags issued minus stage completions,
+// runtime.hpp:299, :668), ties to the lower index, two draws per query from the runtime's
+// mt19937_64 (sim.hpp:80-89 Rng::below = std::uniform_int_distribution over
+// std::mt19937_64, seeded with RuntimeOptions::seed = 7, runtime.hpp:188) — the same
+// standard-library types, so the draws are identical.  With R = 1 no draw is made.
+extern "C" vx_status vx_batcher_simulate_replicas(
+    const uint64_t* arrivals_us, int64_t n, int32_t replicas, int32_t cap,
+    const int32_t* knot_batch, const double* knot_ms, int32_t n_knots, uint64_t seed,
+    int32_t* instance_of, uint64_t* dispatch_us, uint64_t* complete_us, int64_t* n_batches) {
+  if (n < 0 || replicas < 1 || cap < 1 || n_knots < 1 || !knot_batch || !knot_ms ||
+      (n > 0 && !arrivals_us))
+    return VX_ERR_INVALID;
+  vx::LatencyProfile prof;
+  for (int i = 0; i < n_knots; ++i) {
+    if (knot_batch[i] < 1 || (i > 0 && knot_batch[i] <= knot_batch[i - 1])) return VX_ERR_INVALID;
+    prof.b.push_back(knot_batch[i]);
+    prof.ms.push_back(knot_ms[i]);
+  }
+  for (int64_t i = 1; i < n; ++i)
+    if (arrivals_us[i] < arrivals_us[i - 1]) return VX_ERR_INVALID;
+  const int R = replicas;
+  std::vector<vx::OpportunisticBatcher> bat(R, vx::OpportunisticBatcher(cap));
+  std::vector<std::vector<int64_t>> cur(R);
+  std::vector<uint64_t> end(R, 0), seq(R, 0);
+  std::vector<int> outstanding(R, 0);
+  std::mt19937_64 gen(seed);
+  auto below = [&](uint64_t m) { return std::uniform_int_distribution<uint64_t>(0, m - 1)(gen); };
+  auto pick = [&]() -> int {
+    if (R == 1) return 0;
+    uint64_t a = below((uint64_t)R);
+    uint64_t b = below((uint64_t)R - 1);
+    if (b >= a) ++b;
+    const int ia = (int)a, ib = (int)b;
+    if (outstanding[ia] != outstanding[ib]) return outstanding[ia] < outstanding[ib] ? ia : ib;
+    return ia < ib ? ia : ib;
+  };
+  int64_t next = 0, nb = 0;
+  uint64_t order = 0;  // dispatch sequence: equal completion instants run in dispatch order
+  auto dispatch = [&](int r, uint64_t now) {
+    std::vector<int64_t> b = bat[r].maybe_dispatch();
+    if (b.empty()) return;
+    cur[r].swap(b);
+    end[r] = now + (uint64_t)(prof.latency_ms((int)cur[r].size()) * 1000.0);
+    seq[r] = order++;
+    for (int64_t q : cur[r]) {
+      if (instance_of) instance_of[q] = r;
+      if (dispatch_us) dispatch_us[q] = now;
+    }
+    ++nb;
+  };
+  for (;;) {
+    int rc = -1;  // earliest completing replica (ties: dispatch order)
+    for (int r = 0; r < R; ++r)
+      if (bat[r].executing() && (rc < 0 || end[r] < end[rc] || (end[r] == end[rc] && seq[r] < seq[rc])))
+        rc = r;
+    if (next >= n && rc < 0) break;
+    if (next < n && (rc < 0 || arrivals_us[next] <= end[rc])) {
+      const uint64_t now = arrivals_us[next];
+      const int r = pick();
+      ++outstanding[r];
+      bat[r].arrive(next++);
+      dispatch(r, now);
+    } else {
+      for (int64_t q : cur[rc]) {
+        if (complete_us) complete_us[q] = end[rc];
+        --outstanding[rc];
+      }
+      bat[rc].complete();
+      dispatch(rc, end[rc]);
     }
   }
   if (n_batches) *n_batches = nb;

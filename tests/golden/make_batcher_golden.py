@@ -30,6 +30,31 @@ def run_reference(arrivals, cap: int, knots: dict[int, float]):
     return [r[1] for r in rows], [r[2] for r in rows], [r[3] for r in rows]
 
 
+def run_reference_replicas(arrivals, replicas: int, cap: int, knots: dict[int, float]):
+    """The reference runtime with `replicas` members routed by Runtime::pick_member."""
+    with tempfile.NamedTemporaryFile("w", suffix=".txt", delete=False) as f:
+        f.write("\n".join(str(int(a)) for a in arrivals) + "\n")
+        path = f.name
+    ks = ",".join(f"{b}:{ms!r}" for b, ms in sorted(knots.items()))
+    out = subprocess.run([str(DRIVER), "replicas", path, str(cap), ks, str(replicas)], check=True,
+                         capture_output=True, text=True).stdout
+    rows = sorted(tuple(int(x) for x in ln.split()) for ln in out.strip().splitlines())
+    return [r[1] for r in rows], [r[2] for r in rows], [r[3] for r in rows]
+
+
+def replica_cases():
+    rng = np.random.default_rng(12)
+    gpu = {1: 4.8, 16: 5.1, 64: 5.8, 128: 6.1, 256: 8.7}
+    modeld = {1: 125.0, 4: 400.0}
+    out = []
+    pois = np.rint(np.cumsum(rng.exponential(1e6 / 40000.0, 4000))).astype(np.int64).tolist()
+    out.append(("poisson_40kqps_gpu_4replicas_cap128", pois, 4, 128, gpu))
+    pois = np.rint(np.cumsum(rng.exponential(1e6 / 30.0, 300))).astype(np.int64).tolist()
+    out.append(("poisson_30qps_modelD_3replicas_cap4", pois, 3, 4, modeld))
+    out.append(("simultaneous_8replicas", [0] * 50 + [1000] * 50, 8, 16, gpu))
+    return out
+
+
 def cases():
     rng = np.random.default_rng(11)
     modeld = {1: 125.0, 4: 400.0}                       # profiles.csv:17-22
@@ -58,6 +83,13 @@ def main() -> None:
                          "knots": {str(k): v for k, v in knots.items()},
                          "batch": b, "dispatch_us": d, "complete_us": c})
     (HERE / "batcher_ref.json").write_text(json.dumps(fixtures))
+    rep = []
+    for name, arr, R, cap, knots in replica_cases():
+        i, d, c = run_reference_replicas(arr, R, cap, knots)
+        rep.append({"name": name, "arrivals_us": arr, "replicas": R, "cap": cap,
+                    "knots": {str(k): v for k, v in knots.items()},
+                    "instance": i, "dispatch_us": d, "complete_us": c})
+    (HERE / "batcher_replicas_ref.json").write_text(json.dumps(rep))
     print("wrote", len(fixtures), "cases")
 
 

@@ -77,6 +77,41 @@ def test_random_traces_against_reference_binary(bat, seed):
     assert b.tolist() == rb and d.tolist() == rd and c.tolist() == rc
 
 
+def replica_fixtures():
+    return json.loads((ROOT / "tests" / "golden" / "batcher_replicas_ref.json").read_text())
+
+
+@pytest.mark.parametrize("case", replica_fixtures(), ids=lambda c: c["name"])
+def test_replica_routing_matches_reference_fixtures(bat, case):
+    # Runtime::pick_member (runtime.hpp:522-536) in front of per-member batchers
+    knots = {int(k): v for k, v in case["knots"].items()}
+    i, d, c, _ = bat.simulate_replicas(case["arrivals_us"], case["replicas"], case["cap"], knots)
+    assert i.tolist() == case["instance"]
+    assert d.tolist() == case["dispatch_us"]
+    assert c.tolist() == case["complete_us"]
+
+
+@pytest.mark.skipif(not DRIVER.exists(), reason="oracle/_ref not built (needs /root/reference)")
+@pytest.mark.parametrize("seed", range(6))
+def test_random_replica_traces_against_reference_binary(bat, seed):
+    import sys
+    sys.path.insert(0, str(ROOT / "tests" / "golden"))
+    from make_batcher_golden import run_reference_replicas
+    rng = np.random.default_rng(100 + seed)
+    n = int(rng.integers(1, 1500))
+    R = int(rng.integers(1, 9))
+    rate = float(rng.choice([50.0, 2000.0, 40000.0]))
+    arr = np.rint(np.cumsum(rng.exponential(1e6 / rate, n))).astype(np.int64)
+    if seed % 2:
+        arr[rng.integers(0, n, n // 3)] = arr[0]
+        arr = np.sort(arr)
+    cap = int(rng.integers(1, 200))
+    knots = {1: float(rng.uniform(0.5, 5.0)), 64: float(rng.uniform(6.0, 20.0))}
+    ri, rd, rc = run_reference_replicas(arr.tolist(), R, cap, knots)
+    i, d, c, _ = bat.simulate_replicas(arr, R, cap, knots)
+    assert i.tolist() == ri and d.tolist() == rd and c.tolist() == rc
+
+
 def test_bench_helpers(bat):
     # bench.hpp:69-83 semantics
     assert bat.percentile(list(range(1, 101)), 95) == 95.0
