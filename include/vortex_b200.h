@@ -191,6 +191,12 @@ vx_status vx_batcher_simulate_replicas(const uint64_t* arrivals_us, int64_t n, i
                                        const double* knot_ms, int32_t n_knots, uint64_t seed,
                                        int32_t* instance_of, uint64_t* dispatch_us,
                                        uint64_t* complete_us, int64_t* n_batches);
+
+/* Open-loop arrival trace (bench::arrival_times, bench.hpp:54-67): poisson != 0 draws
+ * exponential gaps from std::mt19937_64(seed) exactly as the reference's sim::Rng does
+ * (sim.hpp:95-98), else constant spacing; times in us, llround'ed. */
+vx_status vx_arrival_times(double rate_qps, int64_t count, uint64_t seed, uint64_t start_us,
+                           int32_t poisson, uint64_t* out);
 /* vx_serve_trace: live mode — replays the arrival trace in wall-clock time through the
  * same batcher onto this handle's GPU stage (one batch in flight; each dispatched batch
  * is copied host->device, searched (and re-scored when qtok != NULL), and its results

@@ -15,6 +15,10 @@
 //       runtime.hpp:522-536, RNG seed RuntimeOptions::seed = 7) and each member batches on
 //       its own.  Prints per query: "<index> <instance> <dispatch_us> <complete_us>".
 //
+//   vortex_ref_driver arrivals <rate_qps> <count> <seed> <poisson|constant> <start_us>
+//       The reference's open-loop trace (bench::arrival_times, bench.hpp:54-67) from
+//       sim::Rng(seed); one time (us) per line.
+//
 //   vortex_ref_driver operator <N> <D> <k> <B> <nq> <T>
 //       Registers the B200 stage (include/vortex_b200_component.hpp over
 //       libvortex_b200.so) as "modelD" in the reference Runtime and pushes B synthetic
@@ -27,6 +31,7 @@
 #include <string>
 #include <vector>
 
+#include "vortex/bench.hpp"
 #include "vortex/runtime.hpp"
 
 #ifdef VX_WITH_B200
@@ -133,6 +138,18 @@ static int run_replicas(int argc, char** argv) {
   return 0;
 }
 
+static int run_arrivals(int argc, char** argv) {
+  if (argc < 7) return 2;
+  bench::Phase ph;
+  ph.rate_qps = std::atof(argv[2]);
+  ph.count = std::strtoull(argv[3], nullptr, 10);
+  ph.arrival = argv[5];
+  sim::Rng rng(std::strtoull(argv[4], nullptr, 10));
+  for (auto t : bench::arrival_times(ph, std::strtoull(argv[6], nullptr, 10), rng))
+    std::printf("%llu\n", (unsigned long long)t);
+  return 0;
+}
+
 #ifdef VX_WITH_B200
 static std::vector<float> synth_row(uint64_t seed, uint64_t row, int dim) {
   std::vector<int32_t> v(dim);
@@ -205,6 +222,7 @@ int main(int argc, char** argv) {
   try {
     if (mode == "batcher") return run_batcher(argc, argv);
     if (mode == "replicas") return run_replicas(argc, argv);
+    if (mode == "arrivals") return run_arrivals(argc, argv);
 #ifdef VX_WITH_B200
     if (mode == "operator") return run_operator(argc, argv);
 #endif

@@ -19,17 +19,36 @@ from . import _lib
 from ._lib import FP, LP, check
 
 
+def _arrivals(rate_qps: float, count: int, seed: int, start_us: int, poisson: bool) -> np.ndarray:
+    out = np.empty(count, np.uint64)
+    check(_lib.load().vx_arrival_times(float(rate_qps), count, seed, start_us, 1 if poisson else 0,
+                                       out.ctypes.data_as(C.POINTER(C.c_uint64))))
+    return out
+
+
 def poisson_arrivals(rate_qps: float, count: int, seed: int = 42, start_us: int = 0) -> np.ndarray:
-    """Open-loop Poisson arrivals in integer microseconds: t += Exp(rate) gaps, rounded to
-    the nearest microsecond (bench.hpp:54-67).  numpy's generator, not mt19937_64: the trace
-    is seeded and reproducible but not the reference's exact draw."""
-    rng = np.random.default_rng(seed)
-    gaps = rng.exponential(1e6 / rate_qps, size=count)
-    return np.rint(start_us + np.cumsum(gaps)).astype(np.uint64)
+    """Open-loop Poisson arrivals in integer microseconds (bench.hpp:54-67): exponential gaps
+    from std::mt19937_64(seed), exactly the reference's trace for the same seed."""
+    return _arrivals(rate_qps, count, seed, start_us, True)
 
 
 def constant_arrivals(rate_qps: float, count: int, start_us: int = 0) -> np.ndarray:
-    return np.rint(start_us + np.arange(count) * (1e6 / rate_qps)).astype(np.uint64)
+    return _arrivals(rate_qps, count, 0, start_us, False)
+
+
+def peak(profile: dict[int, float], batch_cap: int | None = None) -> int:
+    """ProfileTable::peak (profile.hpp:110-123): the throughput-peak batch (throughput =
+    1000 b / L(b)) among the profiled batches <= batch_cap; ties resolve to the smaller batch."""
+    best, best_tp = None, -1.0
+    for b in sorted(profile):
+        if batch_cap is not None and b > batch_cap:
+            continue
+        tp = 1000.0 * b / profile[b]
+        if tp > best_tp:
+            best, best_tp = b, tp
+    if best is None:
+        raise ValueError("no profiled batch within the cap")
+    return best
 
 
 def percentile(values, p: float) -> float:

@@ -6,6 +6,7 @@
 //   instant run first (they were scheduled earlier, sim.hpp:19-24 FIFO tie order).
 #include <stdint.h>
 
+#include <cmath>
 #include <random>
 #include <string>
 
@@ -133,5 +134,26 @@ extern "C" vx_status vx_batcher_simulate_replicas(
     }
   }
   if (n_batches) *n_batches = nb;
+  return VX_OK;
+}
+
+// Open-loop arrival schedule (bench::arrival_times, proj/include/vortex/bench.hpp:54-67):
+// poisson: t += Exp(rate / 1e6) gaps drawn from std::mt19937_64(seed) through
+// std::exponential_distribution<double> (sim.hpp:95-98); constant: t = start + i * 1e6/rate;
+// each time rounded with llround.  Same standard-library types as the reference, so the same
+// seed gives the same trace.
+extern "C" vx_status vx_arrival_times(double rate_qps, int64_t count, uint64_t seed,
+                                      uint64_t start_us, int32_t poisson, uint64_t* out) {
+  if (!(rate_qps > 0) || count < 0 || (count > 0 && !out)) return VX_ERR_INVALID;
+  std::mt19937_64 gen(seed);
+  const double gap_us = 1e6 / rate_qps;
+  double t = (double)start_us;
+  for (int64_t i = 0; i < count; ++i) {
+    if (poisson)
+      t += std::exponential_distribution<double>(rate_qps / 1e6)(gen);
+    else
+      t = (double)start_us + (double)i * gap_us;
+    out[i] = (uint64_t)std::llround(t);
+  }
   return VX_OK;
 }

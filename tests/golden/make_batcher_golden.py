@@ -42,6 +42,12 @@ def run_reference_replicas(arrivals, replicas: int, cap: int, knots: dict[int, f
     return [r[1] for r in rows], [r[2] for r in rows], [r[3] for r in rows]
 
 
+def run_reference_arrivals(rate_qps: float, count: int, seed: int, kind: str, start_us: int = 0):
+    out = subprocess.run([str(DRIVER), "arrivals", repr(float(rate_qps)), str(count), str(seed), kind,
+                          str(start_us)], check=True, capture_output=True, text=True).stdout
+    return [int(x) for x in out.split()]
+
+
 def replica_cases():
     rng = np.random.default_rng(12)
     gpu = {1: 4.8, 16: 5.1, 64: 5.8, 128: 6.1, 256: 8.7}
@@ -90,6 +96,11 @@ def main() -> None:
                     "knots": {str(k): v for k, v in knots.items()},
                     "instance": i, "dispatch_us": d, "complete_us": c})
     (HERE / "batcher_replicas_ref.json").write_text(json.dumps(rep))
+    arr = [{"rate_qps": r, "count": n, "seed": sd, "kind": kd, "start_us": st,
+            "times": run_reference_arrivals(r, n, sd, kd, st)}
+           for r, n, sd, kd, st in [(60.0, 500, 42, "poisson", 0), (20000.0, 3000, 7, "poisson", 1234),
+                                    (333.0, 100, 1, "constant", 50)]]
+    (HERE / "arrivals_ref.json").write_text(json.dumps(arr))
     print("wrote", len(fixtures), "cases")
 
 

@@ -112,6 +112,36 @@ def test_random_replica_traces_against_reference_binary(bat, seed):
     assert i.tolist() == ri and d.tolist() == rd and c.tolist() == rc
 
 
+@pytest.mark.parametrize("case", json.loads((ROOT / "tests" / "golden" / "arrivals_ref.json").read_text()),
+                         ids=lambda c: f"{c['kind']}_{c['rate_qps']}")
+def test_arrival_traces_match_reference_fixtures(bat, case):
+    # bench::arrival_times (bench.hpp:54-67) from sim::Rng(seed) (sim.hpp:80-98)
+    if case["kind"] == "poisson":
+        t = bat.poisson_arrivals(case["rate_qps"], case["count"], case["seed"], case["start_us"])
+    else:
+        t = bat.constant_arrivals(case["rate_qps"], case["count"], case["start_us"])
+    assert t.tolist() == case["times"]
+
+
+@pytest.mark.skipif(not DRIVER.exists(), reason="oracle/_ref not built (needs /root/reference)")
+@pytest.mark.parametrize("seed", [0, 5, 42, 2**40 + 3])
+def test_poisson_traces_against_reference_binary(bat, seed):
+    import sys
+    sys.path.insert(0, str(ROOT / "tests" / "golden"))
+    from make_batcher_golden import run_reference_arrivals
+    for rate, n in [(10.0, 50), (1e5, 4000)]:
+        assert bat.poisson_arrivals(rate, n, seed).tolist() == run_reference_arrivals(rate, n, seed, "poisson")
+
+
+def test_profile_peak(bat):
+    # ProfileTable::peak (profile.hpp:110-123): max throughput, ties to the smaller batch
+    prof = {1: 125.0, 4: 400.0}                     # modelD: 8 vs 10 q/s -> 4
+    assert bat.peak(prof) == 4 and bat.peak(prof, batch_cap=3) == 1
+    assert bat.peak({1: 10.0, 2: 20.0, 4: 50.0}) == 1   # 100 = 100 > 80: tie -> smaller
+    with pytest.raises(ValueError):
+        bat.peak({8: 1.0}, batch_cap=4)
+
+
 def test_bench_helpers(bat):
     # bench.hpp:69-83 semantics
     assert bat.percentile(list(range(1, 101)), 95) == 95.0
