@@ -31,9 +31,10 @@ __global__ void __launch_bounds__(kMsThreads)
     if (threadIdx.x == 0) a.out[(size_t)b * a.C + c] = -INFINITY;
     return;
   }
-  const float* qt = a.qtok + (size_t)b * nq * d;
+  const float* qt = a.qtok ? a.qtok + (size_t)b * nq * d : nullptr;
+  const uint16_t* qt16 = a.qtok16 ? a.qtok16 + (size_t)b * nq * d : nullptr;
   for (int i = threadIdx.x; i < nq * d; i += blockDim.x)
-    q_s[i] = vx_bf16_bits_to_f32(vx_f32_to_bf16_bits(qt[i]));
+    q_s[i] = vx_bf16_bits_to_f32(qt16 ? qt16[i] : vx_f32_to_bf16_bits(qt[i]));
   const uint16_t* dt = a.table + (size_t)(id % a.T) * Nd * d;
   for (int i = threadIdx.x; i < Nd * d; i += blockDim.x) {
     int j = i / d, t = i - j * d;

@@ -62,12 +62,19 @@ __global__ void __launch_bounds__(kMsThreads, 2)
 
   // A tile: query tokens -> bf16 (RNE), SWIZZLE_128B K-major; rows >= nq are zero
   {
-    const float* qt = a.qtok + (size_t)b * nq * a.d;
+    const float* qt = a.qtok ? a.qtok + (size_t)b * nq * a.d : nullptr;
+    const uint16_t* qt16 = a.qtok16 ? a.qtok16 + (size_t)b * nq * a.d : nullptr;
     const int chunks16 = DK * 128 * 8;  // 16-byte chunks in the A tile
     for (int i = threadIdx.x; i < chunks16; i += blockDim.x) {
       const int kb = i / (128 * 8), rem = i % (128 * 8), r = rem >> 3, ch = rem & 7;
       uint32_t w[4] = {0, 0, 0, 0};
-      if (r < nq) {
+      if (r < nq && qt16) {
+        const uint4 v = *reinterpret_cast<const uint4*>(qt16 + (size_t)r * a.d + kb * 64 + ch * 8);
+        w[0] = v.x;
+        w[1] = v.y;
+        w[2] = v.z;
+        w[3] = v.w;
+      } else if (r < nq) {
         const float* src = qt + (size_t)r * a.d + kb * 64 + ch * 8;
 #pragma unroll
         for (int e = 0; e < 4; ++e)

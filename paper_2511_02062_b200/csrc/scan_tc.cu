@@ -640,7 +640,11 @@ cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64
                           int64_t* out_ids, float* out_scores, int* flags, cudaStream_t st) {
   const size_t base = (size_t)((D + 3) & ~3) * 4 + (size_t)kp * 8;
   const size_t row = (size_t)(D + 4) * 4;
-  if (const char* e = getenv("VX_DEBUG_RERANK_ROWS")) kRerankRows = atoi(e);  // experiments
+  static const int env_rows = [] {  // timing experiments: VX_DEBUG_RERANK_ROWS, read once
+    const char* e = getenv("VX_DEBUG_RERANK_ROWS");
+    return e ? atoi(e) : 0;
+  }();
+  if (env_rows > 0) kRerankRows = env_rows;
   int R = (int)((220 * 1024 - base) / row);
   R = R > kRerankRows ? kRerankRows : (R < 1 ? 1 : R);
   const size_t smem = base + (size_t)R * row;

@@ -170,6 +170,8 @@ struct vx_index {
   int coarse = VX_COARSE_AUTO;
   int scan_tile = 0;             // documents per tensor-core tile (0 = auto)
   int kprime = 0;                // TC candidate set size k' (0 = auto; VX_OPT_KPRIME)
+  int dbg_tc_bits = 0;           // timing-experiment knobs, read once from the environment at
+  int dbg_tc_stages = 0;         //   create: VX_DEBUG_TC_NOSELECT (bit mask), VX_DEBUG_TC_STAGES
   int use_pairs = 1;             // CTA-pair scan for B > 128: 0 off, 1 on, 2 on + 512-query
                                  // passes (VX_OPT_SCAN_PAIRS)
   // options
@@ -179,6 +181,7 @@ struct vx_index {
   // workspace
   float* d_q = nullptr;          // [maxB][D]
   float* d_qtok = nullptr;       // [maxB][maxNq][d]
+  uint16_t* d_qtok16 = nullptr;  // bf16 copy for the shard exchange (half the broadcast bytes)
   uint64_t* d_part = nullptr;    // [maxB][grid][256]
   uint64_t* d_keys = nullptr;    // [maxB][maxK]
   int64_t* d_ids = nullptr;      // [maxB][maxK]
@@ -280,6 +283,8 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
     vx_index_destroy(h);
     return e;
   };
+  if (const char* e = getenv("VX_DEBUG_TC_NOSELECT")) h->dbg_tc_bits = atoi(e);
+  if (const char* e = getenv("VX_DEBUG_TC_STAGES")) h->dbg_tc_stages = atoi(e);
   if (cudaSetDevice(h->device) != cudaSuccess) return cleanup(fail(VX_ERR_CUDA, "cudaSetDevice"));
   if (h->n_local < 1) return cleanup(fail(VX_ERR_INVALID, "empty shard"));
 #define ALLOC(ptr, bytes)                                                              \
@@ -296,6 +301,7 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
   h->grid = h->num_sms;
   ALLOC(h->d_q, B * D * 4);
   if (d->tok_per_doc > 0) ALLOC(h->d_qtok, B * d->max_qtok * d->tok_dim * 4);
+  if (d->tok_per_doc > 0 && d->n_shards > 1) ALLOC(h->d_qtok16, B * d->max_qtok * d->tok_dim * 2);
   ALLOC(h->d_part, B * (size_t)h->grid * 256 * 8);
   ALLOC(h->d_keys, B * K * 8);
   ALLOC(h->d_ids, B * K * 8);
@@ -368,7 +374,8 @@ extern "C" vx_status vx_index_destroy(vx_index* h) {
   void* ptrs[] = {h->docs,  h->tokens,    h->d_q,      h->d_qtok,    h->d_part, h->d_keys,
                   h->d_ids, h->d_ip,      h->d_ms,     h->d_out_ids, h->d_out_ip,
                   h->d_out_ms, h->d_send, h->d_recv, h->d_hdr, h->d_ckeys, h->d_flags,
-                  h->d_xnorm, h->d_fq, h->docs16, h->d_q16, h->d_fidx, h->d_fcount};
+                  h->d_xnorm, h->d_fq, h->docs16, h->d_q16, h->d_fidx, h->d_fcount,
+                  h->d_qtok16};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->h_stage) cudaFreeHost(h->h_stage);
@@ -650,7 +657,7 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
     a.a_rows = a_rows;
     a.fmt = bf16 ? 1 : 2;
     a.dbg_no_select = 0;
-    if (const char* e = getenv("VX_DEBUG_TC_NOSELECT")) a.dbg_no_select = atoi(e);  // bit mask
+    a.dbg_no_select = h->dbg_tc_bits;  // timing experiments only (VX_DEBUG_TC_NOSELECT)
     a.part = h->d_part + (size_t)g0 * grid * vx::kTcListLen;
     if (on_pairs) {
       // 128 < B: CTA pairs (cta_group::2), 256 documents x 256 QG queries per pair tile
@@ -666,8 +673,8 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
       const int TD = h->scan_tile ? h->scan_tile : 256;
       int ns = 0;
       size_t smem = vx::scan_tc_smem(QT, TD, &ns);
-      if (const char* e = getenv("VX_DEBUG_TC_STAGES")) {  // timing experiments only
-        const int want = atoi(e);
+      if (h->dbg_tc_stages) {  // timing experiments only (VX_DEBUG_TC_STAGES)
+        const int want = h->dbg_tc_stages;
         if (want >= 2 && want < ns) {
           smem -= (size_t)(ns - want) * (QT * 16384 + TD * 128 + 16);
           ns = want;
@@ -742,11 +749,12 @@ static vx_status local_topk(vx_index* h, const float* d_q, int B, int k, uint64_
 
 static vx_status run_maxsim(vx_index* h, const float* d_qtok, int B, int nq, const int64_t* d_cand,
                             int C, float* d_out, cudaStream_t st, int64_t id_lo = 0,
-                            int64_t id_hi = INT64_MAX) {
+                            int64_t id_hi = INT64_MAX, const uint16_t* d_qtok16 = nullptr) {
   if (!h->tokens) return fail(VX_ERR_STATE, "index has no token store");
   if (nq < 1 || nq > h->desc.max_qtok) return fail(VX_ERR_INVALID, "nq %d", nq);
   vx::MaxSimArgs a;
   a.qtok = d_qtok;
+  a.qtok16 = d_qtok16;
   a.cand = d_cand;
   a.table = h->tokens;
   a.T = h->desc.tok_blocks;
@@ -838,13 +846,19 @@ static vx_status core_rescore(vx_index* h, const float* d_qtok, int B, int nq, i
   }
   const int n = B * k;
   const bool root = h->rank == 0;
+  // the tokens travel as bf16 (the MaxSim operand precision: the kernels round fp32 tokens
+  // with the same RNE anyway, so the scores are unchanged) — half the broadcast bytes
+  const int64_t ntok = (int64_t)B * nq * h->desc.tok_dim;
+  if (root) {
+    CU_TRY(vx::launch_to_bf16(d_qtok, h->d_qtok16, ntok, st));
+    count_launch(h);
+  }
   NCCL_TRY(nccl().GroupStart());
-  NCCL_TRY(nccl().Broadcast(root ? d_qtok : h->d_qtok, h->d_qtok,
-                            (size_t)B * nq * h->desc.tok_dim, ncclFloat32, 0, h->comm, st));
+  NCCL_TRY(nccl().Broadcast(h->d_qtok16, h->d_qtok16, (size_t)ntok * 2, ncclUint8, 0, h->comm, st));
   NCCL_TRY(nccl().Broadcast(h->d_ids, h->d_ids, (size_t)n, ncclInt64, 0, h->comm, st));
   NCCL_TRY(nccl().GroupEnd());
-  VX_TRY(run_maxsim(h, h->d_qtok, B, nq, h->d_ids, k, h->d_ms, st, h->row0,
-                    h->row0 + h->n_local));
+  VX_TRY(run_maxsim(h, nullptr, B, nq, h->d_ids, k, h->d_ms, st, h->row0, h->row0 + h->n_local,
+                    h->d_qtok16));
   float* ms_all = reinterpret_cast<float*>(h->d_send);  // [B][k] on rank 0
   NCCL_TRY(nccl().Reduce(h->d_ms, ms_all, (size_t)n, ncclFloat32, ncclMax, 0, h->comm, st));
   if (!root) return VX_OK;

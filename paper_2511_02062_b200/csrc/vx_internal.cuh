@@ -101,6 +101,7 @@ cudaError_t launch_synth_tokens(uint16_t* out, uint64_t seed, int64_t blk0, int6
 // -------- MaxSim (K4): maxsim.cu
 struct MaxSimArgs {
   const float* qtok;     // [B][nq][d] fp32 (rounded to bf16 in-kernel)
+  const uint16_t* qtok16 = nullptr;  // or already-rounded bf16 bits (shard exchange)
   const int64_t* cand;   // [B][C] global doc ids, -1 = skip
   const uint16_t* table; // [T][Nd][d] bf16 bits
   int64_t T;
