@@ -554,6 +554,12 @@ def run_ours(args) -> None:
         out["p99_batch_ms"] = b["p99_ms"] if b else None
         out["slo_met"] = b is not None
         out["trace"] = ladder["rungs"]
+        # the same rungs read against tighter / the reference's SLOs
+        out["max_rate_by_slo_ms"] = {
+            str(slo): max([r["achieved_qps"] for r in ladder["rungs"]
+                           if r["p99_ms"] <= slo and r["achieved_qps"] >= 0.9 * r["rate_qps"]],
+                          default=0.0)
+            for slo in (5.0, 10.0, 20.0, 200.0, 500.0)}
         out["e2e"] = {"value": out["value"], "unit": "queries/s",
                       "h2d_bytes_per_step": int(round(b["mean_batch"] * D * 4)) if b else 0,
                       "d2h_bytes_per_step": int(round(b["mean_batch"] * k * 12)) if b else 0,
