@@ -58,7 +58,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         failed |= p.returncode != 0
     if failed:
         raise RuntimeError("nvcc failed")
-    cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-ldl"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-ldl",
+           "-Xlinker", f"--version-script={CSRC / 'exports.map'}"]
     subprocess.run(cmd, check=True)
     stamp.write_text(dig)
     return LIB

@@ -1,0 +1,190 @@
+// vx_handle.cuh — internals shared by the C-ABI translation units (vx_api.cu: handle
+// lifecycle, data, host-buffer API, live batcher, comm; vx_stage.cu: the per-batch stage and
+// the shard exchange).  Not part of the ABI.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <map>
+
+#include "../../include/vortex_b200.h"
+#include "vx_internal.cuh"
+
+// ---------------------------------------------------------------- NCCL (loaded lazily)
+// NCCL is dlopen'ed on first use instead of linked: a host process (e.g. PyTorch) may
+// already carry its own libnccl.so.2, and two copies under one soname break each other.
+// Order: an already-loaded libnccl.so.2, $VX_NCCL_LIB, then the system library.
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*CommDestroy)(ncclComm_t);
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                            cudaStream_t);
+  ncclResult_t (*Reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
+                         cudaStream_t);
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*GroupStart)();
+  ncclResult_t (*GroupEnd)();
+  const char* (*GetErrorString)(ncclResult_t);
+  bool ok = false;
+};
+
+NcclApi& nccl();
+
+// thread-local error message (vx_last_error) + status
+vx_status fail(vx_status s, const char* fmt, ...);
+
+#define CU_TRY(expr)                                                                     \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess)                                                               \
+      return fail(_e == cudaErrorMemoryAllocation ? VX_ERR_OOM : VX_ERR_CUDA, "%s: %s (%s:%d)", \
+                  #expr, cudaGetErrorString(_e), __FILE__, __LINE__);                    \
+  } while (0)
+
+#define NCCL_TRY(expr)                                                                    \
+  do {                                                                                    \
+    ncclResult_t _r = (expr);                                                             \
+    if (_r != ncclSuccess)                                                                \
+      return fail(VX_ERR_NCCL, "%s: %s (%s:%d)", #expr, nccl().GetErrorString(_r), __FILE__, \
+                  __LINE__);                                                              \
+  } while (0)
+
+#define VX_TRY(expr)                 \
+  do {                               \
+    vx_status _s = (expr);           \
+    if (_s != VX_OK) return _s;      \
+  } while (0)
+
+// 2-D row-major matrix [rows][cols] of `elem` bytes, box {box_cols, box_rows}, 128B swizzle.
+vx_status make_tmap_2d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int elem,
+                       uint64_t rows, uint64_t cols, uint32_t box_cols, uint32_t box_rows);
+
+// ---------------------------------------------------------------- handle
+
+struct vx_index {
+  vx_index_desc desc{};
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  int64_t row0 = 0, n_local = 0;
+  float* docs = nullptr;
+  uint16_t* tokens = nullptr;
+  CUtensorMap tmap_docs{};
+  CUtensorMap tmap_tok{};
+  uint16_t* docs16 = nullptr;    // bf16 shadow of the shard (coarse scan), may be null
+  CUtensorMap tmap_docs16{};
+  uint16_t* d_q16 = nullptr;     // [maxB][D] bf16 queries for the bf16 coarse scan
+  int coarse = VX_COARSE_AUTO;
+  int scan_tile = 0;             // documents per tensor-core tile (0 = auto)
+  int kprime = 0;                // TC candidate set size k' (0 = auto; VX_OPT_KPRIME)
+  int dbg_tc_bits = 0;           // timing-experiment knobs, read once from the environment at
+  int dbg_tc_stages = 0;         //   create: VX_DEBUG_TC_NOSELECT (bit mask), VX_DEBUG_TC_STAGES
+  int use_pairs = 1;             // CTA-pair scan for B > 128: 0 off, 1 on, 2 on + 512-query
+                                 // passes (VX_OPT_SCAN_PAIRS)
+  // options
+  int scan_algo = VX_SCAN_AUTO;
+  int maxsim_algo = VX_MAXSIM_AUTO;
+  int grid = 0;
+  // workspace
+  float* d_q = nullptr;          // [maxB][D]
+  float* d_qtok = nullptr;       // [maxB][maxNq][d]
+  uint16_t* d_qtok16 = nullptr;  // bf16 copy for the shard exchange (half the broadcast bytes)
+  uint64_t* d_part = nullptr;    // [maxB][grid][256]
+  uint64_t* d_keys = nullptr;    // [maxB][maxK]
+  int64_t* d_ids = nullptr;      // [maxB][maxK]
+  float* d_ip = nullptr;         // [maxB][maxK]
+  float* d_ms = nullptr;         // [maxB][maxK]
+  int64_t* d_out_ids = nullptr;  // [maxB][maxK]
+  float* d_out_ip = nullptr;
+  float* d_out_ms = nullptr;
+  void* d_send = nullptr;        // [maxB][maxK] x 8 B scratch (rank 0: the reduced MaxSim)
+  void* d_recv = nullptr;        // [G][maxB][maxK] gathered keys (rank 0)
+  int32_t* d_hdr = nullptr;      // [4]
+  uint64_t* d_ckeys = nullptr;   // [maxB][512] merged coarse keys (TC path)
+  int* d_flags = nullptr;        // [maxB] certificate failures (TC path)
+  unsigned int* d_xnorm = nullptr;  // [3] row-norm maxima of the shard (float bits, row_stats)
+  float* d_fq = nullptr;         // [maxB][D] queries gathered for the exact fallback
+  int* d_fidx = nullptr;         // [maxB] flagged query indices
+  int* d_fcount = nullptr;       // [2] flagged count of the last batch, running total
+  // pinned host staging
+  void* h_stage = nullptr;
+  size_t h_stage_bytes = 0;
+  int32_t* h_hdr = nullptr;
+  int* h_flags = nullptr;
+  // comm
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  // stats
+  vx_stats st{};
+  cudaEvent_t ev[4] = {};        // eager-path timing events: scan begin/end, stage begin/end
+  cudaEvent_t gev[4] = {};       // the same, recorded by captured graph nodes
+  cudaEvent_t* tev = ev;         // events the code being issued records into
+  cudaEvent_t* ev_start = ev;    // last batch: the array holding scan begin/end + stage begin
+  cudaEvent_t* ev_end = ev;      //   ... and the one holding the stage end (read by vx_sync)
+  cudaStream_t stream_last = nullptr;  // stream of the last batch's final part
+  cudaStream_t stream2 = nullptr;      // host API: query-token upload overlapping part 1
+  cudaEvent_t tok_ev = nullptr;
+  cudaEvent_t pev[5] = {};       // sharded rank 0 phases: start, bcast done, local done,
+  bool phases_pending = false;   //   gather done, end
+  bool timing_pending = false;
+  // CUDA graphs per (op, B, k, nq)
+  struct GraphEntry {
+    cudaGraphExec_t exec;
+    int launches;
+  };
+  bool use_graphs = false;
+  std::map<uint64_t, GraphEntry> graphs;
+};
+
+static inline void count_launch(vx_index* h, int n = 1) { h->st.kernel_launches += n; }
+
+// Timing events: inside a stream capture they must be EXTERNAL event nodes, or the graph only
+// uses them for internal ordering and never records them for the host to read.
+static inline cudaError_t record_ev(vx_index* h, cudaEvent_t e, cudaStream_t st) {
+  return cudaEventRecordWithFlags(e, st,
+                                  h->tev == h->gev ? cudaEventRecordExternal : cudaEventRecordDefault);
+}
+
+static inline int next_pow2(int x) {
+  int p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+static inline int kcap_of(int k) { return std::max(16, next_pow2(k)); }
+
+// ---------------------------------------------------------------- pipeline pieces
+
+static inline cudaStream_t pick_stream(vx_index* h, void* s) {
+  return s ? reinterpret_cast<cudaStream_t>(s) : h->stream;
+}
+
+static inline vx_status check_batch(vx_index* h, int32_t B, int32_t k) {
+  if (B < 1 || B > h->desc.max_batch)
+    return fail(VX_ERR_INVALID, "batch %d outside [1, %d]", B, h->desc.max_batch);
+  if (k < 1 || k > h->desc.max_k) return fail(VX_ERR_INVALID, "k %d outside [1, %d]", k, h->desc.max_k);
+  return VX_OK;
+}
+
+// ---------------------------------------------------------------- the stage (vx_stage.cu)
+enum { OP_STOP = 0, OP_SEARCH = 1, OP_RESCORE = 2 };
+
+vx_status run_maxsim(vx_index* h, const float* d_qtok, int B, int nq, const int64_t* d_cand, int C,
+                     float* d_out, cudaStream_t st, int64_t id_lo = 0, int64_t id_hi = INT64_MAX,
+                     const uint16_t* d_qtok16 = nullptr);
+// part 1 / part 2 of the stage on any rank (the shard ranks call these from vx_shard_serve)
+vx_status core_topk(vx_index* h, const float* d_q, int B, int k, cudaStream_t st);
+vx_status core_rescore(vx_index* h, const float* d_qtok, int B, int nq, int k, int64_t* d_ids,
+                       float* d_ip, float* d_ms, cudaStream_t st);
+// rank-0 entry points: announce + part 1; part 2 of a search / of the fused stage
+vx_status stage_begin(vx_index* h, int op, const float* d_q, int B, int nq, int k,
+                      cudaStream_t st);
+vx_status stage_search_out(vx_index* h, int B, int k, int64_t* d_ids, float* d_ip,
+                           cudaStream_t st);
+vx_status stage_finish(vx_index* h, const float* d_qtok, int B, int nq, int k, int64_t* d_ids,
+                       float* d_ip, float* d_ms, cudaStream_t st);

@@ -1,0 +1,554 @@
+// vx_stage.cu — the per-batch retrieval stage behind the C-ABI (include/vortex_b200.h):
+// local certified top-k (tensor-core coarse scan or exact K1 scan, merge, exact re-rank,
+// certificate levels 2-3), MaxSim, the two-phase NCCL shard exchange, CUDA graphs per stage
+// part, the device-pointer entry points, model load (vx_prepare) and vx_sync.
+//
+// The stage a deployment registers as the search operator (reference: ComponentFn,
+// proj/include/vortex/runtime.hpp:179; invoked by Runtime::complete_batch,
+// runtime.hpp:656-672) runs, per batch of B queries:
+//   part 1: [broadcast queries] -> K2 coarse scan + per-CTA top-16 -> K3 merge to k'
+//           -> K2b exact re-rank + certificate (-> K2c / K1 on failure)
+//           -> [gather k x G keys to rank 0 -> K3 merge]
+//   part 2: [broadcast tokens + winners] -> K4 MaxSim (owned winners) -> [max-reduce]
+//           -> order by MaxSim
+// Shard mode mirrors the reference's key->shard placement (kvs.hpp:160-175): contiguous
+// document ranges, a document's row and its token block on one GPU.
+#include "vx_handle.cuh"
+
+// Exact path: K1 scan + merge: d_q [B][D] -> keys (global ids) / ids / scores [B][k]
+static vx_status local_topk_f32(vx_index* h, const float* d_q, int B, int k, uint64_t* keys,
+                                int64_t* ids, float* scores, cudaStream_t st,
+                                const int* d_count = nullptr) {
+  const int D = h->desc.dim;
+  const int kcap = kcap_of(k);
+  const int grid = h->grid;
+  // queries per launch: the largest bucket whose smem plan fits (big k / big D shrink it)
+  int gmax = 32, ns0 = 0, cap0 = 0;
+  while (gmax > 1 && !vx::scan_f32_smem(gmax, D, kcap, &ns0, &cap0)) gmax >>= 1;
+  // device-count launch (certificate fallback): ONE launch loops over the query groups on
+  // the device, sized by the count; host-sized batches launch one kernel per group
+  const int step = d_count ? B : gmax;
+  for (int g0 = 0; g0 < B; g0 += step) {
+    const int Bg = std::min(step, B - g0);
+    const int bucket = d_count ? gmax : vx::scan_f32_bucket(Bg);
+    int ns = 0, cap = 0;
+    size_t smem = vx::scan_f32_smem(bucket, D, kcap, &ns, &cap);
+    if (!smem) return fail(VX_ERR_UNSUPPORTED, "scan config (B=%d, D=%d, k=%d) exceeds smem", Bg, D, k);
+    vx::ScanF32Args a;
+    a.q = d_q + (size_t)g0 * D;
+    a.B = Bg;
+    a.D = D;
+    a.n_local = (uint32_t)h->n_local;
+    a.kcap = kcap;
+    a.cap = cap;
+    a.ns = ns;
+    a.part = h->d_part + (size_t)g0 * grid * kcap;
+    a.d_count = d_count;
+    a.g0 = g0;
+    if (g0 == 0 && !d_count) CU_TRY(record_ev(h, h->tev[0], st));
+    CU_TRY(vx::launch_scan_f32(bucket, &h->tmap_docs, a, grid, smem, st));
+    count_launch(h);
+  }
+  if (!d_count) CU_TRY(record_ev(h, h->tev[1], st));
+  CU_TRY(vx::launch_merge_topk(h->d_part, B, grid * kcap, k, h->row0, keys, ids, scores, st,
+                               d_count));
+  count_launch(h);
+  return VX_OK;
+}
+
+// candidates the TC pass hands to the exact re-rank
+// k' = 4 next_pow2(k) in [64, 256] (VX_OPT_KPRIME overrides, up to 512).  256 is the
+// measured sweet spot for bf16 at k = 100: with 16-entry per-pair lists, k' = 512 fails
+// certificate 1 for ~13% of queries (a pair holding >= 16 of the top-512), k' = 256 for
+// ~0.03% (profiles/cert_rate.py, profiles/r01/cert_rate.jsonl).
+static int kprime_of(const vx_index* h, int k) {
+  if (h->kprime) return std::max(h->kprime, next_pow2(k));
+  return std::min(256, std::max(64, 4 * next_pow2(k)));
+}
+
+static bool tc_eligible(const vx_index* h, int B, int k) {
+  (void)h;
+  (void)B;
+  return k <= 128;
+}
+
+// Tensor-core path: K2 coarse scan (top-16 per CTA) -> K3 merge to top-k' -> K2b exact
+// re-rank + certificate -> exact re-scan of any query whose certificate failed.
+static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint64_t* keys,
+                               int64_t* ids, float* scores, cudaStream_t st) {
+  const int D = h->desc.dim;
+  const int grid = h->grid;
+  const int kp = kprime_of(h, k);
+  const bool bf16 = h->docs16 && h->coarse != VX_COARSE_TF32;
+  if (D % (bf16 ? 64 : 32)) return fail(VX_ERR_UNSUPPORTED, "TC scan: D %d", D);
+  CU_TRY(record_ev(h, h->tev[0], st));
+  if (bf16) {
+    CU_TRY(vx::launch_to_bf16(d_q, h->d_q16, (int64_t)B * D, st));
+    count_launch(h);
+  }
+  // queries per pass over the index: 256 (CTA pairs, or the single-CTA kernel's QT = 2 x
+  // 128); VX_OPT_SCAN_PAIRS = 2 feeds 512 queries per pass on CTA pairs (QG = 2: a single
+  // TMEM buffer for both groups, so the epilogue no longer overlaps the MMA — measured
+  // slower than two QG = 1 passes at 10M x 768, profiles/r01/README.md)
+  const bool pairs = h->use_pairs && grid % 2 == 0;
+  const int GS = (pairs && h->use_pairs == 2) ? 512 : 256;
+  for (int g0 = 0; g0 < B; g0 += GS) {
+    const int Bg = std::min(GS, B - g0);
+    const bool on_pairs = pairs && Bg > 128;
+    const int QT = Bg <= 128 ? 1 : 2;
+    const int a_rows = on_pairs ? 128 : (QT == 1 ? ((Bg + 7) & ~7) : 128);
+    CUtensorMap tq;
+    if (bf16)
+      VX_TRY(make_tmap_2d(&tq, h->d_q16 + (size_t)g0 * D, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                          (uint64_t)Bg, D, 64, (uint32_t)a_rows));
+    else
+      VX_TRY(make_tmap_2d(&tq, d_q + (size_t)g0 * D, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                          (uint64_t)Bg, D, 32, (uint32_t)a_rows));
+    vx::ScanTcArgs a;
+    a.n_local = (uint32_t)h->n_local;
+    a.D = D;
+    a.B = Bg;
+    a.a_rows = a_rows;
+    a.fmt = bf16 ? 1 : 2;
+    a.dbg_no_select = 0;
+    a.dbg_no_select = h->dbg_tc_bits;  // timing experiments only (VX_DEBUG_TC_NOSELECT)
+    a.part = h->d_part + (size_t)g0 * grid * vx::kTcListLen;
+    if (on_pairs) {
+      // 128 < B: CTA pairs (cta_group::2), 256 documents x 256 QG queries per pair tile
+      const int QG = Bg > 256 ? 2 : 1;
+      int ns2 = 0;
+      const size_t smem2 = vx::scan_tc2_smem(QG, &ns2);
+      a.ns = ns2;
+      CU_TRY(vx::launch_scan_tc2(QG, &tq, bf16 ? &h->tmap_docs16 : &h->tmap_docs, a, grid,
+                                 smem2, st));
+    } else {
+      // 256-document tiles halve the per-document query re-streaming from L2 (measured: B=128
+      // bf16 2.31 ms vs 3.78 ms with 128; B=256 3.9 ms vs 4.36 ms) — profiles/r01/
+      const int TD = h->scan_tile ? h->scan_tile : 256;
+      int ns = 0;
+      size_t smem = vx::scan_tc_smem(QT, TD, &ns);
+      if (h->dbg_tc_stages) {  // timing experiments only (VX_DEBUG_TC_STAGES)
+        const int want = h->dbg_tc_stages;
+        if (want >= 2 && want < ns) {
+          smem -= (size_t)(ns - want) * (QT * 16384 + TD * 128 + 16);
+          ns = want;
+        }
+      }
+      a.ns = ns;
+      CU_TRY(vx::launch_scan_tc(QT, TD, &tq, bf16 ? &h->tmap_docs16 : &h->tmap_docs, a, grid,
+                                smem, st));
+    }
+    count_launch(h);
+  }
+  CU_TRY(record_ev(h, h->tev[1], st));
+  // merge each query's lists (P per query, stride grid lists) to the coarse top-k', exact
+  // re-rank — one launch each per run of query groups with the same P (the whole batch
+  // when every group ran on CTA pairs), so the 2-per-SM re-rank CTAs pack full waves
+  const int ldp = grid * vx::kTcListLen;
+  for (int r0 = 0; r0 < B;) {
+    const int P = (pairs && std::min(GS, B - r0) > 128) ? grid / 2 : grid;
+    int r1 = r0;
+    while (r1 < B && ((pairs && std::min(GS, B - r1) > 128) ? grid / 2 : grid) == P) r1 += GS;
+    r1 = std::min(r1, B);
+    const int Bn = r1 - r0;
+    const uint64_t* part = h->d_part + (size_t)r0 * ldp;
+    uint64_t* ck = h->d_ckeys + (size_t)r0 * kp;
+    CU_TRY(vx::launch_merge_topk(part, Bn, P * vx::kTcListLen, kp, 0, ck, nullptr, nullptr, st,
+                                 nullptr, ldp));
+    count_launch(h);
+    CU_TRY(vx::launch_rerank(h->docs, d_q + (size_t)r0 * D, D, ck, Bn, kp, part, P, grid, k,
+                             h->row0,
+                             reinterpret_cast<const float*>(h->d_xnorm), bf16 ? 1 : 0,
+                             keys + (size_t)r0 * k, ids + (size_t)r0 * k,
+                             scores + (size_t)r0 * k, h->d_flags + r0, st));
+    count_launch(h);
+    r0 = r1;
+  }
+  // Certificate failures, entirely on device (no host round trip: the stage stays
+  // capturable in one CUDA graph; every launch below exits at once when its count is 0):
+  //   level 2: compact the failing queries, re-rank all their list entries above the
+  //            deepest truncation point (rerank_wide_kernel) — no index access;
+  //   level 3: the queries that still fail are re-scanned exactly (K1 sized by the device
+  //            count) and scattered back.
+  int* cnt2 = h->d_fcount;      // [count, running total] of level-2 queries
+  int* cnt3 = h->d_fcount + 2;  // [count, running total] of exact re-scans
+  CU_TRY(vx::launch_cert_compact(h->d_flags, B, d_q, D, h->d_fidx, cnt2, h->d_fq, st));
+  count_launch(h);
+  CU_TRY(vx::launch_rerank_wide(h->docs, h->d_fq, D, h->d_fidx, cnt2, h->d_part, B, GS,
+                                pairs ? grid / 2 : 0, grid, k, h->row0,
+                                reinterpret_cast<const float*>(h->d_xnorm), bf16 ? 1 : 0, keys,
+                                ids, scores, h->d_flags, st));
+  count_launch(h);
+  CU_TRY(vx::launch_cert_compact(h->d_flags, B, d_q, D, h->d_fidx, cnt3, h->d_fq, st));
+  count_launch(h);
+  uint64_t* fk = h->d_ckeys;  // reuse: [B][k] (k <= 256)
+  int64_t* fi = h->d_out_ids;
+  float* fs = h->d_out_ms;
+  VX_TRY(local_topk_f32(h, h->d_fq, B, k, fk, fi, fs, st, cnt3));
+  CU_TRY(vx::launch_cert_scatter(h->d_fidx, cnt3, B, k, fk, fi, fs, keys, ids, scores, st));
+  count_launch(h);
+  return VX_OK;
+}
+
+static vx_status local_topk(vx_index* h, const float* d_q, int B, int k, uint64_t* keys,
+                            int64_t* ids, float* scores, cudaStream_t st) {
+  const bool tc = h->scan_algo == VX_SCAN_TC ||
+                  (h->scan_algo == VX_SCAN_AUTO && tc_eligible(h, B, k));
+  if (tc) {
+    if (!tc_eligible(h, B, k)) return fail(VX_ERR_UNSUPPORTED, "tensor-core scan needs k <= 128");
+    return local_topk_tc(h, d_q, B, k, keys, ids, scores, st);
+  }
+  return local_topk_f32(h, d_q, B, k, keys, ids, scores, st);
+}
+
+vx_status run_maxsim(vx_index* h, const float* d_qtok, int B, int nq, const int64_t* d_cand,
+                     int C, float* d_out, cudaStream_t st, int64_t id_lo, int64_t id_hi,
+                     const uint16_t* d_qtok16) {
+  if (!h->tokens) return fail(VX_ERR_STATE, "index has no token store");
+  if (nq < 1 || nq > h->desc.max_qtok) return fail(VX_ERR_INVALID, "nq %d", nq);
+  vx::MaxSimArgs a;
+  a.qtok = d_qtok;
+  a.qtok16 = d_qtok16;
+  a.cand = d_cand;
+  a.table = h->tokens;
+  a.T = h->desc.tok_blocks;
+  a.B = B;
+  a.nq = nq;
+  a.C = C;
+  a.Nd = h->desc.tok_per_doc;
+  a.d = h->desc.tok_dim;
+  a.out = d_out;
+  a.id_lo = id_lo;
+  a.id_hi = id_hi;
+  const bool tc = h->maxsim_algo != VX_MAXSIM_CC &&
+                  vx::maxsim_tc_supported(nq, a.Nd, a.d);
+  if (h->maxsim_algo == VX_MAXSIM_TC && !tc)
+    return fail(VX_ERR_UNSUPPORTED, "tensor-core MaxSim unsupported for nq=%d Nd=%d d=%d", nq, a.Nd, a.d);
+  if (tc)
+    CU_TRY(vx::launch_maxsim_tc(&h->tmap_tok, a, st));
+  else
+    CU_TRY(vx::launch_maxsim(a, st));
+  count_launch(h);
+  return VX_OK;
+}
+
+// ---------------------------------------------------------------- shard exchange
+
+// recv [G][B][k] keys -> [B][G*k] (reusing d_part) for the merge
+__global__ void transpose_shard_kernel(const uint64_t* recv, int G, int B, int k, uint64_t* keys) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int total = G * B * k;
+  if (i < total) {
+    int g = i / (B * k), r = i - g * B * k, b = r / k, j = r - b * k;
+    keys[(size_t)b * G * k + g * k + j] = recv[i];
+  }
+}
+
+// The stage in two parts, shared by rank 0 and the shard ranks:
+//   part 1 (core_topk): the certified local top-k by inner product into h->d_keys/d_ids/d_ip;
+//     G > 1, phase 1: every shard's local top-k KEYS -> rank 0 (grouped send/recv, 8 B per
+//     candidate: a key carries the exact fp32 score and the global id), rank 0 merges to
+//     the global top-k in the same buffers;
+//   part 2 (core_rescore): MaxSim of the top-k, output order (MaxSim desc, id asc).
+//     G > 1, phase 2: rank 0 broadcasts the query tokens and the B x k global winners, each
+//     shard computes MaxSim only for the winners it owns (others -INF, no token loads), an
+//     NCCL max-reduce to rank 0 assembles the scores.  Every shard does 1/G of the MaxSim
+//     work (rescoring each shard's whole local top-k would cost every GPU the full B x k).
+// The split lets the host API upload the query tokens while part 1 runs (they are only
+// read by part 2).
+vx_status core_topk(vx_index* h, const float* d_q, int B, int k, cudaStream_t st) {
+  VX_TRY(local_topk(h, d_q, B, k, h->d_keys, h->d_ids, h->d_ip, st));
+  if (h->nranks == 1) return VX_OK;
+  const int n = B * k;
+  const bool root = h->rank == 0;
+  if (root) CU_TRY(cudaEventRecord(h->pev[2], st));
+  const size_t bytes = (size_t)n * 8;
+  uint64_t* recv = reinterpret_cast<uint64_t*>(h->d_recv);
+  NCCL_TRY(nccl().GroupStart());
+  if (root) {
+    for (int r = 0; r < h->nranks; ++r) {
+      if (r == 0)
+        CU_TRY(cudaMemcpyAsync(recv, h->d_keys, bytes, cudaMemcpyDeviceToDevice, st));
+      else
+        NCCL_TRY(nccl().Recv(recv + (size_t)r * n, bytes, ncclUint8, r, h->comm, st));
+    }
+  } else {
+    NCCL_TRY(nccl().Send(h->d_keys, bytes, ncclUint8, 0, h->comm, st));
+  }
+  NCCL_TRY(nccl().GroupEnd());
+  if (!root) return VX_OK;
+  const int G = h->nranks;
+  transpose_shard_kernel<<<(G * n + 255) / 256, 256, 0, st>>>(recv, G, B, k, h->d_part);
+  count_launch(h);
+  CU_TRY(cudaGetLastError());
+  // keys already carry global ids: id_base 0
+  CU_TRY(vx::launch_merge_topk(h->d_part, B, G * k, k, 0, h->d_keys, h->d_ids, h->d_ip, st));
+  count_launch(h);
+  CU_TRY(cudaEventRecord(h->pev[3], st));
+  return VX_OK;
+}
+
+// d_qtok: rank 0's query tokens (ignored on the shard ranks, which receive them)
+vx_status core_rescore(vx_index* h, const float* d_qtok, int B, int nq, int k,
+                              int64_t* d_ids, float* d_ip, float* d_ms, cudaStream_t st) {
+  if (h->nranks == 1) {
+    VX_TRY(run_maxsim(h, d_qtok, B, nq, h->d_ids, k, h->d_ms, st));
+    CU_TRY(vx::launch_order_by(h->d_ms, h->d_ids, h->d_ip, B, k, d_ids, d_ip, d_ms, st));
+    count_launch(h);
+    return VX_OK;
+  }
+  const int n = B * k;
+  const bool root = h->rank == 0;
+  // the tokens travel as bf16 (the MaxSim operand precision: the kernels round fp32 tokens
+  // with the same RNE anyway, so the scores are unchanged) — half the broadcast bytes
+  const int64_t ntok = (int64_t)B * nq * h->desc.tok_dim;
+  if (root) {
+    CU_TRY(vx::launch_to_bf16(d_qtok, h->d_qtok16, ntok, st));
+    count_launch(h);
+  }
+  NCCL_TRY(nccl().GroupStart());
+  NCCL_TRY(nccl().Broadcast(h->d_qtok16, h->d_qtok16, (size_t)ntok * 2, ncclUint8, 0, h->comm, st));
+  NCCL_TRY(nccl().Broadcast(h->d_ids, h->d_ids, (size_t)n, ncclInt64, 0, h->comm, st));
+  NCCL_TRY(nccl().GroupEnd());
+  VX_TRY(run_maxsim(h, nullptr, B, nq, h->d_ids, k, h->d_ms, st, h->row0, h->row0 + h->n_local,
+                    h->d_qtok16));
+  float* ms_all = reinterpret_cast<float*>(h->d_send);  // [B][k] on rank 0
+  NCCL_TRY(nccl().Reduce(h->d_ms, ms_all, (size_t)n, ncclFloat32, ncclMax, 0, h->comm, st));
+  if (!root) return VX_OK;
+  CU_TRY(vx::launch_order_by(ms_all, h->d_ids, h->d_ip, B, k, d_ids, d_ip, d_ms, st));
+  count_launch(h);
+  return VX_OK;
+}
+
+// CUDA-graph mode (VX_OPT_GRAPHS, single GPU): each part for one (B, k[, nq]) is captured
+// once and replayed — one launch per part instead of ~12 kernels, no host work between the
+// kernels (the batcher hands each batch to the graphs of its size, north star (e)).  The
+// graphs read the handle's fixed input buffers and write its fixed output buffers; user
+// pointers are copied in/out around the replay.  The first batch of a shape runs the part
+// eagerly (it also sets the kernels' smem attributes) and captures it for the next ones.
+enum { PART_TOPK = 1, PART_RESCORE = 2 };
+
+static vx_status part_body(vx_index* h, int part, int B, int nq, int k, cudaStream_t st) {
+  if (part == PART_TOPK) {
+    CU_TRY(record_ev(h, h->tev[2], st));
+    VX_TRY(core_topk(h, h->d_q, B, k, st));
+  } else {
+    VX_TRY(core_rescore(h, h->d_qtok, B, nq, k, h->d_out_ids, h->d_out_ip, h->d_out_ms, st));
+  }
+  CU_TRY(record_ev(h, h->tev[3], st));
+  return VX_OK;
+}
+
+static uint64_t part_key(int part, int B, int nq, int k) {
+  return ((uint64_t)part << 48) | ((uint64_t)B << 24) | ((uint64_t)k << 12) |
+         (uint64_t)(part == PART_RESCORE ? nq : 0);
+}
+
+static vx_status run_part(vx_index* h, int part, int B, int nq, int k, cudaStream_t st) {
+  const uint64_t key = part_key(part, B, nq, k);
+  cudaEvent_t* used;
+  auto it = h->graphs.find(key);
+  if (it != h->graphs.end()) {
+    CU_TRY(cudaGraphLaunch(it->second.exec, st));
+    h->st.kernel_launches += it->second.launches;
+    h->st.graph_replays += 1;
+    used = h->gev;
+  } else {
+    VX_TRY(part_body(h, part, B, nq, k, st));
+    // capture on the handle's stream after the eager run completes (capture records, it
+    // does not execute)
+    CU_TRY(cudaStreamSynchronize(st));
+    const uint64_t before = h->st.kernel_launches;
+    h->tev = h->gev;  // the graph records its own (external) events
+    CU_TRY(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    vx_status s = part_body(h, part, B, nq, k, h->stream);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+    h->tev = h->ev;
+    const int launches = (int)(h->st.kernel_launches - before);
+    h->st.kernel_launches = before;
+    if (s != VX_OK) {
+      if (g) cudaGraphDestroy(g);
+      return s;
+    }
+    if (e != cudaSuccess) return fail(VX_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
+    cudaGraphExec_t ex = nullptr;
+    e = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(VX_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
+    h->graphs[key] = {ex, launches};
+    used = h->ev;  // this call's timing: the eager run
+  }
+  if (part == PART_TOPK) h->ev_start = used;
+  h->ev_end = used;
+  return VX_OK;
+}
+
+// Rank 0 entry, part 1: announce the batch to the shards (header, queries), then top-k.
+vx_status stage_begin(vx_index* h, int op, const float* d_q, int B, int nq, int k,
+                             cudaStream_t st) {
+  if (h->nranks > 1) {
+    if (h->rank != 0) return fail(VX_ERR_STATE, "only rank 0 issues searches; call vx_shard_serve");
+    h->h_hdr[0] = op;
+    h->h_hdr[1] = B;
+    h->h_hdr[2] = k;
+    h->h_hdr[3] = nq;
+    CU_TRY(cudaEventRecord(h->pev[0], st));
+    CU_TRY(cudaMemcpyAsync(h->d_hdr, h->h_hdr, 16, cudaMemcpyHostToDevice, st));
+    NCCL_TRY(nccl().Broadcast(h->d_hdr, h->d_hdr, 4, ncclInt32, 0, h->comm, st));
+    NCCL_TRY(nccl().Broadcast(d_q, h->d_q, (size_t)B * h->desc.dim, ncclFloat32, 0, h->comm, st));
+    CU_TRY(cudaEventRecord(h->pev[1], st));
+  }
+  if (h->use_graphs && h->nranks == 1) {
+    if (d_q != h->d_q)
+      CU_TRY(cudaMemcpyAsync(h->d_q, d_q, (size_t)B * h->desc.dim * 4, cudaMemcpyDeviceToDevice,
+                             st));
+    VX_TRY(run_part(h, PART_TOPK, B, nq, k, st));
+  } else {
+    CU_TRY(record_ev(h, h->tev[2], st));
+    VX_TRY(core_topk(h, d_q, B, k, st));
+    CU_TRY(record_ev(h, h->tev[3], st));
+    h->ev_start = h->ev_end = h->ev;
+  }
+  return VX_OK;
+}
+
+static void stage_done(vx_index* h, int B) {
+  if (h->nranks > 1 && h->rank == 0) {
+    cudaEventRecord(h->pev[4], h->stream_last);
+    h->phases_pending = true;
+  }
+  h->timing_pending = true;
+  h->st.batches += 1;
+  h->st.queries += B;
+}
+
+// part 2 of a search (no rescore): the top-k by inner product to the caller's buffers
+vx_status stage_search_out(vx_index* h, int B, int k, int64_t* d_ids, float* d_ip,
+                                  cudaStream_t st) {
+  const size_t n = (size_t)B * k;
+  CU_TRY(cudaMemcpyAsync(d_ids, h->d_ids, n * 8, cudaMemcpyDeviceToDevice, st));
+  CU_TRY(cudaMemcpyAsync(d_ip, h->d_ip, n * 4, cudaMemcpyDeviceToDevice, st));
+  h->stream_last = st;
+  stage_done(h, B);
+  return VX_OK;
+}
+
+// part 2 of the fused stage: MaxSim rescore + order into the caller's buffers
+vx_status stage_finish(vx_index* h, const float* d_qtok, int B, int nq, int k,
+                              int64_t* d_ids, float* d_ip, float* d_ms, cudaStream_t st) {
+  if (h->use_graphs && h->nranks == 1) {
+    if (d_qtok != h->d_qtok)
+      CU_TRY(cudaMemcpyAsync(h->d_qtok, d_qtok, (size_t)B * nq * h->desc.tok_dim * 4,
+                             cudaMemcpyDeviceToDevice, st));
+    VX_TRY(run_part(h, PART_RESCORE, B, nq, k, st));
+    const size_t n = (size_t)B * k;
+    if (d_ids != h->d_out_ids)
+      CU_TRY(cudaMemcpyAsync(d_ids, h->d_out_ids, n * 8, cudaMemcpyDeviceToDevice, st));
+    if (d_ip != h->d_out_ip)
+      CU_TRY(cudaMemcpyAsync(d_ip, h->d_out_ip, n * 4, cudaMemcpyDeviceToDevice, st));
+    if (d_ms != h->d_out_ms)
+      CU_TRY(cudaMemcpyAsync(d_ms, h->d_out_ms, n * 4, cudaMemcpyDeviceToDevice, st));
+  } else {
+    VX_TRY(core_rescore(h, d_qtok, B, nq, k, d_ids, d_ip, d_ms, st));
+    CU_TRY(record_ev(h, h->tev[3], st));
+    h->ev_end = h->ev;
+  }
+  h->stream_last = st;
+  stage_done(h, B);
+  return VX_OK;
+}
+
+extern "C" vx_status vx_search_dev(vx_index* h, const float* d_q, int32_t B, int32_t k,
+                                   int64_t* d_ids, float* d_scores, void* stream) {
+  if (!h || !d_q || !d_ids || !d_scores) return fail(VX_ERR_INVALID, "null argument");
+  VX_TRY(check_batch(h, B, k));
+  CU_TRY(cudaSetDevice(h->device));
+  cudaStream_t st = pick_stream(h, stream);
+  VX_TRY(stage_begin(h, OP_SEARCH, d_q, B, 0, k, st));
+  return stage_search_out(h, B, k, d_ids, d_scores, st);
+}
+
+extern "C" vx_status vx_search_rescore_dev(vx_index* h, const float* d_q, const float* d_qtok,
+                                           int32_t B, int32_t nq, int32_t k, int64_t* d_ids,
+                                           float* d_ip, float* d_ms, void* stream) {
+  if (!h || !d_q || !d_qtok || !d_ids || !d_ip || !d_ms) return fail(VX_ERR_INVALID, "null argument");
+  VX_TRY(check_batch(h, B, k));
+  if (!h->tokens) return fail(VX_ERR_STATE, "index has no token store");
+  if (nq < 1 || nq > h->desc.max_qtok) return fail(VX_ERR_INVALID, "nq %d", nq);
+  CU_TRY(cudaSetDevice(h->device));
+  cudaStream_t st = pick_stream(h, stream);
+  VX_TRY(stage_begin(h, OP_RESCORE, d_q, B, nq, k, st));
+  return stage_finish(h, d_qtok, B, nq, k, d_ids, d_ip, d_ms, st);
+}
+
+extern "C" vx_status vx_maxsim_dev(vx_index* h, const float* d_qtok, int32_t B, int32_t nq,
+                                   const int64_t* d_cand, int32_t C, float* d_out, void* stream) {
+  if (!h || !d_qtok || !d_cand || !d_out) return fail(VX_ERR_INVALID, "null argument");
+  if (B < 1 || B > h->desc.max_batch || C < 1) return fail(VX_ERR_INVALID, "B %d C %d", B, C);
+  CU_TRY(cudaSetDevice(h->device));
+  return run_maxsim(h, d_qtok, B, nq, d_cand, C, d_out, pick_stream(h, stream));
+}
+
+extern "C" vx_status vx_prepare(vx_index* h, int32_t op, int32_t k, int32_t nq, int32_t b_max) {
+  if (!h) return fail(VX_ERR_INVALID, "null handle");
+  if (op != VX_PREPARE_SEARCH && op != VX_PREPARE_RESCORE) return fail(VX_ERR_INVALID, "op %d", op);
+  VX_TRY(check_batch(h, b_max, k));
+  const bool rescore = op == VX_PREPARE_RESCORE;
+  if (rescore && (!h->tokens || nq < 1 || nq > h->desc.max_qtok))
+    return fail(VX_ERR_INVALID, "rescore needs a token store and 1 <= nq <= max_qtok");
+  if (!h->use_graphs || h->nranks > 1) return VX_OK;
+  CU_TRY(cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  // realistic inputs (generator rows), so every eager run takes the certified fast path
+  CU_TRY(vx::launch_synth_rows(h->d_q, 0x5eedull, 0, b_max, h->desc.dim, st));
+  if (rescore)
+    CU_TRY(vx::launch_synth_rows(h->d_qtok, 0x5eed1ull, 0, (int64_t)b_max * nq, h->desc.tok_dim, st));
+  const vx_stats saved = h->st;
+  for (int B = 1; B <= b_max; ++B) {
+    if (!h->graphs.count(part_key(PART_TOPK, B, 0, k)))
+      VX_TRY(run_part(h, PART_TOPK, B, 0, k, st));
+    if (rescore && !h->graphs.count(part_key(PART_RESCORE, B, nq, k)))
+      VX_TRY(run_part(h, PART_RESCORE, B, nq, k, st));
+  }
+  CU_TRY(cudaStreamSynchronize(st));
+  h->st = saved;  // preload work is not serving work
+  h->timing_pending = false;
+  return VX_OK;
+}
+
+extern "C" vx_status vx_sync(vx_index* h) {
+  if (!h) return fail(VX_ERR_INVALID, "null handle");
+  CU_TRY(cudaSetDevice(h->device));
+  CU_TRY(cudaStreamSynchronize(h->stream));
+  if (h->timing_pending) {
+    cudaEvent_t* E = h->ev_start;
+    cudaEvent_t* F = h->ev_end;
+    CU_TRY(cudaEventSynchronize(F[3]));
+    float a = 0, b = 0;
+    if (cudaEventElapsedTime(&a, E[0], E[1]) == cudaSuccess &&
+        cudaEventElapsedTime(&b, E[2], F[3]) == cudaSuccess) {
+      h->st.last_scan_ms = a;
+      h->st.last_step_ms = b;
+      h->st.scan_ms_total += a;
+      h->st.step_ms_total += b;
+      h->st.timed_batches += 1;
+    }
+    h->timing_pending = false;
+    if (h->phases_pending) {
+      for (int i = 0; i < 4; ++i) {
+        float ms = 0;
+        if (cudaEventElapsedTime(&ms, h->pev[i], h->pev[i + 1]) == cudaSuccess)
+          h->st.phase_ms[i] = ms;
+      }
+      h->phases_pending = false;
+    }
+    int fc[4] = {0, 0, 0, 0};  // certificate levels counted on device
+    CU_TRY(cudaMemcpy(fc, h->d_fcount, 16, cudaMemcpyDeviceToHost));
+    h->st.cert_level2 = (uint64_t)fc[1];
+    h->st.cert_fallbacks = (uint64_t)fc[3];
+  }
+  cudaGetLastError();
+  return VX_OK;
+}
+
