@@ -116,6 +116,37 @@ def test_scan_rejects_bad_shapes(vx):
             idx.search(np.zeros((1, 64), np.float32), 9)
 
 
+def test_errors_are_reported_and_the_handle_stays_usable(vx, oracle):
+    # every rejected call returns a status + message (no exception crosses the ABI, no
+    # partial state): the next valid call on the same handle is exact
+    N, D, k = 2000, 64, 8
+    X = oracle.synth_rows(42, 0, N, D)
+    Q = oracle.synth_rows(43, 0, 3, D)
+    with vx.Index(N, D, tok_per_doc=16, tok_dim=64, tok_blocks=4, max_batch=4, max_k=k,
+                  max_qtok=4) as idx:
+        idx.synth(42)
+        idx.tokens_synth(45)
+        bad = [
+            lambda: idx.set_option(vx.VX_OPT_KPRIME, 3),           # not a power of two
+            lambda: idx.set_option(vx.VX_OPT_KPRIME, 1024),        # > 512
+            lambda: idx.set_option(vx.VX_OPT_SCAN_PAIRS, 5),
+            lambda: idx.set_option(vx.VX_OPT_SCAN_TILE, 64),
+            lambda: idx.set_option(999, 1),                        # unknown option
+            lambda: idx.prepare(k, 5),                             # b_max > max_batch
+            lambda: idx.search(Q, k + 1),                          # k > max_k
+            lambda: idx.search_rescore(Q, np.zeros((3, 5, 64), np.float32), k),  # nq > max_qtok
+            lambda: idx.upload(X[:10], row0=N - 5),                # outside the shard
+            lambda: idx.maxsim(np.zeros((3, 4, 64), np.float32), np.zeros((3, k + 1), np.int64)),
+        ]
+        for f in bad:
+            with pytest.raises(vx.VxError) as e:
+                f()
+            assert str(e.value).split(":", 1)[1].strip()  # a message, not just a code
+        ids, sc = idx.search(Q, k)
+    rid, _ = oracle.flat_topk(X, Q, k, mode=1)
+    assert np.array_equal(ids, rid)
+
+
 def test_maxsim_matches_oracle(vx, oracle, golden):
     g = golden("maxsim_small")
     T, Nd, d = g["table"].shape
