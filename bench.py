@@ -515,7 +515,13 @@ def run_ours(args) -> None:
         kernel_name = ((f"scan_tc{'2' if tc and B > 128 and args.pairs != 0 else ''}_kernel (K2, "
                         f"tcgen05 {'kind::f16 on the bf16 shadow' if bf16 else 'kind::tf32'}"
                         " + fused top-k; exact fp32 re-rank)") if tc else "scan_f32_kernel (K1)")
-        roof.update({"kernel": kernel_name, "scan_ms": scan_ms, "traffic": None})
+        fam = ("scan_tc2" if B > 128 and args.pairs != 0 else "scan_tc") if tc else "scan_f32"
+        tkey = f"{fam}/{'bf16' if bf16 else 'f32'}/{n_local}/{D}"
+        tdb = ROOT / "profiles" / "r01" / "traffic.json"
+        trec = json.loads(tdb.read_text()).get(tkey) if tdb.exists() else None
+        roof.update({"kernel": kernel_name, "scan_ms": scan_ms,
+                     "traffic": trec["dram_bytes"] if trec else None,
+                     "traffic_src": trec["source"] if trec else None})
     cpu = None
     if not args.no_cpu_baseline:
         c = cpu_time(args, args.cpu_budget_s)
