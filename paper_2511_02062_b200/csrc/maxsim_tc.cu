@@ -225,10 +225,21 @@ static cudaError_t launch_ms(const CUtensorMap* tt, const MaxSimArgs& a, cudaStr
   auto kfn = maxsim_tc_kernel<ND, DK>;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
   if (e != cudaSuccess) return e;
-  // enough CTAs to cover 2 per SM, at least 2 candidates per CTA (pipeline)
-  const long pairs = (long)a.B * a.C;
-  int chunk = (int)((pairs + 2 * 148 - 1) / (2 * 148));
-  chunk = chunk < 2 ? 2 : (chunk > 64 ? 64 : chunk);
+  // CTAs: 2 per SM.  Fewer queries than CTA slots: split each query's candidates into
+  // slots / B chunks so the grid is ONE full wave (B = 64, C = 100: 4 x 25 -> 256 CTAs; a
+  // ceil(B*C / slots) chunk gave 320 CTAs = 1.08 waves and a 40 % tail).  Otherwise chunks
+  // of ~B*C / slots candidates (2..64, at least 2 for the pipeline).
+  const int slots = 2 * 148;
+  int chunk;
+  if (a.B < slots) {
+    const int cpq0 = slots / a.B;
+    chunk = (a.C + cpq0 - 1) / cpq0;
+  } else {
+    const long pairs = (long)a.B * a.C;
+    chunk = (int)((pairs + slots - 1) / slots);
+    chunk = chunk > 64 ? 64 : chunk;
+  }
+  chunk = chunk < 2 ? 2 : chunk;
   const int cpq = (a.C + chunk - 1) / chunk;
   kfn<<<a.B * cpq, kMsThreads, C::kSmem, st>>>(*tt, a, chunk, cpq);
   return cudaGetLastError();
