@@ -147,6 +147,16 @@ vx_status vx_maxsim(vx_index* h, const float* qtok, int32_t B, int32_t nq,
 vx_status vx_search_rescore(vx_index* h, const float* queries, const float* qtok, int32_t B,
                             int32_t nq, int32_t k, int64_t* ids, float* ip, float* maxsim);
 
+/* Row-gather variants: query i's vector at q_rows[i] (fp32 [D]) and its tokens at
+ * tok_rows[i] (fp32 [nq][tok_dim]) — e.g. pointers straight into the runtime's query
+ * payloads, so a batch is copied once, into the handle's pinned staging (the C++ operator
+ * adapter uses these: SURVEY §8f "payload codec + pinned-host/H2D zero-copy"). */
+vx_status vx_search_rows(vx_index* h, const float* const* q_rows, int32_t B, int32_t k,
+                         int64_t* ids, float* scores);
+vx_status vx_search_rescore_rows(vx_index* h, const float* const* q_rows,
+                                 const float* const* tok_rows, int32_t B, int32_t nq, int32_t k,
+                                 int64_t* ids, float* ip, float* maxsim);
+
 /* Device-pointer variants (inputs already resident in HBM; asynchronous on stream). */
 vx_status vx_search_dev(vx_index* h, const float* d_queries, int32_t B, int32_t k,
                         int64_t* d_ids, float* d_scores, void* stream);

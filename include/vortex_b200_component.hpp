@@ -159,23 +159,25 @@ inline ComponentFn make_search_component(vx_index* h, std::uint32_t dim, std::ui
     qs.reserve(B);
     for (const auto& p : inputs) qs.push_back(decode_query(p));
     const std::uint32_t nq = qs[0].nq, td = qs[0].tok_dim;
-    std::vector<float> Q(B * dim), T(B * (std::size_t)nq * td);
+    // row pointers straight into the payloads: the library gathers them into its pinned
+    // staging buffer, so every query is copied exactly once on its way to HBM
+    std::vector<const float*> qrows(B), trows(B);
     for (std::size_t i = 0; i < B; ++i) {
       if (qs[i].dim != dim) bad_config("query dim " + std::to_string(qs[i].dim));
       if (qs[i].nq != nq || qs[i].tok_dim != td) bad_config("ragged query tokens in one batch");
-      std::memcpy(Q.data() + i * dim, qs[i].q, 4ull * dim);
-      if (nq) std::memcpy(T.data() + i * (std::size_t)nq * td, qs[i].tok, 4ull * nq * td);
+      qrows[i] = qs[i].q;
+      trows[i] = qs[i].tok;
     }
     std::vector<std::int64_t> ids(B * k);
     std::vector<float> ip(B * k), ms(B * k);
     vx_status s;
     if (nq) {
-      s = vx_search_rescore(h, Q.data(), T.data(), (std::int32_t)B, (std::int32_t)nq,
-                            (std::int32_t)k, ids.data(), ip.data(), ms.data());
-      if (s != VX_OK) gpu_failure("vx_search_rescore", s);
+      s = vx_search_rescore_rows(h, qrows.data(), trows.data(), (std::int32_t)B, (std::int32_t)nq,
+                                 (std::int32_t)k, ids.data(), ip.data(), ms.data());
+      if (s != VX_OK) gpu_failure("vx_search_rescore_rows", s);
     } else {
-      s = vx_search(h, Q.data(), (std::int32_t)B, (std::int32_t)k, ids.data(), ip.data());
-      if (s != VX_OK) gpu_failure("vx_search", s);
+      s = vx_search_rows(h, qrows.data(), (std::int32_t)B, (std::int32_t)k, ids.data(), ip.data());
+      if (s != VX_OK) gpu_failure("vx_search_rows", s);
     }
     out.reserve(B);
     for (std::size_t i = 0; i < B; ++i)

@@ -70,6 +70,8 @@ SIGNATURES = {
     "vx_tokens_download": [P, HP, I64, I64],
     "vx_tokens_upload": [P, HP, I64, I64],
     "vx_search": [P, FP, I32, I32, LP, FP],
+    "vx_search_rows": [P, C.POINTER(FP), I32, I32, LP, FP],
+    "vx_search_rescore_rows": [P, C.POINTER(FP), C.POINTER(FP), I32, I32, I32, LP, FP, FP],
     "vx_maxsim": [P, FP, I32, I32, LP, I32, FP],
     "vx_search_rescore": [P, FP, FP, I32, I32, I32, LP, FP, FP],
     "vx_search_dev": [P, P, I32, I32, P, P, P],

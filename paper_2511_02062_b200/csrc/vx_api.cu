@@ -401,15 +401,32 @@ extern "C" vx_status vx_tokens_upload(vx_index* h, const uint16_t* tok, int64_t 
 }
 
 // ---------------------------------------------------------------- host-buffer API
-extern "C" vx_status vx_search(vx_index* h, const float* q, int32_t B, int32_t k, int64_t* ids,
-                               float* scores) {
-  if (!h || !q || !ids || !scores) return fail(VX_ERR_INVALID, "null argument");
+// Host staging of a batch: one copy into the handle's pinned buffer, either from one
+// contiguous [B][row] array or gathered from B row pointers (e.g. straight out of the
+// runtime's query payloads, so the operator adapter copies each query exactly once).
+static void gather_rows(uint8_t* dst, const float* base, const float* const* rows, int B,
+                        size_t row_bytes) {
+  if (rows)
+    for (int i = 0; i < B; ++i) memcpy(dst + (size_t)i * row_bytes, rows[i], row_bytes);
+  else
+    memcpy(dst, base, (size_t)B * row_bytes);
+}
+
+static bool rows_ok(const float* const* rows, int B) {
+  for (int i = 0; i < B; ++i)
+    if (!rows[i]) return false;
+  return true;
+}
+
+static vx_status host_search(vx_index* h, const float* q, const float* const* q_rows, int32_t B,
+                             int32_t k, int64_t* ids, float* scores) {
   VX_TRY(check_batch(h, B, k));
+  if (q_rows && !rows_ok(q_rows, B)) return fail(VX_ERR_INVALID, "null query row");
   CU_TRY(cudaSetDevice(h->device));
   cudaStream_t st = h->stream;
-  const size_t qb = (size_t)B * h->desc.dim * 4;
+  const size_t qrow = (size_t)h->desc.dim * 4, qb = (size_t)B * qrow;
   uint8_t* stage = static_cast<uint8_t*>(h->h_stage);
-  memcpy(stage, q, qb);
+  gather_rows(stage, q, q_rows, B, qrow);
   CU_TRY(cudaMemcpyAsync(h->d_q, stage, qb, cudaMemcpyHostToDevice, st));
   VX_TRY(stage_begin(h, OP_SEARCH, h->d_q, B, 0, k, st));
   VX_TRY(stage_search_out(h, B, k, h->d_out_ids, h->d_out_ip, st));
@@ -421,6 +438,18 @@ extern "C" vx_status vx_search(vx_index* h, const float* q, int32_t B, int32_t k
   memcpy(ids, hid, (size_t)B * k * 8);
   memcpy(scores, hsc, (size_t)B * k * 4);
   return VX_OK;
+}
+
+extern "C" vx_status vx_search(vx_index* h, const float* q, int32_t B, int32_t k, int64_t* ids,
+                               float* scores) {
+  if (!h || !q || !ids || !scores) return fail(VX_ERR_INVALID, "null argument");
+  return host_search(h, q, nullptr, B, k, ids, scores);
+}
+
+extern "C" vx_status vx_search_rows(vx_index* h, const float* const* q_rows, int32_t B, int32_t k,
+                                    int64_t* ids, float* scores) {
+  if (!h || !q_rows || !ids || !scores) return fail(VX_ERR_INVALID, "null argument");
+  return host_search(h, nullptr, q_rows, B, k, ids, scores);
 }
 
 extern "C" vx_status vx_maxsim(vx_index* h, const float* qtok, int32_t B, int32_t nq,
@@ -446,22 +475,24 @@ extern "C" vx_status vx_maxsim(vx_index* h, const float* qtok, int32_t B, int32_
   return VX_OK;
 }
 
-extern "C" vx_status vx_search_rescore(vx_index* h, const float* q, const float* qtok, int32_t B,
-                                       int32_t nq, int32_t k, int64_t* ids, float* ip,
-                                       float* ms) {
-  if (!h || !q || !qtok || !ids || !ip || !ms) return fail(VX_ERR_INVALID, "null argument");
+static vx_status host_search_rescore(vx_index* h, const float* q, const float* const* q_rows,
+                                     const float* qtok, const float* const* tok_rows, int32_t B,
+                                     int32_t nq, int32_t k, int64_t* ids, float* ip, float* ms) {
   VX_TRY(check_batch(h, B, k));
   if (!h->tokens) return fail(VX_ERR_STATE, "index has no token store");
   if (nq < 1 || nq > h->desc.max_qtok) return fail(VX_ERR_INVALID, "nq %d", nq);
+  if ((q_rows && !rows_ok(q_rows, B)) || (tok_rows && !rows_ok(tok_rows, B)))
+    return fail(VX_ERR_INVALID, "null query row");
   CU_TRY(cudaSetDevice(h->device));
   cudaStream_t st = h->stream;
-  const size_t qb = (size_t)B * h->desc.dim * 4, tb = (size_t)B * nq * h->desc.tok_dim * 4;
+  const size_t qrow = (size_t)h->desc.dim * 4, trow = (size_t)nq * h->desc.tok_dim * 4;
+  const size_t qb = (size_t)B * qrow, tb = (size_t)B * trow;
   uint8_t* stage = static_cast<uint8_t*>(h->h_stage);
-  memcpy(stage, q, qb);
+  gather_rows(stage, q, q_rows, B, qrow);
   CU_TRY(cudaMemcpyAsync(h->d_q, stage, qb, cudaMemcpyHostToDevice, st));
   VX_TRY(stage_begin(h, OP_RESCORE, h->d_q, B, nq, k, st));
   // the query tokens are only read by part 2: stage + upload them while part 1 runs
-  memcpy(stage + qb, qtok, tb);
+  gather_rows(stage + qb, qtok, tok_rows, B, trow);
   CU_TRY(cudaMemcpyAsync(h->d_qtok, stage + qb, tb, cudaMemcpyHostToDevice, h->stream2));
   CU_TRY(cudaEventRecord(h->tok_ev, h->stream2));
   CU_TRY(cudaStreamWaitEvent(st, h->tok_ev, 0));
@@ -475,6 +506,20 @@ extern "C" vx_status vx_search_rescore(vx_index* h, const float* q, const float*
   memcpy(ip, stage + n * 8, n * 4);
   memcpy(ms, stage + n * 12, n * 4);
   return VX_OK;
+}
+
+extern "C" vx_status vx_search_rescore(vx_index* h, const float* q, const float* qtok, int32_t B,
+                                       int32_t nq, int32_t k, int64_t* ids, float* ip,
+                                       float* ms) {
+  if (!h || !q || !qtok || !ids || !ip || !ms) return fail(VX_ERR_INVALID, "null argument");
+  return host_search_rescore(h, q, nullptr, qtok, nullptr, B, nq, k, ids, ip, ms);
+}
+
+extern "C" vx_status vx_search_rescore_rows(vx_index* h, const float* const* q_rows,
+                                            const float* const* tok_rows, int32_t B, int32_t nq,
+                                            int32_t k, int64_t* ids, float* ip, float* ms) {
+  if (!h || !q_rows || !tok_rows || !ids || !ip || !ms) return fail(VX_ERR_INVALID, "null argument");
+  return host_search_rescore(h, nullptr, q_rows, nullptr, tok_rows, B, nq, k, ids, ip, ms);
 }
 
 // ---------------------------------------------------------------- live batcher

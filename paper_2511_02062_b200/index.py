@@ -135,6 +135,30 @@ class Index:
                                          ms.ctypes.data_as(FP)))
         return ids, ip, ms
 
+    def search_rescore_rows(self, q_rows, tok_rows, k: int):
+        """Row-gather variant: per-query arrays (e.g. views into payload buffers); the library
+        copies each once into its pinned staging (vx_search_rescore_rows)."""
+        qs = [_f32(r) for r in q_rows]
+        ts = [_f32(t) for t in tok_rows]
+        B, nq = len(qs), ts[0].shape[0]
+        qp = (FP * B)(*[r.ctypes.data_as(FP) for r in qs])
+        tp = (FP * B)(*[t.ctypes.data_as(FP) for t in ts])
+        ids = np.empty((B, k), np.int64)
+        ip = np.empty((B, k), np.float32)
+        ms = np.empty((B, k), np.float32)
+        check(self.lib.vx_search_rescore_rows(self._h, qp, tp, B, nq, k, ids.ctypes.data_as(LP),
+                                              ip.ctypes.data_as(FP), ms.ctypes.data_as(FP)))
+        return ids, ip, ms
+
+    def search_rows(self, q_rows, k: int) -> tuple[np.ndarray, np.ndarray]:
+        qs = [_f32(r) for r in q_rows]
+        B = len(qs)
+        qp = (FP * B)(*[r.ctypes.data_as(FP) for r in qs])
+        ids = np.empty((B, k), np.int64)
+        sc = np.empty((B, k), np.float32)
+        check(self.lib.vx_search_rows(self._h, qp, B, k, ids.ctypes.data_as(LP), sc.ctypes.data_as(FP)))
+        return ids, sc
+
     # -- device-pointer operators (torch tensors resident in HBM) ------------------------------
     def search_dev(self, q, ids, scores, k: int, stream: int | None = None) -> None:
         check(self.lib.vx_search_dev(self._h, C.c_void_p(q.data_ptr()), q.shape[0], k,

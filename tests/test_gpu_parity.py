@@ -198,6 +198,25 @@ def test_search_rescore_matches_oracle(vx, oracle):
         assert all(ms[b][j] >= ms[b][j + 1] for j in range(k - 1))
 
 
+def test_row_gather_api_equals_contiguous(vx, oracle):
+    # vx_search_rows / vx_search_rescore_rows (payload row pointers, one host copy) give the
+    # same results as the contiguous host API
+    from paper_2511_02062_b200 import synth
+    N, D, k, nq, B = 30_000, 256, 10, 8, 7
+    with vx.Index(N, D, tok_per_doc=64, tok_dim=64, tok_blocks=40, max_batch=B, max_k=k,
+                  max_qtok=nq) as idx:
+        idx.synth(42)
+        idx.tokens_synth(45)
+        Q = synth.rows(43, 3, B, D)
+        qt = synth.query_tokens(B, nq, 64)
+        rows = [Q[i].copy() for i in range(B)]          # separate allocations
+        trows = [qt[i].copy() for i in range(B)]
+        assert all(np.array_equal(a, b) for a, b in zip(idx.search_rows(rows, k), idx.search(Q, k)))
+        got = idx.search_rescore_rows(rows, trows, k)
+        want = idx.search_rescore(Q, qt, k)
+        assert all(np.array_equal(a, b) for a, b in zip(got, want))
+
+
 def test_component_payload_path(vx, oracle):
     N, D, k, T, Nd, d, nq = 5000, 768, 10, 31, 128, 128, 32
     Q = oracle.synth_rows(43, 0, 3, D)
