@@ -25,7 +25,7 @@ def main() -> int:
     import paper_2511_02062_b200 as vx
     N, D, B, k, nq, T = int(os.environ.get("VX_N", "300001")), 768, 9, 100, 32, 211
     idx = vx.Index(N, D, device=local, n_shards=world, shard=rank, tok_per_doc=128, tok_dim=128,
-                   tok_blocks=T, max_batch=16, max_k=128, max_qtok=nq)
+                   tok_blocks=T, max_batch=300, max_k=128, max_qtok=nq)
     idx.synth(42)
     idx.tokens_synth(45)
     uid = [vx.Index.comm_unique_id() if rank == 0 else None]
@@ -39,6 +39,10 @@ def main() -> int:
         qt = synth.query_tokens(B, nq, 128)
         ids_s, sc_s = idx.search(Q, 10)
         ids, ip, ms = idx.search_rescore(Q, qt, k)
+        # a large batch: CTA-pair passes (256 + 44 queries) on every shard, k = 100
+        QL = synth.rows(43, 1000, 300, D)
+        qtl = synth.query_tokens(300, nq, 128, seed=46)
+        ids_l, ip_l, ms_l = idx.search_rescore(QL, qtl, k)
         idx.set_option(vx.VX_OPT_SCAN, vx.VX_SCAN_F32)
         ids_f, sc_f = idx.search(Q[:3], 10)
         idx.shard_stop()
@@ -52,6 +56,11 @@ def main() -> int:
             ok &= sorted(ids[b].tolist()) == sorted(tid[b].tolist())
             lut = dict(zip(tid[b].tolist(), tms[b].tolist()))
             ok &= all(abs(lut[i] - m) <= 1e-5 * abs(lut[i]) for i, m in zip(ids[b].tolist(), ms[b].tolist()))
+        lid, lip, lms = o.search_rescore(X, QL, qtl, table, k, mode=1)
+        for b in range(300):
+            ok &= sorted(ids_l[b].tolist()) == sorted(lid[b].tolist())
+            lut = dict(zip(lid[b].tolist(), lip[b].tolist()))
+            ok &= all(np.float32(lut[i]) == p for i, p in zip(ids_l[b].tolist(), ip_l[b].tolist()))
         print(f"rank0 world={world} parity={'ok' if ok else 'FAIL'} stats={idx.stats()}", flush=True)
     else:
         idx.shard_serve()
