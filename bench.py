@@ -56,15 +56,17 @@ def peaks() -> dict:
             "bf16_tflops": BF16_FALLBACK_TFLOPS, "bf16_tflops_sustained": BF16_FALLBACK_TFLOPS}
 
 
-def scan_roofline(pk: dict, *, tc: bool, bf16: bool, n_local: int, D: int, B: int, k: int,
-                  scan_ms: float) -> dict:
+def scan_roofline(pk: dict, *, tc: bool, coarse: str | None, n_local: int, D: int, B: int,
+                  k: int, scan_ms: float) -> dict:
     """Both ceilings of the candidate scan: HBM (the index bytes it streams +
     queries + results) and compute (2*B*N*D flops on the pipe that runs it).  `bound` is the
     one with the larger minimum time; achieved/peak/frac are reported for it, the other is kept
     alongside.  Tensor peak: MEASURED_PEAKS' sustained cuBLAS bf16 (the scan runs back to back
-    inside a long step); TF32 = half of it (dense kind::tf32 rate); CUDA-core fp32 = 148 SMs x
-    128 FMA/clk x 2 x max clock."""
-    elem = 2 if bf16 else 4
+    inside a long step); TF32 = half of it (dense kind::tf32 rate); s8 = twice it (kind::i8
+    issues M128xN256xK32 in the 128 cycles of a bf16 K16 MMA, profiles/r01/
+    microbench_mma_rate_i8.log); CUDA-core fp32 = 148 SMs x 128 FMA/clk x 2 x max clock.
+    coarse: "bf16" | "tf32" | "i8" for the tensor-core scan (None: the exact K1 scan)."""
+    elem = {"bf16": 2, "i8": 1}.get(coarse, 4)
     hbm_bytes = n_local * D * elem + B * D * elem + B * k * 12
     flops = 2.0 * B * n_local * D
     s = scan_ms / 1e3
@@ -72,9 +74,11 @@ def scan_roofline(pk: dict, *, tc: bool, bf16: bool, n_local: int, D: int, B: in
            "bytes_per_launch": hbm_bytes}
     hbm["frac"] = hbm["achieved"] / hbm["peak"]
     hbm["frac_of_8tbs"] = hbm["achieved"] / 8000.0
+    mult = {"bf16": 1.0, "tf32": 0.5, "i8": 2.0}.get(coarse, 0.0)
     if tc:
-        peak_tf = pk["bf16_tflops_sustained"] * (1.0 if bf16 else 0.5)
-        pipe = "tensor (tcgen05 kind::f16)" if bf16 else "tensor (tcgen05 kind::tf32)"
+        peak_tf = pk["bf16_tflops_sustained"] * mult
+        pipe = {"bf16": "tensor (tcgen05 kind::f16)", "tf32": "tensor (tcgen05 kind::tf32)",
+                "i8": "tensor (tcgen05 kind::i8, TOP/s)"}[coarse]
     else:
         peak_tf = 148 * 128 * 2 * (pk.get("sm_max_mhz") or 1965.0) * 1e6 / 1e12
         pipe = "fp32 FMA (CUDA cores)"
@@ -82,7 +86,7 @@ def scan_roofline(pk: dict, *, tc: bool, bf16: bool, n_local: int, D: int, B: in
             "flops_per_launch": flops}
     comp["frac"] = comp["achieved"] / comp["peak"]
     if tc:
-        comp["frac_of_burst"] = comp["achieved"] / (pk["bf16_tflops"] * (1.0 if bf16 else 0.5))
+        comp["frac_of_burst"] = comp["achieved"] / (pk["bf16_tflops"] * mult)
     t_hbm = hbm_bytes / (hbm["peak"] * 1e9)
     t_comp = flops / (comp["peak"] * 1e12)
     top = hbm if t_hbm >= t_comp else comp
@@ -125,7 +129,7 @@ def parse() -> argparse.Namespace:
     ap.add_argument("--tok-blocks", type=int, default=1 << 18)
     ap.add_argument("--slo-ms", type=float, default=None)
     ap.add_argument("--scan", choices=["auto", "f32", "tc"], default="auto")
-    ap.add_argument("--coarse", choices=["auto", "tf32", "bf16"], default="auto",
+    ap.add_argument("--coarse", choices=["auto", "tf32", "bf16", "i8"], default="auto",
                     help="operand format of the tensor-core candidate scan (exact fp32 re-rank either way)")
     ap.add_argument("--tile", type=int, default=0, choices=[0, 128, 256],
                     help="documents per tensor-core scan tile (0 = library default)")
@@ -314,7 +318,8 @@ def run_ours(args) -> None:
     if args.pairs >= 0:
         idx.set_option(vx.VX_OPT_SCAN_PAIRS, args.pairs)
     if args.coarse != "auto":
-        idx.set_option(vx.VX_OPT_COARSE, {"tf32": vx.VX_COARSE_TF32, "bf16": vx.VX_COARSE_BF16}[args.coarse])
+        idx.set_option(vx.VX_OPT_COARSE, {"tf32": vx.VX_COARSE_TF32, "bf16": vx.VX_COARSE_BF16,
+                                          "i8": vx.VX_COARSE_I8}[args.coarse])
     if args.scan != "auto":
         idx.set_option(vx.VX_OPT_SCAN, {"f32": vx.VX_SCAN_F32, "tc": vx.VX_SCAN_TC}[args.scan])
     if wl != "maxsim":
@@ -504,19 +509,23 @@ def run_ours(args) -> None:
     pk = peaks()
     n_local = idx.n_local
     tc = args.scan == "tc" or (args.scan == "auto" and k <= 128)
-    bf16 = tc and args.coarse != "tf32"
+    coarse = (args.coarse if args.coarse != "auto" else idx.coarse_auto()) if tc else None
+    bf16 = coarse == "bf16"
     if wl == "maxsim":
         roof = maxsim_roofline(pk, B=B, C=C, nq=nq, nd=args.tok_per_doc, d=td, ms=mean_step)
         kernel_name = "maxsim_tc_kernel (K4, tcgen05 kind::f16, fused row-max + sum)"
         roof.update({"kernel": kernel_name, "kernel_ms": mean_step, "traffic": None})
     else:
         scan_ms = st["scan_ms_total"] / max(1, st["timed_batches"])
-        roof = scan_roofline(pk, tc=tc, bf16=bf16, n_local=n_local, D=D, B=B, k=k, scan_ms=scan_ms)
+        roof = scan_roofline(pk, tc=tc, coarse=coarse, n_local=n_local, D=D, B=B, k=k,
+                             scan_ms=scan_ms)
+        kinds = {"bf16": "kind::f16 on the bf16 shadow", "tf32": "kind::tf32",
+                 "i8": "kind::i8 on the s8 shadow"}
         kernel_name = ((f"scan_tc{'2' if tc and B > 128 and args.pairs != 0 else ''}_kernel (K2, "
-                        f"tcgen05 {'kind::f16 on the bf16 shadow' if bf16 else 'kind::tf32'}"
-                        " + fused top-k; exact fp32 re-rank)") if tc else "scan_f32_kernel (K1)")
+                        f"tcgen05 {kinds[coarse]} + fused top-k; exact fp32 re-rank)") if tc
+                       else "scan_f32_kernel (K1)")
         fam = ("scan_tc2" if B > 128 and args.pairs != 0 else "scan_tc") if tc else "scan_f32"
-        tkey = f"{fam}/{'bf16' if bf16 else 'f32'}/{n_local}/{D}"
+        tkey = f"{fam}/{coarse or 'f32'}/{n_local}/{D}"
         tdb = ROOT / "profiles" / "r01" / "traffic.json"
         trec = json.loads(tdb.read_text()).get(tkey) if tdb.exists() else None
         roof.update({"kernel": kernel_name, "scan_ms": scan_ms,
@@ -529,7 +538,7 @@ def run_ours(args) -> None:
     cfg = {"workload": workload_name(args), "baseline_config": WORKLOADS[wl][0],
            "n_docs": args.n_docs, "dim": D, "batch": B, "k": k,
            "shards": world if sharded else 1, "replicas": replicas,
-           "scan": args.scan, "coarse": ("bf16" if bf16 else "tf32") if tc else None}
+           "scan": args.scan, "coarse": coarse}
     if tokens:
         cfg.update({"q_tokens": nq, "doc_tokens": args.tok_per_doc, "tok_dim": td,
                     "tok_blocks": args.tok_blocks})

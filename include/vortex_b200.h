@@ -72,9 +72,12 @@ enum {
 /* Coarse (candidate-selecting) tensor-core scan format.  Either way every reported score is
  * recomputed exactly in fp32 and certified.  BF16 reads a bf16 shadow
  * of the index (half the HBM bytes, 2x the tensor rate); TF32 reads the fp32 rows. */
-enum { VX_COARSE_AUTO = 0, VX_COARSE_TF32 = 1, VX_COARSE_BF16 = 2 };
+enum { VX_COARSE_AUTO = 0, VX_COARSE_TF32 = 1, VX_COARSE_BF16 = 2, VX_COARSE_I8 = 3 };
 /* vx_index_desc.flags */
-enum { VX_FLAG_NO_BF16_SHADOW = 1 /* do not keep the bf16 copy of the index (saves N*D*2 B) */ };
+enum {
+  VX_FLAG_NO_BF16_SHADOW = 1, /* do not keep the bf16 copy of the index (saves N*D*2 B) */
+  VX_FLAG_NO_I8_SHADOW = 2    /* do not keep the s8 copy of the index (saves N*D B) */
+};
 /* MaxSim kernel selection (vx_set_option VX_OPT_MAXSIM). */
 enum { VX_MAXSIM_AUTO = 0, VX_MAXSIM_CC = 1, VX_MAXSIM_TC = 2 };
 
@@ -120,6 +123,9 @@ vx_status vx_index_destroy(vx_index* h);
 /* Rows owned by this handle: [*row0, *row0 + *n_local). */
 vx_status vx_index_shard_range(const vx_index* h, int64_t* row0, int64_t* n_local);
 vx_status vx_set_option(vx_index* h, int32_t option, int64_t value);
+/* Effective value of an option; for VX_OPT_COARSE the format the tensor-core scan will use
+ * (AUTO resolved: VX_COARSE_BF16, VX_COARSE_TF32 or VX_COARSE_I8). */
+vx_status vx_get_option(const vx_index* h, int32_t option, int64_t* value);
 vx_status vx_get_stats(const vx_index* h, vx_stats* out);
 vx_status vx_reset_stats(vx_index* h);
 

@@ -20,8 +20,9 @@ VX_SCAN_AUTO, VX_SCAN_F32, VX_SCAN_TC = 0, 1, 2
 VX_OPT_SCAN, VX_OPT_GRID, VX_OPT_GRAPHS, VX_OPT_MAXSIM = 1, 2, 3, 4
 VX_MAXSIM_AUTO, VX_MAXSIM_CC, VX_MAXSIM_TC = 0, 1, 2
 VX_OPT_COARSE, VX_OPT_SCAN_TILE, VX_OPT_SCAN_PAIRS, VX_OPT_KPRIME = 5, 6, 7, 8
-VX_COARSE_AUTO, VX_COARSE_TF32, VX_COARSE_BF16 = 0, 1, 2
+VX_COARSE_AUTO, VX_COARSE_TF32, VX_COARSE_BF16, VX_COARSE_I8 = 0, 1, 2, 3
 VX_FLAG_NO_BF16_SHADOW = 1
+VX_FLAG_NO_I8_SHADOW = 2
 VX_PREPARE_SEARCH, VX_PREPARE_RESCORE = 1, 2
 
 
@@ -61,6 +62,7 @@ SIGNATURES = {
     "vx_index_destroy": [P],
     "vx_index_shard_range": [P, C.POINTER(I64), C.POINTER(I64)],
     "vx_set_option": [P, I32, I64],
+    "vx_get_option": [P, I32, C.POINTER(I64)],
     "vx_get_stats": [P, C.POINTER(Stats)],
     "vx_reset_stats": [P],
     "vx_index_synth": [P, U64],

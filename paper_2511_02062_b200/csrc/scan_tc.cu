@@ -25,7 +25,6 @@
 
 namespace vx {
 
-constexpr int kTcKC = 16;             // per-CTA list length per query
 constexpr int kTcStageUnit = 16384;   // one 128-row x 128-byte operand tile
 
 // QT: 128-query tiles per launch (A operands); TD: documents per tile (MMA N, 128 or 256).
@@ -40,7 +39,7 @@ struct TcCfg {
   static constexpr int QPT = QT / EG;                               // query tiles per epilogue thread
 };
 
-template <int QT, int TD, bool TF32>
+template <int QT, int TD, int FMT>
 __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
     scan_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tx,
                    const ScanTcArgs a) {
@@ -48,17 +47,18 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   const int ns = a.ns;
-  // per-query candidate lists: [QT*128 queries][16] keys, entry j of query q at [j][q]
+  constexpr int KC = kc_of(FMT);  // per-CTA list length per query
+  // epilogue scratch: the 32 scores of a passing chunk per thread, [32][QT*128] floats
   uint64_t* lists = reinterpret_cast<uint64_t*>(smem + (size_t)ns * C::kStageBytes);
-  uint64_t* full = lists + (size_t)QT * 128 * kTcKC;
+  uint64_t* full = lists + (size_t)QT * 128 * 16;
   uint64_t* empty = full + ns;
   uint64_t* tfull = empty + ns;
   uint64_t* tempty = tfull + C::NBUF;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + C::NBUF);
 
   const int warp = warp_idx_uniform(), lane = threadIdx.x & 31;
-  // K-chunk = one 128-byte swizzle atom: 32 fp32 (kind::tf32) or 64 bf16 (kind::f16)
-  constexpr int cw = TF32 ? 32 : 64;
+  // K-chunk = one 128-byte swizzle atom: 32 fp32 (kind::tf32), 64 bf16 (kind::f16), 128 s8
+  constexpr int cw = FMT == FMT_TF32 ? 32 : (FMT == FMT_I8 ? 128 : 64);
   const int nch = a.D / cw;
   const uint32_t n_local = a.n_local;
   const int ntiles = (int)((n_local + TD - 1) / TD);
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer (whole warp, one elected
     // lane issues; loop state warp-uniform -> uniform-datapath descriptors, see scan_tc2.cu)
-    constexpr uint32_t idesc = make_idesc(TF32 ? 2u : 1u, 128u, (uint32_t)TD);
+    constexpr uint32_t idesc = make_idesc_fmt(FMT, 128u, (uint32_t)TD);
     const uint64_t d0 = umma_desc_sw128(smem_u32(smem));
     int s = 0;
     uint32_t ph = 0;
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
             const uint32_t d = tmem_base + (uint32_t)((buf * QT + qt) * TD);
 #pragma unroll
             for (int j = 0; j < 4; ++j)
-              mma_ss<TF32>(d, ds + (uint64_t)(qt * (kTcStageUnit >> 4) + 2 * j),
+              mma_ss<FMT>(d, ds + (uint64_t)(qt * (kTcStageUnit >> 4) + 2 * j),
                            ds + (uint64_t)(QT * (kTcStageUnit >> 4) + 2 * j), idesc,
                            (c | j) != 0 ? 1u : 0u);
           }
@@ -174,11 +174,11 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
     // chunk are parked in smem so the enumeration can index them.
     constexpr int NEPI = 4 * C::EG * 32;
     float* scratch = reinterpret_cast<float*>(lists) + (e * 32 + lane);  // [32][NEPI]
-    uint64_t L[C::QPT][kTcKC];
+    uint64_t L[C::QPT][KC];
 #pragma unroll
     for (int t = 0; t < C::QPT; ++t)
 #pragma unroll
-      for (int j = 0; j < kTcKC; ++j) L[t][j] = 0ull;
+      for (int j = 0; j < KC; ++j) L[t][j] = 0ull;
     float thr[C::QPT];
 #pragma unroll
     for (int t = 0; t < C::QPT; ++t) thr[t] = -INFINITY;
@@ -199,14 +199,14 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
           tmem_ld32(col + cc * 32, r);
           tmem_ld_wait();
           if (q >= a.B || (a.dbg_no_select & 1)) continue;
-          float mx = __uint_as_float(r[0]);
+          float mx = acc_score<FMT>(r[0]);
 #pragma unroll
-          for (int i = 1; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(r[i]));
+          for (int i = 1; i < 32; ++i) mx = fmaxf(mx, acc_score<FMT>(r[i]));
           if (mx < thr[t]) continue;  // common case after the first tiles
           uint32_t mask = 0;
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
-            const float sc = __uint_as_float(r[i]);
+            const float sc = acc_score<FMT>(r[i]);
             mask |= (sc >= thr[t] ? 1u : 0u) << i;
             scratch[i * NEPI] = sc;
           }
@@ -217,14 +217,14 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
             const uint32_t doc = doc0 + i;
             if (doc >= n_local) break;  // positions are increasing: the rest are padding
             uint64_t key = vx_make_key(scratch[i * NEPI], doc);
-            if (key <= L[t][kTcKC - 1]) continue;
+            if (key <= L[t][KC - 1]) continue;
 #pragma unroll
-            for (int j = 0; j < kTcKC; ++j) {  // insertion into the sorted list
+            for (int j = 0; j < KC; ++j) {  // insertion into the sorted list
               const uint64_t a0 = L[t][j];
               L[t][j] = a0 > key ? a0 : key;
               key = a0 > key ? key : a0;
             }
-            thr[t] = L[t][kTcKC - 1] == 0ull ? -INFINITY : vx_key_score(L[t][kTcKC - 1]);
+            thr[t] = L[t][KC - 1] == 0ull ? -INFINITY : vx_key_score(L[t][KC - 1]);
           }
         }
       }
@@ -241,9 +241,9 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
       const int qt = g + t * C::EG;
       const int q = qt * 128 + m;
       if (q < a.B) {
-        uint64_t* out = a.part + ((size_t)q * gridDim.x + blockIdx.x) * kTcKC;
+        uint64_t* out = a.part + ((size_t)q * gridDim.x + blockIdx.x) * KC;
 #pragma unroll
-        for (int j = 0; j < kTcKC; ++j) out[j] = L[t][j];
+        for (int j = 0; j < KC; ++j) out[j] = L[t][j];
       }
     }
   }
@@ -255,14 +255,59 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
   }
 }
 
-// Certificate-2 error bound E for one query (see rerank_kernel): qn = |q|, q16 = |bf16(q)|,
-// qr = |q - bf16(q)| (each already inflated for fp32 rounding), xstats = shard maxima.
-__device__ __forceinline__ float cert_err_bound(int coarse_bf16, float qn, float q16, float qr,
+// Certificate-2 error bound E for one query (see rerank_kernel): qn = |q|, qh = |q^| and
+// qr = |q - q^| for the coarse operand q^ of the query (bf16(q), or sq * q8), each already
+// inflated for fp32 rounding; xstats = shard maxima [|x|, |bf16 x|, |x - bf16 x|, |sx x8|,
+// |x - sx x8|, sx].
+__device__ __forceinline__ float cert_err_bound(int fmt, float qn, float qh, float qr,
                                                 const float* __restrict__ xstats) {
-  const float xmax = fmaxf(xstats[0], xstats[1]);
-  return (coarse_bf16 ? (q16 * xstats[2] + qr * xstats[1] + qr * xstats[2])
-                      : kErrCoefTF32 * qn * xstats[0]) * 1.001f +
-         0.000244140625f * fmaxf(qn, q16) * xmax + 1e-30f;
+  float e;
+  if (fmt == FMT_TF32) e = kErrCoefTF32 * qn * xstats[0];
+  else if (fmt == FMT_I8) e = qh * xstats[4] + qr * xstats[3] + qr * xstats[4];
+  else e = qh * xstats[2] + qr * xstats[1] + qr * xstats[2];
+  const float xmax = fmaxf(xstats[0], fmt == FMT_I8 ? xstats[3] : xstats[1]);
+  return e * 1.001f + 0.000244140625f * fmaxf(qn, qh) * xmax + 1e-30f;
+}
+
+// The query's coarse operand q^ (bf16 RNE, or sq * rint(q / sq) for s8 — the same rounding
+// as the scan's operands) as squared-norm partial sums: |q|^2, |q^|^2, |q - q^|^2.  The
+// whole block reduces into red[0..2] (smem, 3 x 32 floats); also copies q into qs.
+__device__ __forceinline__ void query_norms(const float* __restrict__ q, int D, int fmt, float sq,
+                                            float* __restrict__ qs, float* red) {
+  float ss = 0.0f, sh = 0.0f, sr = 0.0f;
+  for (int t = threadIdx.x; t < D; t += blockDim.x) {
+    const float v = q[t];
+    const float vh = fmt == FMT_I8 ? sq * (float)vx_quant8(v, sq)
+                                   : vx_bf16_bits_to_f32(vx_f32_to_bf16_bits(v));
+    if (qs) qs[t] = v;
+    ss = fmaf(v, v, ss);
+    sh = fmaf(vh, vh, sh);
+    sr = fmaf(v - vh, v - vh, sr);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    sh += __shfl_xor_sync(0xffffffffu, sh, o);
+    sr += __shfl_xor_sync(0xffffffffu, sr, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[threadIdx.x >> 5] = ss;
+    red[32 + (threadIdx.x >> 5)] = sh;
+    red[64 + (threadIdx.x >> 5)] = sr;
+  }
+}
+// after a __syncthreads: the three norms (inflated for the fp32 sums: s x8 rounds to fp32, so
+// the s8 residual gets 1e-3 of margin, bf16 residuals are exact, Sterbenz)
+__device__ __forceinline__ void query_norms_final(const float* red, int fmt, float* qn, float* qh,
+                                                  float* qr) {
+  float a = 0.0f, b = 0.0f, c = 0.0f;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+    a += red[w];
+    b += red[32 + w];
+    c += red[64 + w];
+  }
+  *qn = sqrtf(a) * 1.0001f;
+  *qh = sqrtf(b) * 1.0001f;
+  *qr = sqrtf(c) * (fmt == FMT_I8 ? 1.001f : 1.0001f);
 }
 
 // ------------------------------------------------------------------- K2b: exact re-rank
@@ -272,39 +317,23 @@ __device__ __forceinline__ float cert_err_bound(int coarse_bf16, float qn, float
 __global__ void __launch_bounds__(256)
     rerank_kernel(const float* __restrict__ docs, const float* __restrict__ qv, int D,
                   const uint64_t* __restrict__ cand, int kp, const uint64_t* __restrict__ part,
-                  int grid, int ldlists, int k, int64_t row0, const float* __restrict__ xstats,
-                  int coarse_bf16,
+                  int grid, int ldlists, int kc, int k, int64_t row0,
+                  const float* __restrict__ xstats, int fmt, const float* __restrict__ qscale,
                   uint64_t* __restrict__ out_keys, int64_t* __restrict__ out_ids,
                   float* __restrict__ out_scores, int* __restrict__ flags, int rows_per_round) {
   extern __shared__ __align__(16) float rsm[];
   float* qs = rsm;                                             // [D]
   uint64_t* keys = reinterpret_cast<uint64_t*>(rsm + ((D + 3) & ~3));  // [kp]
   float* rowbuf = reinterpret_cast<float*>(keys + kp);         // [R][D+4] staged rows
-  __shared__ float s_red[32], s_red16[32], s_redr[32];
+  __shared__ float s_red[96];
   __shared__ int s_fail;
   __shared__ __align__(8) uint64_t s_bar;
   const int b = blockIdx.x;
   const float* q = qv + (size_t)b * D;
-  // ||q||^2, ||bf16(q)||^2, ||q - bf16(q)||^2 (the certificate's error bound, below)
-  float ss = 0.0f, s16 = 0.0f, sr = 0.0f;
-  for (int t = threadIdx.x; t < D; t += blockDim.x) {
-    const float v = q[t];
-    const float v16 = vx_bf16_bits_to_f32(vx_f32_to_bf16_bits(v));
-    qs[t] = v;
-    ss = fmaf(v, v, ss);
-    s16 = fmaf(v16, v16, s16);
-    sr = fmaf(v - v16, v - v16, sr);  // v - v16 is exact (Sterbenz)
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    s16 += __shfl_xor_sync(0xffffffffu, s16, o);
-    sr += __shfl_xor_sync(0xffffffffu, sr, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    s_red[threadIdx.x >> 5] = ss;
-    s_red16[threadIdx.x >> 5] = s16;
-    s_redr[threadIdx.x >> 5] = sr;
-  }
+  // coarse keys are in the coarse pass's units: the s8 pass scores sq * sx * (s32 dot)
+  const float sq = fmt == FMT_I8 ? qscale[b] : 1.0f;
+  const float cscale = fmt == FMT_I8 ? sq * xstats[5] : 1.0f;
+  query_norms(q, D, fmt, sq, qs, s_red);  // the certificate's error bound, below
   if (threadIdx.x == 0) s_fail = 0;
   __syncthreads();
   const uint64_t* cb = cand + (size_t)b * kp;
@@ -352,7 +381,7 @@ __global__ void __launch_bounds__(256)
   }
   // certificate 1: no CTA that truncated its list (16 kept) had its 16th key inside the top-k'
   for (int t = threadIdx.x; t < grid; t += blockDim.x) {
-    const uint64_t last = part[((size_t)b * ldlists + t) * kTcKC + (kTcKC - 1)];
+    const uint64_t last = part[((size_t)b * ldlists + t) * kc + (kc - 1)];
     if (last != 0ull && (tprime == 0ull || last >= tprime)) s_fail = 1;
   }
   __syncthreads();
@@ -380,18 +409,11 @@ __global__ void __launch_bounds__(256)
     //   looser).  TF32 coarse: per-operand truncation <= 2^-10 -> 2^-9 |q| max|x|.
     //   Both: + 2^-12 |q| max|x| for the fp32 accumulation of the tensor core and of the
     //   exact in-order chain (each <= 768 * 2^-24 relative, 5x margin).
-    float qn = 0.0f, q16 = 0.0f, qr = 0.0f;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-      qn += s_red[w];
-      q16 += s_red16[w];
-      qr += s_redr[w];
-    }
-    qn = sqrtf(qn) * 1.0001f;
-    q16 = sqrtf(q16) * 1.0001f;
-    qr = sqrtf(qr) * 1.0001f;
-    const float E = cert_err_bound(coarse_bf16, qn, q16, qr, xstats);
+    float qn, qh, qr;
+    query_norms_final(s_red, fmt, &qn, &qh, &qr);
+    const float E = cert_err_bound(fmt, qn, qh, qr, xstats);
     const uint64_t ek = keys[k - 1];
-    if (ek == 0ull || !(vx_key_score(ek) > vx_key_score(tprime) + E)) s_fail = 1;
+    if (ek == 0ull || !(vx_key_score(ek) > vx_key_score(tprime) * cscale + E)) s_fail = 1;
   }
   __syncthreads();
   for (int i = threadIdx.x; i < k; i += blockDim.x) {
@@ -424,8 +446,9 @@ __global__ void __launch_bounds__(256)
     rerank_wide_kernel(const float* __restrict__ docs, const float* __restrict__ fq, int D,
                        const int* __restrict__ fidx, const int* __restrict__ fcount,
                        const uint64_t* __restrict__ part_all, int B, int GS, int P_pairs,
-                       int P_single, int k, int64_t row0, const float* __restrict__ xstats,
-                       int coarse_bf16, uint64_t* __restrict__ out_keys,
+                       int P_single, int kc, int k, int64_t row0,
+                       const float* __restrict__ xstats, int fmt,
+                       const float* __restrict__ qscale, uint64_t* __restrict__ out_keys,
                        int64_t* __restrict__ out_ids, float* __restrict__ out_scores,
                        int* __restrict__ flags) {
   extern __shared__ __align__(16) float wsm[];
@@ -434,45 +457,28 @@ __global__ void __launch_bounds__(256)
   const int b = fidx[i];
   const int g0 = (b / GS) * GS, Bg = min(GS, B - g0);
   const int P = (P_pairs > 0 && Bg > 128) ? P_pairs : P_single;
-  const int M = P * kTcKC;
+  const int M = P * kc;
   // every query's lists start at a stride of P_single lists (K2 / K2-pairs share it)
-  const uint64_t* lists = part_all + (size_t)b * P_single * kTcKC;
+  const uint64_t* lists = part_all + (size_t)b * P_single * kc;
   int np2 = 16;
   while (np2 < M) np2 <<= 1;
   float* qs = wsm;                                                      // [D]
   uint64_t* keys = reinterpret_cast<uint64_t*>(wsm + ((D + 3) & ~3));   // [np2]
-  __shared__ float s_r0[8], s_r1[8], s_r2[8];
+  __shared__ float s_red[96];
   __shared__ unsigned long long s_t2;
   __shared__ int s_n;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float* q = fq + (size_t)i * D;
-  float ss = 0.0f, s16 = 0.0f, sr = 0.0f;
-  for (int t = threadIdx.x; t < D; t += blockDim.x) {
-    const float v = q[t];
-    const float v16 = vx_bf16_bits_to_f32(vx_f32_to_bf16_bits(v));
-    qs[t] = v;
-    ss = fmaf(v, v, ss);
-    s16 = fmaf(v16, v16, s16);
-    sr = fmaf(v - v16, v - v16, sr);
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    s16 += __shfl_xor_sync(0xffffffffu, s16, o);
-    sr += __shfl_xor_sync(0xffffffffu, sr, o);
-  }
-  if (lane == 0) {
-    s_r0[warp] = ss;
-    s_r1[warp] = s16;
-    s_r2[warp] = sr;
-  }
+  const float sq = fmt == FMT_I8 ? qscale[b] : 1.0f;
+  const float cscale = fmt == FMT_I8 ? sq * xstats[5] : 1.0f;
+  query_norms(q, D, fmt, sq, qs, s_red);
   if (threadIdx.x == 0) {
     s_t2 = 0ull;
     s_n = 0;
   }
   __syncthreads();
-  // T'' = max over full lists of their 16th key (0: no list was truncated)
+  // T'' = max over full lists of their last (kc-th) key (0: no list was truncated)
   for (int p = threadIdx.x; p < P; p += blockDim.x) {
-    const uint64_t last = lists[(size_t)p * kTcKC + (kTcKC - 1)];
+    const uint64_t last = lists[(size_t)p * kc + (kc - 1)];
     if (last) atomicMax(&s_t2, (unsigned long long)last);
   }
   __syncthreads();
@@ -513,16 +519,11 @@ __global__ void __launch_bounds__(256)
   if (threadIdx.x == 0) {
     int fail = 0;
     if (t2 != 0ull) {
-      float qn = 0.0f, q16 = 0.0f, qr = 0.0f;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-        qn += s_r0[w];
-        q16 += s_r1[w];
-        qr += s_r2[w];
-      }
-      const float E = cert_err_bound(coarse_bf16, sqrtf(qn) * 1.0001f, sqrtf(q16) * 1.0001f,
-                                     sqrtf(qr) * 1.0001f, xstats);
+      float qn, qh, qr;
+      query_norms_final(s_red, fmt, &qn, &qh, &qr);
+      const float E = cert_err_bound(fmt, qn, qh, qr, xstats);
       const uint64_t ek = k <= n ? keys[k - 1] : 0ull;
-      fail = (ek == 0ull || !(vx_key_score(ek) > vx_key_score(t2) + E)) ? 1 : 0;
+      fail = (ek == 0ull || !(vx_key_score(ek) > vx_key_score(t2) * cscale + E)) ? 1 : 0;
     }
     s_fail = fail;
     flags[b] = fail;
@@ -548,45 +549,60 @@ __global__ void __launch_bounds__(256)
 // Per-shard maxima for the certificate's error bound: [0] max |x|, [1] max |bf16(x)|,
 // [2] max |x - bf16(x)| over the shard's rows (float bits, atomicMax of non-negative floats).
 __global__ void row_stats_kernel(const float* __restrict__ docs, int64_t n, int D,
-                                 unsigned int* __restrict__ out_bits) {
+                                 unsigned int* __restrict__ out_bits,
+                                 const float* __restrict__ i8_scale) {
   const int lane = threadIdx.x & 31;
   const int64_t wpb = blockDim.x >> 5;
-  float b0 = 0.0f, b1 = 0.0f, b2 = 0.0f;
+  const float sx = i8_scale ? *i8_scale : 0.0f;
+  float b0 = 0.0f, b1 = 0.0f, b2 = 0.0f, b3 = 0.0f, b4 = 0.0f;
   for (int64_t r = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); r < n;
        r += (int64_t)gridDim.x * wpb) {
     const float* x = docs + r * D;
-    float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f;
+    float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f, s3 = 0.0f, s4 = 0.0f;
     for (int c = lane; c < D; c += 32) {
       const float v = x[c];
       const float v16 = vx_bf16_bits_to_f32(vx_f32_to_bf16_bits(v));
       s0 = fmaf(v, v, s0);
       s1 = fmaf(v16, v16, s1);
       s2 = fmaf(v - v16, v - v16, s2);
+      if (i8_scale) {
+        const float v8 = sx * (float)vx_quant8(v, sx);
+        s3 = fmaf(v8, v8, s3);
+        s4 = fmaf(v - v8, v - v8, s4);
+      }
     }
     for (int o = 16; o > 0; o >>= 1) {
       s0 += __shfl_xor_sync(0xffffffffu, s0, o);
       s1 += __shfl_xor_sync(0xffffffffu, s1, o);
       s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      s3 += __shfl_xor_sync(0xffffffffu, s3, o);
+      s4 += __shfl_xor_sync(0xffffffffu, s4, o);
     }
     b0 = fmaxf(b0, sqrtf(s0));
     b1 = fmaxf(b1, sqrtf(s1));
     b2 = fmaxf(b2, sqrtf(s2));
+    b3 = fmaxf(b3, sqrtf(s3));
+    b4 = fmaxf(b4, sqrtf(s4));
   }
   if (lane == 0) {
     atomicMax(&out_bits[0], __float_as_uint(b0 * 1.00001f));
     atomicMax(&out_bits[1], __float_as_uint(b1 * 1.00001f));
     atomicMax(&out_bits[2], __float_as_uint(b2 * 1.00001f));
+    if (i8_scale) {  // s x8 is rounded to fp32 here: 1e-3 of margin for the residual norms
+      atomicMax(&out_bits[3], __float_as_uint(b3 * 1.001f));
+      atomicMax(&out_bits[4], __float_as_uint(b4 * 1.001f));
+    }
   }
 }
 
 // ------------------------------------------------------------------- host side
 cudaError_t launch_rerank_wide(const float* docs, const float* fq, int D, const int* fidx,
                                const int* fcount, const uint64_t* part_all, int B, int GS,
-                               int P_pairs, int P_single, int k, int64_t row0,
-                               const float* xstats, int coarse_bf16, uint64_t* out_keys,
-                               int64_t* out_ids, float* out_scores, int* flags,
-                               cudaStream_t st) {
-  const int M = P_single * kTcKC;
+                               int P_pairs, int P_single, int kc, int k, int64_t row0,
+                               const float* xstats, int fmt, const float* qscale,
+                               uint64_t* out_keys, int64_t* out_ids, float* out_scores,
+                               int* flags, cudaStream_t st) {
+  const int M = P_single * kc;
   int np2 = 16;
   while (np2 < M) np2 <<= 1;
   const size_t smem = (size_t)((D + 3) & ~3) * 4 + (size_t)np2 * 8;
@@ -595,14 +611,15 @@ cudaError_t launch_rerank_wide(const float* docs, const float* fq, int D, const 
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   rerank_wide_kernel<<<B, 256, smem, st>>>(docs, fq, D, fidx, fcount, part_all, B, GS, P_pairs,
-                                           P_single, k, row0, xstats, coarse_bf16, out_keys,
+                                           P_single, kc, k, row0, xstats, fmt, qscale, out_keys,
                                            out_ids, out_scores, flags);
   return cudaGetLastError();
 }
 
-size_t scan_tc_smem(int QT, int TD, int* ns_out) {
+size_t scan_tc_smem(int QT, int TD, int fmt, int* ns_out) {
   const int stage = QT * kTcStageUnit + TD * 128;
-  const size_t fixed = (size_t)QT * 128 * kTcKC * 8 + 16 + 1024;
+  (void)fmt;
+  const size_t fixed = (size_t)QT * 128 * 16 * 8 + 16 + 1024;  // epilogue scratch
   int ns = 6;
   while (ns > 2 && (size_t)ns * stage + fixed + (2 * ns + 4) * 8 > 227 * 1024) --ns;
   *ns_out = ns;
@@ -612,7 +629,9 @@ size_t scan_tc_smem(int QT, int TD, int* ns_out) {
 template <int QT, int TD>
 static cudaError_t launch_tc(const CUtensorMap* tq, const CUtensorMap* tx, const ScanTcArgs& a,
                              int grid, size_t smem, cudaStream_t st) {
-  auto kfn = a.fmt == 2 ? scan_tc_kernel<QT, TD, true> : scan_tc_kernel<QT, TD, false>;
+  auto kfn = a.fmt == FMT_TF32 ? scan_tc_kernel<QT, TD, FMT_TF32>
+                               : (a.fmt == FMT_I8 ? scan_tc_kernel<QT, TD, FMT_I8>
+                                                  : scan_tc_kernel<QT, TD, FMT_BF16>);
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   kfn<<<grid, TcCfg<QT, TD>::kThreads, smem, st>>>(*tq, *tx, a);
@@ -634,9 +653,9 @@ cudaError_t launch_scan_tc(int QT, int TD, const CUtensorMap* tq, const CUtensor
 // (R = 64, one CTA per SM: 4 x 67 us)
 static int kRerankRows = 16;
 cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64_t* cand, int B,
-                          int kp, const uint64_t* part, int grid, int ldlists, int k,
-                          int64_t row0,
-                          const float* xstats, int coarse_bf16, uint64_t* out_keys,
+                          int kp, const uint64_t* part, int grid, int ldlists, int kc, int k,
+                          int64_t row0, const float* xstats, int fmt, const float* qscale,
+                          uint64_t* out_keys,
                           int64_t* out_ids, float* out_scores, int* flags, cudaStream_t st) {
   const size_t base = (size_t)((D + 3) & ~3) * 4 + (size_t)kp * 8;
   const size_t row = (size_t)(D + 4) * 4;
@@ -651,18 +670,18 @@ cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64
   cudaError_t e = cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  rerank_kernel<<<B, 256, smem, st>>>(docs, q, D, cand, kp, part, grid, ldlists, k, row0, xstats,
-                                      coarse_bf16, out_keys, out_ids, out_scores, flags, R);
+  rerank_kernel<<<B, 256, smem, st>>>(docs, q, D, cand, kp, part, grid, ldlists, kc, k, row0,
+                                      xstats, fmt, qscale, out_keys, out_ids, out_scores, flags, R);
   return cudaGetLastError();
 }
 
 cudaError_t launch_row_stats(const float* docs, int64_t n, int D, unsigned int* out_bits,
-                             cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(out_bits, 0, 12, st);
+                             cudaStream_t st, const float* i8_scale) {
+  cudaError_t e = cudaMemsetAsync(out_bits, 0, 20, st);  // [0..4]; [5] = the s8 scale
   if (e != cudaSuccess) return e;
   int64_t blocks = (n + 7) / 8;
   if (blocks > 148 * 32) blocks = 148 * 32;
-  row_stats_kernel<<<(int)(blocks < 1 ? 1 : blocks), 256, 0, st>>>(docs, n, D, out_bits);
+  row_stats_kernel<<<(int)(blocks < 1 ? 1 : blocks), 256, 0, st>>>(docs, n, D, out_bits, i8_scale);
   return cudaGetLastError();
 }
 

@@ -30,7 +30,6 @@
 
 namespace vx {
 
-constexpr int kP2KC = 16;             // per-pair list length per query
 constexpr int kP2Unit = 16384;        // 128 rows x 128 B
 constexpr int kP2SmemLimit = 227 * 1024;
 
@@ -55,7 +54,7 @@ static size_t p2_smem(int nb) {
          (size_t)(2 * C::kNA + 2 * nb + 4) * 8 + 16 + 1024;
 }
 
-template <int QG, bool TF32>
+template <int QG, int FMT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P2Cfg<QG>::kThreads, 1)
     scan_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tx,
                     const ScanTcArgs a) {
@@ -79,7 +78,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P2Cfg<QG>::kThreads,
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-  constexpr int cw = TF32 ? 32 : 64;
+  // K-chunk = one 128-byte swizzle atom: 32 fp32 (tf32), 64 bf16, 128 s8
+  constexpr int cw = FMT == FMT_TF32 ? 32 : (FMT == FMT_I8 ? 128 : 64);
+  constexpr int KC = kc_of(FMT);  // per-pair list length per query
   const int nch = a.D / cw;
   const uint32_t n_local = a.n_local;
   const int ntiles = (int)((n_local + TD - 1) / TD);
@@ -165,7 +166,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P2Cfg<QG>::kThreads,
     // and each MMA is a single UTCHMMA — a single-thread loop paid R2UR waterfalls per
     // MMA and could not keep up with a 2-SM M=256 x N=256 MMA (128 cycles each).
     if (leader) {
-      constexpr uint32_t idesc = make_idesc(TF32 ? 2u : 1u, 256u, 256u);
+      constexpr uint32_t idesc = make_idesc_fmt(FMT, 256u, 256u);
       const uint64_t da0 = umma_desc_sw128(smem_u32(ringA));
       const uint64_t db0 = umma_desc_sw128(smem_u32(ringB));
       int sa = 0, sb = 0, buf = 0;
@@ -188,7 +189,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P2Cfg<QG>::kThreads,
               for (int j = 0; j < 4; ++j)
 #pragma unroll
                 for (int g = 0; g < QG; ++g)
-                  mma_pair_k<TF32>(tmem_base + (uint32_t)((buf * QG + g) * TD),
+                  mma_pair_k<FMT>(tmem_base + (uint32_t)((buf * QG + g) * TD),
                                    da + (uint64_t)(g * (kP2Unit >> 4) + 2 * j), db + 2 * j, idesc,
                                    (c | j) != 0 ? 1u : 0u);
             mma_commit_pair(&emptyA[sa], 0x3);
@@ -222,9 +223,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P2Cfg<QG>::kThreads,
     float* scratch = scratch_base + (e * 32 + lane);  // [32][32*EW]
     constexpr int SS = C::kEpiWarps * 32;             // scratch row stride
     const uint32_t te_leader = mapa_shared(smem_u32(&tempty[0]), 0);
-    uint64_t L[kP2KC];
+    uint64_t L[KC];
 #pragma unroll
-    for (int j = 0; j < kP2KC; ++j) L[j] = 0ull;
+    for (int j = 0; j < KC; ++j) L[j] = 0ull;
     float thr = -INFINITY;
     int buf = 0;
     uint32_t bph = 0;
@@ -238,14 +239,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P2Cfg<QG>::kThreads,
         tmem_ld32(col + cc * 32, r);
         tmem_ld_wait();
         if (q >= a.B || (a.dbg_no_select & 1)) continue;
-        float mx = __uint_as_float(r[0]);
+        float mx = acc_score<FMT>(r[0]);
 #pragma unroll
-        for (int i = 1; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(r[i]));
+        for (int i = 1; i < 32; ++i) mx = fmaxf(mx, acc_score<FMT>(r[i]));
         if (mx < thr) continue;
         uint32_t mask = 0;
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          const float sc = __uint_as_float(r[i]);
+          const float sc = acc_score<FMT>(r[i]);
           mask |= (sc >= thr ? 1u : 0u) << i;
           scratch[i * SS] = sc;
         }
@@ -256,14 +257,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P2Cfg<QG>::kThreads,
           const uint32_t doc = doc0 + i;
           if (doc >= n_local) break;
           uint64_t key = vx_make_key(scratch[i * SS], doc);
-          if (key <= L[kP2KC - 1]) continue;
+          if (key <= L[KC - 1]) continue;
 #pragma unroll
-          for (int j = 0; j < kP2KC; ++j) {
+          for (int j = 0; j < KC; ++j) {
             const uint64_t a0 = L[j];
             L[j] = a0 > key ? a0 : key;
             key = a0 > key ? key : a0;
           }
-          thr = L[kP2KC - 1] == 0ull ? -INFINITY : vx_key_score(L[kP2KC - 1]);
+          thr = L[KC - 1] == 0ull ? -INFINITY : vx_key_score(L[KC - 1]);
         }
       }
       tc_fence_before();
@@ -277,9 +278,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P2Cfg<QG>::kThreads,
     if (q < a.B) {
       // per-query stride = gridDim.x lists (the single-CTA kernel's layout): every query
       // group of a batch shares one layout, so one merge / re-rank launch covers the batch
-      uint64_t* out = a.part + ((size_t)q * gridDim.x + pair) * kP2KC;
+      uint64_t* out = a.part + ((size_t)q * gridDim.x + pair) * KC;
 #pragma unroll
-      for (int j = 0; j < kP2KC; ++j) out[j] = L[j];
+      for (int j = 0; j < KC; ++j) out[j] = L[j];
     }
   }
   tc_fence_before();
@@ -301,9 +302,14 @@ size_t scan_tc2_smem(int QG, int* ns_out) {
 cudaError_t launch_scan_tc2(int QG, const CUtensorMap* tq, const CUtensorMap* tx,
                             const ScanTcArgs& a, int grid, size_t smem, cudaStream_t st) {
   if (grid < 2 || (grid & 1) || (QG != 1 && QG != 2)) return cudaErrorInvalidValue;
-  const bool tf32 = a.fmt == 2;
-  auto kfn = QG == 2 ? (tf32 ? scan_tc2_kernel<2, true> : scan_tc2_kernel<2, false>)
-                     : (tf32 ? scan_tc2_kernel<1, true> : scan_tc2_kernel<1, false>);
+  auto pick = [](int qg, int fmt) {
+    if (qg == 2)
+      return fmt == FMT_TF32 ? scan_tc2_kernel<2, FMT_TF32>
+                             : (fmt == FMT_I8 ? scan_tc2_kernel<2, FMT_I8> : scan_tc2_kernel<2, FMT_BF16>);
+    return fmt == FMT_TF32 ? scan_tc2_kernel<1, FMT_TF32>
+                           : (fmt == FMT_I8 ? scan_tc2_kernel<1, FMT_I8> : scan_tc2_kernel<1, FMT_BF16>);
+  };
+  auto kfn = pick(QG, a.fmt);
   const int threads = QG == 2 ? P2Cfg<2>::kThreads : P2Cfg<1>::kThreads;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

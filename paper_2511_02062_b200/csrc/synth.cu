@@ -72,6 +72,76 @@ cudaError_t launch_to_bf16(const float* in, uint16_t* out, int64_t n, cudaStream
   return cudaGetLastError();
 }
 
+// ---- s8 coarse operands.  The index shadow uses ONE scale per shard, sx = max|x| / 127, so
+// for a fixed query every document's s32 dot product is in the same units and the scan can
+// select on the raw integer; queries use one scale per row, sq = max|q| / 127.  Rounding:
+// v8 = clamp(rint(v / s), -127, 127); the certificate bounds the residual v - s * v8.
+__global__ void absmax_kernel(const float4* __restrict__ in, int64_t n4, unsigned int* out_bits) {
+  float m = 0.0f;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = in[i];
+    m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out_bits, __float_as_uint(m));
+}
+
+__global__ void to_i8_kernel(const float4* __restrict__ in, int64_t n4,
+                             const unsigned int* __restrict__ absmax_bits, char4* __restrict__ out,
+                             float* __restrict__ scale_out) {
+  const float mx = __uint_as_float(*absmax_bits);
+  const float sc = mx > 0.0f ? mx / 127.0f : 1.0f;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *scale_out = sc;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = in[i];
+    out[i] = make_char4(vx_quant8(v.x, sc), vx_quant8(v.y, sc), vx_quant8(v.z, sc), vx_quant8(v.w, sc));
+  }
+}
+
+cudaError_t launch_to_i8_shadow(const float* in, int64_t n, int8_t* out, unsigned int* absmax_bits,
+                                float* scale_out, cudaStream_t st) {
+  if (n % 4) return cudaErrorInvalidValue;
+  const int64_t n4 = n / 4;
+  int64_t blocks = (n4 + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  cudaError_t e = cudaMemsetAsync(absmax_bits, 0, 4, st);
+  if (e != cudaSuccess) return e;
+  absmax_kernel<<<(int)blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(in), n4, absmax_bits);
+  to_i8_kernel<<<(int)blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(in), n4, absmax_bits,
+                                            reinterpret_cast<char4*>(out), scale_out);
+  return cudaGetLastError();
+}
+
+// per-row scales (queries): one block per row
+__global__ void rows_to_i8_kernel(const float* __restrict__ in, int D, int8_t* __restrict__ out,
+                                  float* __restrict__ scales) {
+  __shared__ float s_m[32];
+  const float* x = in + (size_t)blockIdx.x * D;
+  float m = 0.0f;
+  for (int t = threadIdx.x; t < D; t += blockDim.x) m = fmaxf(m, fabsf(x[t]));
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? s_m[threadIdx.x] : 0.0f;
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (threadIdx.x == 0) s_m[0] = v > 0.0f ? v / 127.0f : 1.0f;
+  }
+  __syncthreads();
+  const float sc = s_m[0];
+  if (threadIdx.x == 0) scales[blockIdx.x] = sc;
+  for (int t = threadIdx.x; t < D; t += blockDim.x) out[(size_t)blockIdx.x * D + t] = vx_quant8(x[t], sc);
+}
+
+cudaError_t launch_rows_to_i8(const float* in, int B, int D, int8_t* out, float* scales,
+                              cudaStream_t st) {
+  rows_to_i8_kernel<<<B, 256, 0, st>>>(in, D, out, scales);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_synth_tokens(uint16_t* out, uint64_t seed, int64_t blk0, int64_t nblk, int Nd,
                                 int d, cudaStream_t st) {
   int64_t rows = nblk * Nd;

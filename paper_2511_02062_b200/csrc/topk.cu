@@ -16,7 +16,7 @@
 namespace vx {
 
 constexpr int kMergeThreads = 256;
-constexpr int kMaxK = 512;  // merge: k' up to 512 (the TC candidate set); order_by: k <= 256
+constexpr int kMaxK = 1024;  // merge: k' up to 1024 (the TC candidate set); order_by: k <= 256
 
 __device__ __forceinline__ void block_bitonic_desc(uint64_t* buf, int n) {
   for (int size = 2; size <= n; size <<= 1) {

@@ -166,9 +166,9 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
   if (d->n_shards > 1 && d->shard == 0)
     ALLOC(h->d_recv, (size_t)d->n_shards * B * K * 8);
   ALLOC(h->d_hdr, 16);
-  ALLOC(h->d_ckeys, B * 512 * 8);
+  ALLOC(h->d_ckeys, B * 1024 * 8);
   ALLOC(h->d_flags, B * 4);
-  ALLOC(h->d_xnorm, 16);
+  ALLOC(h->d_xnorm, 32);
   ALLOC(h->d_fq, B * D * 4);
   ALLOC(h->d_fidx, B * 4);
   ALLOC(h->d_fcount, 16);
@@ -177,6 +177,12 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
   if (!(d->flags & VX_FLAG_NO_BF16_SHADOW) && D % 64 == 0) {
     ALLOC(h->docs16, (size_t)h->n_local * D * 2);
     ALLOC(h->d_q16, B * D * 2);
+  }
+  // s8 shadow: K-chunks of 128 s8, and |s32 dot| < 2^24 (exact fp32 keys) needs D <= 1024
+  if (!(d->flags & VX_FLAG_NO_I8_SHADOW) && D % 128 == 0 && D <= 1024) {
+    ALLOC(h->docs8, (size_t)h->n_local * D);
+    ALLOC(h->d_q8, B * D);
+    ALLOC(h->d_qs8, B * 4);
   }
 #undef ALLOC
   if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess ||
@@ -197,7 +203,7 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
     return cleanup(fail(VX_ERR_OOM, "pinned header"));
   if (cudaMallocHost((void**)&h->h_flags, B * 4) != cudaSuccess)
     return cleanup(fail(VX_ERR_OOM, "pinned flags"));
-  if (cudaMemset(h->d_xnorm, 0, 16) != cudaSuccess || cudaMemset(h->d_fcount, 0, 16) != cudaSuccess)
+  if (cudaMemset(h->d_xnorm, 0, 32) != cudaSuccess || cudaMemset(h->d_fcount, 0, 16) != cudaSuccess)
     return cleanup(fail(VX_ERR_CUDA, "memset"));
   if (h->tokens) {
     s = make_tmap_2d(&h->tmap_tok, h->tokens, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
@@ -211,6 +217,11 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
   if (h->docs16) {
     s = make_tmap_2d(&h->tmap_docs16, h->docs16, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                      (uint64_t)h->n_local, D, 64, 128);
+    if (s != VX_OK) return cleanup(s);
+  }
+  if (h->docs8) {
+    s = make_tmap_2d(&h->tmap_docs8, h->docs8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1,
+                     (uint64_t)h->n_local, D, 128, 128);
     if (s != VX_OK) return cleanup(s);
   }
   *out = h;
@@ -227,7 +238,7 @@ extern "C" vx_status vx_index_destroy(vx_index* h) {
                   h->d_ids, h->d_ip,      h->d_ms,     h->d_out_ids, h->d_out_ip,
                   h->d_out_ms, h->d_send, h->d_recv, h->d_hdr, h->d_ckeys, h->d_flags,
                   h->d_xnorm, h->d_fq, h->docs16, h->d_q16, h->d_fidx, h->d_fcount,
-                  h->d_qtok16};
+                  h->d_qtok16, h->docs8, h->d_q8, h->d_qs8};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->h_stage) cudaFreeHost(h->h_stage);
@@ -280,10 +291,13 @@ extern "C" vx_status vx_set_option(vx_index* h, int32_t option, int64_t value) {
       h->scan_tile = (int)value;
       return VX_OK;
     case VX_OPT_COARSE:
-      if (value != VX_COARSE_AUTO && value != VX_COARSE_TF32 && value != VX_COARSE_BF16)
+      if (value != VX_COARSE_AUTO && value != VX_COARSE_TF32 && value != VX_COARSE_BF16 &&
+          value != VX_COARSE_I8)
         return fail(VX_ERR_INVALID, "coarse format %lld", (long long)value);
       if (value == VX_COARSE_BF16 && !h->docs16)
-        return fail(VX_ERR_STATE, "index created with VX_FLAG_NO_BF16_SHADOW");
+        return fail(VX_ERR_STATE, "no bf16 shadow (VX_FLAG_NO_BF16_SHADOW or D %% 64 != 0)");
+      if (value == VX_COARSE_I8 && !h->docs8)
+        return fail(VX_ERR_STATE, "no s8 shadow (VX_FLAG_NO_I8_SHADOW, D %% 128 != 0 or D > 1024)");
       h->coarse = (int)value;
       return VX_OK;
     case VX_OPT_MAXSIM:
@@ -303,6 +317,25 @@ extern "C" vx_status vx_set_option(vx_index* h, int32_t option, int64_t value) {
   }
 }
 
+extern "C" vx_status vx_get_option(const vx_index* h, int32_t option, int64_t* value) {
+  if (!h || !value) return fail(VX_ERR_INVALID, "null argument");
+  switch (option) {
+    case VX_OPT_SCAN: *value = h->scan_algo; return VX_OK;
+    case VX_OPT_GRID: *value = h->grid; return VX_OK;
+    case VX_OPT_GRAPHS: *value = h->use_graphs ? 1 : 0; return VX_OK;
+    case VX_OPT_MAXSIM: *value = h->maxsim_algo; return VX_OK;
+    case VX_OPT_SCAN_TILE: *value = h->scan_tile; return VX_OK;
+    case VX_OPT_SCAN_PAIRS: *value = h->use_pairs; return VX_OK;
+    case VX_OPT_KPRIME: *value = h->kprime; return VX_OK;
+    case VX_OPT_COARSE: {
+      const int f = coarse_fmt(h);
+      *value = f == vx::FMT_I8 ? VX_COARSE_I8 : (f == vx::FMT_TF32 ? VX_COARSE_TF32 : VX_COARSE_BF16);
+      return VX_OK;
+    }
+    default: return fail(VX_ERR_INVALID, "unknown option %d", option);
+  }
+}
+
 extern "C" vx_status vx_get_stats(const vx_index* h, vx_stats* out) {
   if (!h || !out) return fail(VX_ERR_INVALID, "null argument");
   *out = h->st;
@@ -317,17 +350,33 @@ extern "C" vx_status vx_reset_stats(vx_index* h) {
   return VX_OK;
 }
 
+// After the fp32 rows of the shard changed: the coarse-scan shadows and the shard maxima the
+// certificate bounds with.  The s8 scale is shard-wide, so the whole s8 shadow is rebuilt.
+static vx_status refresh_shadows(vx_index* h, int64_t row_off, int64_t nrows) {
+  const int64_t D = h->desc.dim;
+  float* sx = reinterpret_cast<float*>(h->d_xnorm) + 5;
+  if (h->docs8) {
+    CU_TRY(vx::launch_to_i8_shadow(h->docs, h->n_local * D, h->docs8, h->d_xnorm + 6, sx,
+                                   h->stream));
+    count_launch(h, 2);
+  }
+  CU_TRY(vx::launch_row_stats(h->docs, h->n_local, (int)D, h->d_xnorm, h->stream,
+                              h->docs8 ? sx : nullptr));
+  count_launch(h);
+  if (h->docs16 && nrows > 0) {
+    CU_TRY(vx::launch_to_bf16(h->docs + row_off * D, h->docs16 + row_off * D, nrows * D,
+                              h->stream));
+    count_launch(h);
+  }
+  return VX_OK;
+}
+
 extern "C" vx_status vx_index_synth(vx_index* h, uint64_t seed) {
   if (!h) return fail(VX_ERR_INVALID, "null handle");
   CU_TRY(cudaSetDevice(h->device));
   CU_TRY(vx::launch_synth_rows(h->docs, seed, h->row0, h->n_local, h->desc.dim, h->stream));
   count_launch(h);
-  CU_TRY(vx::launch_row_stats(h->docs, h->n_local, h->desc.dim, h->d_xnorm, h->stream));
-  count_launch(h);
-  if (h->docs16) {
-    CU_TRY(vx::launch_to_bf16(h->docs, h->docs16, h->n_local * h->desc.dim, h->stream));
-    count_launch(h);
-  }
+  VX_TRY(refresh_shadows(h, 0, h->n_local));
   CU_TRY(cudaStreamSynchronize(h->stream));
   return VX_OK;
 }
@@ -340,14 +389,8 @@ extern "C" vx_status vx_index_upload(vx_index* h, const float* rows, int64_t row
   CU_TRY(cudaSetDevice(h->device));
   CU_TRY(cudaMemcpyAsync(h->docs + (row0 - h->row0) * h->desc.dim, rows,
                          (size_t)n * h->desc.dim * 4, cudaMemcpyHostToDevice, h->stream));
-  // the TC certificate needs an upper bound on the row norms: recompute over the shard
-  CU_TRY(vx::launch_row_stats(h->docs, h->n_local, h->desc.dim, h->d_xnorm, h->stream));
-  count_launch(h);
-  if (h->docs16 && n > 0) {
-    const size_t off = (size_t)(row0 - h->row0) * h->desc.dim;
-    CU_TRY(vx::launch_to_bf16(h->docs + off, h->docs16 + off, n * h->desc.dim, h->stream));
-    count_launch(h);
-  }
+  // the TC certificate needs the shard maxima and the coarse shadows: recompute
+  VX_TRY(refresh_shadows(h, row0 - h->row0, n));
   CU_TRY(cudaStreamSynchronize(h->stream));
   return VX_OK;
 }

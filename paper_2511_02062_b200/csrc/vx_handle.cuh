@@ -80,6 +80,10 @@ struct vx_index {
   uint16_t* docs16 = nullptr;    // bf16 shadow of the shard (coarse scan), may be null
   CUtensorMap tmap_docs16{};
   uint16_t* d_q16 = nullptr;     // [maxB][D] bf16 queries for the bf16 coarse scan
+  int8_t* docs8 = nullptr;       // s8 shadow (one scale per shard, d_xnorm[5]), may be null
+  CUtensorMap tmap_docs8{};
+  int8_t* d_q8 = nullptr;        // [maxB][D] s8 queries, per-row scales in d_qs8
+  float* d_qs8 = nullptr;
   int coarse = VX_COARSE_AUTO;
   int scan_tile = 0;             // documents per tensor-core tile (0 = auto)
   int kprime = 0;                // TC candidate set size k' (0 = auto; VX_OPT_KPRIME)
@@ -108,7 +112,8 @@ struct vx_index {
   int32_t* d_hdr = nullptr;      // [4]
   uint64_t* d_ckeys = nullptr;   // [maxB][512] merged coarse keys (TC path)
   int* d_flags = nullptr;        // [maxB] certificate failures (TC path)
-  unsigned int* d_xnorm = nullptr;  // [3] row-norm maxima of the shard (float bits, row_stats)
+  unsigned int* d_xnorm = nullptr;  // [8] shard maxima (float bits, row_stats): |x|, |bf16 x|,
+                                    // |x-bf16 x|, |sx x8|, |x-sx x8|; [5] sx; [6] scratch
   float* d_fq = nullptr;         // [maxB][D] queries gathered for the exact fallback
   int* d_fidx = nullptr;         // [maxB] flagged query indices
   int* d_fcount = nullptr;       // [2] flagged count of the last batch, running total
@@ -172,6 +177,7 @@ static inline vx_status check_batch(vx_index* h, int32_t B, int32_t k) {
 }
 
 // ---------------------------------------------------------------- the stage (vx_stage.cu)
+int coarse_fmt(const vx_index* h);  // FMT_* the tensor-core pass uses (VX_OPT_COARSE resolved)
 enum { OP_STOP = 0, OP_SEARCH = 1, OP_RESCORE = 2 };
 
 vx_status run_maxsim(vx_index* h, const float* d_qtok, int B, int nq, const int64_t* d_cand, int C,

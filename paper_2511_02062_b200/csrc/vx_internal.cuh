@@ -38,7 +38,8 @@ struct ScanTcArgs {
   int32_t B;         // queries in this launch (<= QT*128)
   int32_t ns;        // pipeline stages
   int32_t a_rows;    // TMA box rows of the query map (multiple of 8, <= 128)
-  int32_t fmt;       // operand format: 2 = fp32 read as TF32 (kind::tf32), 1 = bf16 (kind::f16)
+  int32_t fmt;       // operand format: FMT_BF16 (kind::f16 on the bf16 shadow), FMT_TF32 (fp32
+                     // rows read as TF32, kind::tf32) or FMT_I8 (s8 shadow, kind::i8, s32)
   int32_t dbg_no_select;  // timing experiments only (VX_DEBUG_TC_NOSELECT): skip the top-k
   uint64_t* part;    // [B][gridDim.x][16] coarse keys
 };
@@ -47,8 +48,24 @@ struct ScanTcArgs {
 // from the actual rounding residuals (rerank_kernel in scan_tc.cu).
 constexpr float kErrCoefTF32 = 0.001953125f;
 cudaError_t launch_to_bf16(const float* in, uint16_t* out, int64_t n, cudaStream_t st);
+// s8 shadow of n fp32 values with one scale (max|x| / 127, written to *scale_out)
+cudaError_t launch_to_i8_shadow(const float* in, int64_t n, int8_t* out, unsigned int* absmax_bits,
+                                float* scale_out, cudaStream_t st);
+// s8 copy of B rows of D with per-row scales (queries)
+cudaError_t launch_rows_to_i8(const float* in, int B, int D, int8_t* out, float* scales,
+                              cudaStream_t st);
+// Coarse operand formats of the tensor-core scan (ScanTcArgs::fmt)
+enum : int { FMT_BF16 = 1, FMT_TF32 = 2, FMT_I8 = 3 };
+// Per-CTA (per-pair) candidate list length per query: 16, or 32 for the s8 coarse pass,
+// whose candidate set k' is 4x larger (its error bound is ~4x the bf16 one).
+__host__ __device__ constexpr int kc_of(int fmt) { return fmt == FMT_I8 ? 32 : 16; }
+// s8 quantisation used by the shadow, the queries and the certificate's residuals
+__device__ __forceinline__ int8_t vx_quant8(float v, float s) {
+  const float r = rintf(v / s);
+  return (int8_t)fminf(fmaxf(r, -127.0f), 127.0f);
+}
 constexpr int kTcListLen = 16;
-size_t scan_tc_smem(int QT, int TD, int* ns_out);
+size_t scan_tc_smem(int QT, int TD, int fmt, int* ns_out);
 cudaError_t launch_scan_tc(int QT, int TD, const CUtensorMap* tq, const CUtensorMap* tx,
                            const ScanTcArgs& a, int grid, size_t smem, cudaStream_t st);
 // CTA-pair variant for 128 < B <= 256 (scan_tc2.cu); grid must be even; lists per pair.
@@ -57,20 +74,21 @@ size_t scan_tc2_smem(int H, int* ns_out);
 cudaError_t launch_scan_tc2(int H, const CUtensorMap* tq, const CUtensorMap* tx,
                             const ScanTcArgs& a, int grid, size_t smem, cudaStream_t st);
 cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64_t* cand, int B,
-                          int kp, const uint64_t* part, int grid, int ldlists, int k,
-                          int64_t row0,
-                          const float* xstats, int coarse_bf16, uint64_t* out_keys,
-                          int64_t* out_ids, float* out_scores, int* flags, cudaStream_t st);
+                          int kp, const uint64_t* part, int grid, int ldlists, int kc, int k,
+                          int64_t row0, const float* xstats, int fmt, const float* qscale,
+                          uint64_t* out_keys, int64_t* out_ids, float* out_scores, int* flags,
+                          cudaStream_t st);
 // second certificate level over the full per-CTA lists (compacted failing queries)
 cudaError_t launch_rerank_wide(const float* docs, const float* fq, int D, const int* fidx,
                                const int* fcount, const uint64_t* part_all, int B, int GS,
-                               int P_pairs, int P_single, int k, int64_t row0,
-                               const float* xstats, int coarse_bf16, uint64_t* out_keys,
-                               int64_t* out_ids, float* out_scores, int* flags,
-                               cudaStream_t st);
-// per-shard maxima [max|x|, max|bf16(x)|, max|x - bf16(x)|] (3 floats as uint bits)
+                               int P_pairs, int P_single, int kc, int k, int64_t row0,
+                               const float* xstats, int fmt, const float* qscale,
+                               uint64_t* out_keys, int64_t* out_ids, float* out_scores,
+                               int* flags, cudaStream_t st);
+// per-shard maxima [max|x|, max|bf16(x)|, max|x - bf16(x)|] (3 floats as uint bits) and, when
+// i8_scale is given, [3] max|sx x8|, [4] max|x - sx x8| of the s8 shadow
 cudaError_t launch_row_stats(const float* docs, int64_t n, int D, unsigned int* out_bits,
-                             cudaStream_t st);
+                             cudaStream_t st, const float* i8_scale = nullptr);
 
 // -------- top-k merge (K3): topk.cu
 // For each query q: select the k largest keys among in[q][0..M), write them

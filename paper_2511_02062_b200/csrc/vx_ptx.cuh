@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "vx_internal.cuh"  // FMT_* operand formats
+
 #define VX_DEV __device__ __forceinline__
 
 namespace vx {
@@ -259,19 +261,61 @@ VX_DEV void mma_pair(uint32_t kind_tf32, uint32_t d_tmem, uint64_t adesc, uint64
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// kind::i8 (s8 x s8, exact s32 accumulate; K = 32 per instruction = the same 32 bytes of K
+// per row as bf16's K = 16)
+VX_DEV void mma_i8_ss(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                      uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+VX_DEV void mma_i8_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// Instruction descriptor per format: f32 accumulate for bf16 / tf32, s32 for s8 x s8.
+//   c_format [4,6) (1 = F32, 2 = S32); a/b_format [7,10)/[10,13) (BF16 = 1, TF32 = 2;
+//   for kind::i8: 1 = signed 8-bit).
+__host__ __device__ constexpr uint32_t make_idesc_fmt(int fmt, uint32_t M, uint32_t N) {
+  return fmt == FMT_I8 ? ((2u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24))
+                       : make_idesc(fmt == FMT_TF32 ? 2u : 1u, M, N);
+}
+
 // Compile-time operand kind (no per-MMA runtime select in the issue loop).
-template <bool TF32>
+template <int FMT>
 VX_DEV void mma_ss(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                    uint32_t accumulate) {
-  if constexpr (TF32)
+  if constexpr (FMT == FMT_TF32)
     mma_tf32_ss(d_tmem, adesc, bdesc, idesc, accumulate);
+  else if constexpr (FMT == FMT_I8)
+    mma_i8_ss(d_tmem, adesc, bdesc, idesc, accumulate);
   else
     mma_f16_ss(d_tmem, adesc, bdesc, idesc, accumulate);
 }
-template <bool TF32>
+template <int FMT>
 VX_DEV void mma_pair_k(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                        uint32_t accumulate) {
-  mma_pair(TF32 ? 1u : 0u, d_tmem, adesc, bdesc, idesc, accumulate);
+  if constexpr (FMT == FMT_I8)
+    mma_i8_pair(d_tmem, adesc, bdesc, idesc, accumulate);
+  else
+    mma_pair(FMT == FMT_TF32 ? 1u : 0u, d_tmem, adesc, bdesc, idesc, accumulate);
+}
+// TMEM accumulator word -> coarse score (s32 products are exact; |sum| < 2^24 converts exactly)
+template <int FMT>
+VX_DEV float acc_score(uint32_t w) {
+  if constexpr (FMT == FMT_I8)
+    return __int2float_rn((int)w);
+  else
+    return __uint_as_float(w);
 }
 // Warp index the compiler can prove warp-uniform (so role branches and the MMA issue loop
 // live on the uniform datapath instead of per-thread registers + R2UR waterfalls).

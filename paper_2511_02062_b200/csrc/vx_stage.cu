@@ -61,9 +61,19 @@ static vx_status local_topk_f32(vx_index* h, const float* d_q, int B, int k, uin
 // measured sweet spot for bf16 at k = 100: with 16-entry per-pair lists, k' = 512 fails
 // certificate 1 for ~13% of queries (a pair holding >= 16 of the top-512), k' = 256 for
 // ~0.03% (profiles/cert_rate.py, profiles/r01/cert_rate.jsonl).
-static int kprime_of(const vx_index* h, int k) {
+// The s8 pass's error bound is ~4x the bf16 one (residual norms of 7-bit integers vs 8-bit
+// mantissas), so its candidate set is 8 next_pow2(k) in [128, 1024] with 32-entry lists.
+static int kprime_of(const vx_index* h, int k, int fmt) {
   if (h->kprime) return std::max(h->kprime, next_pow2(k));
+  if (fmt == vx::FMT_I8) return std::min(1024, std::max(128, 8 * next_pow2(k)));
   return std::min(256, std::max(64, 4 * next_pow2(k)));
+}
+
+// coarse operand format of the tensor-core pass for this handle
+int coarse_fmt(const vx_index* h) {
+  if (h->coarse == VX_COARSE_I8 && h->docs8) return vx::FMT_I8;
+  if (h->coarse == VX_COARSE_TF32 || !h->docs16) return vx::FMT_TF32;
+  return vx::FMT_BF16;
 }
 
 static bool tc_eligible(const vx_index* h, int B, int k) {
@@ -72,18 +82,24 @@ static bool tc_eligible(const vx_index* h, int B, int k) {
   return k <= 128;
 }
 
-// Tensor-core path: K2 coarse scan (top-16 per CTA) -> K3 merge to top-k' -> K2b exact
+// Tensor-core path: K2 coarse scan (top-16/32 per CTA) -> K3 merge to top-k' -> K2b exact
 // re-rank + certificate -> exact re-scan of any query whose certificate failed.
 static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint64_t* keys,
                                int64_t* ids, float* scores, cudaStream_t st) {
   const int D = h->desc.dim;
   const int grid = h->grid;
-  const int kp = kprime_of(h, k);
-  const bool bf16 = h->docs16 && h->coarse != VX_COARSE_TF32;
-  if (D % (bf16 ? 64 : 32)) return fail(VX_ERR_UNSUPPORTED, "TC scan: D %d", D);
+  const int fmt = coarse_fmt(h);
+  const bool bf16 = fmt == vx::FMT_BF16, i8 = fmt == vx::FMT_I8;
+  const int kp = kprime_of(h, k, fmt);
+  const int KC = vx::kc_of(fmt);  // per-CTA list length
+  if (D % (i8 ? 128 : (bf16 ? 64 : 32))) return fail(VX_ERR_UNSUPPORTED, "TC scan: D %d", D);
+  if (kp > 1024) return fail(VX_ERR_UNSUPPORTED, "k' %d > 1024", kp);
   CU_TRY(record_ev(h, h->tev[0], st));
   if (bf16) {
     CU_TRY(vx::launch_to_bf16(d_q, h->d_q16, (int64_t)B * D, st));
+    count_launch(h);
+  } else if (i8) {
+    CU_TRY(vx::launch_rows_to_i8(d_q, B, D, h->d_q8, h->d_qs8, st));
     count_launch(h);
   }
   // queries per pass over the index: 256 (CTA pairs, or the single-CTA kernel's QT = 2 x
@@ -101,6 +117,9 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
     if (bf16)
       VX_TRY(make_tmap_2d(&tq, h->d_q16 + (size_t)g0 * D, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                           (uint64_t)Bg, D, 64, (uint32_t)a_rows));
+    else if (i8)
+      VX_TRY(make_tmap_2d(&tq, h->d_q8 + (size_t)g0 * D, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1,
+                          (uint64_t)Bg, D, 128, (uint32_t)a_rows));
     else
       VX_TRY(make_tmap_2d(&tq, d_q + (size_t)g0 * D, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
                           (uint64_t)Bg, D, 32, (uint32_t)a_rows));
@@ -109,24 +128,23 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
     a.D = D;
     a.B = Bg;
     a.a_rows = a_rows;
-    a.fmt = bf16 ? 1 : 2;
-    a.dbg_no_select = 0;
+    a.fmt = fmt;
     a.dbg_no_select = h->dbg_tc_bits;  // timing experiments only (VX_DEBUG_TC_NOSELECT)
-    a.part = h->d_part + (size_t)g0 * grid * vx::kTcListLen;
+    a.part = h->d_part + (size_t)g0 * grid * KC;
+    const CUtensorMap* tx = i8 ? &h->tmap_docs8 : (bf16 ? &h->tmap_docs16 : &h->tmap_docs);
     if (on_pairs) {
       // 128 < B: CTA pairs (cta_group::2), 256 documents x 256 QG queries per pair tile
       const int QG = Bg > 256 ? 2 : 1;
       int ns2 = 0;
       const size_t smem2 = vx::scan_tc2_smem(QG, &ns2);
       a.ns = ns2;
-      CU_TRY(vx::launch_scan_tc2(QG, &tq, bf16 ? &h->tmap_docs16 : &h->tmap_docs, a, grid,
-                                 smem2, st));
+      CU_TRY(vx::launch_scan_tc2(QG, &tq, tx, a, grid, smem2, st));
     } else {
       // 256-document tiles halve the per-document query re-streaming from L2 (measured: B=128
       // bf16 2.31 ms vs 3.78 ms with 128; B=256 3.9 ms vs 4.36 ms) — profiles/r01/
       const int TD = h->scan_tile ? h->scan_tile : 256;
       int ns = 0;
-      size_t smem = vx::scan_tc_smem(QT, TD, &ns);
+      size_t smem = vx::scan_tc_smem(QT, TD, fmt, &ns);
       if (h->dbg_tc_stages) {  // timing experiments only (VX_DEBUG_TC_STAGES)
         const int want = h->dbg_tc_stages;
         if (want >= 2 && want < ns) {
@@ -135,8 +153,7 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
         }
       }
       a.ns = ns;
-      CU_TRY(vx::launch_scan_tc(QT, TD, &tq, bf16 ? &h->tmap_docs16 : &h->tmap_docs, a, grid,
-                                smem, st));
+      CU_TRY(vx::launch_scan_tc(QT, TD, &tq, tx, a, grid, smem, st));
     }
     count_launch(h);
   }
@@ -144,7 +161,7 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
   // merge each query's lists (P per query, stride grid lists) to the coarse top-k', exact
   // re-rank — one launch each per run of query groups with the same P (the whole batch
   // when every group ran on CTA pairs), so the 2-per-SM re-rank CTAs pack full waves
-  const int ldp = grid * vx::kTcListLen;
+  const int ldp = grid * KC;
   for (int r0 = 0; r0 < B;) {
     const int P = (pairs && std::min(GS, B - r0) > 128) ? grid / 2 : grid;
     int r1 = r0;
@@ -153,14 +170,13 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
     const int Bn = r1 - r0;
     const uint64_t* part = h->d_part + (size_t)r0 * ldp;
     uint64_t* ck = h->d_ckeys + (size_t)r0 * kp;
-    CU_TRY(vx::launch_merge_topk(part, Bn, P * vx::kTcListLen, kp, 0, ck, nullptr, nullptr, st,
-                                 nullptr, ldp));
+    CU_TRY(vx::launch_merge_topk(part, Bn, P * KC, kp, 0, ck, nullptr, nullptr, st, nullptr,
+                                 ldp));
     count_launch(h);
-    CU_TRY(vx::launch_rerank(h->docs, d_q + (size_t)r0 * D, D, ck, Bn, kp, part, P, grid, k,
-                             h->row0,
-                             reinterpret_cast<const float*>(h->d_xnorm), bf16 ? 1 : 0,
-                             keys + (size_t)r0 * k, ids + (size_t)r0 * k,
-                             scores + (size_t)r0 * k, h->d_flags + r0, st));
+    CU_TRY(vx::launch_rerank(h->docs, d_q + (size_t)r0 * D, D, ck, Bn, kp, part, P, grid, KC, k,
+                             h->row0, reinterpret_cast<const float*>(h->d_xnorm), fmt,
+                             i8 ? h->d_qs8 + r0 : nullptr, keys + (size_t)r0 * k,
+                             ids + (size_t)r0 * k, scores + (size_t)r0 * k, h->d_flags + r0, st));
     count_launch(h);
     r0 = r1;
   }
@@ -175,9 +191,9 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
   CU_TRY(vx::launch_cert_compact(h->d_flags, B, d_q, D, h->d_fidx, cnt2, h->d_fq, st));
   count_launch(h);
   CU_TRY(vx::launch_rerank_wide(h->docs, h->d_fq, D, h->d_fidx, cnt2, h->d_part, B, GS,
-                                pairs ? grid / 2 : 0, grid, k, h->row0,
-                                reinterpret_cast<const float*>(h->d_xnorm), bf16 ? 1 : 0, keys,
-                                ids, scores, h->d_flags, st));
+                                pairs ? grid / 2 : 0, grid, KC, k, h->row0,
+                                reinterpret_cast<const float*>(h->d_xnorm), fmt,
+                                i8 ? h->d_qs8 : nullptr, keys, ids, scores, h->d_flags, st));
   count_launch(h);
   CU_TRY(vx::launch_cert_compact(h->d_flags, B, d_q, D, h->d_fidx, cnt3, h->d_fq, st));
   count_launch(h);

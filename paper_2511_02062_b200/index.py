@@ -67,6 +67,16 @@ class Index:
     def set_option(self, option: int, value: int) -> None:
         check(self.lib.vx_set_option(self._h, option, value))
 
+    def get_option(self, option: int) -> int:
+        v = C.c_int64()
+        check(self.lib.vx_get_option(self._h, option, C.byref(v)))
+        return v.value
+
+    def coarse_auto(self) -> str:
+        """The coarse format the tensor-core scan will use: "bf16", "tf32" or "i8"."""
+        return {_lib.VX_COARSE_BF16: "bf16", _lib.VX_COARSE_TF32: "tf32",
+                _lib.VX_COARSE_I8: "i8"}[self.get_option(_lib.VX_OPT_COARSE)]
+
     def stats(self) -> dict:
         s = Stats()
         check(self.lib.vx_get_stats(self._h, C.byref(s)))

@@ -42,7 +42,8 @@ while B <= bmax:
             lat.append(a.elapsed_time(b))
             scan.append(idx.stats()["last_scan_ms"])
     ms, sms = statistics.median(lat), statistics.median(scan)
-    roof = bench.scan_roofline(pk, tc=True, bf16=True, n_local=N, D=D, B=B, k=k, scan_ms=sms)
+    roof = bench.scan_roofline(pk, tc=True, coarse=idx.coarse_auto(), n_local=N, D=D, B=B, k=k,
+                               scan_ms=sms)
     print(json.dumps({"batch": B, "stage_ms": round(ms, 4), "queries_per_s": round(1000.0 * B / ms, 1),
                       "scan_ms": round(sms, 4), "bound": roof["bound"], "frac": round(roof["frac"], 4),
                       "hbm_frac": round(roof["hbm"]["frac"], 4),

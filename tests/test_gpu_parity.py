@@ -267,7 +267,7 @@ def test_tc_scan_bit_identical_to_oracle_f32(vx, oracle, N, D, B, k):
 
 
 @pytest.mark.parametrize("pairs", [1, 2])
-@pytest.mark.parametrize("coarse", ["bf16", "tf32"])
+@pytest.mark.parametrize("coarse", ["bf16", "tf32", "i8"])
 @pytest.mark.parametrize("N,D,B,k", [(60_000, 768, 512, 100), (30_001, 256, 257, 10),
                                      (20_000, 768, 700, 50), (10_000, 128, 1100, 16)])
 def test_tc_pairs_large_batch_bit_identical(vx, oracle, N, D, B, k, coarse, pairs):
@@ -278,7 +278,9 @@ def test_tc_pairs_large_batch_bit_identical(vx, oracle, N, D, B, k, coarse, pair
     with vx.Index(N, D, max_batch=B, max_k=k) as idx:
         idx.synth(42)
         idx.set_option(vx.VX_OPT_SCAN, vx.VX_SCAN_TC)
-        idx.set_option(vx.VX_OPT_COARSE, vx.VX_COARSE_BF16 if coarse == "bf16" else vx.VX_COARSE_TF32)
+        idx.set_option(vx.VX_OPT_COARSE, {"bf16": vx.VX_COARSE_BF16, "tf32": vx.VX_COARSE_TF32,
+                                          "i8": vx.VX_COARSE_I8}[coarse])
+        assert idx.coarse_auto() == coarse
         idx.set_option(vx.VX_OPT_SCAN_PAIRS, pairs)
         ids, sc = idx.search(Q, k)
         fallbacks = idx.stats()["cert_fallbacks"]
@@ -331,6 +333,43 @@ def test_tc_certificate_fallback_many_queries(vx, oracle, B, k):
             assert np.array_equal(sc[v], rsc[v].astype(np.float32))
         st = idx.stats()
     assert st["cert_fallbacks"] >= B // 2
+
+
+@pytest.mark.parametrize("N,D,B,k", [
+    (100_000, 768, 16, 10), (50_000, 768, 1, 1), (20_000, 1024, 8, 100), (12_345, 768, 32, 100),
+    (30_000, 768, 128, 128), (40_000, 256, 129, 10), (25_000, 768, 256, 100), (4097, 128, 5, 7)])
+def test_i8_coarse_bit_identical_to_oracle_f32(vx, oracle, N, D, B, k):
+    # the s8 coarse pass (kind::i8, one scale per shard, per-query scales) only selects;
+    # the certified exact re-rank makes ids and scores the oracle's
+    X = oracle.synth_rows(42, 0, N, D)
+    Q = oracle.synth_rows(43, 0, B, D)
+    with vx.Index(N, D, max_batch=B, max_k=k) as idx:
+        idx.synth(42)
+        idx.set_option(vx.VX_OPT_SCAN, vx.VX_SCAN_TC)
+        idx.set_option(vx.VX_OPT_COARSE, vx.VX_COARSE_I8)
+        ids, sc = idx.search(Q, k)
+        st = idx.stats()
+    rid, rsc = oracle.flat_topk(X, Q, k, mode=1)
+    assert np.array_equal(ids, rid)
+    v = rid >= 0
+    assert np.array_equal(sc[v], rsc[v].astype(np.float32))
+    assert st["cert_fallbacks"] <= max(1, B // 20)
+
+
+def test_i8_shadow_follows_uploads(vx, oracle):
+    # the s8 scale is shard-wide: an upload that raises max|x| must requantise the shadow
+    N, D, B, k = 3000, 128, 6, 10
+    X = oracle.synth_rows(42, 0, N, D)
+    with vx.Index(N, D, max_batch=B, max_k=k) as idx:
+        idx.upload(X)
+        idx.set_option(vx.VX_OPT_COARSE, vx.VX_COARSE_I8)
+        idx.set_option(vx.VX_OPT_SCAN, vx.VX_SCAN_TC)
+        X[17] *= 3.0
+        idx.upload(X[10:20], row0=10)
+        Q = np.stack([X[17] / np.linalg.norm(X[17])] + [X[i] for i in (1, 2, 3, 4, 5)])
+        ids, sc = idx.search(Q, k)
+    rid, rsc = oracle.flat_topk(X, Q, k, mode=1)
+    assert np.array_equal(ids, rid) and ids[0, 0] == 17
 
 
 def test_tc_certificate_forces_exact_fallback(vx, oracle):
