@@ -67,11 +67,13 @@ enum {
                              per pass over the index; 2: 512 queries per pass (two accumulator
                              groups, one TMEM buffer); 0: single-CTA kernels */,
   VX_OPT_KPRIME = 8       /* tensor-core candidate set k' re-ranked exactly: 0 (auto:
-                             4 next_pow2(k) in [64, 256]) or a power of two in [16, 512] */
+                             4 next_pow2(k) in [64, 256] for bf16/tf32, 8 next_pow2(k) in
+                             [128, 1024] for s8) or a power of two in [16, 1024] */
 };
 /* Coarse (candidate-selecting) tensor-core scan format.  Either way every reported score is
  * recomputed exactly in fp32 and certified.  BF16 reads a bf16 shadow
- * of the index (half the HBM bytes, 2x the tensor rate); TF32 reads the fp32 rows. */
+ * of the index (half the HBM bytes, 2x the tensor rate); TF32 reads the fp32 rows; I8 reads an
+ * s8 shadow (one scale per shard, per-query scales; a quarter of the bytes, 2x the bf16 rate). */
 enum { VX_COARSE_AUTO = 0, VX_COARSE_TF32 = 1, VX_COARSE_BF16 = 2, VX_COARSE_I8 = 3 };
 /* vx_index_desc.flags */
 enum {

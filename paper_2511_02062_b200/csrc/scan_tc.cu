@@ -22,6 +22,7 @@
 
 #include "vx_internal.cuh"
 #include "vx_ptx.cuh"
+#include "vx_select.cuh"
 
 namespace vx {
 
@@ -167,13 +168,10 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
     const int g = e >> 2;                 // epilogue group
     const int quad = warp & 3;            // TMEM lane quadrant this warp may access
     const int m = quad * 32 + lane;       // query row within a 128-query tile
-    // Selection.  Fast path: one max over the 32 scores of a column chunk against the
-    // query's admission threshold (the 16th best key so far); only when it passes are the
-    // passing positions enumerated (bit mask) and inserted into the register-resident
-    // descending list with an unrolled compare-exchange network.  The scores of a passing
-    // chunk are parked in smem so the enumeration can index them.
+    // Selection (vx_select.cuh): 64 columns per TMEM load, a max filter per 32-column half
+    // against the query's admission threshold, rare insertions via smem scratch.
     constexpr int NEPI = 4 * C::EG * 32;
-    float* scratch = reinterpret_cast<float*>(lists) + (e * 32 + lane);  // [32][NEPI]
+    uint32_t* scratch = reinterpret_cast<uint32_t*>(lists) + (e * 32 + lane);  // [32][NEPI]
     uint64_t L[C::QPT][KC];
 #pragma unroll
     for (int t = 0; t < C::QPT; ++t)
@@ -194,38 +192,14 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
         const uint32_t col = tmem_base + (uint32_t)((buf * QT + qt) * TD) +
                              ((uint32_t)(quad * 32) << 16);
 #pragma unroll 1
-        for (int cc = 0; cc < TD / 32; ++cc) {
-          uint32_t r[32];
-          tmem_ld32(col + cc * 32, r);
+        for (int cc = 0; cc < TD / 64; ++cc) {
+          uint32_t r[64];
+          tmem_ld64(col + cc * 64, r);
           tmem_ld_wait();
           if (q >= a.B || (a.dbg_no_select & 1)) continue;
-          float mx = acc_score<FMT>(r[0]);
-#pragma unroll
-          for (int i = 1; i < 32; ++i) mx = fmaxf(mx, acc_score<FMT>(r[i]));
-          if (mx < thr[t]) continue;  // common case after the first tiles
-          uint32_t mask = 0;
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const float sc = acc_score<FMT>(r[i]);
-            mask |= (sc >= thr[t] ? 1u : 0u) << i;
-            scratch[i * NEPI] = sc;
-          }
-          const uint32_t doc0 = (uint32_t)tile * TD + cc * 32;
-          while (mask) {
-            const int i = __ffs(mask) - 1;
-            mask &= mask - 1;
-            const uint32_t doc = doc0 + i;
-            if (doc >= n_local) break;  // positions are increasing: the rest are padding
-            uint64_t key = vx_make_key(scratch[i * NEPI], doc);
-            if (key <= L[t][KC - 1]) continue;
-#pragma unroll
-            for (int j = 0; j < KC; ++j) {  // insertion into the sorted list
-              const uint64_t a0 = L[t][j];
-              L[t][j] = a0 > key ? a0 : key;
-              key = a0 > key ? key : a0;
-            }
-            thr[t] = L[t][KC - 1] == 0ull ? -INFINITY : vx_key_score(L[t][KC - 1]);
-          }
+          const uint32_t doc0 = (uint32_t)tile * TD + cc * 64;
+          admit32<FMT, KC>(r, doc0, n_local, scratch, NEPI, L[t], thr[t]);
+          admit32<FMT, KC>(r + 32, doc0 + 32, n_local, scratch, NEPI, L[t], thr[t]);
         }
       }
       tc_fence_before();

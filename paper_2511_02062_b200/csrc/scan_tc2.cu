@@ -27,6 +27,7 @@
 
 #include "vx_internal.cuh"
 #include "vx_ptx.cuh"
+#include "vx_select.cuh"
 
 namespace vx {
 
@@ -65,7 +66,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P2Cfg<QG>::kThreads,
   const int nb = a.ns;  // document stages
   uint8_t* ringA = smem;
   uint8_t* ringB = smem + (size_t)NA * C::kAStage;
-  float* scratch_base = reinterpret_cast<float*>(ringB + (size_t)nb * kP2Unit);  // [32][32*EW]
+  uint32_t* scratch_base = reinterpret_cast<uint32_t*>(ringB + (size_t)nb * kP2Unit);  // [32][32*EW]
   uint64_t* fullA = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(scratch_base) + C::kScratch);
   uint64_t* emptyA = fullA + NA;
   uint64_t* fullB = emptyA + NA;
@@ -220,7 +221,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P2Cfg<QG>::kThreads,
     const int quad = warp & 3;                 // TMEM lane quadrant this warp may access
     const int m = quad * 32 + lane;            // row of this CTA's 128 queries of group g
     const int q = g * 256 + (int)rank * 128 + m;  // query within the launch
-    float* scratch = scratch_base + (e * 32 + lane);  // [32][32*EW]
+    uint32_t* scratch = scratch_base + (e * 32 + lane);  // [32][32*EW]
     constexpr int SS = C::kEpiWarps * 32;             // scratch row stride
     const uint32_t te_leader = mapa_shared(smem_u32(&tempty[0]), 0);
     uint64_t L[KC];
@@ -234,38 +235,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P2Cfg<QG>::kThreads,
       tc_fence_after();
       const uint32_t col = tmem_base + (uint32_t)((buf * QG + g) * TD) + ((uint32_t)(quad * 32) << 16);
 #pragma unroll 1
-      for (int cc = 0; cc < TD / 32; ++cc) {
-        uint32_t r[32];
-        tmem_ld32(col + cc * 32, r);
+      for (int cc = 0; cc < TD / 64; ++cc) {
+        uint32_t r[64];
+        tmem_ld64(col + cc * 64, r);
         tmem_ld_wait();
         if (q >= a.B || (a.dbg_no_select & 1)) continue;
-        float mx = acc_score<FMT>(r[0]);
-#pragma unroll
-        for (int i = 1; i < 32; ++i) mx = fmaxf(mx, acc_score<FMT>(r[i]));
-        if (mx < thr) continue;
-        uint32_t mask = 0;
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float sc = acc_score<FMT>(r[i]);
-          mask |= (sc >= thr ? 1u : 0u) << i;
-          scratch[i * SS] = sc;
-        }
-        const uint32_t doc0 = (uint32_t)tile * TD + cc * 32;  // columns map to docs 1:1
-        while (mask) {
-          const int i = __ffs(mask) - 1;
-          mask &= mask - 1;
-          const uint32_t doc = doc0 + i;
-          if (doc >= n_local) break;
-          uint64_t key = vx_make_key(scratch[i * SS], doc);
-          if (key <= L[KC - 1]) continue;
-#pragma unroll
-          for (int j = 0; j < KC; ++j) {
-            const uint64_t a0 = L[j];
-            L[j] = a0 > key ? a0 : key;
-            key = a0 > key ? key : a0;
-          }
-          thr = L[KC - 1] == 0ull ? -INFINITY : vx_key_score(L[KC - 1]);
-        }
+        const uint32_t doc0 = (uint32_t)tile * TD + cc * 64;  // columns map to docs 1:1
+        admit32<FMT, KC>(r, doc0, n_local, scratch, SS, L, thr);
+        admit32<FMT, KC>(r + 32, doc0 + 32, n_local, scratch, SS, L, thr);
       }
       tc_fence_before();
       __syncwarp();

@@ -277,8 +277,8 @@ extern "C" vx_status vx_set_option(vx_index* h, int32_t option, int64_t value) {
       h->grid = value == 0 ? h->num_sms : (int)value;
       return VX_OK;
     case VX_OPT_KPRIME:
-      if (value != 0 && (value < 16 || value > 512 || (value & (value - 1))))
-        return fail(VX_ERR_INVALID, "kprime %lld (0 or a power of two in [16, 512])", (long long)value);
+      if (value != 0 && (value < 16 || value > 1024 || (value & (value - 1))))
+        return fail(VX_ERR_INVALID, "kprime %lld (0 or a power of two in [16, 1024])", (long long)value);
       h->kprime = (int)value;
       return VX_OK;
     case VX_OPT_SCAN_PAIRS:

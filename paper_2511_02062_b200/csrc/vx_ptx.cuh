@@ -180,6 +180,12 @@ VX_DEV void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
         "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
 }
+VX_DEV void tmem_ld64(uint32_t taddr, uint32_t (&r)[64]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+      : "r"(taddr));
+}
 VX_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // Shared-memory matrix descriptor, K-major operand, SWIZZLE_128B canonical layout:
@@ -217,8 +223,12 @@ VX_DEV uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
   return r;
 }
+// Default .release.cta semantics (as CUTLASS's ClusterBarrier::arrive): the arrive only has
+// to order this thread's completed tcgen05.ld (tcgen05.fence::before_thread_sync) before the
+// peer's MMA, not publish generic memory at cluster scope — .release.cluster compiled to
+// MEMBAR.ALL.GPU + ERRBAR, ~15 % of the scan epilogue's stall samples.
 VX_DEV void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                : "memory");
 }
 // TMA load issued by either CTA of a pair; completion bytes go to the mbarrier at
@@ -316,6 +326,31 @@ VX_DEV float acc_score(uint32_t w) {
     return __int2float_rn((int)w);
   else
     return __uint_as_float(w);
+}
+// Max of a 32-column accumulator chunk as a score, as a balanced tree; for s32 accumulators the
+// max is taken on the integers (IMNMX) and only the winner is converted — the per-chunk filter
+// of the scan epilogues runs on every column, so this is their common-case cost.
+template <int FMT>
+VX_DEV float chunk_max32(const uint32_t (&r)[32]) {
+  if constexpr (FMT == FMT_I8) {
+    int m[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) m[i] = max((int)r[2 * i], (int)r[2 * i + 1]);
+#pragma unroll
+    for (int s = 8; s >= 1; s >>= 1)
+#pragma unroll
+      for (int i = 0; i < s; ++i) m[i] = max(m[i], m[i + s]);
+    return __int2float_rn(m[0]);
+  } else {
+    float m[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) m[i] = fmaxf(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+#pragma unroll
+    for (int s = 8; s >= 1; s >>= 1)
+#pragma unroll
+      for (int i = 0; i < s; ++i) m[i] = fmaxf(m[i], m[i + s]);
+    return m[0];
+  }
 }
 // Warp index the compiler can prove warp-uniform (so role branches and the MMA issue loop
 // live on the uniform datapath instead of per-thread registers + R2UR waterfalls).

@@ -1,0 +1,96 @@
+// vx_select.cuh — the per-query candidate selection shared by the tensor-core scan epilogues
+// (scan_tc.cu, scan_tc2.cu).  One thread owns one query: it reads the query's accumulator row
+// from TMEM 64 columns (= 64 documents) per tcgen05.ld and admits each 32-column half into a
+// register-resident descending list of KC order-preserving (score, id) keys.
+//
+// Fast path: the maxima of the half's four 8-column groups, compared on the raw accumulators
+// (s32 for kind::i8: no conversions) against the query's admission threshold (the KC-th best
+// key so far) — after the first tiles most halves stop here.  Slow path: only the passing
+// groups are compared, their passing positions are enumerated from a bit mask and inserted
+// with an unrolled compare-exchange network; the raw words are parked in smem scratch (stride
+// `ss` words between consecutive columns) so the enumeration can index them.  With 32 queries
+// per warp the slow path is warp-divergent and taken by the warp whenever any lane passes,
+// so its length, not its frequency per query, is what costs.
+#pragma once
+
+#include "vx_ptx.cuh"
+#include "vx_synth.h"
+
+#include <limits.h>
+
+namespace vx {
+
+// Accumulator word -> an order-preserving comparable (s32 for kind::i8, fp32 otherwise).
+template <int FMT>
+struct AccOrd {
+  using T = float;
+  static VX_DEV T of(uint32_t w) { return __uint_as_float(w); }
+  static VX_DEV T thr(float t) { return t; }
+  static VX_DEV T mx(T a, T b) { return fmaxf(a, b); }
+};
+template <>
+struct AccOrd<FMT_I8> {
+  using T = int;
+  static VX_DEV T of(uint32_t w) { return (int)w; }
+  // thresholds are scores of admitted keys (exact integers) or -inf
+  static VX_DEV T thr(float t) { return t == -INFINITY ? INT_MIN : (int)t; }
+  static VX_DEV T mx(T a, T b) { return max(a, b); }
+};
+
+// Insert key (> L[KC-1]) into the descending list.  Every position is computed from the old
+// list at once — new L[j] = key > L[j] ? (key > L[j-1] ? L[j-1] : key) : L[j] — instead of
+// carrying the key through a compare-exchange chain: the same instruction count, but no
+// dependency chain (one epilogue warp per SM sub-partition has nothing else to hide it).
+template <int KC>
+VX_DEV void list_insert(uint64_t (&L)[KC], uint64_t key) {
+  bool c[KC];
+#pragma unroll
+  for (int j = 0; j < KC; ++j) c[j] = key > L[j];
+#pragma unroll
+  for (int j = KC - 1; j > 0; --j) L[j] = c[j] ? (c[j - 1] ? L[j - 1] : key) : L[j];
+  L[0] = c[0] ? key : L[0];
+}
+
+template <int FMT, int KC>
+VX_DEV void admit32(const uint32_t* r, uint32_t doc0, uint32_t n_local, uint32_t* scratch, int ss,
+                    uint64_t (&L)[KC], float& thr) {
+  using O = AccOrd<FMT>;
+  using T = typename O::T;
+  // maxima of the four 8-column groups, then of the half
+  T gm[4];
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    T m0 = O::mx(O::of(r[8 * g + 0]), O::of(r[8 * g + 1]));
+    T m1 = O::mx(O::of(r[8 * g + 2]), O::of(r[8 * g + 3]));
+    T m2 = O::mx(O::of(r[8 * g + 4]), O::of(r[8 * g + 5]));
+    T m3 = O::mx(O::of(r[8 * g + 6]), O::of(r[8 * g + 7]));
+    gm[g] = O::mx(O::mx(m0, m1), O::mx(m2, m3));
+  }
+  const T t = O::thr(thr);
+  if (O::mx(O::mx(gm[0], gm[1]), O::mx(gm[2], gm[3])) < t) return;
+  // only the passing groups are compared and parked (warp-divergent: usually one lane, one
+  // group — the other 31 lanes of the warp wait, so this stays short)
+  uint32_t mask = 0;
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    if (gm[g] < t) continue;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int i = 8 * g + e;
+      mask |= (O::of(r[i]) >= t ? 1u : 0u) << i;
+      scratch[i * ss] = r[i];
+    }
+  }
+  while (mask) {
+    const int i = __ffs(mask) - 1;
+    mask &= mask - 1;
+    const uint32_t doc = doc0 + i;
+    if (doc >= n_local) break;  // positions are increasing: the rest are padding
+    uint64_t key = vx_make_key(acc_score<FMT>(scratch[i * ss]), doc);
+    if (key <= L[KC - 1]) continue;
+    list_insert<KC>(L, key);
+    thr = L[KC - 1] == 0ull ? -INFINITY : vx_key_score(L[KC - 1]);
+  }
+}
+
+}  // namespace vx

@@ -2,7 +2,7 @@
 the HBM-streaming -> tcgen05-GEMM crossover.  One index, search only (top-100), graphs on,
 inputs in HBM; per B: median stage time over 5 reps, the scan kernel time, and both
 rooflines of the scan (bench.scan_roofline).  One JSON line per B.
-usage: python profiles/batch_sweep.py > profiles/r01/batch_sweep.jsonl"""
+usage: python profiles/batch_sweep.py [auto|bf16|tf32|i8] > profiles/r01/batch_sweep.jsonl"""
 import json
 import statistics
 import sys
@@ -21,6 +21,9 @@ bmax = 4096
 idx = vx.Index(N, D, max_batch=bmax, max_k=k)
 idx.synth(42)
 idx.set_option(vx.VX_OPT_GRAPHS, 1)
+if len(sys.argv) > 1:
+    idx.set_option(vx.VX_OPT_COARSE, {"auto": vx.VX_COARSE_AUTO, "bf16": vx.VX_COARSE_BF16,
+                                      "tf32": vx.VX_COARSE_TF32, "i8": vx.VX_COARSE_I8}[sys.argv[1]])
 dev = torch.device("cuda", 0)
 st = torch.cuda.Stream(dev)
 torch.cuda.set_stream(st)

@@ -128,7 +128,7 @@ def test_errors_are_reported_and_the_handle_stays_usable(vx, oracle):
         idx.tokens_synth(45)
         bad = [
             lambda: idx.set_option(vx.VX_OPT_KPRIME, 3),           # not a power of two
-            lambda: idx.set_option(vx.VX_OPT_KPRIME, 1024),        # > 512
+            lambda: idx.set_option(vx.VX_OPT_KPRIME, 2048),        # > 1024
             lambda: idx.set_option(vx.VX_OPT_SCAN_PAIRS, 5),
             lambda: idx.set_option(vx.VX_OPT_SCAN_TILE, 64),
             lambda: idx.set_option(999, 1),                        # unknown option
