@@ -56,8 +56,20 @@ def peaks() -> dict:
             "bf16_tflops": BF16_FALLBACK_TFLOPS, "bf16_tflops_sustained": BF16_FALLBACK_TFLOPS}
 
 
+def scan_passes(tc: bool, B: int, pairs: int) -> tuple[int, int]:
+    """(launches of the scan kernel per batch, queries per launch) for the stage's
+    partitioning (vx_stage.cu local_topk_tc): CTA-pair passes of 512 queries (pairs = 2, the
+    default) or 256 (pairs = 1) for B > 128, one single-CTA pass of <= 256 otherwise; the exact
+    K1 scan (not tc) covers the batch in one launch."""
+    if not tc:
+        return 1, B
+    gs = 512 if pairs in (-1, 2) and B > 256 else 256
+    n = (B + gs - 1) // gs
+    return n, min(B, gs)
+
+
 def scan_roofline(pk: dict, *, tc: bool, coarse: str | None, n_local: int, D: int, B: int,
-                  k: int, scan_ms: float) -> dict:
+                  k: int, scan_ms: float, pairs: int = -1) -> dict:
     """Both ceilings of the candidate scan: HBM (the index bytes it streams +
     queries + results) and compute (2*B*N*D flops on the pipe that runs it).  `bound` is the
     one with the larger minimum time; achieved/peak/frac are reported for it, the other is kept
@@ -67,9 +79,11 @@ def scan_roofline(pk: dict, *, tc: bool, coarse: str | None, n_local: int, D: in
     microbench_mma_rate_i8.log); CUDA-core fp32 = 148 SMs x 128 FMA/clk x 2 x max clock.
     coarse: "bf16" | "tf32" | "i8" for the tensor-core scan (None: the exact K1 scan)."""
     elem = {"bf16": 2, "i8": 1}.get(coarse, 4)
-    hbm_bytes = n_local * D * elem + B * D * elem + B * k * 12
-    flops = 2.0 * B * n_local * D
-    s = scan_ms / 1e3
+    # per launch (one pass over the shard for `bq` queries); the batch takes `launches`
+    launches, bq = scan_passes(tc, B, pairs)
+    hbm_bytes = n_local * D * elem + bq * D * elem + bq * k * 12
+    flops = 2.0 * bq * n_local * D
+    s = scan_ms / 1e3 / launches  # average launch duration
     hbm = {"achieved": hbm_bytes / s / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
            "bytes_per_launch": hbm_bytes}
     hbm["frac"] = hbm["achieved"] / hbm["peak"]
@@ -92,7 +106,8 @@ def scan_roofline(pk: dict, *, tc: bool, coarse: str | None, n_local: int, D: in
     top = hbm if t_hbm >= t_comp else comp
     return {"bound": "hbm" if top is hbm else "tensor", "achieved": top["achieved"],
             "peak": top["peak"], "unit": top["unit"], "frac": top["frac"],
-            "floor_ms": max(t_hbm, t_comp) * 1e3, "hbm": hbm, "compute": comp,
+            "floor_ms": max(t_hbm, t_comp) * 1e3 * launches, "hbm": hbm, "compute": comp,
+            "launches": launches, "queries_per_launch": bq, "launch_ms": s * 1e3,
             "peak_src": pk["src"]}
 
 
@@ -281,7 +296,8 @@ def maxsim_roofline(pk: dict, *, B: int, C: int, nq: int, nd: int, d: int, ms: f
     top = hbm if t_hbm >= t_comp else comp
     return {"bound": "hbm" if top is hbm else "tensor", "achieved": top["achieved"],
             "peak": top["peak"], "unit": top["unit"], "frac": top["frac"],
-            "floor_ms": max(t_hbm, t_comp) * 1e3, "hbm": hbm, "compute": comp,
+            "floor_ms": max(t_hbm, t_comp) * 1e3 * launches, "hbm": hbm, "compute": comp,
+            "launches": launches, "queries_per_launch": bq, "launch_ms": s * 1e3,
             "peak_src": pk["src"]}
 
 
@@ -518,13 +534,15 @@ def run_ours(args) -> None:
     else:
         scan_ms = st["scan_ms_total"] / max(1, st["timed_batches"])
         roof = scan_roofline(pk, tc=tc, coarse=coarse, n_local=n_local, D=D, B=B, k=k,
-                             scan_ms=scan_ms)
+                             scan_ms=scan_ms, pairs=args.pairs)
         kinds = {"bf16": "kind::f16 on the bf16 shadow", "tf32": "kind::tf32",
                  "i8": "kind::i8 on the s8 shadow"}
         kernel_name = ((f"scan_tc{'2' if tc and B > 128 and args.pairs != 0 else ''}_kernel (K2, "
                         f"tcgen05 {kinds[coarse]} + fused top-k; exact fp32 re-rank)") if tc
                        else "scan_f32_kernel (K1)")
         fam = ("scan_tc2" if B > 128 and args.pairs != 0 else "scan_tc") if tc else "scan_f32"
+        if fam == "scan_tc2" and roof["queries_per_launch"] > 256:
+            fam = "scan_tc2_qg2"  # two query groups on 128-document tiles
         tkey = f"{fam}/{coarse or 'f32'}/{n_local}/{D}"
         tdb = ROOT / "profiles" / "r01" / "traffic.json"
         trec = json.loads(tdb.read_text()).get(tkey) if tdb.exists() else None

@@ -63,9 +63,9 @@ enum {
   VX_OPT_MAXSIM = 4,      /* one of VX_MAXSIM_* */
   VX_OPT_COARSE = 5,      /* one of VX_COARSE_*: operand format of the tensor-core scan */
   VX_OPT_SCAN_TILE = 6,   /* documents per tensor-core scan tile: 0 (auto), 128 or 256 */
-  VX_OPT_SCAN_PAIRS = 7   /* 1 (default): CTA-pair (cta_group::2) scan for B > 128, 256 queries
-                             per pass over the index; 2: 512 queries per pass (two accumulator
-                             groups, one TMEM buffer); 0: single-CTA kernels */,
+  VX_OPT_SCAN_PAIRS = 7   /* 2 (default): CTA-pair (cta_group::2) scan for B > 128, 512 queries
+                             per pass (two query groups on 128-document tiles) when B > 256;
+                             1: 256 queries per pass; 0: single-CTA kernels */,
   VX_OPT_KPRIME = 8       /* tensor-core candidate set k' re-ranked exactly: 0 (auto:
                              4 next_pow2(k) in [64, 256] for bf16/tf32, 8 next_pow2(k) in
                              [128, 1024] for s8) or a power of two in [16, 1024] */

@@ -198,8 +198,8 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
           tmem_ld_wait();
           if (q >= a.B || (a.dbg_no_select & 1)) continue;
           const uint32_t doc0 = (uint32_t)tile * TD + cc * 64;
-          admit32<FMT, KC>(r, doc0, n_local, scratch, NEPI, L[t], thr[t]);
-          admit32<FMT, KC>(r + 32, doc0 + 32, n_local, scratch, NEPI, L[t], thr[t]);
+          admit<FMT, KC, 32>(r, doc0, n_local, scratch, NEPI, L[t], thr[t]);
+          admit<FMT, KC, 32>(r + 32, doc0 + 32, n_local, scratch, NEPI, L[t], thr[t]);
         }
       }
       tc_fence_before();
@@ -528,7 +528,7 @@ __global__ void row_stats_kernel(const float* __restrict__ docs, int64_t n, int 
   const int lane = threadIdx.x & 31;
   const int64_t wpb = blockDim.x >> 5;
   const float sx = i8_scale ? *i8_scale : 0.0f;
-  float b0 = 0.0f, b1 = 0.0f, b2 = 0.0f, b3 = 0.0f, b4 = 0.0f;
+  float b0 = 0.0f, b1 = 0.0f, b2 = 0.0f, b3 = 0.0f, b4 = 0.0f, nsum = 0.0f;
   for (int64_t r = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); r < n;
        r += (int64_t)gridDim.x * wpb) {
     const float* x = docs + r * D;
@@ -553,6 +553,7 @@ __global__ void row_stats_kernel(const float* __restrict__ docs, int64_t n, int 
       s4 += __shfl_xor_sync(0xffffffffu, s4, o);
     }
     b0 = fmaxf(b0, sqrtf(s0));
+    nsum += sqrtf(s0);
     b1 = fmaxf(b1, sqrtf(s1));
     b2 = fmaxf(b2, sqrtf(s2));
     b3 = fmaxf(b3, sqrtf(s3));
@@ -562,6 +563,7 @@ __global__ void row_stats_kernel(const float* __restrict__ docs, int64_t n, int 
     atomicMax(&out_bits[0], __float_as_uint(b0 * 1.00001f));
     atomicMax(&out_bits[1], __float_as_uint(b1 * 1.00001f));
     atomicMax(&out_bits[2], __float_as_uint(b2 * 1.00001f));
+    atomicAdd(reinterpret_cast<float*>(out_bits) + 7, nsum);  // sum of row norms (heuristics)
     if (i8_scale) {  // s x8 is rounded to fp32 here: 1e-3 of margin for the residual norms
       atomicMax(&out_bits[3], __float_as_uint(b3 * 1.001f));
       atomicMax(&out_bits[4], __float_as_uint(b4 * 1.001f));
@@ -652,6 +654,7 @@ cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64
 cudaError_t launch_row_stats(const float* docs, int64_t n, int D, unsigned int* out_bits,
                              cudaStream_t st, const float* i8_scale) {
   cudaError_t e = cudaMemsetAsync(out_bits, 0, 20, st);  // [0..4]; [5] = the s8 scale
+  if (e == cudaSuccess) e = cudaMemsetAsync(out_bits + 7, 0, 4, st);  // [7] = sum of |x|
   if (e != cudaSuccess) return e;
   int64_t blocks = (n + 7) / 8;
   if (blocks > 148 * 32) blocks = 148 * 32;

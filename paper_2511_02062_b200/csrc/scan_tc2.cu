@@ -1,16 +1,17 @@
 // scan_tc2.cu — K2 for B > 128: the coarse tensor-core scan on CTA PAIRS
 // (tcgen05.mma.cta_group::2, cluster of 2 on one TPC), 256 x QG queries per pass.
 //
-// One pair owns a 256-document tile and QG query groups of 256.  CTA r stages, per K-chunk,
-// the 128 query rows [256g + 128r, +128) of every group g (A) and documents
-// [tile*256 + 128r, +128) (B) in ITS smem.  Per k-step the leader issues QG MMAs of
-// M=256 x N=256 — MMA g reads group g's A rows of both CTAs and the B rows of both CTAs —
-// into TMEM columns [(buf*QG + g)*256, +256) = documents of the tile (contiguous).  Each
-// CTA's TMEM receives its 128 query rows.
-//   QG = 1 (128 < B <= 256): two accumulator buffers, the epilogue overlaps the next tile.
-//   QG = 2 (256 < B <= 512): the 512 TMEM columns hold one buffer for both groups; every
-//          document byte read from HBM feeds 512 queries (half the HBM traffic per query of
-//          QG = 1, which at B = 256 already shares the pass with the tensor-pipe limit).
+// One pair owns a TD-document tile (TD = 256 / QG) and QG query groups of 256.  CTA r stages,
+// per K-chunk, the 128 query rows [256g + 128r, +128) of every group g (A) and documents
+// [tile*TD + r*TD/2, +TD/2) (B) in ITS smem.  Per k-step the leader issues QG MMAs of
+// M=256 x N=TD — MMA g reads group g's A rows of both CTAs and the B rows of both CTAs —
+// into TMEM columns [(buf*QG + g)*TD, +TD) = documents of the tile (contiguous).  Each
+// CTA's TMEM receives its 128 query rows.  Two accumulator buffers either way (512 columns),
+// so the epilogue of one tile overlaps the MMAs of the next.
+//   QG = 1 (128 < B <= 256): 256-document tiles, 4 epilogue warps.
+//   QG = 2 (B > 256, VX_OPT_SCAN_PAIRS = 2): 128-document tiles, 8 epilogue warps (two per
+//          SM sub-partition: twice the latency hiding for the divergent selection); every
+//          document byte read from HBM feeds 512 queries — half the HBM traffic per query.
 //
 // Pipeline / synchronisation (a 2-SM UMMA pipeline, written out):
 //   full[s]   leader-only, count 1: leader producer arrive.expect_tx(both CTAs' bytes); both
@@ -20,8 +21,8 @@
 //   tempty[b] leader-only, count 2 x 4QG: every epilogue warp of both CTAs (the peer remotely).
 // Warps: 0 document producer, 1 MMA issuer (+ TMEM allocator), 2 query producer,
 //        3 .. 3+4QG-1 epilogue (group g = warps 3+4g .. 6+4g; warp w reads TMEM lanes
-//        32*(w%4) .. +31).  Epilogue = scan_tc.cu's (thread = query, max-of-32 filter,
-//        register-resident 16-list).
+//        32*(w%4) .. +31).  Epilogue: thread = query, vx_select.cuh (group-max filter,
+//        register-resident KC-list).
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -36,14 +37,15 @@ constexpr int kP2SmemLimit = 227 * 1024;
 
 template <int QG>
 struct P2Cfg {
-  static constexpr int TD = 256;                         // documents per pair tile
-  static constexpr int NBUF = 2 / QG;                    // accumulator buffers (512 columns)
+  static constexpr int TD = 256 / QG;                    // documents per pair tile
+  static constexpr int NBUF = 2;                         // accumulator buffers (512 columns)
   static constexpr int kCols = 512;
+  static constexpr int kBUnit = TD / 2 * 128;            // per CTA: TD/2 document rows x 128 B
   static constexpr int kEpiWarps = 4 * QG;
   static constexpr int kThreads = (3 + kEpiWarps) * 32;
   static constexpr int kAStage = QG * kP2Unit;           // per CTA: QG query blocks
   static constexpr int kNA = QG == 1 ? 4 : 3;            // query stages (L2-resident: short)
-  static constexpr int kScratch = kEpiWarps * 32 * 32 * 4;
+  static constexpr int kScratch = kEpiWarps * 32 * 64 * 4;  // 64 words per epilogue thread
 };
 
 // Separate rings for A (queries, from L2) and B (documents, from HBM): the document ring
@@ -51,7 +53,7 @@ struct P2Cfg {
 template <int QG>
 static size_t p2_smem(int nb) {
   using C = P2Cfg<QG>;
-  return (size_t)C::kNA * C::kAStage + (size_t)nb * kP2Unit + C::kScratch +
+  return (size_t)C::kNA * C::kAStage + (size_t)nb * C::kBUnit + C::kScratch +
          (size_t)(2 * C::kNA + 2 * nb + 4) * 8 + 16 + 1024;
 }
 
@@ -66,7 +68,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P2Cfg<QG>::kThreads,
   const int nb = a.ns;  // document stages
   uint8_t* ringA = smem;
   uint8_t* ringB = smem + (size_t)NA * C::kAStage;
-  uint32_t* scratch_base = reinterpret_cast<uint32_t*>(ringB + (size_t)nb * kP2Unit);  // [32][32*EW]
+  uint32_t* scratch_base = reinterpret_cast<uint32_t*>(ringB + (size_t)nb * C::kBUnit);  // [64][32*EW]
   uint64_t* fullA = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(scratch_base) + C::kScratch);
   uint64_t* emptyA = fullA + NA;
   uint64_t* fullB = emptyA + NA;
@@ -119,7 +121,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P2Cfg<QG>::kThreads,
     uint64_t* fullR = docs ? fullB : fullA;
     uint64_t* emptyR = docs ? emptyB : emptyA;
     uint8_t* ring = docs ? ringB : ringA;
-    const int sbytes = docs ? kP2Unit : C::kAStage;
+    const int sbytes = docs ? C::kBUnit : C::kAStage;
     const uint32_t bytes_pair = 2u * (uint32_t)sbytes;
     const uint32_t fb0 = mapa_shared(smem_u32(fullR), 0);  // the leader's full barriers
     int s = 0;
@@ -137,7 +139,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P2Cfg<QG>::kThreads,
           uint8_t* st = ring + (size_t)s * sbytes;
           if (skip) {
           } else if (docs) {
-            tma_load_2d_pair(st, &tx, fb, c * cw, tile * TD + (int)rank * 128, pol);
+            tma_load_2d_pair(st, &tx, fb, c * cw, tile * TD + (int)rank * (TD / 2), pol);
           } else {
 #pragma unroll
             for (int g = 0; g < QG; ++g)
@@ -167,7 +169,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P2Cfg<QG>::kThreads,
     // and each MMA is a single UTCHMMA — a single-thread loop paid R2UR waterfalls per
     // MMA and could not keep up with a 2-SM M=256 x N=256 MMA (128 cycles each).
     if (leader) {
-      constexpr uint32_t idesc = make_idesc_fmt(FMT, 256u, 256u);
+      constexpr uint32_t idesc = make_idesc_fmt(FMT, 256u, (uint32_t)TD);
       const uint64_t da0 = umma_desc_sw128(smem_u32(ringA));
       const uint64_t db0 = umma_desc_sw128(smem_u32(ringB));
       int sa = 0, sb = 0, buf = 0;
@@ -183,7 +185,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P2Cfg<QG>::kThreads,
           if (elect_one()) {
             // descriptor start address is addr >> 4: stage / group / K-step offsets add
             const uint64_t da = da0 + (uint64_t)(sa * (C::kAStage >> 4));
-            const uint64_t db = db0 + (uint64_t)(sb * (kP2Unit >> 4));
+            const uint64_t db = db0 + (uint64_t)(sb * (C::kBUnit >> 4));
             // dbg bit 8 (timing experiments): stream + commit without issuing the MMAs
             if (!(a.dbg_no_select & 8) || tile == pair)
 #pragma unroll
@@ -221,7 +223,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P2Cfg<QG>::kThreads,
     const int quad = warp & 3;                 // TMEM lane quadrant this warp may access
     const int m = quad * 32 + lane;            // row of this CTA's 128 queries of group g
     const int q = g * 256 + (int)rank * 128 + m;  // query within the launch
-    uint32_t* scratch = scratch_base + (e * 32 + lane);  // [32][32*EW]
+    uint32_t* scratch = scratch_base + (e * 32 + lane);  // [64][32*EW]
     constexpr int SS = C::kEpiWarps * 32;             // scratch row stride
     const uint32_t te_leader = mapa_shared(smem_u32(&tempty[0]), 0);
     uint64_t L[KC];
@@ -241,8 +243,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P2Cfg<QG>::kThreads,
         tmem_ld_wait();
         if (q >= a.B || (a.dbg_no_select & 1)) continue;
         const uint32_t doc0 = (uint32_t)tile * TD + cc * 64;  // columns map to docs 1:1
-        admit32<FMT, KC>(r, doc0, n_local, scratch, SS, L, thr);
-        admit32<FMT, KC>(r + 32, doc0 + 32, n_local, scratch, SS, L, thr);
+        admit<FMT, KC, 64>(r, doc0, n_local, scratch, SS, L, thr);
       }
       tc_fence_before();
       __syncwarp();

@@ -211,18 +211,21 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
                      (uint32_t)std::min(d->tok_per_doc, 256));
     if (s != VX_OK) return cleanup(s);
   }
-  s = make_tmap_2d(&h->tmap_docs, h->docs, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
-                   (uint64_t)h->n_local, D, 32, 128);
-  if (s != VX_OK) return cleanup(s);
-  if (h->docs16) {
-    s = make_tmap_2d(&h->tmap_docs16, h->docs16, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
-                     (uint64_t)h->n_local, D, 64, 128);
+  for (int half = 0; half < 2; ++half) {  // 128-row boxes, and 64-row boxes (QG = 2 tiles)
+    const uint32_t rows = half ? 64 : 128;
+    s = make_tmap_2d(half ? &h->tmap_docs_h : &h->tmap_docs, h->docs,
+                     CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (uint64_t)h->n_local, D, 32, rows);
     if (s != VX_OK) return cleanup(s);
-  }
-  if (h->docs8) {
-    s = make_tmap_2d(&h->tmap_docs8, h->docs8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1,
-                     (uint64_t)h->n_local, D, 128, 128);
-    if (s != VX_OK) return cleanup(s);
+    if (h->docs16) {
+      s = make_tmap_2d(half ? &h->tmap_docs16_h : &h->tmap_docs16, h->docs16,
+                       CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)h->n_local, D, 64, rows);
+      if (s != VX_OK) return cleanup(s);
+    }
+    if (h->docs8) {
+      s = make_tmap_2d(half ? &h->tmap_docs8_h : &h->tmap_docs8, h->docs8,
+                       CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, (uint64_t)h->n_local, D, 128, rows);
+      if (s != VX_OK) return cleanup(s);
+    }
   }
   *out = h;
   return VX_OK;
@@ -368,6 +371,10 @@ static vx_status refresh_shadows(vx_index* h, int64_t row_off, int64_t nrows) {
                               h->stream));
     count_launch(h);
   }
+  // host copy of the shard maxima for the AUTO coarse-format choice (coarse_fmt); the callers
+  // synchronise the stream before returning
+  CU_TRY(cudaMemcpyAsync(h->xstats_host, h->d_xnorm, sizeof(h->xstats_host),
+                         cudaMemcpyDeviceToHost, h->stream));
   return VX_OK;
 }
 

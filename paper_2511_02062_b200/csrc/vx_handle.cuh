@@ -82,15 +82,18 @@ struct vx_index {
   uint16_t* d_q16 = nullptr;     // [maxB][D] bf16 queries for the bf16 coarse scan
   int8_t* docs8 = nullptr;       // s8 shadow (one scale per shard, d_xnorm[5]), may be null
   CUtensorMap tmap_docs8{};
+  // 64-row boxes of the same maps: the 128-document pair tiles (scan_tc2, QG = 2)
+  CUtensorMap tmap_docs_h{}, tmap_docs16_h{}, tmap_docs8_h{};
   int8_t* d_q8 = nullptr;        // [maxB][D] s8 queries, per-row scales in d_qs8
   float* d_qs8 = nullptr;
+  float xstats_host[8] = {};     // host copy of d_xnorm after every upload / synth
   int coarse = VX_COARSE_AUTO;
   int scan_tile = 0;             // documents per tensor-core tile (0 = auto)
   int kprime = 0;                // TC candidate set size k' (0 = auto; VX_OPT_KPRIME)
   int dbg_tc_bits = 0;           // timing-experiment knobs, read once from the environment at
   int dbg_tc_stages = 0;         //   create: VX_DEBUG_TC_NOSELECT (bit mask), VX_DEBUG_TC_STAGES
-  int use_pairs = 1;             // CTA-pair scan for B > 128: 0 off, 1 on, 2 on + 512-query
-                                 // passes (VX_OPT_SCAN_PAIRS)
+  int use_pairs = 2;             // CTA-pair scan for B > 128: 0 off, 1 on (256-query passes),
+                                 // 2 on + 512-query passes for B > 256 (VX_OPT_SCAN_PAIRS)
   // options
   int scan_algo = VX_SCAN_AUTO;
   int maxsim_algo = VX_MAXSIM_AUTO;
@@ -113,7 +116,8 @@ struct vx_index {
   uint64_t* d_ckeys = nullptr;   // [maxB][512] merged coarse keys (TC path)
   int* d_flags = nullptr;        // [maxB] certificate failures (TC path)
   unsigned int* d_xnorm = nullptr;  // [8] shard maxima (float bits, row_stats): |x|, |bf16 x|,
-                                    // |x-bf16 x|, |sx x8|, |x-sx x8|; [5] sx; [6] scratch
+                                    // |x-bf16 x|, |sx x8|, |x-sx x8|; [5] sx; [6] scratch;
+                                    // [7] sum of row norms (AUTO coarse heuristic)
   float* d_fq = nullptr;         // [maxB][D] queries gathered for the exact fallback
   int* d_fidx = nullptr;         // [maxB] flagged query indices
   int* d_fcount = nullptr;       // [2] flagged count of the last batch, running total

@@ -1,11 +1,12 @@
 // vx_select.cuh — the per-query candidate selection shared by the tensor-core scan epilogues
 // (scan_tc.cu, scan_tc2.cu).  One thread owns one query: it reads the query's accumulator row
-// from TMEM 64 columns (= 64 documents) per tcgen05.ld and admits each 32-column half into a
-// register-resident descending list of KC order-preserving (score, id) keys.
+// from TMEM 64 columns (= 64 documents) per tcgen05.ld and admits them (as one 64-column unit,
+// or two 32-column halves where smem is short) into a register-resident descending list of
+// KC order-preserving (score, id) keys.
 //
-// Fast path: the maxima of the half's four 8-column groups, compared on the raw accumulators
+// Fast path: the maxima of the unit's 8-column groups, compared on the raw accumulators
 // (s32 for kind::i8: no conversions) against the query's admission threshold (the KC-th best
-// key so far) — after the first tiles most halves stop here.  Slow path: only the passing
+// key so far) — after the first tiles most units stop here.  Slow path: only the passing
 // groups are compared, their passing positions are enumerated from a bit mask and inserted
 // with an unrolled compare-exchange network; the raw words are parked in smem scratch (stride
 // `ss` words between consecutive columns) so the enumeration can index them.  With 32 queries
@@ -17,6 +18,8 @@
 #include "vx_synth.h"
 
 #include <limits.h>
+
+#include <type_traits>
 
 namespace vx {
 
@@ -51,46 +54,56 @@ VX_DEV void list_insert(uint64_t (&L)[KC], uint64_t key) {
   L[0] = c[0] ? key : L[0];
 }
 
-template <int FMT, int KC>
-VX_DEV void admit32(const uint32_t* r, uint32_t doc0, uint32_t n_local, uint32_t* scratch, int ss,
-                    uint64_t (&L)[KC], float& thr) {
+// Admit W (32 or 64) consecutive accumulator columns (documents doc0 ..) of this thread's
+// query.  scratch: W words per thread, stride ss.
+template <int FMT, int KC, int W>
+VX_DEV void admit(const uint32_t* r, uint32_t doc0, uint32_t n_local, uint32_t* scratch, int ss,
+                  uint64_t (&L)[KC], float& thr) {
   using O = AccOrd<FMT>;
   using T = typename O::T;
-  // maxima of the four 8-column groups, then of the half
-  T gm[4];
+  using M = typename std::conditional<W == 64, unsigned long long, uint32_t>::type;
+  constexpr int NG = W / 8;
+  // maxima of the 8-column groups (independent trees), then of all W
+  T gm[NG];
 #pragma unroll
-  for (int g = 0; g < 4; ++g) {
+  for (int g = 0; g < NG; ++g) {
     T m0 = O::mx(O::of(r[8 * g + 0]), O::of(r[8 * g + 1]));
     T m1 = O::mx(O::of(r[8 * g + 2]), O::of(r[8 * g + 3]));
     T m2 = O::mx(O::of(r[8 * g + 4]), O::of(r[8 * g + 5]));
     T m3 = O::mx(O::of(r[8 * g + 6]), O::of(r[8 * g + 7]));
     gm[g] = O::mx(O::mx(m0, m1), O::mx(m2, m3));
   }
-  const T t = O::thr(thr);
-  if (O::mx(O::mx(gm[0], gm[1]), O::mx(gm[2], gm[3])) < t) return;
-  // only the passing groups are compared and parked (warp-divergent: usually one lane, one
-  // group — the other 31 lanes of the warp wait, so this stays short)
-  uint32_t mask = 0;
+  T m = gm[0];
 #pragma unroll
-  for (int g = 0; g < 4; ++g) {
+  for (int g = 1; g < NG; ++g) m = O::mx(m, gm[g]);
+  const T t = O::thr(thr);
+  if (m < t) return;
+  // only the passing groups are compared and parked (warp-divergent: the warp takes this
+  // path when any of its 32 queries passes, so it has to stay short)
+  M mask = 0;
+#pragma unroll
+  for (int g = 0; g < NG; ++g) {
     if (gm[g] < t) continue;
+    uint32_t gmask = 0;
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      const int i = 8 * g + e;
-      mask |= (O::of(r[i]) >= t ? 1u : 0u) << i;
-      scratch[i * ss] = r[i];
+      gmask |= (O::of(r[8 * g + e]) >= t ? 1u : 0u) << e;
+      scratch[(8 * g + e) * ss] = r[8 * g + e];
     }
+    mask |= (M)gmask << (8 * g);
   }
+  bool ins = false;
   while (mask) {
-    const int i = __ffs(mask) - 1;
+    const int i = (W == 64 ? __ffsll((long long)mask) : __ffs((int)mask)) - 1;
     mask &= mask - 1;
     const uint32_t doc = doc0 + i;
     if (doc >= n_local) break;  // positions are increasing: the rest are padding
-    uint64_t key = vx_make_key(acc_score<FMT>(scratch[i * ss]), doc);
+    const uint64_t key = vx_make_key(acc_score<FMT>(scratch[i * ss]), doc);
     if (key <= L[KC - 1]) continue;
     list_insert<KC>(L, key);
-    thr = L[KC - 1] == 0ull ? -INFINITY : vx_key_score(L[KC - 1]);
+    ins = true;
   }
+  if (ins) thr = L[KC - 1] == 0ull ? -INFINITY : vx_key_score(L[KC - 1]);
 }
 
 }  // namespace vx

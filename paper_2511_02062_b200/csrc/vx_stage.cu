@@ -70,8 +70,19 @@ static int kprime_of(const vx_index* h, int k, int fmt) {
 }
 
 // coarse operand format of the tensor-core pass for this handle
+// AUTO takes the s8 pass (a quarter of the fp32 bytes, twice the bf16 tensor rate; measured
+// 10M x 768 B=1024 stage 8.99 ms vs 13.5 ms bf16 — profiles/r01/README.md) when the shard's
+// one-scale quantisation is tight enough for the certificate to hold at k' = 8 next_pow2(k):
+// max |x - sx x8| <= 3 % of the mean row norm (synthetic rows ~1 %, Gaussian rows ~1.5 %).
+// An outlier coordinate inflates the shared scale, widens the error bound E and would push
+// queries to the exact re-scan — bf16 then.
+constexpr float kI8AutoMaxRelResidual = 0.03f;
+
 int coarse_fmt(const vx_index* h) {
   if (h->coarse == VX_COARSE_I8 && h->docs8) return vx::FMT_I8;
+  if (h->coarse == VX_COARSE_AUTO && h->docs8 &&
+      h->xstats_host[4] <= kI8AutoMaxRelResidual * h->xstats_host[7] / (float)std::max<int64_t>(1, h->n_local))
+    return vx::FMT_I8;
   if (h->coarse == VX_COARSE_TF32 || !h->docs16) return vx::FMT_TF32;
   return vx::FMT_BF16;
 }
@@ -102,10 +113,11 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
     CU_TRY(vx::launch_rows_to_i8(d_q, B, D, h->d_q8, h->d_qs8, st));
     count_launch(h);
   }
-  // queries per pass over the index: 256 (CTA pairs, or the single-CTA kernel's QT = 2 x
-  // 128); VX_OPT_SCAN_PAIRS = 2 feeds 512 queries per pass on CTA pairs (QG = 2: a single
-  // TMEM buffer for both groups, so the epilogue no longer overlaps the MMA — measured
-  // slower than two QG = 1 passes at 10M x 768, profiles/r01/README.md)
+  // queries per pass over the index: 512 (default, CTA pairs with two query groups on
+  // 128-document tiles: half the HBM traffic per query, two epilogue warps per SM
+  // sub-partition; measured 10M x 768 B=1024: s8 6.05 ms vs 7.40, bf16 11.7 vs 15.8 with
+  // 256-query passes — profiles/r01/README.md); VX_OPT_SCAN_PAIRS = 1: 256 (one group on
+  // 256-document tiles); 0: the single-CTA kernels (QT = 2 x 128)
   const bool pairs = h->use_pairs && grid % 2 == 0;
   const int GS = (pairs && h->use_pairs == 2) ? 512 : 256;
   for (int g0 = 0; g0 < B; g0 += GS) {
@@ -138,6 +150,8 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
       int ns2 = 0;
       const size_t smem2 = vx::scan_tc2_smem(QG, &ns2);
       a.ns = ns2;
+      if (QG == 2)  // 128-document tiles: 64-row document boxes per CTA
+        tx = i8 ? &h->tmap_docs8_h : (bf16 ? &h->tmap_docs16_h : &h->tmap_docs_h);
       CU_TRY(vx::launch_scan_tc2(QG, &tq, tx, a, grid, smem2, st));
     } else {
       // 256-document tiles halve the per-document query re-streaming from L2 (measured: B=128

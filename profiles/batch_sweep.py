@@ -51,7 +51,7 @@ while B <= bmax:
                       "scan_ms": round(sms, 4), "bound": roof["bound"], "frac": round(roof["frac"], 4),
                       "hbm_frac": round(roof["hbm"]["frac"], 4),
                       "tensor_frac": round(roof["compute"]["frac"], 4),
-                      "passes": (B + 255) // 256,
+                      "passes": roof["launches"],
                       "cert_fallbacks": idx.stats()["cert_fallbacks"]}), flush=True)
     B *= 2
 idx.close()

@@ -61,3 +61,27 @@ def test_upload_refreshes_shadow(vx, oracle):
         ids, sc = idx.search(Q, k)
     rid, rsc = oracle.flat_topk(X, Q, k, mode=1)
     assert np.array_equal(ids, rid)
+
+
+def test_auto_coarse_follows_quantisation_quality(vx, oracle):
+    # AUTO takes the s8 pass when the shard's one-scale quantisation is tight (max residual
+    # norm <= 3 % of the mean row norm: the synthetic rows are at ~1 %), bf16 when an outlier
+    # coordinate inflates the shared scale — exact either way
+    N, D, B, k = 20_000, 768, 40, 10
+    X = oracle.synth_rows(42, 0, N, D)
+    Q = oracle.synth_rows(43, 0, B, D)
+    with vx.Index(N, D, max_batch=B, max_k=k) as idx:
+        idx.upload(X, 0)
+        assert idx.coarse_auto() == "i8"
+        ids, sc = idx.search(Q, k)
+        rid, rsc = oracle.flat_topk(X, Q, k, mode=1)
+        assert np.array_equal(ids, rid) and np.array_equal(sc, rsc.astype(np.float32))
+        Xo = X.copy()
+        Xo[123, 5] = 400.0  # one spike: the scale grows ~10^4 x, residuals ~ the row norms
+        idx.upload(Xo[123:124], 123)
+        assert idx.coarse_auto() == "bf16"
+        ids, sc = idx.search(Q, k)
+        rid, rsc = oracle.flat_topk(Xo, Q, k, mode=1)
+        assert np.array_equal(ids, rid) and np.array_equal(sc, rsc.astype(np.float32))
+        idx.upload(X[123:124], 123)  # back to the tight scale
+        assert idx.coarse_auto() == "i8"
