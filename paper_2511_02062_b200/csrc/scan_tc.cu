@@ -410,113 +410,160 @@ __global__ void __launch_bounds__(256)
 // ------------------------------------------------------------------- K2c: wide re-rank
 // Second certificate level for the (rare) queries whose k'-candidate certificate failed:
 // the per-CTA (per-pair) lists hold more than the k' candidates.  With T'' = the largest
-// 16th key among FULL lists (the deepest truncation point), every document whose coarse key
-// is >= T'' is in some list (a document outside its list has key < that list's 16th key <=
-// T''), so re-ranking all list entries >= T'' exactly (up to P x 16 rows) and checking
+// KC-th key among FULL lists (the deepest truncation point), every document whose coarse key
+// is >= T'' is in some list (a document outside its list has key < that list's last key <=
+// T''), so re-ranking all list entries >= T'' exactly (up to P x KC rows) and checking
 // exact k-th > coarse(T'') + E certifies the query without touching the index again.  T''
 // sits ~5-7x deeper than the k'-th candidate, so the gap almost always clears E; queries
-// that still fail go on to the exact re-scan.  One CTA per compacted failing query.
-__global__ void __launch_bounds__(256)
-    rerank_wide_kernel(const float* __restrict__ docs, const float* __restrict__ fq, int D,
-                       const int* __restrict__ fidx, const int* __restrict__ fcount,
-                       const uint64_t* __restrict__ part_all, int B, int GS, int P_pairs,
-                       int P_single, int kc, int k, int64_t row0,
-                       const float* __restrict__ xstats, int fmt,
-                       const float* __restrict__ qscale, uint64_t* __restrict__ out_keys,
-                       int64_t* __restrict__ out_ids, float* __restrict__ out_scores,
-                       int* __restrict__ flags) {
-  extern __shared__ __align__(16) float wsm[];
-  const int i = blockIdx.x;
-  if (i >= *fcount) return;
-  const int b = fidx[i];
+// that still fail go on to the exact re-scan.
+// Two launches: wide_score_kernel spreads each failing query's rows over S CTAs (one row per
+// thread, the in-order fmaf chain of the exact oracle — a row cannot be split across lanes
+// without changing the rounding, so rows in flight are what hides the gather latency; one
+// CTA per query took ~0.5 ms for 2 queries of a 10M x 768 batch), wide_select_kernel sorts
+// and certifies.  Both walk the compacted failing queries i = blockIdx / S, += gridDim / S.
+
+// T'' and the query's list block; every query's lists start at a stride of P_single lists
+// (K2 / K2-pairs share it)
+__device__ __forceinline__ void wide_lists(const uint64_t* part_all, int b, int B, int GS,
+                                           int P_pairs, int P_single, int kc,
+                                           const uint64_t** lists, int* P) {
   const int g0 = (b / GS) * GS, Bg = min(GS, B - g0);
-  const int P = (P_pairs > 0 && Bg > 128) ? P_pairs : P_single;
-  const int M = P * kc;
-  // every query's lists start at a stride of P_single lists (K2 / K2-pairs share it)
-  const uint64_t* lists = part_all + (size_t)b * P_single * kc;
-  int np2 = 16;
-  while (np2 < M) np2 <<= 1;
-  float* qs = wsm;                                                      // [D]
-  uint64_t* keys = reinterpret_cast<uint64_t*>(wsm + ((D + 3) & ~3));   // [np2]
-  __shared__ float s_red[96];
-  __shared__ unsigned long long s_t2;
-  __shared__ int s_n;
-  const float* q = fq + (size_t)i * D;
-  const float sq = fmt == FMT_I8 ? qscale[b] : 1.0f;
-  const float cscale = fmt == FMT_I8 ? sq * xstats[5] : 1.0f;
-  query_norms(q, D, fmt, sq, qs, s_red);
-  if (threadIdx.x == 0) {
-    s_t2 = 0ull;
-    s_n = 0;
-  }
+  *P = (P_pairs > 0 && Bg > 128) ? P_pairs : P_single;
+  *lists = part_all + (size_t)b * P_single * kc;
+}
+__device__ __forceinline__ uint64_t wide_t2(const uint64_t* lists, int P, int kc,
+                                            unsigned long long* s_t2) {
+  if (threadIdx.x == 0) *s_t2 = 0ull;
   __syncthreads();
-  // T'' = max over full lists of their last (kc-th) key (0: no list was truncated)
   for (int p = threadIdx.x; p < P; p += blockDim.x) {
     const uint64_t last = lists[(size_t)p * kc + (kc - 1)];
-    if (last) atomicMax(&s_t2, (unsigned long long)last);
+    if (last) atomicMax(s_t2, (unsigned long long)last);
   }
   __syncthreads();
-  const uint64_t t2 = s_t2;
-  // candidates: list entries >= T'', re-scored exactly (in-order fmaf chain per row)
-  for (int j = threadIdx.x; j < M; j += blockDim.x) {
-    const uint64_t ck = lists[j];
-    if (ck == 0ull || ck < t2) continue;
-    const float4* x = reinterpret_cast<const float4*>(docs + (size_t)vx_key_id(ck) * D);
-    float acc = 0.0f;
-    for (int c = 0; c < (D >> 2); ++c) {
-      const float4 xv = __ldg(x + c);
-      acc = fmaf(xv.x, qs[4 * c + 0], acc);
-      acc = fmaf(xv.y, qs[4 * c + 1], acc);
-      acc = fmaf(xv.z, qs[4 * c + 2], acc);
-      acc = fmaf(xv.w, qs[4 * c + 3], acc);
+  return *s_t2;
+}
+
+__global__ void __launch_bounds__(256)
+    wide_score_kernel(const float* __restrict__ docs, const float* __restrict__ fq, int D,
+                      const int* __restrict__ fidx, const int* __restrict__ fcount,
+                      const uint64_t* __restrict__ part_all, int B, int GS, int P_pairs,
+                      int P_single, int kc, int S, uint64_t* __restrict__ wkeys) {
+  extern __shared__ __align__(16) float qs[];  // [D]
+  __shared__ unsigned long long s_t2;
+  const int n = *fcount, W = gridDim.x / S, s = blockIdx.x % S;
+  const int Mmax = P_single * kc;
+  for (int i = blockIdx.x / S; i < n; i += W) {
+    const int b = fidx[i];
+    const uint64_t* lists;
+    int P;
+    wide_lists(part_all, b, B, GS, P_pairs, P_single, kc, &lists, &P);
+    const uint64_t t2 = wide_t2(lists, P, kc, &s_t2);
+    for (int t = threadIdx.x; t < D; t += blockDim.x) qs[t] = fq[(size_t)i * D + t];
+    __syncthreads();
+    const int M = P * kc, chunk = (M + S - 1) / S;
+    const int j1 = min(M, (s + 1) * chunk);
+    for (int j = s * chunk + threadIdx.x; j < j1; j += blockDim.x) {
+      const uint64_t ck = lists[j];
+      uint64_t key = 0ull;
+      if (ck != 0ull && ck >= t2) {
+        const float4* x = reinterpret_cast<const float4*>(docs + (size_t)vx_key_id(ck) * D);
+        float acc = 0.0f;
+        const int nv = D >> 2;
+        for (int c0 = 0; c0 < nv; c0 += 8) {  // 8 loads in flight, then the in-order chain
+          float4 v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (c0 + u < nv) v[u] = __ldg(x + c0 + u);
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (c0 + u < nv) {
+              const int c = c0 + u;
+              acc = fmaf(v[u].x, qs[4 * c + 0], acc);
+              acc = fmaf(v[u].y, qs[4 * c + 1], acc);
+              acc = fmaf(v[u].z, qs[4 * c + 2], acc);
+              acc = fmaf(v[u].w, qs[4 * c + 3], acc);
+            }
+        }
+        key = vx_make_key(acc, vx_key_id(ck));
+      }
+      wkeys[(size_t)i * Mmax + j] = key;
     }
-    keys[atomicAdd(&s_n, 1)] = vx_make_key(acc, vx_key_id(ck));
+    __syncthreads();  // qs / s_t2 are reused by the next query
   }
-  __syncthreads();
-  const int n = s_n;
-  for (int j = n + threadIdx.x; j < np2; j += blockDim.x) keys[j] = 0ull;
-  __syncthreads();
-  for (int size = 2; size <= np2; size <<= 1)
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int t = threadIdx.x; t < (np2 >> 1); t += blockDim.x) {
-        int lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
-        bool desc = (lo & size) == 0;
-        uint64_t x0 = keys[lo], x1 = keys[hi];
-        if ((x0 < x1) == desc) {
-          keys[lo] = x1;
-          keys[hi] = x0;
+}
+
+__global__ void __launch_bounds__(256)
+    wide_select_kernel(const float* __restrict__ fq, int D, const int* __restrict__ fidx,
+                       const int* __restrict__ fcount, const uint64_t* __restrict__ part_all,
+                       int B, int GS, int P_pairs, int P_single, int kc, int k, int64_t row0,
+                       const float* __restrict__ xstats, int fmt,
+                       const float* __restrict__ qscale, const uint64_t* __restrict__ wkeys,
+                       uint64_t* __restrict__ out_keys, int64_t* __restrict__ out_ids,
+                       float* __restrict__ out_scores, int* __restrict__ flags) {
+  extern __shared__ __align__(16) uint64_t keys[];  // [np2]
+  __shared__ float s_red[96];
+  __shared__ unsigned long long s_t2;
+  __shared__ int s_fail;
+  const int n = *fcount;
+  const int Mmax = P_single * kc;
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    const int b = fidx[i];
+    const uint64_t* lists;
+    int P;
+    wide_lists(part_all, b, B, GS, P_pairs, P_single, kc, &lists, &P);
+    const uint64_t t2 = wide_t2(lists, P, kc, &s_t2);
+    const int M = P * kc;
+    int np2 = 16;
+    while (np2 < M) np2 <<= 1;
+    const float sq = fmt == FMT_I8 ? qscale[b] : 1.0f;
+    const float cscale = fmt == FMT_I8 ? sq * xstats[5] : 1.0f;
+    query_norms(fq + (size_t)i * D, D, fmt, sq, nullptr, s_red);
+    for (int j = threadIdx.x; j < np2; j += blockDim.x)
+      keys[j] = j < M ? wkeys[(size_t)i * Mmax + j] : 0ull;
+    __syncthreads();
+    for (int size = 2; size <= np2; size <<= 1)
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int t = threadIdx.x; t < (np2 >> 1); t += blockDim.x) {
+          int lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
+          bool desc = (lo & size) == 0;
+          uint64_t x0 = keys[lo], x1 = keys[hi];
+          if ((x0 < x1) == desc) {
+            keys[lo] = x1;
+            keys[hi] = x0;
+          }
+        }
+        __syncthreads();
+      }
+    if (threadIdx.x == 0) {
+      int fail = 0;
+      if (t2 != 0ull) {
+        float qn, qh, qr;
+        query_norms_final(s_red, fmt, &qn, &qh, &qr);
+        const float E = cert_err_bound(fmt, qn, qh, qr, xstats);
+        const uint64_t ek = k <= np2 ? keys[k - 1] : 0ull;
+        fail = (ek == 0ull || !(vx_key_score(ek) > vx_key_score(t2) * cscale + E)) ? 1 : 0;
+      }
+      s_fail = fail;
+      flags[b] = fail;
+    }
+    __syncthreads();
+    if (!s_fail) {  // else the exact re-scan writes this query
+      for (int j = threadIdx.x; j < k; j += blockDim.x) {
+        const uint64_t key = j < np2 ? keys[j] : 0ull;
+        const size_t o = (size_t)b * k + j;
+        if (key == 0ull) {
+          out_keys[o] = 0ull;
+          out_ids[o] = -1;
+          out_scores[o] = -INFINITY;
+        } else {
+          const int64_t gid = (int64_t)vx_key_id(key) + row0;
+          out_keys[o] = (key & 0xFFFFFFFF00000000ull) | (uint64_t)(0xFFFFFFFFu - (uint32_t)gid);
+          out_ids[o] = gid;
+          out_scores[o] = vx_key_score(key);
         }
       }
-      __syncthreads();
     }
-  __shared__ int s_fail;
-  if (threadIdx.x == 0) {
-    int fail = 0;
-    if (t2 != 0ull) {
-      float qn, qh, qr;
-      query_norms_final(s_red, fmt, &qn, &qh, &qr);
-      const float E = cert_err_bound(fmt, qn, qh, qr, xstats);
-      const uint64_t ek = k <= n ? keys[k - 1] : 0ull;
-      fail = (ek == 0ull || !(vx_key_score(ek) > vx_key_score(t2) * cscale + E)) ? 1 : 0;
-    }
-    s_fail = fail;
-    flags[b] = fail;
-  }
-  __syncthreads();
-  if (s_fail) return;  // the exact re-scan writes this query
-  for (int j = threadIdx.x; j < k; j += blockDim.x) {
-    const uint64_t key = j < n ? keys[j] : 0ull;
-    const size_t o = (size_t)b * k + j;
-    if (key == 0ull) {
-      out_keys[o] = 0ull;
-      out_ids[o] = -1;
-      out_scores[o] = -INFINITY;
-    } else {
-      const int64_t gid = (int64_t)vx_key_id(key) + row0;
-      out_keys[o] = (key & 0xFFFFFFFF00000000ull) | (uint64_t)(0xFFFFFFFFu - (uint32_t)gid);
-      out_ids[o] = gid;
-      out_scores[o] = vx_key_score(key);
-    }
+    __syncthreads();  // keys / s_red are reused by the next query
   }
 }
 
@@ -576,19 +623,27 @@ cudaError_t launch_rerank_wide(const float* docs, const float* fq, int D, const 
                                const int* fcount, const uint64_t* part_all, int B, int GS,
                                int P_pairs, int P_single, int kc, int k, int64_t row0,
                                const float* xstats, int fmt, const float* qscale,
-                               uint64_t* out_keys, int64_t* out_ids, float* out_scores,
-                               int* flags, cudaStream_t st) {
+                               uint64_t* wkeys, uint64_t* out_keys, int64_t* out_ids,
+                               float* out_scores, int* flags, cudaStream_t st) {
   const int M = P_single * kc;
   int np2 = 16;
   while (np2 < M) np2 <<= 1;
-  const size_t smem = (size_t)((D + 3) & ~3) * 4 + (size_t)np2 * 8;
+  const size_t smem = (size_t)np2 * 8;
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(rerank_wide_kernel,
+  cudaError_t e = cudaFuncSetAttribute(wide_select_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  rerank_wide_kernel<<<B, 256, smem, st>>>(docs, fq, D, fidx, fcount, part_all, B, GS, P_pairs,
-                                           P_single, kc, k, row0, xstats, fmt, qscale, out_keys,
-                                           out_ids, out_scores, flags);
+  // S CTAs per failing query (about one row per thread), W queries in flight; both loops
+  // exit at once when the device-side count is 0 (the common case)
+  const int S = (M + 255) / 256;
+  const int W = B < 32 ? B : 32;
+  wide_score_kernel<<<W * S, 256, (size_t)D * 4, st>>>(docs, fq, D, fidx, fcount, part_all, B,
+                                                       GS, P_pairs, P_single, kc, S, wkeys);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  wide_select_kernel<<<W, 256, smem, st>>>(fq, D, fidx, fcount, part_all, B, GS, P_pairs,
+                                           P_single, kc, k, row0, xstats, fmt, qscale, wkeys,
+                                           out_keys, out_ids, out_scores, flags);
   return cudaGetLastError();
 }
 

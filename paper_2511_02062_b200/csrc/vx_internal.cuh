@@ -78,13 +78,14 @@ cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64
                           int64_t row0, const float* xstats, int fmt, const float* qscale,
                           uint64_t* out_keys, int64_t* out_ids, float* out_scores, int* flags,
                           cudaStream_t st);
-// second certificate level over the full per-CTA lists (compacted failing queries)
+// second certificate level over the full per-CTA lists (compacted failing queries): two
+// launches; wkeys = scratch of B x P_single x kc keys
 cudaError_t launch_rerank_wide(const float* docs, const float* fq, int D, const int* fidx,
                                const int* fcount, const uint64_t* part_all, int B, int GS,
                                int P_pairs, int P_single, int kc, int k, int64_t row0,
                                const float* xstats, int fmt, const float* qscale,
-                               uint64_t* out_keys, int64_t* out_ids, float* out_scores,
-                               int* flags, cudaStream_t st);
+                               uint64_t* wkeys, uint64_t* out_keys, int64_t* out_ids,
+                               float* out_scores, int* flags, cudaStream_t st);
 // per-shard maxima [max|x|, max|bf16(x)|, max|x - bf16(x)|] (3 floats as uint bits) and, when
 // i8_scale is given, [3] max|sx x8|, [4] max|x - sx x8| of the s8 shadow
 cudaError_t launch_row_stats(const float* docs, int64_t n, int D, unsigned int* out_bits,

@@ -204,11 +204,14 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
   int* cnt3 = h->d_fcount + 2;  // [count, running total] of exact re-scans
   CU_TRY(vx::launch_cert_compact(h->d_flags, B, d_q, D, h->d_fidx, cnt2, h->d_fq, st));
   count_launch(h);
+  // wide-key scratch: the upper part of d_part (the lists use B x grid x KC <= B x grid x 32
+  // of its B x grid x 256 entries; the level-3 re-scan writes d_part only after level 2)
+  uint64_t* wkeys = h->d_part + (size_t)h->desc.max_batch * grid * 32;
   CU_TRY(vx::launch_rerank_wide(h->docs, h->d_fq, D, h->d_fidx, cnt2, h->d_part, B, GS,
                                 pairs ? grid / 2 : 0, grid, KC, k, h->row0,
                                 reinterpret_cast<const float*>(h->d_xnorm), fmt,
-                                i8 ? h->d_qs8 : nullptr, keys, ids, scores, h->d_flags, st));
-  count_launch(h);
+                                i8 ? h->d_qs8 : nullptr, wkeys, keys, ids, scores, h->d_flags, st));
+  count_launch(h, 2);
   CU_TRY(vx::launch_cert_compact(h->d_flags, B, d_q, D, h->d_fidx, cnt3, h->d_fq, st));
   count_launch(h);
   uint64_t* fk = h->d_ckeys;  // reuse: [B][k] (k <= 256)
