@@ -312,6 +312,28 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   const uint64_t* cb = cand + (size_t)b * kp;
   const uint64_t tprime = cb[kp - 1];  // coarse k'-th key (0: fewer than k' candidates)
+  // Certificate error bound E (below) and candidate pruning: |exact - cscale * coarse| <= E
+  // for every document, so the k best coarse candidates all score >= cscale c_k - E exactly,
+  // and a candidate with cscale c_j + E < cscale c_k - E cannot enter the exact top-k.  The
+  // candidates are sorted by coarse key: only the prefix down to cscale c_k - 2E is fetched
+  // (the s8 pass sizes k' = 8k for the certificate, but the prefix is typically ~k'/2).
+  float qn, qh, qr;
+  query_norms_final(s_red, fmt, &qn, &qh, &qr);
+  const float E = cert_err_bound(fmt, qn, qh, qr, xstats);
+  int kpe = kp;  // candidates re-ranked
+  const uint64_t ckk = k <= kp ? cb[k - 1] : 0ull;
+  if (ckk != 0ull) {
+    const float lim = (vx_key_score(ckk) * cscale - E) - E;
+    int lo = k, hi = kp;  // first index whose candidate falls below lim (cb is descending)
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      const uint64_t c = cb[mid];
+      if (c != 0ull && vx_key_score(c) * cscale >= lim) lo = mid + 1;
+      else hi = mid;
+    }
+    kpe = lo;
+  }
+  for (int i = kpe + threadIdx.x; i < kp; i += blockDim.x) keys[i] = 0ull;
   // The candidate rows are random 3 KB gathers from HBM (DRAM-page unfriendly); per-thread
   // loads left too few bytes in flight (measured 85 us at B=128).  Instead each round stages
   // R rows into smem with one TMA bulk copy per row (R x 3 KB in flight per SM), then R
@@ -323,19 +345,19 @@ __global__ void __launch_bounds__(256)
     fence_barrier_init();
   }
   __syncthreads();
-  for (int r0 = 0, round = 0; r0 < kp; r0 += R, ++round) {
+  for (int r0 = 0, round = 0; r0 < kpe; r0 += R, ++round) {
     const int t = threadIdx.x;
     const int idx = r0 + t;
     uint64_t ck = 0ull;
     if (t < R) {
-      ck = idx < kp ? cb[idx] : 0ull;
+      ck = idx < kpe ? cb[idx] : 0ull;
       const uint32_t bytes = ck ? (uint32_t)D * 4u : 0u;
       mbar_expect_tx(&s_bar, bytes);  // every staging thread arrives once (count R)
       if (ck)
         bulk_load(rowbuf + (size_t)t * RS, docs + (size_t)vx_key_id(ck) * D, bytes, &s_bar);
     }
     mbar_wait(&s_bar, (uint32_t)(round & 1));
-    if (t < R && idx < kp) {
+    if (t < R && idx < kpe) {
       uint64_t ek = 0ull;
       if (ck) {
         const float4* x = reinterpret_cast<const float4*>(rowbuf + (size_t)t * RS);
@@ -383,9 +405,6 @@ __global__ void __launch_bounds__(256)
     //   looser).  TF32 coarse: per-operand truncation <= 2^-10 -> 2^-9 |q| max|x|.
     //   Both: + 2^-12 |q| max|x| for the fp32 accumulation of the tensor core and of the
     //   exact in-order chain (each <= 768 * 2^-24 relative, 5x margin).
-    float qn, qh, qr;
-    query_norms_final(s_red, fmt, &qn, &qh, &qr);
-    const float E = cert_err_bound(fmt, qn, qh, qr, xstats);
     const uint64_t ek = keys[k - 1];
     if (ek == 0ull || !(vx_key_score(ek) > vx_key_score(tprime) * cscale + E)) s_fail = 1;
   }
