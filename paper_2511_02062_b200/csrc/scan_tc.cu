@@ -288,18 +288,33 @@ __device__ __forceinline__ void query_norms_final(const float* red, int fmt, flo
 // One CTA per query.  cand: the merged coarse top-k' keys (score desc); part: the per-CTA
 // lists of K2 (certificate 1); docs/queries fp32.  Writes the exact top-k and flags[b] = 1
 // when the certificate fails (the caller re-scans that query with the exact kernel).
+//
+// Candidate pruning (|exact - cscale c| <= E for every document): the k best coarse
+// candidates are re-scored first ("head"); their minimum exact score L is <= the exact k-th,
+// so any later candidate with cscale c_j + E < L cannot enter the top-k, and — candidates
+// being sorted by coarse key — only the prefix down to cscale c >= L - E is fetched
+// ("tail"; 10M x 768 s8, k' = 1024: ~600 of the 1024 rows, where the a-priori bound
+// cscale c_k - 2E keeps all of them).  Sharded, tau[b] (the k-th largest of every shard's
+// head scores, shard_tau_kernel) <= the GLOBAL exact k-th replaces L when larger, so each
+// shard fetches only what can reach the global top-k.
+//   phase 0: head + tail in one launch (one shard);
+//   phase 1: head only — exact head keys to hkeys[b][k], their scores to lb[b][k];
+//   phase 2: tail, from hkeys and tau.
 __global__ void __launch_bounds__(256)
     rerank_kernel(const float* __restrict__ docs, const float* __restrict__ qv, int D,
                   const uint64_t* __restrict__ cand, int kp, const uint64_t* __restrict__ part,
                   int grid, int ldlists, int kc, int k, int64_t row0,
                   const float* __restrict__ xstats, int fmt, const float* __restrict__ qscale,
                   uint64_t* __restrict__ out_keys, int64_t* __restrict__ out_ids,
-                  float* __restrict__ out_scores, int* __restrict__ flags, int rows_per_round) {
+                  float* __restrict__ out_scores, int* __restrict__ flags, int rows_per_round,
+                  int phase, const float* __restrict__ tau, uint64_t* __restrict__ hkeys,
+                  float* __restrict__ lb) {
   extern __shared__ __align__(16) float rsm[];
   float* qs = rsm;                                             // [D]
   uint64_t* keys = reinterpret_cast<uint64_t*>(rsm + ((D + 3) & ~3));  // [kp]
   float* rowbuf = reinterpret_cast<float*>(keys + kp);         // [R][D+4] staged rows
   __shared__ float s_red[96];
+  __shared__ float s_min[8];
   __shared__ int s_fail;
   __shared__ __align__(8) uint64_t s_bar;
   const int b = blockIdx.x;
@@ -308,23 +323,86 @@ __global__ void __launch_bounds__(256)
   const float sq = fmt == FMT_I8 ? qscale[b] : 1.0f;
   const float cscale = fmt == FMT_I8 ? sq * xstats[5] : 1.0f;
   query_norms(q, D, fmt, sq, qs, s_red);  // the certificate's error bound, below
-  if (threadIdx.x == 0) s_fail = 0;
+  if (threadIdx.x == 0) {
+    s_fail = 0;
+    mbar_init(&s_bar, (uint32_t)rows_per_round);
+    fence_barrier_init();
+  }
   __syncthreads();
-  const uint64_t* cb = cand + (size_t)b * kp;
-  const uint64_t tprime = cb[kp - 1];  // coarse k'-th key (0: fewer than k' candidates)
-  // Certificate error bound E (below) and candidate pruning: |exact - cscale * coarse| <= E
-  // for every document, so the k best coarse candidates all score >= cscale c_k - E exactly,
-  // and a candidate with cscale c_j + E < cscale c_k - E cannot enter the exact top-k.  The
-  // candidates are sorted by coarse key: only the prefix down to cscale c_k - 2E is fetched
-  // (the s8 pass sizes k' = 8k for the certificate, but the prefix is typically ~k'/2).
   float qn, qh, qr;
   query_norms_final(s_red, fmt, &qn, &qh, &qr);
   const float E = cert_err_bound(fmt, qn, qh, qr, xstats);
-  int kpe = kp;  // candidates re-ranked
-  const uint64_t ckk = k <= kp ? cb[k - 1] : 0ull;
-  if (ckk != 0ull) {
-    const float lim = (vx_key_score(ckk) * cscale - E) - E;
-    int lo = k, hi = kp;  // first index whose candidate falls below lim (cb is descending)
+  const uint64_t* cb = cand + (size_t)b * kp;
+  const uint64_t tprime = cb[kp - 1];  // coarse k'-th key (0: fewer than k' candidates)
+  const int kh = k < kp ? k : kp;      // head rows
+  // The candidate rows are random 3 KB gathers from HBM (DRAM-page unfriendly); per-thread
+  // loads left too few bytes in flight (measured 85 us at B=128).  Instead each round stages
+  // R rows into smem with one TMA bulk copy per row (R x 3 KB in flight per SM), then R
+  // threads run the in-order fmaf chains from smem (row stride D+4 floats: the LDS.128 of
+  // 8 consecutive lanes hit distinct banks).
+  const int R = rows_per_round, RS = D + 4;
+  int round = 0;
+  auto rescore = [&](int j0, int j1) {  // exact keys of candidates [j0, j1) into keys[]
+    for (int r0 = j0; r0 < j1; r0 += R, ++round) {
+      const int t = threadIdx.x;
+      const int idx = r0 + t;
+      uint64_t ck = 0ull;
+      if (t < R) {
+        ck = idx < j1 ? cb[idx] : 0ull;
+        const uint32_t bytes = ck ? (uint32_t)D * 4u : 0u;
+        mbar_expect_tx(&s_bar, bytes);  // every staging thread arrives once (count R)
+        if (ck)
+          bulk_load(rowbuf + (size_t)t * RS, docs + (size_t)vx_key_id(ck) * D, bytes, &s_bar);
+      }
+      mbar_wait(&s_bar, (uint32_t)(round & 1));
+      if (t < R && idx < j1) {
+        uint64_t ek = 0ull;
+        if (ck) {
+          const float4* x = reinterpret_cast<const float4*>(rowbuf + (size_t)t * RS);
+          float acc = 0.0f;
+          for (int c = 0; c < (D >> 2); ++c) {
+            const float4 xv = x[c];
+            acc = fmaf(xv.x, qs[4 * c + 0], acc);
+            acc = fmaf(xv.y, qs[4 * c + 1], acc);
+            acc = fmaf(xv.z, qs[4 * c + 2], acc);
+            acc = fmaf(xv.w, qs[4 * c + 3], acc);
+          }
+          ek = vx_make_key(acc, vx_key_id(ck));
+        }
+        keys[idx] = ek;
+      }
+      __syncthreads();  // the buffer is reused by the next round's bulk copies
+    }
+  };
+  if (phase == 2) {
+    for (int i = threadIdx.x; i < kh; i += blockDim.x) keys[i] = hkeys[(size_t)b * k + i];
+    __syncthreads();
+  } else {
+    rescore(0, kh);
+  }
+  if (phase == 1) {
+    for (int i = threadIdx.x; i < k; i += blockDim.x) {
+      const uint64_t key = i < kh ? keys[i] : 0ull;
+      hkeys[(size_t)b * k + i] = key;
+      lb[(size_t)b * k + i] = key ? vx_key_score(key) : -INFINITY;
+    }
+    return;
+  }
+  // L = the head's minimum exact score (a bound on the exact k-th once k heads exist)
+  float m = INFINITY;
+  for (int i = threadIdx.x; i < kh; i += blockDim.x)
+    m = fminf(m, keys[i] ? vx_key_score(keys[i]) : -INFINITY);
+  for (int o = 16; o > 0; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) s_min[threadIdx.x >> 5] = m;
+  __syncthreads();
+  float L = s_min[0];
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) L = fminf(L, s_min[w]);
+  if (kh < k) L = -INFINITY;
+  const float tb = tau ? tau[b] : -INFINITY;
+  const float lim = fmaxf(L, tb) - E;
+  int kpe = kp;  // candidates re-ranked: the prefix with cscale c >= lim
+  if (lim > -INFINITY) {
+    int lo = kh, hi = kp;  // first index whose candidate falls below lim (cb is descending)
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
       const uint64_t c = cb[mid];
@@ -334,51 +412,14 @@ __global__ void __launch_bounds__(256)
     kpe = lo;
   }
   for (int i = kpe + threadIdx.x; i < kp; i += blockDim.x) keys[i] = 0ull;
-  // The candidate rows are random 3 KB gathers from HBM (DRAM-page unfriendly); per-thread
-  // loads left too few bytes in flight (measured 85 us at B=128).  Instead each round stages
-  // R rows into smem with one TMA bulk copy per row (R x 3 KB in flight per SM), then R
-  // threads run the in-order fmaf chains from smem (row stride D+4 floats: the LDS.128 of
-  // 8 consecutive lanes hit distinct banks).
-  const int R = rows_per_round, RS = D + 4;
-  if (threadIdx.x == 0) {
-    mbar_init(&s_bar, (uint32_t)R);
-    fence_barrier_init();
-  }
-  __syncthreads();
-  for (int r0 = 0, round = 0; r0 < kpe; r0 += R, ++round) {
-    const int t = threadIdx.x;
-    const int idx = r0 + t;
-    uint64_t ck = 0ull;
-    if (t < R) {
-      ck = idx < kpe ? cb[idx] : 0ull;
-      const uint32_t bytes = ck ? (uint32_t)D * 4u : 0u;
-      mbar_expect_tx(&s_bar, bytes);  // every staging thread arrives once (count R)
-      if (ck)
-        bulk_load(rowbuf + (size_t)t * RS, docs + (size_t)vx_key_id(ck) * D, bytes, &s_bar);
-    }
-    mbar_wait(&s_bar, (uint32_t)(round & 1));
-    if (t < R && idx < kpe) {
-      uint64_t ek = 0ull;
-      if (ck) {
-        const float4* x = reinterpret_cast<const float4*>(rowbuf + (size_t)t * RS);
-        float acc = 0.0f;
-        for (int c = 0; c < (D >> 2); ++c) {
-          const float4 xv = x[c];
-          acc = fmaf(xv.x, qs[4 * c + 0], acc);
-          acc = fmaf(xv.y, qs[4 * c + 1], acc);
-          acc = fmaf(xv.z, qs[4 * c + 2], acc);
-          acc = fmaf(xv.w, qs[4 * c + 3], acc);
-        }
-        ek = vx_make_key(acc, vx_key_id(ck));
-      }
-      keys[idx] = ek;
-    }
-    __syncthreads();  // the buffer is reused by the next round's bulk copies
-  }
-  // certificate 1: no CTA that truncated its list (16 kept) had its 16th key inside the top-k'
+  rescore(kh, kpe);
+  // certificate 1: no CTA that truncated its list (KC kept) had its last key inside the
+  // top-k' (sharded: a truncated list whose dropped keys are all bounded below tau is harmless)
   for (int t = threadIdx.x; t < grid; t += blockDim.x) {
     const uint64_t last = part[((size_t)b * ldlists + t) * kc + (kc - 1)];
-    if (last != 0ull && (tprime == 0ull || last >= tprime)) s_fail = 1;
+    if (last != 0ull && (tprime == 0ull || last >= tprime) &&
+        !(vx_key_score(last) * cscale + E < tb))
+      s_fail = 1;
   }
   __syncthreads();
   // block bitonic sort of the exact keys (kp is a power of two)
@@ -405,8 +446,11 @@ __global__ void __launch_bounds__(256)
     //   looser).  TF32 coarse: per-operand truncation <= 2^-10 -> 2^-9 |q| max|x|.
     //   Both: + 2^-12 |q| max|x| for the fp32 accumulation of the tensor core and of the
     //   exact in-order chain (each <= 768 * 2^-24 relative, 5x margin).
+    // Sharded: a document outside the candidates is also out of the GLOBAL top-k when its
+    // bound is below tau (the shard then reports fewer than k keys, padded with 0).
+    const float bound = vx_key_score(tprime) * cscale + E;
     const uint64_t ek = keys[k - 1];
-    if (ek == 0ull || !(vx_key_score(ek) > vx_key_score(tprime) * cscale + E)) s_fail = 1;
+    if (!(bound < tb) && (ek == 0ull || !(vx_key_score(ek) > bound))) s_fail = 1;
   }
   __syncthreads();
   for (int i = threadIdx.x; i < k; i += blockDim.x) {
@@ -705,8 +749,9 @@ static int kRerankRows = 16;
 cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64_t* cand, int B,
                           int kp, const uint64_t* part, int grid, int ldlists, int kc, int k,
                           int64_t row0, const float* xstats, int fmt, const float* qscale,
-                          uint64_t* out_keys,
-                          int64_t* out_ids, float* out_scores, int* flags, cudaStream_t st) {
+                          uint64_t* out_keys, int64_t* out_ids, float* out_scores, int* flags,
+                          cudaStream_t st, int phase, const float* tau, uint64_t* hkeys,
+                          float* lb) {
   const size_t base = (size_t)((D + 3) & ~3) * 4 + (size_t)kp * 8;
   const size_t row = (size_t)(D + 4) * 4;
   static const int env_rows = [] {  // timing experiments: VX_DEBUG_RERANK_ROWS, read once
@@ -721,7 +766,44 @@ cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64
                                        (int)smem);
   if (e != cudaSuccess) return e;
   rerank_kernel<<<B, 256, smem, st>>>(docs, q, D, cand, kp, part, grid, ldlists, kc, k, row0,
-                                      xstats, fmt, qscale, out_keys, out_ids, out_scores, flags, R);
+                                      xstats, fmt, qscale, out_keys, out_ids, out_scores, flags, R,
+                                      phase, tau, hkeys, lb);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------- sharded threshold tau
+// all[G][B][k]: every shard's head exact scores (rerank phase 1; -inf = empty) — distinct
+// documents, so tau[b] = the largest v with count(all >= v) >= k is <= the global exact k-th.
+__global__ void __launch_bounds__(256)
+    shard_tau_kernel(const float* __restrict__ all, int G, int B, int k, float* __restrict__ tau) {
+  __shared__ float s_v[1024];
+  __shared__ float s_w[8];
+  const int b = blockIdx.x;
+  const int n = G * k;  // <= 1024 (G <= 8, k <= 128)
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    s_v[i] = all[((size_t)(i / k) * B + b) * k + (i % k)];
+  __syncthreads();
+  float best = -INFINITY;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const float v = s_v[i];
+    if (!(v > -INFINITY)) continue;
+    int cnt = 0;
+    for (int j = 0; j < n; ++j) cnt += s_v[j] >= v ? 1 : 0;
+    if (cnt >= k) best = fmaxf(best, v);
+  }
+  for (int o = 16; o > 0; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = s_w[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmaxf(m, s_w[w]);
+    tau[b] = m;
+  }
+}
+
+cudaError_t launch_shard_tau(const float* all, int G, int B, int k, float* tau, cudaStream_t st) {
+  if (G * k > 1024) return cudaErrorInvalidValue;
+  shard_tau_kernel<<<B, 256, 0, st>>>(all, G, B, k, tau);
   return cudaGetLastError();
 }
 

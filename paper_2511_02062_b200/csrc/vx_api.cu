@@ -34,6 +34,7 @@ NcclApi& nccl() {
     SYM(CommDestroy, "ncclCommDestroy");
     SYM(Broadcast, "ncclBroadcast");
     SYM(Reduce, "ncclReduce");
+    SYM(AllGather, "ncclAllGather");
     SYM(Send, "ncclSend");
     SYM(Recv, "ncclRecv");
     SYM(GroupStart, "ncclGroupStart");
@@ -41,7 +42,8 @@ NcclApi& nccl() {
     SYM(GetErrorString, "ncclGetErrorString");
 #undef SYM
     api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Broadcast &&
-             api.Send && api.Recv && api.GroupStart && api.GroupEnd && api.GetErrorString;
+             api.Reduce && api.AllGather && api.Send && api.Recv && api.GroupStart &&
+             api.GroupEnd && api.GetErrorString;
   });
   return api;
 }
@@ -165,6 +167,11 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
   ALLOC(h->d_send, B * K * 8);
   if (d->n_shards > 1 && d->shard == 0)
     ALLOC(h->d_recv, (size_t)d->n_shards * B * K * 8);
+  if (d->n_shards > 1) {  // the sharded re-rank threshold (all-gathered lower bounds)
+    ALLOC(h->d_lball, (size_t)d->n_shards * B * K * 4);
+    ALLOC(h->d_tau, B * 4);
+    ALLOC(h->d_hkeys, B * K * 8);
+  }
   ALLOC(h->d_hdr, 16);
   ALLOC(h->d_ckeys, B * 1024 * 8);
   ALLOC(h->d_flags, B * 4);
@@ -241,7 +248,7 @@ extern "C" vx_status vx_index_destroy(vx_index* h) {
                   h->d_ids, h->d_ip,      h->d_ms,     h->d_out_ids, h->d_out_ip,
                   h->d_out_ms, h->d_send, h->d_recv, h->d_hdr, h->d_ckeys, h->d_flags,
                   h->d_xnorm, h->d_fq, h->docs16, h->d_q16, h->d_fidx, h->d_fcount,
-                  h->d_qtok16, h->docs8, h->d_q8, h->d_qs8};
+                  h->d_qtok16, h->docs8, h->d_q8, h->d_qs8, h->d_lball, h->d_tau, h->d_hkeys};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->h_stage) cudaFreeHost(h->h_stage);

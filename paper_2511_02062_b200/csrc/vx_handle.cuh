@@ -26,6 +26,7 @@ struct NcclApi {
                             cudaStream_t);
   ncclResult_t (*Reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
                          cudaStream_t);
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
   ncclResult_t (*GroupStart)();
@@ -112,6 +113,9 @@ struct vx_index {
   float* d_out_ms = nullptr;
   void* d_send = nullptr;        // [maxB][maxK] x 8 B scratch (rank 0: the reduced MaxSim)
   void* d_recv = nullptr;        // [G][maxB][maxK] gathered keys (rank 0)
+  float* d_lball = nullptr;      // [G][maxB][maxK] all-gathered coarse lower bounds (G > 1)
+  float* d_tau = nullptr;        // [maxB] lower bound of the global exact k-th (G > 1)
+  uint64_t* d_hkeys = nullptr;   // [maxB][maxK] exact keys of the re-rank head (G > 1)
   int32_t* d_hdr = nullptr;      // [4]
   uint64_t* d_ckeys = nullptr;   // [maxB][512] merged coarse keys (TC path)
   int* d_flags = nullptr;        // [maxB] certificate failures (TC path)

@@ -73,11 +73,17 @@ cudaError_t launch_scan_tc(int QT, int TD, const CUtensorMap* tq, const CUtensor
 size_t scan_tc2_smem(int H, int* ns_out);
 cudaError_t launch_scan_tc2(int H, const CUtensorMap* tq, const CUtensorMap* tx,
                             const ScanTcArgs& a, int grid, size_t smem, cudaStream_t st);
+// phase 0: the whole re-rank; sharded: phase 1 (head: exact keys of the k best coarse
+// candidates -> hkeys, their scores -> lb) and phase 2 (tail, pruned by tau) around the
+// exchange of lb (see scan_tc.cu)
 cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64_t* cand, int B,
                           int kp, const uint64_t* part, int grid, int ldlists, int kc, int k,
                           int64_t row0, const float* xstats, int fmt, const float* qscale,
                           uint64_t* out_keys, int64_t* out_ids, float* out_scores, int* flags,
-                          cudaStream_t st);
+                          cudaStream_t st, int phase = 0, const float* tau = nullptr,
+                          uint64_t* hkeys = nullptr, float* lb = nullptr);
+// tau[B] = k-th largest of all[G][B][k] (G k <= 1024)
+cudaError_t launch_shard_tau(const float* all, int G, int B, int k, float* tau, cudaStream_t st);
 // second certificate level over the full per-CTA lists (compacted failing queries): two
 // launches; wkeys = scratch of B x P_single x kc keys
 cudaError_t launch_rerank_wide(const float* docs, const float* fq, int D, const int* fidx,

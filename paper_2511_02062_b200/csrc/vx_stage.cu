@@ -95,6 +95,18 @@ static bool tc_eligible(const vx_index* h, int B, int k) {
 
 // Tensor-core path: K2 coarse scan (top-16/32 per CTA) -> K3 merge to top-k' -> K2b exact
 // re-rank + certificate -> exact re-scan of any query whose certificate failed.
+// Sharded threshold exchange: every rank contributes B x k exact scores of distinct
+// documents (lb; -inf = empty); tau[b] = the k-th largest of the union is <= the global
+// exact k-th.  All ranks call it at the same point of the stage.
+static vx_status shard_tau(vx_index* h, const float* lb, int B, int k, cudaStream_t st,
+                           bool want_tau) {
+  NCCL_TRY(nccl().AllGather(lb, h->d_lball, (size_t)B * k, ncclFloat32, h->comm, st));
+  if (!want_tau) return VX_OK;
+  CU_TRY(vx::launch_shard_tau(h->d_lball, h->nranks, B, k, h->d_tau, st));
+  count_launch(h);
+  return VX_OK;
+}
+
 static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint64_t* keys,
                                int64_t* ids, float* scores, cudaStream_t st) {
   const int D = h->desc.dim;
@@ -176,23 +188,43 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
   // re-rank — one launch each per run of query groups with the same P (the whole batch
   // when every group ran on CTA pairs), so the 2-per-SM re-rank CTAs pack full waves
   const int ldp = grid * KC;
+  auto lists_per_query = [&](int r) {
+    return (pairs && std::min(GS, B - r) > 128) ? grid / 2 : grid;
+  };
   for (int r0 = 0; r0 < B;) {
-    const int P = (pairs && std::min(GS, B - r0) > 128) ? grid / 2 : grid;
+    const int P = lists_per_query(r0);
     int r1 = r0;
-    while (r1 < B && ((pairs && std::min(GS, B - r1) > 128) ? grid / 2 : grid) == P) r1 += GS;
+    while (r1 < B && lists_per_query(r1) == P) r1 += GS;
     r1 = std::min(r1, B);
-    const int Bn = r1 - r0;
-    const uint64_t* part = h->d_part + (size_t)r0 * ldp;
-    uint64_t* ck = h->d_ckeys + (size_t)r0 * kp;
-    CU_TRY(vx::launch_merge_topk(part, Bn, P * KC, kp, 0, ck, nullptr, nullptr, st, nullptr,
+    CU_TRY(vx::launch_merge_topk(h->d_part + (size_t)r0 * ldp, r1 - r0, P * KC, kp, 0,
+                                 h->d_ckeys + (size_t)r0 * kp, nullptr, nullptr, st, nullptr,
                                  ldp));
     count_launch(h);
-    CU_TRY(vx::launch_rerank(h->docs, d_q + (size_t)r0 * D, D, ck, Bn, kp, part, P, grid, KC, k,
-                             h->row0, reinterpret_cast<const float*>(h->d_xnorm), fmt,
-                             i8 ? h->d_qs8 + r0 : nullptr, keys + (size_t)r0 * k,
-                             ids + (size_t)r0 * k, scores + (size_t)r0 * k, h->d_flags + r0, st));
-    count_launch(h);
     r0 = r1;
+  }
+  // exact re-rank.  Sharded: phase 1 re-scores each query's k best coarse candidates, the
+  // shards all-gather those exact scores (shard_tau: tau <= the global exact k-th), phase 2
+  // re-ranks only the candidates that can still reach the GLOBAL top-k
+  const bool sharded = h->nranks > 1;
+  float* lb = reinterpret_cast<float*>(h->d_send);
+  for (int pass = sharded ? 1 : 0; pass <= (sharded ? 2 : 0); ++pass) {
+    if (pass == 2) VX_TRY(shard_tau(h, lb, B, k, st, true));
+    for (int r0 = 0; r0 < B;) {
+      const int P = lists_per_query(r0);
+      int r1 = r0;
+      while (r1 < B && lists_per_query(r1) == P) r1 += GS;
+      r1 = std::min(r1, B);
+      CU_TRY(vx::launch_rerank(h->docs, d_q + (size_t)r0 * D, D, h->d_ckeys + (size_t)r0 * kp,
+                               r1 - r0, kp, h->d_part + (size_t)r0 * ldp, P, grid, KC, k,
+                               h->row0, reinterpret_cast<const float*>(h->d_xnorm), fmt,
+                               i8 ? h->d_qs8 + r0 : nullptr, keys + (size_t)r0 * k,
+                               ids + (size_t)r0 * k, scores + (size_t)r0 * k, h->d_flags + r0,
+                               st, pass, pass == 2 ? h->d_tau + r0 : nullptr,
+                               sharded ? h->d_hkeys + (size_t)r0 * k : nullptr,
+                               lb + (size_t)r0 * k));
+      count_launch(h);
+      r0 = r1;
+    }
   }
   // Certificate failures, entirely on device (no host round trip: the stage stays
   // capturable in one CUDA graph; every launch below exits at once when its count is 0):
@@ -231,7 +263,11 @@ static vx_status local_topk(vx_index* h, const float* d_q, int B, int k, uint64_
     if (!tc_eligible(h, B, k)) return fail(VX_ERR_UNSUPPORTED, "tensor-core scan needs k <= 128");
     return local_topk_tc(h, d_q, B, k, keys, ids, scores, st);
   }
-  return local_topk_f32(h, d_q, B, k, keys, ids, scores, st);
+  VX_TRY(local_topk_f32(h, d_q, B, k, keys, ids, scores, st));
+  // the exact path needs no threshold, but takes part in the exchange whenever a tensor-
+  // core rank could be waiting in it (k <= 128), so mixed paths never deadlock
+  if (h->nranks > 1 && tc_eligible(h, B, k)) VX_TRY(shard_tau(h, scores, B, k, st, false));
+  return VX_OK;
 }
 
 vx_status run_maxsim(vx_index* h, const float* d_qtok, int B, int nq, const int64_t* d_cand,

@@ -91,3 +91,84 @@ def test_two_rank_gloo_two_phase_exchange_equals_global(oracle):
         p.join(timeout=60)
         assert p.exitcode == 0
     assert ok
+
+
+def _tau_worker(rank: int, world: int, port: int, q) -> None:
+    """The sharded re-rank threshold (vx_stage.cu shard_tau, scan_tc.cu shard_lb/shard_tau/
+    rerank_kernel) restated on CPU: s8 coarse scores with the certificate's rigorous bound E,
+    tau = k-th largest of the all-gathered lower bounds, each shard re-ranks only candidates
+    with cscale c + E >= tau and certifies with `bound(T') < tau or exact k-th > bound(T')`;
+    rank 0's merge must equal the single-index oracle."""
+    import torch
+    import torch.distributed as dist
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import vxoracle as o
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    N, D, B, k, kp = 40_000, 128, 6, 10, 80
+    r0, n = shard_range(N, world, rank)
+    X = o.synth_rows(42, r0, n, D).astype(np.float64)
+    Q = o.synth_rows(43, 0, B, D).astype(np.float64)
+    sx = np.abs(X).max() / 127.0
+    X8 = np.clip(np.rint(X / sx), -127, 127)
+    rx, xh = np.linalg.norm(X - X8 * sx, axis=1).max(), np.linalg.norm(X8 * sx, axis=1).max()
+    sq = np.abs(Q).max(axis=1) / 127.0
+    Q8 = np.clip(np.rint(Q / sq[:, None]), -127, 127)
+    rq = np.linalg.norm(Q - Q8 * sq[:, None], axis=1)
+    qh = np.linalg.norm(Q8 * sq[:, None], axis=1)
+    E = (qh * rx + rq * xh + rq * rx) * 1.001 + 1e-9
+    coarse = (Q8 @ X8.T) * (sq[:, None] * sx)          # cscale * s32 dot
+    cand = np.argsort(-coarse, axis=1, kind="stable")[:, :kp]
+    ccand = np.take_along_axis(coarse, cand, axis=1)
+    lb = torch.from_numpy(np.ascontiguousarray(ccand[:, :k] - E[:, None]))
+    allb = [torch.zeros_like(lb) for _ in range(world)]
+    dist.all_gather(allb, lb)
+    tau = np.sort(np.concatenate([t.numpy() for t in allb], axis=1), axis=1)[:, ::-1][:, k - 1]
+    Xe = o.synth_rows(42, r0, n, D)
+    Qe = o.synth_rows(43, 0, B, D)
+    ids = np.full((B, k), -1, np.int64)
+    sc = np.full((B, k), -np.inf, np.float32)
+    ok = True
+    fetched = 0
+    for b in range(B):
+        keep = cand[b][ccand[b] + E[b] >= tau[b]]          # the pruned prefix
+        fetched += keep.size
+        ex = np.array([o.flat_topk(Xe[j:j + 1], Qe[b:b + 1], 1, mode=1)[1][0, 0] for j in keep],
+                      np.float32)
+        order = np.lexsort((keep, -ex))[:k]
+        ids[b, :order.size] = keep[order] + r0
+        sc[b, :order.size] = ex[order]
+        bound = ccand[b, -1] + E[b]
+        ok &= bool(bound < tau[b] or (order.size == k and ex[order[-1]] > bound))
+    gathered = [None] * world
+    dist.all_gather_object(gathered, (ids, sc, ok, fetched))
+    if rank == 0:
+        allid = np.concatenate([g[0] for g in gathered], axis=1)
+        allsc = np.concatenate([g[1] for g in gathered], axis=1)
+        merged = np.zeros((B, k), np.int64)
+        for b in range(B):
+            order = np.lexsort((allid[b], -allsc[b]))[:k]
+            merged[b] = allid[b][order]
+        want, _ = o.flat_topk(o.synth_rows(42, 0, N, D), o.synth_rows(43, 0, B, D), k, mode=1,
+                              threads=2)
+        certified = all(g[2] for g in gathered)
+        q.put((certified, bool(np.array_equal(merged, want)), sum(g[3] for g in gathered)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_gloo_sharded_threshold_prunes_and_stays_exact(oracle):
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29600 + os.getpid() % 1000
+    procs = [ctx.Process(target=_tau_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    certified, exact, fetched = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert certified and exact
+    assert fetched < 2 * 6 * 80  # the threshold pruned candidates on the shards
