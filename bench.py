@@ -296,8 +296,7 @@ def maxsim_roofline(pk: dict, *, B: int, C: int, nq: int, nd: int, d: int, ms: f
     top = hbm if t_hbm >= t_comp else comp
     return {"bound": "hbm" if top is hbm else "tensor", "achieved": top["achieved"],
             "peak": top["peak"], "unit": top["unit"], "frac": top["frac"],
-            "floor_ms": max(t_hbm, t_comp) * 1e3 * launches, "hbm": hbm, "compute": comp,
-            "launches": launches, "queries_per_launch": bq, "launch_ms": s * 1e3,
+            "floor_ms": max(t_hbm, t_comp) * 1e3, "hbm": hbm, "compute": comp,
             "peak_src": pk["src"]}
 
 

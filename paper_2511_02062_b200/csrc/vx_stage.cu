@@ -71,16 +71,22 @@ static int kprime_of(const vx_index* h, int k, int fmt) {
 
 // coarse operand format of the tensor-core pass for this handle
 // AUTO takes the s8 pass (a quarter of the fp32 bytes, twice the bf16 tensor rate; measured
-// 10M x 768 B=1024 stage 8.99 ms vs 13.5 ms bf16 — profiles/r01/README.md) when the shard's
-// one-scale quantisation is tight enough for the certificate to hold at k' = 8 next_pow2(k):
-// max |x - sx x8| <= 3 % of the mean row norm (synthetic rows ~1 %, Gaussian rows ~1.5 %).
-// An outlier coordinate inflates the shared scale, widens the error bound E and would push
-// queries to the exact re-scan — bf16 then.
+// 10M x 768 B=1024 stage 8.99 ms vs 13.5 ms bf16 — profiles/r01/README.md) when
+//  * the shard's one-scale quantisation is tight enough for the certificate to hold at
+//    k' = 8 next_pow2(k): max |x - sx x8| <= 3 % of the mean row norm (synthetic rows ~1 %,
+//    Gaussian rows ~1.5 %) — an outlier coordinate inflates the shared scale, widens the
+//    error bound E and would push queries to the exact re-scan;
+//  * the shard is long enough for the pass to amortise filling the 32-key lists: >= 16
+//    tiles per CTA (100K x 768, B=16: s8 0.093 ms vs bf16 0.063 ms — the first tiles insert
+//    every document).
+// Otherwise bf16.
 constexpr float kI8AutoMaxRelResidual = 0.03f;
+constexpr int kI8AutoMinTilesPerCta = 16;
 
 int coarse_fmt(const vx_index* h) {
   if (h->coarse == VX_COARSE_I8 && h->docs8) return vx::FMT_I8;
   if (h->coarse == VX_COARSE_AUTO && h->docs8 &&
+      h->n_local >= (int64_t)256 * h->num_sms * kI8AutoMinTilesPerCta &&
       h->xstats_host[4] <= kI8AutoMaxRelResidual * h->xstats_host[7] / (float)std::max<int64_t>(1, h->n_local))
     return vx::FMT_I8;
   if (h->coarse == VX_COARSE_TF32 || !h->docs16) return vx::FMT_TF32;

@@ -64,10 +64,11 @@ def test_upload_refreshes_shadow(vx, oracle):
 
 
 def test_auto_coarse_follows_quantisation_quality(vx, oracle):
-    # AUTO takes the s8 pass when the shard's one-scale quantisation is tight (max residual
-    # norm <= 3 % of the mean row norm: the synthetic rows are at ~1 %), bf16 when an outlier
-    # coordinate inflates the shared scale — exact either way
-    N, D, B, k = 20_000, 768, 40, 10
+    # AUTO takes the s8 pass when the shard is long enough (>= 16 tiles of 256 rows per CTA)
+    # and its one-scale quantisation is tight (max residual norm <= 3 % of the mean row norm:
+    # the synthetic rows are at ~1 %), bf16 when an outlier coordinate inflates the shared
+    # scale or the shard is short — exact either way
+    N, D, B, k = 700_000, 256, 24, 10
     X = oracle.synth_rows(42, 0, N, D)
     Q = oracle.synth_rows(43, 0, B, D)
     with vx.Index(N, D, max_batch=B, max_k=k) as idx:
@@ -85,3 +86,6 @@ def test_auto_coarse_follows_quantisation_quality(vx, oracle):
         assert np.array_equal(ids, rid) and np.array_equal(sc, rsc.astype(np.float32))
         idx.upload(X[123:124], 123)  # back to the tight scale
         assert idx.coarse_auto() == "i8"
+    with vx.Index(50_000, D, max_batch=B, max_k=k) as idx:  # 1-2 tiles per CTA
+        idx.synth(42)
+        assert idx.coarse_auto() == "bf16"
