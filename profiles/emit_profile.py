@@ -38,7 +38,7 @@ qt = torch.from_numpy(synth.query_tokens(bmax, nq, td)).to(dev)
 ids = torch.empty((bmax, k), dtype=torch.int64, device=dev)
 ip = torch.empty((bmax, k), dtype=torch.float32, device=dev)
 ms = torch.empty((bmax, k), dtype=torch.float32, device=dev)
-mem_gb = (N * D * 4 + N * D * 2 + T * Nd * td * 2) / 1e9  # fp32 rows + bf16 shadow + tokens
+mem_gb = (N * D * (4 + 2 + 1) + T * Nd * td * 2) / 1e9  # fp32 rows + bf16 + s8 shadows + tokens
 profile = {}
 for B in BATCHES:
     lat = []
