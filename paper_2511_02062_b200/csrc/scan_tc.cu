@@ -744,8 +744,10 @@ cudaError_t launch_scan_tc(int QT, int TD, const CUtensorMap* tq, const CUtensor
 // rows per staging round: 16 rows (~54 KB of smem) lets four CTAs share an SM, so the
 // CTAs' row gathers overlap each other's fmaf chains.  Measured at B = 1024, k' = 256
 // (one launch): R = 8/10/12/14/16/21/24/32: - / 255 / 222 / 201 / 179 / 221 / 251 / 208 us
-// (R = 64, one CTA per SM: 4 x 67 us)
-static int kRerankRows = 16;
+// (R = 64, one CTA per SM: 4 x 67 us).  With the s8 pass's k' = 1024 (~600 rows fetched
+// per query) 32 rows per round do better: stage 7.65 vs 7.83 ms at B = 1024 (R = 8 / 16 /
+// 24 / 32 / 48 / 64: 7.92 / 7.83 / 7.75 / 7.65 / 7.79 / 7.65 ms).
+static int rerank_rows(int kp) { return kp >= 512 ? 32 : 16; }
 cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64_t* cand, int B,
                           int kp, const uint64_t* part, int grid, int ldlists, int kc, int k,
                           int64_t row0, const float* xstats, int fmt, const float* qscale,
@@ -758,9 +760,9 @@ cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64
     const char* e = getenv("VX_DEBUG_RERANK_ROWS");
     return e ? atoi(e) : 0;
   }();
-  if (env_rows > 0) kRerankRows = env_rows;
+  const int want = env_rows > 0 ? env_rows : rerank_rows(kp);
   int R = (int)((220 * 1024 - base) / row);
-  R = R > kRerankRows ? kRerankRows : (R < 1 ? 1 : R);
+  R = R > want ? want : (R < 1 ? 1 : R);
   const size_t smem = base + (size_t)R * row;
   cudaError_t e = cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
