@@ -89,3 +89,32 @@ def test_auto_coarse_follows_quantisation_quality(vx, oracle):
     with vx.Index(50_000, D, max_batch=B, max_k=k) as idx:  # 1-2 tiles per CTA
         idx.synth(42)
         assert idx.coarse_auto() == "bf16"
+
+
+def _clustered(rng, n, D, n_centers, spread):
+    centers = rng.standard_normal((n_centers, D)).astype(np.float32)
+    lab = rng.integers(0, n_centers, n)
+    return (centers[lab] + spread * rng.standard_normal((n, D))).astype(np.float32), centers
+
+
+@pytest.mark.parametrize("coarse", ["i8", "bf16"])
+@pytest.mark.parametrize("spread", [0.05, 0.002])
+def test_coarse_exact_on_clustered_near_duplicates(vx, oracle, coarse, spread):
+    # near-duplicate documents (tight clusters, queries at the centres): the coarse error
+    # bound E exceeds the gaps between many candidates, so certificates fail and the level-2
+    # / level-3 paths carry the queries — the answer must still be the exact oracle's
+    rng = np.random.default_rng(7)
+    N, D, B, k = 700_000, 256, 48, 16
+    X, centers = _clustered(rng, N, D, 300, spread)
+    Q = (centers[rng.integers(0, 300, B)] + 0.01 * rng.standard_normal((B, D))).astype(np.float32)
+    with vx.Index(N, D, max_batch=B, max_k=k) as idx:
+        idx.upload(X, 0)
+        idx.set_option(vx.VX_OPT_SCAN, vx.VX_SCAN_TC)
+        idx.set_option(vx.VX_OPT_COARSE, {"i8": vx.VX_COARSE_I8, "bf16": vx.VX_COARSE_BF16}[coarse])
+        ids, sc = idx.search(Q, k)
+        st = idx.stats()
+    rid, rsc = oracle.flat_topk(X, Q, k, mode=1)
+    assert np.array_equal(ids, rid)
+    assert np.array_equal(sc, rsc.astype(np.float32))
+    if spread < 0.01:  # the tight case must have exercised the fallbacks
+        assert st["cert_level2"] + st["cert_fallbacks"] > 0
