@@ -101,14 +101,23 @@ def scan_roofline(pk: dict, *, tc: bool, coarse: str | None, n_local: int, D: in
     comp["frac"] = comp["achieved"] / comp["peak"]
     if tc:
         comp["frac_of_burst"] = comp["achieved"] / (pk["bf16_tflops"] * mult)
+        # datasheet dense figures (B200_PROFILING.md, context only): bf16 2250, tf32 1100,
+        # 8-bit 4500 T(FL)OP/s
+        comp["frac_of_nominal"] = comp["achieved"] / {"bf16": 2250.0, "tf32": 1100.0,
+                                                      "i8": 4500.0}[coarse]
     t_hbm = hbm_bytes / (hbm["peak"] * 1e9)
     t_comp = flops / (comp["peak"] * 1e12)
     top = hbm if t_hbm >= t_comp else comp
+    src = pk["src"]
+    if top is comp and coarse in ("i8", "tf32"):
+        src += (f" ({mult:g} x bf16_tflops_sustained: kind::{'i8' if coarse == 'i8' else 'tf32'} "
+                f"issues {mult:g}x the MACs of a bf16 MMA per tensor cycle — "
+                f"profiles/r01/microbench_mma_rate*.log)")
     return {"bound": "hbm" if top is hbm else "tensor", "achieved": top["achieved"],
             "peak": top["peak"], "unit": top["unit"], "frac": top["frac"],
             "floor_ms": max(t_hbm, t_comp) * 1e3 * launches, "hbm": hbm, "compute": comp,
             "launches": launches, "queries_per_launch": bq, "launch_ms": s * 1e3,
-            "peak_src": pk["src"]}
+            "peak_src": src}
 
 
 WORKLOADS = {
