@@ -196,15 +196,18 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
           uint32_t r[64];
           tmem_ld64(col + cc * 64, r);
           tmem_ld_wait();
+          if (t == C::QPT - 1 && cc == TD / 64 - 1) {
+            // last chunk of the buffer in registers: release it before the selection
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[buf]);
+          }
           if (q >= a.B || (a.dbg_no_select & 1)) continue;
           const uint32_t doc0 = (uint32_t)tile * TD + cc * 64;
           admit<FMT, KC, 32>(r, doc0, n_local, scratch, NEPI, L[t], thr[t]);
           admit<FMT, KC, 32>(r + 32, doc0 + 32, n_local, scratch, NEPI, L[t], thr[t]);
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[buf]);
       if (++buf == C::NBUF) {
         buf = 0;
         bph ^= 1;

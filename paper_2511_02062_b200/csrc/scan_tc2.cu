@@ -241,13 +241,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P2Cfg<QG>::kThreads,
         uint32_t r[64];
         tmem_ld64(col + cc * 64, r);
         tmem_ld_wait();
+        if (cc == TD / 64 - 1) {
+          // the tile's last chunk is in registers: hand the accumulator buffer back to the
+          // MMA now, not after the selection — the next-but-one tile's MMAs overlap it
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(te_leader + (uint32_t)(buf * 8));
+        }
         if (q >= a.B || (a.dbg_no_select & 1)) continue;
         const uint32_t doc0 = (uint32_t)tile * TD + cc * 64;  // columns map to docs 1:1
         admit<FMT, KC, 64>(r, doc0, n_local, scratch, SS, L, thr);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(te_leader + (uint32_t)(buf * 8));
       if (++buf == C::NBUF) {
         buf = 0;
         bph ^= 1;

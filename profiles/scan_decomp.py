@@ -21,7 +21,7 @@ from paper_2511_02062_b200 import synth  # noqa: E402
 coarse = sys.argv[1] if len(sys.argv) > 1 else "i8"
 Bs = [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "128,256,1024").split(",")]
 bits = [int(x) for x in (sys.argv[3] if len(sys.argv) > 3 else "0,1,7,9").split(",")]
-pairs = int(sys.argv[4]) if len(sys.argv) > 4 else 1
+pairs = int(sys.argv[4]) if len(sys.argv) > 4 else -1  # -1: the library default
 CO = {"bf16": vx.VX_COARSE_BF16, "tf32": vx.VX_COARSE_TF32, "i8": vx.VX_COARSE_I8}[coarse]
 N, D, k = 10_000_000, 768, 100
 bmax = max(Bs)
@@ -34,7 +34,8 @@ for bit in bits:
     with vx.Index(N, D, max_batch=bmax, max_k=k) as idx:
         idx.synth(42)
         idx.set_option(vx.VX_OPT_COARSE, CO)
-        idx.set_option(vx.VX_OPT_SCAN_PAIRS, pairs)
+        if pairs >= 0:
+            idx.set_option(vx.VX_OPT_SCAN_PAIRS, pairs)
         for B in Bs:
             scan = []
             for rep in range(6):
@@ -42,6 +43,6 @@ for bit in bits:
                 idx.sync()
                 if rep >= 2:
                     scan.append(idx.stats()["last_scan_ms"])
-            print(json.dumps({"coarse": idx.coarse_auto(), "B": B, "bits": bit, "scan_pairs": pairs,
+            print(json.dumps({"coarse": idx.coarse_auto(), "B": B, "bits": bit, "scan_pairs": idx.get_option(vx.VX_OPT_SCAN_PAIRS),
                               "scan_ms": round(statistics.median(scan), 4)}), flush=True)
 os.environ.pop("VX_DEBUG_TC_NOSELECT", None)
