@@ -68,7 +68,10 @@ enum {
                              1: 256 queries per pass; 0: single-CTA kernels */,
   VX_OPT_KPRIME = 8       /* tensor-core candidate set k' re-ranked exactly: 0 (auto:
                              4 next_pow2(k) in [64, 256] for bf16/tf32, 8 next_pow2(k) in
-                             [128, 1024] for s8) or a power of two in [16, 1024] */
+                             [128, 1024] for s8) or a power of two in [16, 1024] */,
+  VX_OPT_SCAN_SEED = 9    /* 1 (default): seed each query's tensor-core scan admission
+                             threshold from a 1/64 row sample of the shard (shards of
+                             >= 512K rows); 0: off.  Results are identical either way. */
 };
 /* Coarse (candidate-selecting) tensor-core scan format.  Either way every reported score is
  * recomputed exactly in fp32 and certified.  BF16 reads a bf16 shadow

@@ -40,7 +40,7 @@ struct TcCfg {
   static constexpr int QPT = QT / EG;                               // query tiles per epilogue thread
 };
 
-template <int QT, int TD, int FMT>
+template <int QT, int TD, int FMT, int KC>
 __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
     scan_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tx,
                    const ScanTcArgs a) {
@@ -48,7 +48,6 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   const int ns = a.ns;
-  constexpr int KC = kc_of(FMT);  // per-CTA list length per query
   // epilogue scratch: the 32 scores of a passing chunk per thread, [32][QT*128] floats
   uint64_t* lists = reinterpret_cast<uint64_t*>(smem + (size_t)ns * C::kStageBytes);
   uint64_t* full = lists + (size_t)QT * 128 * 16;
@@ -179,7 +178,10 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
       for (int j = 0; j < KC; ++j) L[t][j] = 0ull;
     float thr[C::QPT];
 #pragma unroll
-    for (int t = 0; t < C::QPT; ++t) thr[t] = -INFINITY;
+    for (int t = 0; t < C::QPT; ++t) {
+      const int q = (g + t * C::EG) * 128 + m;
+      thr[t] = q < a.B ? seed_thr(a.seed, a.seed_ld, q) : -INFINITY;
+    }
     int buf = 0;
     uint32_t bph = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -311,7 +313,7 @@ __global__ void __launch_bounds__(256)
                   uint64_t* __restrict__ out_keys, int64_t* __restrict__ out_ids,
                   float* __restrict__ out_scores, int* __restrict__ flags, int rows_per_round,
                   int phase, const float* __restrict__ tau, uint64_t* __restrict__ hkeys,
-                  float* __restrict__ lb) {
+                  float* __restrict__ lb, const uint64_t* __restrict__ seed, int seed_ld) {
   extern __shared__ __align__(16) float rsm[];
   float* qs = rsm;                                             // [D]
   uint64_t* keys = reinterpret_cast<uint64_t*>(rsm + ((D + 3) & ~3));  // [kp]
@@ -439,7 +441,11 @@ __global__ void __launch_bounds__(256)
       }
       __syncthreads();
     }
-  if (threadIdx.x == 0 && tprime != 0ull) {
+  // seeded scan (ScanTcArgs::seed): the lists also dropped every document whose coarse score
+  // is below the seed, so a document outside the candidates has coarse score
+  // <= max(s(T'), seed)
+  const float sd = seed_thr(seed, seed_ld, b);
+  if (threadIdx.x == 0 && (tprime != 0ull || sd > -INFINITY)) {
     // certificate 2: every document outside the candidates has coarse score <= s(T'), so
     // its exact score <= s(T') + E; the exact k-th must beat that bound strictly.
     //   bf16 coarse: with q16 = bf16(q), rq = q - q16 (x16, rx likewise, per shard maxima
@@ -451,7 +457,7 @@ __global__ void __launch_bounds__(256)
     //   exact in-order chain (each <= 768 * 2^-24 relative, 5x margin).
     // Sharded: a document outside the candidates is also out of the GLOBAL top-k when its
     // bound is below tau (the shard then reports fewer than k keys, padded with 0).
-    const float bound = vx_key_score(tprime) * cscale + E;
+    const float bound = fmaxf(tprime ? vx_key_score(tprime) : -INFINITY, sd) * cscale + E;
     const uint64_t ek = keys[k - 1];
     if (!(bound < tb) && (ek == 0ull || !(vx_key_score(ek) > bound))) s_fail = 1;
   }
@@ -565,7 +571,8 @@ __global__ void __launch_bounds__(256)
                        const float* __restrict__ xstats, int fmt,
                        const float* __restrict__ qscale, const uint64_t* __restrict__ wkeys,
                        uint64_t* __restrict__ out_keys, int64_t* __restrict__ out_ids,
-                       float* __restrict__ out_scores, int* __restrict__ flags) {
+                       float* __restrict__ out_scores, int* __restrict__ flags,
+                       const uint64_t* __restrict__ seed, int seed_ld) {
   extern __shared__ __align__(16) uint64_t keys[];  // [np2]
   __shared__ float s_red[96];
   __shared__ unsigned long long s_t2;
@@ -602,12 +609,14 @@ __global__ void __launch_bounds__(256)
       }
     if (threadIdx.x == 0) {
       int fail = 0;
-      if (t2 != 0ull) {
+      // documents outside every list: coarse <= max(s(T''), seed) (seeded scan)
+      const float cb = fmaxf(t2 ? vx_key_score(t2) : -INFINITY, seed_thr(seed, seed_ld, b));
+      if (cb > -INFINITY) {
         float qn, qh, qr;
         query_norms_final(s_red, fmt, &qn, &qh, &qr);
         const float E = cert_err_bound(fmt, qn, qh, qr, xstats);
         const uint64_t ek = k <= np2 ? keys[k - 1] : 0ull;
-        fail = (ek == 0ull || !(vx_key_score(ek) > vx_key_score(t2) * cscale + E)) ? 1 : 0;
+        fail = (ek == 0ull || !(vx_key_score(ek) > cb * cscale + E)) ? 1 : 0;
       }
       s_fail = fail;
       flags[b] = fail;
@@ -690,7 +699,8 @@ cudaError_t launch_rerank_wide(const float* docs, const float* fq, int D, const 
                                int P_pairs, int P_single, int kc, int k, int64_t row0,
                                const float* xstats, int fmt, const float* qscale,
                                uint64_t* wkeys, uint64_t* out_keys, int64_t* out_ids,
-                               float* out_scores, int* flags, cudaStream_t st) {
+                               float* out_scores, int* flags, cudaStream_t st,
+                               const uint64_t* seed, int seed_ld) {
   const int M = P_single * kc;
   int np2 = 16;
   while (np2 < M) np2 <<= 1;
@@ -709,7 +719,7 @@ cudaError_t launch_rerank_wide(const float* docs, const float* fq, int D, const 
   if (e != cudaSuccess) return e;
   wide_select_kernel<<<W, 256, smem, st>>>(fq, D, fidx, fcount, part_all, B, GS, P_pairs,
                                            P_single, kc, k, row0, xstats, fmt, qscale, wkeys,
-                                           out_keys, out_ids, out_scores, flags);
+                                           out_keys, out_ids, out_scores, flags, seed, seed_ld);
   return cudaGetLastError();
 }
 
@@ -726,9 +736,16 @@ size_t scan_tc_smem(int QT, int TD, int fmt, int* ns_out) {
 template <int QT, int TD>
 static cudaError_t launch_tc(const CUtensorMap* tq, const CUtensorMap* tx, const ScanTcArgs& a,
                              int grid, size_t smem, cudaStream_t st) {
-  auto kfn = a.fmt == FMT_TF32 ? scan_tc_kernel<QT, TD, FMT_TF32>
-                               : (a.fmt == FMT_I8 ? scan_tc_kernel<QT, TD, FMT_I8>
-                                                  : scan_tc_kernel<QT, TD, FMT_BF16>);
+  // per-CTA list length: kc_of(fmt), or kSampleKC for the seed's sample pass
+  const int kc = a.kc ? a.kc : kc_of(a.fmt);
+  if (kc != kc_of(a.fmt) && kc != kSampleKC) return cudaErrorInvalidValue;
+  auto kfn = kc == kSampleKC
+                 ? (a.fmt == FMT_TF32 ? scan_tc_kernel<QT, TD, FMT_TF32, kSampleKC>
+                                      : (a.fmt == FMT_I8 ? scan_tc_kernel<QT, TD, FMT_I8, kSampleKC>
+                                                         : scan_tc_kernel<QT, TD, FMT_BF16, kSampleKC>))
+                 : (a.fmt == FMT_TF32 ? scan_tc_kernel<QT, TD, FMT_TF32, kc_of(FMT_TF32)>
+                                      : (a.fmt == FMT_I8 ? scan_tc_kernel<QT, TD, FMT_I8, kc_of(FMT_I8)>
+                                                         : scan_tc_kernel<QT, TD, FMT_BF16, kc_of(FMT_BF16)>));
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   kfn<<<grid, TcCfg<QT, TD>::kThreads, smem, st>>>(*tq, *tx, a);
@@ -756,7 +773,7 @@ cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64
                           int64_t row0, const float* xstats, int fmt, const float* qscale,
                           uint64_t* out_keys, int64_t* out_ids, float* out_scores, int* flags,
                           cudaStream_t st, int phase, const float* tau, uint64_t* hkeys,
-                          float* lb) {
+                          float* lb, const uint64_t* seed, int seed_ld) {
   const size_t base = (size_t)((D + 3) & ~3) * 4 + (size_t)kp * 8;
   const size_t row = (size_t)(D + 4) * 4;
   static const int env_rows = [] {  // timing experiments: VX_DEBUG_RERANK_ROWS, read once
@@ -772,7 +789,7 @@ cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64
   if (e != cudaSuccess) return e;
   rerank_kernel<<<B, 256, smem, st>>>(docs, q, D, cand, kp, part, grid, ldlists, kc, k, row0,
                                       xstats, fmt, qscale, out_keys, out_ids, out_scores, flags, R,
-                                      phase, tau, hkeys, lb);
+                                      phase, tau, hkeys, lb, seed, seed_ld);
   return cudaGetLastError();
 }
 

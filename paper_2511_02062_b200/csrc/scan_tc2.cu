@@ -26,6 +26,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#include <type_traits>
+
 #include "vx_internal.cuh"
 #include "vx_ptx.cuh"
 #include "vx_select.cuh"
@@ -57,7 +59,7 @@ static size_t p2_smem(int nb) {
          (size_t)(2 * C::kNA + 2 * nb + 4) * 8 + 16 + 1024;
 }
 
-template <int QG, int FMT>
+template <int QG, int FMT, int KC>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P2Cfg<QG>::kThreads, 1)
     scan_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tx,
                     const ScanTcArgs a) {
@@ -83,7 +85,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P2Cfg<QG>::kThreads,
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   // K-chunk = one 128-byte swizzle atom: 32 fp32 (tf32), 64 bf16, 128 s8
   constexpr int cw = FMT == FMT_TF32 ? 32 : (FMT == FMT_I8 ? 128 : 64);
-  constexpr int KC = kc_of(FMT);  // per-pair list length per query
   const int nch = a.D / cw;
   const uint32_t n_local = a.n_local;
   const int ntiles = (int)((n_local + TD - 1) / TD);
@@ -229,7 +230,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P2Cfg<QG>::kThreads,
     uint64_t L[KC];
 #pragma unroll
     for (int j = 0; j < KC; ++j) L[j] = 0ull;
-    float thr = -INFINITY;
+    // admission threshold: the query's seed, else -inf
+    float thr = q < a.B ? seed_thr(a.seed, a.seed_ld, q) : -INFINITY;
+    if (a.dbg_no_select & 16) thr = 2e9f;  // timing only: the filter's fast path alone
     int buf = 0;
     uint32_t bph = 0;
     for (int tile = pair; tile < ntiles; tile += npairs) {
@@ -284,14 +287,20 @@ size_t scan_tc2_smem(int QG, int* ns_out) {
 cudaError_t launch_scan_tc2(int QG, const CUtensorMap* tq, const CUtensorMap* tx,
                             const ScanTcArgs& a, int grid, size_t smem, cudaStream_t st) {
   if (grid < 2 || (grid & 1) || (QG != 1 && QG != 2)) return cudaErrorInvalidValue;
-  auto pick = [](int qg, int fmt) {
-    if (qg == 2)
-      return fmt == FMT_TF32 ? scan_tc2_kernel<2, FMT_TF32>
-                             : (fmt == FMT_I8 ? scan_tc2_kernel<2, FMT_I8> : scan_tc2_kernel<2, FMT_BF16>);
-    return fmt == FMT_TF32 ? scan_tc2_kernel<1, FMT_TF32>
-                           : (fmt == FMT_I8 ? scan_tc2_kernel<1, FMT_I8> : scan_tc2_kernel<1, FMT_BF16>);
+  // per-pair list length: kc_of(fmt), or kSampleKC for the seed's sample pass
+  const int kc = a.kc ? a.kc : kc_of(a.fmt);
+  if (kc != kc_of(a.fmt) && kc != kSampleKC) return cudaErrorInvalidValue;
+  auto pick = [&](auto qg) {
+    constexpr int Q = decltype(qg)::value;
+    if (kc == kSampleKC)
+      return a.fmt == FMT_TF32 ? scan_tc2_kernel<Q, FMT_TF32, kSampleKC>
+                               : (a.fmt == FMT_I8 ? scan_tc2_kernel<Q, FMT_I8, kSampleKC>
+                                                  : scan_tc2_kernel<Q, FMT_BF16, kSampleKC>);
+    return a.fmt == FMT_TF32 ? scan_tc2_kernel<Q, FMT_TF32, kc_of(FMT_TF32)>
+                             : (a.fmt == FMT_I8 ? scan_tc2_kernel<Q, FMT_I8, kc_of(FMT_I8)>
+                                                : scan_tc2_kernel<Q, FMT_BF16, kc_of(FMT_BF16)>);
   };
-  auto kfn = pick(QG, a.fmt);
+  auto kfn = QG == 2 ? pick(std::integral_constant<int, 2>{}) : pick(std::integral_constant<int, 1>{});
   const int threads = QG == 2 ? P2Cfg<2>::kThreads : P2Cfg<1>::kThreads;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

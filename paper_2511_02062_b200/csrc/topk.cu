@@ -39,7 +39,8 @@ __device__ __forceinline__ void block_bitonic_desc(uint64_t* buf, int n) {
 __global__ void __launch_bounds__(kMergeThreads)
     merge_topk_kernel(const uint64_t* __restrict__ in, int M, int64_t ldin, int k, int64_t id_base,
                       uint64_t* __restrict__ out_keys, int64_t* __restrict__ out_ids,
-                      float* __restrict__ out_scores, const int* __restrict__ d_count) {
+                      float* __restrict__ out_scores, const int* __restrict__ d_count,
+                      int64_t ldout) {
   if (d_count && (int)blockIdx.x >= *d_count) return;  // device-sized batch (cert fallback)
   __shared__ uint32_t hist[256];
   __shared__ uint64_t s_prefix, s_mask;
@@ -143,7 +144,7 @@ __global__ void __launch_bounds__(kMergeThreads)
   block_bitonic_desc(sel, kp);
   for (int i = threadIdx.x; i < k; i += blockDim.x) {
     uint64_t key = sel[i];
-    size_t o = (size_t)blockIdx.x * k + i;
+    size_t o = (size_t)blockIdx.x * ldout + i;
     if (key == 0ull) {
       if (out_keys) out_keys[o] = 0ull;
       if (out_ids) out_ids[o] = -1;
@@ -160,10 +161,12 @@ __global__ void __launch_bounds__(kMergeThreads)
 
 cudaError_t launch_merge_topk(const uint64_t* in, int B, int M, int k, int64_t id_base,
                               uint64_t* out_keys, int64_t* out_ids, float* out_scores,
-                              cudaStream_t st, const int* d_count, int64_t ldin) {
+                              cudaStream_t st, const int* d_count, int64_t ldin,
+                              int64_t ldout) {
   if (k < 1 || k > kMaxK || M < k) return cudaErrorInvalidValue;
   merge_topk_kernel<<<B, kMergeThreads, 0, st>>>(in, M, ldin > 0 ? ldin : M, k, id_base,
-                                                 out_keys, out_ids, out_scores, d_count);
+                                                 out_keys, out_ids, out_scores, d_count,
+                                                 ldout > 0 ? ldout : k);
   return cudaGetLastError();
 }
 

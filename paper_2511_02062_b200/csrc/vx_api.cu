@@ -85,11 +85,11 @@ static PFN_encodeTiled get_encode() {
 // 2-D row-major matrix [rows][cols] of `elem` bytes, box {box_cols, box_rows}, 128B swizzle.
 vx_status make_tmap_2d(CUtensorMap* m, const void* base, CUtensorMapDataType dt,
                               int elem, uint64_t rows, uint64_t cols, uint32_t box_cols,
-                              uint32_t box_rows) {
+                              uint32_t box_rows, uint64_t pitch) {
   PFN_encodeTiled enc = get_encode();
   if (!enc) return fail(VX_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {cols * (uint64_t)elem};
+  cuuint64_t strides[1] = {(pitch ? pitch : cols) * (uint64_t)elem};
   cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t es[2] = {1, 1};
   CUresult r = enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, es,
@@ -139,6 +139,7 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
   };
   if (const char* e = getenv("VX_DEBUG_TC_NOSELECT")) h->dbg_tc_bits = atoi(e);
   if (const char* e = getenv("VX_DEBUG_TC_STAGES")) h->dbg_tc_stages = atoi(e);
+  if (const char* e = getenv("VX_DEBUG_SEED_M")) h->dbg_seed_m = std::min(32, std::max(1, atoi(e)));
   if (cudaSetDevice(h->device) != cudaSuccess) return cleanup(fail(VX_ERR_CUDA, "cudaSetDevice"));
   if (h->n_local < 1) return cleanup(fail(VX_ERR_INVALID, "empty shard"));
 #define ALLOC(ptr, bytes)                                                              \
@@ -174,6 +175,7 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
   }
   ALLOC(h->d_hdr, 16);
   ALLOC(h->d_ckeys, B * 1024 * 8);
+  ALLOC(h->d_seedk, B * 32 * 8);
   ALLOC(h->d_flags, B * 4);
   ALLOC(h->d_xnorm, 32);
   ALLOC(h->d_fq, B * D * 4);
@@ -246,7 +248,7 @@ extern "C" vx_status vx_index_destroy(vx_index* h) {
   for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second.exec);
   void* ptrs[] = {h->docs,  h->tokens,    h->d_q,      h->d_qtok,    h->d_part, h->d_keys,
                   h->d_ids, h->d_ip,      h->d_ms,     h->d_out_ids, h->d_out_ip,
-                  h->d_out_ms, h->d_send, h->d_recv, h->d_hdr, h->d_ckeys, h->d_flags,
+                  h->d_out_ms, h->d_send, h->d_recv, h->d_hdr, h->d_ckeys, h->d_seedk, h->d_flags,
                   h->d_xnorm, h->d_fq, h->docs16, h->d_q16, h->d_fidx, h->d_fcount,
                   h->d_qtok16, h->docs8, h->d_q8, h->d_qs8, h->d_lball, h->d_tau, h->d_hkeys};
   for (void* p : ptrs)
@@ -290,6 +292,10 @@ extern "C" vx_status vx_set_option(vx_index* h, int32_t option, int64_t value) {
       if (value != 0 && (value < 16 || value > 1024 || (value & (value - 1))))
         return fail(VX_ERR_INVALID, "kprime %lld (0 or a power of two in [16, 1024])", (long long)value);
       h->kprime = (int)value;
+      return VX_OK;
+    case VX_OPT_SCAN_SEED:
+      if (value != 0 && value != 1) return fail(VX_ERR_INVALID, "scan seed %lld", (long long)value);
+      h->scan_seed = (int)value;
       return VX_OK;
     case VX_OPT_SCAN_PAIRS:
       if (value < 0 || value > 2) return fail(VX_ERR_INVALID, "pairs %lld", (long long)value);
@@ -337,6 +343,7 @@ extern "C" vx_status vx_get_option(const vx_index* h, int32_t option, int64_t* v
     case VX_OPT_SCAN_TILE: *value = h->scan_tile; return VX_OK;
     case VX_OPT_SCAN_PAIRS: *value = h->use_pairs; return VX_OK;
     case VX_OPT_KPRIME: *value = h->kprime; return VX_OK;
+    case VX_OPT_SCAN_SEED: *value = h->scan_seed; return VX_OK;
     case VX_OPT_COARSE: {
       const int f = coarse_fmt(h);
       *value = f == vx::FMT_I8 ? VX_COARSE_I8 : (f == vx::FMT_TF32 ? VX_COARSE_TF32 : VX_COARSE_BF16);

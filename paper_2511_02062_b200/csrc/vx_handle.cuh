@@ -64,7 +64,8 @@ vx_status fail(vx_status s, const char* fmt, ...);
 
 // 2-D row-major matrix [rows][cols] of `elem` bytes, box {box_cols, box_rows}, 128B swizzle.
 vx_status make_tmap_2d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int elem,
-                       uint64_t rows, uint64_t cols, uint32_t box_cols, uint32_t box_rows);
+                       uint64_t rows, uint64_t cols, uint32_t box_cols, uint32_t box_rows,
+                       uint64_t pitch = 0);  // row pitch in elements (0: cols)
 
 // ---------------------------------------------------------------- handle
 
@@ -92,7 +93,9 @@ struct vx_index {
   int scan_tile = 0;             // documents per tensor-core tile (0 = auto)
   int kprime = 0;                // TC candidate set size k' (0 = auto; VX_OPT_KPRIME)
   int dbg_tc_bits = 0;           // timing-experiment knobs, read once from the environment at
-  int dbg_tc_stages = 0;         //   create: VX_DEBUG_TC_NOSELECT (bit mask), VX_DEBUG_TC_STAGES
+  int dbg_tc_stages = 0;         //   create: VX_DEBUG_TC_NOSELECT (bit mask), VX_DEBUG_TC_STAGES,
+  int dbg_seed_m = 0;            //   VX_DEBUG_SEED_M (sample rank of the scan seed, <= 32)
+  int scan_seed = 1;             // seed the TC scan's admission thresholds (VX_OPT_SCAN_SEED)
   int use_pairs = 2;             // CTA-pair scan for B > 128: 0 off, 1 on (256-query passes),
                                  // 2 on + 512-query passes for B > 256 (VX_OPT_SCAN_PAIRS)
   // options
@@ -117,7 +120,8 @@ struct vx_index {
   float* d_tau = nullptr;        // [maxB] lower bound of the global exact k-th (G > 1)
   uint64_t* d_hkeys = nullptr;   // [maxB][maxK] exact keys of the re-rank head (G > 1)
   int32_t* d_hdr = nullptr;      // [4]
-  uint64_t* d_ckeys = nullptr;   // [maxB][512] merged coarse keys (TC path)
+  uint64_t* d_ckeys = nullptr;   // [maxB][1024] merged coarse keys (TC path)
+  uint64_t* d_seedk = nullptr;   // [maxB][32] best sample keys per query (TC scan seeds)
   int* d_flags = nullptr;        // [maxB] certificate failures (TC path)
   unsigned int* d_xnorm = nullptr;  // [8] shard maxima (float bits, row_stats): |x|, |bf16 x|,
                                     // |x-bf16 x|, |sx x8|, |x-sx x8|; [5] sx; [6] scratch;

@@ -41,8 +41,21 @@ struct ScanTcArgs {
   int32_t fmt;       // operand format: FMT_BF16 (kind::f16 on the bf16 shadow), FMT_TF32 (fp32
                      // rows read as TF32, kind::tf32) or FMT_I8 (s8 shadow, kind::i8, s32)
   int32_t dbg_no_select;  // timing experiments only (VX_DEBUG_TC_NOSELECT): skip the top-k
-  uint64_t* part;    // [B][gridDim.x][16] coarse keys
+  uint64_t* part;    // [B][gridDim.x][KC] coarse keys
+  // admission-threshold seeds (nullable): query q starts admitting at the coarse score of
+  // key seed[q * seed_ld] (0 = no seed) instead of -inf — the m-th best coarse key of a
+  // strided sample of the shard (vx_stage.cu local_topk_tc), so the lists skip the fill
+  // phase; the re-rank's certificate bounds the documents the seed dropped
+  const uint64_t* seed;
+  int32_t seed_ld;
+  int32_t kc;        // list length per CTA (pair) and query: 0 = kc_of(fmt), or kSampleKC
 };
+// admission threshold a seed key stands for (-inf: none)
+__device__ __forceinline__ float seed_thr(const uint64_t* seed, int ld, int q) {
+  if (!seed) return -INFINITY;
+  const uint64_t key = seed[(size_t)q * ld];
+  return key ? vx_key_score(key) : -INFINITY;
+}
 // TF32 coarse-score error bound coefficient E = coef * ||q|| * max||x||: the tensor core
 // truncates both operands to 10 mantissa bits (<= 2^-10 each).  The bf16 bound is computed
 // from the actual rounding residuals (rerank_kernel in scan_tc.cu).
@@ -59,6 +72,9 @@ enum : int { FMT_BF16 = 1, FMT_TF32 = 2, FMT_I8 = 3 };
 // Per-CTA (per-pair) candidate list length per query: 16, or 32 for the s8 coarse pass,
 // whose candidate set k' is 4x larger (its error bound is ~4x the bf16 one).
 __host__ __device__ constexpr int kc_of(int fmt) { return fmt == FMT_I8 ? 32 : 16; }
+// list length of the seed's sample pass (vx_stage.cu): the seed is the m-th best of the
+// union of the lists, and truncated lists only lower it (a valid, slightly looser seed)
+constexpr int kSampleKC = 4;
 // s8 quantisation used by the shadow, the queries and the certificate's residuals
 __device__ __forceinline__ int8_t vx_quant8(float v, float s) {
   const float r = rintf(v / s);
@@ -81,7 +97,8 @@ cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64
                           int64_t row0, const float* xstats, int fmt, const float* qscale,
                           uint64_t* out_keys, int64_t* out_ids, float* out_scores, int* flags,
                           cudaStream_t st, int phase = 0, const float* tau = nullptr,
-                          uint64_t* hkeys = nullptr, float* lb = nullptr);
+                          uint64_t* hkeys = nullptr, float* lb = nullptr,
+                          const uint64_t* seed = nullptr, int seed_ld = 0);
 // tau[B] = k-th largest of all[G][B][k] (G k <= 1024)
 cudaError_t launch_shard_tau(const float* all, int G, int B, int k, float* tau, cudaStream_t st);
 // second certificate level over the full per-CTA lists (compacted failing queries): two
@@ -91,7 +108,8 @@ cudaError_t launch_rerank_wide(const float* docs, const float* fq, int D, const 
                                int P_pairs, int P_single, int kc, int k, int64_t row0,
                                const float* xstats, int fmt, const float* qscale,
                                uint64_t* wkeys, uint64_t* out_keys, int64_t* out_ids,
-                               float* out_scores, int* flags, cudaStream_t st);
+                               float* out_scores, int* flags, cudaStream_t st,
+                               const uint64_t* seed = nullptr, int seed_ld = 0);
 // per-shard maxima [max|x|, max|bf16(x)|, max|x - bf16(x)|] (3 floats as uint bits) and, when
 // i8_scale is given, [3] max|sx x8|, [4] max|x - sx x8| of the s8 shadow
 cudaError_t launch_row_stats(const float* docs, int64_t n, int D, unsigned int* out_bits,
@@ -103,7 +121,8 @@ cudaError_t launch_row_stats(const float* docs, int64_t n, int D, unsigned int* 
 // ldin: keys between consecutive queries' candidate lists (0: M, i.e. contiguous)
 cudaError_t launch_merge_topk(const uint64_t* in, int B, int M, int k, int64_t id_base,
                               uint64_t* out_keys, int64_t* out_ids, float* out_scores,
-                              cudaStream_t st, const int* d_count = nullptr, int64_t ldin = 0);
+                              cudaStream_t st, const int* d_count = nullptr, int64_t ldin = 0,
+                              int64_t ldout = 0);
 // Certificate failures (flags[B]) -> compacted list fidx/fcount and the flagged query rows
 // gathered into fq; after the exact re-scan, scatter its [fcount][k] results back.
 cudaError_t launch_cert_compact(const int* flags, int B, const float* q, int D, int* fidx,

@@ -103,7 +103,8 @@ VX_DEV void admit(const uint32_t* r, uint32_t doc0, uint32_t n_local, uint32_t* 
     list_insert<KC>(L, key);
     ins = true;
   }
-  if (ins) thr = L[KC - 1] == 0ull ? -INFINITY : vx_key_score(L[KC - 1]);
+  // a list that is not full keeps its threshold (-inf, or the query's seed)
+  if (ins && L[KC - 1] != 0ull) thr = vx_key_score(L[KC - 1]);
 }
 
 }  // namespace vx

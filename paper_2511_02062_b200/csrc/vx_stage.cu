@@ -138,76 +138,135 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
   // 256-document tiles); 0: the single-CTA kernels (QT = 2 x 128)
   const bool pairs = h->use_pairs && grid % 2 == 0;
   const int GS = (pairs && h->use_pairs == 2) ? 512 : 256;
-  for (int g0 = 0; g0 < B; g0 += GS) {
-    const int Bg = std::min(GS, B - g0);
-    const bool on_pairs = pairs && Bg > 128;
-    const int QT = Bg <= 128 ? 1 : 2;
-    const int a_rows = on_pairs ? 128 : (QT == 1 ? ((Bg + 7) & ~7) : 128);
-    CUtensorMap tq;
-    if (bf16)
-      VX_TRY(make_tmap_2d(&tq, h->d_q16 + (size_t)g0 * D, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
-                          (uint64_t)Bg, D, 64, (uint32_t)a_rows));
-    else if (i8)
-      VX_TRY(make_tmap_2d(&tq, h->d_q8 + (size_t)g0 * D, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1,
-                          (uint64_t)Bg, D, 128, (uint32_t)a_rows));
-    else
-      VX_TRY(make_tmap_2d(&tq, d_q + (size_t)g0 * D, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
-                          (uint64_t)Bg, D, 32, (uint32_t)a_rows));
-    vx::ScanTcArgs a;
-    a.n_local = (uint32_t)h->n_local;
-    a.D = D;
-    a.B = Bg;
-    a.a_rows = a_rows;
-    a.fmt = fmt;
-    a.dbg_no_select = h->dbg_tc_bits;  // timing experiments only (VX_DEBUG_TC_NOSELECT)
-    a.part = h->d_part + (size_t)g0 * grid * KC;
-    const CUtensorMap* tx = i8 ? &h->tmap_docs8 : (bf16 ? &h->tmap_docs16 : &h->tmap_docs);
-    if (on_pairs) {
-      // 128 < B: CTA pairs (cta_group::2), 256 documents x 256 QG queries per pair tile
-      const int QG = Bg > 256 ? 2 : 1;
-      int ns2 = 0;
-      const size_t smem2 = vx::scan_tc2_smem(QG, &ns2);
-      a.ns = ns2;
-      if (QG == 2)  // 128-document tiles: 64-row document boxes per CTA
-        tx = i8 ? &h->tmap_docs8_h : (bf16 ? &h->tmap_docs16_h : &h->tmap_docs_h);
-      CU_TRY(vx::launch_scan_tc2(QG, &tq, tx, a, grid, smem2, st));
-    } else {
-      // 256-document tiles halve the per-document query re-streaming from L2 (measured: B=128
-      // bf16 2.31 ms vs 3.78 ms with 128; B=256 3.9 ms vs 4.36 ms) — profiles/r01/
-      const int TD = h->scan_tile ? h->scan_tile : 256;
-      int ns = 0;
-      size_t smem = vx::scan_tc_smem(QT, TD, fmt, &ns);
-      if (h->dbg_tc_stages) {  // timing experiments only (VX_DEBUG_TC_STAGES)
-        const int want = h->dbg_tc_stages;
-        if (want >= 2 && want < ns) {
-          smem -= (size_t)(ns - want) * (QT * 16384 + TD * 128 + 16);
-          ns = want;
-        }
-      }
-      a.ns = ns;
-      CU_TRY(vx::launch_scan_tc(QT, TD, &tq, tx, a, grid, smem, st));
-    }
-    count_launch(h);
-  }
-  CU_TRY(record_ev(h, h->tev[1], st));
-  // merge each query's lists (P per query, stride grid lists) to the coarse top-k', exact
-  // re-rank — one launch each per run of query groups with the same P (the whole batch
-  // when every group ran on CTA pairs), so the 2-per-SM re-rank CTAs pack full waves
   const int ldp = grid * KC;
   auto lists_per_query = [&](int r) {
     return (pairs && std::min(GS, B - r) > 128) ? grid / 2 : grid;
   };
-  for (int r0 = 0; r0 < B;) {
-    const int P = lists_per_query(r0);
-    int r1 = r0;
-    while (r1 < B && lists_per_query(r1) == P) r1 += GS;
-    r1 = std::min(r1, B);
-    CU_TRY(vx::launch_merge_topk(h->d_part + (size_t)r0 * ldp, r1 - r0, P * KC, kp, 0,
-                                 h->d_ckeys + (size_t)r0 * kp, nullptr, nullptr, st, nullptr,
-                                 ldp));
-    count_launch(h);
-    r0 = r1;
+  // Admission-threshold seeds.  A query's empty list admits every document of the first
+  // tiles and ~KC ln(n/KC) in all, and with 32 queries per epilogue warp any passing lane
+  // sends the warp down the insertion path: a selection cost that does not shrink with the
+  // shard (512-query s8 passes, threshold pinned above every score vs the real selection:
+  // 10M rows 2.45 vs 2.92 ms, 2.5M 0.59 vs 0.92, 1.25M 0.28 vs 0.57 —
+  // profiles/r01/decomp_seed.jsonl).  So the same kernel first scans a strided
+  // 1/kSeedStride row sample of the shard (its tensor map skips rows) with kSampleKC-key
+  // lists (short lists keep the sample's own fill cheap: 34 us vs 124 us with 32-key lists
+  // at 2.5M rows), the lists merge to each query's kSeedM best keys, and the full pass starts
+  // admitting at the kSeedM-th: expected shard rank kSeedM x kSeedStride = 2048 >= k' for
+  // every k <= 128; it lands above the k'-th coarse score with probability
+  // P(Poisson(k'/64) >= 32) ~ 1e-4 at k' = 1024 (measured: m = 16 sent 1-9 % of the queries
+  // to the exact re-scan, m = 32 none — profiles/r01/seed_m.jsonl).  Documents below the
+  // seed never enter a list; the re-rank certificate bounds them by the seed (rerank_kernel,
+  // wide_select_kernel), so results are unchanged.  10M x 768 s8 B = 1024: scan 5.95 ->
+  // 5.24 ms; one shard of 4 / 8: 1.89 -> 1.49, 1.18 -> 0.84 ms (seed_stage2.jsonl).
+  constexpr int kSeedStride = 64, kSeedLd = 32;
+  const int kSeedM = h->dbg_seed_m ? h->dbg_seed_m : 32;
+  const int64_t n_sample = h->n_local / kSeedStride;
+  const bool seeded = h->scan_seed && n_sample >= 8192;
+  // the sample's lists: the upper part of d_part (the level-2 scratch, free until then)
+  uint64_t* sample_lists = h->d_part + (size_t)h->desc.max_batch * grid * 32;
+  auto scan_pass = [&](bool sample) -> vx_status {
+    for (int g0 = 0; g0 < B; g0 += GS) {
+      const int Bg = std::min(GS, B - g0);
+      const bool on_pairs = pairs && Bg > 128;
+      const int QT = Bg <= 128 ? 1 : 2;
+      const int QG = on_pairs && Bg > 256 ? 2 : 1;
+      const int a_rows = on_pairs ? 128 : (QT == 1 ? ((Bg + 7) & ~7) : 128);
+      CUtensorMap tq;
+      if (bf16)
+        VX_TRY(make_tmap_2d(&tq, h->d_q16 + (size_t)g0 * D, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                            (uint64_t)Bg, D, 64, (uint32_t)a_rows));
+      else if (i8)
+        VX_TRY(make_tmap_2d(&tq, h->d_q8 + (size_t)g0 * D, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1,
+                            (uint64_t)Bg, D, 128, (uint32_t)a_rows));
+      else
+        VX_TRY(make_tmap_2d(&tq, d_q + (size_t)g0 * D, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                            (uint64_t)Bg, D, 32, (uint32_t)a_rows));
+      vx::ScanTcArgs a;
+      a.n_local = (uint32_t)(sample ? n_sample : h->n_local);
+      a.D = D;
+      a.B = Bg;
+      a.a_rows = a_rows;
+      a.fmt = fmt;
+      a.dbg_no_select = h->dbg_tc_bits;  // timing experiments only (VX_DEBUG_TC_NOSELECT)
+      a.kc = sample ? vx::kSampleKC : 0;
+      a.part = sample ? sample_lists + (size_t)g0 * grid * vx::kSampleKC : h->d_part + (size_t)g0 * ldp;
+      a.seed = (seeded && !sample) ? h->d_seedk + (size_t)g0 * kSeedLd + (kSeedM - 1) : nullptr;
+      a.seed_ld = kSeedLd;
+      // 128-document pair tiles (QG = 2) load 64-row document boxes per CTA
+      const CUtensorMap* tx;
+      if (QG == 2)
+        tx = i8 ? &h->tmap_docs8_h : (bf16 ? &h->tmap_docs16_h : &h->tmap_docs_h);
+      else
+        tx = i8 ? &h->tmap_docs8 : (bf16 ? &h->tmap_docs16 : &h->tmap_docs);
+      CUtensorMap txs;  // the sample: every kSeedStride-th row, same boxes
+      if (sample) {
+        const uint32_t rows = QG == 2 ? 64 : 128;
+        if (i8)
+          VX_TRY(make_tmap_2d(&txs, h->docs8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1,
+                              (uint64_t)n_sample, D, 128, rows, (uint64_t)kSeedStride * D));
+        else if (bf16)
+          VX_TRY(make_tmap_2d(&txs, h->docs16, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                              (uint64_t)n_sample, D, 64, rows, (uint64_t)kSeedStride * D));
+        else
+          VX_TRY(make_tmap_2d(&txs, h->docs, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                              (uint64_t)n_sample, D, 32, rows, (uint64_t)kSeedStride * D));
+        tx = &txs;
+      }
+      if (on_pairs) {
+        // 128 < B: CTA pairs (cta_group::2), 256 documents x 256 QG queries per pair tile
+        int ns2 = 0;
+        const size_t smem2 = vx::scan_tc2_smem(QG, &ns2);
+        a.ns = ns2;
+        CU_TRY(vx::launch_scan_tc2(QG, &tq, tx, a, grid, smem2, st));
+      } else {
+        // 256-document tiles halve the per-document query re-streaming from L2 (measured:
+        // B=128 bf16 2.31 ms vs 3.78 ms with 128; B=256 3.9 ms vs 4.36 ms) — profiles/r01/
+        const int TD = h->scan_tile ? h->scan_tile : 256;
+        int ns = 0;
+        size_t smem = vx::scan_tc_smem(QT, TD, fmt, &ns);
+        if (h->dbg_tc_stages) {  // timing experiments only (VX_DEBUG_TC_STAGES)
+          const int want = h->dbg_tc_stages;
+          if (want >= 2 && want < ns) {
+            smem -= (size_t)(ns - want) * (QT * 16384 + TD * 128 + 16);
+            ns = want;
+          }
+        }
+        a.ns = ns;
+        CU_TRY(vx::launch_scan_tc(QT, TD, &tq, tx, a, grid, smem, st));
+      }
+      count_launch(h);
+    }
+    return VX_OK;
+  };
+  // merge each query's P lists (stride grid lists) to its best kout keys — one launch per
+  // run of query groups with the same P (the whole batch when every group ran on CTA pairs)
+  auto merge_lists = [&](const uint64_t* lists, int kc, int kout, uint64_t* out,
+                         int ldout) -> vx_status {
+    const int64_t ld = (int64_t)grid * kc;
+    for (int r0 = 0; r0 < B;) {
+      const int P = lists_per_query(r0);
+      int r1 = r0;
+      while (r1 < B && lists_per_query(r1) == P) r1 += GS;
+      r1 = std::min(r1, B);
+      CU_TRY(vx::launch_merge_topk(lists + (size_t)r0 * ld, r1 - r0, P * kc, kout, 0,
+                                   out + (size_t)r0 * ldout, nullptr, nullptr, st, nullptr, ld,
+                                   ldout));
+      count_launch(h);
+      r0 = r1;
+    }
+    return VX_OK;
+  };
+  if (seeded) {
+    VX_TRY(scan_pass(true));
+    VX_TRY(merge_lists(sample_lists, vx::kSampleKC, kSeedM, h->d_seedk, kSeedLd));
   }
+  VX_TRY(scan_pass(false));
+  // each query's seed key (the certificate bounds what it dropped), stride kSeedLd
+  const uint64_t* seed_keys = seeded ? h->d_seedk + (kSeedM - 1) : nullptr;
+  CU_TRY(record_ev(h, h->tev[1], st));
+  // merge each query's lists to the coarse top-k', exact re-rank (per run of query groups
+  // with the same P, so the 2-per-SM re-rank CTAs pack full waves)
+  VX_TRY(merge_lists(h->d_part, KC, kp, h->d_ckeys, kp));
   // exact re-rank.  Sharded: phase 1 re-scores each query's k best coarse candidates, the
   // shards all-gather those exact scores (shard_tau: tau <= the global exact k-th), phase 2
   // re-ranks only the candidates that can still reach the GLOBAL top-k
@@ -227,7 +286,8 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
                                ids + (size_t)r0 * k, scores + (size_t)r0 * k, h->d_flags + r0,
                                st, pass, pass == 2 ? h->d_tau + r0 : nullptr,
                                sharded ? h->d_hkeys + (size_t)r0 * k : nullptr,
-                               lb + (size_t)r0 * k));
+                               lb + (size_t)r0 * k,
+                               seed_keys ? seed_keys + (size_t)r0 * kSeedLd : nullptr, kSeedLd));
       count_launch(h);
       r0 = r1;
     }
@@ -248,7 +308,8 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
   CU_TRY(vx::launch_rerank_wide(h->docs, h->d_fq, D, h->d_fidx, cnt2, h->d_part, B, GS,
                                 pairs ? grid / 2 : 0, grid, KC, k, h->row0,
                                 reinterpret_cast<const float*>(h->d_xnorm), fmt,
-                                i8 ? h->d_qs8 : nullptr, wkeys, keys, ids, scores, h->d_flags, st));
+                                i8 ? h->d_qs8 : nullptr, wkeys, keys, ids, scores, h->d_flags, st,
+                                seed_keys, kSeedLd));
   count_launch(h, 2);
   CU_TRY(vx::launch_cert_compact(h->d_flags, B, d_q, D, h->d_fidx, cnt3, h->d_fq, st));
   count_launch(h);

@@ -7,6 +7,7 @@ usage: python profiles/stage_kernels.py [coarse=bf16|i8|tf32] [B] [reps] [G]
 G > 1: shard 0 of G on this one GPU (the per-shard share of a G-GPU stage; search only —
 the MaxSim owner step needs the other ranks)."""
 import json
+import os
 import statistics
 import sys
 from pathlib import Path
@@ -32,6 +33,7 @@ else:
     idx.synth(42)
     idx.tokens_synth(45)
 idx.set_option(vx.VX_OPT_COARSE, CO)
+idx.set_option(vx.VX_OPT_SCAN_SEED, int(os.environ.get("VX_SCAN_SEED", "1")))
 dev = torch.device("cuda", 0)
 st = torch.cuda.Stream(dev)
 torch.cuda.set_stream(st)
@@ -53,7 +55,7 @@ for rep in range(reps):
     idx.sync()
     lat.append(a.elapsed_time(b))
 s = idx.stats()
-print(json.dumps({"coarse": idx.coarse_auto(), "B": B, "stage_ms": round(statistics.median(lat[1:]), 4),
+print(json.dumps({"coarse": idx.coarse_auto(), "seed": idx.get_option(vx.VX_OPT_SCAN_SEED), "B": B, "stage_ms": round(statistics.median(lat[1:]), 4),
                   "scan_ms": round(s["last_scan_ms"], 4), "level2": s["cert_level2"],
                   "rescans": s["cert_fallbacks"], "launches": s["kernel_launches"]}), flush=True)
 idx.close()

@@ -118,3 +118,48 @@ def test_coarse_exact_on_clustered_near_duplicates(vx, oracle, coarse, spread):
     assert np.array_equal(sc, rsc.astype(np.float32))
     if spread < 0.01:  # the tight case must have exercised the fallbacks
         assert st["cert_level2"] + st["cert_fallbacks"] > 0
+
+
+@pytest.mark.parametrize("coarse", ["i8", "bf16"])
+@pytest.mark.parametrize("B", [48, 300])
+def test_seeded_scan_exact_and_equal_to_unseeded(vx, oracle, coarse, B):
+    # shards of >= 512K rows seed each query's admission threshold from a 1/64 row sample
+    # (VX_OPT_SCAN_SEED, vx_stage.cu local_topk_tc); the lists then skip every document below
+    # the seed and the certificate bounds them by it — ids and scores must not move.
+    # B = 300: the CTA-pair kernel with two query groups; 48: the single-CTA kernel
+    N, D, k = 700_000, 256, 100
+    X = oracle.synth_rows(42, 0, N, D)
+    Q = oracle.synth_rows(43, 0, B, D)
+    rid, rsc = oracle.flat_topk(X, Q, k, mode=1)
+    out = {}
+    with vx.Index(N, D, max_batch=B, max_k=k) as idx:
+        idx.upload(X, 0)
+        idx.set_option(vx.VX_OPT_SCAN, vx.VX_SCAN_TC)
+        idx.set_option(vx.VX_OPT_COARSE, {"i8": vx.VX_COARSE_I8, "bf16": vx.VX_COARSE_BF16}[coarse])
+        assert idx.get_option(vx.VX_OPT_SCAN_SEED) == 1
+        for seed in (1, 0):
+            idx.set_option(vx.VX_OPT_SCAN_SEED, seed)
+            out[seed] = idx.search(Q, k)
+            assert idx.stats()["cert_fallbacks"] == 0
+    for seed in (1, 0):
+        assert np.array_equal(out[seed][0], rid)
+        assert np.array_equal(out[seed][1], rsc.astype(np.float32))
+
+
+@pytest.mark.parametrize("coarse", ["i8", "bf16"])
+def test_seeded_scan_exact_when_the_sample_is_unrepresentative(vx, oracle, coarse):
+    # every sampled row (row % 64 == 0) is scaled up 4x: the seed lands far above the k'-th
+    # coarse score of the other rows, the lists miss documents that belong in the top-k, and
+    # only the certificate's seed bound notices — the fallbacks must restore the exact answer
+    N, D, B, k = 700_000, 256, 40, 50
+    X = oracle.synth_rows(42, 0, N, D)
+    X[::64] *= 4.0
+    Q = oracle.synth_rows(43, 0, B, D)
+    with vx.Index(N, D, max_batch=B, max_k=k) as idx:
+        idx.upload(X, 0)
+        idx.set_option(vx.VX_OPT_SCAN, vx.VX_SCAN_TC)
+        idx.set_option(vx.VX_OPT_COARSE, {"i8": vx.VX_COARSE_I8, "bf16": vx.VX_COARSE_BF16}[coarse])
+        ids, sc = idx.search(Q, k)
+    rid, rsc = oracle.flat_topk(X, Q, k, mode=1)
+    assert np.array_equal(ids, rid)
+    assert np.array_equal(sc, rsc.astype(np.float32))
