@@ -312,16 +312,16 @@ __global__ void __launch_bounds__(256)
                   const float* __restrict__ xstats, int fmt, const float* __restrict__ qscale,
                   uint64_t* __restrict__ out_keys, int64_t* __restrict__ out_ids,
                   float* __restrict__ out_scores, int* __restrict__ flags, int rows_per_round,
-                  int phase, const float* __restrict__ tau, uint64_t* __restrict__ hkeys,
+                  int dchunk, int phase, const float* __restrict__ tau, uint64_t* __restrict__ hkeys,
                   float* __restrict__ lb, const uint64_t* __restrict__ seed, int seed_ld) {
   extern __shared__ __align__(16) float rsm[];
   float* qs = rsm;                                             // [D]
   uint64_t* keys = reinterpret_cast<uint64_t*>(rsm + ((D + 3) & ~3));  // [kp]
-  float* rowbuf = reinterpret_cast<float*>(keys + kp);         // [R][D+4] staged rows
+  float* rowbuf = reinterpret_cast<float*>(keys + kp);         // [2][R][DC+4] row chunks
   __shared__ float s_red[96];
   __shared__ float s_min[8];
   __shared__ int s_fail;
-  __shared__ __align__(8) uint64_t s_bar;
+  __shared__ __align__(8) uint64_t s_bar[2];
   const int b = blockIdx.x;
   const float* q = qv + (size_t)b * D;
   // coarse keys are in the coarse pass's units: the s8 pass scores sq * sx * (s32 dot)
@@ -330,7 +330,8 @@ __global__ void __launch_bounds__(256)
   query_norms(q, D, fmt, sq, qs, s_red);  // the certificate's error bound, below
   if (threadIdx.x == 0) {
     s_fail = 0;
-    mbar_init(&s_bar, (uint32_t)rows_per_round);
+    mbar_init(&s_bar[0], (uint32_t)rows_per_round);
+    mbar_init(&s_bar[1], (uint32_t)rows_per_round);
     fence_barrier_init();
   }
   __syncthreads();
@@ -345,39 +346,58 @@ __global__ void __launch_bounds__(256)
   // R rows into smem with one TMA bulk copy per row (R x 3 KB in flight per SM), then R
   // threads run the in-order fmaf chains from smem (row stride D+4 floats: the LDS.128 of
   // 8 consecutive lanes hit distinct banks).
-  const int R = rows_per_round, RS = D + 4;
-  int round = 0;
+  // Rows are staged in DC-float chunks, double-buffered: chunk c+1 of the R rows of a round
+  // is in flight while R threads run the in-order chains over chunk c (the accumulators
+  // carry across chunks, so the fmaf order is the oracle's).  Chunks instead of whole rows
+  // keep R chains going per CTA in the same smem — the chains, not the gathers, set the
+  // pace (whole rows, 32 per round: 7 of 8 warps parked at the barrier 64 % of the time).
+  const int R = rows_per_round, DC = dchunk, RS = DC + 4, nch = D / DC;
+  int chunk_no = 0;  // chunks issued so far (both calls); chunk i uses buffer / barrier i & 1
   auto rescore = [&](int j0, int j1) {  // exact keys of candidates [j0, j1) into keys[]
-    for (int r0 = j0; r0 < j1; r0 += R, ++round) {
+    for (int r0 = j0; r0 < j1; r0 += R) {
       const int t = threadIdx.x;
       const int idx = r0 + t;
-      uint64_t ck = 0ull;
-      if (t < R) {
-        ck = idx < j1 ? cb[idx] : 0ull;
-        const uint32_t bytes = ck ? (uint32_t)D * 4u : 0u;
-        mbar_expect_tx(&s_bar, bytes);  // every staging thread arrives once (count R)
-        if (ck)
-          bulk_load(rowbuf + (size_t)t * RS, docs + (size_t)vx_key_id(ck) * D, bytes, &s_bar);
-      }
-      mbar_wait(&s_bar, (uint32_t)(round & 1));
-      if (t < R && idx < j1) {
-        uint64_t ek = 0ull;
-        if (ck) {
-          const float4* x = reinterpret_cast<const float4*>(rowbuf + (size_t)t * RS);
-          float acc = 0.0f;
-          for (int c = 0; c < (D >> 2); ++c) {
-            const float4 xv = x[c];
-            acc = fmaf(xv.x, qs[4 * c + 0], acc);
-            acc = fmaf(xv.y, qs[4 * c + 1], acc);
-            acc = fmaf(xv.z, qs[4 * c + 2], acc);
-            acc = fmaf(xv.w, qs[4 * c + 3], acc);
-          }
-          ek = vx_make_key(acc, vx_key_id(ck));
+      const uint64_t ck = (t < R && idx < j1) ? cb[idx] : 0ull;
+      const float* xrow = docs + (size_t)(ck ? vx_key_id(ck) : 0u) * D;
+      auto issue = [&](int c, int no) {  // chunk c of this round's rows -> buffer no & 1
+        if (t < R) {
+          const uint32_t bytes = ck ? (uint32_t)DC * 4u : 0u;
+          uint64_t* bar = &s_bar[no & 1];
+          mbar_expect_tx(bar, bytes);  // every staging thread arrives once (count R)
+          if (ck) bulk_load(rowbuf + ((size_t)(no & 1) * R + t) * RS, xrow + (size_t)c * DC, bytes, bar);
         }
-        keys[idx] = ek;
+      };
+      issue(0, chunk_no);
+      float acc = 0.0f;
+      for (int c = 0; c < nch; ++c, ++chunk_no) {
+        // the other buffer was released by the previous chunk's __syncthreads
+        if (c + 1 < nch) issue(c + 1, chunk_no + 1);
+        mbar_wait(&s_bar[chunk_no & 1], (uint32_t)((chunk_no >> 1) & 1));
+        if (ck) {
+          const float4* x =
+              reinterpret_cast<const float4*>(rowbuf + ((size_t)(chunk_no & 1) * R + t) * RS);
+          const float4* q4 = reinterpret_cast<const float4*>(qs + (size_t)c * DC);
+          for (int u0 = 0; u0 < (DC >> 2); u0 += 8) {  // 8 float4s loaded ahead of 32 fmafs
+            float4 xv[8], qv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              xv[u] = x[u0 + u];
+              qv[u] = q4[u0 + u];
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              acc = fmaf(xv[u].x, qv[u].x, acc);
+              acc = fmaf(xv[u].y, qv[u].y, acc);
+              acc = fmaf(xv[u].z, qv[u].z, acc);
+              acc = fmaf(xv[u].w, qv[u].w, acc);
+            }
+          }
+        }
+        __syncthreads();  // this buffer is refilled two chunks later
       }
-      __syncthreads();  // the buffer is reused by the next round's bulk copies
+      if (t < R && idx < j1) keys[idx] = ck ? vx_make_key(acc, vx_key_id(ck)) : 0ull;
     }
+    __syncthreads();  // keys[] complete
   };
   if (phase == 2) {
     for (int i = threadIdx.x; i < kh; i += blockDim.x) keys[i] = hkeys[(size_t)b * k + i];
@@ -761,13 +781,13 @@ cudaError_t launch_scan_tc(int QT, int TD, const CUtensorMap* tq, const CUtensor
   return cudaErrorInvalidValue;
 }
 
-// rows per staging round: 16 rows (~54 KB of smem) lets four CTAs share an SM, so the
-// CTAs' row gathers overlap each other's fmaf chains.  Measured at B = 1024, k' = 256
-// (one launch): R = 8/10/12/14/16/21/24/32: - / 255 / 222 / 201 / 179 / 221 / 251 / 208 us
-// (R = 64, one CTA per SM: 4 x 67 us).  With the s8 pass's k' = 1024 (~600 rows fetched
-// per query) 32 rows per round do better: stage 7.65 vs 7.83 ms at B = 1024 (R = 8 / 16 /
-// 24 / 32 / 48 / 64: 7.92 / 7.83 / 7.75 / 7.65 / 7.79 / 7.65 ms).
-static int rerank_rows(int kp) { return kp >= 512 ? 32 : 16; }
+// Staging: R rows per round in DC-float chunks (the largest multiple of 32 <= 192 dividing
+// D), two chunk buffers.  Whole rows before (R = 16 / 32 rows per round, 2-4 CTAs per SM):
+// s8 k' = 1024 at B = 1024 took 635 us at 3.6 TB/s with the CTAs' single computing warp the
+// critical path (profiles/r01/README.md).  Now (ncu, same 1.96 GHz clock, B = 1024 s8
+// k' = 1024, profiles/r01/rerank_chunks.txt): R = 64 / DC = 192 (two CTAs per SM) 519-539 us
+// at 4.4 TB/s, R = 128 533-558, R = 256 / DC = 96 563-585, R = 192 / DC = 64 740-760.
+// VX_DEBUG_RERANK_ROWS / _DC: timing experiments.
 cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64_t* cand, int B,
                           int kp, const uint64_t* part, int grid, int ldlists, int kc, int k,
                           int64_t row0, const float* xstats, int fmt, const float* qscale,
@@ -775,21 +795,26 @@ cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64
                           cudaStream_t st, int phase, const float* tau, uint64_t* hkeys,
                           float* lb, const uint64_t* seed, int seed_ld) {
   const size_t base = (size_t)((D + 3) & ~3) * 4 + (size_t)kp * 8;
-  const size_t row = (size_t)(D + 4) * 4;
-  static const int env_rows = [] {  // timing experiments: VX_DEBUG_RERANK_ROWS, read once
+  static const int env_rows = [] {
     const char* e = getenv("VX_DEBUG_RERANK_ROWS");
     return e ? atoi(e) : 0;
   }();
-  const int want = env_rows > 0 ? env_rows : rerank_rows(kp);
-  int R = (int)((220 * 1024 - base) / row);
-  R = R > want ? want : (R < 1 ? 1 : R);
-  const size_t smem = base + (size_t)R * row;
+  static const int env_dc = [] {
+    const char* e = getenv("VX_DEBUG_RERANK_DC");
+    return e ? atoi(e) : 0;
+  }();
+  int DC = env_dc > 0 && env_dc % 32 == 0 && D % env_dc == 0 ? env_dc : 192;
+  while (DC > 32 && D % DC) DC -= 32;
+  int R = env_rows > 0 ? std::min(env_rows, 256) : 64;
+  auto smem_of = [&](int r) { return base + 2 * (size_t)r * (DC + 4) * 4; };
+  while (R > 32 && smem_of(R) > 220 * 1024) R -= 32;
+  const size_t smem = smem_of(R);
   cudaError_t e = cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
   rerank_kernel<<<B, 256, smem, st>>>(docs, q, D, cand, kp, part, grid, ldlists, kc, k, row0,
                                       xstats, fmt, qscale, out_keys, out_ids, out_scores, flags, R,
-                                      phase, tau, hkeys, lb, seed, seed_ld);
+                                      DC, phase, tau, hkeys, lb, seed, seed_ld);
   return cudaGetLastError();
 }
 
