@@ -395,6 +395,17 @@ def run_ours(args) -> None:
         q = torch.from_numpy(q_h).to(dev) if q_h is not None else None
         qt = torch.from_numpy(qt_h).to(dev) if qt_h is not None else None
         cand = torch.from_numpy(cand_h).to(dev) if cand_h is not None else None
+        # the e2e leg's host inputs live in page-locked memory (the contract's "pinned host
+        # memory"; the library then DMAs them without its staging memcpy)
+        pinned_keep = []
+
+        def pinned(a):
+            if a is None:
+                return None
+            t = torch.from_numpy(a).pin_memory()
+            pinned_keep.append(t)
+            return t.numpy()
+        q_h, qt_h, cand_h = pinned(q_h), pinned(qt_h), pinned(cand_h)
         ids = torch.empty((B, k), dtype=torch.int64, device=dev)
         ip = torch.empty((B, k), dtype=torch.float32, device=dev)
         msc = torch.empty((B, k), dtype=torch.float32, device=dev)

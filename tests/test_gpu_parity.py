@@ -217,6 +217,37 @@ def test_row_gather_api_equals_contiguous(vx, oracle):
         assert all(np.array_equal(a, b) for a, b in zip(got, want))
 
 
+def test_pinned_host_buffers_equal_pageable(vx, oracle):
+    # page-locked caller buffers are DMA'd directly (no staging memcpy, vx_api.cu upload_src /
+    # download), pageable ones through the staging: same results either way, outputs included
+    import torch
+    from paper_2511_02062_b200 import synth
+    N, D, k, nq, B = 30_000, 256, 10, 8, 7
+    with vx.Index(N, D, tok_per_doc=64, tok_dim=64, tok_blocks=40, max_batch=B, max_k=k,
+                  max_qtok=nq) as idx:
+        idx.synth(42)
+        idx.tokens_synth(45)
+        Q = synth.rows(43, 3, B, D)
+        qt = synth.query_tokens(B, nq, 64)
+        Qp_t, qtp_t = torch.from_numpy(Q).pin_memory(), torch.from_numpy(qt).pin_memory()
+        Qp, qtp = Qp_t.numpy(), qtp_t.numpy()
+        assert all(np.array_equal(a, b) for a, b in zip(idx.search(Qp, k), idx.search(Q, k)))
+        want = idx.search_rescore(Q, qt, k)
+        got = idx.search_rescore(Qp, qtp, k)
+        assert all(np.array_equal(a, b) for a, b in zip(got, want))
+        # pinned outputs through the C-ABI directly
+        lib = idx.lib
+        from paper_2511_02062_b200._lib import FP, LP
+        ids_t = torch.empty((B, k), dtype=torch.int64).pin_memory()
+        ip_t = torch.empty((B, k), dtype=torch.float32).pin_memory()
+        ms_t = torch.empty((B, k), dtype=torch.float32).pin_memory()
+        ids, ip, ms = ids_t.numpy(), ip_t.numpy(), ms_t.numpy()
+        assert lib.vx_search_rescore(idx._h, Qp.ctypes.data_as(FP), qtp.ctypes.data_as(FP), B, nq, k,
+                                     ids.ctypes.data_as(LP), ip.ctypes.data_as(FP),
+                                     ms.ctypes.data_as(FP)) == 0
+        assert np.array_equal(ids, want[0]) and np.array_equal(ip, want[1]) and np.array_equal(ms, want[2])
+
+
 def test_component_payload_path(vx, oracle):
     N, D, k, T, Nd, d, nq = 5000, 768, 10, 31, 128, 128, 32
     Q = oracle.synth_rows(43, 0, 3, D)
