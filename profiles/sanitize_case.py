@@ -37,3 +37,15 @@ with vx.Index(N, D, tok_per_doc=64, tok_dim=64, tok_blocks=50, max_batch=600, ma
     for _ in range(2):
         idx.search_rescore(synth.rows(43, 5, 16, D), qt, k)
     print("sanitize case done", idx.stats()["cert_level2"], idx.stats()["cert_fallbacks"])
+
+# seeded scans (shards >= 512K rows): the strided sample pass (4-key lists), the seed merge,
+# the seeded full pass and the seed-bounded certificate — s8 and bf16, single-CTA and pairs
+N2 = 600_000
+with vx.Index(N2, D, max_batch=300, max_k=20) as idx:
+    idx.synth(42)
+    idx.set_option(vx.VX_OPT_SCAN, vx.VX_SCAN_TC)
+    for co in (vx.VX_COARSE_I8, vx.VX_COARSE_BF16):
+        idx.set_option(vx.VX_OPT_COARSE, co)
+        for B in (40, 300):
+            idx.search(synth.rows(43, 13, B, D), k)
+    print("seeded case done", idx.stats()["cert_level2"], idx.stats()["cert_fallbacks"])
