@@ -83,8 +83,14 @@ enum {
   VX_FLAG_NO_BF16_SHADOW = 1, /* do not keep the bf16 copy of the index (saves N*D*2 B) */
   VX_FLAG_NO_I8_SHADOW = 2    /* do not keep the s8 copy of the index (saves N*D B) */
 };
-/* MaxSim kernel selection (vx_set_option VX_OPT_MAXSIM). */
-enum { VX_MAXSIM_AUTO = 0, VX_MAXSIM_CC = 1, VX_MAXSIM_TC = 2 };
+/* MaxSim kernel selection (vx_set_option VX_OPT_MAXSIM).
+ *  AUTO / TC: tensor-core kernel; for nq <= 64 the fp32 query tokens enter as bf16 hi + lo
+ *             pairs (fp32-faithful: ~1e-6 relative to the fp64 MaxSim of the fp32 tokens),
+ *             else rounded to bf16;
+ *  TC_BF16Q:  tensor-core kernel, query tokens rounded to bf16 (~1e-3 relative);
+ *  CC:        CUDA-core kernel, bf16-rounded query tokens, in-order fmaf chains
+ *             (bit-identical to the oracle's VXO_F32 mode). */
+enum { VX_MAXSIM_AUTO = 0, VX_MAXSIM_CC = 1, VX_MAXSIM_TC = 2, VX_MAXSIM_TC_BF16Q = 3 };
 
 typedef struct vx_index_desc {
   int64_t n_docs;      /* global document count N (1 <= N < 2^32) */
@@ -118,6 +124,9 @@ typedef struct vx_stats {
                                  broadcast, owner MaxSim, max-reduce, order) */
   uint64_t cert_level2;       /* queries whose k'-candidate certificate failed and that went
                                  to the wide re-rank over the full per-CTA lists */
+  uint64_t host_staged_bytes; /* host-buffer API: bytes memcpy'd through the handle's pinned
+                                 staging (0 when every caller buffer was page-locked and DMA'd
+                                 directly) */
 } vx_stats;
 
 int32_t vx_abi_version(void);

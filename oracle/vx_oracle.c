@@ -40,25 +40,33 @@ void vxo_synth_rows(uint64_t seed, int64_t row0, int64_t n, int32_t dim, float* 
   }
 }
 
+static void vxo_synth_tokens_one(uint64_t seed, int64_t blk, int32_t ntok, int32_t dim,
+                                 uint16_t* out) {
+  int32_t v[4096];
+  for (int32_t j = 0; j < ntok; ++j) {
+    uint64_t grow = (uint64_t)(blk * ntok + j);
+    int64_t ss = 0;
+    for (int32_t c = 0; c < dim; ++c) {
+      v[c] = vx_synth_int(seed, grow, (uint64_t)c);
+      ss += (int64_t)v[c] * (int64_t)v[c];
+    }
+    uint16_t* o = out + (int64_t)j * dim;
+    for (int32_t c = 0; c < dim; ++c) o[c] = vx_f32_to_bf16_bits(vx_synth_finish(v[c], ss));
+  }
+}
+
 void vxo_synth_tokens(uint64_t seed, int64_t blk0, int64_t nblk, int32_t ntok, int32_t dim,
                       uint16_t* out) {
-  int64_t rows = nblk * (int64_t)ntok;
-#pragma omp parallel
-  {
-    int32_t* v = (int32_t*)malloc(sizeof(int32_t) * (size_t)dim);
-#pragma omp for schedule(static)
-    for (int64_t r = 0; r < rows; ++r) {
-      uint64_t grow = (uint64_t)(blk0 * ntok + r);
-      int64_t ss = 0;
-      for (int32_t c = 0; c < dim; ++c) {
-        v[c] = vx_synth_int(seed, grow, (uint64_t)c);
-        ss += (int64_t)v[c] * (int64_t)v[c];
-      }
-      uint16_t* o = out + r * (int64_t)dim;
-      for (int32_t c = 0; c < dim; ++c) o[c] = vx_f32_to_bf16_bits(vx_synth_finish(v[c], ss));
-    }
-    free(v);
-  }
+#pragma omp parallel for schedule(static)
+  for (int64_t b = 0; b < nblk; ++b)
+    vxo_synth_tokens_one(seed, blk0 + b, ntok, dim, out + b * (int64_t)ntok * dim);
+}
+
+void vxo_synth_token_blocks(uint64_t seed, const int64_t* blks, int64_t n, int32_t ntok,
+                            int32_t dim, uint16_t* out) {
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t i = 0; i < n; ++i)
+    vxo_synth_tokens_one(seed, blks[i], ntok, dim, out + i * (int64_t)ntok * dim);
 }
 
 double vxo_dot(const float* x, const float* q, int32_t dim, int32_t mode) {
@@ -208,7 +216,7 @@ int vxo_flat_topk(const float* X, int64_t n, int32_t dim, int64_t id_base, const
 
 /* ---- MaxSim ------------------------------------------------------------- */
 
-static double maxsim_one(const float* qb /* bf16-rounded fp32 [nq][dim] */, int32_t nq,
+static double maxsim_one(const float* qb /* bf16-rounded (VXO_F64_Q32: raw) fp32 [nq][dim] */, int32_t nq,
                          int32_t dim, const uint16_t* dt /* [Nd][dim] */, int32_t Nd,
                          int32_t mode) {
   if (mode == VXO_F32) {
@@ -246,7 +254,8 @@ int vxo_maxsim(const float* qtok, int32_t B, int32_t nq, int32_t dim, const int6
   int nt = nthreads_of(threads);
   int64_t qn = (int64_t)B * nq * dim;
   float* qb = (float*)malloc(sizeof(float) * (size_t)qn);
-  for (int64_t i = 0; i < qn; ++i) qb[i] = vx_bf16_bits_to_f32(vx_f32_to_bf16_bits(qtok[i]));
+  for (int64_t i = 0; i < qn; ++i)
+    qb[i] = mode == VXO_F64_Q32 ? qtok[i] : vx_bf16_bits_to_f32(vx_f32_to_bf16_bits(qtok[i]));
 #pragma omp parallel for num_threads(nt) schedule(dynamic, 4)
   for (int64_t bc = 0; bc < (int64_t)B * C; ++bc) {
     int64_t b = bc / C;

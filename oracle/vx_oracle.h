@@ -36,7 +36,10 @@
 extern "C" {
 #endif
 
-enum { VXO_F64 = 0, VXO_F32 = 1 };
+enum { VXO_F64 = 0, VXO_F32 = 1, VXO_F64_Q32 = 2 };
+/* VXO_F64_Q32 (vxo_maxsim only): fp64 accumulation with the query tokens kept in fp32 — the
+ * truth against the fp32 tokens a VXQ1 payload carries, so the bf16 rounding of the query
+ * tokens on the GPU path shows up as error instead of being part of the reference. */
 
 int vxo_threads(void);
 
@@ -46,6 +49,12 @@ void vxo_synth_rows(uint64_t seed, int64_t row0, int64_t n, int32_t dim, float* 
  * synthetic row b*ntok + j. */
 void vxo_synth_tokens(uint64_t seed, int64_t blk0, int64_t nblk, int32_t ntok, int32_t dim,
                       uint16_t* out);
+
+/* Token blocks blks[0..n) (any order, repeats allowed): bf16 bits [n][ntok][dim], block
+ * blks[i] as in vxo_synth_tokens — the blocks a batch's candidates touch, without the whole
+ * table. */
+void vxo_synth_token_blocks(uint64_t seed, const int64_t* blks, int64_t n, int32_t ntok,
+                            int32_t dim, uint16_t* out);
 
 /* Single inner product in the given mode. */
 double vxo_dot(const float* x, const float* q, int32_t dim, int32_t mode);
@@ -58,7 +67,7 @@ int vxo_flat_topk(const float* X, int64_t n, int32_t dim, int64_t id_base, const
                   double* scores);
 
 /* MaxSim of query tokens qtok fp32 [B][nq][dim] (rounded to bf16 first, as the
- * GPU does) against cand [B][C] ids; doc id uses token block (id mod T) of
+ * GPU does, except in VXO_F64_Q32) against cand [B][C] ids; doc id uses token block (id mod T) of
  * `table` (bf16 [T][Nd][dim]).  cand -1 -> -INF.  out [B][C]. */
 int vxo_maxsim(const float* qtok, int32_t B, int32_t nq, int32_t dim, const int64_t* cand,
                int32_t C, const uint16_t* table, int64_t T, int32_t Nd, int32_t mode,

@@ -12,7 +12,7 @@ import numpy as np
 
 HERE = Path(__file__).resolve().parent
 LIB = HERE / "libvx_oracle.so"
-F64, F32 = 0, 1
+F64, F32, F64_Q32 = 0, 1, 2
 _lib = None
 
 
@@ -35,6 +35,8 @@ def lib():
         L.vxo_synth_rows.restype = None
         L.vxo_synth_tokens.argtypes = [u64, i64, i64, i32, i32, hp]
         L.vxo_synth_tokens.restype = None
+        L.vxo_synth_token_blocks.argtypes = [u64, lp, i64, i32, i32, hp]
+        L.vxo_synth_token_blocks.restype = None
         L.vxo_dot.argtypes = [fp, fp, i32, i32]
         L.vxo_dot.restype = C.c_double
         L.vxo_flat_topk.argtypes = [fp, i64, i32, i64, fp, i32, i32, i32, i32, lp, dp]
@@ -64,6 +66,14 @@ def synth_rows(seed: int, row0: int, n: int, dim: int) -> np.ndarray:
 def synth_tokens(seed: int, blk0: int, nblk: int, ntok: int, dim: int) -> np.ndarray:
     out = np.empty((nblk, ntok, dim), np.uint16)
     lib().vxo_synth_tokens(seed, blk0, nblk, ntok, dim, _p(out, C.c_uint16))
+    return out
+
+
+def synth_token_blocks(seed: int, blks, ntok: int, dim: int) -> np.ndarray:
+    blks = np.ascontiguousarray(blks, np.int64)
+    out = np.empty((blks.shape[0], ntok, dim), np.uint16)
+    lib().vxo_synth_token_blocks(seed, _p(blks, C.c_int64), blks.shape[0], ntok, dim,
+                                 _p(out, C.c_uint16))
     return out
 
 
@@ -116,3 +126,65 @@ def percentile(v, p: float) -> float:
 
 def bf16_to_f32(bits: np.ndarray) -> np.ndarray:
     return (np.asarray(bits, np.uint32) << 16).view(np.float32)
+
+
+# ---- full-size helpers: the headline index (10M x 768 = 30.7 GB) never exists on the host;
+# rows are generated chunk by chunk and the per-chunk lists merged, so the oracle checks the
+# benched configuration itself.
+
+def merge_topk(ids_a, sc_a, ids_b, sc_b, k):
+    """Top-k of the union of two per-query lists, ordered (score desc, id asc); -1 ids pad."""
+    ids = np.concatenate([ids_a, ids_b], axis=1)
+    sc = np.concatenate([sc_a, sc_b], axis=1)
+    sc = np.where(ids < 0, -np.inf, sc)
+    idk = np.where(ids < 0, np.iinfo(np.int64).max, ids)
+    out_i = np.empty((ids.shape[0], k), np.int64)
+    out_s = np.empty((ids.shape[0], k), np.float64)
+    for b in range(ids.shape[0]):
+        o = np.lexsort((idk[b], -sc[b]))[:k]
+        out_i[b], out_s[b] = ids[b][o], sc[b][o]
+    out_i[~np.isfinite(out_s)] = -1
+    return out_i, out_s
+
+
+def flat_topk_synth(seed, n_docs, dim, Q, k, mode=F32, row0=0, chunk=1 << 20, threads=0):
+    """Exact top-k of Q over the synthetic rows [row0, row0 + n_docs) (vx_synth.h, seed),
+    generated in chunks.  Returns (ids, scores, scan_seconds): scan_seconds times only the
+    top-k passes (row generation is input preparation, untimed)."""
+    import time
+    Q = np.ascontiguousarray(Q, np.float32)
+    B = Q.shape[0]
+    ids = np.full((B, k), -1, np.int64)
+    sc = np.full((B, k), -np.inf)
+    t_scan = 0.0
+    for r0 in range(row0, row0 + n_docs, chunk):
+        n = min(chunk, row0 + n_docs - r0)
+        X = synth_rows(seed, r0, n, dim)
+        t0 = time.perf_counter()
+        ci, cs = flat_topk(X, Q, k, mode=mode, id_base=r0, threads=threads)
+        t_scan += time.perf_counter() - t0
+        ids, sc = merge_topk(ids, sc, ci, cs, k)
+        del X
+    return ids, sc, t_scan
+
+
+def maxsim_synth(qtok, cand, seed, T, ntok, dim, mode=F64, threads=0):
+    """MaxSim of qtok [B][nq][d] against cand [B][C] over the synthetic token table (seed,
+    T blocks), generating only the blocks the candidates use (doc id -> block id mod T)."""
+    cand = np.asarray(cand, np.int64)
+    blk = np.where(cand >= 0, cand % T, 0)
+    uniq, inv = np.unique(blk, return_inverse=True)
+    table = synth_token_blocks(seed, uniq, ntok, dim)
+    local = np.where(cand >= 0, inv.reshape(cand.shape), -1).astype(np.int64)
+    # ids index the compact table directly (local < len(uniq) = its T)
+    return maxsim(qtok, local, table, mode=mode, threads=threads)
+
+
+def order_by_maxsim(ids, ms):
+    """The fused stage's output order: MaxSim desc, id asc (-1 / -inf last)."""
+    out_i, out_m = np.empty_like(ids), np.empty_like(ms)
+    for b in range(ids.shape[0]):
+        idk = np.where(ids[b] < 0, np.iinfo(np.int64).max, ids[b])
+        o = np.lexsort((idk, -np.where(ids[b] < 0, -np.inf, ms[b])))
+        out_i[b], out_m[b] = ids[b][o], ms[b][o]
+    return out_i, out_m

@@ -7,7 +7,7 @@ csrc/, reached through the C-ABI of include/vortex_b200.h (libvortex_b200.so).
 """
 from ._lib import (VX_COARSE_AUTO, VX_COARSE_BF16, VX_COARSE_I8, VX_COARSE_TF32,
                    VX_FLAG_NO_BF16_SHADOW, VX_FLAG_NO_I8_SHADOW,
-                   VX_MAXSIM_AUTO, VX_MAXSIM_CC, VX_MAXSIM_TC, VX_OPT_COARSE, VX_OPT_GRAPHS,
+                   VX_MAXSIM_AUTO, VX_MAXSIM_CC, VX_MAXSIM_TC, VX_MAXSIM_TC_BF16Q, VX_OPT_COARSE, VX_OPT_GRAPHS,
                    VX_OPT_GRID, VX_OPT_KPRIME, VX_OPT_MAXSIM, VX_OPT_SCAN, VX_OPT_SCAN_PAIRS,
                    VX_OPT_SCAN_SEED, VX_OPT_SCAN_TILE,
                    VX_PREPARE_RESCORE, VX_PREPARE_SEARCH, VX_SCAN_AUTO,
@@ -19,4 +19,4 @@ from .index import Index
 __all__ = ["Index", "SearchComponent", "Registry", "VortexError", "VxError", "load",
            "encode_query", "decode_query", "encode_result", "decode_result", "VX_SCAN_AUTO",
            "VX_SCAN_F32", "VX_SCAN_TC", "VX_OPT_SCAN", "VX_OPT_GRID", "VX_OPT_GRAPHS", "VX_OPT_MAXSIM",
-           "VX_MAXSIM_AUTO", "VX_MAXSIM_CC", "VX_MAXSIM_TC", "VX_PREPARE_SEARCH", "VX_PREPARE_RESCORE"]
+           "VX_MAXSIM_AUTO", "VX_MAXSIM_CC", "VX_MAXSIM_TC", "VX_MAXSIM_TC_BF16Q", "VX_PREPARE_SEARCH", "VX_PREPARE_RESCORE"]

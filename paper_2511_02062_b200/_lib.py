@@ -18,7 +18,7 @@ STATUS = {0: "VX_OK", 1: "VX_ERR_INVALID", 2: "VX_ERR_CUDA", 3: "VX_ERR_OOM", 4:
           5: "VX_ERR_STATE", 6: "VX_ERR_UNSUPPORTED"}
 VX_SCAN_AUTO, VX_SCAN_F32, VX_SCAN_TC = 0, 1, 2
 VX_OPT_SCAN, VX_OPT_GRID, VX_OPT_GRAPHS, VX_OPT_MAXSIM = 1, 2, 3, 4
-VX_MAXSIM_AUTO, VX_MAXSIM_CC, VX_MAXSIM_TC = 0, 1, 2
+VX_MAXSIM_AUTO, VX_MAXSIM_CC, VX_MAXSIM_TC, VX_MAXSIM_TC_BF16Q = 0, 1, 2, 3
 VX_OPT_COARSE, VX_OPT_SCAN_TILE, VX_OPT_SCAN_PAIRS, VX_OPT_KPRIME, VX_OPT_SCAN_SEED = 5, 6, 7, 8, 9
 VX_COARSE_AUTO, VX_COARSE_TF32, VX_COARSE_BF16, VX_COARSE_I8 = 0, 1, 2, 3
 VX_FLAG_NO_BF16_SHADOW = 1
@@ -47,7 +47,7 @@ class Stats(C.Structure):
                 ("last_scan_ms", C.c_float), ("last_step_ms", C.c_float),
                 ("scan_ms_total", C.c_double), ("step_ms_total", C.c_double),
                 ("timed_batches", C.c_uint64), ("phase_ms", C.c_float * 4),
-                ("cert_level2", C.c_uint64)]
+                ("cert_level2", C.c_uint64), ("host_staged_bytes", C.c_uint64)]
 
 
 P = C.c_void_p

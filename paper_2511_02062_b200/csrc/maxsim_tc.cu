@@ -10,6 +10,15 @@
 // Epilogue (4 warps): thread = query token; tcgen05.ld its Nd scores, row max in registers,
 // warp-sum over query tokens, cross-warp sum in smem -> one fp32 score per candidate.  The
 // token x token matrix never leaves the SM.
+//
+// fp32-faithful query tokens (a.split, nq <= 64): the fp32 tokens the payload carries are
+// split into bf16 hi = RNE(q) and lo = RNE(q - hi) (|q - hi - lo| <= 2^-17 |q|; every
+// bf16 x bf16 product is exact in fp32).  The A tile has 128 rows and nq <= 64 of them would
+// be padding, so the lo rows take the padding: lane quadrant w holds tokens 16w..16w+15, hi
+// in its lanes 0-15 and lo in lanes 16-31.  The epilogue adds lane l + 16's accumulator to
+// lane l's (one shuffle per column) before the row max, so <hi + lo, d_j> costs no extra MMA
+// and no HBM bytes.  Measured vs the fp64 MaxSim of the fp32 tokens: ~1e-6 relative, where
+// rounding the query tokens to bf16 alone leaves ~1e-3 (tests/test_gpu_headline.py).
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -60,26 +69,32 @@ __global__ void __launch_bounds__(kMsThreads, 2)
     return id >= 0 && id >= a.id_lo && id < a.id_hi;
   };
 
-  // A tile: query tokens -> bf16 (RNE), SWIZZLE_128B K-major; rows >= nq are zero
+  // A tile: query tokens -> bf16 (RNE), SWIZZLE_128B K-major; rows without a token are zero.
+  // Split: row r = 32 w + l holds token 16 w + (l & 15), its hi part for l < 16, lo for l >= 16.
   {
     const float* qt = a.qtok ? a.qtok + (size_t)b * nq * a.d : nullptr;
     const uint16_t* qt16 = a.qtok16 ? a.qtok16 + (size_t)b * nq * a.d : nullptr;
     const int chunks16 = DK * 128 * 8;  // 16-byte chunks in the A tile
     for (int i = threadIdx.x; i < chunks16; i += blockDim.x) {
       const int kb = i / (128 * 8), rem = i % (128 * 8), r = rem >> 3, ch = rem & 7;
+      const int tok = a.split ? ((r >> 5) << 4) + (r & 15) : r;
+      const int part = a.split ? (r >> 4) & 1 : 0;  // 0: hi (or plain RNE), 1: lo
       uint32_t w[4] = {0, 0, 0, 0};
-      if (r < nq && qt16) {
-        const uint4 v = *reinterpret_cast<const uint4*>(qt16 + (size_t)r * a.d + kb * 64 + ch * 8);
+      if (tok < nq && qt16) {
+        const uint16_t* src16 = qt16 + (part ? a.lo_off : 0);
+        const uint4 v = *reinterpret_cast<const uint4*>(src16 + (size_t)tok * a.d + kb * 64 + ch * 8);
         w[0] = v.x;
         w[1] = v.y;
         w[2] = v.z;
         w[3] = v.w;
-      } else if (r < nq) {
-        const float* src = qt + (size_t)r * a.d + kb * 64 + ch * 8;
+      } else if (tok < nq) {
+        const float* src = qt + (size_t)tok * a.d + kb * 64 + ch * 8;
+        auto conv = [&](float v) -> uint32_t {
+          const uint16_t h = vx_f32_to_bf16_bits(v);
+          return part ? vx_f32_to_bf16_bits(v - vx_bf16_bits_to_f32(h)) : h;
+        };
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-          w[e] = (uint32_t)vx_f32_to_bf16_bits(src[2 * e]) |
-                 ((uint32_t)vx_f32_to_bf16_bits(src[2 * e + 1]) << 16);
+        for (int e = 0; e < 4; ++e) w[e] = conv(src[2 * e]) | (conv(src[2 * e + 1]) << 16);
       }
       uint4* dst = reinterpret_cast<uint4*>(sA + kb * C::kATile + r * 128 + ((ch ^ (r & 7)) << 4));
       *dst = make_uint4(w[0], w[1], w[2], w[3]);
@@ -170,7 +185,9 @@ __global__ void __launch_bounds__(kMsThreads, 2)
     }
   } else {
     const int quad = warp & 3;
-    const bool active = quad * 32 < nq;  // warp-uniform: does this lane quadrant hold tokens?
+    const bool split = a.split != 0;
+    const int tok0 = split ? quad * 16 : quad * 32;  // first token of this lane quadrant
+    const bool active = tok0 < nq;  // warp-uniform: does this lane quadrant hold tokens?
     int buf = 0;
     uint32_t bph = 0;
     for (int c = c0; c < c1; ++c) {
@@ -188,14 +205,23 @@ __global__ void __launch_bounds__(kMsThreads, 2)
           uint32_t r[32];
           tmem_ld32(col + cc * 32, r);
           tmem_ld_wait();
+          if (split) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(r[i]));
+            for (int i = 0; i < 32; ++i) {
+              const float v = __uint_as_float(r[i]);
+              mx = fmaxf(mx, v + __shfl_down_sync(0xffffffffu, v, 16));
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(r[i]));
+          }
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[buf]);
-      float v = (active && quad * 32 + lane < nq) ? mx : 0.0f;
+      const bool mine = split ? (lane < 16 && tok0 + lane < nq) : (tok0 + lane < nq);
+      float v = (active && mine) ? mx : 0.0f;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
       if (lane == 0) partial[buf * 4 + quad] = v;
@@ -245,12 +271,13 @@ static cudaError_t launch_ms(const CUtensorMap* tt, const MaxSimArgs& a, cudaStr
   return cudaGetLastError();
 }
 
-bool maxsim_tc_supported(int nq, int Nd, int d) {
+bool maxsim_tc_supported(int nq, int Nd, int d) {  // split additionally needs nq <= 64
   return nq >= 1 && nq <= 128 && (Nd == 64 || Nd == 128 || Nd == 256) && (d == 64 || d == 128);
 }
 
 cudaError_t launch_maxsim_tc(const CUtensorMap* tt, const MaxSimArgs& a, cudaStream_t st) {
   if (a.B <= 0 || a.C <= 0) return cudaSuccess;
+  if (a.split && a.nq > kMaxSimSplitMaxNq) return cudaErrorInvalidValue;
   if (a.d == 128) {
     if (a.Nd == 128) return launch_ms<128, 2>(tt, a, st);
     if (a.Nd == 64) return launch_ms<64, 2>(tt, a, st);

@@ -238,14 +238,18 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
 // qr = |q - q^| for the coarse operand q^ of the query (bf16(q), or sq * q8), each already
 // inflated for fp32 rounding; xstats = shard maxima [|x|, |bf16 x|, |x - bf16 x|, |sx x8|,
 // |x - sx x8|, sx].
-__device__ __forceinline__ float cert_err_bound(int fmt, float qn, float qh, float qr,
+__device__ __forceinline__ float cert_err_bound(int fmt, int D, float qn, float qh, float qr,
                                                 const float* __restrict__ xstats) {
   float e;
   if (fmt == FMT_TF32) e = kErrCoefTF32 * qn * xstats[0];
   else if (fmt == FMT_I8) e = qh * xstats[4] + qr * xstats[3] + qr * xstats[4];
   else e = qh * xstats[2] + qr * xstats[1] + qr * xstats[2];
   const float xmax = fmaxf(xstats[0], fmt == FMT_I8 ? xstats[3] : xstats[1]);
-  return e * 1.001f + 0.000244140625f * fmaxf(qn, qh) * xmax + 1e-30f;
+  // fp32 accumulation slack: the exact in-order chain and the tensor core's fp32 sum each
+  // err <= ~D 2^-24 |q||x| (2x margin for the tensor core's accumulation rounding): 2^-12
+  // covers D <= 1008; longer rows scale it
+  const float slack = fmaxf(0.000244140625f, (float)(4 * D + 64) * 5.9604645e-8f);
+  return e * 1.001f + slack * fmaxf(qn, qh) * xmax + 1e-30f;
 }
 
 // The query's coarse operand q^ (bf16 RNE, or sq * rint(q / sq) for s8 — the same rounding
@@ -337,7 +341,7 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   float qn, qh, qr;
   query_norms_final(s_red, fmt, &qn, &qh, &qr);
-  const float E = cert_err_bound(fmt, qn, qh, qr, xstats);
+  const float E = cert_err_bound(fmt, D, qn, qh, qr, xstats);
   const uint64_t* cb = cand + (size_t)b * kp;
   const uint64_t tprime = cb[kp - 1];  // coarse k'-th key (0: fewer than k' candidates)
   const int kh = k < kp ? k : kp;      // head rows
@@ -473,8 +477,8 @@ __global__ void __launch_bounds__(256)
     //   |q.x - q16.x16| <= |q16| max|rx| + |rq| max|x16| + |rq| max|rx|: a rigorous bound
     //   from the actual rounding residuals (the worst case 2u|q||x| = 2^-7 |q||x| is ~2x
     //   looser).  TF32 coarse: per-operand truncation <= 2^-10 -> 2^-9 |q| max|x|.
-    //   Both: + 2^-12 |q| max|x| for the fp32 accumulation of the tensor core and of the
-    //   exact in-order chain (each <= 768 * 2^-24 relative, 5x margin).
+    //   Both: + max(2^-12, (4D+64) 2^-24) |q| max|x| for the fp32 accumulation of the tensor
+    //   core and of the exact in-order chain (each <= D 2^-24 relative; cert_err_bound).
     // Sharded: a document outside the candidates is also out of the GLOBAL top-k when its
     // bound is below tau (the shard then reports fewer than k keys, padded with 0).
     const float bound = fmaxf(tprime ? vx_key_score(tprime) : -INFINITY, sd) * cscale + E;
@@ -634,7 +638,7 @@ __global__ void __launch_bounds__(256)
       if (cb > -INFINITY) {
         float qn, qh, qr;
         query_norms_final(s_red, fmt, &qn, &qh, &qr);
-        const float E = cert_err_bound(fmt, qn, qh, qr, xstats);
+        const float E = cert_err_bound(fmt, D, qn, qh, qr, xstats);
         const uint64_t ek = k <= np2 ? keys[k - 1] : 0ull;
         fail = (ek == 0ull || !(vx_key_score(ek) > cb * cscale + E)) ? 1 : 0;
       }
@@ -848,8 +852,17 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+__global__ void fill_neg_inf_kernel(float* __restrict__ v, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    v[i] = -INFINITY;
+}
+
 cudaError_t launch_shard_tau(const float* all, int G, int B, int k, float* tau, cudaStream_t st) {
-  if (G * k > 1024) return cudaErrorInvalidValue;
+  if (G * k > 1024) {  // beyond the kernel's smem list: no threshold (every shard re-ranks its
+                       // whole candidate set; still exact, just no pruning)
+    fill_neg_inf_kernel<<<(B + 255) / 256, 256, 0, st>>>(tau, B);
+    return cudaGetLastError();
+  }
   shard_tau_kernel<<<B, 256, 0, st>>>(all, G, B, k, tau);
   return cudaGetLastError();
 }

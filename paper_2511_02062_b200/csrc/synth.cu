@@ -72,6 +72,27 @@ cudaError_t launch_to_bf16(const float* in, uint16_t* out, int64_t n, cudaStream
   return cudaGetLastError();
 }
 
+// fp32 -> (hi, lo) bf16 planes for the fp32-faithful MaxSim operand (maxsim_tc.cu): the
+// residual v - hi is exact in fp32, its RNE lo leaves |v - hi - lo| <= 2^-17 |v|.
+__global__ void split_bf16_kernel(const float* __restrict__ in, uint16_t* __restrict__ hi,
+                                  uint16_t* __restrict__ lo, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = in[i];
+    const uint16_t h = vx_f32_to_bf16_bits(v);
+    hi[i] = h;
+    lo[i] = vx_f32_to_bf16_bits(v - vx_bf16_bits_to_f32(h));
+  }
+}
+
+cudaError_t launch_split_bf16(const float* in, uint16_t* out, int64_t n, cudaStream_t st) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  split_bf16_kernel<<<(int)blocks, 256, 0, st>>>(in, out, out + n, n);
+  return cudaGetLastError();
+}
+
 // ---- s8 coarse operands.  The index shadow uses ONE scale per shard, sx = max|x| / 127, so
 // for a fixed query every document's s32 dot product is in the same units and the scan can
 // select on the raw integer; queries use one scale per row, sq = max|q| / 127.  Rounding:

@@ -156,7 +156,8 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
   h->grid = h->num_sms;
   ALLOC(h->d_q, B * D * 4);
   if (d->tok_per_doc > 0) ALLOC(h->d_qtok, B * d->max_qtok * d->tok_dim * 4);
-  if (d->tok_per_doc > 0 && d->n_shards > 1) ALLOC(h->d_qtok16, B * d->max_qtok * d->tok_dim * 2);
+  if (d->tok_per_doc > 0 && d->n_shards > 1)  // bf16 hi + lo planes (shard exchange)
+    ALLOC(h->d_qtok16, 2 * B * d->max_qtok * d->tok_dim * 2);
   ALLOC(h->d_part, B * (size_t)h->grid * 256 * 8);
   ALLOC(h->d_keys, B * K * 8);
   ALLOC(h->d_ids, B * K * 8);
@@ -278,6 +279,7 @@ extern "C" vx_status vx_index_shard_range(const vx_index* h, int64_t* row0, int6
 
 extern "C" vx_status vx_set_option(vx_index* h, int32_t option, int64_t value) {
   if (!h) return fail(VX_ERR_INVALID, "null handle");
+  drop_graphs(h);  // every option below changes what a captured stage would run
   switch (option) {
     case VX_OPT_SCAN:
       if (value != VX_SCAN_AUTO && value != VX_SCAN_F32 && value != VX_SCAN_TC)
@@ -317,9 +319,10 @@ extern "C" vx_status vx_set_option(vx_index* h, int32_t option, int64_t value) {
       h->coarse = (int)value;
       return VX_OK;
     case VX_OPT_MAXSIM:
-      if (value != VX_MAXSIM_AUTO && value != VX_MAXSIM_CC && value != VX_MAXSIM_TC)
+      if (value != VX_MAXSIM_AUTO && value != VX_MAXSIM_CC && value != VX_MAXSIM_TC &&
+          value != VX_MAXSIM_TC_BF16Q)
         return fail(VX_ERR_INVALID, "maxsim algorithm %lld", (long long)value);
-      if (value == VX_MAXSIM_TC && h->tokens &&
+      if ((value == VX_MAXSIM_TC || value == VX_MAXSIM_TC_BF16Q) && h->tokens &&
           !vx::maxsim_tc_supported(h->desc.max_qtok, h->desc.tok_per_doc, h->desc.tok_dim))
         return fail(VX_ERR_UNSUPPORTED, "tensor-core MaxSim needs Nd in {64,128,256}, d in {64,128}");
       h->maxsim_algo = (int)value;
@@ -371,6 +374,7 @@ extern "C" vx_status vx_reset_stats(vx_index* h) {
 // certificate bounds with.  The s8 scale is shard-wide, so the whole s8 shadow is rebuilt.
 static vx_status refresh_shadows(vx_index* h, int64_t row_off, int64_t nrows) {
   const int64_t D = h->desc.dim;
+  drop_graphs(h);  // the AUTO coarse format and the certificate inputs may change
   float* sx = reinterpret_cast<float*>(h->d_xnorm) + 5;
   if (h->docs8) {
     CU_TRY(vx::launch_to_i8_shadow(h->docs, h->n_local * D, h->docs8, h->d_xnorm + 6, sx,
@@ -476,36 +480,63 @@ static void gather_rows(uint8_t* dst, const float* base, const float* const* row
     memcpy(dst, base, (size_t)B * row_bytes);
 }
 
-// Page-locked host memory (cudaMallocHost / cudaHostRegister, first and last byte): the
-// DMA engines read / write it directly, so the host API skips the staging memcpy — at
-// B = 1024 the 16.8 MB of fp32 query tokens took ~1 ms of host memcpy per batch.
+// Page-locked host memory (cudaMallocHost / cudaHostRegister): the DMA engines read / write
+// it directly, so the host API skips the staging memcpy — at B = 1024 the 16.8 MB of fp32
+// query tokens took ~1 ms of host memcpy per batch.  The WHOLE range [p, p + bytes) must lie
+// inside one page-locked allocation (a buffer straddling two pinned allocations with pageable
+// memory between them is not DMA-safe); anything else goes through the staging buffer.
+typedef CUresult (*PFN_ptrAttr)(void*, CUpointer_attribute, CUdeviceptr);
+static PFN_ptrAttr get_ptr_attr() {
+  static PFN_ptrAttr fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuPointerGetAttribute", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_ptrAttr>(p);
+  });
+  return fn;
+}
+
 static bool is_pinned(const void* p, size_t bytes) {
   if (!p || !bytes) return false;
-  for (const void* a : {p, static_cast<const void*>(static_cast<const uint8_t*>(p) + bytes - 1)}) {
-    cudaPointerAttributes at;
-    if (cudaPointerGetAttributes(&at, a) != cudaSuccess) {
-      cudaGetLastError();
-      return false;
-    }
-    if (at.type != cudaMemoryTypeHost) return false;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
   }
-  return true;
+  if (at.type != cudaMemoryTypeHost) return false;
+  PFN_ptrAttr fn = get_ptr_attr();
+  if (!fn) return false;
+  CUdeviceptr start = 0;
+  size_t size = 0;
+  const CUdeviceptr dp = (CUdeviceptr)(uintptr_t)(at.devicePointer ? at.devicePointer : p);
+  if (fn(&start, CU_POINTER_ATTRIBUTE_RANGE_START_ADDR, dp) != CUDA_SUCCESS ||
+      fn(&size, CU_POINTER_ATTRIBUTE_RANGE_SIZE, dp) != CUDA_SUCCESS)
+    return false;
+  // the range is reported in the allocation's device address space; p's offset into it is
+  // the same in host and device views
+  return (uint64_t)dp >= (uint64_t)start && (uint64_t)dp + bytes <= (uint64_t)start + size;
 }
 
 // source of a batch upload: the caller's contiguous pinned buffer itself, else the rows
 // gathered into the handle's pinned staging
-static const void* upload_src(uint8_t* stage, const float* base, const float* const* rows, int B,
-                              size_t row_bytes) {
+static const void* upload_src(vx_index* h, uint8_t* stage, const float* base,
+                              const float* const* rows, int B, size_t row_bytes) {
   if (!rows && is_pinned(base, (size_t)B * row_bytes)) return base;
   gather_rows(stage, base, rows, B, row_bytes);
+  h->st.host_staged_bytes += (uint64_t)B * row_bytes;
   return stage;
 }
 
 // device -> host result copy: straight into a pinned destination, else via the staging
 // (*deferred set: memcpy after the sync)
-static cudaError_t download(void* dst, uint8_t* stage, const void* src, size_t bytes,
+static cudaError_t download(vx_index* h, void* dst, uint8_t* stage, const void* src, size_t bytes,
                             cudaStream_t st, bool* deferred) {
   *deferred = !is_pinned(dst, bytes);
+  if (*deferred) h->st.host_staged_bytes += bytes;
   return cudaMemcpyAsync(*deferred ? static_cast<void*>(stage) : dst, src, bytes,
                          cudaMemcpyDeviceToHost, st);
 }
@@ -516,6 +547,17 @@ static bool rows_ok(const float* const* rows, int B) {
   return true;
 }
 
+// A failed call may have left a DMA from / to the caller's own (pinned) buffers in flight:
+// drain both streams before returning the error, so the caller may free them at once.
+static vx_status drained(vx_index* h, vx_status s) {
+  if (s != VX_OK) {
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    if (h->stream2) cudaStreamSynchronize(h->stream2);
+    cudaGetLastError();
+  }
+  return s;
+}
+
 static vx_status host_search(vx_index* h, const float* q, const float* const* q_rows, int32_t B,
                              int32_t k, int64_t* ids, float* scores) {
   VX_TRY(check_batch(h, B, k));
@@ -524,14 +566,14 @@ static vx_status host_search(vx_index* h, const float* q, const float* const* q_
   cudaStream_t st = h->stream;
   const size_t qrow = (size_t)h->desc.dim * 4, qb = (size_t)B * qrow;
   uint8_t* stage = static_cast<uint8_t*>(h->h_stage);
-  CU_TRY(cudaMemcpyAsync(h->d_q, upload_src(stage, q, q_rows, B, qrow), qb,
+  CU_TRY(cudaMemcpyAsync(h->d_q, upload_src(h, stage, q, q_rows, B, qrow), qb,
                          cudaMemcpyHostToDevice, st));
   VX_TRY(stage_begin(h, OP_SEARCH, h->d_q, B, 0, k, st));
   VX_TRY(stage_search_out(h, B, k, h->d_out_ids, h->d_out_ip, st));
   const size_t n = (size_t)B * k;
   bool d_ids, d_sc;
-  CU_TRY(download(ids, stage, h->d_out_ids, n * 8, st, &d_ids));
-  CU_TRY(download(scores, stage + n * 8, h->d_out_ip, n * 4, st, &d_sc));
+  CU_TRY(download(h, ids, stage, h->d_out_ids, n * 8, st, &d_ids));
+  CU_TRY(download(h, scores, stage + n * 8, h->d_out_ip, n * 4, st, &d_sc));
   VX_TRY(vx_sync(h));
   if (d_ids) memcpy(ids, stage, n * 8);
   if (d_sc) memcpy(scores, stage + n * 8, n * 4);
@@ -541,18 +583,17 @@ static vx_status host_search(vx_index* h, const float* q, const float* const* q_
 extern "C" vx_status vx_search(vx_index* h, const float* q, int32_t B, int32_t k, int64_t* ids,
                                float* scores) {
   if (!h || !q || !ids || !scores) return fail(VX_ERR_INVALID, "null argument");
-  return host_search(h, q, nullptr, B, k, ids, scores);
+  return drained(h, host_search(h, q, nullptr, B, k, ids, scores));
 }
 
 extern "C" vx_status vx_search_rows(vx_index* h, const float* const* q_rows, int32_t B, int32_t k,
                                     int64_t* ids, float* scores) {
   if (!h || !q_rows || !ids || !scores) return fail(VX_ERR_INVALID, "null argument");
-  return host_search(h, nullptr, q_rows, B, k, ids, scores);
+  return drained(h, host_search(h, nullptr, q_rows, B, k, ids, scores));
 }
 
-extern "C" vx_status vx_maxsim(vx_index* h, const float* qtok, int32_t B, int32_t nq,
-                               const int64_t* cand, int32_t C, float* out) {
-  if (!h || !qtok || !cand || !out) return fail(VX_ERR_INVALID, "null argument");
+static vx_status host_maxsim(vx_index* h, const float* qtok, int32_t B, int32_t nq,
+                             const int64_t* cand, int32_t C, float* out) {
   if (!h->tokens) return fail(VX_ERR_STATE, "index has no token store");
   if (B < 1 || B > h->desc.max_batch || C < 1 || C > h->desc.max_k)
     return fail(VX_ERR_INVALID, "B %d / C %d outside [1,%d] / [1,%d]", B, C, h->desc.max_batch,
@@ -562,15 +603,27 @@ extern "C" vx_status vx_maxsim(vx_index* h, const float* qtok, int32_t B, int32_
   cudaStream_t st = h->stream;
   const size_t tb = (size_t)B * nq * h->desc.tok_dim * 4, cb = (size_t)B * C * 8;
   uint8_t* stage = static_cast<uint8_t*>(h->h_stage);
-  memcpy(stage, qtok, tb);
-  CU_TRY(cudaMemcpyAsync(h->d_qtok, stage, tb, cudaMemcpyHostToDevice, st));
-  memcpy(stage + tb, cand, cb);
-  CU_TRY(cudaMemcpyAsync(h->d_out_ids, stage + tb, cb, cudaMemcpyHostToDevice, st));
+  CU_TRY(cudaMemcpyAsync(h->d_qtok, upload_src(h, stage, qtok, nullptr, B, tb / B), tb,
+                         cudaMemcpyHostToDevice, st));
+  const void* csrc = cand;
+  if (!is_pinned(cand, cb)) {
+    memcpy(stage + tb, cand, cb);
+    h->st.host_staged_bytes += cb;
+    csrc = stage + tb;
+  }
+  CU_TRY(cudaMemcpyAsync(h->d_out_ids, csrc, cb, cudaMemcpyHostToDevice, st));
   VX_TRY(run_maxsim(h, h->d_qtok, B, nq, h->d_out_ids, C, h->d_out_ms, st));
-  CU_TRY(cudaMemcpyAsync(stage, h->d_out_ms, (size_t)B * C * 4, cudaMemcpyDeviceToHost, st));
+  bool d_out;
+  CU_TRY(download(h, out, stage, h->d_out_ms, (size_t)B * C * 4, st, &d_out));
   VX_TRY(vx_sync(h));
-  memcpy(out, stage, (size_t)B * C * 4);
+  if (d_out) memcpy(out, stage, (size_t)B * C * 4);
   return VX_OK;
+}
+
+extern "C" vx_status vx_maxsim(vx_index* h, const float* qtok, int32_t B, int32_t nq,
+                               const int64_t* cand, int32_t C, float* out) {
+  if (!h || !qtok || !cand || !out) return fail(VX_ERR_INVALID, "null argument");
+  return drained(h, host_maxsim(h, qtok, B, nq, cand, C, out));
 }
 
 static vx_status host_search_rescore(vx_index* h, const float* q, const float* const* q_rows,
@@ -586,20 +639,20 @@ static vx_status host_search_rescore(vx_index* h, const float* q, const float* c
   const size_t qrow = (size_t)h->desc.dim * 4, trow = (size_t)nq * h->desc.tok_dim * 4;
   const size_t qb = (size_t)B * qrow, tb = (size_t)B * trow;
   uint8_t* stage = static_cast<uint8_t*>(h->h_stage);
-  CU_TRY(cudaMemcpyAsync(h->d_q, upload_src(stage, q, q_rows, B, qrow), qb,
+  CU_TRY(cudaMemcpyAsync(h->d_q, upload_src(h, stage, q, q_rows, B, qrow), qb,
                          cudaMemcpyHostToDevice, st));
   VX_TRY(stage_begin(h, OP_RESCORE, h->d_q, B, nq, k, st));
   // the query tokens are only read by part 2: (stage and) upload them while part 1 runs
-  CU_TRY(cudaMemcpyAsync(h->d_qtok, upload_src(stage + qb, qtok, tok_rows, B, trow), tb,
+  CU_TRY(cudaMemcpyAsync(h->d_qtok, upload_src(h, stage + qb, qtok, tok_rows, B, trow), tb,
                          cudaMemcpyHostToDevice, h->stream2));
   CU_TRY(cudaEventRecord(h->tok_ev, h->stream2));
   CU_TRY(cudaStreamWaitEvent(st, h->tok_ev, 0));
   VX_TRY(stage_finish(h, h->d_qtok, B, nq, k, h->d_out_ids, h->d_out_ip, h->d_out_ms, st));
   const size_t n = (size_t)B * k;
   bool d_ids, d_ip, d_ms;
-  CU_TRY(download(ids, stage, h->d_out_ids, n * 8, st, &d_ids));
-  CU_TRY(download(ip, stage + n * 8, h->d_out_ip, n * 4, st, &d_ip));
-  CU_TRY(download(ms, stage + n * 12, h->d_out_ms, n * 4, st, &d_ms));
+  CU_TRY(download(h, ids, stage, h->d_out_ids, n * 8, st, &d_ids));
+  CU_TRY(download(h, ip, stage + n * 8, h->d_out_ip, n * 4, st, &d_ip));
+  CU_TRY(download(h, ms, stage + n * 12, h->d_out_ms, n * 4, st, &d_ms));
   VX_TRY(vx_sync(h));
   if (d_ids) memcpy(ids, stage, n * 8);
   if (d_ip) memcpy(ip, stage + n * 8, n * 4);
@@ -611,14 +664,14 @@ extern "C" vx_status vx_search_rescore(vx_index* h, const float* q, const float*
                                        int32_t nq, int32_t k, int64_t* ids, float* ip,
                                        float* ms) {
   if (!h || !q || !qtok || !ids || !ip || !ms) return fail(VX_ERR_INVALID, "null argument");
-  return host_search_rescore(h, q, nullptr, qtok, nullptr, B, nq, k, ids, ip, ms);
+  return drained(h, host_search_rescore(h, q, nullptr, qtok, nullptr, B, nq, k, ids, ip, ms));
 }
 
 extern "C" vx_status vx_search_rescore_rows(vx_index* h, const float* const* q_rows,
                                             const float* const* tok_rows, int32_t B, int32_t nq,
                                             int32_t k, int64_t* ids, float* ip, float* ms) {
   if (!h || !q_rows || !tok_rows || !ids || !ip || !ms) return fail(VX_ERR_INVALID, "null argument");
-  return host_search_rescore(h, nullptr, q_rows, nullptr, tok_rows, B, nq, k, ids, ip, ms);
+  return drained(h, host_search_rescore(h, nullptr, q_rows, nullptr, tok_rows, B, nq, k, ids, ip, ms));
 }
 
 // ---------------------------------------------------------------- live batcher

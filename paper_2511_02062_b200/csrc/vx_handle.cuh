@@ -161,6 +161,18 @@ struct vx_index {
 
 static inline void count_launch(vx_index* h, int n = 1) { h->st.kernel_launches += n; }
 
+// Captured stage graphs bake in every choice made at capture time (coarse format from the
+// shard statistics, k', seed, tile, pairs, grid, scan / MaxSim algorithm), so any option
+// change and any index upload / synth throws them away; the next batch of each shape
+// re-captures.
+static inline void drop_graphs(vx_index* h) {
+  if (h->graphs.empty()) return;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second.exec);
+  h->graphs.clear();
+}
+
 // Timing events: inside a stream capture they must be EXTERNAL event nodes, or the graph only
 // uses them for internal ordering and never records them for the host to read.
 static inline cudaError_t record_ev(vx_index* h, cudaEvent_t e, cudaStream_t st) {

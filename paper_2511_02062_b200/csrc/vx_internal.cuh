@@ -145,7 +145,10 @@ cudaError_t launch_synth_tokens(uint16_t* out, uint64_t seed, int64_t blk0, int6
 // -------- MaxSim (K4): maxsim.cu
 struct MaxSimArgs {
   const float* qtok;     // [B][nq][d] fp32 (rounded to bf16 in-kernel)
-  const uint16_t* qtok16 = nullptr;  // or already-rounded bf16 bits (shard exchange)
+  const uint16_t* qtok16 = nullptr;  // or already-rounded bf16 bits (shard exchange); with
+                                     // split, two planes: hi at qtok16, lo at qtok16 + lo_off
+  int64_t lo_off = 0;
+  int split = 0;         // TC kernel: query tokens as bf16 hi + lo pairs (fp32-faithful)
   const int64_t* cand;   // [B][C] global doc ids, -1 = skip
   const uint16_t* table; // [T][Nd][d] bf16 bits
   int64_t T;
@@ -154,6 +157,9 @@ struct MaxSimArgs {
   int64_t id_lo = 0, id_hi = INT64_MAX;  // ids outside [lo, hi) (another shard's) -> -INF, no loads
 };
 cudaError_t launch_maxsim(const MaxSimArgs& a, cudaStream_t st);
+// fp32 -> bf16 hi plane (out) + lo plane (out + n): hi = RNE(v), lo = RNE(v - hi)
+cudaError_t launch_split_bf16(const float* in, uint16_t* out, int64_t n, cudaStream_t st);
+constexpr int kMaxSimSplitMaxNq = 64;  // hi/lo rows share the 128-row A tile
 bool maxsim_tc_supported(int nq, int Nd, int d);
 cudaError_t launch_maxsim_tc(const CUtensorMap* tt, const MaxSimArgs& a, cudaStream_t st);
 

@@ -337,6 +337,14 @@ static vx_status local_topk(vx_index* h, const float* d_q, int B, int k, uint64_
   return VX_OK;
 }
 
+// Does the tensor-core MaxSim take the fp32-faithful hi/lo query split for nq tokens?
+// (AUTO / TC: yes when nq <= 64; VX_MAXSIM_TC_BF16Q: tokens rounded to bf16.)
+static bool maxsim_split(const vx_index* h, int nq) {
+  return (h->maxsim_algo == VX_MAXSIM_AUTO || h->maxsim_algo == VX_MAXSIM_TC) &&
+         nq <= vx::kMaxSimSplitMaxNq &&
+         vx::maxsim_tc_supported(nq, h->desc.tok_per_doc, h->desc.tok_dim);
+}
+
 vx_status run_maxsim(vx_index* h, const float* d_qtok, int B, int nq, const int64_t* d_cand,
                      int C, float* d_out, cudaStream_t st, int64_t id_lo, int64_t id_hi,
                      const uint16_t* d_qtok16) {
@@ -358,8 +366,10 @@ vx_status run_maxsim(vx_index* h, const float* d_qtok, int B, int nq, const int6
   a.id_hi = id_hi;
   const bool tc = h->maxsim_algo != VX_MAXSIM_CC &&
                   vx::maxsim_tc_supported(nq, a.Nd, a.d);
-  if (h->maxsim_algo == VX_MAXSIM_TC && !tc)
+  if ((h->maxsim_algo == VX_MAXSIM_TC || h->maxsim_algo == VX_MAXSIM_TC_BF16Q) && !tc)
     return fail(VX_ERR_UNSUPPORTED, "tensor-core MaxSim unsupported for nq=%d Nd=%d d=%d", nq, a.Nd, a.d);
+  a.split = maxsim_split(h, nq) ? 1 : 0;
+  a.lo_off = (int64_t)B * nq * a.d;  // the shard exchange's two-plane layout
   if (tc)
     CU_TRY(vx::launch_maxsim_tc(&h->tmap_tok, a, st));
   else
@@ -435,15 +445,21 @@ vx_status core_rescore(vx_index* h, const float* d_qtok, int B, int nq, int k,
   }
   const int n = B * k;
   const bool root = h->rank == 0;
-  // the tokens travel as bf16 (the MaxSim operand precision: the kernels round fp32 tokens
+  // the tokens travel in the MaxSim operand format: bf16 hi + lo planes for the fp32-faithful
+  // tensor-core kernel (the fp32 bytes), else one bf16 plane (the kernels round fp32 tokens
   // with the same RNE anyway, so the scores are unchanged) — half the broadcast bytes
   const int64_t ntok = (int64_t)B * nq * h->desc.tok_dim;
+  const int64_t nplanes = maxsim_split(h, nq) ? 2 : 1;
   if (root) {
-    CU_TRY(vx::launch_to_bf16(d_qtok, h->d_qtok16, ntok, st));
+    if (nplanes == 2)
+      CU_TRY(vx::launch_split_bf16(d_qtok, h->d_qtok16, ntok, st));
+    else
+      CU_TRY(vx::launch_to_bf16(d_qtok, h->d_qtok16, ntok, st));
     count_launch(h);
   }
   NCCL_TRY(nccl().GroupStart());
-  NCCL_TRY(nccl().Broadcast(h->d_qtok16, h->d_qtok16, (size_t)ntok * 2, ncclUint8, 0, h->comm, st));
+  NCCL_TRY(nccl().Broadcast(h->d_qtok16, h->d_qtok16, (size_t)(ntok * nplanes) * 2, ncclUint8, 0,
+                            h->comm, st));
   NCCL_TRY(nccl().Broadcast(h->d_ids, h->d_ids, (size_t)n, ncclInt64, 0, h->comm, st));
   NCCL_TRY(nccl().GroupEnd());
   VX_TRY(run_maxsim(h, nullptr, B, nq, h->d_ids, k, h->d_ms, st, h->row0, h->row0 + h->n_local,

@@ -1,9 +1,14 @@
 """Tensor-core MaxSim (K4, tcgen05 kind::f16) against the oracle.  Runs on a B200.
 
-Stated tolerance of this bf16 path (north star: "the stated tolerance must be reported for
-any bf16 path"): inputs are bf16 (query tokens rounded RNE on device, doc tokens stored
-bf16), products are exact in fp32, accumulation is fp32 inside the tensor core; the result
-must be within MS_RTOL = 1e-5 relative of the fp64 MaxSim of the same bf16 inputs.
+Stated tolerance (north star: "the stated tolerance must be reported for any bf16 path"):
+doc tokens are stored bf16 (the data), products are exact in fp32, accumulation is fp32
+inside the tensor core.
+  * default (nq <= 64): the fp32 query tokens enter as bf16 hi + lo pairs; the result must be
+    within MS_RTOL = 1e-5 relative (+1e-6) of the fp64 MaxSim of the FP32 query tokens
+    (oracle VXO_F64_Q32);
+  * VX_MAXSIM_TC_BF16Q (and nq > 64): query tokens rounded to bf16; within MS_RTOL of the
+    fp64 MaxSim of the same bf16-rounded inputs (against the fp32 tokens ~1e-3 relative,
+    tests/test_gpu_headline.py prints the measured figure).
 """
 from __future__ import annotations
 
@@ -24,7 +29,8 @@ def vx(vxlib):
     (1, 100, 32, 128, 128, 257), (8, 100, 32, 128, 128, 1000), (64, 100, 32, 128, 128, 4096),
     (3, 7, 17, 128, 128, 11), (2, 40, 128, 128, 128, 50), (5, 33, 32, 64, 128, 64),
     (4, 20, 32, 256, 128, 30), (6, 50, 32, 128, 64, 99), (2, 1, 1, 64, 64, 3)])
-def test_maxsim_tc_matches_oracle(vx, oracle, B, C, nq, Nd, d, T):
+@pytest.mark.parametrize("bf16q", [False, True])
+def test_maxsim_tc_matches_oracle(vx, oracle, B, C, nq, Nd, d, T, bf16q):
     rng = np.random.default_rng(B * 1000 + C)
     cand = np.stack([rng.choice(10_000_000, C, replace=False) for _ in range(B)]).astype(np.int64)
     if C > 3:
@@ -33,10 +39,11 @@ def test_maxsim_tc_matches_oracle(vx, oracle, B, C, nq, Nd, d, T):
     with vx.Index(1000, 32, tok_per_doc=Nd, tok_dim=d, tok_blocks=T, max_batch=B, max_k=max(C, 1),
                   max_qtok=nq) as idx:
         idx.tokens_synth(45)
-        idx.set_option(vx.VX_OPT_MAXSIM, vx.VX_MAXSIM_TC)
+        idx.set_option(vx.VX_OPT_MAXSIM, vx.VX_MAXSIM_TC_BF16Q if bf16q else vx.VX_MAXSIM_TC)
         out = idx.maxsim(qtok, cand)
     table = oracle.synth_tokens(45, 0, T, Nd, d)
-    ref = oracle.maxsim(qtok, cand, table, mode=0)
+    split = not bf16q and nq <= 64
+    ref = oracle.maxsim(qtok, cand, table, mode=oracle.F64_Q32 if split else oracle.F64)
     fin = np.isfinite(ref)
     np.testing.assert_allclose(out[fin], ref[fin], rtol=MS_RTOL, atol=1e-6)
     assert np.isneginf(out[~fin]).all()
@@ -50,7 +57,7 @@ def test_maxsim_tc_equals_cc_within_tolerance(vx, oracle):
     with vx.Index(1000, 32, tok_per_doc=Nd, tok_dim=d, tok_blocks=T, max_batch=B, max_k=C,
                   max_qtok=nq) as idx:
         idx.tokens_synth(45)
-        idx.set_option(vx.VX_OPT_MAXSIM, vx.VX_MAXSIM_TC)
+        idx.set_option(vx.VX_OPT_MAXSIM, vx.VX_MAXSIM_TC_BF16Q)  # the same bf16 query tokens
         tc = idx.maxsim(qtok, cand)
         idx.set_option(vx.VX_OPT_MAXSIM, vx.VX_MAXSIM_CC)
         cc = idx.maxsim(qtok, cand)

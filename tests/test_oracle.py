@@ -116,3 +116,67 @@ def test_percentile_reference_cases(oracle):
         r = oracle.percentile(s, p)
         rank = math.ceil(p / 100 * len(s))
         assert r in s and (s <= r).sum() >= rank and (s < r).sum() < rank
+
+
+# ---- full-size helpers (chunked generation) and the fp32-query MaxSim truth
+
+def test_flat_topk_synth_equals_whole_matrix(oracle):
+    Q = oracle.synth_rows(43, 0, 5, 256)
+    for mode in (oracle.F32, oracle.F64):
+        ids, sc, t = oracle.flat_topk_synth(42, 30_001, 256, Q, 17, mode=mode, chunk=4096)
+        wid, wsc = oracle.flat_topk(oracle.synth_rows(42, 0, 30_001, 256), Q, 17, mode=mode)
+        assert np.array_equal(ids, wid) and np.array_equal(sc, wsc) and t > 0
+    # an offset range (a shard's rows) reports global ids
+    ids, _, _ = oracle.flat_topk_synth(42, 1000, 256, Q, 5, row0=7000, chunk=300)
+    wid, _ = oracle.flat_topk(oracle.synth_rows(42, 7000, 1000, 256), Q, 5, mode=oracle.F32,
+                              id_base=7000)
+    assert np.array_equal(ids, wid)
+
+
+def test_merge_topk_orders_and_pads(oracle):
+    a_i = np.array([[5, 3, -1]]); a_s = np.array([[2.0, 1.0, -np.inf]])
+    b_i = np.array([[4, 9, -1]]); b_s = np.array([[2.0, 0.5, -np.inf]])
+    i, s = oracle.merge_topk(a_i, a_s, b_i, b_s, 5)
+    assert i.tolist() == [[4, 5, 3, 9, -1]] and s[0, :4].tolist() == [2.0, 2.0, 1.0, 0.5]
+
+
+def test_maxsim_synth_and_fp32_query_truth(oracle):
+    T, Nd, d, B, nq, C = 37, 16, 64, 3, 5, 9
+    table = oracle.synth_tokens(45, 0, T, Nd, d)
+    assert np.array_equal(oracle.synth_token_blocks(45, [4, 0, 4, 36], Nd, d), table[[4, 0, 4, 36]])
+    qt = oracle.synth_rows(44, 0, B * nq, d).reshape(B, nq, d)
+    cand = np.random.default_rng(1).integers(0, 10_000, (B, C)).astype(np.int64)
+    cand[0, 3] = -1
+    for mode in (oracle.F64, oracle.F32, oracle.F64_Q32):
+        assert np.array_equal(oracle.maxsim(qt, cand, table, mode=mode),
+                              oracle.maxsim_synth(qt, cand, 45, T, Nd, d, mode=mode))
+    # VXO_F64_Q32 = numpy fp64 of the UNROUNDED query tokens
+    want = np.empty((B, C))
+    for b in range(B):
+        for c in range(C):
+            if cand[b, c] < 0:
+                want[b, c] = -np.inf
+                continue
+            D = oracle.bf16_to_f32(table[cand[b, c] % T]).astype(np.float64)
+            want[b, c] = (qt[b].astype(np.float64) @ D.T).max(axis=1).sum()
+    got = oracle.maxsim(qt, cand, table, mode=oracle.F64_Q32)
+    fin = np.isfinite(want)
+    np.testing.assert_allclose(got[fin], want[fin], rtol=1e-12)
+    assert np.isneginf(got[~fin]).all()
+    # and it differs from the bf16-rounded-query truth by the rounding (~1e-3 relative)
+    t16 = oracle.maxsim(qt, cand, table, mode=oracle.F64)
+    assert np.abs(t16[fin] - got[fin]).max() > 1e-5
+
+
+def test_stagecheck_accepts_near_ties_and_rejects_real_swaps():
+    from stagecheck import check_stage_query
+    rid = np.array([1, 2, 3]); rip = np.array([0.9, 0.8, 0.7])
+    truth = np.array([5.0, 5.0 + 1e-7, 4.0])
+    # GPU order 1 before 2 with its own MaxSim equal -> id asc; the truth swap is a near-tie
+    r = check_stage_query(np.array([1, 2, 3]), np.float32(rip), np.array([5.0, 5.0, 4.0]), rid, rip, truth)
+    assert r["order_swaps"] == 1
+    with pytest.raises(AssertionError):  # a swap far outside the tolerance
+        check_stage_query(np.array([3, 1, 2]), np.float32(rip[[2, 0, 1]]), np.array([5.0, 4.9, 4.8]),
+                          rid, rip, np.array([5.0, 4.9, 5.0]))
+    with pytest.raises(AssertionError):  # an IP score off by one ulp
+        check_stage_query(np.array([1, 2, 3]), np.nextafter(np.float32(rip), 2), truth, rid, rip, truth)
