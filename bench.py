@@ -165,7 +165,6 @@ def parse() -> argparse.Namespace:
                     help="replay one captured CUDA graph per batch shape (single GPU)")
     ap.add_argument("--trace-s", type=float, default=0.5,
                     help="audio: seconds of Poisson arrivals per rate rung")
-    ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -243,48 +242,109 @@ class ClockSampler:
 def _oracle():
     """Test-infrastructure import, allowed for the cpu_baseline / --impl reference legs only."""
     sys.path.insert(0, str(ROOT / "oracle"))
+    sys.path.insert(0, str(ROOT / "tests"))
     import vxoracle as o
     o.build()
     return o
 
 
-def cpu_time(args, budget_s: float) -> dict:
-    """Times the oracle port (fp32 AVX-512, all host cores) on a bounded sample of the
-    workload: the scan on a row sample (scaled linearly to the full index) and the MaxSim of
-    the batch's candidates on a token-block sample."""
+def mem_available_gb() -> float:
+    try:
+        for ln in Path("/proc/meminfo").read_text().splitlines():
+            if ln.startswith("MemAvailable:"):
+                return int(ln.split()[1]) / 2**20
+    except OSError:
+        pass
+    return 0.0
+
+
+def sample_rows(B: int, S: int) -> np.ndarray:
+    """S query rows spread evenly over a batch of B (both 512-query passes of a 1024 batch)."""
+    return np.unique(np.linspace(0, B - 1, min(S, B)).round().astype(np.int64))
+
+
+def _compact_blocks(o, cand: np.ndarray, args):
+    """The token blocks a candidate list touches (doc id -> block id mod T), generated from the
+    same seed as the device store (untimed input preparation); returns (table, local ids)."""
+    T = args.tok_blocks
+    blk = np.where(cand >= 0, cand % T, 0)
+    uniq, inv = np.unique(blk, return_inverse=True)
+    table = o.synth_token_blocks(45, uniq, args.tok_per_doc, args.tok_dim)
+    return table, np.where(cand >= 0, inv.reshape(cand.shape), -1).astype(np.int64)
+
+
+def cpu_check(args, world: int, gpu: dict, timed: bool) -> tuple[dict | None, dict]:
+    """The oracle on a sample of the TIMED batch's own queries over the FULL index: checks the
+    GPU step's outputs (tests/stagecheck.py bar) and, when `timed`, times the oracle's scan and
+    MaxSim on the host cores (the cpu_baseline).  Index rows are generated chunk by chunk (the
+    10M x 768 index never exists on the host); generation is untimed input preparation, like
+    the GPU index fill."""
+    from stagecheck import check_ip_topk, check_stage
     o = _oracle()
     wl, B, D, k = args.workload, args.batch, args.dim, args.k
-    do_scan, do_ms = wl != "maxsim", wl in ("stage", "maxsim")
-    per_batch, parts = 0.0, []
-    if do_scan:
-        # ~budget seconds: scan cost ~ rows*D*B FMAs at O(3e11) FMA/s on a many-core host
-        rows = min(args.n_docs, 2_000_000, max(50_000, int(budget_s * 3e11 / (D * max(B, 16)))))
-        est = rows * D * max(B, 16) / 3e11
-        reps = max(1, min(20, int(budget_s / max(est, 1e-3))))
-        X = o.synth_rows(42, 0, rows, D)
-        Q = o.synth_rows(43, 0, B, D)
-        if est < 1.0:
-            o.flat_topk(X, Q, k, mode=1)  # warm (page-in, thread pool)
-        t0 = time.perf_counter()
-        for _ in range(reps):
-            o.flat_topk(X, Q, k, mode=1)
-        t_scan = (time.perf_counter() - t0) / reps * (args.n_docs / rows)
-        per_batch += t_scan
-        parts.append(f"scan: {rows} of {args.n_docs} rows x {D} fp32, B={B}, k={k}, {reps} reps, "
-                     f"scaled x{args.n_docs / rows:.1f} to the full index")
-    if do_ms:
-        T = min(args.tok_blocks, 4096)
-        qtok = o.synth_rows(44, 0, B * args.nq, args.tok_dim).reshape(B, args.nq, args.tok_dim)
-        table = o.synth_tokens(45, 0, T, args.tok_per_doc, args.tok_dim)
-        rng = np.random.default_rng(7)
-        cand = np.stack([rng.choice(args.n_docs, k, replace=False) for _ in range(B)]).astype(np.int64)
-        t0 = time.perf_counter()
-        o.maxsim(qtok, cand, table, mode=1)
-        per_batch += time.perf_counter() - t0
-        parts.append(f"MaxSim of {B} x {k} candidates ({args.nq}x{args.tok_per_doc}x{args.tok_dim} "
-                     f"bf16) on {T} token blocks")
-    return {"value": B / per_batch, "unit": "queries/s", "cores": o.threads(), "kind": "port",
-            "sample": "; ".join(parts), "batch_s": per_batch}
+    S = {"flat": B, "maxsim": B}.get(wl, 64)
+    sel = sample_rows(B, S)
+    t_scan = t_ms = 0.0
+    reps = 1
+    parity = {"queries_checked": int(len(sel)), "of_batch": B}
+    try:
+        if wl != "maxsim":
+            Qs = gpu["q"][sel]
+            if wl == "flat":  # 100K rows: resident; repeat the scan for a measurable time
+                X = o.synth_rows(42, 0, args.n_docs, D)
+                rid, rsc = o.flat_topk(X, Qs, k, mode=o.F32)
+                t0 = time.perf_counter()
+                while True:
+                    o.flat_topk(X, Qs, k, mode=o.F32)
+                    t_scan = time.perf_counter() - t0
+                    if t_scan > 1.0 or reps >= 200:
+                        break
+                    reps += 1
+                t_scan /= reps
+            else:
+                rid, rsc, t_scan = o.flat_topk_synth(42, args.n_docs, D, Qs, k, mode=o.F32)
+        if wl in ("stage", "maxsim"):
+            qts = gpu["qt"][sel]
+            cand = rid if wl == "stage" else gpu["cand"][sel]
+            table, local = _compact_blocks(o, cand, args)
+            t0 = time.perf_counter()
+            o.maxsim(qts, local, table, mode=o.F32)
+            t_ms = time.perf_counter() - t0
+            truth = o.maxsim(qts, local, table, mode=o.F64_Q32)
+        if wl == "stage":
+            r = check_stage(gpu["ids"][sel], gpu["ip"][sel], gpu["ms"][sel], rid, rsc, truth)
+            parity.update(r)
+            parity["bar"] = ("IP ids + scores bit-equal to the oracle's in-order fp32 chains; MaxSim "
+                             "<= 1e-5 rel (+1e-6) of the fp64 MaxSim of the fp32 query tokens; order "
+                             "(MaxSim desc, id asc) equal to the oracle's except within-tolerance swaps")
+        elif wl == "maxsim":
+            err = np.abs(gpu["ms"][sel].astype(np.float64) - truth)
+            assert (err <= 1e-5 * np.abs(truth) + 1e-6).all(), float(err.max())
+            parity.update({"ms_max_abs_err": float(err.max()),
+                           "ms_max_rel_err": float((err / np.abs(truth)).max()),
+                           "bar": "<= 1e-5 rel (+1e-6) of the fp64 MaxSim of the fp32 query tokens"})
+        else:
+            for j, b in enumerate(sel):
+                check_ip_topk(gpu["ids"][b], gpu["ip"][b], rid[j], rsc[j])
+                assert np.array_equal(gpu["ids"][b], rid[j])  # order too: (score desc, id asc)
+            parity["bar"] = "ids (in order) + scores bit-equal to the oracle's in-order fp32 chains"
+        parity["ok"] = True
+    except AssertionError as e:
+        parity.update({"ok": False, "error": repr(e)[:300]})
+    cpu = None
+    if timed:
+        parts = []
+        if wl != "maxsim":
+            parts.append(f"scan of {len(sel)} of the batch's {B} queries over all {args.n_docs} rows "
+                         f"x {D} fp32, k={k}" + (f" ({reps} reps)" if reps > 1 else ""))
+        if wl in ("stage", "maxsim"):
+            parts.append(f"MaxSim of their {k if wl == 'stage' else gpu['cand'].shape[1]} candidates "
+                         f"({args.nq}x{args.tok_per_doc}x{args.tok_dim}, bf16 doc tokens, "
+                         f"{table.shape[0]} distinct blocks of the {args.tok_blocks}-block store)")
+        cpu = {"value": len(sel) / (t_scan + t_ms), "unit": "queries/s", "cores": o.threads(),
+               "kind": "port", "sample": "; ".join(parts) + " — the queries the GPU step was checked on",
+               "batch_s": (t_scan + t_ms) * B / len(sel)}
+    return cpu, parity
 
 
 # ----------------------------------------------------------------------------- rooflines
@@ -513,6 +573,13 @@ def run_ours(args) -> None:
     with ClockSampler(local) as clk:  # sampling spans the timed phase (started before its barrier)
         result = phase(timed)
     result["clocks"] = clk.summary()
+    # the timed batch's outputs, for the oracle check after the e2e leg (rank 0)
+    gpu_out = None
+    if rank == 0:
+        gpu_out = {"q": q_h, "qt": qt_h, "cand": cand_h,
+                   "ids": ids.cpu().numpy() if wl != "maxsim" else None,
+                   "ip": ip.cpu().numpy() if wl != "maxsim" else None,
+                   "ms": msc.cpu().numpy() if tokens else None}
     # max over ranks of the timed span (rank 0: CUDA events; shard servers: their serve span)
     max_ms = result["span_ms"]
     if world > 1:
@@ -570,28 +637,27 @@ def run_ours(args) -> None:
         roof.update({"kernel": kernel_name, "scan_ms": scan_ms,
                      "traffic": trec["dram_bytes"] if trec else None,
                      "traffic_src": trec["source"] if trec else None})
-    cpu = None
+    cpu, parity = None, None
     if not args.no_cpu_baseline:
-        c = cpu_time(args, args.cpu_budget_s)
-        cpu = {k_: c[k_] for k_ in ("value", "unit", "cores", "kind", "sample")}
-    cfg = {"workload": workload_name(args), "baseline_config": WORKLOADS[wl][0],
-           "n_docs": args.n_docs, "dim": D, "batch": B, "k": k,
-           "shards": world if sharded else 1, "replicas": replicas,
-           "scan": args.scan, "coarse": coarse}
-    if tokens:
-        cfg.update({"q_tokens": nq, "doc_tokens": args.tok_per_doc, "tok_dim": td,
-                    "tok_blocks": args.tok_blocks})
-    cfg["l2"] = ("256 MB buffer written between timed steps (untimed); value = sum of per-step event times"
-                 if flush_l2 else "index (GB) >> 126 MB L2: every step streams from HBM")
-    cfg["exactness"] = ("MaxSim: fp32 sums of bf16 products, bit-identical to the oracle" if wl == "maxsim"
-                        else "ids+scores bit-identical to the fp32 oracle (certified re-rank)")
+        # cpu_baseline (N = 1 only: rank 0's host cores) and, at every N, the oracle check of
+        # the timed batch's own outputs over the full index
+        c, parity = cpu_check(args, world, gpu_out, timed=world == 1)
+        if c:
+            cpu = {k_: c[k_] for k_ in ("value", "unit", "cores", "kind", "sample")}
+    cfg = config_of(args, world)
+    path = {"scan": "tc" if tc else "f32", "coarse": coarse,
+            "maxsim": ("tcgen05 kind::f16, fp32 query tokens as bf16 hi+lo (nq <= 64)"
+                       if tokens else None)}
     out = {
         "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "p99_batch_ms": p99,
         "mean_batch_ms": mean_step,
         "slo_ms": args.slo_ms, "slo_met": p99 <= args.slo_ms, "higher_is_better": True,
         "scaling": "strong" if sharded or world == 1 else "weak", "vs_baseline": None,
-        "dtype": "f32", "data": "synthetic", "config": cfg,
+        "dtype": "f32", "data": "synthetic", "config": cfg, "path": path,
+        "exactness": (("checked: " if parity.get("ok") else "CHECK FAILED: ") + parity["bar"]
+                      if parity else "not checked (--no-cpu-baseline)"),
+        "parity": parity,
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": int(st["kernel_launches"]),
         "cert_fallbacks": int(st["cert_fallbacks"]), "cert_level2": int(st["cert_level2"]),
@@ -628,25 +694,82 @@ def run_ours(args) -> None:
 
 
 def run_reference(args) -> None:
+    """The reference arm: the CPU oracle port of the stage (the reference has no retrieval
+    arithmetic of its own — its search stage is a profiled latency, profiles.csv:17-22) on
+    this host's cores, all threads.  Each step = S of the batch's queries over the FULL index
+    (resident in host memory when it fits, else generated chunk-wise with only the scan timed)
+    + MaxSim of their top-k on the token store; exactly `steps` timed steps after `warmup`."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    c = cpu_time(args, args.cpu_budget_s)
+    o = _oracle()
+    wl, B, D, k = args.workload, args.batch, args.dim, args.k
+    S = min(B, {"flat": B, "maxsim": B, "audio": 32}.get(wl, 16))
+    from paper_2511_02062_b200 import synth  # pure-numpy generator (no GPU library call)
+    Qall = synth.queries(B, D, seed=43) if wl != "maxsim" else None
+    QT = synth.query_tokens(B, args.nq, args.tok_dim) if wl in ("stage", "maxsim") else None
+    rng = np.random.default_rng(7)
+    CAND = (np.stack([rng.choice(args.n_docs, k, replace=False) for _ in range(B)]).astype(np.int64)
+            if wl == "maxsim" else None)
+    need_gb = args.n_docs * D * 4 / 2**30 if wl != "maxsim" else 0.0
+    resident = need_gb < 0.6 * mem_available_gb()
+    X = o.synth_rows(42, 0, args.n_docs, D) if (resident and wl != "maxsim") else None
+    steps_t = []
+    for step in range(args.warmup + args.steps):
+        sel = (np.arange(S) + step * S) % B  # walk through the batch
+        t = 0.0
+        if wl != "maxsim":
+            if X is not None:
+                t0 = time.perf_counter()
+                rid, _ = o.flat_topk(X, Qall[sel], k, mode=o.F32)
+                t += time.perf_counter() - t0
+            else:
+                rid, _, ts = o.flat_topk_synth(42, args.n_docs, D, Qall[sel], k, mode=o.F32)
+                t += ts
+        if wl in ("stage", "maxsim"):
+            cand = rid if wl == "stage" else CAND[sel]
+            table, local = _compact_blocks(o, cand, args)
+            t0 = time.perf_counter()
+            o.maxsim(QT[sel], local, table, mode=o.F32)
+            t += time.perf_counter() - t0
+        if step >= args.warmup:
+            steps_t.append(t)
+    step_s = sum(steps_t) / len(steps_t)
+    value = S / step_s
     out = {
-        "metric": METRIC, "impl": "reference", "value": c["value"], "unit": "queries/s",
+        "metric": METRIC, "impl": "reference", "value": value, "unit": "queries/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": c["batch_s"] * 1e3, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": step_s * 1e3, "higher_is_better": True,
+        "scaling": "strong" if wl in ("stage", "flat", "search") else "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": workload_name(args), "baseline_config": WORKLOADS[args.workload][0],
-                   "n_docs": args.n_docs, "dim": args.dim, "batch": args.batch, "k": args.k},
-        "cpu_baseline": {k_: c[k_] for k_ in ("value", "unit", "cores", "kind", "sample")},
-        "e2e": {"value": c["value"], "unit": "queries/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
+        "config": config_of(args, args.gpus),
+        "sample_fraction": S / B,
+        "cpu_baseline": {"value": value, "unit": "queries/s", "cores": o.threads(), "kind": "port",
+                         "sample": (f"each step: {S} of the {B}-query batch over all {args.n_docs} rows x "
+                                    f"{D} fp32 (index {'resident in host memory' if X is not None else 'generated chunk-wise, scan timed'})"
+                                    + (f" + MaxSim of their top-{k} ({args.nq}x{args.tok_per_doc}x"
+                                       f"{args.tok_dim}, bf16 doc tokens)" if wl in ("stage", "maxsim") else ""))},
+        "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": ("the reference contains no retrieval arithmetic (its search stage is a profiled "
                  "latency, proj/assets/profiles.csv:17-22); this arm times the oracle port of the "
-                 "stage on the host cores, each step a bounded sample scaled to the full index"),
+                 "stage (fp32 AVX-512, in-order chains, all host threads) on the same workload"),
     }
     print(json.dumps(out), flush=True)
+
+
+def config_of(args, world: int) -> dict:
+    """The workload description both arms print (identical keys and values for one command)."""
+    wl = args.workload
+    sharded = wl in ("stage", "flat", "search") and world > 1
+    cfg = {"workload": workload_name(args), "baseline_config": WORKLOADS[wl][0],
+           "n_docs": args.n_docs, "dim": args.dim, "batch": args.batch, "k": args.k,
+           "shards": world if sharded else 1, "replicas": 1 if sharded else world}
+    if wl in ("stage", "maxsim"):
+        cfg.update({"q_tokens": args.nq, "doc_tokens": args.tok_per_doc, "tok_dim": args.tok_dim,
+                    "tok_blocks": args.tok_blocks})
+    cfg["l2"] = ("256 MB buffer written between timed steps (untimed); value = sum of per-step event times"
+                 if wl in ("flat", "maxsim") else "index (GB) >> 126 MB L2: every step streams from HBM")
+    return cfg
 
 
 def main() -> None:
