@@ -279,8 +279,8 @@ def cpu_check(args, world: int, gpu: dict, timed: bool) -> tuple[dict | None, di
     MaxSim on the host cores (the cpu_baseline).  Index rows are generated chunk by chunk (the
     10M x 768 index never exists on the host); generation is untimed input preparation, like
     the GPU index fill."""
+    o = _oracle()  # (also puts tests/ on the path for the checker)
     from stagecheck import check_ip_topk, check_stage
-    o = _oracle()
     wl, B, D, k = args.workload, args.batch, args.dim, args.k
     S = {"flat": B, "maxsim": B}.get(wl, 64)
     sel = sample_rows(B, S)

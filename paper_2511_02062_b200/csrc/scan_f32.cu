@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(kScanThreads, 1)
   X(2, 1, 2, 1)            \
   X(4, 2, 2, 1)            \
   X(8, 4, 2, 1)            \
-  X(16, 4, 4, 2)           \
+  X(16, 4, 4, 4)           \
   X(32, 8, 4, 2)
 
 int scan_f32_bucket(int B) {
