@@ -487,6 +487,9 @@ def run_ours(args) -> None:
         return {}
 
     def timed():
+        # every step is enqueued without a host round trip in between (the host runs ahead, as
+        # a serving loop does), so the event pairs see device time only; the kernels time
+        # themselves on the device (vx_stats.kt_*: every launch, inside the graphs)
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(args.steps)]
         for a, b in evs:
@@ -495,9 +498,8 @@ def run_ours(args) -> None:
             a.record(stream)
             step()
             b.record(stream)
-            b.synchronize()
-            idx.sync()  # samples the scan / stage device times of this batch
         torch.cuda.synchronize(dev)
+        idx.sync()
         lat = [a.elapsed_time(b) for a, b in evs]
         span = sum(lat) if l2buf is not None else evs[0][0].elapsed_time(evs[-1][1])
         return {"lat": lat, "span_ms": span, "stats": idx.stats()}
@@ -615,14 +617,38 @@ def run_ours(args) -> None:
     tc = args.scan == "tc" or (args.scan == "auto" and k <= 128)
     coarse = (args.coarse if args.coarse != "auto" else idx.coarse_auto()) if tc else None
     bf16 = coarse == "bf16"
+    def kt(i):  # device-side launch timer i: (launches, mean launch ms, SM MHz in-kernel)
+        n = int(st["kt_launches"][i])
+        return n, (st["kt_ms"][i] / n if n else None), (st["kt_sm_mhz"][i] or None)
     if wl == "maxsim":
-        roof = maxsim_roofline(pk, B=B, C=C, nq=nq, nd=args.tok_per_doc, d=td, ms=mean_step)
+        n_ms, ms_launch, ms_mhz = kt(3)
+        kms = ms_launch if ms_launch else mean_step
+        roof = maxsim_roofline(pk, B=B, C=C, nq=nq, nd=args.tok_per_doc, d=td, ms=kms)
         kernel_name = "maxsim_tc_kernel (K4, tcgen05 kind::f16, fused row-max + sum)"
-        roof.update({"kernel": kernel_name, "kernel_ms": mean_step, "traffic": None})
+        roof.update({"kernel": kernel_name, "kernel_ms": kms, "kernel_launches": n_ms,
+                     "kernel_sm_mhz": ms_mhz, "traffic": None,
+                     "timing": "device-side per-launch timer (first CTA start -> last CTA end)"})
     else:
-        scan_ms = st["scan_ms_total"] / max(1, st["timed_batches"])
+        n_sc, sc_launch, sc_mhz = kt(0 if tc else 2)
+        # per batch: the summed device time of its scan launches over the timed steps
+        scan_ms = (st["kt_ms"][0 if tc else 2] / args.steps if sc_launch
+                   else st["scan_ms_total"] / max(1, st["timed_batches"]))
         roof = scan_roofline(pk, tc=tc, coarse=coarse, n_local=n_local, D=D, B=B, k=k,
                              scan_ms=scan_ms, pairs=args.pairs)
+        roof["timing"] = ("device-side per-launch timer over every timed launch (first CTA start -> "
+                          "last CTA end, %globaltimer)" if sc_launch else "CUDA events")
+        roof["kernel_launches"] = n_sc
+        roof["kernel_sm_mhz"] = sc_mhz
+        if tc and sc_mhz:
+            # the tensor pipe's own ceiling at the clock the kernel ran at (tcgen05: 8192 bf16 /
+            # 16384 s8 / 4096 tf32 MACs x2 per SM per cycle, profiles/r01/microbench_mma_rate*.log)
+            per_clk = {"bf16": 8192, "i8": 16384, "tf32": 4096}[coarse] * 148
+            roof["compute"]["peak_at_kernel_clock"] = per_clk * sc_mhz * 1e6 / 1e12
+            roof["compute"]["frac_at_kernel_clock"] = (roof["compute"]["achieved"] /
+                                                       roof["compute"]["peak_at_kernel_clock"])
+        n_smp, smp_launch, _ = kt(1)
+        if n_smp:
+            roof["sample_pass_ms"] = smp_launch
         kinds = {"bf16": "kind::f16 on the bf16 shadow", "tf32": "kind::tf32",
                  "i8": "kind::i8 on the s8 shadow"}
         kernel_name = ((f"scan_tc{'2' if tc and B > 128 and args.pairs != 0 else ''}_kernel (K2, "

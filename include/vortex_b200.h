@@ -127,6 +127,13 @@ typedef struct vx_stats {
   uint64_t host_staged_bytes; /* host-buffer API: bytes memcpy'd through the handle's pinned
                                  staging (0 when every caller buffer was page-locked and DMA'd
                                  directly) */
+  /* Device-side kernel timing (every launch, inside CUDA graphs, no host sync): [0] the
+   * tensor-core scan passes, [1] the seeded sample pass, [2] the exact K1 scan, [3] MaxSim.
+   * Duration = first CTA start -> last CTA end (%globaltimer); SM clock = CTA 0's clock64()
+   * cycles over its %globaltimer span. */
+  uint64_t kt_launches[4];
+  double kt_ms[4];            /* summed durations */
+  double kt_sm_mhz[4];        /* mean SM clock during those launches */
 } vx_stats;
 
 int32_t vx_abi_version(void);

@@ -47,7 +47,8 @@ class Stats(C.Structure):
                 ("last_scan_ms", C.c_float), ("last_step_ms", C.c_float),
                 ("scan_ms_total", C.c_double), ("step_ms_total", C.c_double),
                 ("timed_batches", C.c_uint64), ("phase_ms", C.c_float * 4),
-                ("cert_level2", C.c_uint64), ("host_staged_bytes", C.c_uint64)]
+                ("cert_level2", C.c_uint64), ("host_staged_bytes", C.c_uint64),
+                ("kt_launches", C.c_uint64 * 4), ("kt_ms", C.c_double * 4), ("kt_sm_mhz", C.c_double * 4)]
 
 
 P = C.c_void_p

@@ -62,6 +62,8 @@ __global__ void __launch_bounds__(kMsThreads, 2)
   const int c1 = min(a.C, c0 + chunk);
   const int nq = a.nq;
   const int64_t* cand = a.cand + (size_t)b * a.C;
+  uint64_t kt_c0 = 0, kt_g0 = 0;
+  ktimer_begin(a.ktimer, kt_c0, kt_g0);
   // candidates another shard owns (or none, id < 0) are skipped by every role: no loads,
   // no MMA, the epilogue writes -INF; the ring advances only over owned candidates
   auto owned = [&](int c) {
@@ -239,6 +241,7 @@ __global__ void __launch_bounds__(kMsThreads, 2)
   }
   tc_fence_before();
   __syncthreads();
+  ktimer_end(a.ktimer, kt_c0, kt_g0);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, C::kTmemCols);

@@ -100,6 +100,8 @@ __global__ void __launch_bounds__(kScanThreads, 1)
     if (nBtot <= 0) return;
   }
   const int ngroups = (nBtot + BQ - 1) / BQ;
+  uint64_t kt_c0 = 0, kt_g0 = 0;
+  ktimer_begin(a.ktimer, kt_c0, kt_g0);  // (a.ktimer is null for device-count launches)
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmap);
@@ -251,6 +253,7 @@ __global__ void __launch_bounds__(kScanThreads, 1)
   }
   named_bar_sync(1, kCT);  // the next group reuses q_s / cand / thr / cnt
   }
+  ktimer_end(a.ktimer, kt_c0, kt_g0);  // thread 0 is a compute thread (the producer returned)
 }
 
 // ---------------------------------------------------------------- host side

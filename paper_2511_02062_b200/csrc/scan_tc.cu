@@ -62,6 +62,8 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
   const int nch = a.D / cw;
   const uint32_t n_local = a.n_local;
   const int ntiles = (int)((n_local + TD - 1) / TD);
+  uint64_t kt_c0 = 0, kt_g0 = 0;
+  ktimer_begin(a.ktimer, kt_c0, kt_g0);
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tq);
@@ -87,7 +89,7 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
     if (lane == 0) {
       const uint64_t pol_x = policy_evict_first();
       const uint64_t pol_q = policy_evict_last();
-      const uint32_t bytes = (uint32_t)(QT * a.a_rows * 128 + TD * 128);
+      const uint32_t bytes = (uint32_t)(QT * a.rep * a.a_rows * 128 + TD * 128);
       int s = 0;
       uint32_t ph = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -98,6 +100,10 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
 #pragma unroll
           for (int qt = 0; qt < QT; ++qt)
             tma_load_2d(st + qt * kTcStageUnit, &tq, &full[s], c * cw, qt * 128, pol_q);
+          // replicated small batch (QT = 1): the same a_rows query rows again at row offsets
+          // r a_rows (the SW128 swizzle is address-based, so every copy is laid out alike)
+          for (int r = 1; r < a.rep; ++r)
+            tma_load_2d(st + r * a.a_rows * 128, &tq, &full[s], c * cw, 0, pol_q);
 #pragma unroll
           for (int h = 0; h < TD; h += 128)  // the document map's box is 128 rows
             tma_load_2d(st + QT * kTcStageUnit + h * 128, &tx, &full[s], c * cw, tile * TD + h,
@@ -176,10 +182,16 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
     for (int t = 0; t < C::QPT; ++t)
 #pragma unroll
       for (int j = 0; j < KC; ++j) L[t][j] = 0ull;
+    // replicated small batch (rep > 1, QT = 1, TD = 256): row m holds query m % a_rows, its
+    // replica m / a_rows selects over columns [replica TD/rep, +TD/rep).  a_rows >= 32: one
+    // replica per warp; a_rows = 16: two per warp (lane halves), one 64-column load.
+    const int rep = QT == 1 && TD == 256 ? a.rep : 1;
+    const int qrow = rep > 1 ? m % a.a_rows : m;
+    const int repl = rep > 1 ? m / a.a_rows : 0;
     float thr[C::QPT];
 #pragma unroll
     for (int t = 0; t < C::QPT; ++t) {
-      const int q = (g + t * C::EG) * 128 + m;
+      const int q = (g + t * C::EG) * 128 + qrow;
       thr[t] = q < a.B ? seed_thr(a.seed, a.seed_ld, q) : -INFINITY;
     }
     int buf = 0;
@@ -187,6 +199,43 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       mbar_wait(&tfull[buf], bph);
       tc_fence_after();
+      if (rep > 1) {
+        const int q = qrow;
+        const uint32_t colq = tmem_base + (uint32_t)(buf * TD) + ((uint32_t)(quad * 32) << 16);
+        if (a.a_rows == 16) {
+          // warp = replicas 2 quad, 2 quad + 1 (32 columns each): one 64-column load
+          uint32_t r[64];
+          tmem_ld64(colq + quad * 64, r);
+          tmem_ld_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[buf]);
+          const int half = lane >> 4;
+          uint32_t v[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = half ? r[32 + i] : r[i];
+          if (q < a.B && !(a.dbg_no_select & 1))
+            admit<FMT, KC, 32>(v, (uint32_t)tile * TD + quad * 64 + half * 32, n_local, scratch,
+                               NEPI, L[0], thr[0]);
+        } else {
+          const int cr = TD / rep;  // 64 (rep 4) or 128 (rep 2) columns per replica
+#pragma unroll 1
+          for (int cc = 0; cc < cr / 64; ++cc) {
+            uint32_t r[64];
+            tmem_ld64(colq + repl * cr + cc * 64, r);
+            tmem_ld_wait();
+            if (cc == cr / 64 - 1) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&tempty[buf]);
+            }
+            if (q >= a.B || (a.dbg_no_select & 1)) continue;
+            const uint32_t doc0 = (uint32_t)tile * TD + repl * cr + cc * 64;
+            admit<FMT, KC, 32>(r, doc0, n_local, scratch, NEPI, L[0], thr[0]);
+            admit<FMT, KC, 32>(r + 32, doc0 + 32, n_local, scratch, NEPI, L[0], thr[0]);
+          }
+        }
+      } else {
 #pragma unroll
       for (int t = 0; t < C::QPT; ++t) {
         const int qt = g + t * C::EG;
@@ -210,11 +259,45 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
           admit<FMT, KC, 32>(r + 32, doc0 + 32, n_local, scratch, NEPI, L[t], thr[t]);
         }
       }
+      }
       if (++buf == C::NBUF) {
         buf = 0;
         bph ^= 1;
       }
     }
+    if (rep > 1) {
+      // merge each query's rep replica lists into ONE per-CTA list: its KC-th key is >= every
+      // replica's KC-th key, so "every document of this CTA outside the list has key <= the
+      // list's last key" still holds (certificate 1).  Buffer: the operand ring, idle now
+      // (the last tile's MMAs completed before its tfull arrive).
+      uint64_t* mb = reinterpret_cast<uint64_t*>(smem);  // [128][KC]
+#pragma unroll
+      for (int j = 0; j < KC; ++j) mb[m * KC + j] = L[0][j];
+      named_bar_sync(1, 128);
+      if (m < a.a_rows && m < a.B) {
+        int pos[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) pos[r] = 0;
+        uint64_t* out = a.part + ((size_t)m * gridDim.x + blockIdx.x) * KC;
+        for (int j = 0; j < KC; ++j) {
+          uint64_t best = 0ull;
+          int br = 0;
+#pragma unroll
+          for (int r = 0; r < 8; ++r) {
+            if (r >= rep || pos[r] >= KC) continue;
+            const uint64_t k_ = mb[(r * a.a_rows + m) * KC + pos[r]];
+            if (k_ > best) {
+              best = k_;
+              br = r;
+            }
+          }
+#pragma unroll
+          for (int r = 0; r < 8; ++r)
+            if (r == br && best != 0ull) ++pos[r];
+          out[j] = best;
+        }
+      }
+    } else {
 #pragma unroll
     for (int t = 0; t < C::QPT; ++t) {
       const int qt = g + t * C::EG;
@@ -225,9 +308,11 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
         for (int j = 0; j < KC; ++j) out[j] = L[t][j];
       }
     }
+    }
   }
   tc_fence_before();
   __syncthreads();
+  ktimer_end(a.ktimer, kt_c0, kt_g0);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, C::kTmemCols);
@@ -317,7 +402,8 @@ __global__ void __launch_bounds__(256)
                   uint64_t* __restrict__ out_keys, int64_t* __restrict__ out_ids,
                   float* __restrict__ out_scores, int* __restrict__ flags, int rows_per_round,
                   int dchunk, int phase, const float* __restrict__ tau, uint64_t* __restrict__ hkeys,
-                  float* __restrict__ lb, const uint64_t* __restrict__ seed, int seed_ld) {
+                  float* __restrict__ lb, const uint64_t* __restrict__ seed, int seed_ld,
+                  int head_all) {
   extern __shared__ __align__(16) float rsm[];
   float* qs = rsm;                                             // [D]
   uint64_t* keys = reinterpret_cast<uint64_t*>(rsm + ((D + 3) & ~3));  // [kp]
@@ -344,7 +430,9 @@ __global__ void __launch_bounds__(256)
   const float E = cert_err_bound(fmt, D, qn, qh, qr, xstats);
   const uint64_t* cb = cand + (size_t)b * kp;
   const uint64_t tprime = cb[kp - 1];  // coarse k'-th key (0: fewer than k' candidates)
-  const int kh = k < kp ? k : kp;      // head rows
+  // head rows; head_all (small batch, latency-bound: the pruning saves bytes nobody waits
+  // for, and a second gather round costs its full latency) re-scores all k' in one round
+  const int kh = head_all ? kp : (k < kp ? k : kp);
   // The candidate rows are random 3 KB gathers from HBM (DRAM-page unfriendly); per-thread
   // loads left too few bytes in flight (measured 85 us at B=128).  Instead each round stages
   // R rows into smem with one TMA bulk copy per row (R x 3 KB in flight per SM), then R
@@ -816,9 +904,10 @@ cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64
   cudaError_t e = cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
+  const int head_all = phase == 0 && B <= 64 ? 1 : 0;
   rerank_kernel<<<B, 256, smem, st>>>(docs, q, D, cand, kp, part, grid, ldlists, kc, k, row0,
                                       xstats, fmt, qscale, out_keys, out_ids, out_scores, flags, R,
-                                      DC, phase, tau, hkeys, lb, seed, seed_ld);
+                                      DC, phase, tau, hkeys, lb, seed, seed_ld, head_all);
   return cudaGetLastError();
 }
 

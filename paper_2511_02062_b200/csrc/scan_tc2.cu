@@ -88,6 +88,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P2Cfg<QG>::kThreads,
   const int nch = a.D / cw;
   const uint32_t n_local = a.n_local;
   const int ntiles = (int)((n_local + TD - 1) / TD);
+  uint64_t kt_c0 = 0, kt_g0 = 0;
+  ktimer_begin(a.ktimer, kt_c0, kt_g0);
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tq);
@@ -270,6 +272,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P2Cfg<QG>::kThreads,
   }
   tc_fence_before();
   cluster_sync();  // both CTAs done with TMEM and with each other's barriers
+  ktimer_end(a.ktimer, kt_c0, kt_g0);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc_pair(tmem_base, C::kCols);

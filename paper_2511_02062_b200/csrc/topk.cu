@@ -3,7 +3,9 @@
 //
 // One CTA per query.  MSB-first radix select over the u64 keys (8-bit digits,
 // histogram in smem) narrows to the bin holding the k-th key — usually 2-3 passes
-// over the M = P*kcap candidates, which are L2-resident — then one collection
+// over the M = P*kcap candidates, staged once into smem (M <= kMergeSmemKeys: every pass
+// re-reading them from L2 made each pass a chain of dependent ~0.5 us loads — 14-18 us per
+// merge at B = 16, where a few CTAs run alone) — then one collection
 // pass gathers exactly k keys and a block bitonic sort orders them
 // (score desc, id asc; the key encodes both, vx_synth.h vx_make_key).
 // Padding keys (0) rank below every real key and come out as id -1 / -INF.
@@ -17,6 +19,7 @@ namespace vx {
 
 constexpr int kMergeThreads = 256;
 constexpr int kMaxK = 1024;  // merge: k' up to 1024 (the TC candidate set); order_by: k <= 256
+constexpr int kMergeSmemKeys = 12288;  // 96 KB of dynamic smem
 
 __device__ __forceinline__ void block_bitonic_desc(uint64_t* buf, int n) {
   for (int size = 2; size <= n; size <<= 1) {
@@ -42,12 +45,24 @@ __global__ void __launch_bounds__(kMergeThreads)
                       float* __restrict__ out_scores, const int* __restrict__ d_count,
                       int64_t ldout) {
   if (d_count && (int)blockIdx.x >= *d_count) return;  // device-sized batch (cert fallback)
+  extern __shared__ uint64_t staged[];  // [M] when launched with M * 8 bytes of dynamic smem
   __shared__ uint32_t hist[256];
   __shared__ uint64_t s_prefix, s_mask;
   __shared__ int s_kk, s_done, s_above, s_eq;
   __shared__ uint64_t sel[kMaxK];
   const uint64_t* L = in + (size_t)blockIdx.x * ldin;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (M <= kMergeSmemKeys && (M & 1) == 0) {  // stage (16-byte loads, all in flight)
+    const uint4* src = reinterpret_cast<const uint4*>(L);
+    uint4* dst = reinterpret_cast<uint4*>(staged);
+    if ((reinterpret_cast<uintptr_t>(L) & 15) == 0) {
+      for (int i = threadIdx.x; i < (M >> 1); i += blockDim.x) dst[i] = src[i];
+    } else {
+      for (int i = threadIdx.x; i < M; i += blockDim.x) staged[i] = L[i];
+    }
+    __syncthreads();
+    L = staged;
+  }
 
   uint64_t prefix = 0, mask = 0;
   int kk = k;
@@ -164,7 +179,17 @@ cudaError_t launch_merge_topk(const uint64_t* in, int B, int M, int k, int64_t i
                               cudaStream_t st, const int* d_count, int64_t ldin,
                               int64_t ldout) {
   if (k < 1 || k > kMaxK || M < k) return cudaErrorInvalidValue;
-  merge_topk_kernel<<<B, kMergeThreads, 0, st>>>(in, M, ldin > 0 ? ldin : M, k, id_base,
+  const size_t smem = (M <= kMergeSmemKeys && (M & 1) == 0) ? (size_t)M * 8 : 0;
+  static bool attr[64] = {};  // once per device: the largest staging size
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !attr[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(merge_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kMergeSmemKeys * 8);
+    if (e != cudaSuccess) return e;
+    if (dev >= 0 && dev < 64) attr[dev] = true;
+  }
+  merge_topk_kernel<<<B, kMergeThreads, smem, st>>>(in, M, ldin > 0 ? ldin : M, k, id_base,
                                                  out_keys, out_ids, out_scores, d_count,
                                                  ldout > 0 ? ldout : k);
   return cudaGetLastError();
@@ -237,7 +262,8 @@ namespace vx {
 // whole stage can live in one CUDA graph)
 __global__ void __launch_bounds__(1024)
     cert_compact_kernel(const int* __restrict__ flags, int B, const float* __restrict__ q, int D,
-                        int* __restrict__ fidx, int* __restrict__ fcount, float* __restrict__ fq) {
+                        int* __restrict__ fidx, int* __restrict__ fcount, float* __restrict__ fq,
+                        cudaGraphConditionalHandle cond, int use_cond) {
   // stream compaction of the flagged queries (ascending order), 1024 flags per round:
   // warp ballots + a prefix over the 32 warp counts
   __shared__ int s_warp[32];
@@ -272,6 +298,9 @@ __global__ void __launch_bounds__(1024)
   if (threadIdx.x == 0) {
     fcount[0] = n;   // this batch
     fcount[1] += n;  // running total (vx_stats.cert_fallbacks)
+    // captured stage: the rest of the certificate chain is the body of a conditional graph
+    // node that runs only when some query failed (vx_stage.cu local_topk_tc)
+    if (use_cond) cudaGraphSetConditional(cond, n > 0 ? 1u : 0u);
   }
   __threadfence_block();
   __syncthreads();
@@ -297,8 +326,10 @@ __global__ void cert_scatter_kernel(const int* __restrict__ fidx, const int* __r
 }
 
 cudaError_t launch_cert_compact(const int* flags, int B, const float* q, int D, int* fidx,
-                                int* fcount, float* fq, cudaStream_t st) {
-  cert_compact_kernel<<<1, 1024, 0, st>>>(flags, B, q, D, fidx, fcount, fq);
+                                int* fcount, float* fq, cudaStream_t st, unsigned long long cond,
+                                int use_cond) {
+  cert_compact_kernel<<<1, 1024, 0, st>>>(flags, B, q, D, fidx, fcount, fq,
+                                          (cudaGraphConditionalHandle)cond, use_cond);
   return cudaGetLastError();
 }
 

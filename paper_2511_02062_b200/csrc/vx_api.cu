@@ -139,6 +139,7 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
   };
   if (const char* e = getenv("VX_DEBUG_TC_NOSELECT")) h->dbg_tc_bits = atoi(e);
   if (const char* e = getenv("VX_DEBUG_TC_STAGES")) h->dbg_tc_stages = atoi(e);
+  if (const char* e = getenv("VX_DEBUG_NO_REP")) h->dbg_no_rep = atoi(e);
   if (const char* e = getenv("VX_DEBUG_SEED_M")) h->dbg_seed_m = std::min(32, std::max(1, atoi(e)));
   if (cudaSetDevice(h->device) != cudaSuccess) return cleanup(fail(VX_ERR_CUDA, "cudaSetDevice"));
   if (h->n_local < 1) return cleanup(fail(VX_ERR_INVALID, "empty shard"));
@@ -182,6 +183,7 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
   ALLOC(h->d_fq, B * D * 4);
   ALLOC(h->d_fidx, B * 4);
   ALLOC(h->d_fcount, 16);
+  ALLOC(h->d_ktimer, sizeof(vx::KTimer) * vx::KT_N);
   // bf16 shadow for the coarse scan: K-chunks of 64 bf16 (one 128-byte swizzle atom), so
   // D % 64 == 0; otherwise the coarse scan reads the fp32 rows as TF32 (32-wide chunks)
   if (!(d->flags & VX_FLAG_NO_BF16_SHADOW) && D % 64 == 0) {
@@ -197,6 +199,7 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
 #undef ALLOC
   if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&h->stream_cond, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->tok_ev, cudaEventDisableTiming) != cudaSuccess)
     return cleanup(fail(VX_ERR_CUDA, "stream create"));
   for (auto& e : h->ev)
@@ -213,7 +216,8 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
     return cleanup(fail(VX_ERR_OOM, "pinned header"));
   if (cudaMallocHost((void**)&h->h_flags, B * 4) != cudaSuccess)
     return cleanup(fail(VX_ERR_OOM, "pinned flags"));
-  if (cudaMemset(h->d_xnorm, 0, 32) != cudaSuccess || cudaMemset(h->d_fcount, 0, 16) != cudaSuccess)
+  if (cudaMemset(h->d_xnorm, 0, 32) != cudaSuccess || cudaMemset(h->d_fcount, 0, 16) != cudaSuccess ||
+      ktimer_reset(h) != VX_OK)
     return cleanup(fail(VX_ERR_CUDA, "memset"));
   if (h->tokens) {
     s = make_tmap_2d(&h->tmap_tok, h->tokens, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
@@ -251,7 +255,8 @@ extern "C" vx_status vx_index_destroy(vx_index* h) {
                   h->d_ids, h->d_ip,      h->d_ms,     h->d_out_ids, h->d_out_ip,
                   h->d_out_ms, h->d_send, h->d_recv, h->d_hdr, h->d_ckeys, h->d_seedk, h->d_flags,
                   h->d_xnorm, h->d_fq, h->docs16, h->d_q16, h->d_fidx, h->d_fcount,
-                  h->d_qtok16, h->docs8, h->d_q8, h->d_qs8, h->d_lball, h->d_tau, h->d_hkeys};
+                  h->d_qtok16, h->docs8, h->d_q8, h->d_qs8, h->d_lball, h->d_tau, h->d_hkeys,
+                  h->d_ktimer};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->h_stage) cudaFreeHost(h->h_stage);
@@ -265,6 +270,7 @@ extern "C" vx_status vx_index_destroy(vx_index* h) {
     if (e) cudaEventDestroy(e);
   if (h->tok_ev) cudaEventDestroy(h->tok_ev);
   if (h->stream2) cudaStreamDestroy(h->stream2);
+  if (h->stream_cond) cudaStreamDestroy(h->stream_cond);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
   return VX_OK;
@@ -366,6 +372,7 @@ extern "C" vx_status vx_reset_stats(vx_index* h) {
   CU_TRY(cudaSetDevice(h->device));
   CU_TRY(cudaStreamSynchronize(h->stream));
   CU_TRY(cudaMemset(h->d_fcount, 0, 16));
+  VX_TRY(ktimer_reset(h));
   h->st = vx_stats{};
   return VX_OK;
 }

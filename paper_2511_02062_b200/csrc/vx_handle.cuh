@@ -94,7 +94,8 @@ struct vx_index {
   int kprime = 0;                // TC candidate set size k' (0 = auto; VX_OPT_KPRIME)
   int dbg_tc_bits = 0;           // timing-experiment knobs, read once from the environment at
   int dbg_tc_stages = 0;         //   create: VX_DEBUG_TC_NOSELECT (bit mask), VX_DEBUG_TC_STAGES,
-  int dbg_seed_m = 0;            //   VX_DEBUG_SEED_M (sample rank of the scan seed, <= 32)
+  int dbg_seed_m = 0;            //   VX_DEBUG_SEED_M (sample rank of the scan seed, <= 32),
+  int dbg_no_rep = 0;            //   VX_DEBUG_NO_REP (no small-batch query replication)
   int scan_seed = 1;             // seed the TC scan's admission thresholds (VX_OPT_SCAN_SEED)
   int use_pairs = 2;             // CTA-pair scan for B > 128: 0 off, 1 on (256-query passes),
                                  // 2 on + 512-query passes for B > 256 (VX_OPT_SCAN_PAIRS)
@@ -129,6 +130,7 @@ struct vx_index {
   float* d_fq = nullptr;         // [maxB][D] queries gathered for the exact fallback
   int* d_fidx = nullptr;         // [maxB] flagged query indices
   int* d_fcount = nullptr;       // [2] flagged count of the last batch, running total
+  vx::KTimer* d_ktimer = nullptr;  // [KT_N] device-side launch timers (vx_stats.kt_*)
   // pinned host staging
   void* h_stage = nullptr;
   size_t h_stage_bytes = 0;
@@ -146,6 +148,7 @@ struct vx_index {
   cudaEvent_t* ev_end = ev;      //   ... and the one holding the stage end (read by vx_sync)
   cudaStream_t stream_last = nullptr;  // stream of the last batch's final part
   cudaStream_t stream2 = nullptr;      // host API: query-token upload overlapping part 1
+  cudaStream_t stream_cond = nullptr;  // captures the body of the certificate IF node
   cudaEvent_t tok_ev = nullptr;
   cudaEvent_t pev[5] = {};       // sharded rank 0 phases: start, bcast done, local done,
   bool phases_pending = false;   //   gather done, end
@@ -160,6 +163,15 @@ struct vx_index {
 };
 
 static inline void count_launch(vx_index* h, int n = 1) { h->st.kernel_launches += n; }
+
+// arm the device-side launch timers (start = max, everything else 0)
+static inline vx_status ktimer_reset(vx_index* h) {
+  vx::KTimer t[vx::KT_N] = {};
+  for (auto& x : t) x.start = ~0ull;
+  if (cudaMemcpy(h->d_ktimer, t, sizeof t, cudaMemcpyHostToDevice) != cudaSuccess)
+    return fail(VX_ERR_CUDA, "ktimer reset");
+  return VX_OK;
+}
 
 // Captured stage graphs bake in every choice made at capture time (coarse format from the
 // shard statistics, k', seed, tile, pairs, grid, scan / MaxSim algorithm), so any option

@@ -9,6 +9,17 @@
 
 namespace vx {
 
+// Device-side launch timing, kept per kernel kind (vx_ptx.cuh ktimer_begin / ktimer_end):
+// every CTA folds its %globaltimer start / end into [start, end] with atomics, the last CTA to
+// finish adds end - start to total_ns and re-arms the slot, so every launch — inside CUDA
+// graphs, with no host synchronisation — is timed first-CTA-start to last-CTA-end.  CTA 0
+// also accumulates clock64() cycles over its own %globaltimer span: the SM clock the kernel
+// actually ran at.
+struct KTimer {
+  unsigned long long start, end, done, total_ns, launches, clk_cycles, clk_ns, pad;
+};
+enum { KT_SCAN = 0, KT_SAMPLE = 1, KT_F32 = 2, KT_MAXSIM = 3, KT_N = 4 };
+
 // -------- exact fp32 scan (K1): scan_f32.cu
 struct ScanF32Args {
   const float* q;      // [B][D] device, fp32
@@ -21,6 +32,7 @@ struct ScanF32Args {
   uint64_t* part;      // [B][gridDim.x][kcap] keys (score desc, local id asc)
   const int* d_count;  // optional: queries actually present = min(B, *d_count - g0) (device)
   int32_t g0;
+  KTimer* ktimer = nullptr;
 };
 
 // Returns the queries-per-launch bucket the f32 scan uses for a batch of B.
@@ -49,6 +61,10 @@ struct ScanTcArgs {
   const uint64_t* seed;
   int32_t seed_ld;
   int32_t kc;        // list length per CTA (pair) and query: 0 = kc_of(fmt), or kSampleKC
+  KTimer* ktimer = nullptr;
+  int32_t rep = 1;   // single-CTA kernel, TD = 256, B <= 64: each query occupies rep = 128 /
+                     // a_rows rows of the A tile, replica r selects over columns
+                     // [r TD/rep, (r+1) TD/rep) — rep x the epilogue lanes on a small batch
 };
 // admission threshold a seed key stands for (-inf: none)
 __device__ __forceinline__ float seed_thr(const uint64_t* seed, int ld, int q) {
@@ -126,7 +142,8 @@ cudaError_t launch_merge_topk(const uint64_t* in, int B, int M, int k, int64_t i
 // Certificate failures (flags[B]) -> compacted list fidx/fcount and the flagged query rows
 // gathered into fq; after the exact re-scan, scatter its [fcount][k] results back.
 cudaError_t launch_cert_compact(const int* flags, int B, const float* q, int D, int* fidx,
-                                int* fcount, float* fq, cudaStream_t st);
+                                int* fcount, float* fq, cudaStream_t st,
+                                unsigned long long cond = 0, int use_cond = 0);
 cudaError_t launch_cert_scatter(const int* fidx, const int* fcount, int B, int k,
                                 const uint64_t* fkeys, const int64_t* fids, const float* fsc,
                                 uint64_t* keys, int64_t* ids, float* scores, cudaStream_t st);
@@ -155,6 +172,7 @@ struct MaxSimArgs {
   int32_t B, nq, C, Nd, d;
   float* out;            // [B][C]
   int64_t id_lo = 0, id_hi = INT64_MAX;  // ids outside [lo, hi) (another shard's) -> -INF, no loads
+  KTimer* ktimer = nullptr;
 };
 cudaError_t launch_maxsim(const MaxSimArgs& a, cudaStream_t st);
 // fp32 -> bf16 hi plane (out) + lo plane (out + n): hi = RNE(v), lo = RNE(v - hi)

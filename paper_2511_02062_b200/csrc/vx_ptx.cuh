@@ -386,4 +386,38 @@ VX_DEV void warp_bitonic_desc(uint64_t* buf, int n) {
   }
 }
 
+// ---- device-side launch timing (KTimer, vx_internal.cuh); thread 0 of every CTA
+VX_DEV uint64_t gtimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+VX_DEV void ktimer_begin(KTimer* t, uint64_t& c0, uint64_t& g0) {
+  if (!t || threadIdx.x != 0) return;
+  g0 = gtimer_ns();
+  c0 = clock64();
+  atomicMin(&t->start, (unsigned long long)g0);
+}
+// after the CTA's last work (its final barrier)
+VX_DEV void ktimer_end(KTimer* t, uint64_t c0, uint64_t g0) {
+  if (!t || threadIdx.x != 0) return;
+  const uint64_t g1 = gtimer_ns(), c1 = clock64();
+  atomicMax(&t->end, (unsigned long long)g1);
+  if (blockIdx.x == 0) {
+    atomicAdd(&t->clk_cycles, (unsigned long long)(c1 - c0));
+    atomicAdd(&t->clk_ns, (unsigned long long)(g1 - g0));
+  }
+  __threadfence();
+  const unsigned long long n = (unsigned long long)gridDim.x * gridDim.y * gridDim.z;
+  if (atomicAdd(&t->done, 1ull) == n - 1) {  // last CTA: fold this launch, re-arm the slot
+    __threadfence();
+    const unsigned long long s = atomicAdd(&t->start, 0ull), e = atomicAdd(&t->end, 0ull);
+    atomicAdd(&t->total_ns, e - s);
+    atomicAdd(&t->launches, 1ull);
+    atomicExch(&t->start, ~0ull);
+    atomicExch(&t->end, 0ull);
+    atomicExch(&t->done, 0ull);
+  }
+}
+
 }  // namespace vx

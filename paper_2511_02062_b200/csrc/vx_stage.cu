@@ -45,6 +45,7 @@ static vx_status local_topk_f32(vx_index* h, const float* d_q, int B, int k, uin
     a.part = h->d_part + (size_t)g0 * grid * kcap;
     a.d_count = d_count;
     a.g0 = g0;
+    a.ktimer = d_count ? nullptr : h->d_ktimer + vx::KT_F32;
     if (g0 == 0 && !d_count) CU_TRY(record_ev(h, h->tev[0], st));
     CU_TRY(vx::launch_scan_f32(bucket, &h->tmap_docs, a, grid, smem, st));
     count_launch(h);
@@ -170,7 +171,13 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
       const bool on_pairs = pairs && Bg > 128;
       const int QT = Bg <= 128 ? 1 : 2;
       const int QG = on_pairs && Bg > 256 ? 2 : 1;
-      const int a_rows = on_pairs ? 128 : (QT == 1 ? ((Bg + 7) & ~7) : 128);
+      const int TD1 = h->scan_tile ? h->scan_tile : 256;
+      // small batch on the single-CTA kernel: replicate the queries over the 128 A-tile rows
+      // so every epilogue lane selects (ScanTcArgs::rep): 16 rows x 8, 32 x 4, 64 x 2
+      const int rep = (!on_pairs && QT == 1 && TD1 == 256 && !h->dbg_no_rep)
+                          ? (Bg <= 16 ? 8 : (Bg <= 32 ? 4 : (Bg <= 64 ? 2 : 1)))
+                          : 1;
+      const int a_rows = on_pairs ? 128 : (rep > 1 ? 128 / rep : (QT == 1 ? ((Bg + 7) & ~7) : 128));
       CUtensorMap tq;
       if (bf16)
         VX_TRY(make_tmap_2d(&tq, h->d_q16 + (size_t)g0 * D, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
@@ -189,6 +196,8 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
       a.fmt = fmt;
       a.dbg_no_select = h->dbg_tc_bits;  // timing experiments only (VX_DEBUG_TC_NOSELECT)
       a.kc = sample ? vx::kSampleKC : 0;
+      a.rep = rep;
+      a.ktimer = h->d_ktimer + (sample ? vx::KT_SAMPLE : vx::KT_SCAN);
       a.part = sample ? sample_lists + (size_t)g0 * grid * vx::kSampleKC : h->d_part + (size_t)g0 * ldp;
       a.seed = (seeded && !sample) ? h->d_seedk + (size_t)g0 * kSeedLd + (kSeedM - 1) : nullptr;
       a.seed_ld = kSeedLd;
@@ -221,7 +230,7 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
       } else {
         // 256-document tiles halve the per-document query re-streaming from L2 (measured:
         // B=128 bf16 2.31 ms vs 3.78 ms with 128; B=256 3.9 ms vs 4.36 ms) — profiles/r01/
-        const int TD = h->scan_tile ? h->scan_tile : 256;
+        const int TD = TD1;
         int ns = 0;
         size_t smem = vx::scan_tc_smem(QT, TD, fmt, &ns);
         if (h->dbg_tc_stages) {  // timing experiments only (VX_DEBUG_TC_STAGES)
@@ -300,25 +309,63 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
   //            count) and scattered back.
   int* cnt2 = h->d_fcount;      // [count, running total] of level-2 queries
   int* cnt3 = h->d_fcount + 2;  // [count, running total] of exact re-scans
-  CU_TRY(vx::launch_cert_compact(h->d_flags, B, d_q, D, h->d_fidx, cnt2, h->d_fq, st));
-  count_launch(h);
   // wide-key scratch: the upper part of d_part (the lists use B x grid x KC <= B x grid x 32
   // of its B x grid x 256 entries; the level-3 re-scan writes d_part only after level 2)
   uint64_t* wkeys = h->d_part + (size_t)h->desc.max_batch * grid * 32;
-  CU_TRY(vx::launch_rerank_wide(h->docs, h->d_fq, D, h->d_fidx, cnt2, h->d_part, B, GS,
-                                pairs ? grid / 2 : 0, grid, KC, k, h->row0,
-                                reinterpret_cast<const float*>(h->d_xnorm), fmt,
-                                i8 ? h->d_qs8 : nullptr, wkeys, keys, ids, scores, h->d_flags, st,
-                                seed_keys, kSeedLd));
-  count_launch(h, 2);
-  CU_TRY(vx::launch_cert_compact(h->d_flags, B, d_q, D, h->d_fidx, cnt3, h->d_fq, st));
+  auto chain = [&](cudaStream_t cs, bool count) -> vx_status {  // levels 2 and 3
+    CU_TRY(vx::launch_rerank_wide(h->docs, h->d_fq, D, h->d_fidx, cnt2, h->d_part, B, GS,
+                                  pairs ? grid / 2 : 0, grid, KC, k, h->row0,
+                                  reinterpret_cast<const float*>(h->d_xnorm), fmt,
+                                  i8 ? h->d_qs8 : nullptr, wkeys, keys, ids, scores, h->d_flags, cs,
+                                  seed_keys, kSeedLd));
+    CU_TRY(vx::launch_cert_compact(h->d_flags, B, d_q, D, h->d_fidx, cnt3, h->d_fq, cs));
+    uint64_t* fk = h->d_ckeys;  // reuse: [B][k] (k <= 256)
+    int64_t* fi = h->d_out_ids;
+    float* fs = h->d_out_ms;
+    const uint64_t before = h->st.kernel_launches;
+    VX_TRY(local_topk_f32(h, h->d_fq, B, k, fk, fi, fs, cs, cnt3));
+    CU_TRY(vx::launch_cert_scatter(h->d_fidx, cnt3, B, k, fk, fi, fs, keys, ids, scores, cs));
+    if (count) count_launch(h, 4);
+    else h->st.kernel_launches = before;  // conditional body: runs only on a failure
+    return VX_OK;
+  };
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  CU_TRY(cudaStreamIsCapturing(st, &cap));
+  if (cap != cudaStreamCaptureStatusActive) {
+    // eager: every launch below exits at once when its device-side count is 0
+    CU_TRY(vx::launch_cert_compact(h->d_flags, B, d_q, D, h->d_fidx, cnt2, h->d_fq, st));
+    count_launch(h);
+    return chain(st, true);
+  }
+  // Captured (CUDA graph): the compaction sets a conditional handle, and levels 2-3 are the
+  // body of an IF node — a batch whose queries all pass certificate 1 (the common case)
+  // replays no level-2/3 launches at all (six ~2.5 us empty launches at B = 16, 100K rows).
+  cudaGraph_t g = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  CU_TRY(cudaStreamGetCaptureInfo(st, &cap, nullptr, &g, &deps, &ndeps));
+  cudaGraphConditionalHandle hc;
+  CU_TRY(cudaGraphConditionalHandleCreate(&hc, g, 0, cudaGraphCondAssignDefault));
+  CU_TRY(vx::launch_cert_compact(h->d_flags, B, d_q, D, h->d_fidx, cnt2, h->d_fq, st,
+                                 (unsigned long long)hc, 1));
   count_launch(h);
-  uint64_t* fk = h->d_ckeys;  // reuse: [B][k] (k <= 256)
-  int64_t* fi = h->d_out_ids;
-  float* fs = h->d_out_ms;
-  VX_TRY(local_topk_f32(h, h->d_fq, B, k, fk, fi, fs, st, cnt3));
-  CU_TRY(vx::launch_cert_scatter(h->d_fidx, cnt3, B, k, fk, fi, fs, keys, ids, scores, st));
-  count_launch(h);
+  CU_TRY(cudaStreamGetCaptureInfo(st, &cap, nullptr, &g, &deps, &ndeps));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = hc;
+  cp.conditional.type = cudaGraphCondTypeIf;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  CU_TRY(cudaGraphAddNode(&node, g, deps, ndeps, &cp));
+  CU_TRY(cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  CU_TRY(cudaStreamBeginCaptureToGraph(h->stream_cond, body, nullptr, nullptr, 0,
+                                       cudaStreamCaptureModeThreadLocal));
+  const vx_status bs = chain(h->stream_cond, false);
+  cudaGraph_t out = nullptr;
+  const cudaError_t ee = cudaStreamEndCapture(h->stream_cond, &out);
+  VX_TRY(bs);
+  CU_TRY(ee);
   return VX_OK;
 }
 
@@ -364,6 +411,7 @@ vx_status run_maxsim(vx_index* h, const float* d_qtok, int B, int nq, const int6
   a.out = d_out;
   a.id_lo = id_lo;
   a.id_hi = id_hi;
+  a.ktimer = h->d_ktimer + vx::KT_MAXSIM;
   const bool tc = h->maxsim_algo != VX_MAXSIM_CC &&
                   vx::maxsim_tc_supported(nq, a.Nd, a.d);
   if ((h->maxsim_algo == VX_MAXSIM_TC || h->maxsim_algo == VX_MAXSIM_TC_BF16Q) && !tc)
@@ -665,6 +713,7 @@ extern "C" vx_status vx_prepare(vx_index* h, int32_t op, int32_t k, int32_t nq, 
   }
   CU_TRY(cudaStreamSynchronize(st));
   h->st = saved;  // preload work is not serving work
+  VX_TRY(ktimer_reset(h));
   h->timing_pending = false;
   return VX_OK;
 }
@@ -699,6 +748,13 @@ extern "C" vx_status vx_sync(vx_index* h) {
     CU_TRY(cudaMemcpy(fc, h->d_fcount, 16, cudaMemcpyDeviceToHost));
     h->st.cert_level2 = (uint64_t)fc[1];
     h->st.cert_fallbacks = (uint64_t)fc[3];
+  }
+  vx::KTimer kt[vx::KT_N];  // device-side launch timers (every launch since the last reset)
+  CU_TRY(cudaMemcpy(kt, h->d_ktimer, sizeof kt, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < vx::KT_N; ++i) {
+    h->st.kt_launches[i] = kt[i].launches;
+    h->st.kt_ms[i] = (double)kt[i].total_ns * 1e-6;
+    h->st.kt_sm_mhz[i] = kt[i].clk_ns ? (double)kt[i].clk_cycles * 1e3 / (double)kt[i].clk_ns : 0.0;
   }
   cudaGetLastError();
   return VX_OK;
