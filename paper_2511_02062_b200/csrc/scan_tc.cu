@@ -23,6 +23,7 @@
 #include "vx_internal.cuh"
 #include "vx_ptx.cuh"
 #include "vx_select.cuh"
+#include "vx_sort.cuh"
 
 namespace vx {
 
@@ -539,20 +540,8 @@ __global__ void __launch_bounds__(256)
       s_fail = 1;
   }
   __syncthreads();
-  // block bitonic sort of the exact keys (kp is a power of two)
-  for (int size = 2; size <= kp; size <<= 1)
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = threadIdx.x; i < (kp >> 1); i += blockDim.x) {
-        int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
-        bool desc = (lo & size) == 0;
-        uint64_t x0 = keys[lo], x1 = keys[hi];
-        if ((x0 < x1) == desc) {
-          keys[lo] = x1;
-          keys[hi] = x0;
-        }
-      }
-      __syncthreads();
-    }
+  // sort the exact keys (kp is a power of two <= 1024; registers + shuffles, vx_sort.cuh)
+  block_sort_desc(keys, kp);
   // seeded scan (ScanTcArgs::seed): the lists also dropped every document whose coarse score
   // is below the seed, so a document outside the candidates has coarse score
   // <= max(s(T'), seed)
@@ -900,11 +889,18 @@ cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64
   int R = env_rows > 0 ? std::min(env_rows, 256) : 64;
   auto smem_of = [&](int r) { return base + 2 * (size_t)r * (DC + 4) * 4; };
   while (R > 32 && smem_of(R) > 220 * 1024) R -= 32;
-  const size_t smem = smem_of(R);
+  size_t smem = smem_of(R);
+  const int head_all = phase == 0 && B <= 64 ? 1 : 0;
+  // small batch, latency-bound: ALL k' whole rows in one burst of bulk copies and one wait
+  // (one round, one chunk: only buffer 0 is used), instead of double-buffered chunk rounds
+  if (head_all && env_dc == 0 && base + (size_t)kp * (D + 4) * 4 <= 220 * 1024) {
+    DC = D;
+    R = kp;
+    smem = base + (size_t)kp * (D + 4) * 4;
+  }
   cudaError_t e = cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  const int head_all = phase == 0 && B <= 64 ? 1 : 0;
   rerank_kernel<<<B, 256, smem, st>>>(docs, q, D, cand, kp, part, grid, ldlists, kc, k, row0,
                                       xstats, fmt, qscale, out_keys, out_ids, out_scores, flags, R,
                                       DC, phase, tau, hkeys, lb, seed, seed_ld, head_all);

@@ -14,6 +14,7 @@
 
 #include "vx_internal.cuh"
 #include "vx_ptx.cuh"
+#include "vx_sort.cuh"
 
 namespace vx {
 
@@ -64,22 +65,66 @@ __global__ void __launch_bounds__(kMergeThreads)
     L = staged;
   }
 
-  uint64_t prefix = 0, mask = 0;
+  // the digits every key shares need no pass: start at the first byte where the largest
+  // and the smallest key differ (scores of one query's candidates share sign, exponent and
+  // often leading mantissa bits — one or two of the ~3 passes)
+  uint64_t kmax = 0ull, kmin = ~0ull;
+  for (int i = threadIdx.x; i < M; i += blockDim.x) {
+    const uint64_t v = L[i];
+    kmax = v > kmax ? v : kmax;
+    kmin = v < kmin ? v : kmin;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t a = shfl_xor_u64(kmax, o), b = shfl_xor_u64(kmin, o);
+    kmax = a > kmax ? a : kmax;
+    kmin = b < kmin ? b : kmin;
+  }
+  __shared__ uint64_t s_mx[kMergeThreads / 32], s_mn[kMergeThreads / 32];
+  if (lane == 0) {
+    s_mx[warp] = kmax;
+    s_mn[warp] = kmin;
+  }
+  __syncthreads();
+  kmax = s_mx[0];
+  kmin = s_mn[0];
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+    kmax = s_mx[w] > kmax ? s_mx[w] : kmax;
+    kmin = s_mn[w] < kmin ? s_mn[w] : kmin;
+  }
+  const int common_bytes = (kmax == kmin) ? 7 : (__clzll((long long)(kmax ^ kmin)) >> 3);
+  uint64_t mask = common_bytes ? (~0ull << (64 - 8 * common_bytes)) : 0ull;
+  uint64_t prefix = kmax & mask;
   int kk = k;
-  for (int shift = 56; shift >= 0; shift -= 8) {
+  for (int shift = 56 - 8 * common_bytes; shift >= 0; shift -= 8) {
     for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
     __syncthreads();
-    // histogram of the next digit over the keys still matching the prefix; lanes with the
-    // same digit aggregate first (top digits are shared by most keys: one atomic per warp)
-    for (int i0 = 0; i0 < M; i0 += blockDim.x) {
-      const int i = i0 + (int)threadIdx.x;
-      const uint64_t key = i < M ? L[i] : 0ull;
-      const bool live = i < M && (key & mask) == prefix;
-      const unsigned act = __ballot_sync(0xffffffffu, live);
-      if (live) {
-        const uint32_t dg = (uint32_t)(key >> shift) & 255u;
-        const unsigned same = __match_any_sync(act, dg);
-        if (lane == __ffs(same) - 1) atomicAdd(&hist[dg], (uint32_t)__popc(same));
+    // histogram of the next digit over the keys still matching the prefix.  Top digits are
+    // shared by most keys, so a warp whose live lanes all carry one digit adds once; mixed
+    // warps add per lane (match.any aggregation was the kernel's critical path: its result
+    // latency stalled every iteration — profiles/r02)
+    // Four keys per thread per iteration: their chains are independent, so the warp keeps
+    // four in flight (one key at a time left every iteration a ~300-cycle dependent chain).
+    for (int i0 = 0; i0 < M; i0 += 4 * (int)blockDim.x) {
+      uint64_t kx[4];
+      bool lv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * (int)blockDim.x + (int)threadIdx.x;
+        kx[u] = i < M ? L[i] : 0ull;
+        lv[u] = i < M && (kx[u] & mask) == prefix;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const unsigned act = __ballot_sync(0xffffffffu, lv[u]);
+        if (act == 0u) continue;
+        const uint32_t dg = (uint32_t)(kx[u] >> shift) & 255u;
+        const uint32_t d0 = __shfl_sync(0xffffffffu, dg, __ffs(act) - 1);
+        const bool uni = __all_sync(0xffffffffu, !lv[u] || dg == d0);
+        if (uni) {
+          if (lane == 0) atomicAdd(&hist[d0], (uint32_t)__popc(act));
+        } else if (lv[u]) {
+          atomicAdd(&hist[dg], 1u);
+        }
       }
     }
     __syncthreads();
@@ -144,19 +189,29 @@ __global__ void __launch_bounds__(kMergeThreads)
   }
   __syncthreads();
   const int n_above = k - kk;
-  for (int i = threadIdx.x; i < M; i += blockDim.x) {
-    uint64_t key = L[i];
-    uint64_t m = key & mask;
-    if (m > prefix) {
-      int slot = atomicAdd(&s_above, 1);
-      sel[slot] = key;
-    } else if (m == prefix) {
-      int slot = atomicAdd(&s_eq, 1);
-      if (slot < kk) sel[n_above + slot] = key;
+  for (int i0 = 0; i0 < M; i0 += 4 * (int)blockDim.x) {
+    uint64_t kx[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * (int)blockDim.x + (int)threadIdx.x;
+      kx[u] = i < M ? L[i] : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * (int)blockDim.x + (int)threadIdx.x;
+      if (i >= M) continue;
+      const uint64_t m = kx[u] & mask;
+      if (m > prefix) {
+        const int slot = atomicAdd(&s_above, 1);
+        sel[slot] = kx[u];
+      } else if (m == prefix) {
+        const int slot = atomicAdd(&s_eq, 1);
+        if (slot < kk) sel[n_above + slot] = kx[u];
+      }
     }
   }
   __syncthreads();
-  block_bitonic_desc(sel, kp);
+  block_sort_desc(sel, kp);
   for (int i = threadIdx.x; i < k; i += blockDim.x) {
     uint64_t key = sel[i];
     size_t o = (size_t)blockIdx.x * ldout + i;
@@ -223,7 +278,7 @@ __global__ void __launch_bounds__(256)
     buf[i] = key;
   }
   __syncthreads();
-  block_bitonic_desc(buf, kp);
+  block_sort_desc(buf, kp);
   for (int i = threadIdx.x; i < k; i += blockDim.x) {
     uint64_t key = buf[i];
     if (key == 0ull) {
