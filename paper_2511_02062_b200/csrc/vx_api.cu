@@ -249,8 +249,11 @@ extern "C" vx_status vx_index_destroy(vx_index* h) {
   if (!h) return VX_OK;
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
-  if (h->comm) nccl().CommDestroy(h->comm);
+  // graphs first: captured NCCL operations hold references on the communicator, and
+  // destroying it under live graphs hangs
   for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second.exec);
+  h->graphs.clear();
+  if (h->comm) nccl().CommDestroy(h->comm);
   void* ptrs[] = {h->docs,  h->tokens,    h->d_q,      h->d_qtok,    h->d_part, h->d_keys,
                   h->d_ids, h->d_ip,      h->d_ms,     h->d_out_ids, h->d_out_ip,
                   h->d_out_ms, h->d_send, h->d_recv, h->d_hdr, h->d_ckeys, h->d_seedk, h->d_flags,
@@ -782,6 +785,11 @@ extern "C" vx_status vx_comm_init(vx_index* h, const uint8_t id[128], int32_t nr
   return VX_OK;
 }
 
+// The shard ranks' serve loop.  Per batch the host must learn the 16-byte header (B picks
+// the graph), so it waits for the header broadcast — polling an event instead of a blocking
+// stream sync (the wake-up of a yielding sync was tens of us per batch) — then launches the
+// batch's parts: the captured graphs of its shape (VX_OPT_GRAPHS; the first batch of a shape
+// runs eagerly and captures, like rank 0), else the eager stage.
 extern "C" vx_status vx_shard_serve(vx_index* h) {
   if (!h) return fail(VX_ERR_INVALID, "null handle");
   if (!h->comm || h->rank == 0) return fail(VX_ERR_STATE, "vx_shard_serve is for ranks != 0");
@@ -790,17 +798,26 @@ extern "C" vx_status vx_shard_serve(vx_index* h) {
   for (;;) {
     NCCL_TRY(nccl().Broadcast(h->d_hdr, h->d_hdr, 4, ncclInt32, 0, h->comm, st));
     CU_TRY(cudaMemcpyAsync(h->h_hdr, h->d_hdr, 16, cudaMemcpyDeviceToHost, st));
-    CU_TRY(cudaStreamSynchronize(st));
+    CU_TRY(cudaEventRecord(h->tok_ev, st));
+    cudaError_t q;
+    while ((q = cudaEventQuery(h->tok_ev)) == cudaErrorNotReady) {
+    }
+    CU_TRY(q);
     const int op = h->h_hdr[0], B = h->h_hdr[1], k = h->h_hdr[2], nq = h->h_hdr[3];
     if (op == OP_STOP) return VX_OK;
     if (B < 1 || B > h->desc.max_batch || k < 1 || k > h->desc.max_k)
       return fail(VX_ERR_STATE, "bad batch header %d/%d/%d", op, B, k);
     if (op == OP_RESCORE && (nq < 1 || nq > h->desc.max_qtok))
       return fail(VX_ERR_STATE, "bad batch header nq %d", nq);
-    NCCL_TRY(nccl().Broadcast(h->d_q, h->d_q, (size_t)B * h->desc.dim, ncclFloat32, 0, h->comm, st));
-    VX_TRY(core_topk(h, h->d_q, B, k, st));
-    if (op == OP_RESCORE)  // phase 2: receives the tokens + winners, MaxSim on owned winners
-      VX_TRY(core_rescore(h, nullptr, B, nq, k, h->d_out_ids, h->d_out_ip, h->d_out_ms, st));
+    if (h->use_graphs) {
+      VX_TRY(run_part(h, 1 /*PART_TOPK*/, B, op == OP_RESCORE ? nq : 0, k, st));
+      if (op == OP_RESCORE) VX_TRY(run_part(h, 2 /*PART_RESCORE*/, B, nq, k, st));
+    } else {
+      NCCL_TRY(nccl().Broadcast(h->d_q, h->d_q, (size_t)B * h->desc.dim, ncclFloat32, 0, h->comm, st));
+      VX_TRY(core_topk(h, h->d_q, B, k, st));
+      if (op == OP_RESCORE)  // phase 2: receives the tokens + winners, MaxSim on owned winners
+        VX_TRY(core_rescore(h, nullptr, B, nq, k, h->d_out_ids, h->d_out_ip, h->d_out_ms, st));
+    }
     h->st.batches += 1;
     h->st.queries += B;
   }

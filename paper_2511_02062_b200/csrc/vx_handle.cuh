@@ -191,6 +191,13 @@ static inline cudaError_t record_ev(vx_index* h, cudaEvent_t e, cudaStream_t st)
   return cudaEventRecordWithFlags(e, st,
                                   h->tev == h->gev ? cudaEventRecordExternal : cudaEventRecordDefault);
 }
+// the same for events recorded without the tev indirection (sharded phase events)
+static inline cudaError_t record_ext(cudaEvent_t e, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  return cudaEventRecordWithFlags(
+      e, st, cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault);
+}
 
 static inline int next_pow2(int x) {
   int p = 1;
@@ -226,6 +233,8 @@ vx_status core_rescore(vx_index* h, const float* d_qtok, int B, int nq, int k, i
 // rank-0 entry points: announce + part 1; part 2 of a search / of the fused stage
 vx_status stage_begin(vx_index* h, int op, const float* d_q, int B, int nq, int k,
                       cudaStream_t st);
+// one part of the stage (1: broadcast + top-k, 2: rescore) through its captured graph
+vx_status run_part(vx_index* h, int part, int B, int nq, int k, cudaStream_t st);
 vx_status stage_search_out(vx_index* h, int B, int k, int64_t* d_ids, float* d_ip,
                            cudaStream_t st);
 vx_status stage_finish(vx_index* h, const float* d_qtok, int B, int nq, int k, int64_t* d_ids,

@@ -455,7 +455,7 @@ vx_status core_topk(vx_index* h, const float* d_q, int B, int k, cudaStream_t st
   if (h->nranks == 1) return VX_OK;
   const int n = B * k;
   const bool root = h->rank == 0;
-  if (root) CU_TRY(cudaEventRecord(h->pev[2], st));
+  if (root) CU_TRY(record_ext(h->pev[2], st));
   const size_t bytes = (size_t)n * 8;
   uint64_t* recv = reinterpret_cast<uint64_t*>(h->d_recv);
   NCCL_TRY(nccl().GroupStart());
@@ -478,7 +478,7 @@ vx_status core_topk(vx_index* h, const float* d_q, int B, int k, cudaStream_t st
   // keys already carry global ids: id_base 0
   CU_TRY(vx::launch_merge_topk(h->d_part, B, G * k, k, 0, h->d_keys, h->d_ids, h->d_ip, st));
   count_launch(h);
-  CU_TRY(cudaEventRecord(h->pev[3], st));
+  CU_TRY(record_ext(h->pev[3], st));
   return VX_OK;
 }
 
@@ -520,20 +520,30 @@ vx_status core_rescore(vx_index* h, const float* d_qtok, int B, int nq, int k,
   return VX_OK;
 }
 
-// CUDA-graph mode (VX_OPT_GRAPHS, single GPU): each part for one (B, k[, nq]) is captured
-// once and replayed — one launch per part instead of ~12 kernels, no host work between the
-// kernels (the batcher hands each batch to the graphs of its size, north star (e)).  The
-// graphs read the handle's fixed input buffers and write its fixed output buffers; user
-// pointers are copied in/out around the replay.  The first batch of a shape runs the part
-// eagerly (it also sets the kernels' smem attributes) and captures it for the next ones.
+// CUDA-graph mode (VX_OPT_GRAPHS): each part for one (B, k[, nq]) is captured once and
+// replayed — one launch per part instead of ~12 kernels, no host work between the kernels
+// (the batcher hands each batch to the graphs of its size, north star (e)).  The graphs read
+// the handle's fixed input buffers and write its fixed output buffers; user pointers are copied
+// in/out around the replay.  The first batch of a shape runs the part eagerly (it also sets
+// the kernels' smem attributes) and captures it for the next ones.
+// Sharded (G > 1): EVERY rank captures the same parts — part 1 = the NCCL broadcast of the
+// queries + the local certified top-k with its threshold all-gather + the key gather to rank
+// 0; part 2 = the token / winner broadcast, the owner MaxSim and the max-reduce — so the
+// collectives inside the graphs match rank for rank.  Only the 16-byte batch header travels
+// outside a graph (the shard ranks need B to pick the graph).
 enum { PART_TOPK = 1, PART_RESCORE = 2 };
 
 static vx_status part_body(vx_index* h, int part, int B, int nq, int k, cudaStream_t st) {
   if (part == PART_TOPK) {
     CU_TRY(record_ev(h, h->tev[2], st));
+    if (h->nranks > 1) {
+      NCCL_TRY(nccl().Broadcast(h->d_q, h->d_q, (size_t)B * h->desc.dim, ncclFloat32, 0, h->comm, st));
+      if (h->rank == 0) CU_TRY(record_ext(h->pev[1], st));
+    }
     VX_TRY(core_topk(h, h->d_q, B, k, st));
   } else {
-    VX_TRY(core_rescore(h, h->d_qtok, B, nq, k, h->d_out_ids, h->d_out_ip, h->d_out_ms, st));
+    VX_TRY(core_rescore(h, h->rank == 0 ? h->d_qtok : nullptr, B, nq, k, h->d_out_ids,
+                        h->d_out_ip, h->d_out_ms, st));
   }
   CU_TRY(record_ev(h, h->tev[3], st));
   return VX_OK;
@@ -544,7 +554,7 @@ static uint64_t part_key(int part, int B, int nq, int k) {
          (uint64_t)(part == PART_RESCORE ? nq : 0);
 }
 
-static vx_status run_part(vx_index* h, int part, int B, int nq, int k, cudaStream_t st) {
+vx_status run_part(vx_index* h, int part, int B, int nq, int k, cudaStream_t st) {
   const uint64_t key = part_key(part, B, nq, k);
   cudaEvent_t* used;
   auto it = h->graphs.find(key);
@@ -556,7 +566,7 @@ static vx_status run_part(vx_index* h, int part, int B, int nq, int k, cudaStrea
   } else {
     VX_TRY(part_body(h, part, B, nq, k, st));
     // capture on the handle's stream after the eager run completes (capture records, it
-    // does not execute)
+    // does not execute; sharded, every rank captures at the same batch)
     CU_TRY(cudaStreamSynchronize(st));
     const uint64_t before = h->st.kernel_launches;
     h->tev = h->gev;  // the graph records its own (external) events
@@ -584,9 +594,9 @@ static vx_status run_part(vx_index* h, int part, int B, int nq, int k, cudaStrea
   return VX_OK;
 }
 
-// Rank 0 entry, part 1: announce the batch to the shards (header, queries), then top-k.
+// Rank 0 entry, part 1: announce the batch to the shards (header), then broadcast + top-k.
 vx_status stage_begin(vx_index* h, int op, const float* d_q, int B, int nq, int k,
-                             cudaStream_t st) {
+                      cudaStream_t st) {
   if (h->nranks > 1) {
     if (h->rank != 0) return fail(VX_ERR_STATE, "only rank 0 issues searches; call vx_shard_serve");
     h->h_hdr[0] = op;
@@ -596,17 +606,19 @@ vx_status stage_begin(vx_index* h, int op, const float* d_q, int B, int nq, int 
     CU_TRY(cudaEventRecord(h->pev[0], st));
     CU_TRY(cudaMemcpyAsync(h->d_hdr, h->h_hdr, 16, cudaMemcpyHostToDevice, st));
     NCCL_TRY(nccl().Broadcast(h->d_hdr, h->d_hdr, 4, ncclInt32, 0, h->comm, st));
-    NCCL_TRY(nccl().Broadcast(d_q, h->d_q, (size_t)B * h->desc.dim, ncclFloat32, 0, h->comm, st));
-    CU_TRY(cudaEventRecord(h->pev[1], st));
   }
-  if (h->use_graphs && h->nranks == 1) {
+  if (h->use_graphs) {
     if (d_q != h->d_q)
       CU_TRY(cudaMemcpyAsync(h->d_q, d_q, (size_t)B * h->desc.dim * 4, cudaMemcpyDeviceToDevice,
                              st));
     VX_TRY(run_part(h, PART_TOPK, B, nq, k, st));
   } else {
     CU_TRY(record_ev(h, h->tev[2], st));
-    VX_TRY(core_topk(h, d_q, B, k, st));
+    if (h->nranks > 1) {
+      NCCL_TRY(nccl().Broadcast(d_q, h->d_q, (size_t)B * h->desc.dim, ncclFloat32, 0, h->comm, st));
+      CU_TRY(cudaEventRecord(h->pev[1], st));
+    }
+    VX_TRY(core_topk(h, h->nranks > 1 ? h->d_q : d_q, B, k, st));
     CU_TRY(record_ev(h, h->tev[3], st));
     h->ev_start = h->ev_end = h->ev;
   }
@@ -637,7 +649,7 @@ vx_status stage_search_out(vx_index* h, int B, int k, int64_t* d_ids, float* d_i
 // part 2 of the fused stage: MaxSim rescore + order into the caller's buffers
 vx_status stage_finish(vx_index* h, const float* d_qtok, int B, int nq, int k,
                               int64_t* d_ids, float* d_ip, float* d_ms, cudaStream_t st) {
-  if (h->use_graphs && h->nranks == 1) {
+  if (h->use_graphs) {
     if (d_qtok != h->d_qtok)
       CU_TRY(cudaMemcpyAsync(h->d_qtok, d_qtok, (size_t)B * nq * h->desc.tok_dim * 4,
                              cudaMemcpyDeviceToDevice, st));
@@ -697,7 +709,9 @@ extern "C" vx_status vx_prepare(vx_index* h, int32_t op, int32_t k, int32_t nq, 
   const bool rescore = op == VX_PREPARE_RESCORE;
   if (rescore && (!h->tokens || nq < 1 || nq > h->desc.max_qtok))
     return fail(VX_ERR_INVALID, "rescore needs a token store and 1 <= nq <= max_qtok");
-  if (!h->use_graphs || h->nranks > 1) return VX_OK;
+  if (!h->use_graphs) return VX_OK;
+  if (h->nranks > 1 && h->rank != 0)
+    return fail(VX_ERR_STATE, "vx_prepare is issued by rank 0 (the shard ranks capture in vx_shard_serve)");
   CU_TRY(cudaSetDevice(h->device));
   cudaStream_t st = h->stream;
   // realistic inputs (generator rows), so every eager run takes the certified fast path
@@ -706,15 +720,27 @@ extern "C" vx_status vx_prepare(vx_index* h, int32_t op, int32_t k, int32_t nq, 
     CU_TRY(vx::launch_synth_rows(h->d_qtok, 0x5eed1ull, 0, (int64_t)b_max * nq, h->desc.tok_dim, st));
   const vx_stats saved = h->st;
   for (int B = 1; B <= b_max; ++B) {
-    if (!h->graphs.count(part_key(PART_TOPK, B, 0, k)))
-      VX_TRY(run_part(h, PART_TOPK, B, 0, k, st));
-    if (rescore && !h->graphs.count(part_key(PART_RESCORE, B, nq, k)))
-      VX_TRY(run_part(h, PART_RESCORE, B, nq, k, st));
+    const bool have1 = h->graphs.count(part_key(PART_TOPK, B, 0, k)) != 0;
+    const bool have2 = !rescore || h->graphs.count(part_key(PART_RESCORE, B, nq, k)) != 0;
+    if (have1 && have2) continue;
+    if (h->nranks > 1) {
+      // a real (synthetic) batch through the protocol: the shard ranks, serving, run and
+      // capture their parts of it at the same batch
+      VX_TRY(stage_begin(h, rescore ? OP_RESCORE : OP_SEARCH, h->d_q, B, nq, k, st));
+      if (rescore)
+        VX_TRY(stage_finish(h, h->d_qtok, B, nq, k, h->d_out_ids, h->d_out_ip, h->d_out_ms, st));
+      else
+        VX_TRY(stage_search_out(h, B, k, h->d_out_ids, h->d_out_ip, st));
+      continue;
+    }
+    if (!have1) VX_TRY(run_part(h, PART_TOPK, B, 0, k, st));
+    if (!have2) VX_TRY(run_part(h, PART_RESCORE, B, nq, k, st));
   }
   CU_TRY(cudaStreamSynchronize(st));
   h->st = saved;  // preload work is not serving work
   VX_TRY(ktimer_reset(h));
   h->timing_pending = false;
+  h->phases_pending = false;
   return VX_OK;
 }
 

@@ -27,6 +27,9 @@ def main() -> int:
     N, D, B, k, nq, T = int(os.environ.get("VX_N", "300001")), 768, 9, 100, 32, 211
     idx = vx.Index(N, D, device=local, n_shards=world, shard=rank, tok_per_doc=128, tok_dim=128,
                    tok_blocks=T, max_batch=1024, max_k=128, max_qtok=nq)
+    graphs = os.environ.get("VX_TEST_GRAPHS") == "1"
+    if graphs:  # every rank: captured parts (NCCL collectives inside the graphs)
+        idx.set_option(vx.VX_OPT_GRAPHS, 1)
     idx.synth(42)
     idx.tokens_synth(45)
     uid = [vx.Index.comm_unique_id() if rank == 0 else None]
@@ -38,7 +41,12 @@ def main() -> int:
         from paper_2511_02062_b200 import synth
         Q = synth.rows(43, 0, B, D)
         qt = synth.query_tokens(B, nq, 128)
+        if graphs:  # model load across the shards: every rank captures B = 1..9 (k = 100)
+            idx.prepare(k, B, nq=nq)
         ids_s, sc_s = idx.search(Q, 10)
+        if graphs:  # a second search of the same shape replays the captured graphs everywhere
+            ids_s2, _ = idx.search(Q, 10)
+            ok &= np.array_equal(ids_s, ids_s2)
         ids, ip, ms = idx.search_rescore(Q, qt, k)
         # a large batch: two 512-query CTA-pair passes on every shard, k = 100 (the headline
         # batch shape), checked in full including the output order

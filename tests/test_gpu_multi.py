@@ -21,14 +21,16 @@ def ngpus() -> int:
 
 
 @pytest.mark.skipif(ngpus() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("graphs", [0, 1])
 @pytest.mark.parametrize("world", [2, 4])
-def test_sharded_stage_matches_oracle(world):
+def test_sharded_stage_matches_oracle(world, graphs):
     if ngpus() < world:
         pytest.skip(f"needs {world} GPUs")
-    port = 29600 + world
+    port = 29600 + world + 10 * graphs
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "tests" / "mgpu_worker.py")]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=dict(os.environ))
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, VX_TEST_GRAPHS=str(graphs)))
     sys.stdout.write(r.stdout[-3000:])
     sys.stderr.write(r.stderr[-3000:])
     assert r.returncode == 0
