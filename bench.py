@@ -165,6 +165,9 @@ def parse() -> argparse.Namespace:
                     help="replay one captured CUDA graph per batch shape (single GPU)")
     ap.add_argument("--trace-s", type=float, default=0.5,
                     help="audio: seconds of Poisson arrivals per rate rung")
+    ap.add_argument("--dist", choices=["iso", "aniso"], default="iso",
+                    help="synthetic rows: isotropic, or anisotropic (power-law per-dimension scales "
+                         "+ outlier dimensions, include/vx_synth.h dist 1) — index AND queries")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -177,6 +180,8 @@ def parse() -> argparse.Namespace:
 def workload_name(args) -> str:
     D, k, B = args.dim, args.k, args.batch
     n = (f"{args.n_docs // 1_000_000}M" if args.n_docs >= 1_000_000 else f"{args.n_docs // 1000}K")
+    if getattr(args, "dist", "iso") == "aniso":
+        n += " anisotropic"
     tok = f"{args.nq}x{args.tok_per_doc}x{args.tok_dim} bf16"
     return {
         "stage": f"sharded {n}x{D} fp32 flat-IP top-{k} + MaxSim rescore ({tok}), batch {B}",
@@ -291,7 +296,7 @@ def cpu_check(args, world: int, gpu: dict, timed: bool) -> tuple[dict | None, di
         if wl != "maxsim":
             Qs = gpu["q"][sel]
             if wl == "flat":  # 100K rows: resident; repeat the scan for a measurable time
-                X = o.synth_rows(42, 0, args.n_docs, D)
+                X = o.synth_rows(42, 0, args.n_docs, D, 1 if args.dist == "aniso" else 0)
                 rid, rsc = o.flat_topk(X, Qs, k, mode=o.F32)
                 t0 = time.perf_counter()
                 while True:
@@ -302,7 +307,8 @@ def cpu_check(args, world: int, gpu: dict, timed: bool) -> tuple[dict | None, di
                     reps += 1
                 t_scan /= reps
             else:
-                rid, rsc, t_scan = o.flat_topk_synth(42, args.n_docs, D, Qs, k, mode=o.F32)
+                rid, rsc, t_scan = o.flat_topk_synth(42, args.n_docs, D, Qs, k, mode=o.F32,
+                                                     dist=1 if args.dist == "aniso" else 0)
         if wl in ("stage", "maxsim"):
             qts = gpu["qt"][sel]
             cand = rid if wl == "stage" else gpu["cand"][sel]
@@ -408,8 +414,9 @@ def run_ours(args) -> None:
                                           "i8": vx.VX_COARSE_I8}[args.coarse])
     if args.scan != "auto":
         idx.set_option(vx.VX_OPT_SCAN, {"f32": vx.VX_SCAN_F32, "tc": vx.VX_SCAN_TC}[args.scan])
+    rdist = 1 if args.dist == "aniso" else 0  # row distribution (vx_synth.h)
     if wl != "maxsim":
-        idx.synth(42)
+        idx.synth(42, dist=rdist)
     if tokens:
         idx.tokens_synth(45)
     if sharded:
@@ -447,7 +454,7 @@ def run_ours(args) -> None:
     l2buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if flush_l2 else None
     C = k
     if driver:
-        q_h = synth.queries(B, D, seed=43 + 1000 * rank) if wl != "maxsim" else None
+        q_h = synth.queries(B, D, seed=43 + 1000 * rank, dist=rdist) if wl != "maxsim" else None
         qt_h = synth.query_tokens(B, nq, td) if tokens else None
         rng = np.random.default_rng(7 + rank)
         cand_h = (np.stack([rng.choice(args.n_docs, C, replace=False) for _ in range(B)]).astype(np.int64)
@@ -531,7 +538,7 @@ def run_ours(args) -> None:
         # until p99 > SLO or the stage saturates; report the best rate that meets the SLO.
         from paper_2511_02062_b200 import batcher
         idx.prepare(k, B)  # model load: the graph of every batch size 1..cap, before serving
-        pool = synth.queries(4096, D, seed=43 + 1000 * rank)
+        pool = synth.queries(4096, D, seed=43 + 1000 * rank, dist=rdist)
         def rung(rate):
             n = int(min(100_000, max(2000, rate * args.trace_s)))
             arr = batcher.poisson_arrivals(rate, n, seed=11 + rank)
@@ -734,14 +741,15 @@ def run_reference(args) -> None:
     wl, B, D, k = args.workload, args.batch, args.dim, args.k
     S = min(B, {"flat": B, "maxsim": B, "audio": 32}.get(wl, 16))
     from paper_2511_02062_b200 import synth  # pure-numpy generator (no GPU library call)
-    Qall = synth.queries(B, D, seed=43) if wl != "maxsim" else None
+    dist = 1 if args.dist == "aniso" else 0
+    Qall = synth.queries(B, D, seed=43, dist=dist) if wl != "maxsim" else None
     QT = synth.query_tokens(B, args.nq, args.tok_dim) if wl in ("stage", "maxsim") else None
     rng = np.random.default_rng(7)
     CAND = (np.stack([rng.choice(args.n_docs, k, replace=False) for _ in range(B)]).astype(np.int64)
             if wl == "maxsim" else None)
     need_gb = args.n_docs * D * 4 / 2**30 if wl != "maxsim" else 0.0
     resident = need_gb < 0.6 * mem_available_gb()
-    X = o.synth_rows(42, 0, args.n_docs, D) if (resident and wl != "maxsim") else None
+    X = o.synth_rows(42, 0, args.n_docs, D, dist) if (resident and wl != "maxsim") else None
     steps_t = []
     for step in range(args.warmup + args.steps):
         sel = (np.arange(S) + step * S) % B  # walk through the batch
@@ -752,7 +760,7 @@ def run_reference(args) -> None:
                 rid, _ = o.flat_topk(X, Qall[sel], k, mode=o.F32)
                 t += time.perf_counter() - t0
             else:
-                rid, _, ts = o.flat_topk_synth(42, args.n_docs, D, Qall[sel], k, mode=o.F32)
+                rid, _, ts = o.flat_topk_synth(42, args.n_docs, D, Qall[sel], k, mode=o.F32, dist=dist)
                 t += ts
         if wl in ("stage", "maxsim"):
             cand = rid if wl == "stage" else CAND[sel]

@@ -152,6 +152,9 @@ vx_status vx_reset_stats(vx_index* h);
 
 /* Fill this shard's rows with the synthetic generator of vx_synth.h (seed). */
 vx_status vx_index_synth(vx_index* h, uint64_t seed);
+/* The same with a row distribution: 0 isotropic (= vx_index_synth), 1 anisotropic (power-law
+ * per-dimension scales + outlier dimensions, vx_synth.h). */
+vx_status vx_index_synth_dist(vx_index* h, uint64_t seed, int32_t dist);
 /* Upload rows [row0, row0+n) (global ids, must lie inside this shard), fp32 row-major. */
 vx_status vx_index_upload(vx_index* h, const float* rows, int64_t row0, int64_t n);
 /* Copy rows [row0, row0+n) (global ids inside this shard) back to the host. */

@@ -18,6 +18,13 @@
  *
  * Seeds used by the benches/tests: docs 42, queries 43,
  * query tokens 44, doc tokens 45.
+ *
+ * Distributions (dist): 0 = the isotropic rows above; 1 = ANISOTROPIC — before the
+ * normalisation v(row,col) is multiplied by the integer m(col) = (1 + 32 / (1 + col/4)) x
+ * (4 if col % 97 == 13 else 1): power-law per-dimension scale (the leading dimensions carry up
+ * to 33x the spread of the tail) plus sparse outlier dimensions (x4), the shape of real text
+ * embeddings that defeats one quantisation scale per shard.  Still exact integer arithmetic
+ * (|v m| < 2^25, sum of squares < 2^61).
  */
 #ifndef VX_SYNTH_H_
 #define VX_SYNTH_H_
@@ -44,6 +51,17 @@ VX_HD int32_t vx_synth_int(uint64_t seed, uint64_t row, uint64_t col) {
   int32_t s = (int32_t)(h & 0xFFFFu) + (int32_t)((h >> 16) & 0xFFFFu) +
               (int32_t)((h >> 32) & 0xFFFFu) + (int32_t)(h >> 48);
   return s - 131070;
+}
+
+/* Integer column multiplier of distribution dist (see the header comment). */
+VX_HD int32_t vx_synth_mult(uint32_t dist, uint64_t col) {
+  if (dist == 0) return 1;
+  const int32_t m = 1 + (int32_t)(32u / (1u + (uint32_t)(col / 4u)));
+  return (col % 97u == 13u) ? 4 * m : m;
+}
+
+VX_HD int32_t vx_synth_int_d(uint64_t seed, uint64_t row, uint64_t col, uint32_t dist) {
+  return vx_synth_int(seed, row, col) * vx_synth_mult(dist, col);
 }
 
 /* Final fp32 element given the row's exact integer sum of squares. */

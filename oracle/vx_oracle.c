@@ -23,6 +23,11 @@ int vxo_threads(void) { return omp_get_max_threads(); }
 static int nthreads_of(int32_t threads) { return threads > 0 ? threads : omp_get_max_threads(); }
 
 void vxo_synth_rows(uint64_t seed, int64_t row0, int64_t n, int32_t dim, float* out) {
+  vxo_synth_rows_dist(seed, row0, n, dim, 0, out);
+}
+
+void vxo_synth_rows_dist(uint64_t seed, int64_t row0, int64_t n, int32_t dim, int32_t dist,
+                         float* out) {
 #pragma omp parallel
   {
     int32_t* v = (int32_t*)malloc(sizeof(int32_t) * (size_t)dim);
@@ -30,7 +35,7 @@ void vxo_synth_rows(uint64_t seed, int64_t row0, int64_t n, int32_t dim, float* 
     for (int64_t r = 0; r < n; ++r) {
       int64_t ss = 0;
       for (int32_t c = 0; c < dim; ++c) {
-        v[c] = vx_synth_int(seed, (uint64_t)(row0 + r), (uint64_t)c);
+        v[c] = vx_synth_int_d(seed, (uint64_t)(row0 + r), (uint64_t)c, (uint32_t)dist);
         ss += (int64_t)v[c] * (int64_t)v[c];
       }
       float* o = out + r * (int64_t)dim;

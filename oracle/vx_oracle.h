@@ -45,6 +45,9 @@ int vxo_threads(void);
 
 /* Rows [row0, row0+n) of the synthetic matrix (vx_synth.h), fp32 [n][dim]. */
 void vxo_synth_rows(uint64_t seed, int64_t row0, int64_t n, int32_t dim, float* out);
+/* ... of distribution dist (0 isotropic, 1 anisotropic: vx_synth_mult). */
+void vxo_synth_rows_dist(uint64_t seed, int64_t row0, int64_t n, int32_t dim, int32_t dist,
+                         float* out);
 /* Token blocks [blk0, blk0+nblk): bf16 bits [nblk][ntok][dim]; block b token j is
  * synthetic row b*ntok + j. */
 void vxo_synth_tokens(uint64_t seed, int64_t blk0, int64_t nblk, int32_t ntok, int32_t dim,

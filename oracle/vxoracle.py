@@ -33,6 +33,8 @@ def lib():
         L.vxo_threads.restype = C.c_int
         L.vxo_synth_rows.argtypes = [u64, i64, i64, i32, fp]
         L.vxo_synth_rows.restype = None
+        L.vxo_synth_rows_dist.argtypes = [u64, i64, i64, i32, i32, fp]
+        L.vxo_synth_rows_dist.restype = None
         L.vxo_synth_tokens.argtypes = [u64, i64, i64, i32, i32, hp]
         L.vxo_synth_tokens.restype = None
         L.vxo_synth_token_blocks.argtypes = [u64, lp, i64, i32, i32, hp]
@@ -57,9 +59,9 @@ def threads() -> int:
     return lib().vxo_threads()
 
 
-def synth_rows(seed: int, row0: int, n: int, dim: int) -> np.ndarray:
+def synth_rows(seed: int, row0: int, n: int, dim: int, dist: int = 0) -> np.ndarray:
     out = np.empty((n, dim), np.float32)
-    lib().vxo_synth_rows(seed, row0, n, dim, _p(out, C.c_float))
+    lib().vxo_synth_rows_dist(seed, row0, n, dim, dist, _p(out, C.c_float))
     return out
 
 
@@ -147,7 +149,7 @@ def merge_topk(ids_a, sc_a, ids_b, sc_b, k):
     return out_i, out_s
 
 
-def flat_topk_synth(seed, n_docs, dim, Q, k, mode=F32, row0=0, chunk=1 << 20, threads=0):
+def flat_topk_synth(seed, n_docs, dim, Q, k, mode=F32, row0=0, chunk=1 << 20, threads=0, dist=0):
     """Exact top-k of Q over the synthetic rows [row0, row0 + n_docs) (vx_synth.h, seed),
     generated in chunks.  Returns (ids, scores, scan_seconds): scan_seconds times only the
     top-k passes (row generation is input preparation, untimed)."""
@@ -159,7 +161,7 @@ def flat_topk_synth(seed, n_docs, dim, Q, k, mode=F32, row0=0, chunk=1 << 20, th
     t_scan = 0.0
     for r0 in range(row0, row0 + n_docs, chunk):
         n = min(chunk, row0 + n_docs - r0)
-        X = synth_rows(seed, r0, n, dim)
+        X = synth_rows(seed, r0, n, dim, dist)
         t0 = time.perf_counter()
         ci, cs = flat_topk(X, Q, k, mode=mode, id_base=r0, threads=threads)
         t_scan += time.perf_counter() - t0

@@ -67,6 +67,7 @@ SIGNATURES = {
     "vx_get_stats": [P, C.POINTER(Stats)],
     "vx_reset_stats": [P],
     "vx_index_synth": [P, U64],
+    "vx_index_synth_dist": [P, U64, I32],
     "vx_index_upload": [P, FP, I64, I64],
     "vx_index_download": [P, FP, I64, I64],
     "vx_tokens_synth": [P, U64],

@@ -328,9 +328,12 @@ __device__ __forceinline__ float cert_err_bound(int fmt, int D, float qn, float 
                                                 const float* __restrict__ xstats) {
   float e;
   if (fmt == FMT_TF32) e = kErrCoefTF32 * qn * xstats[0];
-  else if (fmt == FMT_I8) e = qh * xstats[4] + qr * xstats[3] + qr * xstats[4];
+  // s8 (column scales s_c folded into the query, q' = q s): with x^ = s x8 and the query's
+  // coarse operand q~ = sq q8 / s, q.x - sq (q8.x8) = q.(x - x^) + (q' - sq q8).x8 exactly, so
+  // |err| <= |q| max|x - x^| + |q' - sq q8| max|x8|  (qr = |q' - sq q8|, xstats[3] = max|x8|)
+  else if (fmt == FMT_I8) e = qn * xstats[4] + qr * xstats[3];
   else e = qh * xstats[2] + qr * xstats[1] + qr * xstats[2];
-  const float xmax = fmaxf(xstats[0], fmt == FMT_I8 ? xstats[3] : xstats[1]);
+  const float xmax = fmt == FMT_I8 ? xstats[0] : fmaxf(xstats[0], xstats[1]);
   // fp32 accumulation slack: the exact in-order chain and the tensor core's fp32 sum each
   // err <= ~D 2^-24 |q||x| (2x margin for the tensor core's accumulation rounding): 2^-12
   // covers D <= 1008; longer rows scale it
@@ -342,16 +345,20 @@ __device__ __forceinline__ float cert_err_bound(int fmt, int D, float qn, float 
 // as the scan's operands) as squared-norm partial sums: |q|^2, |q^|^2, |q - q^|^2.  The
 // whole block reduces into red[0..2] (smem, 3 x 32 floats); also copies q into qs.
 __device__ __forceinline__ void query_norms(const float* __restrict__ q, int D, int fmt, float sq,
-                                            float* __restrict__ qs, float* red) {
+                                            float* __restrict__ qs, float* red,
+                                            const float* __restrict__ xstats) {
   float ss = 0.0f, sh = 0.0f, sr = 0.0f;
+  const float* colscale = xstats + kXstatColScale;
   for (int t = threadIdx.x; t < D; t += blockDim.x) {
     const float v = q[t];
-    const float vh = fmt == FMT_I8 ? sq * (float)vx_quant8(v, sq)
+    // s8: the residual of q' = q s (the scan's own q8 rounding, rows_to_i8_kernel)
+    const float vq = fmt == FMT_I8 ? v * colscale[t] : v;
+    const float vh = fmt == FMT_I8 ? sq * (float)vx_quant8(vq, sq)
                                    : vx_bf16_bits_to_f32(vx_f32_to_bf16_bits(v));
     if (qs) qs[t] = v;
     ss = fmaf(v, v, ss);
     sh = fmaf(vh, vh, sh);
-    sr = fmaf(v - vh, v - vh, sr);
+    sr = fmaf(vq - vh, vq - vh, sr);
   }
   for (int o = 16; o > 0; o >>= 1) {
     ss += __shfl_xor_sync(0xffffffffu, ss, o);
@@ -418,7 +425,7 @@ __global__ void __launch_bounds__(256)
   // coarse keys are in the coarse pass's units: the s8 pass scores sq * sx * (s32 dot)
   const float sq = fmt == FMT_I8 ? qscale[b] : 1.0f;
   const float cscale = fmt == FMT_I8 ? sq * xstats[5] : 1.0f;
-  query_norms(q, D, fmt, sq, qs, s_red);  // the certificate's error bound, below
+  query_norms(q, D, fmt, sq, qs, s_red, xstats);  // the certificate's error bound, below
   if (threadIdx.x == 0) {
     s_fail = 0;
     mbar_init(&s_bar[0], (uint32_t)rows_per_round);
@@ -691,7 +698,7 @@ __global__ void __launch_bounds__(256)
     while (np2 < M) np2 <<= 1;
     const float sq = fmt == FMT_I8 ? qscale[b] : 1.0f;
     const float cscale = fmt == FMT_I8 ? sq * xstats[5] : 1.0f;
-    query_norms(fq + (size_t)i * D, D, fmt, sq, nullptr, s_red);
+    query_norms(fq + (size_t)i * D, D, fmt, sq, nullptr, s_red, xstats);
     for (int j = threadIdx.x; j < np2; j += blockDim.x)
       keys[j] = j < M ? wkeys[(size_t)i * Mmax + j] : 0ull;
     __syncthreads();
@@ -747,10 +754,9 @@ __global__ void __launch_bounds__(256)
 // [2] max |x - bf16(x)| over the shard's rows (float bits, atomicMax of non-negative floats).
 __global__ void row_stats_kernel(const float* __restrict__ docs, int64_t n, int D,
                                  unsigned int* __restrict__ out_bits,
-                                 const float* __restrict__ i8_scale) {
+                                 const float* __restrict__ colscale) {
   const int lane = threadIdx.x & 31;
   const int64_t wpb = blockDim.x >> 5;
-  const float sx = i8_scale ? *i8_scale : 0.0f;
   float b0 = 0.0f, b1 = 0.0f, b2 = 0.0f, b3 = 0.0f, b4 = 0.0f, nsum = 0.0f;
   for (int64_t r = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); r < n;
        r += (int64_t)gridDim.x * wpb) {
@@ -762,10 +768,11 @@ __global__ void row_stats_kernel(const float* __restrict__ docs, int64_t n, int 
       s0 = fmaf(v, v, s0);
       s1 = fmaf(v16, v16, s1);
       s2 = fmaf(v - v16, v - v16, s2);
-      if (i8_scale) {
-        const float v8 = sx * (float)vx_quant8(v, sx);
-        s3 = fmaf(v8, v8, s3);
-        s4 = fmaf(v - v8, v - v8, s4);
+      if (colscale) {  // s8 shadow with column scales: |x8| (integer) and |x - s x8|
+        const float sc = colscale[c];
+        const float q8 = sc > 0.0f ? (float)vx_quant8(v, sc) : 0.0f;
+        s3 = fmaf(q8, q8, s3);
+        s4 = fmaf(v - sc * q8, v - sc * q8, s4);
       }
     }
     for (int o = 16; o > 0; o >>= 1) {
@@ -787,8 +794,8 @@ __global__ void row_stats_kernel(const float* __restrict__ docs, int64_t n, int 
     atomicMax(&out_bits[1], __float_as_uint(b1 * 1.00001f));
     atomicMax(&out_bits[2], __float_as_uint(b2 * 1.00001f));
     atomicAdd(reinterpret_cast<float*>(out_bits) + 7, nsum);  // sum of row norms (heuristics)
-    if (i8_scale) {  // s x8 is rounded to fp32 here: 1e-3 of margin for the residual norms
-      atomicMax(&out_bits[3], __float_as_uint(b3 * 1.001f));
+    if (colscale) {  // s x8 is rounded to fp32 here: 1e-3 of margin for the residual norm
+      atomicMax(&out_bits[3], __float_as_uint(b3 * 1.00001f));  // integer squares: exact sum
       atomicMax(&out_bits[4], __float_as_uint(b4 * 1.001f));
     }
   }
@@ -953,13 +960,14 @@ cudaError_t launch_shard_tau(const float* all, int G, int B, int k, float* tau, 
 }
 
 cudaError_t launch_row_stats(const float* docs, int64_t n, int D, unsigned int* out_bits,
-                             cudaStream_t st, const float* i8_scale) {
-  cudaError_t e = cudaMemsetAsync(out_bits, 0, 20, st);  // [0..4]; [5] = the s8 scale
+                             cudaStream_t st, const float* colscale) {
+  cudaError_t e = cudaMemsetAsync(out_bits, 0, 20, st);  // [0..4]; [5] = the s8 doc factor
   if (e == cudaSuccess) e = cudaMemsetAsync(out_bits + 7, 0, 4, st);  // [7] = sum of |x|
   if (e != cudaSuccess) return e;
   int64_t blocks = (n + 7) / 8;
   if (blocks > 148 * 32) blocks = 148 * 32;
-  row_stats_kernel<<<(int)(blocks < 1 ? 1 : blocks), 256, 0, st>>>(docs, n, D, out_bits, i8_scale);
+  if (blocks < 1) blocks = 1;
+  row_stats_kernel<<<(int)blocks, 256, 0, st>>>(docs, n, D, out_bits, colscale);
   return cudaGetLastError();
 }
 

@@ -11,21 +11,21 @@ namespace vx {
 
 template <typename OutT, bool kBf16>
 __global__ void synth_rows_kernel(OutT* __restrict__ out, uint64_t seed, int64_t row0,
-                                  int64_t n, int D) {
+                                  int64_t n, int D, uint32_t dist = 0) {
   const int lane = threadIdx.x & 31;
   const int64_t wpb = blockDim.x >> 5;
   for (int64_t r = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); r < n;
        r += (int64_t)gridDim.x * wpb) {
     int64_t ss = 0;
     for (int c = lane; c < D; c += 32) {
-      int64_t v = vx_synth_int(seed, (uint64_t)(row0 + r), (uint64_t)c);
+      int64_t v = vx_synth_int_d(seed, (uint64_t)(row0 + r), (uint64_t)c, dist);
       ss += v * v;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
     OutT* o = out + r * (int64_t)D;
     for (int c = lane; c < D; c += 32) {
-      float x = vx_synth_finish(vx_synth_int(seed, (uint64_t)(row0 + r), (uint64_t)c), ss);
+      float x = vx_synth_finish(vx_synth_int_d(seed, (uint64_t)(row0 + r), (uint64_t)c, dist), ss);
       if constexpr (kBf16)
         o[c] = vx_f32_to_bf16_bits(x);
       else
@@ -41,8 +41,8 @@ static int fill_grid(int64_t rows) {
 }
 
 cudaError_t launch_synth_rows(float* out, uint64_t seed, int64_t row0, int64_t n, int D,
-                              cudaStream_t st) {
-  synth_rows_kernel<float, false><<<fill_grid(n), 256, 0, st>>>(out, seed, row0, n, D);
+                              cudaStream_t st, uint32_t dist) {
+  synth_rows_kernel<float, false><<<fill_grid(n), 256, 0, st>>>(out, seed, row0, n, D, dist);
   return cudaGetLastError();
 }
 
@@ -97,52 +97,73 @@ cudaError_t launch_split_bf16(const float* in, uint16_t* out, int64_t n, cudaStr
 // for a fixed query every document's s32 dot product is in the same units and the scan can
 // select on the raw integer; queries use one scale per row, sq = max|q| / 127.  Rounding:
 // v8 = clamp(rint(v / s), -127, 127); the certificate bounds the residual v - s * v8.
-__global__ void absmax_kernel(const float4* __restrict__ in, int64_t n4, unsigned int* out_bits) {
-  float m = 0.0f;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const float4 v = in[i];
-    m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+// Per-column maxima: a block walks rows (coalesced: threads own columns), keeps its columns'
+// running |max| in registers (D <= 1024 = 4 per thread) and folds them with one atomicMax
+// per column at the end (float bits of non-negative values order like the floats).
+__global__ void col_absmax_kernel(const float* __restrict__ in, int64_t n, int D,
+                                  unsigned int* __restrict__ colmax_bits) {
+  float m[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  for (int64_t r = blockIdx.x; r < n; r += gridDim.x) {
+    const float* x = in + r * D;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = threadIdx.x + j * blockDim.x;
+      if (c < D) m[j] = fmaxf(m[j], fabsf(x[c]));
+    }
   }
-  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(out_bits, __float_as_uint(m));
-}
-
-__global__ void to_i8_kernel(const float4* __restrict__ in, int64_t n4,
-                             const unsigned int* __restrict__ absmax_bits, char4* __restrict__ out,
-                             float* __restrict__ scale_out) {
-  const float mx = __uint_as_float(*absmax_bits);
-  const float sc = mx > 0.0f ? mx / 127.0f : 1.0f;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *scale_out = sc;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const float4 v = in[i];
-    out[i] = make_char4(vx_quant8(v.x, sc), vx_quant8(v.y, sc), vx_quant8(v.z, sc), vx_quant8(v.w, sc));
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int c = threadIdx.x + j * blockDim.x;
+    if (c < D) atomicMax(&colmax_bits[c], __float_as_uint(m[j]));
   }
 }
 
-cudaError_t launch_to_i8_shadow(const float* in, int64_t n, int8_t* out, unsigned int* absmax_bits,
-                                float* scale_out, cudaStream_t st) {
-  if (n % 4) return cudaErrorInvalidValue;
-  const int64_t n4 = n / 4;
+__global__ void col_scale_kernel(const unsigned int* __restrict__ colmax_bits, int D,
+                                 float* __restrict__ colscale) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < D) {
+    const float mx = __uint_as_float(colmax_bits[c]);
+    colscale[c] = mx > 0.0f ? mx / 127.0f : 0.0f;
+  }
+}
+
+__global__ void to_i8_cols_kernel(const float4* __restrict__ in, int64_t n4, int D4,
+                                  const float4* __restrict__ colscale, char4* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = in[i];
+    const float4 s = colscale[i % D4];
+    out[i] = make_char4(s.x > 0.0f ? vx_quant8(v.x, s.x) : 0, s.y > 0.0f ? vx_quant8(v.y, s.y) : 0,
+                        s.z > 0.0f ? vx_quant8(v.z, s.z) : 0, s.w > 0.0f ? vx_quant8(v.w, s.w) : 0);
+  }
+}
+
+cudaError_t launch_to_i8_shadow(const float* in, int64_t n, int D, int8_t* out,
+                                unsigned int* colmax_bits, float* colscale, cudaStream_t st) {
+  if (D % 4 || D > 1024) return cudaErrorInvalidValue;
+  cudaError_t e = cudaMemsetAsync(colmax_bits, 0, (size_t)D * 4, st);
+  if (e != cudaSuccess) return e;
+  int64_t rb = n < 148 * 8 ? n : 148 * 8;
+  col_absmax_kernel<<<(int)(rb < 1 ? 1 : rb), 256, 0, st>>>(in, n, D, colmax_bits);
+  col_scale_kernel<<<(D + 255) / 256, 256, 0, st>>>(colmax_bits, D, colscale);
+  const int64_t n4 = n * D / 4;
   int64_t blocks = (n4 + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
-  cudaError_t e = cudaMemsetAsync(absmax_bits, 0, 4, st);
-  if (e != cudaSuccess) return e;
-  absmax_kernel<<<(int)blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(in), n4, absmax_bits);
-  to_i8_kernel<<<(int)blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(in), n4, absmax_bits,
-                                            reinterpret_cast<char4*>(out), scale_out);
+  to_i8_cols_kernel<<<(int)blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(in), n4, D / 4,
+                                                 reinterpret_cast<const float4*>(colscale),
+                                                 reinterpret_cast<char4*>(out));
   return cudaGetLastError();
 }
 
-// per-row scales (queries): one block per row
-__global__ void rows_to_i8_kernel(const float* __restrict__ in, int D, int8_t* __restrict__ out,
+// per-row scales (queries), document column scales folded in: one block per row
+__global__ void rows_to_i8_kernel(const float* __restrict__ in, int D,
+                                  const float* __restrict__ colscale, int8_t* __restrict__ out,
                                   float* __restrict__ scales) {
   __shared__ float s_m[32];
   const float* x = in + (size_t)blockIdx.x * D;
   float m = 0.0f;
-  for (int t = threadIdx.x; t < D; t += blockDim.x) m = fmaxf(m, fabsf(x[t]));
+  for (int t = threadIdx.x; t < D; t += blockDim.x) m = fmaxf(m, fabsf(x[t] * colscale[t]));
   for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
   if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = m;
   __syncthreads();
@@ -154,12 +175,13 @@ __global__ void rows_to_i8_kernel(const float* __restrict__ in, int D, int8_t* _
   __syncthreads();
   const float sc = s_m[0];
   if (threadIdx.x == 0) scales[blockIdx.x] = sc;
-  for (int t = threadIdx.x; t < D; t += blockDim.x) out[(size_t)blockIdx.x * D + t] = vx_quant8(x[t], sc);
+  for (int t = threadIdx.x; t < D; t += blockDim.x)
+    out[(size_t)blockIdx.x * D + t] = vx_quant8(x[t] * colscale[t], sc);
 }
 
-cudaError_t launch_rows_to_i8(const float* in, int B, int D, int8_t* out, float* scales,
-                              cudaStream_t st) {
-  rows_to_i8_kernel<<<B, 256, 0, st>>>(in, D, out, scales);
+cudaError_t launch_rows_to_i8(const float* in, int B, int D, const float* colscale, int8_t* out,
+                              float* scales, cudaStream_t st) {
+  rows_to_i8_kernel<<<B, 256, 0, st>>>(in, D, colscale, out, scales);
   return cudaGetLastError();
 }
 

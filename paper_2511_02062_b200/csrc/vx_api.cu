@@ -179,7 +179,8 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
   ALLOC(h->d_ckeys, B * 1024 * 8);
   ALLOC(h->d_seedk, B * 32 * 8);
   ALLOC(h->d_flags, B * 4);
-  ALLOC(h->d_xnorm, 32);
+  ALLOC(h->d_xnorm, (8 + D) * 4);  // shard statistics + the s8 column scales
+  ALLOC(h->d_colmax, D * 4);
   ALLOC(h->d_fq, B * D * 4);
   ALLOC(h->d_fidx, B * 4);
   ALLOC(h->d_fcount, 16);
@@ -216,7 +217,7 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
     return cleanup(fail(VX_ERR_OOM, "pinned header"));
   if (cudaMallocHost((void**)&h->h_flags, B * 4) != cudaSuccess)
     return cleanup(fail(VX_ERR_OOM, "pinned flags"));
-  if (cudaMemset(h->d_xnorm, 0, 32) != cudaSuccess || cudaMemset(h->d_fcount, 0, 16) != cudaSuccess ||
+  if (cudaMemset(h->d_xnorm, 0, (8 + D) * 4) != cudaSuccess || cudaMemset(h->d_fcount, 0, 16) != cudaSuccess ||
       ktimer_reset(h) != VX_OK)
     return cleanup(fail(VX_ERR_CUDA, "memset"));
   if (h->tokens) {
@@ -259,7 +260,7 @@ extern "C" vx_status vx_index_destroy(vx_index* h) {
                   h->d_out_ms, h->d_send, h->d_recv, h->d_hdr, h->d_ckeys, h->d_seedk, h->d_flags,
                   h->d_xnorm, h->d_fq, h->docs16, h->d_q16, h->d_fidx, h->d_fcount,
                   h->d_qtok16, h->docs8, h->d_q8, h->d_qs8, h->d_lball, h->d_tau, h->d_hkeys,
-                  h->d_ktimer};
+                  h->d_ktimer, h->d_colmax};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->h_stage) cudaFreeHost(h->h_stage);
@@ -385,14 +386,19 @@ extern "C" vx_status vx_reset_stats(vx_index* h) {
 static vx_status refresh_shadows(vx_index* h, int64_t row_off, int64_t nrows) {
   const int64_t D = h->desc.dim;
   drop_graphs(h);  // the AUTO coarse format and the certificate inputs may change
-  float* sx = reinterpret_cast<float*>(h->d_xnorm) + 5;
+  float* colscale = reinterpret_cast<float*>(h->d_xnorm) + vx::kXstatColScale;
   if (h->docs8) {
-    CU_TRY(vx::launch_to_i8_shadow(h->docs, h->n_local * D, h->docs8, h->d_xnorm + 6, sx,
+    // column scales, then the shadow; the s8 coarse units' document factor xstats[5] = 1
+    // (the scales ride on the query side, vx::launch_rows_to_i8)
+    CU_TRY(vx::launch_to_i8_shadow(h->docs, h->n_local, (int)D, h->docs8, h->d_colmax, colscale,
                                    h->stream));
-    count_launch(h, 2);
+    const float one = 1.0f;
+    CU_TRY(cudaMemcpyAsync(h->d_xnorm + 5, &one, 4, cudaMemcpyHostToDevice, h->stream));
+    CU_TRY(cudaStreamSynchronize(h->stream));  // `one` is a host stack value
+    count_launch(h, 3);
   }
   CU_TRY(vx::launch_row_stats(h->docs, h->n_local, (int)D, h->d_xnorm, h->stream,
-                              h->docs8 ? sx : nullptr));
+                              h->docs8 ? colscale : nullptr));
   count_launch(h);
   if (h->docs16 && nrows > 0) {
     CU_TRY(vx::launch_to_bf16(h->docs + row_off * D, h->docs16 + row_off * D, nrows * D,
@@ -407,9 +413,15 @@ static vx_status refresh_shadows(vx_index* h, int64_t row_off, int64_t nrows) {
 }
 
 extern "C" vx_status vx_index_synth(vx_index* h, uint64_t seed) {
+  return vx_index_synth_dist(h, seed, 0);
+}
+
+extern "C" vx_status vx_index_synth_dist(vx_index* h, uint64_t seed, int32_t dist) {
   if (!h) return fail(VX_ERR_INVALID, "null handle");
+  if (dist != 0 && dist != 1) return fail(VX_ERR_INVALID, "dist %d (0 isotropic, 1 anisotropic)", dist);
   CU_TRY(cudaSetDevice(h->device));
-  CU_TRY(vx::launch_synth_rows(h->docs, seed, h->row0, h->n_local, h->desc.dim, h->stream));
+  CU_TRY(vx::launch_synth_rows(h->docs, seed, h->row0, h->n_local, h->desc.dim, h->stream,
+                               (uint32_t)dist));
   count_launch(h);
   VX_TRY(refresh_shadows(h, 0, h->n_local));
   CU_TRY(cudaStreamSynchronize(h->stream));

@@ -127,6 +127,7 @@ struct vx_index {
   unsigned int* d_xnorm = nullptr;  // [8] shard maxima (float bits, row_stats): |x|, |bf16 x|,
                                     // |x-bf16 x|, |sx x8|, |x-sx x8|; [5] sx; [6] scratch;
                                     // [7] sum of row norms (AUTO coarse heuristic)
+  unsigned int* d_colmax = nullptr;  // [D] scratch: per-column |max| (s8 column scales)
   float* d_fq = nullptr;         // [maxB][D] queries gathered for the exact fallback
   int* d_fidx = nullptr;         // [maxB] flagged query indices
   int* d_fcount = nullptr;       // [2] flagged count of the last batch, running total

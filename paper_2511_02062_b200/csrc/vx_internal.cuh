@@ -77,12 +77,21 @@ __device__ __forceinline__ float seed_thr(const uint64_t* seed, int ld, int q) {
 // from the actual rounding residuals (rerank_kernel in scan_tc.cu).
 constexpr float kErrCoefTF32 = 0.001953125f;
 cudaError_t launch_to_bf16(const float* in, uint16_t* out, int64_t n, cudaStream_t st);
-// s8 shadow of n fp32 values with one scale (max|x| / 127, written to *scale_out)
-cudaError_t launch_to_i8_shadow(const float* in, int64_t n, int8_t* out, unsigned int* absmax_bits,
-                                float* scale_out, cudaStream_t st);
-// s8 copy of B rows of D with per-row scales (queries)
-cudaError_t launch_rows_to_i8(const float* in, int B, int D, int8_t* out, float* scales,
-                              cudaStream_t st);
+// s8 shadow of an n x D fp32 shard with ONE SCALE PER COLUMN: s_c = max_r |x[r][c]| / 127
+// (0 for an all-zero column), x8[r][c] = rint(x[r][c] / s_c).  colmax_bits: D words of
+// scratch; colscale: the D scales.
+cudaError_t launch_to_i8_shadow(const float* in, int64_t n, int D, int8_t* out,
+                                unsigned int* colmax_bits, float* colscale, cudaStream_t st);
+// s8 copy of B query rows of D: q'[c] = q[c] s_c folds the document column scales into the
+// query, then one scale per row sq = max|q'| / 127, q8 = rint(q' / sq); sq * (q8 . x8)
+// approximates q . x (the certificate bounds the difference, scan_tc.cu cert_err_bound)
+cudaError_t launch_rows_to_i8(const float* in, int B, int D, const float* colscale, int8_t* out,
+                              float* scales, cudaStream_t st);
+// xstats layout (d_xnorm, floats): [0] max|x|, [1] max|bf16 x|, [2] max|x - bf16 x|,
+// [3] max|x8| (integer norm of the s8 row), [4] max|x - x^| (x^[c] = s_c x8[c]), [5] the s8
+// coarse units' document factor (1: the column scales live in the query), [6] scratch,
+// [7] sum of |x|; [8 .. 8+D) the column scales s_c
+constexpr int kXstatColScale = 8;
 // Coarse operand formats of the tensor-core scan (ScanTcArgs::fmt)
 enum : int { FMT_BF16 = 1, FMT_TF32 = 2, FMT_I8 = 3 };
 // Per-CTA (per-pair) candidate list length per query: 16, or 32 for the s8 coarse pass,
@@ -126,10 +135,10 @@ cudaError_t launch_rerank_wide(const float* docs, const float* fq, int D, const 
                                uint64_t* wkeys, uint64_t* out_keys, int64_t* out_ids,
                                float* out_scores, int* flags, cudaStream_t st,
                                const uint64_t* seed = nullptr, int seed_ld = 0);
-// per-shard maxima [max|x|, max|bf16(x)|, max|x - bf16(x)|] (3 floats as uint bits) and, when
-// i8_scale is given, [3] max|sx x8|, [4] max|x - sx x8| of the s8 shadow
+// per-shard maxima [max|x|, max|bf16(x)|, max|x - bf16(x)|] (floats as uint bits) and, when
+// the s8 column scales are given, [3] max|x8| (integer norm), [4] max|x - s x8|
 cudaError_t launch_row_stats(const float* docs, int64_t n, int D, unsigned int* out_bits,
-                             cudaStream_t st, const float* i8_scale = nullptr);
+                             cudaStream_t st, const float* colscale = nullptr);
 
 // -------- top-k merge (K3): topk.cu
 // For each query q: select the k largest keys among in[q][0..M), write them
@@ -155,7 +164,7 @@ cudaError_t launch_order_by(const float* key_score, const int64_t* ids, const fl
 
 // -------- synthetic fill: synth.cu
 cudaError_t launch_synth_rows(float* out, uint64_t seed, int64_t row0, int64_t n, int D,
-                              cudaStream_t st);
+                              cudaStream_t st, uint32_t dist = 0);
 cudaError_t launch_synth_tokens(uint16_t* out, uint64_t seed, int64_t blk0, int64_t nblk, int Nd,
                                 int d, cudaStream_t st);
 

@@ -129,7 +129,9 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
     CU_TRY(vx::launch_to_bf16(d_q, h->d_q16, (int64_t)B * D, st));
     count_launch(h);
   } else if (i8) {
-    CU_TRY(vx::launch_rows_to_i8(d_q, B, D, h->d_q8, h->d_qs8, st));
+    CU_TRY(vx::launch_rows_to_i8(d_q, B, D,
+                                 reinterpret_cast<const float*>(h->d_xnorm) + vx::kXstatColScale,
+                                 h->d_q8, h->d_qs8, st));
     count_launch(h);
   }
   // queries per pass over the index: 512 (default, CTA pairs with two query groups on

@@ -90,8 +90,9 @@ class Index:
         check(self.lib.vx_reset_stats(self._h))
 
     # -- data ---------------------------------------------------------------------------
-    def synth(self, seed: int = 42) -> None:
-        check(self.lib.vx_index_synth(self._h, seed))
+    def synth(self, seed: int = 42, dist: int = 0) -> None:
+        """Device fill with the vx_synth.h generator; dist 1 = anisotropic rows."""
+        check(self.lib.vx_index_synth_dist(self._h, seed, dist))
 
     def upload(self, rows: np.ndarray, row0: int | None = None) -> None:
         rows = _f32(rows)

@@ -14,7 +14,16 @@ def _splitmix64(x: np.ndarray) -> np.ndarray:
         return x ^ (x >> np.uint64(31))
 
 
-def rows(seed: int, row0: int, n: int, dim: int) -> np.ndarray:
+def mult(dist: int, dim: int) -> np.ndarray:
+    """vx_synth_mult: integer column multipliers of distribution dist (1: anisotropic)."""
+    c = np.arange(dim, dtype=np.int64)
+    if dist == 0:
+        return np.ones(dim, np.int64)
+    m = 1 + 32 // (1 + c // 4)
+    return np.where(c % 97 == 13, 4 * m, m)
+
+
+def rows(seed: int, row0: int, n: int, dim: int, dist: int = 0) -> np.ndarray:
     """Rows [row0, row0+n) of the unit-norm synthetic matrix, fp32 [n][dim]."""
     r = np.arange(row0, row0 + n, dtype=np.uint64)[:, None]
     c = np.arange(dim, dtype=np.uint64)[None, :]
@@ -24,12 +33,13 @@ def rows(seed: int, row0: int, n: int, dim: int) -> np.ndarray:
     m = np.uint64(0xFFFF)
     v = ((h & m) + ((h >> np.uint64(16)) & m) + ((h >> np.uint64(32)) & m)
          + (h >> np.uint64(48))).astype(np.int64) - 131070
+    v = v * mult(dist, dim)[None, :]
     nrm = np.sqrt((v * v).sum(axis=1).astype(np.float64))
     return (v.astype(np.float64) / nrm[:, None]).astype(np.float32)
 
 
-def queries(B: int, dim: int, seed: int = 43) -> np.ndarray:
-    return rows(seed, 0, B, dim)
+def queries(B: int, dim: int, seed: int = 43, dist: int = 0) -> np.ndarray:
+    return rows(seed, 0, B, dim, dist)
 
 
 def query_tokens(B: int, nq: int, dim: int, seed: int = 44) -> np.ndarray:

@@ -65,9 +65,9 @@ def test_upload_refreshes_shadow(vx, oracle):
 
 def test_auto_coarse_follows_quantisation_quality(vx, oracle):
     # AUTO takes the s8 pass when the shard is long enough (>= 16 tiles of 256 rows per CTA)
-    # and its one-scale quantisation is tight (max residual norm <= 3 % of the mean row norm:
-    # the synthetic rows are at ~1 %), bf16 when an outlier coordinate inflates the shared
-    # scale or the shard is short — exact either way
+    # and its per-column quantisation is tight (max residual norm <= 3 % of the mean row norm:
+    # the synthetic rows are at ~1 %), bf16 when an outlier inflates a column scale so far that
+    # the other rows lose that coordinate, or the shard is short — exact either way
     N, D, B, k = 700_000, 256, 24, 10
     X = oracle.synth_rows(42, 0, N, D)
     Q = oracle.synth_rows(43, 0, B, D)
@@ -163,3 +163,40 @@ def test_seeded_scan_exact_when_the_sample_is_unrepresentative(vx, oracle, coars
     rid, rsc = oracle.flat_topk(X, Q, k, mode=1)
     assert np.array_equal(ids, rid)
     assert np.array_equal(sc, rsc.astype(np.float32))
+
+
+@pytest.mark.parametrize("B,k", [(24, 10), (300, 100)])
+def test_anisotropic_rows_keep_s8_and_stay_exact(vx, oracle, B, k):
+    # power-law per-dimension scales + outlier dimensions (vx_synth.h dist 1): one scale per
+    # shard would leave the tail dimensions a few quantisation steps and push AUTO to bf16;
+    # per-column scales keep the s8 residual small, AUTO stays on s8, results exact
+    N, D = 700_000, 768
+    X = oracle.synth_rows(42, 0, N, D, 1)
+    Q = oracle.synth_rows(43, 0, B, D, 1)
+    with vx.Index(N, D, max_batch=B, max_k=k) as idx:
+        idx.synth(42, dist=1)
+        assert np.array_equal(idx.download(1000, 64).view(np.uint32), X[1000:1064].view(np.uint32))
+        assert idx.coarse_auto() == "i8"
+        ids, sc = idx.search(Q, k)
+        st = idx.stats()
+    rid, rsc = oracle.flat_topk(X, Q, k, mode=1)
+    assert np.array_equal(ids, rid) and np.array_equal(sc, rsc.astype(np.float32))
+    print(f"anisotropic B={B}: cert level2 {st['cert_level2']}, re-scans {st['cert_fallbacks']}")
+
+
+def test_outlier_row_switches_auto_to_bf16(vx, oracle):
+    # a row 1000x longer than the rest inflates EVERY column scale: the other rows quantise
+    # to ~0 and AUTO must leave s8
+    N, D, B, k = 700_000, 256, 8, 10
+    X = oracle.synth_rows(42, 0, N, D)
+    Q = oracle.synth_rows(43, 0, B, D)
+    with vx.Index(N, D, max_batch=B, max_k=k) as idx:
+        idx.upload(X, 0)
+        assert idx.coarse_auto() == "i8"
+        Xo = X.copy()
+        Xo[77] *= 1000.0
+        idx.upload(Xo[77:78], 77)
+        assert idx.coarse_auto() == "bf16"
+        ids, sc = idx.search(Q, k)
+    rid, rsc = oracle.flat_topk(Xo, Q, k, mode=1)
+    assert np.array_equal(ids, rid) and np.array_equal(sc, rsc.astype(np.float32))

@@ -180,3 +180,22 @@ def test_stagecheck_accepts_near_ties_and_rejects_real_swaps():
                           rid, rip, np.array([5.0, 4.9, 5.0]))
     with pytest.raises(AssertionError):  # an IP score off by one ulp
         check_stage_query(np.array([1, 2, 3]), np.nextafter(np.float32(rip), 2), truth, rid, rip, truth)
+
+
+def test_anisotropic_generator_matches_numpy_restatement(oracle):
+    """vx_synth.h dist 1 (anisotropic): the C oracle, the numpy host generator and (on the GPU,
+    tests/test_gpu_coarse.py) the device fill agree bit for bit."""
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    from paper_2511_02062_b200 import synth
+    for dist in (0, 1):
+        a = oracle.synth_rows(42, 123_456, 40, 768, dist)
+        b = synth.rows(42, 123_456, 40, 768, dist)
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+        assert np.allclose(np.linalg.norm(a.astype(np.float64), axis=1), 1.0, atol=1e-6)
+    m = synth.mult(1, 768)
+    assert m[0] == 33 and m[13] == 4 * 1 + 4 * 32 // 4 and m.min() == 1
+    # the anisotropy the bench's --dist aniso runs on: leading dims ~20x the tail's spread
+    a = oracle.synth_rows(42, 0, 2000, 768, 1)
+    assert a[:, :4].std() > 15 * a[:, 400:].std()
