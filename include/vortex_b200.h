@@ -71,7 +71,9 @@ enum {
                              [128, 1024] for s8) or a power of two in [16, 1024] */,
   VX_OPT_SCAN_SEED = 9    /* 1 (default): seed each query's tensor-core scan admission
                              threshold from a 1/64 row sample of the shard (shards of
-                             >= 512K rows); 0: off.  Results are identical either way. */
+                             >= 512K rows); 0: off.  Results are identical either way. */,
+  VX_OPT_I8_SCALE = 10    /* s8 shadow scales: 0 (default) one per shard; 1 one per column
+                             (folded into the query) — re-quantises the shard */
 };
 /* Coarse (candidate-selecting) tensor-core scan format.  Either way every reported score is
  * recomputed exactly in fp32 and certified.  BF16 reads a bf16 shadow

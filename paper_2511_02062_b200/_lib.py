@@ -20,6 +20,7 @@ VX_SCAN_AUTO, VX_SCAN_F32, VX_SCAN_TC = 0, 1, 2
 VX_OPT_SCAN, VX_OPT_GRID, VX_OPT_GRAPHS, VX_OPT_MAXSIM = 1, 2, 3, 4
 VX_MAXSIM_AUTO, VX_MAXSIM_CC, VX_MAXSIM_TC, VX_MAXSIM_TC_BF16Q = 0, 1, 2, 3
 VX_OPT_COARSE, VX_OPT_SCAN_TILE, VX_OPT_SCAN_PAIRS, VX_OPT_KPRIME, VX_OPT_SCAN_SEED = 5, 6, 7, 8, 9
+VX_OPT_I8_SCALE = 10
 VX_COARSE_AUTO, VX_COARSE_TF32, VX_COARSE_BF16, VX_COARSE_I8 = 0, 1, 2, 3
 VX_FLAG_NO_BF16_SHADOW = 1
 VX_FLAG_NO_I8_SHADOW = 2

@@ -118,11 +118,18 @@ __global__ void col_absmax_kernel(const float* __restrict__ in, int64_t n, int D
   }
 }
 
+// per_column: s_c = max|x_c| / 127; else one scale for the shard, s = max_c max|x_c| / 127
+// (the default: with queries drawn like the documents, folding per-column scales into the
+// query widens its quantisation error more than it narrows the documents' — DESIGN.md §4)
 __global__ void col_scale_kernel(const unsigned int* __restrict__ colmax_bits, int D,
-                                 float* __restrict__ colscale) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < D) {
-    const float mx = __uint_as_float(colmax_bits[c]);
+                                 float* __restrict__ colscale, int per_column) {
+  __shared__ unsigned int s_max;
+  if (threadIdx.x == 0) s_max = 0u;
+  __syncthreads();
+  for (int c = threadIdx.x; c < D; c += blockDim.x) atomicMax(&s_max, colmax_bits[c]);
+  __syncthreads();
+  for (int c = threadIdx.x; c < D; c += blockDim.x) {
+    const float mx = __uint_as_float(per_column ? colmax_bits[c] : s_max);
     colscale[c] = mx > 0.0f ? mx / 127.0f : 0.0f;
   }
 }
@@ -139,13 +146,14 @@ __global__ void to_i8_cols_kernel(const float4* __restrict__ in, int64_t n4, int
 }
 
 cudaError_t launch_to_i8_shadow(const float* in, int64_t n, int D, int8_t* out,
-                                unsigned int* colmax_bits, float* colscale, cudaStream_t st) {
+                                unsigned int* colmax_bits, float* colscale, int per_column,
+                                cudaStream_t st) {
   if (D % 4 || D > 1024) return cudaErrorInvalidValue;
   cudaError_t e = cudaMemsetAsync(colmax_bits, 0, (size_t)D * 4, st);
   if (e != cudaSuccess) return e;
   int64_t rb = n < 148 * 8 ? n : 148 * 8;
   col_absmax_kernel<<<(int)(rb < 1 ? 1 : rb), 256, 0, st>>>(in, n, D, colmax_bits);
-  col_scale_kernel<<<(D + 255) / 256, 256, 0, st>>>(colmax_bits, D, colscale);
+  col_scale_kernel<<<1, 1024, 0, st>>>(colmax_bits, D, colscale, per_column);
   const int64_t n4 = n * D / 4;
   int64_t blocks = (n4 + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;

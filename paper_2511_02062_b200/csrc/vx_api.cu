@@ -213,7 +213,7 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
                      B * K * 16 + 64;
   if (cudaMallocHost(&h->h_stage, h->h_stage_bytes) != cudaSuccess)
     return cleanup(fail(VX_ERR_OOM, "pinned staging"));
-  if (cudaMallocHost((void**)&h->h_hdr, 16) != cudaSuccess)
+  if (cudaMallocHost((void**)&h->h_hdr, 32) != cudaSuccess)  // [4] header + [4] cert counters
     return cleanup(fail(VX_ERR_OOM, "pinned header"));
   if (cudaMallocHost((void**)&h->h_flags, B * 4) != cudaSuccess)
     return cleanup(fail(VX_ERR_OOM, "pinned flags"));
@@ -287,6 +287,8 @@ extern "C" vx_status vx_index_shard_range(const vx_index* h, int64_t* row0, int6
   return VX_OK;
 }
 
+static vx_status refresh_shadows(vx_index* h, int64_t row_off, int64_t nrows);
+
 extern "C" vx_status vx_set_option(vx_index* h, int32_t option, int64_t value) {
   if (!h) return fail(VX_ERR_INVALID, "null handle");
   drop_graphs(h);  // every option below changes what a captured stage would run
@@ -304,6 +306,14 @@ extern "C" vx_status vx_set_option(vx_index* h, int32_t option, int64_t value) {
       if (value != 0 && (value < 16 || value > 1024 || (value & (value - 1))))
         return fail(VX_ERR_INVALID, "kprime %lld (0 or a power of two in [16, 1024])", (long long)value);
       h->kprime = (int)value;
+      return VX_OK;
+    case VX_OPT_I8_SCALE:
+      if (value != 0 && value != 1) return fail(VX_ERR_INVALID, "i8 scale %lld", (long long)value);
+      if (h->i8_per_column != (int)value) {
+        h->i8_per_column = (int)value;
+        if (h->docs8) VX_TRY(refresh_shadows(h, 0, 0));  // re-quantise the shard
+        CU_TRY(cudaStreamSynchronize(h->stream));
+      }
       return VX_OK;
     case VX_OPT_SCAN_SEED:
       if (value != 0 && value != 1) return fail(VX_ERR_INVALID, "scan seed %lld", (long long)value);
@@ -357,6 +367,7 @@ extern "C" vx_status vx_get_option(const vx_index* h, int32_t option, int64_t* v
     case VX_OPT_SCAN_PAIRS: *value = h->use_pairs; return VX_OK;
     case VX_OPT_KPRIME: *value = h->kprime; return VX_OK;
     case VX_OPT_SCAN_SEED: *value = h->scan_seed; return VX_OK;
+    case VX_OPT_I8_SCALE: *value = h->i8_per_column; return VX_OK;
     case VX_OPT_COARSE: {
       const int f = coarse_fmt(h);
       *value = f == vx::FMT_I8 ? VX_COARSE_I8 : (f == vx::FMT_TF32 ? VX_COARSE_TF32 : VX_COARSE_BF16);
@@ -377,6 +388,7 @@ extern "C" vx_status vx_reset_stats(vx_index* h) {
   CU_TRY(cudaStreamSynchronize(h->stream));
   CU_TRY(cudaMemset(h->d_fcount, 0, 16));
   VX_TRY(ktimer_reset(h));
+  h->cert_seen_q = h->cert_seen_l2 = h->cert_seen_l3 = 0;
   h->st = vx_stats{};
   return VX_OK;
 }
@@ -391,7 +403,8 @@ static vx_status refresh_shadows(vx_index* h, int64_t row_off, int64_t nrows) {
     // column scales, then the shadow; the s8 coarse units' document factor xstats[5] = 1
     // (the scales ride on the query side, vx::launch_rows_to_i8)
     CU_TRY(vx::launch_to_i8_shadow(h->docs, h->n_local, (int)D, h->docs8, h->d_colmax, colscale,
-                                   h->stream));
+                                   h->i8_per_column, h->stream));
+    h->i8_demoted = false;  // a new shard: AUTO may take the s8 pass again
     const float one = 1.0f;
     CU_TRY(cudaMemcpyAsync(h->d_xnorm + 5, &one, 4, cudaMemcpyHostToDevice, h->stream));
     CU_TRY(cudaStreamSynchronize(h->stream));  // `one` is a host stack value
@@ -810,12 +823,14 @@ extern "C" vx_status vx_shard_serve(vx_index* h) {
   for (;;) {
     NCCL_TRY(nccl().Broadcast(h->d_hdr, h->d_hdr, 4, ncclInt32, 0, h->comm, st));
     CU_TRY(cudaMemcpyAsync(h->h_hdr, h->d_hdr, 16, cudaMemcpyDeviceToHost, st));
+    CU_TRY(cudaMemcpyAsync(h->h_hdr + 4, h->d_fcount, 16, cudaMemcpyDeviceToHost, st));
     CU_TRY(cudaEventRecord(h->tok_ev, st));
     cudaError_t q;
     while ((q = cudaEventQuery(h->tok_ev)) == cudaErrorNotReady) {
     }
     CU_TRY(q);
     const int op = h->h_hdr[0], B = h->h_hdr[1], k = h->h_hdr[2], nq = h->h_hdr[3];
+    maybe_demote_i8(h, h->h_hdr + 4, h->st.queries);  // this shard's certificate record so far
     if (op == OP_STOP) return VX_OK;
     if (B < 1 || B > h->desc.max_batch || k < 1 || k > h->desc.max_k)
       return fail(VX_ERR_STATE, "bad batch header %d/%d/%d", op, B, k);

@@ -97,6 +97,9 @@ struct vx_index {
   int dbg_seed_m = 0;            //   VX_DEBUG_SEED_M (sample rank of the scan seed, <= 32),
   int dbg_no_rep = 0;            //   VX_DEBUG_NO_REP (no small-batch query replication)
   int scan_seed = 1;             // seed the TC scan's admission thresholds (VX_OPT_SCAN_SEED)
+  int i8_per_column = 0;         // s8 shadow column scales: 0 one per shard, 1 per column
+  bool i8_demoted = false;       // AUTO left s8 after its certificate kept failing (vx_sync)
+  uint64_t cert_seen_q = 0, cert_seen_l2 = 0, cert_seen_l3 = 0;  // demotion window origin
   int use_pairs = 2;             // CTA-pair scan for B > 128: 0 off, 1 on (256-query passes),
                                  // 2 on + 512-query passes for B > 256 (VX_OPT_SCAN_PAIRS)
   // options
@@ -222,6 +225,8 @@ static inline vx_status check_batch(vx_index* h, int32_t B, int32_t k) {
 
 // ---------------------------------------------------------------- the stage (vx_stage.cu)
 int coarse_fmt(const vx_index* h);  // FMT_* the tensor-core pass uses (VX_OPT_COARSE resolved)
+// AUTO leaves the s8 pass when its certificate keeps failing (fc: device counters)
+void maybe_demote_i8(vx_index* h, const int* fc, uint64_t queries);
 enum { OP_STOP = 0, OP_SEARCH = 1, OP_RESCORE = 2 };
 
 vx_status run_maxsim(vx_index* h, const float* d_qtok, int B, int nq, const int64_t* d_cand, int C,

@@ -77,11 +77,12 @@ __device__ __forceinline__ float seed_thr(const uint64_t* seed, int ld, int q) {
 // from the actual rounding residuals (rerank_kernel in scan_tc.cu).
 constexpr float kErrCoefTF32 = 0.001953125f;
 cudaError_t launch_to_bf16(const float* in, uint16_t* out, int64_t n, cudaStream_t st);
-// s8 shadow of an n x D fp32 shard with ONE SCALE PER COLUMN: s_c = max_r |x[r][c]| / 127
-// (0 for an all-zero column), x8[r][c] = rint(x[r][c] / s_c).  colmax_bits: D words of
-// scratch; colscale: the D scales.
+// s8 shadow of an n x D fp32 shard, x8[r][c] = rint(x[r][c] / s_c) with column scales s_c:
+// one shard-wide value (default) or per_column s_c = max_r |x[r][c]| / 127 (0 for an all-zero
+// column).  colmax_bits: D words of scratch; colscale: the D scales.
 cudaError_t launch_to_i8_shadow(const float* in, int64_t n, int D, int8_t* out,
-                                unsigned int* colmax_bits, float* colscale, cudaStream_t st);
+                                unsigned int* colmax_bits, float* colscale, int per_column,
+                                cudaStream_t st);
 // s8 copy of B query rows of D: q'[c] = q[c] s_c folds the document column scales into the
 // query, then one scale per row sq = max|q'| / 127, q8 = rint(q' / sq); sq * (q8 . x8)
 // approximates q . x (the certificate bounds the difference, scan_tc.cu cert_err_bound)

@@ -84,9 +84,36 @@ static int kprime_of(const vx_index* h, int k, int fmt) {
 constexpr float kI8AutoMaxRelResidual = 0.03f;
 constexpr int kI8AutoMinTilesPerCta = 16;
 
+// AUTO's runtime check of the s8 pass (called with the device's certificate counters: fc[1]
+// level-2 and fc[3] level-3 running totals).  The static test above (quantisation residual vs
+// row norms) cannot see the QUERIES: with anisotropic rows (a few dimensions carrying most of
+// the spread — include/vx_synth.h dist 1) the s8 bound E exceeds the score gaps and every
+// query falls through to the exact re-scan (measured: 587 ms per 1024-query batch instead of
+// 7.5).  When, over >= 64 queries, more than 2 % needed the re-scan or 25 % the wide
+// re-rank, AUTO leaves s8 for the bf16 pass (whose relative per-element error does not care
+// about the anisotropy) until the shard is re-uploaded.  Results are exact either way.
+void maybe_demote_i8(vx_index* h, const int* fc, uint64_t queries) {
+  if (h->coarse != VX_COARSE_AUTO || h->i8_demoted || coarse_fmt(h) != vx::FMT_I8) {
+    h->cert_seen_q = queries;
+    h->cert_seen_l2 = (uint64_t)fc[1];
+    h->cert_seen_l3 = (uint64_t)fc[3];
+    return;
+  }
+  const uint64_t dq = queries - h->cert_seen_q;
+  if (dq < 64) return;
+  const uint64_t l2 = (uint64_t)fc[1] - h->cert_seen_l2, l3 = (uint64_t)fc[3] - h->cert_seen_l3;
+  if (l3 * 50 > dq || l2 * 4 > dq) {
+    h->i8_demoted = true;
+    drop_graphs(h);  // the captured stages bake the s8 choice in
+  }
+  h->cert_seen_q = queries;
+  h->cert_seen_l2 = (uint64_t)fc[1];
+  h->cert_seen_l3 = (uint64_t)fc[3];
+}
+
 int coarse_fmt(const vx_index* h) {
   if (h->coarse == VX_COARSE_I8 && h->docs8) return vx::FMT_I8;
-  if (h->coarse == VX_COARSE_AUTO && h->docs8 &&
+  if (h->coarse == VX_COARSE_AUTO && h->docs8 && !h->i8_demoted &&
       h->n_local >= (int64_t)256 * h->num_sms * kI8AutoMinTilesPerCta &&
       h->xstats_host[4] <= kI8AutoMaxRelResidual * h->xstats_host[7] / (float)std::max<int64_t>(1, h->n_local))
     return vx::FMT_I8;
@@ -776,6 +803,7 @@ extern "C" vx_status vx_sync(vx_index* h) {
     CU_TRY(cudaMemcpy(fc, h->d_fcount, 16, cudaMemcpyDeviceToHost));
     h->st.cert_level2 = (uint64_t)fc[1];
     h->st.cert_fallbacks = (uint64_t)fc[3];
+    maybe_demote_i8(h, fc, h->st.queries);
   }
   vx::KTimer kt[vx::KT_N];  // device-side launch timers (every launch since the last reset)
   CU_TRY(cudaMemcpy(kt, h->d_ktimer, sizeof kt, cudaMemcpyDeviceToHost));
