@@ -168,9 +168,10 @@ def test_seeded_scan_exact_when_the_sample_is_unrepresentative(vx, oracle, coars
 @pytest.mark.parametrize("B,k", [(24, 10), (300, 100)])
 def test_anisotropic_rows_exact_and_auto_demotes_s8(vx, oracle, B, k):
     # power-law per-dimension scales + outlier dimensions (vx_synth.h dist 1), queries drawn
-    # alike: the quantisation residual test passes (AUTO starts on s8) but the s8 error bound
-    # exceeds the score gaps, so every query needs the exact re-scan.  Results are exact
-    # anyway; the certificate record then demotes AUTO to bf16, which certifies them.
+    # alike.  One s8 scale per shard: the residual test already sends AUTO to bf16.  Per-column
+    # scales (VX_OPT_I8_SCALE = 1) pass the residual test (AUTO starts on s8), but folding them
+    # into the query widens ITS error beyond the score gaps, so every query needs the exact
+    # re-scan — results exact anyway — and the certificate record then demotes AUTO to bf16.
     N, D = 700_000, 768
     X = oracle.synth_rows(42, 0, N, D, 1)
     Q = oracle.synth_rows(43, 0, B, D, 1)
@@ -178,6 +179,8 @@ def test_anisotropic_rows_exact_and_auto_demotes_s8(vx, oracle, B, k):
     with vx.Index(N, D, max_batch=B, max_k=k) as idx:
         idx.synth(42, dist=1)
         assert np.array_equal(idx.download(1000, 64).view(np.uint32), X[1000:1064].view(np.uint32))
+        assert idx.coarse_auto() == "bf16"  # static test: one shard scale is too coarse
+        idx.set_option(vx.VX_OPT_I8_SCALE, 1)
         assert idx.coarse_auto() == "i8"
         ids, sc = idx.search(Q, k)
         assert np.array_equal(ids, rid) and np.array_equal(sc, rsc.astype(np.float32))
@@ -190,6 +193,7 @@ def test_anisotropic_rows_exact_and_auto_demotes_s8(vx, oracle, B, k):
         assert st1["cert_fallbacks"] - st0["cert_fallbacks"] <= B // 50
         idx.synth(42, dist=0)  # a new shard resets the decision
         assert idx.coarse_auto() == "i8"
+        idx.set_option(vx.VX_OPT_I8_SCALE, 0)
     print(f"anisotropic B={B}: s8 re-scans {st0['cert_fallbacks']}, then bf16 re-scans "
           f"{st1['cert_fallbacks'] - st0['cert_fallbacks']}")
 
