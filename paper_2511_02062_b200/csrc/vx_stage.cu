@@ -89,8 +89,8 @@ constexpr int kI8AutoMinTilesPerCta = 16;
 // row norms) cannot see the QUERIES: with anisotropic rows (a few dimensions carrying most of
 // the spread — include/vx_synth.h dist 1) the s8 bound E exceeds the score gaps and every
 // query falls through to the exact re-scan (measured: 587 ms per 1024-query batch instead of
-// 7.5).  When, over >= 64 queries, more than 2 % needed the re-scan or 25 % the wide
-// re-rank, AUTO leaves s8 for the bf16 pass (whose relative per-element error does not care
+// 7.5).  When, over >= 16 queries, more than 1/8 needed the re-scan or half the wide
+// re-rank (the isotropic headline: ~0.5 % level 2, no re-scans), AUTO leaves s8 for the bf16 pass (whose relative per-element error does not care
 // about the anisotropy) until the shard is re-uploaded.  Results are exact either way.
 void maybe_demote_i8(vx_index* h, const int* fc, uint64_t queries) {
   if (h->coarse != VX_COARSE_AUTO || h->i8_demoted || coarse_fmt(h) != vx::FMT_I8) {
@@ -100,9 +100,9 @@ void maybe_demote_i8(vx_index* h, const int* fc, uint64_t queries) {
     return;
   }
   const uint64_t dq = queries - h->cert_seen_q;
-  if (dq < 64) return;
+  if (dq < 16) return;
   const uint64_t l2 = (uint64_t)fc[1] - h->cert_seen_l2, l3 = (uint64_t)fc[3] - h->cert_seen_l3;
-  if (l3 * 50 > dq || l2 * 4 > dq) {
+  if (l3 * 8 > dq || l2 * 2 > dq) {
     h->i8_demoted = true;
     drop_graphs(h);  // the captured stages bake the s8 choice in
   }
