@@ -19,6 +19,22 @@
 //       The reference's open-loop trace (bench::arrival_times, bench.hpp:54-67) from
 //       sim::Rng(seed); one time (us) per line.
 //
+//   vortex_ref_driver profile <csv> <model> <size_gb> <b_max> <batch_cap>
+//       Loads a profile CSV with the reference's ProfileTable::from_csv_file (profile.hpp:42-61)
+//       and prints "lat <b> <latency_ms(model, size, b)>" for b = 1..b_max, then
+//       "peak <batch> <throughput>" for peak(model, size, batch_cap) (profile.hpp:110-123) —
+//       the round trip of the B200 stage's measured rows (profiles/emit_profile.py).
+//
+//   vortex_ref_driver pipeline <N> <D> <k> <B> <nq> <T>
+//       Two stages C -> D in the reference Runtime (pipeline.json:7's "C" feeding "D"): modelC
+//       is an upstream stand-in whose ComponentFn turns query i into its VXQ1 payload (vector
+//       + late-interaction tokens, the cross-attention output of PreFLMR); the runtime hands
+//       those outputs to D through emit_results / trigger_put_routed / deliver_bundle
+//       (runtime.hpp:674-704, 570-592); modelD is the B200 stage.  Prints per query
+//       "<index> batch=<b> id:ip:ms ...", then per D batch "handoff <B> <call_us>
+//       <device_stage_us>": the wall time of the modelD call and the GPU stage inside it (needs
+//       a GPU).
+//
 //   vortex_ref_driver operator <N> <D> <k> <B> <nq> <T>
 //       Registers the B200 stage (include/vortex_b200_component.hpp over
 //       libvortex_b200.so) as "modelD" in the reference Runtime and pushes B synthetic
@@ -35,6 +51,8 @@
 #include "vortex/runtime.hpp"
 
 #ifdef VX_WITH_B200
+#include <array>
+#include <chrono>
 #include <cmath>
 
 #include "vortex_b200_component.hpp"
@@ -138,6 +156,18 @@ static int run_replicas(int argc, char** argv) {
   return 0;
 }
 
+static int run_profile(int argc, char** argv) {
+  if (argc < 7) return 2;
+  auto t = exec::ProfileTable::from_csv_file(argv[2]);
+  const std::string model = argv[3];
+  const double size = std::atof(argv[4]);
+  const int bmax = std::atoi(argv[5]), cap = std::atoi(argv[6]);
+  for (int b = 1; b <= bmax; ++b) std::printf("lat %d %.17g\n", b, t.latency_ms(model, size, b));
+  const auto& pk = t.peak(model, size, cap);
+  std::printf("peak %d %.9g\n", pk.batch, pk.throughput_qps);
+  return 0;
+}
+
 static int run_arrivals(int argc, char** argv) {
   if (argc < 7) return 2;
   bench::Phase ph;
@@ -211,6 +241,85 @@ static int run_operator(int argc, char** argv) {
   vx_index_destroy(h);
   return 0;
 }
+
+static int run_pipeline(int argc, char** argv) {
+  if (argc < 8) return 2;
+  const int64_t N = std::atoll(argv[2]);
+  const int D = std::atoi(argv[3]), k = std::atoi(argv[4]), B = std::atoi(argv[5]);
+  const int nq = std::atoi(argv[6]);
+  const int64_t T = std::atoll(argv[7]);
+  const int Nd = 128, td = 128;
+  vx_index_desc d{};
+  d.n_docs = N;
+  d.dim = D;
+  d.n_shards = 1;
+  d.tok_per_doc = Nd;
+  d.tok_dim = td;
+  d.tok_blocks = T;
+  d.max_batch = 4;
+  d.max_k = k;
+  d.max_qtok = nq;
+  vx_index* h = nullptr;
+  if (vx_index_create(&d, &h) != VX_OK || vx_index_synth(h, 42) != VX_OK ||
+      vx_tokens_synth(h, 45) != VX_OK || vx_set_option(h, VX_OPT_GRAPHS, 1) != VX_OK) {
+    std::fprintf(stderr, "vx: %s\n", vx_last_error());
+    return 3;
+  }
+  // pipeline.json's tail: C (cap 4) -> D (cap 4); profiles.csv's modelD rows for both members
+  World w(4, {{1, 125}, {4, 400}});
+  w.prof.add("modelC", 24, exec::ProfileEntry{1, 20.0, 50.0, 1});
+  w.prof.add("modelC", 24, exec::ProfileEntry{4, 60.0, 66.7, 1});
+  int nodeC = w.ex->add_node(24);
+  w.ex->partition_node(nodeC, exec::MIGLayout{{24}});
+  w.pools["modelC"].push_back(&w.ex->instance(nodeC, 0));
+  w.spec.stages = {{"C", "modelC", 4, {}, {}}, {"D", "modelD", 4, {}, {}}};
+  w.spec.edges = {{"C", "D"}};
+  w.spec.ingress = "C";
+  w.spec.egress = "D";
+  // upstream stand-in: query index -> VXQ1 payload (vector + tokens)
+  w.rt->register_component("modelC", [&](const std::vector<Payload>& inputs) {
+    std::vector<Payload> out;
+    for (const auto& p : inputs) {
+      const int i = std::stoi(payload_str(p));
+      auto q = synth_row(43, i, D);
+      std::vector<float> tok;
+      for (int j = 0; j < nq; ++j) {
+        auto r = synth_row(44, (uint64_t)i * nq + j, td);
+        tok.insert(tok.end(), r.begin(), r.end());
+      }
+      out.push_back(vortex_b200::encode_query(q.data(), D, tok.data(), nq, td));
+    }
+    return out;
+  });
+  auto search = vortex_b200::make_search_component(h, D, k);
+  std::vector<std::array<double, 3>> handoffs;
+  w.rt->register_component("modelD", [&](const std::vector<Payload>& inputs) {
+    const auto t0 = std::chrono::steady_clock::now();
+    auto out = search(inputs);
+    const auto t1 = std::chrono::steady_clock::now();
+    vx_stats st{};
+    vx_get_stats(h, &st);
+    handoffs.push_back({(double)inputs.size(),
+                        std::chrono::duration<double, std::micro>(t1 - t0).count(),
+                        (double)st.last_step_ms * 1000.0});
+    return out;
+  });
+  w.rt->load_pipeline(w.spec, w.pools);
+  std::vector<std::uint64_t> qids;
+  for (int i = 0; i < B; ++i)
+    qids.push_back(w.rt->ingress_submit("search", make_payload(std::to_string(i))));
+  w.loop.run_all();
+  for (int i = 0; i < B; ++i) {
+    const auto& rec = w.rt->record("search", qids[i]);
+    auto res = vortex_b200::decode_result(rec.outputs.at("D"));
+    std::printf("%d batch=%d", i, rec.stages.at("D").batch);
+    for (const auto& r : res) std::printf(" %lld:%.9g:%.9g", (long long)r.id, r.ip, r.ms);
+    std::printf("\n");
+  }
+  for (const auto& hf : handoffs) std::printf("handoff %d %.1f %.1f\n", (int)hf[0], hf[1], hf[2]);
+  vx_index_destroy(h);
+  return 0;
+}
 #endif
 
 int main(int argc, char** argv) {
@@ -223,8 +332,10 @@ int main(int argc, char** argv) {
     if (mode == "batcher") return run_batcher(argc, argv);
     if (mode == "replicas") return run_replicas(argc, argv);
     if (mode == "arrivals") return run_arrivals(argc, argv);
+    if (mode == "profile") return run_profile(argc, argv);
 #ifdef VX_WITH_B200
     if (mode == "operator") return run_operator(argc, argv);
+    if (mode == "pipeline") return run_pipeline(argc, argv);
 #endif
   } catch (const std::exception& e) {
     std::fprintf(stderr, "error: %s\n", e.what());

@@ -163,3 +163,42 @@ def test_slo_cap_and_profile_rows(bat):
     rows = bat.profile_rows("modelD", 180, prof, 40.0).splitlines()
     assert rows[0] == "model_id,instance_size_gb,batch_size,latency_ms,throughput_qps,memory_gb"
     assert rows[2].startswith("modelD,180,16,5.1")
+
+
+@pytest.mark.skipif(not DRIVER.exists(), reason="oracle/_ref not built (needs /root/reference)")
+@pytest.mark.parametrize("csv", ["profiles/r01/modelD_b200_profile.csv", "profiles/r02/modelD_b200_profile.csv"])
+def test_measured_profile_round_trips_through_reference_profile_table(bat, csv, tmp_path):
+    """The B200 stage's measured rows (profiles/emit_profile.py, batcher.profile_rows) are read
+    by the REFERENCE's ProfileTable::from_csv_file (profile.hpp:42-61): its latency_ms
+    interpolation (profile.hpp:90-109) returns the rows at the knots and interpolates between
+    them as the restatement does, and its peak (profile.hpp:110-123) is batcher.peak's."""
+    import subprocess
+    path = ROOT / csv
+    if not path.exists():
+        pytest.skip(f"{csv} not produced yet")
+    rows = [ln.split(",") for ln in path.read_text().splitlines()[1:] if ln.strip()]
+    prof = {int(r[2]): float(r[3]) for r in rows}
+    size = rows[0][1]
+    bmax = max(prof) + 100
+    for cap in (max(prof), 64, 4):
+        out = subprocess.run([str(DRIVER), "profile", str(path), "modelD", size, str(bmax), str(cap)],
+                             check=True, capture_output=True, text=True).stdout.split("\n")
+        lat = {int(a.split()[1]): float(a.split()[2]) for a in out if a.startswith("lat")}
+        peak = [a for a in out if a.startswith("peak")][0].split()
+        assert int(peak[1]) == bat.peak(prof, batch_cap=cap)
+    knots = sorted(prof)
+    for b in range(1, bmax + 1):
+        if b in prof:
+            assert lat[b] == prof[b]
+        elif b < knots[0]:
+            assert lat[b] == pytest.approx(prof[knots[0]] * b / knots[0], rel=1e-12)
+        elif b <= knots[-1]:
+            assert lat[b] == pytest.approx(float(np.interp(b, knots, [prof[x] for x in knots])), rel=1e-12)
+    # and a profile written by batcher.profile_rows round-trips at the knots (6 decimals)
+    p2 = {1: 1.234567, 8: 1.5, 64: 2.75, 1024: 7.125}
+    f = tmp_path / "p.csv"
+    f.write_text(bat.profile_rows("modelD", 180.0, p2, 62.3))
+    out = subprocess.run([str(DRIVER), "profile", str(f), "modelD", "180", "1024", "1024"],
+                         check=True, capture_output=True, text=True).stdout.split("\n")
+    lat = {int(a.split()[1]): float(a.split()[2]) for a in out if a.startswith("lat")}
+    assert all(lat[b] == pytest.approx(v, abs=1e-6) for b, v in p2.items())

@@ -86,3 +86,37 @@ def test_live_batcher_with_rescore(vx):
         want, _, _ = idx.search_rescore(Q[:5], qt[:5], k)
     assert np.array_equal(ids[:5], want)
     assert np.bincount(bo).max() <= cap
+
+
+@pytest.mark.skipif(not OPERATOR.exists(), reason="oracle/_ref/vortex_ref_operator not built")
+def test_reference_pipeline_c_to_d_handoff(vx, oracle):
+    """Upstream hand-off C -> D through the REFERENCE runtime: stage C's
+    ComponentFn emits VXQ1 payloads (query vector + tokens), the runtime carries them with
+    emit_results / trigger_put_routed / deliver_bundle (runtime.hpp:674-704, 570-592) into
+    the B200 modelD stage.  Results must be the oracle's; the hand-off — the modelD call's
+    wall time outside the GPU stage (payload decode, one gather into pinned staging, H2D,
+    D2H, result encode) — must stay under the paper's 2 ms stage hand-off."""
+    from stagecheck import check_stage
+    N, D, k, B, nq, T = 50_000, 768, 10, 11, 32, 97
+    out = subprocess.run([str(OPERATOR), "pipeline", str(N), str(D), str(k), str(B), str(nq), str(T)],
+                         check=True, capture_output=True, text=True, timeout=300).stdout
+    lines = out.strip().splitlines()
+    rows = [ln.split() for ln in lines if not ln.startswith("handoff")]
+    hand = [ln.split() for ln in lines if ln.startswith("handoff")]
+    assert len(rows) == B and sum(int(h[1]) for h in hand) == B
+    assert all(int(h[1]) <= 4 for h in hand)  # D's stage cap (pipeline.json:7)
+    X = oracle.synth_rows(42, 0, N, D)
+    Q = oracle.synth_rows(43, 0, B, D)
+    qt = oracle.synth_rows(44, 0, B * nq, 128).reshape(B, nq, 128)
+    table = oracle.synth_tokens(45, 0, T, 128, 128)
+    rid, rsc = oracle.flat_topk(X, Q, k, mode=oracle.F32)
+    rms = oracle.maxsim(qt, rid, table, mode=oracle.F64_Q32)
+    ids = np.array([[int(x.split(":")[0]) for x in r[2:]] for r in rows])
+    ip = np.array([[np.float32(float(x.split(":")[1])) for x in r[2:]] for r in rows])
+    ms = np.array([[float(x.split(":")[2]) for x in r[2:]] for r in rows])
+    check_stage(ids, ip, ms, rid, rsc, rms)
+    # per batch after the first (which also captures the graphs): call wall - device stage
+    extra = [float(h[2]) - float(h[3]) for h in hand[1:]]
+    print(f"C->D hand-off overhead per D batch: {[round(e) for e in extra]} us "
+          f"(call {[h[2] for h in hand[1:]]} us, device stage {[h[3] for h in hand[1:]]} us)")
+    assert extra and max(extra) < 2000.0
