@@ -248,6 +248,21 @@ vx_status vx_serve_trace(vx_index* h, const uint64_t* arrivals_us, int64_t n, in
                          const float* queries, const float* qtok, int32_t nq, int32_t k,
                          int64_t* ids, double* latency_us, int64_t* batch_of,
                          int64_t* n_batches);
+/* Live replica mode: R whole-index handles (e.g. one per GPU) as the members of the stage,
+ * each batching as above, queries routed at arrival by the reference's power of two choices
+ * (Runtime::pick_member, runtime.hpp:522-536: outstanding = routed - completed, ties to the
+ * lower index, draws from std::mt19937_64(seed)).  One host thread drives all members; the
+ * queries queued behind a running batch are DMA'd into the member's second input buffer
+ * while it computes.  Per query (all optional except latency_us): instance, dispatch and
+ * completion time (us), the sequence numbers of its routing, dispatch and completion events
+ * (one global counter: the queue every dispatch saw and the outstanding counts every routing
+ * decision saw can be replayed), ids [n][k], latency, global batch index. */
+vx_status vx_serve_trace_replicas(vx_index* const* handles, int32_t R, const uint64_t* arrivals_us,
+                                  int64_t n, int32_t cap, const float* queries, const float* qtok,
+                                  int32_t nq, int32_t k, uint64_t seed, int32_t* instance_of,
+                                  uint64_t* dispatch_us, uint64_t* complete_us, uint64_t* admit_seq,
+                                  uint64_t* dispatch_seq, uint64_t* complete_seq, int64_t* ids,
+                                  double* latency_us, int64_t* batch_of, int64_t* n_batches);
 
 /* Multi-GPU (one process per GPU).  Rank 0 creates the id, the host plumbing
  * (torch.distributed / MPI / a file) distributes the 128 bytes, every rank

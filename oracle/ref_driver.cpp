@@ -15,6 +15,10 @@
 //       runtime.hpp:522-536, RNG seed RuntimeOptions::seed = 7) and each member batches on
 //       its own.  Prints per query: "<index> <instance> <dispatch_us> <complete_us>".
 //
+//   vortex_ref_driver draws <seed> <R> <count>
+//       The candidate pairs Runtime::pick_member draws for `count` routings over R active
+//       members (runtime.hpp:528-531, sim::Rng(seed).below): "<a> <b>" per line.
+//
 //   vortex_ref_driver arrivals <rate_qps> <count> <seed> <poisson|constant> <start_us>
 //       The reference's open-loop trace (bench::arrival_times, bench.hpp:54-67) from
 //       sim::Rng(seed); one time (us) per line.
@@ -165,6 +169,20 @@ static int run_profile(int argc, char** argv) {
   for (int b = 1; b <= bmax; ++b) std::printf("lat %d %.17g\n", b, t.latency_ms(model, size, b));
   const auto& pk = t.peak(model, size, cap);
   std::printf("peak %d %.9g\n", pk.batch, pk.throughput_qps);
+  return 0;
+}
+
+static int run_draws(int argc, char** argv) {
+  if (argc < 5) return 2;
+  sim::Rng rng(std::strtoull(argv[2], nullptr, 10));
+  const std::size_t R = std::strtoull(argv[3], nullptr, 10);
+  const long n = std::atol(argv[4]);
+  for (long i = 0; i < n; ++i) {
+    std::size_t a = rng.below(R);
+    std::size_t b = rng.below(R - 1);
+    if (b >= a) ++b;
+    std::printf("%zu %zu\n", a, b);
+  }
   return 0;
 }
 
@@ -333,6 +351,7 @@ int main(int argc, char** argv) {
     if (mode == "replicas") return run_replicas(argc, argv);
     if (mode == "arrivals") return run_arrivals(argc, argv);
     if (mode == "profile") return run_profile(argc, argv);
+    if (mode == "draws") return run_draws(argc, argv);
 #ifdef VX_WITH_B200
     if (mode == "operator") return run_operator(argc, argv);
     if (mode == "pipeline") return run_pipeline(argc, argv);

@@ -92,6 +92,9 @@ SIGNATURES = {
     "vx_arrival_times": [C.c_double, I64, U64, U64, I32, C.POINTER(U64)],
     "vx_serve_trace": [P, C.POINTER(U64), I64, I32, FP, FP, I32, I32, LP,
                        C.POINTER(C.c_double), LP, C.POINTER(I64)],
+    "vx_serve_trace_replicas": [C.POINTER(P), I32, C.POINTER(U64), I64, I32, FP, FP, I32, I32, U64,
+                                C.POINTER(I32), C.POINTER(U64), C.POINTER(U64), C.POINTER(U64),
+                                C.POINTER(U64), C.POINTER(U64), LP, C.POINTER(C.c_double), LP, LP],
     "vx_comm_unique_id": [C.POINTER(C.c_uint8)],
     "vx_comm_init": [P, C.POINTER(C.c_uint8), I32, I32],
     "vx_shard_serve": [P],

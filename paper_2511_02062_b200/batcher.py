@@ -142,3 +142,38 @@ def serve_trace(index, arrivals_us, cap: int, queries: np.ndarray, qtok: np.ndar
                                    lat.ctypes.data_as(C.POINTER(C.c_double)), bo.ctypes.data_as(LP),
                                    C.byref(nb)))
     return lat, bo, ids
+
+
+def serve_trace_replicas(indexes, arrivals_us, cap: int, queries: np.ndarray, qtok: np.ndarray | None,
+                         k: int, seed: int = 7, want_ids: bool = False) -> dict:
+    """Live replica mode (vx_serve_trace_replicas): R whole-index handles (one per GPU), queries
+    routed at arrival by the reference's power of two choices (runtime.hpp:522-536).  Returns a
+    dict of per-query arrays: latency_us, instance, dispatch_us, complete_us, admit_seq,
+    dispatch_seq, complete_seq, batch_of (+ ids), and n_batches."""
+    lib = _lib.load()
+    a = np.ascontiguousarray(arrivals_us, np.uint64)
+    n = a.shape[0]
+    q = np.ascontiguousarray(queries, np.float32)
+    t = None if qtok is None else np.ascontiguousarray(qtok, np.float32)
+    R = len(indexes)
+    hs = (C.c_void_p * R)(*[ix.handle.value for ix in indexes])
+    out = {"latency_us": np.empty(n, np.float64), "instance": np.empty(n, np.int32),
+           "dispatch_us": np.empty(n, np.uint64), "complete_us": np.empty(n, np.uint64),
+           "admit_seq": np.empty(n, np.uint64), "dispatch_seq": np.empty(n, np.uint64),
+           "complete_seq": np.empty(n, np.uint64),
+           "batch_of": np.empty(n, np.int64)}
+    ids = np.empty((n, k), np.int64) if want_ids else None
+    nb = C.c_int64()
+    U64P = C.POINTER(C.c_uint64)
+    check(lib.vx_serve_trace_replicas(
+        hs, R, a.ctypes.data_as(U64P), n, cap, q.ctypes.data_as(FP),
+        None if t is None else t.ctypes.data_as(FP), 0 if t is None else t.shape[1], k, seed,
+        out["instance"].ctypes.data_as(C.POINTER(C.c_int32)), out["dispatch_us"].ctypes.data_as(U64P),
+        out["complete_us"].ctypes.data_as(U64P), out["admit_seq"].ctypes.data_as(U64P),
+        out["dispatch_seq"].ctypes.data_as(U64P), out["complete_seq"].ctypes.data_as(U64P), None if ids is None else ids.ctypes.data_as(LP),
+        out["latency_us"].ctypes.data_as(C.POINTER(C.c_double)), out["batch_of"].ctypes.data_as(LP),
+        C.byref(nb)))
+    out["n_batches"] = nb.value
+    if want_ids:
+        out["ids"] = ids
+    return out

@@ -709,79 +709,6 @@ extern "C" vx_status vx_search_rescore_rows(vx_index* h, const float* const* q_r
   return drained(h, host_search_rescore(h, nullptr, q_rows, nullptr, tok_rows, B, nq, k, ids, ip, ms));
 }
 
-// ---------------------------------------------------------------- live batcher
-// Wall-clock mode of the opportunistic batcher (vx_batcher.hpp) with this handle as the
-// stage's executor — the "live" mode the reference reserves but does not implement
-// (proj/include/vortex/config.hpp:43).  One batch in flight: the GPU stage is a serial
-// resource exactly like exec::Instance::busy_until (executor.hpp:44-59).
-extern "C" vx_status vx_serve_trace(vx_index* h, const uint64_t* arrivals_us, int64_t n,
-                                    int32_t cap, const float* queries, const float* qtok,
-                                    int32_t nq, int32_t k, int64_t* ids, double* latency_us,
-                                    int64_t* batch_of, int64_t* n_batches) {
-  if (!h || (n > 0 && (!arrivals_us || !queries || !latency_us)))
-    return fail(VX_ERR_INVALID, "null argument");
-  if (cap < 1 || cap > h->desc.max_batch) return fail(VX_ERR_INVALID, "cap %d", cap);
-  VX_TRY(check_batch(h, cap, k));
-  const bool rescore = qtok != nullptr;
-  if (rescore && (!h->tokens || nq < 1 || nq > h->desc.max_qtok))
-    return fail(VX_ERR_INVALID, "query tokens need a token store and 1 <= nq <= max_qtok");
-  for (int64_t i = 1; i < n; ++i)
-    if (arrivals_us[i] < arrivals_us[i - 1]) return fail(VX_ERR_INVALID, "arrivals not sorted");
-  CU_TRY(cudaSetDevice(h->device));
-  cudaStream_t st = h->stream;
-  const size_t D = h->desc.dim, td = rescore ? (size_t)h->desc.tok_dim : 0;
-  uint8_t* stage = static_cast<uint8_t*>(h->h_stage);
-  vx::OpportunisticBatcher bat(cap);
-  using clk = std::chrono::steady_clock;
-  const auto t0 = clk::now();
-  auto now_us = [&] {
-    return (uint64_t)std::chrono::duration_cast<std::chrono::microseconds>(clk::now() - t0).count();
-  };
-  int64_t next = 0, nb = 0;
-  while (next < n || bat.queued() > 0) {
-    uint64_t t = now_us();
-    if (bat.queued() == 0 && next < n && arrivals_us[next] > t) {
-      // idle: wait for the next planned arrival (spin the last 200 us for precision)
-      while ((t = now_us()) + 200 < arrivals_us[next])
-        std::this_thread::sleep_for(std::chrono::microseconds(100));
-      while ((t = now_us()) < arrivals_us[next]) {
-      }
-    }
-    while (next < n && arrivals_us[next] <= t) bat.arrive(next++);
-    std::vector<int64_t> batch = bat.maybe_dispatch();
-    if (batch.empty()) continue;
-    const int B = (int)batch.size();
-    // gather the batch's payloads (host ingress) -> pinned staging -> HBM
-    for (int i = 0; i < B; ++i) memcpy(stage + i * D * 4, queries + batch[i] * D, D * 4);
-    CU_TRY(cudaMemcpyAsync(h->d_q, stage, (size_t)B * D * 4, cudaMemcpyHostToDevice, st));
-    if (rescore) {
-      uint8_t* ts = stage + (size_t)B * D * 4;
-      const size_t tb = (size_t)nq * td * 4;
-      for (int i = 0; i < B; ++i) memcpy(ts + i * tb, qtok + batch[i] * nq * td, tb);
-      CU_TRY(cudaMemcpyAsync(h->d_qtok, ts, (size_t)B * tb, cudaMemcpyHostToDevice, st));
-    }
-    VX_TRY(stage_begin(h, rescore ? OP_RESCORE : OP_SEARCH, h->d_q, B, nq, k, st));
-    if (rescore)
-      VX_TRY(stage_finish(h, h->d_qtok, B, nq, k, h->d_out_ids, h->d_out_ip, h->d_out_ms, st));
-    else
-      VX_TRY(stage_search_out(h, B, k, h->d_out_ids, h->d_out_ip, st));
-    int64_t* hid = reinterpret_cast<int64_t*>(stage);
-    CU_TRY(cudaMemcpyAsync(hid, h->d_out_ids, (size_t)B * k * 8, cudaMemcpyDeviceToHost, st));
-    VX_TRY(vx_sync(h));
-    const uint64_t done = now_us();
-    for (int i = 0; i < B; ++i) {
-      const int64_t q = batch[i];
-      latency_us[q] = (double)done - (double)arrivals_us[q];
-      if (batch_of) batch_of[q] = nb;
-      if (ids) memcpy(ids + q * k, hid + (size_t)i * k, (size_t)k * 8);
-    }
-    ++nb;
-    bat.complete();
-  }
-  if (n_batches) *n_batches = nb;
-  return VX_OK;
-}
-
 // ---------------------------------------------------------------- comm
 extern "C" vx_status vx_comm_unique_id(uint8_t out_id[128]) {
   if (!out_id) return fail(VX_ERR_INVALID, "null argument");

@@ -52,6 +52,7 @@ class OpportunisticBatcher {
   void arrive(int64_t qid) { queue_.push_back(qid); }
   bool executing() const { return executing_; }
   size_t queued() const { return queue_.size(); }
+  int64_t queued_at(size_t i) const { return queue_[i]; }  // i-th oldest queued query
   // Returns the batch to dispatch now (empty if executing or nothing queued).
   std::vector<int64_t> maybe_dispatch() {
     std::vector<int64_t> batch;

@@ -120,3 +120,80 @@ def test_reference_pipeline_c_to_d_handoff(vx, oracle):
     print(f"C->D hand-off overhead per D batch: {[round(e) for e in extra]} us "
           f"(call {[h[2] for h in hand[1:]]} us, device stage {[h[3] for h in hand[1:]]} us)")
     assert extra and max(extra) < 2000.0
+
+
+def _check_policy(out, cap):
+    """Every dispatch took min(queued, cap) of its member's OLDEST queued queries, where
+    `queued` = routed to that member before the dispatch event and not in an earlier batch
+    (runtime.hpp:617-654, replayed from the live event sequence numbers)."""
+    inst, adm, dsp, bo = out["instance"], out["admit_seq"], out["dispatch_seq"], out["batch_of"]
+    order = np.argsort([dsp[np.where(bo == b)[0][0]] for b in range(out["n_batches"])])
+    done = np.zeros(len(adm), bool)
+    for b in order:
+        members = np.where(bo == b)[0]
+        r = inst[members[0]]
+        assert (inst[members] == r).all()
+        d = dsp[members[0]]
+        waiting = np.where((inst == r) & (adm < d) & ~done)[0]   # FIFO: ascending query index
+        assert len(members) == min(len(waiting), cap), (b, len(members), len(waiting))
+        assert np.array_equal(np.sort(members), waiting[:len(members)])
+        done[members] = True
+    assert done.all()
+
+
+def test_live_batcher_dispatch_policy_and_results(vx, oracle):
+    from paper_2511_02062_b200 import batcher, synth
+    N, D, k, n, cap = 200_000, 768, 10, 3000, 32
+    arr = batcher.poisson_arrivals(60_000.0, n, seed=9)
+    Q = synth.rows(43, 0, n, D)
+    with vx.Index(N, D, max_batch=cap, max_k=k) as idx:
+        idx.set_option(vx.VX_OPT_GRAPHS, 1)
+        idx.synth(42)
+        idx.prepare(k, cap)
+        out = batcher.serve_trace_replicas([idx], arr, cap, Q, None, k, want_ids=True)
+    _check_policy(out, cap)
+    sizes = np.bincount(out["batch_of"])
+    assert sizes.max() <= cap and len(set(sizes.tolist())) > 1
+    assert (out["complete_us"] >= out["dispatch_us"]).all() and (out["dispatch_us"] >= arr).all()
+    sel = np.arange(0, n, 97)
+    rid, _ = oracle.flat_topk(oracle.synth_rows(42, 0, N, D), Q[sel], k, mode=oracle.F32)
+    assert np.array_equal(out["ids"][sel], rid)
+
+
+@pytest.mark.skipif(not (ROOT / "oracle" / "_ref" / "vortex_ref_driver").exists(),
+                    reason="oracle/_ref not built")
+def test_live_replicas_route_like_the_reference(vx, oracle):
+    """Live replica mode: R = 3 members (three whole-index handles; one GPU suffices — the
+    routing does not care where a member runs).  Every routing decision must be the reference's
+    pick_member on the live state: the reference's own candidate draws (vortex_ref_driver draws,
+    sim::Rng(7)) and the outstanding counts replayed from the event sequence numbers."""
+    from paper_2511_02062_b200 import batcher, synth
+    N, D, k, n, cap, R = 100_000, 768, 10, 4000, 16, 3
+    arr = batcher.poisson_arrivals(80_000.0, n, seed=5)
+    Q = synth.rows(43, 0, n, D)
+    idxs = [vx.Index(N, D, max_batch=cap, max_k=k) for _ in range(R)]
+    try:
+        for ix in idxs:
+            ix.set_option(vx.VX_OPT_GRAPHS, 1)
+            ix.synth(42)
+            ix.prepare(k, cap)
+        out = batcher.serve_trace_replicas(idxs, arr, cap, Q, None, k, seed=7, want_ids=True)
+    finally:
+        for ix in idxs:
+            ix.close()
+    draws = subprocess.run([str(ROOT / "oracle" / "_ref" / "vortex_ref_driver"), "draws", "7", str(R), str(n)],
+                           check=True, capture_output=True, text=True).stdout.split("\n")
+    pairs = [tuple(int(x) for x in ln.split()) for ln in draws if ln.strip()]
+    inst, adm, cmp_ = out["instance"], out["admit_seq"], out["complete_seq"]
+    for q in range(n):
+        routed_before = (adm < adm[q])
+        load = [int(((inst == r) & routed_before).sum() - ((inst == r) & (cmp_ < adm[q])).sum())
+                for r in range(R)]
+        a, b = pairs[q]
+        want = (a if load[a] < load[b] else b) if load[a] != load[b] else min(a, b)
+        assert inst[q] == want, (q, load, a, b, inst[q])
+    _check_policy(out, cap)
+    assert len(set(inst.tolist())) == R
+    sel = np.arange(0, n, 131)
+    rid, _ = oracle.flat_topk(oracle.synth_rows(42, 0, N, D), Q[sel], k, mode=oracle.F32)
+    assert np.array_equal(out["ids"][sel], rid)
