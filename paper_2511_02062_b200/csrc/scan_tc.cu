@@ -21,6 +21,7 @@
 #include <stdlib.h>
 
 #include "vx_internal.cuh"
+#include "vx_merge.cuh"
 #include "vx_ptx.cuh"
 #include "vx_select.cuh"
 #include "vx_sort.cuh"
@@ -28,6 +29,7 @@
 namespace vx {
 
 constexpr int kTcStageUnit = 16384;   // one 128-row x 128-byte operand tile
+constexpr int kRerankMaxBufs = 4;      // re-rank: chunk buffers in the staging stream
 
 // QT: 128-query tiles per launch (A operands); TD: documents per tile (MMA N, 128 or 256).
 // A bigger TD re-streams the query tiles from L2 half as often per document byte.
@@ -404,14 +406,14 @@ __device__ __forceinline__ void query_norms_final(const float* red, int fmt, flo
 //   phase 2: tail, from hkeys and tau.
 __global__ void __launch_bounds__(256)
     rerank_kernel(const float* __restrict__ docs, const float* __restrict__ qv, int D,
-                  const uint64_t* __restrict__ cand, int kp, const uint64_t* __restrict__ part,
+                  uint64_t* __restrict__ cand, int kp, const uint64_t* __restrict__ part,
                   int grid, int ldlists, int kc, int k, int64_t row0,
                   const float* __restrict__ xstats, int fmt, const float* __restrict__ qscale,
                   uint64_t* __restrict__ out_keys, int64_t* __restrict__ out_ids,
                   float* __restrict__ out_scores, int* __restrict__ flags, int rows_per_round,
                   int dchunk, int phase, const float* __restrict__ tau, uint64_t* __restrict__ hkeys,
                   float* __restrict__ lb, const uint64_t* __restrict__ seed, int seed_ld,
-                  int head_all) {
+                  int head_all, int nbuf, const RerankFuse fz) {
   extern __shared__ __align__(16) float rsm[];
   float* qs = rsm;                                             // [D]
   uint64_t* keys = reinterpret_cast<uint64_t*>(rsm + ((D + 3) & ~3));  // [kp]
@@ -419,7 +421,7 @@ __global__ void __launch_bounds__(256)
   __shared__ float s_red[96];
   __shared__ float s_min[8];
   __shared__ int s_fail;
-  __shared__ __align__(8) uint64_t s_bar[2];
+  __shared__ __align__(8) uint64_t s_bar[kRerankMaxBufs];
   const int b = blockIdx.x;
   const float* q = qv + (size_t)b * D;
   // coarse keys are in the coarse pass's units: the s8 pass scores sq * sx * (s32 dot)
@@ -428,14 +430,18 @@ __global__ void __launch_bounds__(256)
   query_norms(q, D, fmt, sq, qs, s_red, xstats);  // the certificate's error bound, below
   if (threadIdx.x == 0) {
     s_fail = 0;
-    mbar_init(&s_bar[0], (uint32_t)rows_per_round);
-    mbar_init(&s_bar[1], (uint32_t)rows_per_round);
-    fence_barrier_init();
+    for (int i = 0; i < (nbuf & 15); ++i) mbar_init(&s_bar[i], (uint32_t)rows_per_round);
   }
+  if (threadIdx.x == 0) fence_barrier_init();
   __syncthreads();
   float qn, qh, qr;
   query_norms_final(s_red, fmt, &qn, &qh, &qr);
   const float E = cert_err_bound(fmt, D, qn, qh, qr, xstats);
+  if (fz.mlists) {  // fused K3: this query's lists -> its coarse top-k' (staged in rowbuf)
+    uint64_t* staged = reinterpret_cast<uint64_t*>(rowbuf);
+    merge_topk_block(fz.mlists + (size_t)b * fz.mld, fz.mM, kp, 0, cand + (size_t)b * kp, nullptr,
+                     nullptr, 0, kp, staged, staged + ((fz.mM + 1) & ~1));
+  }
   const uint64_t* cb = cand + (size_t)b * kp;
   const uint64_t tprime = cb[kp - 1];  // coarse k'-th key (0: fewer than k' candidates)
   // head rows; head_all (small batch, latency-bound: the pruning saves bytes nobody waits
@@ -446,57 +452,90 @@ __global__ void __launch_bounds__(256)
   // R rows into smem with one TMA bulk copy per row (R x 3 KB in flight per SM), then R
   // threads run the in-order fmaf chains from smem (row stride D+4 floats: the LDS.128 of
   // 8 consecutive lanes hit distinct banks).
-  // Rows are staged in DC-float chunks, double-buffered: chunk c+1 of the R rows of a round
-  // is in flight while R threads run the in-order chains over chunk c (the accumulators
-  // carry across chunks, so the fmaf order is the oracle's).  Chunks instead of whole rows
-  // keep R chains going per CTA in the same smem — the chains, not the gathers, set the
-  // pace (whole rows, 32 per round: 7 of 8 warps parked at the barrier 64 % of the time).
-  const int R = rows_per_round, DC = dchunk, RS = DC + 4, nch = D / DC;
-  int chunk_no = 0;  // chunks issued so far (both calls); chunk i uses buffer / barrier i & 1
+  // Rows are staged in DC-float chunks through NB buffers (one mbarrier each, R arrivals):
+  // the chunks of all rounds form ONE stream (item i = round i / nch, chunk i % nch), NB - 1
+  // items ahead of the chains, across round boundaries — the next round's first chunk is in
+  // flight while this round's last one is scored (a double buffer that restarted at every
+  // round exposed one full gather latency per 64 rows: ~0.73 of the copy peak).  The
+  // accumulators carry across a row's chunks, so the fmaf order is the oracle's.
+  // (Per-thread rings and cp.async variants were measured slower: lanes waiting on their own
+  // slots diverge, and LDGSTS keeps too few bytes in flight — profiles/r02/README.md.)
+  const int R = rows_per_round, DC = dchunk, RS = DC + 4, nch = D / DC, NB = nbuf & 15,
+            PF = nbuf >> 4;
+  int chunk_no = 0;  // items issued so far (both calls); item i uses buffer / barrier i % NB
   auto rescore = [&](int j0, int j1) {  // exact keys of candidates [j0, j1) into keys[]
-    for (int r0 = j0; r0 < j1; r0 += R) {
-      const int t = threadIdx.x;
-      const int idx = r0 + t;
-      const uint64_t ck = (t < R && idx < j1) ? cb[idx] : 0ull;
-      const float* xrow = docs + (size_t)(ck ? vx_key_id(ck) : 0u) * D;
-      auto issue = [&](int c, int no) {  // chunk c of this round's rows -> buffer no & 1
-        if (t < R) {
-          const uint32_t bytes = ck ? (uint32_t)DC * 4u : 0u;
-          uint64_t* bar = &s_bar[no & 1];
-          mbar_expect_tx(bar, bytes);  // every staging thread arrives once (count R)
-          if (ck) bulk_load(rowbuf + ((size_t)(no & 1) * R + t) * RS, xrow + (size_t)c * DC, bytes, bar);
+    const int t = threadIdx.x;
+    const int nitems = ((j1 - j0 + R - 1) / R) * nch;
+    const int base = chunk_no;
+    auto row_key = [&](int r) -> uint64_t {
+      const int idx = j0 + r * R + t;
+      return (t < R && idx < j1) ? cb[idx] : 0ull;
+    };
+    auto issue = [&](int i) {  // item i of this call -> buffer (base + i) % NB
+      if (t < R) {
+        const int r = i / nch, c = i - r * nch, no = base + i;
+        const uint64_t ck = row_key(r);
+        const uint32_t bytes = ck ? (uint32_t)DC * 4u : 0u;
+        uint64_t* bar = &s_bar[no % NB];
+        mbar_expect_tx(bar, bytes);  // every staging thread arrives once (count R)
+        if (ck)
+          bulk_load(rowbuf + ((size_t)(no % NB) * R + t) * RS,
+                    docs + (size_t)vx_key_id(ck) * D + (size_t)c * DC, bytes, bar);
+      }
+    };
+    // L2 prefetch PF items beyond the staging window: the bulk copies then find their lines in
+    // L2 (the CTA keeps only NB - 1 chunks in flight in smem — 2 of 8 warps stream, and with a
+    // full HBM latency per item the chain warps sat at the barrier half the time, ncu)
+    auto prefetch = [&](int i) {
+      if (t < R && i < nitems) {
+        const int r = i / nch, c = i - r * nch;
+        const uint64_t pk = row_key(r);
+        if (pk) {
+          const float* src = docs + (size_t)vx_key_id(pk) * D + (size_t)c * DC;
+          for (int o = 0; o < DC; o += 32) prefetch_l2(src + o);
         }
-      };
-      issue(0, chunk_no);
-      float acc = 0.0f;
-      for (int c = 0; c < nch; ++c, ++chunk_no) {
-        // the other buffer was released by the previous chunk's __syncthreads
-        if (c + 1 < nch) issue(c + 1, chunk_no + 1);
-        mbar_wait(&s_bar[chunk_no & 1], (uint32_t)((chunk_no >> 1) & 1));
-        if (ck) {
-          const float4* x =
-              reinterpret_cast<const float4*>(rowbuf + ((size_t)(chunk_no & 1) * R + t) * RS);
-          const float4* q4 = reinterpret_cast<const float4*>(qs + (size_t)c * DC);
-          for (int u0 = 0; u0 < (DC >> 2); u0 += 8) {  // 8 float4s loaded ahead of 32 fmafs
-            float4 xv[8], qv[8];
+      }
+    };
+    for (int i = 0; i < NB - 1 && i < nitems; ++i) issue(i);
+    for (int i = NB - 1; i < NB - 1 + PF; ++i) prefetch(i);
+    float acc = 0.0f;
+    uint64_t ck = 0ull;
+    for (int i = 0; i < nitems; ++i) {
+      // the buffer item i - 1 used: released by the __syncthreads that closed item i - 1
+      if (i + NB - 1 < nitems) issue(i + NB - 1);
+      if (PF) prefetch(i + NB - 1 + PF);
+      const int r = i / nch, c = i - r * nch, no = base + i;
+      if (c == 0) {
+        ck = row_key(r);
+        acc = 0.0f;
+      }
+      mbar_wait(&s_bar[no % NB], (uint32_t)((no / NB) & 1));
+      if (ck) {
+        const float4* x = reinterpret_cast<const float4*>(rowbuf + ((size_t)(no % NB) * R + t) * RS);
+        const float4* q4 = reinterpret_cast<const float4*>(qs + (size_t)c * DC);
+        for (int u0 = 0; u0 < (DC >> 2); u0 += 8) {  // 8 float4s loaded ahead of 32 fmafs
+          float4 xv[8], qv[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              xv[u] = x[u0 + u];
-              qv[u] = q4[u0 + u];
-            }
+          for (int u = 0; u < 8; ++u) {
+            xv[u] = x[u0 + u];
+            qv[u] = q4[u0 + u];
+          }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              acc = fmaf(xv[u].x, qv[u].x, acc);
-              acc = fmaf(xv[u].y, qv[u].y, acc);
-              acc = fmaf(xv[u].z, qv[u].z, acc);
-              acc = fmaf(xv[u].w, qv[u].w, acc);
-            }
+          for (int u = 0; u < 8; ++u) {
+            acc = fmaf(xv[u].x, qv[u].x, acc);
+            acc = fmaf(xv[u].y, qv[u].y, acc);
+            acc = fmaf(xv[u].z, qv[u].z, acc);
+            acc = fmaf(xv[u].w, qv[u].w, acc);
           }
         }
-        __syncthreads();  // this buffer is refilled two chunks later
       }
-      if (t < R && idx < j1) keys[idx] = ck ? vx_make_key(acc, vx_key_id(ck)) : 0ull;
+      if (c == nch - 1) {
+        const int idx = j0 + r * R + t;
+        if (t < R && idx < j1) keys[idx] = ck ? vx_make_key(acc, vx_key_id(ck)) : 0ull;
+      }
+      __syncthreads();  // this buffer is refilled NB - 1 items later
     }
+    chunk_no = base + nitems;
     __syncthreads();  // keys[] complete
   };
   if (phase == 2) {
@@ -585,6 +624,20 @@ __global__ void __launch_bounds__(256)
     }
   }
   if (threadIdx.x == 0) flags[b] = s_fail;
+  if (fz.ctr) {  // fused compaction: the last CTA of the launch takes the whole batch
+    __shared__ int s_last;
+    if (threadIdx.x == 0) {
+      __threadfence();  // this CTA's flag before its ticket
+      s_last = atomicAdd(fz.ctr, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();  // every other CTA's flag (they fenced before their tickets)
+      cert_compact_block(fz.flags_all, fz.Ball, fz.qall, D, fz.fidx, fz.fcount, fz.fq,
+                         (cudaGraphConditionalHandle)fz.cond, fz.use_cond);
+      if (threadIdx.x == 0) *fz.ctr = 0u;  // re-armed for the next launch (graph replays)
+    }
+  }
 }
 
 // ------------------------------------------------------------------- K2c: wide re-rank
@@ -876,12 +929,14 @@ cudaError_t launch_scan_tc(int QT, int TD, const CUtensorMap* tq, const CUtensor
 // k' = 1024, profiles/r01/rerank_chunks.txt): R = 64 / DC = 192 (two CTAs per SM) 519-539 us
 // at 4.4 TB/s, R = 128 533-558, R = 256 / DC = 96 563-585, R = 192 / DC = 64 740-760.
 // VX_DEBUG_RERANK_ROWS / _DC: timing experiments.
-cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64_t* cand, int B,
+cudaError_t launch_rerank(const float* docs, const float* q, int D, uint64_t* cand, int B,
                           int kp, const uint64_t* part, int grid, int ldlists, int kc, int k,
                           int64_t row0, const float* xstats, int fmt, const float* qscale,
                           uint64_t* out_keys, int64_t* out_ids, float* out_scores, int* flags,
                           cudaStream_t st, int phase, const float* tau, uint64_t* hkeys,
-                          float* lb, const uint64_t* seed, int seed_ld) {
+                          float* lb, const uint64_t* seed, int seed_ld, const RerankFuse& fz) {
+  if (fz.mlists && (fz.mM > kMergeSmemKeys || (fz.mM & 1) || fz.mM < kp))
+    return cudaErrorInvalidValue;
   const size_t base = (size_t)((D + 3) & ~3) * 4 + (size_t)kp * 8;
   static const int env_rows = [] {
     const char* e = getenv("VX_DEBUG_RERANK_ROWS");
@@ -891,26 +946,46 @@ cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64
     const char* e = getenv("VX_DEBUG_RERANK_DC");
     return e ? atoi(e) : 0;
   }();
+  static const int env_bufs = [] {
+    const char* e = getenv("VX_DEBUG_RERANK_BUFS");
+    return e ? atoi(e) : 0;
+  }();
+  static const int env_pf = [] {
+    const char* e = getenv("VX_DEBUG_RERANK_PF");
+    return e ? atoi(e) : -1;
+  }();
+  const int head_all = phase == 0 && B <= 64 ? 1 : 0;
+  int NB = env_bufs >= 2 ? std::min(env_bufs, kRerankMaxBufs) : 2;
   int DC = env_dc > 0 && env_dc % 32 == 0 && D % env_dc == 0 ? env_dc : 192;
   while (DC > 32 && D % DC) DC -= 32;
   int R = env_rows > 0 ? std::min(env_rows, 256) : 64;
-  auto smem_of = [&](int r) { return base + 2 * (size_t)r * (DC + 4) * 4; };
-  while (R > 32 && smem_of(R) > 220 * 1024) R -= 32;
+  static const int env_smem_kb = [] {
+    const char* e = getenv("VX_DEBUG_RERANK_SMEM_KB");
+    return e ? atoi(e) : 0;
+  }();
+  auto smem_of = [&](int r) { return base + (size_t)NB * r * (DC + 4) * 4; };
+  const size_t smem_cap = (size_t)(env_smem_kb > 0 ? std::min(env_smem_kb, 220) : 110) * 1024;
+  while (R > 16 && smem_of(R) > smem_cap) R -= 16;  // default: two CTAs per SM
   size_t smem = smem_of(R);
-  const int head_all = phase == 0 && B <= 64 ? 1 : 0;
   // small batch, latency-bound: ALL k' whole rows in one burst of bulk copies and one wait
-  // (one round, one chunk: only buffer 0 is used), instead of double-buffered chunk rounds
+  // (one round, one chunk), instead of the chunk stream
   if (head_all && env_dc == 0 && base + (size_t)kp * (D + 4) * 4 <= 220 * 1024) {
     DC = D;
     R = kp;
+    NB = 2;
     smem = base + (size_t)kp * (D + 4) * 4;
   }
+  // L2 prefetch distance in items beyond the staging window (packed into nbuf's high bits)
+  const int PF = head_all ? 0 : std::min(env_pf >= 0 ? env_pf : 0, 15);
+  // the fused merge stages the lists and its selection in the row buffers
+  if (fz.mlists) smem = std::max(smem, base + (size_t)(fz.mM + 2 * kp) * 8);
   cudaError_t e = cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
   rerank_kernel<<<B, 256, smem, st>>>(docs, q, D, cand, kp, part, grid, ldlists, kc, k, row0,
                                       xstats, fmt, qscale, out_keys, out_ids, out_scores, flags, R,
-                                      DC, phase, tau, hkeys, lb, seed, seed_ld, head_all);
+                                      DC, phase, tau, hkeys, lb, seed, seed_ld, head_all,
+                                      NB | (PF << 4), fz);
   return cudaGetLastError();
 }
 

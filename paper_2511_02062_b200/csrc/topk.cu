@@ -15,12 +15,9 @@
 #include "vx_internal.cuh"
 #include "vx_ptx.cuh"
 #include "vx_sort.cuh"
+#include "vx_merge.cuh"
 
 namespace vx {
-
-constexpr int kMergeThreads = 256;
-constexpr int kMaxK = 1024;  // merge: k' up to 1024 (the TC candidate set); order_by: k <= 256
-constexpr int kMergeSmemKeys = 12288;  // 96 KB of dynamic smem
 
 __device__ __forceinline__ void block_bitonic_desc(uint64_t* buf, int n) {
   for (int size = 2; size <= n; size <<= 1) {
@@ -47,186 +44,10 @@ __global__ void __launch_bounds__(kMergeThreads)
                       int64_t ldout) {
   if (d_count && (int)blockIdx.x >= *d_count) return;  // device-sized batch (cert fallback)
   extern __shared__ uint64_t staged[];  // [M] when launched with M * 8 bytes of dynamic smem
-  __shared__ uint32_t hist[256];
-  __shared__ uint64_t s_prefix, s_mask;
-  __shared__ int s_kk, s_done, s_above, s_eq;
   __shared__ uint64_t sel[kMaxK];
-  const uint64_t* L = in + (size_t)blockIdx.x * ldin;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (M <= kMergeSmemKeys && (M & 1) == 0) {  // stage (16-byte loads, all in flight)
-    const uint4* src = reinterpret_cast<const uint4*>(L);
-    uint4* dst = reinterpret_cast<uint4*>(staged);
-    if ((reinterpret_cast<uintptr_t>(L) & 15) == 0) {
-      for (int i = threadIdx.x; i < (M >> 1); i += blockDim.x) dst[i] = src[i];
-    } else {
-      for (int i = threadIdx.x; i < M; i += blockDim.x) staged[i] = L[i];
-    }
-    __syncthreads();
-    L = staged;
-  }
-
-  // the digits every key shares need no pass: start at the first byte where the largest
-  // and the smallest key differ (scores of one query's candidates share sign, exponent and
-  // often leading mantissa bits — one or two of the ~3 passes)
-  uint64_t kmax = 0ull, kmin = ~0ull;
-  for (int i = threadIdx.x; i < M; i += blockDim.x) {
-    const uint64_t v = L[i];
-    kmax = v > kmax ? v : kmax;
-    kmin = v < kmin ? v : kmin;
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    const uint64_t a = shfl_xor_u64(kmax, o), b = shfl_xor_u64(kmin, o);
-    kmax = a > kmax ? a : kmax;
-    kmin = b < kmin ? b : kmin;
-  }
-  __shared__ uint64_t s_mx[kMergeThreads / 32], s_mn[kMergeThreads / 32];
-  if (lane == 0) {
-    s_mx[warp] = kmax;
-    s_mn[warp] = kmin;
-  }
-  __syncthreads();
-  kmax = s_mx[0];
-  kmin = s_mn[0];
-  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
-    kmax = s_mx[w] > kmax ? s_mx[w] : kmax;
-    kmin = s_mn[w] < kmin ? s_mn[w] : kmin;
-  }
-  const int common_bytes = (kmax == kmin) ? 7 : (__clzll((long long)(kmax ^ kmin)) >> 3);
-  uint64_t mask = common_bytes ? (~0ull << (64 - 8 * common_bytes)) : 0ull;
-  uint64_t prefix = kmax & mask;
-  int kk = k;
-  for (int shift = 56 - 8 * common_bytes; shift >= 0; shift -= 8) {
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
-    __syncthreads();
-    // histogram of the next digit over the keys still matching the prefix.  Top digits are
-    // shared by most keys, so a warp whose live lanes all carry one digit adds once; mixed
-    // warps add per lane (match.any aggregation was the kernel's critical path: its result
-    // latency stalled every iteration — profiles/r02)
-    // Four keys per thread per iteration: their chains are independent, so the warp keeps
-    // four in flight (one key at a time left every iteration a ~300-cycle dependent chain).
-    for (int i0 = 0; i0 < M; i0 += 4 * (int)blockDim.x) {
-      uint64_t kx[4];
-      bool lv[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int i = i0 + u * (int)blockDim.x + (int)threadIdx.x;
-        kx[u] = i < M ? L[i] : 0ull;
-        lv[u] = i < M && (kx[u] & mask) == prefix;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const unsigned act = __ballot_sync(0xffffffffu, lv[u]);
-        if (act == 0u) continue;
-        const uint32_t dg = (uint32_t)(kx[u] >> shift) & 255u;
-        const uint32_t d0 = __shfl_sync(0xffffffffu, dg, __ffs(act) - 1);
-        const bool uni = __all_sync(0xffffffffu, !lv[u] || dg == d0);
-        if (uni) {
-          if (lane == 0) atomicAdd(&hist[d0], (uint32_t)__popc(act));
-        } else if (lv[u]) {
-          atomicAdd(&hist[dg], 1u);
-        }
-      }
-    }
-    __syncthreads();
-    if (warp == 0) {
-      // bins from the top: lane l owns digits 255-8l .. 248-8l; find the digit d holding
-      // the kk-th key (descending) with a suffix scan over the lanes
-      uint32_t c[8];
-      uint32_t tot = 0;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        c[j] = hist[255 - 8 * lane - j];
-        tot += c[j];
-      }
-      uint32_t incl = tot;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      const uint32_t excl = incl - tot;  // keys in higher digits than this lane's
-      const bool mine = excl < (uint32_t)kk && incl >= (uint32_t)kk;
-      const unsigned who = __ballot_sync(0xffffffffu, mine);
-      if (who == 0) {
-        // fewer than kk keys match at all: every one of them is selected; digit 0 (lane 31,
-        // j = 7) becomes the "equal" bin, the other digits count as above it
-        if (lane == 31) {
-          s_prefix = prefix;
-          s_mask = mask | (0xFFull << shift);
-          s_kk = kk - (int)(incl - c[7]);
-          s_done = 1;
-        }
-      } else if (lane == __ffs(who) - 1) {
-        uint32_t above = excl;
-        int d = 255 - 8 * lane;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (above + c[j] >= (uint32_t)kk) {
-            d = 255 - 8 * lane - j;
-            s_kk = kk - (int)above;
-            s_done = (c[j] == (uint32_t)kk - above);
-            break;
-          }
-          above += c[j];
-        }
-        s_prefix = prefix | ((uint64_t)d << shift);
-        s_mask = mask | (0xFFull << shift);
-      }
-    }
-    __syncthreads();
-    prefix = s_prefix;
-    mask = s_mask;
-    kk = s_kk;
-    if (s_done) break;
-    __syncthreads();
-  }
-  int kp = 16;
-  while (kp < k) kp <<= 1;
-  for (int i = threadIdx.x; i < kp; i += blockDim.x) sel[i] = 0ull;
-  if (threadIdx.x == 0) {
-    s_above = 0;
-    s_eq = 0;
-  }
-  __syncthreads();
-  const int n_above = k - kk;
-  for (int i0 = 0; i0 < M; i0 += 4 * (int)blockDim.x) {
-    uint64_t kx[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i = i0 + u * (int)blockDim.x + (int)threadIdx.x;
-      kx[u] = i < M ? L[i] : 0ull;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i = i0 + u * (int)blockDim.x + (int)threadIdx.x;
-      if (i >= M) continue;
-      const uint64_t m = kx[u] & mask;
-      if (m > prefix) {
-        const int slot = atomicAdd(&s_above, 1);
-        sel[slot] = kx[u];
-      } else if (m == prefix) {
-        const int slot = atomicAdd(&s_eq, 1);
-        if (slot < kk) sel[n_above + slot] = kx[u];
-      }
-    }
-  }
-  __syncthreads();
-  block_sort_desc(sel, kp);
-  for (int i = threadIdx.x; i < k; i += blockDim.x) {
-    uint64_t key = sel[i];
-    size_t o = (size_t)blockIdx.x * ldout + i;
-    if (key == 0ull) {
-      if (out_keys) out_keys[o] = 0ull;
-      if (out_ids) out_ids[o] = -1;
-      if (out_scores) out_scores[o] = -INFINITY;
-    } else {
-      int64_t gid = (int64_t)vx_key_id(key) + id_base;
-      if (out_keys)
-        out_keys[o] = (key & 0xFFFFFFFF00000000ull) | (uint64_t)(0xFFFFFFFFu - (uint32_t)gid);
-      if (out_ids) out_ids[o] = gid;
-      if (out_scores) out_scores[o] = vx_key_score(key);
-    }
-  }
+  merge_topk_block(in + (size_t)blockIdx.x * ldin, M, k, id_base, out_keys, out_ids, out_scores,
+                   blockIdx.x, ldout, (M <= kMergeSmemKeys && (M & 1) == 0) ? staged : nullptr,
+                   sel);
 }
 
 cudaError_t launch_merge_topk(const uint64_t* in, int B, int M, int k, int64_t id_base,
@@ -315,55 +136,6 @@ namespace vx {
 
 // ---- device-side handling of tensor-core certificate failures (no host round trip, so the
 // whole stage can live in one CUDA graph)
-__global__ void __launch_bounds__(1024)
-    cert_compact_kernel(const int* __restrict__ flags, int B, const float* __restrict__ q, int D,
-                        int* __restrict__ fidx, int* __restrict__ fcount, float* __restrict__ fq,
-                        cudaGraphConditionalHandle cond, int use_cond) {
-  // stream compaction of the flagged queries (ascending order), 1024 flags per round:
-  // warp ballots + a prefix over the 32 warp counts
-  __shared__ int s_warp[32];
-  __shared__ int s_base;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_base = 0;
-  __syncthreads();
-  for (int b0 = 0; b0 < B; b0 += 1024) {
-    const int b = b0 + (int)threadIdx.x;
-    const bool f = b < B && flags[b] != 0;
-    const unsigned m = __ballot_sync(0xffffffffu, f);
-    if (lane == 0) s_warp[warp] = __popc(m);
-    __syncthreads();
-    if (warp == 0) {
-      const int c = s_warp[lane];
-      int x = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-      }
-      s_warp[lane] = x - c;  // exclusive prefix
-    }
-    __syncthreads();
-    const int base = s_base;
-    if (f) fidx[base + s_warp[warp] + __popc(m & ((1u << lane) - 1u))] = b;
-    __syncthreads();
-    if (threadIdx.x == 1023) s_base = base + s_warp[31] + __popc(m);
-    __syncthreads();
-  }
-  const int n = s_base;
-  if (threadIdx.x == 0) {
-    fcount[0] = n;   // this batch
-    fcount[1] += n;  // running total (vx_stats.cert_fallbacks)
-    // captured stage: the rest of the certificate chain is the body of a conditional graph
-    // node that runs only when some query failed (vx_stage.cu local_topk_tc)
-    if (use_cond) cudaGraphSetConditional(cond, n > 0 ? 1u : 0u);
-  }
-  __threadfence_block();
-  __syncthreads();
-  for (int i = threadIdx.x; i < n * D; i += blockDim.x) {
-    const int r = i / D;
-    fq[i] = q[(size_t)fidx[r] * D + (i - r * D)];
-  }
-}
 
 __global__ void cert_scatter_kernel(const int* __restrict__ fidx, const int* __restrict__ fcount,
                                     int k, const uint64_t* __restrict__ fkeys,
@@ -378,6 +150,13 @@ __global__ void cert_scatter_kernel(const int* __restrict__ fidx, const int* __r
     ids[dst + j] = fids[src + j];
     scores[dst + j] = fsc[src + j];
   }
+}
+
+__global__ void __launch_bounds__(1024)
+    cert_compact_kernel(const int* __restrict__ flags, int B, const float* __restrict__ q, int D,
+                        int* __restrict__ fidx, int* __restrict__ fcount, float* __restrict__ fq,
+                        cudaGraphConditionalHandle cond, int use_cond) {
+  cert_compact_block(flags, B, q, D, fidx, fcount, fq, cond, use_cond);
 }
 
 cudaError_t launch_cert_compact(const int* flags, int B, const float* q, int D, int* fidx,

@@ -184,6 +184,7 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
   ALLOC(h->d_fq, B * D * 4);
   ALLOC(h->d_fidx, B * 4);
   ALLOC(h->d_fcount, 16);
+  ALLOC(h->d_ctr, 16);
   ALLOC(h->d_ktimer, sizeof(vx::KTimer) * vx::KT_N);
   // bf16 shadow for the coarse scan: K-chunks of 64 bf16 (one 128-byte swizzle atom), so
   // D % 64 == 0; otherwise the coarse scan reads the fp32 rows as TF32 (32-wide chunks)
@@ -217,7 +218,7 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
     return cleanup(fail(VX_ERR_OOM, "pinned header"));
   if (cudaMallocHost((void**)&h->h_flags, B * 4) != cudaSuccess)
     return cleanup(fail(VX_ERR_OOM, "pinned flags"));
-  if (cudaMemset(h->d_xnorm, 0, (8 + D) * 4) != cudaSuccess || cudaMemset(h->d_fcount, 0, 16) != cudaSuccess ||
+  if (cudaMemset(h->d_xnorm, 0, (8 + D) * 4) != cudaSuccess || cudaMemset(h->d_fcount, 0, 16) != cudaSuccess || cudaMemset(h->d_ctr, 0, 16) != cudaSuccess ||
       ktimer_reset(h) != VX_OK)
     return cleanup(fail(VX_ERR_CUDA, "memset"));
   if (h->tokens) {
@@ -254,13 +255,15 @@ extern "C" vx_status vx_index_destroy(vx_index* h) {
   // destroying it under live graphs hangs
   for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second.exec);
   h->graphs.clear();
+  for (auto& kv : h->io_graphs) cudaGraphExecDestroy(kv.second.exec);
+  h->io_graphs.clear();
   if (h->comm) nccl().CommDestroy(h->comm);
   void* ptrs[] = {h->docs,  h->tokens,    h->d_q,      h->d_qtok,    h->d_part, h->d_keys,
                   h->d_ids, h->d_ip,      h->d_ms,     h->d_out_ids, h->d_out_ip,
                   h->d_out_ms, h->d_send, h->d_recv, h->d_hdr, h->d_ckeys, h->d_seedk, h->d_flags,
                   h->d_xnorm, h->d_fq, h->docs16, h->d_q16, h->d_fidx, h->d_fcount,
                   h->d_qtok16, h->docs8, h->d_q8, h->d_qs8, h->d_lball, h->d_tau, h->d_hkeys,
-                  h->d_ktimer, h->d_colmax};
+                  h->d_ktimer, h->d_colmax, h->d_ctr};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->h_stage) cudaFreeHost(h->h_stage);
@@ -603,12 +606,19 @@ static vx_status host_search(vx_index* h, const float* q, const float* const* q_
   uint8_t* stage = static_cast<uint8_t*>(h->h_stage);
   CU_TRY(cudaMemcpyAsync(h->d_q, upload_src(h, stage, q, q_rows, B, qrow), qb,
                          cudaMemcpyHostToDevice, st));
-  VX_TRY(stage_begin(h, OP_SEARCH, h->d_q, B, 0, k, st));
-  VX_TRY(stage_search_out(h, B, k, h->d_out_ids, h->d_out_ip, st));
+  // the direct graph writes the stage's own result buffers (d_ids / d_ip: the certificate
+  // chain uses d_out_* as level-3 scratch), the two-part path copies them to d_out_*
+  bool done = false;
+  VX_TRY(stage_direct(h, OP_SEARCH, h->d_q, nullptr, B, 0, k, h->d_ids, h->d_ip, nullptr, st,
+                      &done));
+  if (!done) {
+    VX_TRY(stage_begin(h, OP_SEARCH, h->d_q, B, 0, k, st));
+    VX_TRY(stage_search_out(h, B, k, h->d_out_ids, h->d_out_ip, st));
+  }
   const size_t n = (size_t)B * k;
   bool d_ids, d_sc;
-  CU_TRY(download(h, ids, stage, h->d_out_ids, n * 8, st, &d_ids));
-  CU_TRY(download(h, scores, stage + n * 8, h->d_out_ip, n * 4, st, &d_sc));
+  CU_TRY(download(h, ids, stage, done ? h->d_ids : h->d_out_ids, n * 8, st, &d_ids));
+  CU_TRY(download(h, scores, stage + n * 8, done ? h->d_ip : h->d_out_ip, n * 4, st, &d_sc));
   VX_TRY(vx_sync(h));
   if (d_ids) memcpy(ids, stage, n * 8);
   if (d_sc) memcpy(scores, stage + n * 8, n * 4);

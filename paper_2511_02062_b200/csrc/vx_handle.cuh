@@ -134,6 +134,7 @@ struct vx_index {
   float* d_fq = nullptr;         // [maxB][D] queries gathered for the exact fallback
   int* d_fidx = nullptr;         // [maxB] flagged query indices
   int* d_fcount = nullptr;       // [2] flagged count of the last batch, running total
+  unsigned* d_ctr = nullptr;     // ticket counter of the re-rank's fused compaction (0 at rest)
   vx::KTimer* d_ktimer = nullptr;  // [KT_N] device-side launch timers (vx_stats.kt_*)
   // pinned host staging
   void* h_stage = nullptr;
@@ -164,6 +165,25 @@ struct vx_index {
   };
   bool use_graphs = false;
   std::map<uint64_t, GraphEntry> graphs;
+  // Direct-I/O graphs (one GPU): the whole stage captured against the caller's own device
+  // buffers, so a replay needs no copies in or out (each D2D copy around a replay is a
+  // separate ~2-4 us operation — a fifth of a 100K-row small-batch step).  Keyed by shape AND
+  // the buffer addresses; captured on the second sighting of an address tuple (a one-off
+  // buffer never pays a capture), at most kIoGraphsPerShape tuples per shape.
+  struct IoKey {
+    uint64_t shape;
+    uintptr_t p[5];
+    bool operator<(const IoKey& o) const {
+      if (shape != o.shape) return shape < o.shape;
+      for (int i = 0; i < 5; ++i)
+        if (p[i] != o.p[i]) return p[i] < o.p[i];
+      return false;
+    }
+  };
+  static constexpr int kIoGraphsPerShape = 4;
+  std::map<IoKey, GraphEntry> io_graphs;
+  std::map<IoKey, int> io_seen;
+  std::map<uint64_t, int> io_per_shape;
 };
 
 static inline void count_launch(vx_index* h, int n = 1) { h->st.kernel_launches += n; }
@@ -182,11 +202,15 @@ static inline vx_status ktimer_reset(vx_index* h) {
 // change and any index upload / synth throws them away; the next batch of each shape
 // re-captures.
 static inline void drop_graphs(vx_index* h) {
-  if (h->graphs.empty()) return;
+  h->io_seen.clear();
+  if (h->graphs.empty() && h->io_graphs.empty()) return;
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second.exec);
+  for (auto& kv : h->io_graphs) cudaGraphExecDestroy(kv.second.exec);
   h->graphs.clear();
+  h->io_graphs.clear();
+  h->io_per_shape.clear();
 }
 
 // Timing events: inside a stream capture they must be EXTERNAL event nodes, or the graph only
@@ -243,5 +267,8 @@ vx_status stage_begin(vx_index* h, int op, const float* d_q, int B, int nq, int 
 vx_status run_part(vx_index* h, int part, int B, int nq, int k, cudaStream_t st);
 vx_status stage_search_out(vx_index* h, int B, int k, int64_t* d_ids, float* d_ip,
                            cudaStream_t st);
+vx_status stage_direct(vx_index* h, int op, const float* d_q, const float* d_qtok, int B, int nq,
+                       int k, int64_t* d_ids, float* d_ip, float* d_ms, cudaStream_t st,
+                       bool* done);
 vx_status stage_finish(vx_index* h, const float* d_qtok, int B, int nq, int k, int64_t* d_ids,
                        float* d_ip, float* d_ms, cudaStream_t st);

@@ -101,6 +101,9 @@ __host__ __device__ constexpr int kc_of(int fmt) { return fmt == FMT_I8 ? 32 : 1
 // list length of the seed's sample pass (vx_stage.cu): the seed is the m-th best of the
 // union of the lists, and truncated lists only lower it (a valid, slightly looser seed)
 constexpr int kSampleKC = 4;
+// K3 merge: most keys per query staged in shared memory (96 KB; also the bound for fusing
+// the merge into the re-rank)
+constexpr int kMergeSmemKeys = 12288;
 // s8 quantisation used by the shadow, the queries and the certificate's residuals
 __device__ __forceinline__ int8_t vx_quant8(float v, float s) {
   const float r = rintf(v / s);
@@ -118,13 +121,34 @@ cudaError_t launch_scan_tc2(int H, const CUtensorMap* tq, const CUtensorMap* tx,
 // phase 0: the whole re-rank; sharded: phase 1 (head: exact keys of the k best coarse
 // candidates -> hkeys, their scores -> lb) and phase 2 (tail, pruned by tau) around the
 // exchange of lb (see scan_tc.cu)
-cudaError_t launch_rerank(const float* docs, const float* q, int D, const uint64_t* cand, int B,
+// Fusions into the re-rank launch (all optional):
+//  * merge: each CTA first merges its query's per-CTA lists (mlists + b * mld, mM keys) to
+//    the coarse top-k' in cand (the K3 launch it replaces, vx_merge.cuh merge_topk_block);
+//  * compact: the launch's last CTA (ticket counter ctr, zero on entry and reset on exit)
+//    compacts the certificate failures of the WHOLE batch (flags_all[0, Ball)) for levels
+//    2-3 and sets the captured stage's conditional handle (the cert_compact launch).
+struct RerankFuse {
+  const uint64_t* mlists = nullptr;
+  int mM = 0;
+  int64_t mld = 0;
+  unsigned* ctr = nullptr;
+  const int* flags_all = nullptr;
+  int Ball = 0;
+  const float* qall = nullptr;
+  int* fidx = nullptr;
+  int* fcount = nullptr;
+  float* fq = nullptr;
+  unsigned long long cond = 0;
+  int use_cond = 0;
+};
+cudaError_t launch_rerank(const float* docs, const float* q, int D, uint64_t* cand, int B,
                           int kp, const uint64_t* part, int grid, int ldlists, int kc, int k,
                           int64_t row0, const float* xstats, int fmt, const float* qscale,
                           uint64_t* out_keys, int64_t* out_ids, float* out_scores, int* flags,
                           cudaStream_t st, int phase = 0, const float* tau = nullptr,
                           uint64_t* hkeys = nullptr, float* lb = nullptr,
-                          const uint64_t* seed = nullptr, int seed_ld = 0);
+                          const uint64_t* seed = nullptr, int seed_ld = 0,
+                          const RerankFuse& fuse = RerankFuse{});
 // tau[B] = k-th largest of all[G][B][k] (G k <= 1024)
 cudaError_t launch_shard_tau(const float* all, int G, int B, int k, float* tau, cudaStream_t st);
 // second certificate level over the full per-CTA lists (compacted failing queries): two

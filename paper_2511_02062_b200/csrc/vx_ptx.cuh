@@ -82,6 +82,10 @@ VX_DEV void tma_load_2d(void* smem_dst, const void* tmap, uint64_t* bar, int32_t
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
       : "memory");
 }
+// L2 prefetch of one 128-byte line (no register result, fire and forget).
+VX_DEV void prefetch_l2(const void* g) {
+  asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(reinterpret_cast<uint64_t>(g)));
+}
 // 1-D bulk copy global -> smem (16 B aligned, size multiple of 16).
 VX_DEV void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
   asm volatile(

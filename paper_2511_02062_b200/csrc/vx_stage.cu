@@ -302,34 +302,6 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
   // each query's seed key (the certificate bounds what it dropped), stride kSeedLd
   const uint64_t* seed_keys = seeded ? h->d_seedk + (kSeedM - 1) : nullptr;
   CU_TRY(record_ev(h, h->tev[1], st));
-  // merge each query's lists to the coarse top-k', exact re-rank (per run of query groups
-  // with the same P, so the 2-per-SM re-rank CTAs pack full waves)
-  VX_TRY(merge_lists(h->d_part, KC, kp, h->d_ckeys, kp));
-  // exact re-rank.  Sharded: phase 1 re-scores each query's k best coarse candidates, the
-  // shards all-gather those exact scores (shard_tau: tau <= the global exact k-th), phase 2
-  // re-ranks only the candidates that can still reach the GLOBAL top-k
-  const bool sharded = h->nranks > 1;
-  float* lb = reinterpret_cast<float*>(h->d_send);
-  for (int pass = sharded ? 1 : 0; pass <= (sharded ? 2 : 0); ++pass) {
-    if (pass == 2) VX_TRY(shard_tau(h, lb, B, k, st, true));
-    for (int r0 = 0; r0 < B;) {
-      const int P = lists_per_query(r0);
-      int r1 = r0;
-      while (r1 < B && lists_per_query(r1) == P) r1 += GS;
-      r1 = std::min(r1, B);
-      CU_TRY(vx::launch_rerank(h->docs, d_q + (size_t)r0 * D, D, h->d_ckeys + (size_t)r0 * kp,
-                               r1 - r0, kp, h->d_part + (size_t)r0 * ldp, P, grid, KC, k,
-                               h->row0, reinterpret_cast<const float*>(h->d_xnorm), fmt,
-                               i8 ? h->d_qs8 + r0 : nullptr, keys + (size_t)r0 * k,
-                               ids + (size_t)r0 * k, scores + (size_t)r0 * k, h->d_flags + r0,
-                               st, pass, pass == 2 ? h->d_tau + r0 : nullptr,
-                               sharded ? h->d_hkeys + (size_t)r0 * k : nullptr,
-                               lb + (size_t)r0 * k,
-                               seed_keys ? seed_keys + (size_t)r0 * kSeedLd : nullptr, kSeedLd));
-      count_launch(h);
-      r0 = r1;
-    }
-  }
   // Certificate failures, entirely on device (no host round trip: the stage stays
   // capturable in one CUDA graph; every launch below exits at once when its count is 0):
   //   level 2: compact the failing queries, re-rank all their list entries above the
@@ -338,6 +310,70 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
   //            count) and scattered back.
   int* cnt2 = h->d_fcount;      // [count, running total] of level-2 queries
   int* cnt3 = h->d_fcount + 2;  // [count, running total] of exact re-scans
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  CU_TRY(cudaStreamIsCapturing(st, &cap));
+  const bool captured = cap == cudaStreamCaptureStatusActive;
+  // Captured (CUDA graph): the compaction sets a conditional handle, and levels 2-3 are the
+  // body of an IF node — a batch whose queries all pass certificate 1 (the common case)
+  // replays no level-2/3 launches at all (six ~2.5 us empty launches at B = 16, 100K rows).
+  cudaGraphConditionalHandle hc = 0;
+  if (captured) {
+    cudaGraph_t g = nullptr;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    CU_TRY(cudaStreamGetCaptureInfo(st, &cap, nullptr, &g, &deps, &ndeps));
+    CU_TRY(cudaGraphConditionalHandleCreate(&hc, g, 0, cudaGraphCondAssignDefault));
+  }
+  // exact re-rank (per run of query groups with the same P, so the 2-per-SM re-rank CTAs pack
+  // full waves), with the K3 merge of each query's lists to its coarse top-k' fused in front
+  // (no merge launch, no candidate round trip) and the compaction of the batch's certificate
+  // failures in the last CTA of the last launch (no compaction launch).  Sharded: phase 1
+  // re-scores each query's k best coarse candidates, the shards all-gather those exact scores
+  // (shard_tau: tau <= the global exact k-th), phase 2 re-ranks only the candidates that can
+  // still reach the GLOBAL top-k
+  const bool sharded = h->nranks > 1;
+  static const bool no_fuse = getenv("VX_DEBUG_NO_FUSE_MERGE") != nullptr;  // A/B timing only
+  const bool fuse_merge = !no_fuse && (int64_t)h->grid * KC <= vx::kMergeSmemKeys;
+  if (!fuse_merge) VX_TRY(merge_lists(h->d_part, KC, kp, h->d_ckeys, kp));
+  float* lb = reinterpret_cast<float*>(h->d_send);
+  for (int pass = sharded ? 1 : 0; pass <= (sharded ? 2 : 0); ++pass) {
+    if (pass == 2) VX_TRY(shard_tau(h, lb, B, k, st, true));
+    for (int r0 = 0; r0 < B;) {
+      const int P = lists_per_query(r0);
+      int r1 = r0;
+      while (r1 < B && lists_per_query(r1) == P) r1 += GS;
+      r1 = std::min(r1, B);
+      vx::RerankFuse fz;
+      if (fuse_merge && pass <= 1) {
+        fz.mlists = h->d_part + (size_t)r0 * ldp;
+        fz.mM = P * KC;
+        fz.mld = ldp;
+      }
+      if (pass != 1 && r1 == B) {
+        fz.ctr = h->d_ctr;
+        fz.flags_all = h->d_flags;
+        fz.Ball = B;
+        fz.qall = d_q;
+        fz.fidx = h->d_fidx;
+        fz.fcount = cnt2;
+        fz.fq = h->d_fq;
+        fz.cond = (unsigned long long)hc;
+        fz.use_cond = captured ? 1 : 0;
+      }
+      CU_TRY(vx::launch_rerank(h->docs, d_q + (size_t)r0 * D, D, h->d_ckeys + (size_t)r0 * kp,
+                               r1 - r0, kp, h->d_part + (size_t)r0 * ldp, P, grid, KC, k,
+                               h->row0, reinterpret_cast<const float*>(h->d_xnorm), fmt,
+                               i8 ? h->d_qs8 + r0 : nullptr, keys + (size_t)r0 * k,
+                               ids + (size_t)r0 * k, scores + (size_t)r0 * k, h->d_flags + r0,
+                               st, pass, pass == 2 ? h->d_tau + r0 : nullptr,
+                               sharded ? h->d_hkeys + (size_t)r0 * k : nullptr,
+                               lb + (size_t)r0 * k,
+                               seed_keys ? seed_keys + (size_t)r0 * kSeedLd : nullptr, kSeedLd,
+                               fz));
+      count_launch(h);
+      r0 = r1;
+    }
+  }
   // wide-key scratch: the upper part of d_part (the lists use B x grid x KC <= B x grid x 32
   // of its B x grid x 256 entries; the level-3 re-scan writes d_part only after level 2)
   uint64_t* wkeys = h->d_part + (size_t)h->desc.max_batch * grid * 32;
@@ -358,26 +394,11 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
     else h->st.kernel_launches = before;  // conditional body: runs only on a failure
     return VX_OK;
   };
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  CU_TRY(cudaStreamIsCapturing(st, &cap));
-  if (cap != cudaStreamCaptureStatusActive) {
-    // eager: every launch below exits at once when its device-side count is 0
-    CU_TRY(vx::launch_cert_compact(h->d_flags, B, d_q, D, h->d_fidx, cnt2, h->d_fq, st));
-    count_launch(h);
-    return chain(st, true);
-  }
-  // Captured (CUDA graph): the compaction sets a conditional handle, and levels 2-3 are the
-  // body of an IF node — a batch whose queries all pass certificate 1 (the common case)
-  // replays no level-2/3 launches at all (six ~2.5 us empty launches at B = 16, 100K rows).
+  // eager: every launch below exits at once when its device-side count is 0
+  if (!captured) return chain(st, true);
   cudaGraph_t g = nullptr;
   const cudaGraphNode_t* deps = nullptr;
   size_t ndeps = 0;
-  CU_TRY(cudaStreamGetCaptureInfo(st, &cap, nullptr, &g, &deps, &ndeps));
-  cudaGraphConditionalHandle hc;
-  CU_TRY(cudaGraphConditionalHandleCreate(&hc, g, 0, cudaGraphCondAssignDefault));
-  CU_TRY(vx::launch_cert_compact(h->d_flags, B, d_q, D, h->d_fidx, cnt2, h->d_fq, st,
-                                 (unsigned long long)hc, 1));
-  count_launch(h);
   CU_TRY(cudaStreamGetCaptureInfo(st, &cap, nullptr, &g, &deps, &ndeps));
   cudaGraphNodeParams cp = {};
   cp.type = cudaGraphNodeTypeConditional;
@@ -623,6 +644,83 @@ vx_status run_part(vx_index* h, int part, int B, int nq, int k, cudaStream_t st)
   return VX_OK;
 }
 
+static void stage_done(vx_index* h, int B);
+
+// One GPU, graphs on: the whole stage (top-k [+ MaxSim and order]) as ONE graph captured
+// against the caller's buffers (vx_index::io_graphs).  *done = false: not taken (sharded,
+// graphs off, first sighting of these buffers, or the per-shape budget spent) — the caller
+// runs the two-part path with its copies.
+vx_status stage_direct(vx_index* h, int op, const float* d_q, const float* d_qtok, int B, int nq,
+                       int k, int64_t* d_ids, float* d_ip, float* d_ms, cudaStream_t st,
+                       bool* done) {
+  *done = false;
+  if (!h->use_graphs || h->nranks > 1) return VX_OK;
+  // d_out_ids / d_out_ms are the certificate chain's level-3 scratch: never the direct outputs
+  if ((void*)d_ids == (void*)h->d_out_ids || (void*)d_ip == (void*)h->d_out_ms ||
+      (void*)d_ms == (void*)h->d_out_ms)
+    return VX_OK;
+  const bool rescore = op == OP_RESCORE;
+  vx_index::IoKey key{part_key(rescore ? 4 : 3, B, nq, k),
+                      {(uintptr_t)d_q, (uintptr_t)d_qtok, (uintptr_t)d_ids, (uintptr_t)d_ip,
+                       (uintptr_t)d_ms}};
+  auto it = h->io_graphs.find(key);
+  if (it == h->io_graphs.end()) {
+    int& per = h->io_per_shape[key.shape];
+    if (per >= vx_index::kIoGraphsPerShape) return VX_OK;
+    int& seen = h->io_seen[key];
+    if (seen++ == 0) {
+      if (h->io_seen.size() > 64) h->io_seen.clear();  // bounded: one-off buffers
+      return VX_OK;
+    }
+    // capture (the eager run of this shape already happened on the first sighting)
+    CU_TRY(cudaStreamSynchronize(st));
+    CU_TRY(cudaStreamSynchronize(h->stream));
+    const uint64_t before = h->st.kernel_launches;
+    h->tev = h->gev;
+    CU_TRY(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    vx_status s = VX_OK;
+    {
+      cudaStream_t cs = h->stream;
+      s = record_ev(h, h->tev[2], cs) == cudaSuccess ? VX_OK : fail(VX_ERR_CUDA, "event");
+      if (s == VX_OK) {
+        if (rescore) {
+          s = core_topk(h, d_q, B, k, cs);
+          if (s == VX_OK) s = core_rescore(h, d_qtok, B, nq, k, d_ids, d_ip, d_ms, cs);
+        } else {
+          s = local_topk(h, d_q, B, k, h->d_keys, d_ids, d_ip, cs);
+        }
+      }
+      if (s == VX_OK && record_ev(h, h->tev[3], cs) != cudaSuccess) s = fail(VX_ERR_CUDA, "event");
+    }
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+    h->tev = h->ev;
+    const int launches = (int)(h->st.kernel_launches - before);
+    h->st.kernel_launches = before;
+    if (s != VX_OK) {
+      if (g) cudaGraphDestroy(g);
+      return s;
+    }
+    if (e != cudaSuccess) return fail(VX_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
+    cudaGraphExec_t ex = nullptr;
+    e = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(VX_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
+    it = h->io_graphs.emplace(key, vx_index::GraphEntry{ex, launches}).first;
+    h->io_seen.erase(key);
+    ++per;
+  }
+  // the capture stream and the caller's stream: the replay runs on the caller's
+  CU_TRY(cudaGraphLaunch(it->second.exec, st));
+  h->st.kernel_launches += it->second.launches;
+  h->st.graph_replays += 1;
+  h->ev_start = h->ev_end = h->gev;
+  h->stream_last = st;
+  stage_done(h, B);
+  *done = true;
+  return VX_OK;
+}
+
 // Rank 0 entry, part 1: announce the batch to the shards (header), then broadcast + top-k.
 vx_status stage_begin(vx_index* h, int op, const float* d_q, int B, int nq, int k,
                       cudaStream_t st) {
@@ -706,6 +804,9 @@ extern "C" vx_status vx_search_dev(vx_index* h, const float* d_q, int32_t B, int
   VX_TRY(check_batch(h, B, k));
   CU_TRY(cudaSetDevice(h->device));
   cudaStream_t st = pick_stream(h, stream);
+  bool done = false;
+  VX_TRY(stage_direct(h, OP_SEARCH, d_q, nullptr, B, 0, k, d_ids, d_scores, nullptr, st, &done));
+  if (done) return VX_OK;
   VX_TRY(stage_begin(h, OP_SEARCH, d_q, B, 0, k, st));
   return stage_search_out(h, B, k, d_ids, d_scores, st);
 }
@@ -719,6 +820,9 @@ extern "C" vx_status vx_search_rescore_dev(vx_index* h, const float* d_q, const 
   if (nq < 1 || nq > h->desc.max_qtok) return fail(VX_ERR_INVALID, "nq %d", nq);
   CU_TRY(cudaSetDevice(h->device));
   cudaStream_t st = pick_stream(h, stream);
+  bool done = false;
+  VX_TRY(stage_direct(h, OP_RESCORE, d_q, d_qtok, B, nq, k, d_ids, d_ip, d_ms, st, &done));
+  if (done) return VX_OK;
   VX_TRY(stage_begin(h, OP_RESCORE, d_q, B, nq, k, st));
   return stage_finish(h, d_qtok, B, nq, k, d_ids, d_ip, d_ms, st);
 }

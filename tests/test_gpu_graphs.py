@@ -97,3 +97,46 @@ def test_prepare_precaptures_every_batch_size(vx, oracle):
             idx.search_rescore(Q, synth.query_tokens(B, nq, 64, seed=50 + B), k)
         st = idx.stats()
     assert st["graph_replays"] == 3 + 2 * 3 and st["batches"] == 6  # search 1 graph, stage 2
+
+
+def test_direct_io_graphs_replay_against_caller_buffers(vx):
+    """Single GPU, graphs on: from the second call with the same device buffers the whole stage
+    is ONE graph captured against those buffers (no copies in or out); other buffers keep
+    working and every result equals the eager path's."""
+    import torch
+    from paper_2511_02062_b200 import synth
+    N, D, k, B, nq = 40_000, 768, 10, 8, 32
+    with vx.Index(N, D, tok_per_doc=128, tok_dim=128, tok_blocks=300, max_batch=B, max_k=k,
+                  max_qtok=nq) as idx:
+        idx.synth(42)
+        idx.tokens_synth(45)
+        Q = synth.rows(43, 0, B, D)
+        qt = synth.query_tokens(B, nq, 128, seed=44)
+        ref_ids, ref_sc = idx.search(Q, k)
+        r_ids, r_ip, r_ms = idx.search_rescore(Q, qt, k)
+        idx.set_option(vx.VX_OPT_GRAPHS, 1)
+        q = torch.from_numpy(Q).cuda()
+        qtd = torch.from_numpy(qt).cuda()
+        s = torch.cuda.Stream()
+        bufs = [(torch.empty((B, k), dtype=torch.int64, device="cuda"),
+                 torch.empty((B, k), dtype=torch.float32, device="cuda"),
+                 torch.empty((B, k), dtype=torch.float32, device="cuda")) for _ in range(2)]
+        idx.reset_stats()
+        for rep in range(4):
+            for ids, sc, ms in bufs:
+                ids.zero_(), sc.zero_(), ms.zero_()
+                idx.search_dev(q, ids, sc, k, stream=s.cuda_stream)
+                s.synchronize()
+                assert np.array_equal(ids.cpu().numpy(), ref_ids)
+                assert np.array_equal(sc.cpu().numpy(), ref_sc)
+                ids.zero_(), sc.zero_(), ms.zero_()
+                idx.search_rescore_dev(q, qtd, ids, sc, ms, k, stream=s.cuda_stream)
+                s.synchronize()
+                assert np.array_equal(ids.cpu().numpy(), r_ids)
+                assert np.array_equal(sc.cpu().numpy(), r_ip)
+                assert np.array_equal(ms.cpu().numpy(), r_ms)
+        st = idx.stats()
+    # per (op, buffers): call 1 eager + capture of the two-part graphs (or replay), call 2
+    # captures the direct graph and replays it, calls 3-4 replay it
+    assert st["batches"] == 16
+    assert st["graph_replays"] >= 12
