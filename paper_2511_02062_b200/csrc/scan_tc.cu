@@ -67,6 +67,8 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
   const int ntiles = (int)((n_local + TD - 1) / TD);
   uint64_t kt_c0 = 0, kt_g0 = 0;
   ktimer_begin(a.ktimer, kt_c0, kt_g0);
+  uint64_t* trc = a.trace ? a.trace + (size_t)blockIdx.x * 16 : nullptr;
+  if (trc && threadIdx.x == 0) trc[0] = gtimer_ns();
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tq);
@@ -86,6 +88,7 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (trc && threadIdx.x == 0) trc[1] = gtimer_ns();
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
@@ -137,12 +140,15 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
     uint32_t ph = 0;
     int buf = 0;
     uint32_t bph = 0;
+    bool first = true;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       mbar_wait(&tempty[buf], bph ^ 1);
       tc_fence_after();
       for (int c = 0; c < nch; ++c) {
         mbar_wait(&full[s], ph);
         tc_fence_after();
+        if (trc && first && lane == 0) trc[2] = gtimer_ns();
+        first = false;
         __syncwarp();
         if (elect_one()) {
           const uint64_t ds = d0 + (uint64_t)(s * (C::kStageBytes >> 4));  // start addr >> 4
@@ -170,6 +176,7 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
         bph ^= 1;
       }
     }
+    if (trc && lane == 0) trc[3] = gtimer_ns();
   } else {
     // ------------------------------------------------ epilogue: thread = query
     const int e = warp - 2;
@@ -202,6 +209,7 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       mbar_wait(&tfull[buf], bph);
       tc_fence_after();
+      if (trc && warp == 2 && lane == 0) trc[7] = gtimer_ns();  // last tile's accumulator ready
       if (rep > 1) {
         const int q = qrow;
         const uint32_t colq = tmem_base + (uint32_t)(buf * TD) + ((uint32_t)(quad * 32) << 16);
@@ -268,37 +276,54 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
         bph ^= 1;
       }
     }
+    if (trc && warp == 2 && lane == 0) trc[4] = gtimer_ns();
+    if (trc && warp >= 3 && lane == 0) trc[10 + warp] = gtimer_ns();  // [13..15]
     if (rep > 1) {
       // merge each query's rep replica lists into ONE per-CTA list: its KC-th key is >= every
       // replica's KC-th key, so "every document of this CTA outside the list has key <= the
       // list's last key" still holds (certificate 1).  Buffer: the operand ring, idle now
       // (the last tile's MMAs completed before its tfull arrive).
-      uint64_t* mb = reinterpret_cast<uint64_t*>(smem);  // [128][KC]
+      // rows padded to KC + 1 keys (the 16 merging lanes read distinct banks); the heads of the
+      // rep lists stay in registers and only the consumed list's next key is loaded per step
+      // (the per-step reload of all rep heads, bank-conflicted, took ~7 us at the end of a
+      // one-tile scan — VX_DEBUG_SCAN_TRACE)
+      constexpr int MS = KC + 1;
+      uint64_t* mb = reinterpret_cast<uint64_t*>(smem);  // [128][KC + 1]
 #pragma unroll
-      for (int j = 0; j < KC; ++j) mb[m * KC + j] = L[0][j];
+      for (int j = 0; j < KC; ++j) mb[m * MS + j] = L[0][j];
+      mb[m * MS + KC] = 0ull;  // sentinel past each list's end
+      if (trc && threadIdx.x == 128) trc[8] = gtimer_ns();
       named_bar_sync(1, 128);
+      if (trc && threadIdx.x == 128) trc[9] = gtimer_ns();
       if (m < a.a_rows && m < a.B) {
         int pos[8];
+        uint64_t head[8];
 #pragma unroll
-        for (int r = 0; r < 8; ++r) pos[r] = 0;
+        for (int r = 0; r < 8; ++r) {
+          pos[r] = 0;
+          head[r] = r < rep ? mb[(r * a.a_rows + m) * MS] : 0ull;
+        }
         uint64_t* out = a.part + ((size_t)m * gridDim.x + blockIdx.x) * KC;
+#pragma unroll 1
         for (int j = 0; j < KC; ++j) {
-          uint64_t best = 0ull;
+          uint64_t best = head[0];
           int br = 0;
 #pragma unroll
-          for (int r = 0; r < 8; ++r) {
-            if (r >= rep || pos[r] >= KC) continue;
-            const uint64_t k_ = mb[(r * a.a_rows + m) * KC + pos[r]];
-            if (k_ > best) {
-              best = k_;
+          for (int r = 1; r < 8; ++r) {
+            if (head[r] > best) {
+              best = head[r];
               br = r;
             }
           }
+          out[j] = best;
 #pragma unroll
           for (int r = 0; r < 8; ++r)
-            if (r == br && best != 0ull) ++pos[r];
-          out[j] = best;
+            if (r == br) {
+              pos[r] = min(pos[r] + 1, KC);
+              head[r] = mb[(r * a.a_rows + m) * MS + pos[r]];
+            }
         }
+        if (trc && threadIdx.x == 128) trc[10] = gtimer_ns();
       }
     } else {
 #pragma unroll
@@ -313,8 +338,12 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
     }
     }
   }
+  if (trc && threadIdx.x == 128) trc[11] = gtimer_ns();
   tc_fence_before();
+  if (trc && threadIdx.x == 128) trc[12] = gtimer_ns();
   __syncthreads();
+  if (trc && threadIdx.x == 0) trc[5] = gtimer_ns();
+  if (trc && threadIdx.x == 64) trc[6] = gtimer_ns();
   ktimer_end(a.ktimer, kt_c0, kt_g0);
   if (warp == 1) {
     tc_fence_after();

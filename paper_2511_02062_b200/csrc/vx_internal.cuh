@@ -62,6 +62,9 @@ struct ScanTcArgs {
   int32_t seed_ld;
   int32_t kc;        // list length per CTA (pair) and query: 0 = kc_of(fmt), or kSampleKC
   KTimer* ktimer = nullptr;
+  uint64_t* trace = nullptr;  // timing experiments only (VX_DEBUG_SCAN_TRACE): per CTA 8
+                             // %globaltimer stamps (entry, setup done, first stage landed, last
+                             // MMA issued, epilogue done, lists written)
   int32_t rep = 1;   // single-CTA kernel, TD = 256, B <= 64: each query occupies rep = 128 /
                      // a_rows rows of the A tile, replica r selects over columns
                      // [r TD/rep, (r+1) TD/rep) — rep x the epilogue lanes on a small batch

@@ -54,6 +54,38 @@ VX_DEV void list_insert(uint64_t (&L)[KC], uint64_t key) {
   L[0] = c[0] ? key : L[0];
 }
 
+// Fill of an EMPTY list (the thread's first unit, no seed): every column passes the -inf
+// threshold, and inserting the 32 one by one (a 16-wide insert network each, no ILP between
+// them) cost ~7 us at the end of a one-tile scan (VX_DEBUG_SCAN_TRACE, profiles/r02).  Instead
+// sort the 32 keys with a register bitonic network (240 compare-exchanges, independent within
+// a stage) and keep the best KC.  Same list as the inserts: keys are unique (distinct ids).
+template <int FMT, int KC>
+VX_DEV void fill_sorted32(const uint32_t* r, uint32_t doc0, uint32_t n_local, uint64_t (&L)[KC]) {
+  uint64_t v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    v[i] = doc0 + i < n_local ? vx_make_key(acc_score<FMT>(r[i]), doc0 + i) : 0ull;
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int l = i ^ j;
+        if (l > i) {
+          const bool desc = (i & k) == 0;
+          const uint64_t a = v[i], b = v[l];
+          const bool sw = desc ? (a < b) : (a > b);
+          v[i] = sw ? b : a;
+          v[l] = sw ? a : b;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < KC; ++j) L[j] = j < 32 ? v[j] : 0ull;
+}
+
 // Admit W (32 or 64) consecutive accumulator columns (documents doc0 ..) of this thread's
 // query.  scratch: W words per thread, stride ss.
 template <int FMT, int KC, int W>
@@ -78,6 +110,13 @@ VX_DEV void admit(const uint32_t* r, uint32_t doc0, uint32_t n_local, uint32_t* 
   for (int g = 1; g < NG; ++g) m = O::mx(m, gm[g]);
   const T t = O::thr(thr);
   if (m < t) return;
+  if constexpr (W == 32 && KC <= 32) {
+    if (L[0] == 0ull && thr == -INFINITY) {  // empty, unseeded list: bulk fill
+      fill_sorted32<FMT, KC>(r, doc0, n_local, L);
+      if (L[KC - 1] != 0ull) thr = vx_key_score(L[KC - 1]);
+      return;
+    }
+  }
   // only the passing groups are compared and parked (warp-divergent: the warp takes this
   // path when any of its 32 queries passes, so it has to stay short)
   M mask = 0;

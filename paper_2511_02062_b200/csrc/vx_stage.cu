@@ -13,6 +13,11 @@
 //           -> order by MaxSim
 // Shard mode mirrors the reference's key->shard placement (kvs.hpp:160-175): contiguous
 // document ranges, a document's row and its token block on one GPU.
+#include <stdio.h>
+
+#include <algorithm>
+#include <vector>
+
 #include "vx_handle.cuh"
 
 // Exact path: K1 scan + merge: d_q [B][D] -> keys (global ids) / ids / scores [B][k]
@@ -270,7 +275,33 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
           }
         }
         a.ns = ns;
+        // timing experiments only: per-CTA phase stamps of the full pass, summarised on stderr
+        static const bool trace = getenv("VX_DEBUG_SCAN_TRACE") != nullptr;
+        static uint64_t* d_trace = nullptr;
+        if (trace && !sample) {
+          if (!d_trace) CU_TRY(cudaMalloc(&d_trace, (size_t)1024 * 16 * 8));
+          CU_TRY(cudaMemsetAsync(d_trace, 0, (size_t)grid * 16 * 8, st));
+          a.trace = d_trace;
+        }
         CU_TRY(vx::launch_scan_tc(QT, TD, &tq, tx, a, grid, smem, st));
+        if (trace && !sample) {
+          std::vector<uint64_t> tr((size_t)grid * 16);
+          CU_TRY(cudaStreamSynchronize(st));
+          CU_TRY(cudaMemcpy(tr.data(), d_trace, tr.size() * 8, cudaMemcpyDeviceToHost));
+          uint64_t t0 = ~0ull;
+          for (int c = 0; c < grid; ++c) t0 = std::min(t0, tr[(size_t)c * 16]);
+          const char* names[16] = {"entry", "setup", "first-stage", "last-mma", "epilogue", "end", "end(w2)", "acc-ready", "mb-written", "after-nbar", "merged", "pre-fence", "pre-sync", "epi(w3)", "epi(w4)", "epi(w5)"};
+          fprintf(stderr, "[scan trace] B=%d n=%lld grid=%d (us after the first CTA entry: min / median / max)\n",
+                  Bg, (long long)a.n_local, grid);
+          for (int f = 0; f < 16; ++f) {
+            std::vector<double> v;
+            for (int c = 0; c < grid; ++c)
+              if (tr[(size_t)c * 16 + f]) v.push_back((tr[(size_t)c * 16 + f] - t0) * 1e-3);
+            if (v.empty()) continue;
+            std::sort(v.begin(), v.end());
+            fprintf(stderr, "  %-12s %8.2f %8.2f %8.2f\n", names[f], v.front(), v[v.size() / 2], v.back());
+          }
+        }
       }
       count_launch(h);
     }
