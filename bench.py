@@ -703,12 +703,16 @@ def run_ours(args) -> None:
         "parity": parity,
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": int(st["kernel_launches"]),
-        "last_batch_device_ms": {"stage": st["last_step_ms"], "scan_part": st["last_scan_ms"],
-                                 "note": "CUDA events recorded by the stage itself (inside its graph)"},
+        "last_batch_device_ms": ({"stage": st["last_step_ms"], "scan_part": st["last_scan_ms"],
+                                  "note": "CUDA events recorded by the stage itself"}
+                                 if st["last_step_ms"] >= 0 else None),
         "cert_fallbacks": int(st["cert_fallbacks"]), "cert_level2": int(st["cert_level2"]),
         "root_phases_ms": ({"broadcast": st["phase_ms"][0], "local_stage": st["phase_ms"][1],
                             "gather_merge": st["phase_ms"][2],
-                            "rescore_phase2": st["phase_ms"][3]}
+                            "rescore_phase2": st["phase_ms"][3],
+                            "detail": dict(zip(["local_scan", "local_rerank_tau", "local_rest",
+                                                "p2_bcast", "p2_maxsim", "p2_reduce_order"],
+                                               st["phase_detail_ms"]))}
                            if sharded else None),
         "clocks": result["clocks"],
     }

@@ -73,7 +73,10 @@ enum {
                              threshold from a 1/64 row sample of the shard (shards of
                              >= 512K rows); 0: off.  Results are identical either way. */,
   VX_OPT_I8_SCALE = 10    /* s8 shadow scales: 0 (default) one per shard; 1 one per column
-                             (folded into the query) — re-quantises the shard */
+                             (folded into the query) — re-quantises the shard */,
+  VX_OPT_STAGE_EVENTS = 11 /* 1: captured stages record their begin / end CUDA events
+                             (vx_stats.last_step_ms on graph replays); 0 (default): only eager
+                             runs do — each event node costs a replay ~2 us */
 };
 /* Coarse (candidate-selecting) tensor-core scan format.  Either way every reported score is
  * recomputed exactly in fp32 and certified.  BF16 reads a bf16 shadow
@@ -136,6 +139,10 @@ typedef struct vx_stats {
   uint64_t kt_launches[4];
   double kt_ms[4];            /* summed durations */
   double kt_sm_mhz[4];        /* mean SM clock during those launches */
+  float phase_detail_ms[6];   /* sharded rank 0, last batch, finer: local scan (sample + full
+                                 passes), local re-rank incl. the tau all-gather, the rest of
+                                 the local stage, phase-2 token + winner broadcast, owner
+                                 MaxSim, max-reduce + order */
 } vx_stats;
 
 int32_t vx_abi_version(void);

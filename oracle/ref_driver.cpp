@@ -279,7 +279,8 @@ static int run_pipeline(int argc, char** argv) {
   d.max_qtok = nq;
   vx_index* h = nullptr;
   if (vx_index_create(&d, &h) != VX_OK || vx_index_synth(h, 42) != VX_OK ||
-      vx_tokens_synth(h, 45) != VX_OK || vx_set_option(h, VX_OPT_GRAPHS, 1) != VX_OK) {
+      vx_tokens_synth(h, 45) != VX_OK || vx_set_option(h, VX_OPT_GRAPHS, 1) != VX_OK ||
+      vx_set_option(h, VX_OPT_STAGE_EVENTS, 1) != VX_OK) {  // the device stage time below
     std::fprintf(stderr, "vx: %s\n", vx_last_error());
     return 3;
   }

@@ -21,6 +21,7 @@ VX_OPT_SCAN, VX_OPT_GRID, VX_OPT_GRAPHS, VX_OPT_MAXSIM = 1, 2, 3, 4
 VX_MAXSIM_AUTO, VX_MAXSIM_CC, VX_MAXSIM_TC, VX_MAXSIM_TC_BF16Q = 0, 1, 2, 3
 VX_OPT_COARSE, VX_OPT_SCAN_TILE, VX_OPT_SCAN_PAIRS, VX_OPT_KPRIME, VX_OPT_SCAN_SEED = 5, 6, 7, 8, 9
 VX_OPT_I8_SCALE = 10
+VX_OPT_STAGE_EVENTS = 11
 VX_COARSE_AUTO, VX_COARSE_TF32, VX_COARSE_BF16, VX_COARSE_I8 = 0, 1, 2, 3
 VX_FLAG_NO_BF16_SHADOW = 1
 VX_FLAG_NO_I8_SHADOW = 2
@@ -49,7 +50,8 @@ class Stats(C.Structure):
                 ("scan_ms_total", C.c_double), ("step_ms_total", C.c_double),
                 ("timed_batches", C.c_uint64), ("phase_ms", C.c_float * 4),
                 ("cert_level2", C.c_uint64), ("host_staged_bytes", C.c_uint64),
-                ("kt_launches", C.c_uint64 * 4), ("kt_ms", C.c_double * 4), ("kt_sm_mhz", C.c_double * 4)]
+                ("kt_launches", C.c_uint64 * 4), ("kt_ms", C.c_double * 4), ("kt_sm_mhz", C.c_double * 4),
+                ("phase_detail_ms", C.c_float * 6)]
 
 
 P = C.c_void_p

@@ -89,6 +89,9 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (trc && threadIdx.x == 0) trc[1] = gtimer_ns();
+  // the re-rank behind this pass may be scheduled now (it waits for our completion before
+  // reading the lists; its prologue — smem carve-out, query norms — overlaps our tail)
+  pdl_trigger();
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
@@ -457,6 +460,9 @@ __global__ void __launch_bounds__(256)
   const float sq = fmt == FMT_I8 ? qscale[b] : 1.0f;
   const float cscale = fmt == FMT_I8 ? sq * xstats[5] : 1.0f;
   query_norms(q, D, fmt, sq, qs, s_red, xstats);  // the certificate's error bound, below
+  // everything below reads the scan's output (lists, candidates, seeds, scales of the query
+  // conversion): with programmatic dependent launch this CTA may have started early
+  pdl_wait();
   if (threadIdx.x == 0) {
     s_fail = 0;
     for (int i = 0; i < (nbuf & 15); ++i) mbar_init(&s_bar[i], (uint32_t)rows_per_round);
@@ -1011,11 +1017,21 @@ cudaError_t launch_rerank(const float* docs, const float* q, int D, uint64_t* ca
   cudaError_t e = cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  rerank_kernel<<<B, 256, smem, st>>>(docs, q, D, cand, kp, part, grid, ldlists, kc, k, row0,
-                                      xstats, fmt, qscale, out_keys, out_ids, out_scores, flags, R,
-                                      DC, phase, tau, hkeys, lb, seed, seed_ld, head_all,
-                                      NB | (PF << 4), fz);
-  return cudaGetLastError();
+  static const bool no_pdl = getenv("VX_DEBUG_NO_PDL") != nullptr;  // A/B timing only
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(B);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = no_pdl ? 0 : 1;
+  return cudaLaunchKernelEx(&cfg, rerank_kernel, docs, q, D, cand, kp, part, grid, ldlists, kc,
+                            k, row0, xstats, fmt, qscale, out_keys, out_ids, out_scores, flags, R,
+                            DC, phase, tau, hkeys, lb, seed, seed_ld, head_all, NB | (PF << 4),
+                            fz);
 }
 
 // ------------------------------------------------------------------- sharded threshold tau

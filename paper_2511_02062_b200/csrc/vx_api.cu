@@ -305,6 +305,10 @@ extern "C" vx_status vx_set_option(vx_index* h, int32_t option, int64_t value) {
       if (value < 0 || value > h->num_sms) return fail(VX_ERR_INVALID, "grid %lld", (long long)value);
       h->grid = value == 0 ? h->num_sms : (int)value;
       return VX_OK;
+    case VX_OPT_STAGE_EVENTS:
+      if (value != 0 && value != 1) return fail(VX_ERR_INVALID, "stage events %lld", (long long)value);
+      h->stage_events = value == 1;
+      return VX_OK;
     case VX_OPT_KPRIME:
       if (value != 0 && (value < 16 || value > 1024 || (value & (value - 1))))
         return fail(VX_ERR_INVALID, "kprime %lld (0 or a power of two in [16, 1024])", (long long)value);
@@ -371,6 +375,7 @@ extern "C" vx_status vx_get_option(const vx_index* h, int32_t option, int64_t* v
     case VX_OPT_KPRIME: *value = h->kprime; return VX_OK;
     case VX_OPT_SCAN_SEED: *value = h->scan_seed; return VX_OK;
     case VX_OPT_I8_SCALE: *value = h->i8_per_column; return VX_OK;
+    case VX_OPT_STAGE_EVENTS: *value = h->stage_events ? 1 : 0; return VX_OK;
     case VX_OPT_COARSE: {
       const int f = coarse_fmt(h);
       *value = f == vx::FMT_I8 ? VX_COARSE_I8 : (f == vx::FMT_TF32 ? VX_COARSE_TF32 : VX_COARSE_BF16);

@@ -82,6 +82,12 @@ VX_DEV void tma_load_2d(void* smem_dst, const void* tmap, uint64_t* bar, int32_t
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
       : "memory");
 }
+// Programmatic dependent launch: a kernel launched with the PDL attribute may start while its
+// predecessor still runs; pdl_wait() blocks until the predecessor grid has completed and its
+// memory is visible (a no-op without the attribute); pdl_trigger() lets the dependent grid be
+// scheduled as soon as every CTA of this grid has issued it (or exited).
+VX_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+VX_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 // L2 prefetch of one 128-byte line (no register result, fire and forget).
 VX_DEV void prefetch_l2(const void* g) {
   asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(reinterpret_cast<uint64_t>(g)));

@@ -51,11 +51,11 @@ static vx_status local_topk_f32(vx_index* h, const float* d_q, int B, int k, uin
     a.d_count = d_count;
     a.g0 = g0;
     a.ktimer = d_count ? nullptr : h->d_ktimer + vx::KT_F32;
-    if (g0 == 0 && !d_count) CU_TRY(record_ev(h, h->tev[0], st));
+    if (g0 == 0 && !d_count) CU_TRY(record_scan_ev(h, h->tev[0], st));
     CU_TRY(vx::launch_scan_f32(bucket, &h->tmap_docs, a, grid, smem, st));
     count_launch(h);
   }
-  if (!d_count) CU_TRY(record_ev(h, h->tev[1], st));
+  if (!d_count) CU_TRY(record_scan_ev(h, h->tev[1], st));
   CU_TRY(vx::launch_merge_topk(h->d_part, B, grid * kcap, k, h->row0, keys, ids, scores, st,
                                d_count));
   count_launch(h);
@@ -156,7 +156,7 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
   const int KC = vx::kc_of(fmt);  // per-CTA list length
   if (D % (i8 ? 128 : (bf16 ? 64 : 32))) return fail(VX_ERR_UNSUPPORTED, "TC scan: D %d", D);
   if (kp > 1024) return fail(VX_ERR_UNSUPPORTED, "k' %d > 1024", kp);
-  CU_TRY(record_ev(h, h->tev[0], st));
+  CU_TRY(record_scan_ev(h, h->tev[0], st));
   if (bf16) {
     CU_TRY(vx::launch_to_bf16(d_q, h->d_q16, (int64_t)B * D, st));
     count_launch(h);
@@ -330,9 +330,10 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
     VX_TRY(merge_lists(sample_lists, vx::kSampleKC, kSeedM, h->d_seedk, kSeedLd));
   }
   VX_TRY(scan_pass(false));
+  if (h->nranks > 1 && h->rank == 0) CU_TRY(record_ext(h->pev[5], st));
   // each query's seed key (the certificate bounds what it dropped), stride kSeedLd
   const uint64_t* seed_keys = seeded ? h->d_seedk + (kSeedM - 1) : nullptr;
-  CU_TRY(record_ev(h, h->tev[1], st));
+  CU_TRY(record_scan_ev(h, h->tev[1], st));
   // Certificate failures, entirely on device (no host round trip: the stage stays
   // capturable in one CUDA graph; every launch below exits at once when its count is 0):
   //   level 2: compact the failing queries, re-rank all their list entries above the
@@ -405,6 +406,7 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
       r0 = r1;
     }
   }
+  if (sharded && h->rank == 0) CU_TRY(record_ext(h->pev[6], st));
   // wide-key scratch: the upper part of d_part (the lists use B x grid x KC <= B x grid x 32
   // of its B x grid x 256 entries; the level-3 re-scan writes d_part only after level 2)
   uint64_t* wkeys = h->d_part + (size_t)h->desc.max_batch * grid * 32;
@@ -591,8 +593,10 @@ vx_status core_rescore(vx_index* h, const float* d_qtok, int B, int nq, int k,
                             h->comm, st));
   NCCL_TRY(nccl().Broadcast(h->d_ids, h->d_ids, (size_t)n, ncclInt64, 0, h->comm, st));
   NCCL_TRY(nccl().GroupEnd());
+  if (root) CU_TRY(record_ext(h->pev[7], st));
   VX_TRY(run_maxsim(h, nullptr, B, nq, h->d_ids, k, h->d_ms, st, h->row0, h->row0 + h->n_local,
                     h->d_qtok16));
+  if (root) CU_TRY(record_ext(h->pev[8], st));
   float* ms_all = reinterpret_cast<float*>(h->d_send);  // [B][k] on rank 0
   NCCL_TRY(nccl().Reduce(h->d_ms, ms_all, (size_t)n, ncclFloat32, ncclMax, 0, h->comm, st));
   if (!root) return VX_OK;
@@ -644,13 +648,16 @@ vx_status run_part(vx_index* h, int part, int B, int nq, int k, cudaStream_t st)
     h->st.kernel_launches += it->second.launches;
     h->st.graph_replays += 1;
     used = h->gev;
+    h->step_ev_valid = it->second.events;
   } else {
     VX_TRY(part_body(h, part, B, nq, k, st));
+    h->step_ev_valid = true;
     // capture on the handle's stream after the eager run completes (capture records, it
     // does not execute; sharded, every rank captures at the same batch)
     CU_TRY(cudaStreamSynchronize(st));
     const uint64_t before = h->st.kernel_launches;
     h->tev = h->gev;  // the graph records its own (external) events
+    h->graph_events = false;
     CU_TRY(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
     vx_status s = part_body(h, part, B, nq, k, h->stream);
     cudaGraph_t g = nullptr;
@@ -667,7 +674,7 @@ vx_status run_part(vx_index* h, int part, int B, int nq, int k, cudaStream_t st)
     e = cudaGraphInstantiate(&ex, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return fail(VX_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
-    h->graphs[key] = {ex, launches};
+    h->graphs[key] = {ex, launches, h->graph_events};
     used = h->ev;  // this call's timing: the eager run
   }
   if (part == PART_TOPK) h->ev_start = used;
@@ -708,6 +715,7 @@ vx_status stage_direct(vx_index* h, int op, const float* d_q, const float* d_qto
     CU_TRY(cudaStreamSynchronize(h->stream));
     const uint64_t before = h->st.kernel_launches;
     h->tev = h->gev;
+    h->graph_events = false;
     CU_TRY(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
     vx_status s = VX_OK;
     {
@@ -737,7 +745,7 @@ vx_status stage_direct(vx_index* h, int op, const float* d_q, const float* d_qto
     e = cudaGraphInstantiate(&ex, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return fail(VX_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
-    it = h->io_graphs.emplace(key, vx_index::GraphEntry{ex, launches}).first;
+    it = h->io_graphs.emplace(key, vx_index::GraphEntry{ex, launches, h->graph_events}).first;
     h->io_seen.erase(key);
     ++per;
   }
@@ -746,6 +754,7 @@ vx_status stage_direct(vx_index* h, int op, const float* d_q, const float* d_qto
   h->st.kernel_launches += it->second.launches;
   h->st.graph_replays += 1;
   h->ev_start = h->ev_end = h->gev;
+  h->step_ev_valid = it->second.events;
   h->stream_last = st;
   stage_done(h, B);
   *done = true;
@@ -779,6 +788,7 @@ vx_status stage_begin(vx_index* h, int op, const float* d_q, int B, int nq, int 
     VX_TRY(core_topk(h, h->nranks > 1 ? h->d_q : d_q, B, k, st));
     CU_TRY(record_ev(h, h->tev[3], st));
     h->ev_start = h->ev_end = h->ev;
+    h->step_ev_valid = true;
   }
   return VX_OK;
 }
@@ -915,22 +925,36 @@ extern "C" vx_status vx_sync(vx_index* h) {
   if (h->timing_pending) {
     cudaEvent_t* E = h->ev_start;
     cudaEvent_t* F = h->ev_end;
-    CU_TRY(cudaEventSynchronize(F[3]));
+    if (h->step_ev_valid) CU_TRY(cudaEventSynchronize(F[3]));
     float a = 0, b = 0;
-    if (cudaEventElapsedTime(&a, E[0], E[1]) == cudaSuccess &&
-        cudaEventElapsedTime(&b, E[2], F[3]) == cudaSuccess) {
+    if (!h->step_ev_valid) {
+      h->st.last_step_ms = -1.0f;  // a replay without stage events (VX_OPT_STAGE_EVENTS 0)
+      h->st.last_scan_ms = -1.0f;
+    } else if (cudaEventElapsedTime(&b, E[2], F[3]) == cudaSuccess) {
+      // the scan span: events on eager runs, else the scan kernels' device timers
+      if (!(h->scan_ev_valid && cudaEventElapsedTime(&a, h->ev[0], h->ev[1]) == cudaSuccess))
+        a = -1.0f;
       h->st.last_scan_ms = a;
       h->st.last_step_ms = b;
-      h->st.scan_ms_total += a;
+      if (a >= 0) h->st.scan_ms_total += a;
       h->st.step_ms_total += b;
       h->st.timed_batches += 1;
     }
+    h->scan_ev_valid = false;
     h->timing_pending = false;
     if (h->phases_pending) {
       for (int i = 0; i < 4; ++i) {
         float ms = 0;
         if (cudaEventElapsedTime(&ms, h->pev[i], h->pev[i + 1]) == cudaSuccess)
           h->st.phase_ms[i] = ms;
+      }
+      // finer: bcast done -> scan done -> re-rank done -> local done; gather done -> phase-2
+      // bcast done -> MaxSim done -> end
+      const int from[6] = {1, 5, 6, 3, 7, 8}, to[6] = {5, 6, 2, 7, 8, 4};
+      for (int i = 0; i < 6; ++i) {
+        float ms = -1.0f;
+        if (cudaEventElapsedTime(&ms, h->pev[from[i]], h->pev[to[i]]) != cudaSuccess) ms = -1.0f;
+        h->st.phase_detail_ms[i] = ms;
       }
       h->phases_pending = false;
     }
