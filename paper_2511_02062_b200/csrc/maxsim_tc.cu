@@ -258,17 +258,24 @@ static cudaError_t launch_ms(const CUtensorMap* tt, const MaxSimArgs& a, cudaStr
   // slots / B chunks so the grid is ONE full wave (B = 64, C = 100: 4 x 25 -> 256 CTAs; a
   // ceil(B*C / slots) chunk gave 320 CTAs = 1.08 waves and a 40 % tail).  Otherwise chunks
   // of ~B*C / slots candidates (2..64, at least 2 for the pipeline).
+  // Sharded (own_frac = 1/G): chunks are sized by the candidates this shard OWNS, so a CTA
+  // still streams ~the same number of blocks and the grid shrinks G-fold (each CTA pays its
+  // A-tile build, barrier and TMEM setup once: 2048 CTAs for ~16 owned candidates each at
+  // G = 4 spent that setup on 1/4 of the work).
   const int slots = 2 * 148;
+  const float of = a.own_frac > 0.f && a.own_frac < 1.f ? a.own_frac : 1.f;
   int chunk;
   if (a.B < slots) {
     const int cpq0 = slots / a.B;
     chunk = (a.C + cpq0 - 1) / cpq0;
   } else {
-    const long pairs = (long)a.B * a.C;
+    const long pairs = (long)((double)a.B * a.C * of + 0.5);
     chunk = (int)((pairs + slots - 1) / slots);
     chunk = chunk > 64 ? 64 : chunk;
+    chunk = (int)(chunk / of);  // positions per CTA for `chunk` owned candidates
   }
   chunk = chunk < 2 ? 2 : chunk;
+  chunk = chunk > a.C ? a.C : chunk;
   const int cpq = (a.C + chunk - 1) / chunk;
   kfn<<<a.B * cpq, kMsThreads, C::kSmem, st>>>(*tt, a, chunk, cpq);
   return cudaGetLastError();

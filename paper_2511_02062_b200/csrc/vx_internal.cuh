@@ -209,6 +209,8 @@ struct MaxSimArgs {
   int32_t B, nq, C, Nd, d;
   float* out;            // [B][C]
   int64_t id_lo = 0, id_hi = INT64_MAX;  // ids outside [lo, hi) (another shard's) -> -INF, no loads
+  float own_frac = 1.0f;  // expected fraction of candidates inside [lo, hi) (the launch sizes
+                          // its candidate chunks by the OWNED work: 1 / G when sharded)
   KTimer* ktimer = nullptr;
 };
 cudaError_t launch_maxsim(const MaxSimArgs& a, cudaStream_t st);

@@ -494,6 +494,8 @@ vx_status run_maxsim(vx_index* h, const float* d_qtok, int B, int nq, const int6
   a.out = d_out;
   a.id_lo = id_lo;
   a.id_hi = id_hi;
+  if (h->nranks > 1 && id_hi - id_lo < h->desc.n_docs)
+    a.own_frac = (float)((double)(id_hi - id_lo) / (double)h->desc.n_docs);
   a.ktimer = h->d_ktimer + vx::KT_MAXSIM;
   const bool tc = h->maxsim_algo != VX_MAXSIM_CC &&
                   vx::maxsim_tc_supported(nq, a.Nd, a.d);
