@@ -69,10 +69,19 @@ static vx_status local_topk_f32(vx_index* h, const float* d_q, int B, int k, uin
 // ~0.03% (profiles/cert_rate.py, profiles/r01/cert_rate.jsonl).
 // The s8 pass's error bound is ~4x the bf16 one (residual norms of 7-bit integers vs 8-bit
 // mantissas), so its candidate set is 8 next_pow2(k) in [128, 1024] with 32-entry lists.
+// Sharded (G shards, the tau exchange on): what a shard must certify is its share of the
+// candidates that can reach the GLOBAL top-k — certificate 2 holds when the shard's k'-th
+// coarse key + E is below tau, and a shard's (k'/G)-th best coarse key sits at the same
+// quantile of its N/G rows as the k'-th of the whole index.  So a shard takes k'/G (not below
+// 2 next_pow2(k): the head re-scores k rows): s8 k = 100 -> 512 at G = 2, 256 at G >= 4 — the
+// fused merge, the exact-key sort and the list certificate shrink with it (the level-2 and
+// level-3 fallbacks still catch a query whose shard was unusually dense).
 static int kprime_of(const vx_index* h, int k, int fmt) {
   if (h->kprime) return std::max(h->kprime, next_pow2(k));
-  if (fmt == vx::FMT_I8) return std::min(1024, std::max(128, 8 * next_pow2(k)));
-  return std::min(256, std::max(64, 4 * next_pow2(k)));
+  int kp = fmt == vx::FMT_I8 ? std::min(1024, std::max(128, 8 * next_pow2(k)))
+                             : std::min(256, std::max(64, 4 * next_pow2(k)));
+  if (h->nranks > 1) kp = std::max(std::min(kp, 2 * next_pow2(k)), kp / next_pow2(h->nranks));
+  return kp;
 }
 
 // coarse operand format of the tensor-core pass for this handle

@@ -55,6 +55,12 @@ def main() -> int:
         ids_l, ip_l, ms_l = idx.search_rescore(QL, qtl, k)
         ids_l2, ip_l2, ms_l2 = idx.search_rescore(QL, qtl, k)  # deterministic across batches
         ok &= np.array_equal(ids_l, ids_l2) and np.array_equal(ms_l, ms_l2)
+        # the s8 coarse pass on rank 0's shard (the headline's format; AUTO picks bf16 for these
+        # short shards; options are per handle, so the other shards stay bf16 — a mixed stage
+        # must be exact too): the per-shard candidate set k'/G and the tau-pruned tail
+        idx.set_option(vx.VX_OPT_COARSE, vx.VX_COARSE_I8)
+        ids_8, ip_8, ms_8 = idx.search_rescore(QL, qtl, k)
+        idx.set_option(vx.VX_OPT_COARSE, vx.VX_COARSE_AUTO)
         idx.set_option(vx.VX_OPT_SCAN, vx.VX_SCAN_F32)
         ids_f, sc_f = idx.search(Q[:3], 10)
         idx.shard_stop()
@@ -65,7 +71,8 @@ def main() -> int:
         ok &= np.array_equal(ids_f, rid[:3])
         table = o.synth_tokens(45, 0, T, 128, 128)
         try:
-            for q_, t_, out in ((Q, qt, (ids, ip, ms)), (QL, qtl, (ids_l, ip_l, ms_l))):
+            for q_, t_, out in ((Q, qt, (ids, ip, ms)), (QL, qtl, (ids_l, ip_l, ms_l)),
+                                (QL, qtl, (ids_8, ip_8, ms_8))):
                 tid, tsc = o.flat_topk(X, q_, k, mode=1)
                 tms = o.maxsim(t_, tid, table, mode=o.F64_Q32)
                 r = check_stage(*out, tid, tsc, tms)
