@@ -446,6 +446,8 @@ __global__ void __launch_bounds__(256)
                   int dchunk, int phase, const float* __restrict__ tau, uint64_t* __restrict__ hkeys,
                   float* __restrict__ lb, const uint64_t* __restrict__ seed, int seed_ld,
                   int head_all, int nbuf, const RerankFuse fz) {
+  uint64_t* trc = fz.trace ? fz.trace + (size_t)blockIdx.x * 8 : nullptr;
+  if (trc && threadIdx.x == 0) trc[0] = gtimer_ns();
   extern __shared__ __align__(16) float rsm[];
   float* qs = rsm;                                             // [D]
   uint64_t* keys = reinterpret_cast<uint64_t*>(rsm + ((D + 3) & ~3));  // [kp]
@@ -462,7 +464,9 @@ __global__ void __launch_bounds__(256)
   query_norms(q, D, fmt, sq, qs, s_red, xstats);  // the certificate's error bound, below
   // everything below reads the scan's output (lists, candidates, seeds, scales of the query
   // conversion): with programmatic dependent launch this CTA may have started early
+  if (trc && threadIdx.x == 0) trc[1] = gtimer_ns();
   pdl_wait();
+  if (trc && threadIdx.x == 0) trc[2] = gtimer_ns();
   if (threadIdx.x == 0) {
     s_fail = 0;
     for (int i = 0; i < (nbuf & 15); ++i) mbar_init(&s_bar[i], (uint32_t)rows_per_round);
@@ -477,6 +481,7 @@ __global__ void __launch_bounds__(256)
     merge_topk_block(fz.mlists + (size_t)b * fz.mld, fz.mM, kp, 0, cand + (size_t)b * kp, nullptr,
                      nullptr, 0, kp, staged, staged + ((fz.mM + 1) & ~1));
   }
+  if (trc && threadIdx.x == 0) trc[3] = gtimer_ns();
   const uint64_t* cb = cand + (size_t)b * kp;
   const uint64_t tprime = cb[kp - 1];  // coarse k'-th key (0: fewer than k' candidates)
   // head rows; head_all (small batch, latency-bound: the pruning saves bytes nobody waits
@@ -587,6 +592,7 @@ __global__ void __launch_bounds__(256)
     }
     return;
   }
+  if (trc && threadIdx.x == 0) trc[4] = gtimer_ns();
   // L = the head's minimum exact score (a bound on the exact k-th once k heads exist)
   float m = INFINITY;
   for (int i = threadIdx.x; i < kh; i += blockDim.x)
@@ -612,6 +618,7 @@ __global__ void __launch_bounds__(256)
   }
   for (int i = kpe + threadIdx.x; i < kp; i += blockDim.x) keys[i] = 0ull;
   rescore(kh, kpe);
+  if (trc && threadIdx.x == 0) trc[5] = gtimer_ns();
   // certificate 1: no CTA that truncated its list (KC kept) had its last key inside the
   // top-k' (sharded: a truncated list whose dropped keys are all bounded below tau is harmless)
   for (int t = threadIdx.x; t < grid; t += blockDim.x) {
@@ -623,6 +630,7 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   // sort the exact keys (kp is a power of two <= 1024; registers + shuffles, vx_sort.cuh)
   block_sort_desc(keys, kp);
+  if (trc && threadIdx.x == 0) trc[6] = gtimer_ns();
   // seeded scan (ScanTcArgs::seed): the lists also dropped every document whose coarse score
   // is below the seed, so a document outside the candidates has coarse score
   // <= max(s(T'), seed)
@@ -659,6 +667,7 @@ __global__ void __launch_bounds__(256)
     }
   }
   if (threadIdx.x == 0) flags[b] = s_fail;
+  if (trc && threadIdx.x == 0) trc[7] = gtimer_ns();
   if (fz.ctr) {  // fused compaction: the last CTA of the launch takes the whole batch
     __shared__ int s_last;
     if (threadIdx.x == 0) {

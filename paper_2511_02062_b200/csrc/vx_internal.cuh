@@ -143,6 +143,9 @@ struct RerankFuse {
   float* fq = nullptr;
   unsigned long long cond = 0;
   int use_cond = 0;
+  uint64_t* trace = nullptr;  // timing experiments only (VX_DEBUG_RERANK_TRACE): per CTA 8
+                              // %globaltimer stamps (entry, norms, dependency, merge, head,
+                              // tail, sort, end)
 };
 cudaError_t launch_rerank(const float* docs, const float* q, int D, uint64_t* cand, int B,
                           int kp, const uint64_t* part, int grid, int ldlists, int kc, int k,

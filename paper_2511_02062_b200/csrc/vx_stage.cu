@@ -401,6 +401,13 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
         fz.cond = (unsigned long long)hc;
         fz.use_cond = captured ? 1 : 0;
       }
+      static const bool rtrace = getenv("VX_DEBUG_RERANK_TRACE") != nullptr;
+      static uint64_t* d_rtrace = nullptr;
+      if (rtrace) {
+        if (!d_rtrace) CU_TRY(cudaMalloc(&d_rtrace, (size_t)8192 * 8 * 8));
+        CU_TRY(cudaMemsetAsync(d_rtrace, 0, (size_t)(r1 - r0) * 8 * 8, st));
+        fz.trace = d_rtrace;
+      }
       CU_TRY(vx::launch_rerank(h->docs, d_q + (size_t)r0 * D, D, h->d_ckeys + (size_t)r0 * kp,
                                r1 - r0, kp, h->d_part + (size_t)r0 * ldp, P, grid, KC, k,
                                h->row0, reinterpret_cast<const float*>(h->d_xnorm), fmt,
@@ -412,6 +419,30 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
                                seed_keys ? seed_keys + (size_t)r0 * kSeedLd : nullptr, kSeedLd,
                                fz));
       count_launch(h);
+      if (rtrace) {  // per-CTA phase spans (us): median / max over the launch's CTAs
+        std::vector<uint64_t> tr((size_t)(r1 - r0) * 8);
+        CU_TRY(cudaStreamSynchronize(st));
+        CU_TRY(cudaMemcpy(tr.data(), d_rtrace, tr.size() * 8, cudaMemcpyDeviceToHost));
+        const char* names[7] = {"norms", "dependency", "merge", "head", "tail", "sort", "cert+out"};
+        uint64_t t0 = ~0ull, t1 = 0;
+        for (int c = 0; c < r1 - r0; ++c) {
+          t0 = std::min(t0, tr[(size_t)c * 8]);
+          t1 = std::max(t1, tr[(size_t)c * 8 + 7]);
+        }
+        fprintf(stderr, "[rerank trace] pass %d B=%d kp=%d: launch span %.1f us; per CTA (median / max):",
+                pass, r1 - r0, kp, (t1 - t0) * 1e-3);
+        for (int f = 0; f < 7; ++f) {
+          std::vector<double> v;
+          for (int c = 0; c < r1 - r0; ++c) {
+            const uint64_t a0 = tr[(size_t)c * 8 + f], a1 = tr[(size_t)c * 8 + f + 1];
+            if (a0 && a1 && a1 >= a0) v.push_back((a1 - a0) * 1e-3);
+          }
+          if (v.empty()) continue;
+          std::sort(v.begin(), v.end());
+          fprintf(stderr, " %s %.2f/%.2f", names[f], v[v.size() / 2], v.back());
+        }
+        fprintf(stderr, "\n");
+      }
       r0 = r1;
     }
   }
