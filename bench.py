@@ -703,6 +703,15 @@ def run_ours(args) -> None:
         "parity": parity,
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": int(st["kernel_launches"]),
+        # device-side kernel timers over the timed steps (first CTA start -> last CTA end per
+        # launch) and the last step's kernel timeline: what the stage spends between kernels
+        "kernel_ms_per_step": {
+            "scan": st["kt_ms"][0] / args.steps, "sample": st["kt_ms"][1] / args.steps,
+            "exact_scan": st["kt_ms"][2] / args.steps, "maxsim": st["kt_ms"][3] / args.steps,
+            "rerank": st["kt_rerank_ms"] / args.steps},
+        "last_step_timeline_us": {n: [round(st["kt_last_us"][2 * i], 2), round(st["kt_last_us"][2 * i + 1], 2)]
+                                  for i, n in enumerate(["scan", "sample", "exact_scan", "maxsim", "rerank"])
+                                  if st["kt_last_us"][2 * i + 1] > 0},
         "last_batch_device_ms": ({"stage": st["last_step_ms"], "scan_part": st["last_scan_ms"],
                                   "note": "CUDA events recorded by the stage itself"}
                                  if st["last_step_ms"] >= 0 else None),

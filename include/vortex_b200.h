@@ -143,6 +143,11 @@ typedef struct vx_stats {
                                  passes), local re-rank incl. the tau all-gather, the rest of
                                  the local stage, phase-2 token + winner broadcast, owner
                                  MaxSim, max-reduce + order */
+  uint64_t kt_rerank_launches; /* device-side timing of the exact re-rank launches (as kt_*) */
+  double kt_rerank_ms;
+  double kt_last_us[10];       /* [scan, sample, f32, maxsim, re-rank] x [start, end] of each
+                                  kind's LAST launch, us after the earliest of those starts
+                                  (both 0: no launch) — the gaps between a stage's kernels */
 } vx_stats;
 
 int32_t vx_abi_version(void);

@@ -30,6 +30,8 @@ namespace vx {
 
 constexpr int kTcStageUnit = 16384;   // one 128-row x 128-byte operand tile
 constexpr int kRerankMaxBufs = 4;      // re-rank: chunk buffers in the staging stream
+constexpr int kRerankMergeSel = 1024;   // fused merge: selection buffer (k' <= 1024)
+constexpr int kRerankMergeFilter = 1024;  // fused merge: sorted-list filter buffer
 
 // QT: 128-query tiles per launch (A operands); TD: documents per tile (MMA N, 128 or 256).
 // A bigger TD re-streams the query tiles from L2 half as often per document byte.
@@ -448,6 +450,8 @@ __global__ void __launch_bounds__(256)
                   int head_all, int nbuf, const RerankFuse fz) {
   uint64_t* trc = fz.trace ? fz.trace + (size_t)blockIdx.x * 8 : nullptr;
   if (trc && threadIdx.x == 0) trc[0] = gtimer_ns();
+  uint64_t kt_c0 = 0, kt_g0 = 0;
+  ktimer_begin(fz.ktimer, kt_c0, kt_g0);
   extern __shared__ __align__(16) float rsm[];
   float* qs = rsm;                                             // [D]
   uint64_t* keys = reinterpret_cast<uint64_t*>(rsm + ((D + 3) & ~3));  // [kp]
@@ -478,8 +482,10 @@ __global__ void __launch_bounds__(256)
   const float E = cert_err_bound(fmt, D, qn, qh, qr, xstats);
   if (fz.mlists) {  // fused K3: this query's lists -> its coarse top-k' (staged in rowbuf)
     uint64_t* staged = reinterpret_cast<uint64_t*>(rowbuf);
+    uint64_t* msel = staged + ((fz.mM + 1) & ~1);
     merge_topk_block(fz.mlists + (size_t)b * fz.mld, fz.mM, kp, 0, cand + (size_t)b * kp, nullptr,
-                     nullptr, 0, kp, staged, staged + ((fz.mM + 1) & ~1));
+                     nullptr, 0, kp, staged, msel, grid, kc, msel + kRerankMergeSel,
+                     kRerankMergeFilter);
   }
   if (trc && threadIdx.x == 0) trc[3] = gtimer_ns();
   const uint64_t* cb = cand + (size_t)b * kp;
@@ -628,8 +634,19 @@ __global__ void __launch_bounds__(256)
       s_fail = 1;
   }
   __syncthreads();
-  // sort the exact keys (kp is a power of two <= 1024; registers + shuffles, vx_sort.cuh)
-  block_sort_desc(keys, kp);
+  // order the exact keys: only the best k are reported and the certificate reads the k-th,
+  // so a large candidate set (kp > 128) is reduced by the merge's radix select to its top k
+  // in order (~3 passes) instead of a full bitonic sort of kp keys (8.8 us of a 1024-key
+  // re-rank CTA, VX_DEBUG_RERANK_TRACE); small sets sort in registers (vx_sort.cuh)
+  if (kp > 128 && k <= 128) {
+    uint64_t* sel = reinterpret_cast<uint64_t*>(rowbuf);  // free since the last rescore
+    uint64_t* top = sel + 128;
+    merge_topk_block(keys, kp, k, 0, top, nullptr, nullptr, 0, k, nullptr, sel);
+    for (int i = threadIdx.x; i < k; i += blockDim.x) keys[i] = top[i];
+    __syncthreads();
+  } else {
+    block_sort_desc(keys, kp);
+  }
   if (trc && threadIdx.x == 0) trc[6] = gtimer_ns();
   // seeded scan (ScanTcArgs::seed): the lists also dropped every document whose coarse score
   // is below the seed, so a document outside the candidates has coarse score
@@ -668,6 +685,8 @@ __global__ void __launch_bounds__(256)
   }
   if (threadIdx.x == 0) flags[b] = s_fail;
   if (trc && threadIdx.x == 0) trc[7] = gtimer_ns();
+  __syncthreads();
+  ktimer_end(fz.ktimer, kt_c0, kt_g0);
   if (fz.ctr) {  // fused compaction: the last CTA of the launch takes the whole batch
     __shared__ int s_last;
     if (threadIdx.x == 0) {
@@ -1022,11 +1041,15 @@ cudaError_t launch_rerank(const float* docs, const float* q, int D, uint64_t* ca
   // L2 prefetch distance in items beyond the staging window (packed into nbuf's high bits)
   const int PF = head_all ? 0 : std::min(env_pf >= 0 ? env_pf : 0, 15);
   // the fused merge stages the lists and its selection in the row buffers
-  if (fz.mlists) smem = std::max(smem, base + (size_t)(fz.mM + 2 * kp) * 8);
+  if (fz.mlists)
+    smem = std::max(smem, base + (size_t)(((fz.mM + 1) & ~1) + kRerankMergeSel + kRerankMergeFilter) * 8);
   cudaError_t e = cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  static const bool no_pdl = getenv("VX_DEBUG_NO_PDL") != nullptr;  // A/B timing only
+  // programmatic dependent launch: opt-in (VX_PDL=1).  Measured on the 100K-row B = 16 stage
+  // it made the step slower (93 vs 88 us: the early CTAs' wait + the dependency flush cost
+  // more than the launch latency they hide), and within noise on the 10M-row stage.
+  static const bool no_pdl = getenv("VX_PDL") == nullptr || getenv("VX_DEBUG_NO_PDL") != nullptr;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(B);
   cfg.blockDim = dim3(256);

@@ -41,33 +41,36 @@ __global__ void __launch_bounds__(kMergeThreads)
     merge_topk_kernel(const uint64_t* __restrict__ in, int M, int64_t ldin, int k, int64_t id_base,
                       uint64_t* __restrict__ out_keys, int64_t* __restrict__ out_ids,
                       float* __restrict__ out_scores, const int* __restrict__ d_count,
-                      int64_t ldout) {
+                      int64_t ldout, int P, int KC) {
   if (d_count && (int)blockIdx.x >= *d_count) return;  // device-sized batch (cert fallback)
-  extern __shared__ uint64_t staged[];  // [M] when launched with M * 8 bytes of dynamic smem
+  // dynamic smem: [M] staged keys, then [kMergeFilterKeys] for the sorted-list filter
+  extern __shared__ uint64_t staged[];
   __shared__ uint64_t sel[kMaxK];
+  const bool st = M <= kMergeSmemKeys && (M & 1) == 0;
   merge_topk_block(in + (size_t)blockIdx.x * ldin, M, k, id_base, out_keys, out_ids, out_scores,
-                   blockIdx.x, ldout, (M <= kMergeSmemKeys && (M & 1) == 0) ? staged : nullptr,
-                   sel);
+                   blockIdx.x, ldout, st ? staged : nullptr, sel, st ? P : 0, KC,
+                   st ? staged + M : nullptr, kMergeFilterKeys);
 }
 
 cudaError_t launch_merge_topk(const uint64_t* in, int B, int M, int k, int64_t id_base,
                               uint64_t* out_keys, int64_t* out_ids, float* out_scores,
                               cudaStream_t st, const int* d_count, int64_t ldin,
-                              int64_t ldout) {
+                              int64_t ldout, int P, int KC) {
   if (k < 1 || k > kMaxK || M < k) return cudaErrorInvalidValue;
-  const size_t smem = (M <= kMergeSmemKeys && (M & 1) == 0) ? (size_t)M * 8 : 0;
+  const size_t smem =
+      (M <= kMergeSmemKeys && (M & 1) == 0) ? (size_t)(M + kMergeFilterKeys) * 8 : 0;
   static bool attr[64] = {};  // once per device: the largest staging size
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64 || !attr[dev]) {
     cudaError_t e = cudaFuncSetAttribute(merge_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kMergeSmemKeys * 8);
+                                         (kMergeSmemKeys + kMergeFilterKeys) * 8);
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < 64) attr[dev] = true;
   }
   merge_topk_kernel<<<B, kMergeThreads, smem, st>>>(in, M, ldin > 0 ? ldin : M, k, id_base,
                                                  out_keys, out_ids, out_scores, d_count,
-                                                 ldout > 0 ? ldout : k);
+                                                 ldout > 0 ? ldout : k, P, KC);
   return cudaGetLastError();
 }
 

@@ -16,9 +16,10 @@ namespace vx {
 // also accumulates clock64() cycles over its own %globaltimer span: the SM clock the kernel
 // actually ran at.
 struct KTimer {
-  unsigned long long start, end, done, total_ns, launches, clk_cycles, clk_ns, pad;
+  unsigned long long start, end, done, total_ns, launches, clk_cycles, clk_ns, last_start,
+      last_end;  // the last launch's span (%globaltimer ns): the gaps between a stage's kernels
 };
-enum { KT_SCAN = 0, KT_SAMPLE = 1, KT_F32 = 2, KT_MAXSIM = 3, KT_N = 4 };
+enum { KT_SCAN = 0, KT_SAMPLE = 1, KT_F32 = 2, KT_MAXSIM = 3, KT_RERANK = 4, KT_N = 5 };
 
 // -------- exact fp32 scan (K1): scan_f32.cu
 struct ScanF32Args {
@@ -143,6 +144,7 @@ struct RerankFuse {
   float* fq = nullptr;
   unsigned long long cond = 0;
   int use_cond = 0;
+  KTimer* ktimer = nullptr;
   uint64_t* trace = nullptr;  // timing experiments only (VX_DEBUG_RERANK_TRACE): per CTA 8
                               // %globaltimer stamps (entry, norms, dependency, merge, head,
                               // tail, sort, end)
@@ -175,10 +177,12 @@ cudaError_t launch_row_stats(const float* docs, int64_t n, int D, unsigned int* 
 // For each query q: select the k largest keys among in[q][0..M), write them
 // descending to out_keys[q][k] (re-keyed with id + id_base), ids (-1 for empty) and scores.
 // ldin: keys between consecutive queries' candidate lists (0: M, i.e. contiguous)
+// P, KC > 0: the input is P descending lists of KC keys per query (enables the sorted-list
+// filter of vx_merge.cuh merge_topk_block)
 cudaError_t launch_merge_topk(const uint64_t* in, int B, int M, int k, int64_t id_base,
                               uint64_t* out_keys, int64_t* out_ids, float* out_scores,
                               cudaStream_t st, const int* d_count = nullptr, int64_t ldin = 0,
-                              int64_t ldout = 0);
+                              int64_t ldout = 0, int P = 0, int KC = 0);
 // Certificate failures (flags[B]) -> compacted list fidx/fcount and the flagged query rows
 // gathered into fq; after the exact re-scan, scatter its [fcount][k] results back.
 cudaError_t launch_cert_compact(const int* flags, int B, const float* q, int D, int* fidx,

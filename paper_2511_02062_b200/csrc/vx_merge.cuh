@@ -13,21 +13,50 @@
 
 namespace vx {
 
+// timing experiments only (profiles/microbench/merge_bench.cu defines VX_MERGE_TRACE): clock64
+// stamps of CTA 0's phases
+#ifdef VX_MERGE_TRACE
+__device__ unsigned long long g_merge_trace[32];
+__device__ int g_merge_trace_n;
+#define MERGE_STAMP()                                                             \
+  do {                                                                            \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && g_merge_trace_n < 32)             \
+      g_merge_trace[g_merge_trace_n++] = clock64();                               \
+  } while (0)
+#else
+#define MERGE_STAMP() \
+  do {                \
+  } while (0)
+#endif
+
 constexpr int kMergeThreads = 256;
 constexpr int kMaxK = 1024;  // merge: k' up to 1024 (the TC candidate set); order_by: k <= 256
+constexpr int kMergeFilterKeys = 512;  // standalone merge: the sorted-list filter's buffer
 
 // The merge of ONE query's lists L[0, M) to its best k keys, by the whole block (blockDim.x a
 // multiple of 32, <= 1024; every thread calls it).  staged: nullable smem for the M keys
 // (M <= kMergeSmemKeys, M even); sel: smem for next_pow2(max(k, 16)) keys.  Row `row` of the
 // outputs (stride ldout).  Also the prologue of the fused re-rank (scan_tc.cu rerank_kernel).
+//
+// Sorted lists (P > 0: L = P lists of KC keys, each descending — the per-CTA lists of the scan,
+// the shards' top-k lists): a filter first.  With S = the (j+1)-th key of every list and
+// m (j+1) >= k, the m-th largest of S, T0, has at least m (j+1) >= k keys at or above it, so
+// the k best keys are all >= T0; binary searches count each list's keys >= T0 and, when those
+// (C) fit fbuf (fcap keys, a power of two), one register sort of them gives the answer — no
+// radix passes (each pass is a chain of barriers and atomics: 2 passes + collection + sort took
+// ~17 K cycles for 2368 keys -> 64, profiles/microbench/merge_bench.cu).  Otherwise (C > fcap,
+// or T0 = 0: short lists) the radix select below runs as before.
 static __device__ __noinline__ void merge_topk_block(const uint64_t* __restrict__ L, int M, int k, int64_t id_base,
                                  uint64_t* __restrict__ out_keys, int64_t* __restrict__ out_ids,
                                  float* __restrict__ out_scores, size_t row, int64_t ldout,
-                                 uint64_t* staged, uint64_t* sel) {
+                                 uint64_t* staged, uint64_t* sel, int P = 0, int KC = 0,
+                                 uint64_t* fbuf = nullptr, int fcap = 0) {
   __shared__ uint32_t hist[256];
   __shared__ uint64_t s_prefix, s_mask;
   __shared__ int s_kk, s_done, s_above, s_eq;
+  __shared__ int s_wsum[32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  MERGE_STAMP();
   if (staged && M <= kMergeSmemKeys && (M & 1) == 0) {  // stage (16-byte loads, all in flight)
     const uint4* src = reinterpret_cast<const uint4*>(L);
     uint4* dst = reinterpret_cast<uint4*>(staged);
@@ -39,15 +68,94 @@ static __device__ __noinline__ void merge_topk_block(const uint64_t* __restrict_
     __syncthreads();
     L = staged;
   }
+  MERGE_STAMP();
+  if (P > 0 && KC > 0 && fbuf && P <= (int)blockDim.x && P <= fcap && k <= fcap &&
+      (int64_t)P * KC == M) {
+    const int j1 = (k + P - 1) / P;  // j + 1
+    if (j1 <= KC) {
+      const int m = (k + j1 - 1) / j1;  // <= P
+      int n2 = 16;
+      while (n2 < P) n2 <<= 1;
+      for (int i = threadIdx.x; i < n2; i += blockDim.x)
+        fbuf[i] = i < P ? L[(size_t)i * KC + (j1 - 1)] : 0ull;
+      __syncthreads();
+      block_sort_desc(fbuf, n2);
+      const uint64_t t0 = fbuf[m - 1];
+      __syncthreads();
+      if (t0 != 0ull) {
+        // keys >= t0 in list p (descending: a prefix), by binary search; block prefix sum
+        int c = 0;
+        if ((int)threadIdx.x < P) {
+          const uint64_t* lp = L + (size_t)threadIdx.x * KC;
+          int lo = 0, hi = KC;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (lp[mid] >= t0) lo = mid + 1;
+            else hi = mid;
+          }
+          c = lo;
+        }
+        int x = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        if (lane == 31) s_wsum[warp] = x;
+        __syncthreads();
+        int base = 0, C = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+          const int v = s_wsum[w];
+          if (w < warp) base += v;
+          C += v;
+        }
+        int n3 = 16;
+        while (n3 < C || n3 < k) n3 <<= 1;
+        if (n3 <= fcap) {
+          const int off = base + x - c;  // exclusive prefix of this list
+          if (c) {
+            const uint64_t* lp = L + (size_t)threadIdx.x * KC;
+            for (int i = 0; i < c; ++i) fbuf[off + i] = lp[i];
+          }
+          for (int i = C + (int)threadIdx.x; i < n3; i += blockDim.x) fbuf[i] = 0ull;
+          __syncthreads();
+          block_sort_desc(fbuf, n3);
+          MERGE_STAMP();
+          for (int i = threadIdx.x; i < k; i += blockDim.x) {
+            const uint64_t key = fbuf[i];
+            const size_t o = row * ldout + i;
+            if (key == 0ull) {
+              if (out_keys) out_keys[o] = 0ull;
+              if (out_ids) out_ids[o] = -1;
+              if (out_scores) out_scores[o] = -INFINITY;
+            } else {
+              const int64_t gid = (int64_t)vx_key_id(key) + id_base;
+              if (out_keys)
+                out_keys[o] = (key & 0xFFFFFFFF00000000ull) | (uint64_t)(0xFFFFFFFFu - (uint32_t)gid);
+              if (out_ids) out_ids[o] = gid;
+              if (out_scores) out_scores[o] = vx_key_score(key);
+            }
+          }
+          __syncthreads();
+          MERGE_STAMP();
+          return;
+        }
+      }
+    }
+  }
 
   // the digits every key shares need no pass: start at the first byte where the largest
   // and the smallest key differ (scores of one query's candidates share sign, exponent and
-  // often leading mantissa bits — one or two of the ~3 passes)
+  // often leading mantissa bits — one or two of the ~3 passes).  Padding keys (0: a list
+  // shorter than its slots, a pruned candidate) do not count for the smallest key — one of
+  // them zeroed the shared prefix and cost every merge all eight passes (11-15 us of a
+  // 16-query re-rank, VX_DEBUG_RERANK_TRACE); they never outrank a real key, and when fewer
+  // than k real keys exist the selection below takes them all and pads with 0.
   uint64_t kmax = 0ull, kmin = ~0ull;
   for (int i = threadIdx.x; i < M; i += blockDim.x) {
     const uint64_t v = L[i];
     kmax = v > kmax ? v : kmax;
-    kmin = v < kmin ? v : kmin;
+    kmin = (v != 0ull && v < kmin) ? v : kmin;
   }
   for (int o = 16; o > 0; o >>= 1) {
     const uint64_t a = shfl_xor_u64(kmax, o), b = shfl_xor_u64(kmin, o);
@@ -66,6 +174,8 @@ static __device__ __noinline__ void merge_topk_block(const uint64_t* __restrict_
     kmax = s_mx[w] > kmax ? s_mx[w] : kmax;
     kmin = s_mn[w] < kmin ? s_mn[w] : kmin;
   }
+  MERGE_STAMP();
+  if (kmax == 0ull) kmin = 0ull;  // no real key at all
   const int common_bytes = (kmax == kmin) ? 7 : (__clzll((long long)(kmax ^ kmin)) >> 3);
   uint64_t mask = common_bytes ? (~0ull << (64 - 8 * common_bytes)) : 0ull;
   uint64_t prefix = kmax & mask;
@@ -152,6 +262,7 @@ static __device__ __noinline__ void merge_topk_block(const uint64_t* __restrict_
     prefix = s_prefix;
     mask = s_mask;
     kk = s_kk;
+    MERGE_STAMP();
     if (s_done) break;
     __syncthreads();
   }
@@ -186,7 +297,9 @@ static __device__ __noinline__ void merge_topk_block(const uint64_t* __restrict_
     }
   }
   __syncthreads();
+  MERGE_STAMP();
   block_sort_desc(sel, kp);
+  MERGE_STAMP();
   for (int i = threadIdx.x; i < k; i += blockDim.x) {
     uint64_t key = sel[i];
     size_t o = row * ldout + i;
@@ -203,6 +316,7 @@ static __device__ __noinline__ void merge_topk_block(const uint64_t* __restrict_
     }
   }
   __syncthreads();  // sel / staged / the shared scalars are free again
+  MERGE_STAMP();
 }
 
 

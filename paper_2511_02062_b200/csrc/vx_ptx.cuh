@@ -424,6 +424,8 @@ VX_DEV void ktimer_end(KTimer* t, uint64_t c0, uint64_t g0) {
     const unsigned long long s = atomicAdd(&t->start, 0ull), e = atomicAdd(&t->end, 0ull);
     atomicAdd(&t->total_ns, e - s);
     atomicAdd(&t->launches, 1ull);
+    atomicExch(&t->last_start, s);
+    atomicExch(&t->last_end, e);
     atomicExch(&t->start, ~0ull);
     atomicExch(&t->end, 0ull);
     atomicExch(&t->done, 0ull);

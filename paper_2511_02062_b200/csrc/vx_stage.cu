@@ -328,7 +328,7 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
       r1 = std::min(r1, B);
       CU_TRY(vx::launch_merge_topk(lists + (size_t)r0 * ld, r1 - r0, P * kc, kout, 0,
                                    out + (size_t)r0 * ldout, nullptr, nullptr, st, nullptr, ld,
-                                   ldout));
+                                   ldout, P, kc));
       count_launch(h);
       r0 = r1;
     }
@@ -357,8 +357,9 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
   // Captured (CUDA graph): the compaction sets a conditional handle, and levels 2-3 are the
   // body of an IF node — a batch whose queries all pass certificate 1 (the common case)
   // replays no level-2/3 launches at all (six ~2.5 us empty launches at B = 16, 100K rows).
+  static const bool no_cond = getenv("VX_DEBUG_NO_COND") != nullptr;  // A/B timing only
   cudaGraphConditionalHandle hc = 0;
-  if (captured) {
+  if (captured && !no_cond) {
     cudaGraph_t g = nullptr;
     const cudaGraphNode_t* deps = nullptr;
     size_t ndeps = 0;
@@ -385,6 +386,7 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
       while (r1 < B && lists_per_query(r1) == P) r1 += GS;
       r1 = std::min(r1, B);
       vx::RerankFuse fz;
+      fz.ktimer = h->d_ktimer + vx::KT_RERANK;
       if (fuse_merge && pass <= 1) {
         fz.mlists = h->d_part + (size_t)r0 * ldp;
         fz.mM = P * KC;
@@ -399,7 +401,7 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
         fz.fcount = cnt2;
         fz.fq = h->d_fq;
         fz.cond = (unsigned long long)hc;
-        fz.use_cond = captured ? 1 : 0;
+        fz.use_cond = captured && !no_cond ? 1 : 0;
       }
       static const bool rtrace = getenv("VX_DEBUG_RERANK_TRACE") != nullptr;
       static uint64_t* d_rtrace = nullptr;
@@ -468,7 +470,7 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
     return VX_OK;
   };
   // eager: every launch below exits at once when its device-side count is 0
-  if (!captured) return chain(st, true);
+  if (!captured || no_cond) return chain(st, true);
   cudaGraph_t g = nullptr;
   const cudaGraphNode_t* deps = nullptr;
   size_t ndeps = 0;
@@ -601,7 +603,9 @@ vx_status core_topk(vx_index* h, const float* d_q, int B, int k, cudaStream_t st
   count_launch(h);
   CU_TRY(cudaGetLastError());
   // keys already carry global ids: id_base 0
-  CU_TRY(vx::launch_merge_topk(h->d_part, B, G * k, k, 0, h->d_keys, h->d_ids, h->d_ip, st));
+  // the shards' top-k lists are each descending: G lists of k keys
+  CU_TRY(vx::launch_merge_topk(h->d_part, B, G * k, k, 0, h->d_keys, h->d_ids, h->d_ip, st,
+                               nullptr, 0, 0, G, k));
   count_launch(h);
   CU_TRY(record_ext(h->pev[3], st));
   return VX_OK;
@@ -1008,10 +1012,20 @@ extern "C" vx_status vx_sync(vx_index* h) {
   }
   vx::KTimer kt[vx::KT_N];  // device-side launch timers (every launch since the last reset)
   CU_TRY(cudaMemcpy(kt, h->d_ktimer, sizeof kt, cudaMemcpyDeviceToHost));
-  for (int i = 0; i < vx::KT_N; ++i) {
+  for (int i = 0; i < 4; ++i) {  // the ABI's four kinds
     h->st.kt_launches[i] = kt[i].launches;
     h->st.kt_ms[i] = (double)kt[i].total_ns * 1e-6;
     h->st.kt_sm_mhz[i] = kt[i].clk_ns ? (double)kt[i].clk_cycles * 1e3 / (double)kt[i].clk_ns : 0.0;
+  }
+  h->st.kt_rerank_launches = kt[vx::KT_RERANK].launches;
+  h->st.kt_rerank_ms = (double)kt[vx::KT_RERANK].total_ns * 1e-6;
+  unsigned long long t0 = ~0ull;
+  for (int i = 0; i < vx::KT_N; ++i)
+    if (kt[i].launches && kt[i].last_start < t0) t0 = kt[i].last_start;
+  for (int i = 0; i < vx::KT_N; ++i) {
+    const bool on = kt[i].launches && t0 != ~0ull;
+    h->st.kt_last_us[2 * i] = on ? (double)(kt[i].last_start - t0) * 1e-3 : 0.0;
+    h->st.kt_last_us[2 * i + 1] = on ? (double)(kt[i].last_end - t0) * 1e-3 : 0.0;
   }
   cudaGetLastError();
   return VX_OK;

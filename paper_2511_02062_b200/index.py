@@ -82,7 +82,7 @@ class Index:
         check(self.lib.vx_get_stats(self._h, C.byref(s)))
         out = {f: getattr(s, f) for f, _ in Stats._fields_}
         out["phase_ms"] = list(s.phase_ms)
-        for f in ("kt_launches", "kt_ms", "kt_sm_mhz", "phase_detail_ms"):
+        for f in ("kt_launches", "kt_ms", "kt_sm_mhz", "phase_detail_ms", "kt_last_us"):
             out[f] = list(getattr(s, f))
         return out
 

@@ -7,6 +7,7 @@
 #include <random>
 #include <vector>
 
+#define VX_MERGE_TRACE 1
 #include "../../paper_2511_02062_b200/csrc/topk.cu"
 
 __global__ void empty_kernel() {}
@@ -14,7 +15,9 @@ __global__ void empty_kernel() {}
 int main() {
   struct Case { int B, P, KC, k; };
   const Case cases[] = {{16, 148, 16, 64}, {16, 148, 32, 1024}, {1024, 74, 32, 1024}, {16, 148, 16, 10}};
+  for (int filt = 0; filt < 2; ++filt)
   for (const Case& c : cases) {
+    const int fP = filt ? c.P : 0, fKC = filt ? c.KC : 0;  // 1: the sorted-list filter
     const int M = c.P * c.KC;
     std::vector<uint64_t> h((size_t)c.B * M);
     std::mt19937_64 rng(1);
@@ -36,14 +39,14 @@ int main() {
     cudaEvent_t a, z;
     cudaEventCreate(&a);
     cudaEventCreate(&z);
-    for (int w = 0; w < 3; ++w) vx::launch_merge_topk(din, c.B, M, c.k, 0, dout, nullptr, nullptr, 0);
+    for (int w = 0; w < 3; ++w) vx::launch_merge_topk(din, c.B, M, c.k, 0, dout, nullptr, nullptr, 0, nullptr, 0, 0, fP, fKC);
     const int it = 50;
     cudaStream_t st;
     cudaStreamCreate(&st);
     cudaGraph_t g;
     cudaGraphExec_t ge;
     cudaStreamBeginCapture(st, cudaStreamCaptureModeGlobal);
-    for (int i = 0; i < it; ++i) vx::launch_merge_topk(din, c.B, M, c.k, 0, dout, nullptr, nullptr, st);
+    for (int i = 0; i < it; ++i) vx::launch_merge_topk(din, c.B, M, c.k, 0, dout, nullptr, nullptr, st, nullptr, 0, 0, fP, fKC);
     cudaStreamEndCapture(st, &g);
     cudaGraphInstantiate(&ge, g, 0);
     cudaGraphLaunch(ge, st);
@@ -53,8 +56,32 @@ int main() {
     cudaEventSynchronize(z);
     float ms = 0;
     cudaEventElapsedTime(&ms, a, z);
-    printf("merge B=%d M=%d (P=%d x KC=%d) -> k'=%d: %.2f us/launch (%s)\n", c.B, M, c.P, c.KC, c.k,
+    {  // the outputs against a host sort of each query's keys
+      std::vector<uint64_t> got((size_t)c.B * c.k);
+      cudaMemcpy(got.data(), dout, got.size() * 8, cudaMemcpyDeviceToHost);
+      int bad = 0;
+      for (int b = 0; b < c.B; ++b) {
+        std::vector<uint64_t> all(h.begin() + (size_t)b * M, h.begin() + (size_t)(b + 1) * M);
+        std::sort(all.rbegin(), all.rend());
+        for (int j = 0; j < c.k; ++j) bad += got[(size_t)b * c.k + j] != all[j];
+      }
+      printf("%s", bad ? "MISMATCH " : "");
+    }
+    printf("merge%s B=%d M=%d (P=%d x KC=%d) -> k'=%d: %.2f us/launch (%s)\n", filt ? "[filter]" : "", c.B, M, c.P, c.KC, c.k,
            ms * 1e3 / it, cudaGetErrorString(cudaGetLastError()));
+    {  // CTA 0 phase cycles of one more launch (stamps: entry, staged, kmax, passes..., collected, sorted, end)
+      int zero = 0;
+      cudaMemcpyToSymbol(vx::g_merge_trace_n, &zero, sizeof zero);
+      vx::launch_merge_topk(din, c.B, M, c.k, 0, dout, nullptr, nullptr, 0, nullptr, 0, 0, fP, fKC);
+      cudaDeviceSynchronize();
+      unsigned long long tr[32];
+      int n = 0;
+      cudaMemcpyFromSymbol(tr, vx::g_merge_trace, sizeof tr);
+      cudaMemcpyFromSymbol(&n, vx::g_merge_trace_n, sizeof n);
+      printf("   CTA 0 phase cycles:");
+      for (int i = 1; i < n; ++i) printf(" %llu", tr[i] - tr[i - 1]);
+      printf("  (total %llu)\n", n > 1 ? tr[n - 1] - tr[0] : 0ull);
+    }
     cudaFree(din);
     cudaFree(dout);
   }
