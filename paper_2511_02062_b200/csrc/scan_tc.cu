@@ -438,7 +438,8 @@ __device__ __forceinline__ void query_norms_final(const float* red, int fmt, flo
 //   phase 0: head + tail in one launch (one shard);
 //   phase 1: head only — exact head keys to hkeys[b][k], their scores to lb[b][k];
 //   phase 2: tail, from hkeys and tau.
-__global__ void __launch_bounds__(256)
+// two CTAs per SM (the staging stream is sized for it): at most 128 registers
+__global__ void __launch_bounds__(256, 2)
     rerank_kernel(const float* __restrict__ docs, const float* __restrict__ qv, int D,
                   uint64_t* __restrict__ cand, int kp, const uint64_t* __restrict__ part,
                   int grid, int ldlists, int kc, int k, int64_t row0,
@@ -483,8 +484,11 @@ __global__ void __launch_bounds__(256)
   if (fz.mlists) {  // fused K3: this query's lists -> its coarse top-k' (staged in rowbuf)
     uint64_t* staged = reinterpret_cast<uint64_t*>(rowbuf);
     uint64_t* msel = staged + ((fz.mM + 1) & ~1);
+    // the sorted-list filter pays off when its survivors fit one register sort (k' <= 512;
+    // at k' = 1024 they never do and the filter's own sort would be wasted)
+    const bool filt = fz.filter && kp <= kRerankMergeFilter / 2;
     merge_topk_block(fz.mlists + (size_t)b * fz.mld, fz.mM, kp, 0, cand + (size_t)b * kp, nullptr,
-                     nullptr, 0, kp, staged, msel, grid, kc, msel + kRerankMergeSel,
+                     nullptr, 0, kp, staged, msel, filt ? grid : 0, kc, msel + kRerankMergeSel,
                      kRerankMergeFilter);
   }
   if (trc && threadIdx.x == 0) trc[3] = gtimer_ns();
@@ -634,19 +638,10 @@ __global__ void __launch_bounds__(256)
       s_fail = 1;
   }
   __syncthreads();
-  // order the exact keys: only the best k are reported and the certificate reads the k-th,
-  // so a large candidate set (kp > 128) is reduced by the merge's radix select to its top k
-  // in order (~3 passes) instead of a full bitonic sort of kp keys (8.8 us of a 1024-key
-  // re-rank CTA, VX_DEBUG_RERANK_TRACE); small sets sort in registers (vx_sort.cuh)
-  if (kp > 128 && k <= 128) {
-    uint64_t* sel = reinterpret_cast<uint64_t*>(rowbuf);  // free since the last rescore
-    uint64_t* top = sel + 128;
-    merge_topk_block(keys, kp, k, 0, top, nullptr, nullptr, 0, k, nullptr, sel);
-    for (int i = threadIdx.x; i < k; i += blockDim.x) keys[i] = top[i];
-    __syncthreads();
-  } else {
-    block_sort_desc(keys, kp);
-  }
+  // sort the exact keys (kp is a power of two <= 1024; registers + shuffles, vx_sort.cuh).
+  // (A radix top-k of the exact keys instead was ~2 us faster per CTA at k' = 1024 but, as a
+  // second call site of the merge, took the kernel from 80 to 173 registers: one CTA per SM.)
+  block_sort_desc(keys, kp);
   if (trc && threadIdx.x == 0) trc[6] = gtimer_ns();
   // seeded scan (ScanTcArgs::seed): the lists also dropped every document whose coarse score
   // is below the seed, so a document outside the candidates has coarse score

@@ -134,6 +134,7 @@ cudaError_t launch_scan_tc2(int H, const CUtensorMap* tq, const CUtensorMap* tx,
 struct RerankFuse {
   const uint64_t* mlists = nullptr;
   int mM = 0;
+  int filter = 1;  // the merge's sorted-list filter (VX_DEBUG_NO_MERGE_FILTER: A/B timing)
   int64_t mld = 0;
   unsigned* ctr = nullptr;
   const int* flags_all = nullptr;

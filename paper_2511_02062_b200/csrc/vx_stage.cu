@@ -387,6 +387,8 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
       r1 = std::min(r1, B);
       vx::RerankFuse fz;
       fz.ktimer = h->d_ktimer + vx::KT_RERANK;
+      static const bool no_filter = getenv("VX_DEBUG_NO_MERGE_FILTER") != nullptr;
+      fz.filter = no_filter ? 0 : 1;
       if (fuse_merge && pass <= 1) {
         fz.mlists = h->d_part + (size_t)r0 * ldp;
         fz.mM = P * KC;
