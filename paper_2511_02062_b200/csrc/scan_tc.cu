@@ -496,7 +496,8 @@ __global__ void __launch_bounds__(256, 2)
   const uint64_t tprime = cb[kp - 1];  // coarse k'-th key (0: fewer than k' candidates)
   // head rows; head_all (small batch, latency-bound: the pruning saves bytes nobody waits
   // for, and a second gather round costs its full latency) re-scores all k' in one round
-  const int kh = head_all ? kp : (k < kp ? k : kp);
+  const int kh0 = fz.head > 0 && fz.head < k ? fz.head : k;
+  const int kh = head_all ? kp : (kh0 < kp ? kh0 : kp);
   // The candidate rows are random 3 KB gathers from HBM (DRAM-page unfriendly); per-thread
   // loads left too few bytes in flight (measured 85 us at B=128).  Instead each round stages
   // R rows into smem with one TMA bulk copy per row (R x 3 KB in flight per SM), then R

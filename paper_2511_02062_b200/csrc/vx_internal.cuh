@@ -132,6 +132,8 @@ cudaError_t launch_scan_tc2(int H, const CUtensorMap* tq, const CUtensorMap* tx,
 //    compacts the certificate failures of the WHOLE batch (flags_all[0, Ball)) for levels
 //    2-3 and sets the captured stage's conditional handle (the cert_compact launch).
 struct RerankFuse {
+  int head = 0;  // sharded: head rows re-scored before the tau exchange (0: k).  G shards
+                 // contribute G x head exact scores; tau = their k-th largest needs G head >= k
   const uint64_t* mlists = nullptr;
   int mM = 0;
   int filter = 1;  // the merge's sorted-list filter (VX_DEBUG_NO_MERGE_FILTER: A/B timing)

@@ -387,6 +387,11 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
       r1 = std::min(r1, B);
       vx::RerankFuse fz;
       fz.ktimer = h->d_ktimer + vx::KT_RERANK;
+      // G > 2 shards: each re-scores 2k/G head rows before the tau exchange instead of k (the
+      // union of G x 2k/G head scores still holds k distinct exact scores, so tau stays a lower
+      // bound of the global k-th; the local bound L is dropped and tau alone prunes the tail)
+      if (sharded && h->nranks > 2)
+        fz.head = std::min(k, std::max(16, (2 * k + h->nranks - 1) / h->nranks));
       static const bool no_filter = getenv("VX_DEBUG_NO_MERGE_FILTER") != nullptr;
       fz.filter = no_filter ? 0 : 1;
       if (fuse_merge && pass <= 1) {
