@@ -75,10 +75,13 @@ cudaError_t launch_merge_topk(const uint64_t* in, int B, int M, int k, int64_t i
 }
 
 // Stage output order: MaxSim descending, then id ascending.  k <= 256, one CTA per query.
+// planes > 1 (sharded phase 2): ms holds `planes` [B][k] arrays (one per shard, -inf where the
+// shard does not own the winner) and each score is their max — the max-reduce fused in.
 __global__ void __launch_bounds__(256)
     order_by_kernel(const float* __restrict__ ms, const int64_t* __restrict__ ids,
                     const float* __restrict__ ip, int k, int64_t* __restrict__ out_ids,
-                    float* __restrict__ out_ip, float* __restrict__ out_ms) {
+                    float* __restrict__ out_ip, float* __restrict__ out_ms, int planes,
+                    size_t plane_stride) {
   __shared__ uint64_t buf[256];
   __shared__ float s_ip[256], s_ms[256];
   __shared__ int64_t s_id[256];
@@ -89,13 +92,15 @@ __global__ void __launch_bounds__(256)
     uint64_t key = 0ull;
     if (i < k) {
       int64_t id = ids[base + i];
+      float m = ms[base + i];
+      for (int g = 1; g < planes; ++g) m = fmaxf(m, ms[(size_t)g * plane_stride + base + i]);
       s_ip[i] = ip[base + i];
-      s_ms[i] = ms[base + i];
+      s_ms[i] = m;
       s_id[i] = id;
       // position i is carried in the low bits; ties on MaxSim resolve by id
       // because the IP top-k list is id-unique and we rank (ms desc, id asc).
       if (id >= 0) {
-        uint32_t ord = vx_order_f32(ms[base + i]);
+        uint32_t ord = vx_order_f32(m);
         key = ((uint64_t)ord << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)id);
       }
     }
@@ -127,9 +132,10 @@ __global__ void __launch_bounds__(256)
 
 cudaError_t launch_order_by(const float* key_score, const int64_t* ids, const float* ip, int B,
                             int k, int64_t* out_ids, float* out_ip, float* out_ms,
-                            cudaStream_t st) {
-  if (k < 1 || k > 256) return cudaErrorInvalidValue;
-  order_by_kernel<<<B, 256, 0, st>>>(key_score, ids, ip, k, out_ids, out_ip, out_ms);
+                            cudaStream_t st, int planes, size_t plane_stride) {
+  if (k < 1 || k > 256 || planes < 1) return cudaErrorInvalidValue;
+  order_by_kernel<<<B, 256, 0, st>>>(key_score, ids, ip, k, out_ids, out_ip, out_ms, planes,
+                                     plane_stride);
   return cudaGetLastError();
 }
 

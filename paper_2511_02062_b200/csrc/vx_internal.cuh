@@ -198,7 +198,8 @@ cudaError_t launch_cert_scatter(const int* fidx, const int* fcount, int B, int k
 // permute the companion arrays: used to order by MaxSim after the IP top-k.
 cudaError_t launch_order_by(const float* key_score, const int64_t* ids, const float* ip, int B,
                             int k, int64_t* out_ids, float* out_ip, float* out_ms,
-                            cudaStream_t st);
+                            cudaStream_t st, int planes = 1,
+                            size_t plane_stride = 0);
 
 // -------- synthetic fill: synth.cu
 cudaError_t launch_synth_rows(float* out, uint64_t seed, int64_t row0, int64_t n, int D,
