@@ -18,7 +18,10 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <mutex>
+#include <string>
 #include <random>
 #include <thread>
 #include <vector>
@@ -138,12 +141,34 @@ extern "C" vx_status vx_serve_trace_replicas(
   auto now_us = [&] {
     return (uint64_t)std::chrono::duration_cast<std::chrono::microseconds>(clk::now() - t0).count();
   };
-  // rows [i0, i1) of member m's queue head -> its next input buffer (gather + one DMA each)
-  auto stage_rows = [&](Member& m, int i0, int i1) -> vx_status {
+  // Threads: the calling thread is the ingress (routes each arrival at its planned time); each
+  // member has its own dispatcher thread (completion, dispatch, pre-staging on its GPU).  One
+  // host thread serving every member was the bottleneck at R > 1 (4 members: 335 K q/s at
+  // p99 <= 10 ms, below one member's 549 K — small batches, ~10 CUDA calls and a row gather per
+  // dispatch, all serialised).  The reference's single event loop is kept where it matters:
+  // every routing decision, dispatch snapshot and completion takes `mu` together with the
+  // global sequence number, so the event order the replay tests check is one total order.
+  std::mutex mu;
+  uint64_t seq = 0;
+  std::atomic<int64_t> remaining(n);
+  std::atomic<bool> stop(false), failed(false);
+  std::string err_msg;
+  vx_status err_code = VX_OK;
+  auto record_error = [&](vx_status code) {
+    std::lock_guard<std::mutex> g(mu);
+    if (!failed.exchange(true)) {
+      err_code = code;
+      err_msg = vx_last_error();  // thread-local in the failing thread
+    }
+  };
+  const int stage_chunk = std::max(8, std::min(64, cap / 16));
+  int64_t nb_total = 0;
+  // rows [i0, i1) of the queue snapshot `rows` -> member m's next input buffer (gather + DMA)
+  auto stage_rows = [&](Member& m, const int64_t* rows, int i0, int i1) -> vx_status {
     if (i1 <= i0) return VX_OK;
     uint8_t* p = m.pin[m.nextbuf];
     for (int i = i0; i < i1; ++i) {
-      const int64_t q = m.bat.queued_at((size_t)i);
+      const int64_t q = rows[i - i0];
       memcpy(p + (size_t)i * qrow, queries + q * D, qrow);
       if (rescore) memcpy(p + (size_t)cap * qrow + (size_t)i * trow, qtok + q * (int64_t)nq * td, trow);
     }
@@ -156,23 +181,135 @@ extern "C" vx_status vx_serve_trace_replicas(
                              cudaMemcpyHostToDevice, m.up));
     return VX_OK;
   };
-  const int stage_chunk = std::max(8, std::min(64, cap / 16));
-  int cur_dev = -1;
-  int64_t next = 0, nb = 0;
-  uint64_t seq = 0;
-  int64_t remaining = n;
-  while (remaining > 0) {
+  auto member_loop = [&](int r) {
+    Member& m = mem[r];
+    if (cudaSetDevice(m.h->device) != cudaSuccess) {
+      fail(VX_ERR_CUDA, "cudaSetDevice");
+      record_error(VX_ERR_CUDA);
+      return;
+    }
+    std::vector<int64_t> snap;
+    std::vector<int64_t> batch;
+    while (!stop.load(std::memory_order_relaxed) && !failed.load(std::memory_order_relaxed)) {
+      bool progressed = false;
+      if (m.busy) {
+        const cudaError_t q = cudaEventQuery(m.done);
+        if (q == cudaSuccess) {  // complete_batch (runtime.hpp:656-672)
+          const uint64_t tc = now_us();
+          const int B = (int)m.cur.size();
+          uint64_t cs;
+          {
+            std::lock_guard<std::mutex> g(mu);
+            cs = seq++;
+            m.outstanding -= B;
+            m.bat.complete();
+          }
+          for (int i = 0; i < B; ++i) {
+            const int64_t qq = m.cur[i];
+            latency_us[qq] = (double)tc - (double)arrivals_us[qq];
+            if (complete_us) complete_us[qq] = tc;
+            if (complete_seq) complete_seq[qq] = cs;
+            if (ids) memcpy(ids + qq * k, m.res + (size_t)i * k, (size_t)k * 8);
+          }
+          m.busy = false;
+          remaining.fetch_sub(B);
+          progressed = true;
+        } else if (q != cudaErrorNotReady) {
+          fail(VX_ERR_CUDA, "live batch: %s", cudaGetErrorString(q));
+          record_error(VX_ERR_CUDA);
+          return;
+        }
+      }
+      if (!m.busy) {  // maybe_dispatch (runtime.hpp:617-654): snapshot + sequence number
+        int B = 0, pre = m.staged;
+        uint64_t ds = 0;
+        {
+          std::lock_guard<std::mutex> g(mu);
+          if (m.bat.queued() > 0) {
+            B = (int)std::min<size_t>(m.bat.queued(), (size_t)cap);
+            snap.clear();
+            for (int i = pre; i < B; ++i) snap.push_back(m.bat.queued_at((size_t)i));
+            batch = m.bat.maybe_dispatch();
+            ds = seq++;
+          }
+        }
+        if (B > 0) {
+          vx_status s = stage_rows(m, snap.data(), pre, B);
+          const uint64_t td_us = now_us();
+          for (int64_t qq : batch) {
+            if (dispatch_us) dispatch_us[qq] = td_us;
+            if (dispatch_seq) dispatch_seq[qq] = ds;
+          }
+          vx_index* h = m.h;
+          cudaStream_t st = h->stream;
+          if (s == VX_OK && (cudaEventRecord(m.up_ev, m.up) != cudaSuccess ||
+                             cudaStreamWaitEvent(st, m.up_ev, 0) != cudaSuccess))
+            s = fail(VX_ERR_CUDA, "live: staging event");
+          if (s == VX_OK)
+            s = stage_begin(h, rescore ? OP_RESCORE : OP_SEARCH, m.dq[m.nextbuf], B, nq, k, st);
+          if (s == VX_OK)
+            s = rescore ? stage_finish(h, m.dt[m.nextbuf], B, nq, k, h->d_out_ids, h->d_out_ip,
+                                       h->d_out_ms, st)
+                        : stage_search_out(h, B, k, h->d_out_ids, h->d_out_ip, st);
+          if (s == VX_OK &&
+              (cudaMemcpyAsync(m.res, h->d_out_ids, (size_t)B * k * 8, cudaMemcpyDeviceToHost,
+                               st) != cudaSuccess ||
+               cudaEventRecord(m.done, st) != cudaSuccess))
+            s = fail(VX_ERR_CUDA, "live: result copy");
+          if (s != VX_OK) {
+            record_error(s);
+            return;
+          }
+          {
+            std::lock_guard<std::mutex> g(mu);
+            const int64_t id = nb_total++;
+            if (batch_of)
+              for (int64_t qq : batch) batch_of[qq] = id;
+          }
+          m.cur.swap(batch);
+          m.busy = true;
+          m.nextbuf ^= 1;
+          m.staged = 0;
+          progressed = true;
+        }
+      }
+      if (m.busy) {  // pre-stage the queries queued behind the running batch, in chunks
+        int target = 0;
+        {
+          std::lock_guard<std::mutex> g(mu);
+          target = (int)std::min<size_t>(m.bat.queued(), (size_t)cap);
+          if (target - m.staged >= stage_chunk) {
+            snap.clear();
+            for (int i = m.staged; i < target; ++i) snap.push_back(m.bat.queued_at((size_t)i));
+          } else {
+            target = m.staged;
+          }
+        }
+        if (target > m.staged) {
+          const vx_status s = stage_rows(m, snap.data(), m.staged, target);
+          if (s != VX_OK) {
+            record_error(s);
+            return;
+          }
+          m.staged = target;
+          progressed = true;
+        }
+      }
+      if (!progressed) std::this_thread::yield();
+    }
+  };
+  std::vector<std::thread> workers;
+  for (int r = 0; r < R; ++r) workers.emplace_back(member_loop, r);
+  // ingress: route every arrival at its planned time (runtime.hpp:289-290 tags at submit)
+  for (int64_t next = 0; next < n && !failed.load();) {
     uint64_t t = now_us();
-    bool any_busy = false, progressed = false;
-    for (auto& m : mem) any_busy |= m.busy || m.bat.queued() > 0;
-    if (!any_busy && next < n && arrivals_us[next] > t) {
-      // idle: wait for the next planned arrival (spin the last 200 us for precision)
-      while ((t = now_us()) + 200 < arrivals_us[next])
+    if (arrivals_us[next] > t) {
+      while ((t = now_us()) + 200 < arrivals_us[next] && !failed.load())
         std::this_thread::sleep_for(std::chrono::microseconds(100));
       while ((t = now_us()) < arrivals_us[next]) {
       }
     }
-    // ingress: route every arrival due (runtime.hpp:289-290 tags at submit)
+    std::lock_guard<std::mutex> g(mu);
     while (next < n && arrivals_us[next] <= t) {
       const int r = pick();
       ++mem[r].outstanding;
@@ -180,82 +317,13 @@ extern "C" vx_status vx_serve_trace_replicas(
       if (instance_of) instance_of[next] = r;
       if (admit_seq) admit_seq[next] = seq++;
       ++next;
-      progressed = true;
     }
-    for (int r = 0; r < R; ++r) {
-      Member& m = mem[r];
-      if (m.h->device != cur_dev) {
-        LIVE_CU(cudaSetDevice(m.h->device));
-        cur_dev = m.h->device;
-      }
-      if (m.busy) {
-        const cudaError_t q = cudaEventQuery(m.done);
-        if (q == cudaSuccess) {  // complete_batch (runtime.hpp:656-672)
-          const uint64_t tc = now_us();
-          const int B = (int)m.cur.size();
-          for (int i = 0; i < B; ++i) {
-            const int64_t qq = m.cur[i];
-            latency_us[qq] = (double)tc - (double)arrivals_us[qq];
-            if (complete_us) complete_us[qq] = tc;
-            if (complete_seq) complete_seq[qq] = seq;
-            if (ids) memcpy(ids + qq * k, m.res + (size_t)i * k, (size_t)k * 8);
-          }
-          ++seq;
-          m.outstanding -= B;
-          remaining -= B;
-          m.bat.complete();
-          m.busy = false;
-          progressed = true;
-        } else if (q != cudaErrorNotReady) {
-          return cleanup(fail(VX_ERR_CUDA, "live batch: %s", cudaGetErrorString(q)));
-        }
-      }
-      if (!m.busy && m.bat.queued() > 0) {  // maybe_dispatch (runtime.hpp:617-654)
-        const int pre = m.staged;
-        std::vector<int64_t> batch;
-        const int B = (int)std::min<size_t>(m.bat.queued(), (size_t)cap);
-        LIVE_TRY(stage_rows(m, pre, B));
-        batch = m.bat.maybe_dispatch();
-        const uint64_t td_us = now_us();
-        for (int64_t qq : batch) {
-          if (dispatch_us) dispatch_us[qq] = td_us;
-          if (dispatch_seq) dispatch_seq[qq] = seq;
-          if (batch_of) batch_of[qq] = nb;
-        }
-        ++seq;
-        ++nb;
-        vx_index* h = m.h;
-        cudaStream_t st = h->stream;
-        LIVE_CU(cudaEventRecord(m.up_ev, m.up));
-        LIVE_CU(cudaStreamWaitEvent(st, m.up_ev, 0));
-        vx_status s = stage_begin(h, rescore ? OP_RESCORE : OP_SEARCH, m.dq[m.nextbuf], B, nq, k, st);
-        if (s == VX_OK)
-          s = rescore ? stage_finish(h, m.dt[m.nextbuf], B, nq, k, h->d_out_ids, h->d_out_ip,
-                                     h->d_out_ms, st)
-                      : stage_search_out(h, B, k, h->d_out_ids, h->d_out_ip, st);
-        if (s != VX_OK) return cleanup(s);
-        LIVE_CU(cudaMemcpyAsync(m.res, h->d_out_ids, (size_t)B * k * 8, cudaMemcpyDeviceToHost, st));
-        LIVE_CU(cudaEventRecord(m.done, st));
-        m.cur.swap(batch);
-        m.busy = true;
-        m.nextbuf ^= 1;
-        m.staged = 0;
-        progressed = true;
-      }
-      if (m.busy) {  // pre-stage the queries queued behind the running batch
-        // in chunks: one DMA per arriving row (a ~5 us API call each) made the host thread the
-        // bottleneck with several members at high rates (4 members: 335 K q/s vs 549 K for
-        // one); the rows left at dispatch are uploaded then
-        const int target = (int)std::min<size_t>(m.bat.queued(), (size_t)cap);
-        if (target - m.staged >= stage_chunk) {
-          LIVE_TRY(stage_rows(m, m.staged, target));
-          m.staged = target;
-        }
-      }
-    }
-    if (!progressed) std::this_thread::yield();
   }
-  if (n_batches) *n_batches = nb;
+  while (remaining.load() > 0 && !failed.load()) std::this_thread::yield();
+  stop.store(true);
+  for (auto& w : workers) w.join();
+  if (failed.load()) return cleanup(fail(err_code, "%s", err_msg.c_str()));
+  if (n_batches) *n_batches = nb_total;
   for (auto& m : mem) {
     LIVE_CU(cudaSetDevice(m.h->device));
     LIVE_TRY(vx_sync(m.h));
