@@ -675,7 +675,7 @@ def run_ours(args) -> None:
         if fam == "scan_tc2" and roof["queries_per_launch"] > 256:
             fam = "scan_tc2_qg2"  # two query groups on 128-document tiles
         tkey = f"{fam}/{coarse or 'f32'}/{n_local}/{D}"
-        tdb = ROOT / "profiles" / "r01" / "traffic.json"
+        tdb = ROOT / "profiles" / "r02" / "traffic.json"
         trec = json.loads(tdb.read_text()).get(tkey) if tdb.exists() else None
         roof.update({"kernel": kernel_name, "scan_ms": scan_ms,
                      "traffic": trec["dram_bytes"] if trec else None,
