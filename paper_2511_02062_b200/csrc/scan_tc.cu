@@ -309,24 +309,29 @@ __global__ void __launch_bounds__(TcCfg<QT, TD>::kThreads, 1)
           head[r] = r < rep ? mb[(r * a.a_rows + m) * MS] : 0ull;
         }
         uint64_t* out = a.part + ((size_t)m * gridDim.x + blockIdx.x) * KC;
+        // branch-free: the winner's list index selects one refill load (lanes picking different
+        // lists diverged into up to 8 serial load paths per step — ~4 us of a one-tile pass)
 #pragma unroll 1
         for (int j = 0; j < KC; ++j) {
           uint64_t best = head[0];
           int br = 0;
 #pragma unroll
           for (int r = 1; r < 8; ++r) {
-            if (head[r] > best) {
-              best = head[r];
-              br = r;
-            }
+            const bool gt = head[r] > best;
+            best = gt ? head[r] : best;
+            br = gt ? r : br;
           }
           out[j] = best;
+          int np = 0;
 #pragma unroll
-          for (int r = 0; r < 8; ++r)
-            if (r == br) {
-              pos[r] = min(pos[r] + 1, KC);
-              head[r] = mb[(r * a.a_rows + m) * MS + pos[r]];
-            }
+          for (int r = 0; r < 8; ++r) np = r == br ? pos[r] + 1 : np;
+          np = min(np, KC);
+          const uint64_t nk = mb[(br * a.a_rows + m) * MS + np];
+#pragma unroll
+          for (int r = 0; r < 8; ++r) {
+            pos[r] = r == br ? np : pos[r];
+            head[r] = r == br ? nk : head[r];
+          }
         }
         if (trc && threadIdx.x == 128) trc[10] = gtimer_ns();
       }
