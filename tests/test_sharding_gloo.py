@@ -94,11 +94,15 @@ def test_two_rank_gloo_two_phase_exchange_equals_global(oracle):
 
 
 def _tau_worker(rank: int, world: int, port: int, q) -> None:
-    """The sharded re-rank threshold (vx_stage.cu shard_tau, scan_tc.cu shard_lb/shard_tau/
-    rerank_kernel) restated on CPU: s8 coarse scores with the certificate's rigorous bound E,
-    tau = k-th largest of the all-gathered lower bounds, each shard re-ranks only candidates
-    with cscale c + E >= tau and certifies with `bound(T') < tau or exact k-th > bound(T')`;
-    rank 0's merge must equal the single-index oracle."""
+    """The sharded re-rank (vx_stage.cu kprime_of / local_topk_tc, scan_tc.cu rerank_kernel
+    phases 1-2, shard_tau_kernel) restated on CPU, as the GPU runs it: s8 coarse scores with the
+    certificate's rigorous bound E; each shard keeps k'/G candidates (not below 2 next_pow2(k));
+    phase 1 re-scores its head — the k best coarse candidates, 2k/G of them for G > 2 — EXACTLY
+    and the shards all-gather those exact scores; tau = their k-th largest (k distinct
+    documents score >= tau, so tau <= the global exact k-th); phase 2 re-ranks only the tail
+    candidates with cscale c >= max(L, tau) - E (L = the head's minimum exact score when the
+    head holds k rows) and certifies with `bound(T') < tau or exact k-th > bound(T')`; rank 0's
+    merge must equal the single-index oracle."""
     import torch
     import torch.distributed as dist
     sys.path.insert(0, str(ROOT / "oracle"))
@@ -106,7 +110,17 @@ def _tau_worker(rank: int, world: int, port: int, q) -> None:
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    N, D, B, k, kp = 40_000, 128, 6, 10, 80
+    N, D, B, k = 40_000, 128, 6, 10
+
+    def np2(x):
+        p = 1
+        while p < x:
+            p <<= 1
+        return p
+    kp1 = min(1024, max(128, 8 * np2(k)))                    # the single-index s8 k'
+    kp = max(min(kp1, 2 * np2(k)), kp1 // np2(world))        # the shard's k'/G
+    kh = k if world <= 2 else min(k, max(16, (2 * k + world - 1) // world))
+    kh = min(kh, kp)
     r0, n = shard_range(N, world, rank)
     X = o.synth_rows(42, r0, n, D).astype(np.float64)
     Q = o.synth_rows(43, 0, B, D).astype(np.float64)
@@ -121,21 +135,32 @@ def _tau_worker(rank: int, world: int, port: int, q) -> None:
     coarse = (Q8 @ X8.T) * (sq[:, None] * sx)          # cscale * s32 dot
     cand = np.argsort(-coarse, axis=1, kind="stable")[:, :kp]
     ccand = np.take_along_axis(coarse, cand, axis=1)
-    lb = torch.from_numpy(np.ascontiguousarray(ccand[:, :k] - E[:, None]))
-    allb = [torch.zeros_like(lb) for _ in range(world)]
-    dist.all_gather(allb, lb)
-    tau = np.sort(np.concatenate([t.numpy() for t in allb], axis=1), axis=1)[:, ::-1][:, k - 1]
     Xe = o.synth_rows(42, r0, n, D)
     Qe = o.synth_rows(43, 0, B, D)
+
+    def exact(b, rows):  # the in-order fp32 chains (VXO_F32), one row at a time
+        return np.array([o.flat_topk(Xe[j:j + 1], Qe[b:b + 1], 1, mode=1)[1][0, 0] for j in rows],
+                        np.float32)
+    # phase 1: exact scores of the head, all-gathered
+    head_ex = [exact(b, cand[b, :kh]) for b in range(B)]
+    lb_np = np.full((B, k), -np.inf, np.float32)
+    for b in range(B):
+        lb_np[b, :kh] = head_ex[b]
+    allb = [torch.zeros((B, k), dtype=torch.float32) for _ in range(world)]
+    dist.all_gather(allb, torch.from_numpy(lb_np))
+    tau = np.sort(np.concatenate([t.numpy() for t in allb], axis=1), axis=1)[:, ::-1][:, k - 1]
     ids = np.full((B, k), -1, np.int64)
     sc = np.full((B, k), -np.inf, np.float32)
     ok = True
     fetched = 0
     for b in range(B):
-        keep = cand[b][ccand[b] + E[b] >= tau[b]]          # the pruned prefix
+        L = float(head_ex[b].min()) if kh >= k else -np.inf
+        lim = max(L, float(tau[b])) - E[b]
+        tail = np.arange(kh, kp)
+        tail = tail[ccand[b, tail] >= lim]                    # the pruned prefix (descending)
+        keep = np.concatenate([cand[b, :kh], cand[b, tail]])
+        ex = np.concatenate([head_ex[b], exact(b, cand[b, tail])])
         fetched += keep.size
-        ex = np.array([o.flat_topk(Xe[j:j + 1], Qe[b:b + 1], 1, mode=1)[1][0, 0] for j in keep],
-                      np.float32)
         order = np.lexsort((keep, -ex))[:k]
         ids[b, :order.size] = keep[order] + r0
         sc[b, :order.size] = ex[order]
@@ -158,12 +183,13 @@ def _tau_worker(rank: int, world: int, port: int, q) -> None:
     dist.destroy_process_group()
 
 
-def test_two_rank_gloo_sharded_threshold_prunes_and_stays_exact(oracle):
+@pytest.mark.parametrize("world", [2, 4])
+def test_gloo_sharded_threshold_prunes_and_stays_exact(oracle, world):
     import multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29600 + os.getpid() % 1000
-    procs = [ctx.Process(target=_tau_worker, args=(r, 2, port, q)) for r in range(2)]
+    port = 29600 + os.getpid() % 1000 + 7 * world
+    procs = [ctx.Process(target=_tau_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     certified, exact, fetched = q.get(timeout=240)
@@ -171,4 +197,5 @@ def test_two_rank_gloo_sharded_threshold_prunes_and_stays_exact(oracle):
         p.join(timeout=60)
         assert p.exitcode == 0
     assert certified and exact
-    assert fetched < 2 * 6 * 80  # the threshold pruned candidates on the shards
+    kp = max(min(128, 32), 128 // world)
+    assert fetched < world * 6 * kp  # the threshold pruned candidates on the shards
