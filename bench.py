@@ -153,6 +153,9 @@ def parse() -> argparse.Namespace:
     ap.add_argument("--tok-per-doc", type=int, default=128)
     ap.add_argument("--tok-dim", type=int, default=128)
     ap.add_argument("--tok-blocks", type=int, default=1 << 18)
+    ap.add_argument("--tok-f32", action="store_true",
+                    help="fp32 doc-token store (SURVEY C2's fp32 variant): exact fp32 MaxSim on "
+                         "the CUDA cores; default bf16 store")
     ap.add_argument("--slo-ms", type=float, default=None)
     ap.add_argument("--scan", choices=["auto", "f32", "tc"], default="auto")
     ap.add_argument("--coarse", choices=["auto", "tf32", "bf16", "i8"], default="auto",
@@ -274,7 +277,11 @@ def _compact_blocks(o, cand: np.ndarray, args):
     T = args.tok_blocks
     blk = np.where(cand >= 0, cand % T, 0)
     uniq, inv = np.unique(blk, return_inverse=True)
-    table = o.synth_token_blocks(45, uniq, args.tok_per_doc, args.tok_dim)
+    if getattr(args, "tok_f32", False):  # the fp32 store: the generator's rows, unrounded
+        table = np.stack([o.synth_rows(45, int(u) * args.tok_per_doc, args.tok_per_doc,
+                                       args.tok_dim) for u in uniq])
+    else:
+        table = o.synth_token_blocks(45, uniq, args.tok_per_doc, args.tok_dim)
     return table, np.where(cand >= 0, inv.reshape(cand.shape), -1).astype(np.int64)
 
 
@@ -316,7 +323,7 @@ def cpu_check(args, world: int, gpu: dict, timed: bool) -> tuple[dict | None, di
             t0 = time.perf_counter()
             o.maxsim(qts, local, table, mode=o.F32)
             t_ms = time.perf_counter() - t0
-            truth = o.maxsim(qts, local, table, mode=o.F64_Q32)
+            truth = o.maxsim(qts, local, table, mode=o.F64_Q32 if not args.tok_f32 else o.F64)
         if wl == "stage":
             r = check_stage(gpu["ids"][sel], gpu["ip"][sel], gpu["ms"][sel], rid, rsc, truth)
             parity.update(r)
@@ -354,20 +361,29 @@ def cpu_check(args, world: int, gpu: dict, timed: bool) -> tuple[dict | None, di
 
 
 # ----------------------------------------------------------------------------- rooflines
-def maxsim_roofline(pk: dict, *, B: int, C: int, nq: int, nd: int, d: int, ms: float) -> dict:
-    """K4 (MaxSim) ceilings: HBM bytes = the candidates' bf16 token blocks +
-    query tokens + ids/scores; flops = 2*B*C*Nq*Nd*d (algorithmic; the tcgen05 tile issues
-    M=128 rows, so the tensor pipe executes 128/Nq x that)."""
-    hbm_bytes = B * C * nd * d * 2 + B * nq * d * 4 + B * C * 12
+def maxsim_roofline(pk: dict, *, B: int, C: int, nq: int, nd: int, d: int, ms: float,
+                    f32: bool = False, mhz: float | None = None) -> dict:
+    """K4 (MaxSim) ceilings: HBM bytes = the candidates' token blocks (bf16,
+    or fp32 for the fp32 store) + query tokens + ids/scores; flops = 2*B*C*Nq*Nd*d (algorithmic;
+    the tcgen05 tile issues M=128 rows, so the tensor pipe executes 128/Nq x that).  The fp32
+    store runs on the CUDA cores: its compute ceiling is 148 SMs x 128 fp32 FMA/clk."""
+    hbm_bytes = B * C * nd * d * (4 if f32 else 2) + B * nq * d * 4 + B * C * 12
     flops = 2.0 * B * C * nq * nd * d
     issued = 2.0 * B * C * 128 * nd * d
     s = ms / 1e3
     hbm = {"achieved": hbm_bytes / s / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
            "bytes_per_launch": hbm_bytes}
     hbm["frac"] = hbm["achieved"] / hbm["peak"]
-    comp = {"achieved": flops / s / 1e12, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
-            "pipe": "tensor (tcgen05 kind::f16)", "flops_per_launch": flops,
-            "issued_flops_per_launch": issued, "issued_frac": issued / s / 1e12 / pk["bf16_tflops"]}
+    if f32:
+        clk = (mhz or pk.get("sm_max_mhz") or 1965.0) * 1e6
+        peak = 148 * 128 * 2 * clk / 1e12
+        comp = {"achieved": flops / s / 1e12, "peak": peak, "unit": "TFLOP/s",
+                "pipe": "fp32 FMA (CUDA cores) at the kernel's clock", "flops_per_launch": flops}
+    else:
+        comp = {"achieved": flops / s / 1e12, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                "pipe": "tensor (tcgen05 kind::f16)", "flops_per_launch": flops,
+                "issued_flops_per_launch": issued,
+                "issued_frac": issued / s / 1e12 / pk["bf16_tflops"]}
     comp["frac"] = comp["achieved"] / comp["peak"]
     t_hbm, t_comp = hbm_bytes / (hbm["peak"] * 1e9), flops / (comp["peak"] * 1e12)
     top = hbm if t_hbm >= t_comp else comp
@@ -402,7 +418,8 @@ def run_ours(args) -> None:
                    shard=rank if sharded else 0,
                    tok_per_doc=args.tok_per_doc if tokens else 0, tok_dim=td,
                    tok_blocks=args.tok_blocks, max_batch=B, max_k=k, max_qtok=nq,
-                   flags=vx.VX_FLAG_NO_BF16_SHADOW if wl == "maxsim" else 0)
+                   flags=(vx.VX_FLAG_NO_BF16_SHADOW if wl == "maxsim" else 0)
+                   | (vx.VX_FLAG_TOKENS_F32 if (tokens and args.tok_f32) else 0))
     if args.graphs:
         idx.set_option(vx.VX_OPT_GRAPHS, 1)
     if args.tile:
@@ -640,8 +657,11 @@ def run_ours(args) -> None:
     if wl == "maxsim":
         n_ms, ms_launch, ms_mhz = kt(3)
         kms = ms_launch if ms_launch else mean_step
-        roof = maxsim_roofline(pk, B=B, C=C, nq=nq, nd=args.tok_per_doc, d=td, ms=kms)
-        kernel_name = "maxsim_tc_kernel (K4, tcgen05 kind::f16, fused row-max + sum)"
+        roof = maxsim_roofline(pk, B=B, C=C, nq=nq, nd=args.tok_per_doc, d=td, ms=kms,
+                               f32=args.tok_f32, mhz=ms_mhz)
+        kernel_name = ("maxsim_cc_kernel (K4', fp32 token store: exact in-order fp32 chains on "
+                       "the CUDA cores)" if args.tok_f32 else
+                       "maxsim_tc_kernel (K4, tcgen05 kind::f16, fused row-max + sum)")
         roof.update({"kernel": kernel_name, "kernel_ms": kms, "kernel_launches": n_ms,
                      "kernel_sm_mhz": ms_mhz, "traffic": None,
                      "timing": "device-side per-launch timer (first CTA start -> last CTA end)"})
@@ -689,7 +709,8 @@ def run_ours(args) -> None:
             cpu = {k_: c[k_] for k_ in ("value", "unit", "cores", "kind", "sample")}
     cfg = config_of(args, world)
     path = {"scan": "tc" if tc else "f32", "coarse": coarse,
-            "maxsim": ("tcgen05 kind::f16, fp32 query tokens as bf16 hi+lo (nq <= 64)"
+            "maxsim": (("fp32 token store: exact in-order fp32 on the CUDA cores" if args.tok_f32
+                        else "tcgen05 kind::f16, fp32 query tokens as bf16 hi+lo (nq <= 64)")
                        if tokens else None)}
     out = {
         "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
@@ -825,7 +846,8 @@ def config_of(args, world: int) -> dict:
            "shards": world if sharded else 1, "replicas": 1 if sharded else world}
     if wl in ("stage", "maxsim"):
         cfg.update({"q_tokens": args.nq, "doc_tokens": args.tok_per_doc, "tok_dim": args.tok_dim,
-                    "tok_blocks": args.tok_blocks})
+                    "tok_blocks": args.tok_blocks,
+                    "tok_store": "f32" if getattr(args, "tok_f32", False) else "bf16"})
     cfg["l2"] = ("L2 flushed between timed steps (untimed): a 256 MB buffer written, then read back so the L2 holds clean lines; value = sum of per-step event times"
                  if wl in ("flat", "maxsim") else "index (GB) >> 126 MB L2: every step streams from HBM")
     return cfg

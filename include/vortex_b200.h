@@ -86,7 +86,10 @@ enum { VX_COARSE_AUTO = 0, VX_COARSE_TF32 = 1, VX_COARSE_BF16 = 2, VX_COARSE_I8 
 /* vx_index_desc.flags */
 enum {
   VX_FLAG_NO_BF16_SHADOW = 1, /* do not keep the bf16 copy of the index (saves N*D*2 B) */
-  VX_FLAG_NO_I8_SHADOW = 2    /* do not keep the s8 copy of the index (saves N*D B) */
+  VX_FLAG_NO_I8_SHADOW = 2,   /* do not keep the s8 copy of the index (saves N*D B) */
+  VX_FLAG_TOKENS_F32 = 4      /* fp32 doc-token store (SURVEY C2's fp32 variant: 4 B per
+                                 element, MaxSim in exact in-order fp32 on the CUDA cores,
+                                 query tokens unrounded); default bf16 */
 };
 /* MaxSim kernel selection (vx_set_option VX_OPT_MAXSIM).
  *  AUTO / TC: tensor-core kernel; for nq <= 64 the fp32 query tokens enter as bf16 hi + lo
@@ -178,6 +181,9 @@ vx_status vx_tokens_synth(vx_index* h, uint64_t seed);
 /* Upload token blocks [blk0, blk0+n): bf16 bits, [n][Nd][d]. */
 vx_status vx_tokens_upload(vx_index* h, const uint16_t* tokens_bf16, int64_t blk0, int64_t n);
 vx_status vx_tokens_download(const vx_index* h, uint16_t* tokens_bf16, int64_t blk0, int64_t n);
+/* The same for an fp32 token store (VX_FLAG_TOKENS_F32). */
+vx_status vx_tokens_upload_f32(vx_index* h, const float* tokens, int64_t blk0, int64_t n);
+vx_status vx_tokens_download_f32(const vx_index* h, float* tokens, int64_t blk0, int64_t n);
 
 /* Exact inner-product top-k of B queries (fp32 [B][D]).  Host buffers. */
 vx_status vx_search(vx_index* h, const float* queries, int32_t B, int32_t k, int64_t* ids,

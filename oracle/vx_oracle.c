@@ -252,6 +252,59 @@ static double maxsim_one(const float* qb /* bf16-rounded (VXO_F64_Q32: raw) fp32
   return total;
 }
 
+/* MaxSim against an fp32 doc-token table (the fp32 token store, VX_FLAG_TOKENS_F32): the
+ * query tokens stay fp32 in every mode; VXO_F32 = one in-order fmaf chain per (query token,
+ * doc token), max in order, the sum over query tokens in order (maxsim.cu maxsim_cc_kernel);
+ * VXO_F64 / VXO_F64_Q32 = the same in fp64 (the truth). */
+static double maxsim_one_f32(const float* q, int32_t nq, int32_t dim, const float* dt, int32_t Nd,
+                             int32_t mode) {
+  if (mode == VXO_F32) {
+    float total = 0.0f;
+    for (int32_t i = 0; i < nq; ++i) {
+      float best = -INFINITY;
+      for (int32_t j = 0; j < Nd; ++j) {
+        float acc = 0.0f;
+        for (int32_t t = 0; t < dim; ++t)
+          acc = fmaf(q[(int64_t)i * dim + t], dt[(int64_t)j * dim + t], acc);
+        if (acc > best) best = acc;
+      }
+      total += best;
+    }
+    return (double)total;
+  }
+  double total = 0.0;
+  for (int32_t i = 0; i < nq; ++i) {
+    double best = -INFINITY;
+    for (int32_t j = 0; j < Nd; ++j) {
+      double acc = 0.0;
+      for (int32_t t = 0; t < dim; ++t)
+        acc += (double)q[(int64_t)i * dim + t] * (double)dt[(int64_t)j * dim + t];
+      if (acc > best) best = acc;
+    }
+    total += best;
+  }
+  return total;
+}
+
+int vxo_maxsim_f32tab(const float* qtok, int32_t B, int32_t nq, int32_t dim, const int64_t* cand,
+                      int32_t C, const float* table, int64_t T, int32_t Nd, int32_t mode,
+                      int32_t threads, double* out) {
+  if (B <= 0 || nq <= 0 || dim <= 0 || C < 0 || T <= 0 || Nd <= 0) return -1;
+  int nt = nthreads_of(threads);
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 4)
+  for (int64_t bc = 0; bc < (int64_t)B * C; ++bc) {
+    int64_t b = bc / C;
+    int64_t id = cand[bc];
+    if (id < 0) {
+      out[bc] = -INFINITY;
+      continue;
+    }
+    out[bc] = maxsim_one_f32(qtok + b * nq * dim, nq, dim, table + (id % T) * (int64_t)Nd * dim, Nd,
+                             mode);
+  }
+  return 0;
+}
+
 int vxo_maxsim(const float* qtok, int32_t B, int32_t nq, int32_t dim, const int64_t* cand,
                int32_t C, const uint16_t* table, int64_t T, int32_t Nd, int32_t mode,
                int32_t threads, double* out) {

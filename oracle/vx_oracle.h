@@ -75,6 +75,10 @@ int vxo_flat_topk(const float* X, int64_t n, int32_t dim, int64_t id_base, const
 int vxo_maxsim(const float* qtok, int32_t B, int32_t nq, int32_t dim, const int64_t* cand,
                int32_t C, const uint16_t* table, int64_t T, int32_t Nd, int32_t mode,
                int32_t threads, double* out);
+/* The same against an fp32 table [T][Nd][dim] (query tokens kept in fp32 in every mode). */
+int vxo_maxsim_f32tab(const float* qtok, int32_t B, int32_t nq, int32_t dim, const int64_t* cand,
+                      int32_t C, const float* table, int64_t T, int32_t Nd, int32_t mode,
+                      int32_t threads, double* out);
 
 /* The fused stage: IP top-k, MaxSim of those k, re-ordered by MaxSim desc (ties
  * id asc).  ids/ip/ms [B][k]. */

@@ -43,6 +43,7 @@ def lib():
         L.vxo_dot.restype = C.c_double
         L.vxo_flat_topk.argtypes = [fp, i64, i32, i64, fp, i32, i32, i32, i32, lp, dp]
         L.vxo_maxsim.argtypes = [fp, i32, i32, i32, lp, i32, hp, i64, i32, i32, i32, dp]
+        L.vxo_maxsim_f32tab.argtypes = [fp, i32, i32, i32, lp, i32, fp, i64, i32, i32, i32, dp]
         L.vxo_search_rescore.argtypes = [fp, i64, i32, fp, fp, i32, i32, i32, i32, hp, i64, i32, i32,
                                          i32, lp, dp, dp]
         L.vxo_percentile.argtypes = [dp, i64, C.c_double]
@@ -92,11 +93,20 @@ def flat_topk(X, Q, k, mode=F64, id_base=0, threads=0):
 
 
 def maxsim(qtok, cand, table, mode=F64, threads=0):
+    """table: uint16 bf16 bits [T][Nd][d] (the bf16 store) or float32 (the fp32 store,
+    vx_oracle.c vxo_maxsim_f32tab)."""
     qtok = np.ascontiguousarray(qtok, np.float32)
     cand = np.ascontiguousarray(cand, np.int64)
-    table = np.ascontiguousarray(table, np.uint16)
     B, nq, d = qtok.shape
     out = np.empty(cand.shape, np.float64)
+    if np.asarray(table).dtype == np.float32:
+        table = np.ascontiguousarray(table, np.float32)
+        rc = lib().vxo_maxsim_f32tab(_p(qtok, C.c_float), B, nq, d, _p(cand, C.c_int64),
+                                     cand.shape[1], _p(table, C.c_float), table.shape[0],
+                                     table.shape[1], mode, threads, _p(out, C.c_double))
+        assert rc == 0
+        return out
+    table = np.ascontiguousarray(table, np.uint16)
     rc = lib().vxo_maxsim(_p(qtok, C.c_float), B, nq, d, _p(cand, C.c_int64), cand.shape[1],
                           _p(table, C.c_uint16), table.shape[0], table.shape[1], mode, threads,
                           _p(out, C.c_double))

@@ -6,7 +6,7 @@ include/vortex_b200_component.hpp).  Compute is hand-written sm_100a CUDA in
 csrc/, reached through the C-ABI of include/vortex_b200.h (libvortex_b200.so).
 """
 from ._lib import (VX_COARSE_AUTO, VX_COARSE_BF16, VX_COARSE_I8, VX_COARSE_TF32,
-                   VX_FLAG_NO_BF16_SHADOW, VX_FLAG_NO_I8_SHADOW,
+                   VX_FLAG_NO_BF16_SHADOW, VX_FLAG_NO_I8_SHADOW, VX_FLAG_TOKENS_F32,
                    VX_MAXSIM_AUTO, VX_MAXSIM_CC, VX_MAXSIM_TC, VX_MAXSIM_TC_BF16Q, VX_OPT_COARSE, VX_OPT_GRAPHS,
                    VX_OPT_GRID, VX_OPT_KPRIME, VX_OPT_MAXSIM, VX_OPT_SCAN, VX_OPT_SCAN_PAIRS,
                    VX_OPT_SCAN_SEED, VX_OPT_SCAN_TILE, VX_OPT_I8_SCALE, VX_OPT_STAGE_EVENTS,

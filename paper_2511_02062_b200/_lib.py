@@ -25,6 +25,7 @@ VX_OPT_STAGE_EVENTS = 11
 VX_COARSE_AUTO, VX_COARSE_TF32, VX_COARSE_BF16, VX_COARSE_I8 = 0, 1, 2, 3
 VX_FLAG_NO_BF16_SHADOW = 1
 VX_FLAG_NO_I8_SHADOW = 2
+VX_FLAG_TOKENS_F32 = 4
 VX_PREPARE_SEARCH, VX_PREPARE_RESCORE = 1, 2
 
 
@@ -77,6 +78,8 @@ SIGNATURES = {
     "vx_tokens_synth": [P, U64],
     "vx_tokens_download": [P, HP, I64, I64],
     "vx_tokens_upload": [P, HP, I64, I64],
+    "vx_tokens_upload_f32": [P, FP, I64, I64],
+    "vx_tokens_download_f32": [P, FP, I64, I64],
     "vx_search": [P, FP, I32, I32, LP, FP],
     "vx_search_rows": [P, C.POINTER(FP), I32, I32, LP, FP],
     "vx_search_rescore_rows": [P, C.POINTER(FP), C.POINTER(FP), I32, I32, I32, LP, FP, FP],

@@ -153,7 +153,12 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
   const size_t D = d->dim, B = d->max_batch, K = d->max_k;
   ALLOC(h->docs, (size_t)h->n_local * D * 4);
   if (d->tok_per_doc > 0)
-    ALLOC(h->tokens, (size_t)d->tok_blocks * d->tok_per_doc * d->tok_dim * 2);
+  {
+    if (d->flags & VX_FLAG_TOKENS_F32)
+      ALLOC(h->tokens32, (size_t)d->tok_blocks * d->tok_per_doc * d->tok_dim * 4);
+    else
+      ALLOC(h->tokens, (size_t)d->tok_blocks * d->tok_per_doc * d->tok_dim * 2);
+  }
   h->grid = h->num_sms;
   ALLOC(h->d_q, B * D * 4);
   if (d->tok_per_doc > 0) ALLOC(h->d_qtok, B * d->max_qtok * d->tok_dim * 4);
@@ -258,7 +263,7 @@ extern "C" vx_status vx_index_destroy(vx_index* h) {
   for (auto& kv : h->io_graphs) cudaGraphExecDestroy(kv.second.exec);
   h->io_graphs.clear();
   if (h->comm) nccl().CommDestroy(h->comm);
-  void* ptrs[] = {h->docs,  h->tokens,    h->d_q,      h->d_qtok,    h->d_part, h->d_keys,
+  void* ptrs[] = {h->docs,  h->tokens, h->tokens32, h->d_q,      h->d_qtok,    h->d_part, h->d_keys,
                   h->d_ids, h->d_ip,      h->d_ms,     h->d_out_ids, h->d_out_ip,
                   h->d_out_ms, h->d_send, h->d_recv, h->d_hdr, h->d_ckeys, h->d_seedk, h->d_flags,
                   h->d_xnorm, h->d_fq, h->docs16, h->d_q16, h->d_fidx, h->d_fcount,
@@ -352,6 +357,8 @@ extern "C" vx_status vx_set_option(vx_index* h, int32_t option, int64_t value) {
       if ((value == VX_MAXSIM_TC || value == VX_MAXSIM_TC_BF16Q) && h->tokens &&
           !vx::maxsim_tc_supported(h->desc.max_qtok, h->desc.tok_per_doc, h->desc.tok_dim))
         return fail(VX_ERR_UNSUPPORTED, "tensor-core MaxSim needs Nd in {64,128,256}, d in {64,128}");
+      if ((value == VX_MAXSIM_TC || value == VX_MAXSIM_TC_BF16Q) && h->tokens32)
+        return fail(VX_ERR_UNSUPPORTED, "the fp32 token store runs the CUDA-core MaxSim");
       h->maxsim_algo = (int)value;
       return VX_OK;
     case VX_OPT_GRAPHS:
@@ -476,7 +483,7 @@ extern "C" vx_status vx_index_download(const vx_index* h, float* rows, int64_t r
 
 extern "C" vx_status vx_tokens_download(const vx_index* h, uint16_t* tok, int64_t blk0, int64_t n) {
   if (!h || (!tok && n > 0)) return fail(VX_ERR_INVALID, "null argument");
-  if (!h->tokens) return fail(VX_ERR_STATE, "index has no token store");
+  if (!h->tokens) return fail(VX_ERR_STATE, "index has no bf16 token store");
   if (blk0 < 0 || n < 0 || blk0 + n > h->desc.tok_blocks)
     return fail(VX_ERR_INVALID, "token blocks out of range");
   const size_t blk = (size_t)h->desc.tok_per_doc * h->desc.tok_dim;
@@ -489,18 +496,49 @@ extern "C" vx_status vx_tokens_download(const vx_index* h, uint16_t* tok, int64_
 
 extern "C" vx_status vx_tokens_synth(vx_index* h, uint64_t seed) {
   if (!h) return fail(VX_ERR_INVALID, "null handle");
-  if (!h->tokens) return fail(VX_ERR_STATE, "index has no token store");
+  if (!has_tokens(h)) return fail(VX_ERR_STATE, "index has no token store");
   CU_TRY(cudaSetDevice(h->device));
-  CU_TRY(vx::launch_synth_tokens(h->tokens, seed, 0, h->desc.tok_blocks, h->desc.tok_per_doc,
+  if (h->tokens32)  // the same generator, unrounded (the bf16 store holds its RNE)
+    CU_TRY(vx::launch_synth_rows(h->tokens32, seed, 0,
+                                 (int64_t)h->desc.tok_blocks * h->desc.tok_per_doc,
                                  h->desc.tok_dim, h->stream));
+  else
+    CU_TRY(vx::launch_synth_tokens(h->tokens, seed, 0, h->desc.tok_blocks, h->desc.tok_per_doc,
+                                   h->desc.tok_dim, h->stream));
   count_launch(h);
+  CU_TRY(cudaStreamSynchronize(h->stream));
+  return VX_OK;
+}
+
+extern "C" vx_status vx_tokens_upload_f32(vx_index* h, const float* tok, int64_t blk0, int64_t n) {
+  if (!h || (!tok && n > 0)) return fail(VX_ERR_INVALID, "null argument");
+  if (!h->tokens32) return fail(VX_ERR_STATE, "index has no fp32 token store");
+  if (blk0 < 0 || n < 0 || blk0 + n > h->desc.tok_blocks)
+    return fail(VX_ERR_INVALID, "token blocks out of range");
+  const size_t blk = (size_t)h->desc.tok_per_doc * h->desc.tok_dim;
+  CU_TRY(cudaSetDevice(h->device));
+  CU_TRY(cudaMemcpyAsync(h->tokens32 + blk0 * blk, tok, n * blk * 4, cudaMemcpyHostToDevice,
+                         h->stream));
+  CU_TRY(cudaStreamSynchronize(h->stream));
+  return VX_OK;
+}
+
+extern "C" vx_status vx_tokens_download_f32(const vx_index* h, float* tok, int64_t blk0, int64_t n) {
+  if (!h || (!tok && n > 0)) return fail(VX_ERR_INVALID, "null argument");
+  if (!h->tokens32) return fail(VX_ERR_STATE, "index has no fp32 token store");
+  if (blk0 < 0 || n < 0 || blk0 + n > h->desc.tok_blocks)
+    return fail(VX_ERR_INVALID, "token blocks out of range");
+  const size_t blk = (size_t)h->desc.tok_per_doc * h->desc.tok_dim;
+  CU_TRY(cudaSetDevice(h->device));
+  CU_TRY(cudaMemcpyAsync(tok, h->tokens32 + blk0 * blk, n * blk * 4, cudaMemcpyDeviceToHost,
+                         h->stream));
   CU_TRY(cudaStreamSynchronize(h->stream));
   return VX_OK;
 }
 
 extern "C" vx_status vx_tokens_upload(vx_index* h, const uint16_t* tok, int64_t blk0, int64_t n) {
   if (!h || (!tok && n > 0)) return fail(VX_ERR_INVALID, "null argument");
-  if (!h->tokens) return fail(VX_ERR_STATE, "index has no token store");
+  if (!h->tokens) return fail(VX_ERR_STATE, "index has no bf16 token store");
   if (blk0 < 0 || n < 0 || blk0 + n > h->desc.tok_blocks)
     return fail(VX_ERR_INVALID, "token blocks out of range");
   const size_t blk = (size_t)h->desc.tok_per_doc * h->desc.tok_dim;
@@ -644,7 +682,7 @@ extern "C" vx_status vx_search_rows(vx_index* h, const float* const* q_rows, int
 
 static vx_status host_maxsim(vx_index* h, const float* qtok, int32_t B, int32_t nq,
                              const int64_t* cand, int32_t C, float* out) {
-  if (!h->tokens) return fail(VX_ERR_STATE, "index has no token store");
+  if (!has_tokens(h)) return fail(VX_ERR_STATE, "index has no token store");
   if (B < 1 || B > h->desc.max_batch || C < 1 || C > h->desc.max_k)
     return fail(VX_ERR_INVALID, "B %d / C %d outside [1,%d] / [1,%d]", B, C, h->desc.max_batch,
                 h->desc.max_k);
@@ -680,7 +718,7 @@ static vx_status host_search_rescore(vx_index* h, const float* q, const float* c
                                      const float* qtok, const float* const* tok_rows, int32_t B,
                                      int32_t nq, int32_t k, int64_t* ids, float* ip, float* ms) {
   VX_TRY(check_batch(h, B, k));
-  if (!h->tokens) return fail(VX_ERR_STATE, "index has no token store");
+  if (!has_tokens(h)) return fail(VX_ERR_STATE, "index has no token store");
   if (nq < 1 || nq > h->desc.max_qtok) return fail(VX_ERR_INVALID, "nq %d", nq);
   if ((q_rows && !rows_ok(q_rows, B)) || (tok_rows && !rows_ok(tok_rows, B)))
     return fail(VX_ERR_INVALID, "null query row");

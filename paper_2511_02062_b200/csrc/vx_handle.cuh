@@ -76,7 +76,8 @@ struct vx_index {
   cudaStream_t stream = nullptr;
   int64_t row0 = 0, n_local = 0;
   float* docs = nullptr;
-  uint16_t* tokens = nullptr;
+  uint16_t* tokens = nullptr;    // bf16 doc-token store [T][Nd][d] (default)
+  float* tokens32 = nullptr;     // fp32 doc-token store (VX_FLAG_TOKENS_F32)
   CUtensorMap tmap_docs{};
   CUtensorMap tmap_tok{};
   uint16_t* docs16 = nullptr;    // bf16 shadow of the shard (coarse scan), may be null
@@ -194,6 +195,7 @@ struct vx_index {
 };
 
 static inline void count_launch(vx_index* h, int n = 1) { h->st.kernel_launches += n; }
+static inline bool has_tokens(const vx_index* h) { return h->tokens || h->tokens32; }
 
 // arm the device-side launch timers (start = max, everything else 0)
 static inline vx_status ktimer_reset(vx_index* h) {

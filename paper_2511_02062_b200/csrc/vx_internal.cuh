@@ -216,6 +216,8 @@ struct MaxSimArgs {
   int split = 0;         // TC kernel: query tokens as bf16 hi + lo pairs (fp32-faithful)
   const int64_t* cand;   // [B][C] global doc ids, -1 = skip
   const uint16_t* table; // [T][Nd][d] bf16 bits
+  const float* table32 = nullptr;  // or an fp32 store (VX_FLAG_TOKENS_F32): the CUDA-core
+                                   // kernel then keeps the query tokens in fp32 too
   int64_t T;
   int32_t B, nq, C, Nd, d;
   float* out;            // [B][C]
@@ -225,6 +227,8 @@ struct MaxSimArgs {
   KTimer* ktimer = nullptr;
 };
 cudaError_t launch_maxsim(const MaxSimArgs& a, cudaStream_t st);
+// the fp32 token store (a.table32; nq <= 32, Nd <= 128, d % 4 == 0): register-tiled exact fp32
+cudaError_t launch_maxsim_f32(const MaxSimArgs& a, cudaStream_t st);
 // fp32 -> bf16 hi plane (out) + lo plane (out + n): hi = RNE(v), lo = RNE(v - hi)
 cudaError_t launch_split_bf16(const float* in, uint16_t* out, int64_t n, cudaStream_t st);
 constexpr int kMaxSimSplitMaxNq = 64;  // hi/lo rows share the 128-row A tile

@@ -84,7 +84,7 @@ extern "C" vx_status vx_serve_trace_replicas(
       return fail(VX_ERR_INVALID, "replicas must share the index shape");
     if (cap < 1 || cap > h->desc.max_batch) return fail(VX_ERR_INVALID, "cap %d", cap);
     VX_TRY(check_batch(h, cap, k));
-    if (rescore && (!h->tokens || nq < 1 || nq > h->desc.max_qtok))
+    if (rescore && (!has_tokens(h) || nq < 1 || nq > h->desc.max_qtok))
       return fail(VX_ERR_INVALID, "query tokens need a token store and 1 <= nq <= max_qtok");
   }
   for (int64_t i = 1; i < n; ++i)

@@ -519,7 +519,7 @@ static vx_status local_topk(vx_index* h, const float* d_q, int B, int k, uint64_
 // Does the tensor-core MaxSim take the fp32-faithful hi/lo query split for nq tokens?
 // (AUTO / TC: yes when nq <= 64; VX_MAXSIM_TC_BF16Q: tokens rounded to bf16.)
 static bool maxsim_split(const vx_index* h, int nq) {
-  return (h->maxsim_algo == VX_MAXSIM_AUTO || h->maxsim_algo == VX_MAXSIM_TC) &&
+  return !h->tokens32 && (h->maxsim_algo == VX_MAXSIM_AUTO || h->maxsim_algo == VX_MAXSIM_TC) &&
          nq <= vx::kMaxSimSplitMaxNq &&
          vx::maxsim_tc_supported(nq, h->desc.tok_per_doc, h->desc.tok_dim);
 }
@@ -527,13 +527,14 @@ static bool maxsim_split(const vx_index* h, int nq) {
 vx_status run_maxsim(vx_index* h, const float* d_qtok, int B, int nq, const int64_t* d_cand,
                      int C, float* d_out, cudaStream_t st, int64_t id_lo, int64_t id_hi,
                      const uint16_t* d_qtok16) {
-  if (!h->tokens) return fail(VX_ERR_STATE, "index has no token store");
+  if (!has_tokens(h)) return fail(VX_ERR_STATE, "index has no token store");
   if (nq < 1 || nq > h->desc.max_qtok) return fail(VX_ERR_INVALID, "nq %d", nq);
   vx::MaxSimArgs a;
   a.qtok = d_qtok;
   a.qtok16 = d_qtok16;
   a.cand = d_cand;
   a.table = h->tokens;
+  a.table32 = h->tokens32;
   a.T = h->desc.tok_blocks;
   a.B = B;
   a.nq = nq;
@@ -546,16 +547,21 @@ vx_status run_maxsim(vx_index* h, const float* d_qtok, int B, int nq, const int6
   if (h->nranks > 1 && id_hi - id_lo < h->desc.n_docs)
     a.own_frac = (float)((double)(id_hi - id_lo) / (double)h->desc.n_docs);
   a.ktimer = h->d_ktimer + vx::KT_MAXSIM;
-  const bool tc = h->maxsim_algo != VX_MAXSIM_CC &&
+  const bool tc = !h->tokens32 && h->maxsim_algo != VX_MAXSIM_CC &&
                   vx::maxsim_tc_supported(nq, a.Nd, a.d);
   if ((h->maxsim_algo == VX_MAXSIM_TC || h->maxsim_algo == VX_MAXSIM_TC_BF16Q) && !tc)
     return fail(VX_ERR_UNSUPPORTED, "tensor-core MaxSim unsupported for nq=%d Nd=%d d=%d", nq, a.Nd, a.d);
   a.split = maxsim_split(h, nq) ? 1 : 0;
   a.lo_off = (int64_t)B * nq * a.d;  // the shard exchange's two-plane layout
-  if (tc)
+  if (h->tokens32) {
+    if (nq > 32 || a.Nd > 128 || (a.d & 3))
+      return fail(VX_ERR_UNSUPPORTED, "fp32 token store MaxSim: nq <= 32, Nd <= 128, d %% 4 == 0");
+    CU_TRY(vx::launch_maxsim_f32(a, st));
+  } else if (tc) {
     CU_TRY(vx::launch_maxsim_tc(&h->tmap_tok, a, st));
-  else
+  } else {
     CU_TRY(vx::launch_maxsim(a, st));
+  }
   count_launch(h);
   return VX_OK;
 }
@@ -618,6 +624,9 @@ vx_status core_topk(vx_index* h, const float* d_q, int B, int k, cudaStream_t st
   return VX_OK;
 }
 
+static vx_status gather_order(vx_index* h, int B, int k, int n, int64_t* d_ids, float* d_ip,
+                              float* d_ms, cudaStream_t st);
+
 // d_qtok: rank 0's query tokens (ignored on the shard ranks, which receive them)
 vx_status core_rescore(vx_index* h, const float* d_qtok, int B, int nq, int k,
                               int64_t* d_ids, float* d_ip, float* d_ms, cudaStream_t st) {
@@ -633,6 +642,21 @@ vx_status core_rescore(vx_index* h, const float* d_qtok, int B, int nq, int k,
   // tensor-core kernel (the fp32 bytes), else one bf16 plane (the kernels round fp32 tokens
   // with the same RNE anyway, so the scores are unchanged) — half the broadcast bytes
   const int64_t ntok = (int64_t)B * nq * h->desc.tok_dim;
+  if (h->tokens32) {
+    // fp32 token store: the fp32 query tokens travel as they are (the CUDA-core MaxSim keeps
+    // them unrounded), into every rank's d_qtok
+    if (root && d_qtok != h->d_qtok)
+      CU_TRY(cudaMemcpyAsync(h->d_qtok, d_qtok, (size_t)ntok * 4, cudaMemcpyDeviceToDevice, st));
+    NCCL_TRY(nccl().GroupStart());
+    NCCL_TRY(nccl().Broadcast(h->d_qtok, h->d_qtok, (size_t)ntok, ncclFloat32, 0, h->comm, st));
+    NCCL_TRY(nccl().Broadcast(h->d_ids, h->d_ids, (size_t)n, ncclInt64, 0, h->comm, st));
+    NCCL_TRY(nccl().GroupEnd());
+    if (root) CU_TRY(record_ext(h->pev[7], st));
+    VX_TRY(run_maxsim(h, h->d_qtok, B, nq, h->d_ids, k, h->d_ms, st, h->row0,
+                      h->row0 + h->n_local));
+    if (root) CU_TRY(record_ext(h->pev[8], st));
+    return gather_order(h, B, k, n, d_ids, d_ip, d_ms, st);
+  }
   const int64_t nplanes = maxsim_split(h, nq) ? 2 : 1;
   if (root) {
     if (nplanes == 2)
@@ -650,9 +674,14 @@ vx_status core_rescore(vx_index* h, const float* d_qtok, int B, int nq, int k,
   VX_TRY(run_maxsim(h, nullptr, B, nq, h->d_ids, k, h->d_ms, st, h->row0, h->row0 + h->n_local,
                     h->d_qtok16));
   if (root) CU_TRY(record_ext(h->pev[8], st));
-  // every winner has one owner (the others hold -inf): the shards' score arrays go to rank 0
-  // in one grouped send / receive step and the order kernel takes their max — an NCCL
-  // max-reduce walked its ring / tree in G - 1 dependent steps (0.13 ms at G = 4)
+  return gather_order(h, B, k, n, d_ids, d_ip, d_ms, st);
+}
+
+// every winner has one owner (the others hold -inf): the shards' score arrays go to rank 0 in
+// one grouped send / receive step and the order kernel takes their max (no NCCL max-reduce)
+static vx_status gather_order(vx_index* h, int B, int k, int n, int64_t* d_ids, float* d_ip,
+                              float* d_ms, cudaStream_t st) {
+  const bool root = h->rank == 0;
   const int G = h->nranks;
   float* ms_all = reinterpret_cast<float*>(h->d_recv);  // [G][B][k] on rank 0 (phase 1 is done)
   NCCL_TRY(nccl().GroupStart());
@@ -922,7 +951,7 @@ extern "C" vx_status vx_search_rescore_dev(vx_index* h, const float* d_q, const 
                                            float* d_ip, float* d_ms, void* stream) {
   if (!h || !d_q || !d_qtok || !d_ids || !d_ip || !d_ms) return fail(VX_ERR_INVALID, "null argument");
   VX_TRY(check_batch(h, B, k));
-  if (!h->tokens) return fail(VX_ERR_STATE, "index has no token store");
+  if (!has_tokens(h)) return fail(VX_ERR_STATE, "index has no token store");
   if (nq < 1 || nq > h->desc.max_qtok) return fail(VX_ERR_INVALID, "nq %d", nq);
   CU_TRY(cudaSetDevice(h->device));
   cudaStream_t st = pick_stream(h, stream);
@@ -946,7 +975,7 @@ extern "C" vx_status vx_prepare(vx_index* h, int32_t op, int32_t k, int32_t nq, 
   if (op != VX_PREPARE_SEARCH && op != VX_PREPARE_RESCORE) return fail(VX_ERR_INVALID, "op %d", op);
   VX_TRY(check_batch(h, b_max, k));
   const bool rescore = op == VX_PREPARE_RESCORE;
-  if (rescore && (!h->tokens || nq < 1 || nq > h->desc.max_qtok))
+  if (rescore && (!has_tokens(h) || nq < 1 || nq > h->desc.max_qtok))
     return fail(VX_ERR_INVALID, "rescore needs a token store and 1 <= nq <= max_qtok");
   if (!h->use_graphs) return VX_OK;
   if (h->nranks > 1 && h->rank != 0)

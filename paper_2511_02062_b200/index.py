@@ -104,7 +104,17 @@ class Index:
         check(self.lib.vx_index_download(self._h, out.ctypes.data_as(FP), row0, n))
         return out
 
+    @property
+    def tokens_f32(self) -> bool:
+        """The token store is fp32 (VX_FLAG_TOKENS_F32), else bf16."""
+        return bool(self.desc.flags & _lib.VX_FLAG_TOKENS_F32)
+
     def tokens_download(self, blk0: int, n: int) -> np.ndarray:
+        """Token blocks [n][Nd][d]: uint16 bf16 bits (bf16 store) or float32 (fp32 store)."""
+        if self.tokens_f32:
+            out = np.empty((n, self.tok_per_doc, self.tok_dim), np.float32)
+            check(self.lib.vx_tokens_download_f32(self._h, out.ctypes.data_as(FP), blk0, n))
+            return out
         out = np.empty((n, self.tok_per_doc, self.tok_dim), np.uint16)
         check(self.lib.vx_tokens_download(self._h, out.ctypes.data_as(HP), blk0, n))
         return out
@@ -112,8 +122,13 @@ class Index:
     def tokens_synth(self, seed: int = 45) -> None:
         check(self.lib.vx_tokens_synth(self._h, seed))
 
-    def tokens_upload(self, tokens_bf16: np.ndarray, blk0: int = 0) -> None:
-        t = np.ascontiguousarray(tokens_bf16, dtype=np.uint16)
+    def tokens_upload(self, tokens: np.ndarray, blk0: int = 0) -> None:
+        """bf16 store: uint16 bf16 bits; fp32 store (VX_FLAG_TOKENS_F32): float32 values."""
+        if self.tokens_f32:
+            t = np.ascontiguousarray(tokens, dtype=np.float32)
+            check(self.lib.vx_tokens_upload_f32(self._h, t.ctypes.data_as(FP), blk0, t.shape[0]))
+            return
+        t = np.ascontiguousarray(tokens, dtype=np.uint16)
         check(self.lib.vx_tokens_upload(self._h, t.ctypes.data_as(HP), blk0, t.shape[0]))
 
     # -- host-buffer operators ------------------------------------------------------------

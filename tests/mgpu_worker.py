@@ -85,8 +85,42 @@ def main() -> int:
         idx.shard_serve()
         print(f"rank{rank} served {idx.stats()['batches']} batches", flush=True)
     dist.barrier()
-    dist.destroy_process_group()
     idx.close()
+    # the fp32 token store across the shards (its phase 2 broadcasts the fp32 query tokens and
+    # every owner runs the exact CUDA-core MaxSim): a small second index
+    N2, T2 = 50_000, 61
+    idx2 = vx.Index(N2, D, device=local, n_shards=world, shard=rank, tok_per_doc=128, tok_dim=128,
+                    tok_blocks=T2, max_batch=16, max_k=16, max_qtok=nq,
+                    flags=vx.VX_FLAG_TOKENS_F32)
+    idx2.synth(42)
+    idx2.tokens_synth(45)
+    uid2 = [vx.Index.comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid2, src=0)
+    idx2.comm_init(uid2[0], world, rank)
+    if rank == 0:
+        import vxoracle as o
+        from paper_2511_02062_b200 import synth
+        from stagecheck import check_stage
+        Q2 = synth.rows(43, 500, 5, D)
+        qt2 = synth.query_tokens(5, nq, 128, seed=47)
+        ids2, ip2, ms2 = idx2.search_rescore(Q2, qt2, 10)
+        idx2.shard_stop()
+        tab32 = o.synth_rows(45, 0, T2 * 128, 128).reshape(T2, 128, 128)
+        rid2, rsc2 = o.flat_topk(o.synth_rows(42, 0, N2, D), Q2, 10, mode=1)
+        try:
+            check_stage(ids2, ip2, ms2, rid2, rsc2, o.maxsim(qt2, rid2, tab32, mode=o.F64))
+            want = o.maxsim(qt2, ids2, tab32, mode=o.F32)
+            ok &= bool(np.array_equal(ms2.astype(np.float64), want.astype(np.float32).astype(np.float64)))
+            print(f"rank0 fp32 token store: ok={ok}", flush=True)
+        except AssertionError as e:
+            print(f"rank0 fp32 token store check failed: {e!r}", flush=True)
+            ok = False
+        print(f"rank0 world={world} parity={'ok' if ok else 'FAIL'} (fp32 store)", flush=True)
+    else:
+        idx2.shard_serve()
+    dist.barrier()
+    dist.destroy_process_group()
+    idx2.close()
     return 0 if ok else 1
 
 

@@ -16,7 +16,7 @@ ROOT = Path(__file__).resolve().parents[1]
 
 def declared_symbols() -> set[str]:
     text = (ROOT / "include" / "vortex_b200.h").read_text()
-    return set(re.findall(r"\b(vx_[a-z_]+)\s*\(", text))
+    return set(re.findall(r"\b(vx_[a-z0-9_]+)\s*\(", text))
 
 
 def test_exports_every_declared_symbol(vxlib):

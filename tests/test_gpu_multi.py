@@ -34,4 +34,5 @@ def test_sharded_stage_matches_oracle(world, graphs):
     sys.stdout.write(r.stdout[-3000:])
     sys.stderr.write(r.stderr[-3000:])
     assert r.returncode == 0
-    assert "parity=ok" in r.stdout
+    assert "parity=ok" in r.stdout and "parity=FAIL" not in r.stdout
+    assert "(fp32 store)" in r.stdout  # the fp32 token store ran across the shards too
