@@ -91,3 +91,23 @@ def test_fp32_store_refuses_tensor_core_maxsim(vx):
     with _index(vx) as idx:
         with pytest.raises(vx.VxError):
             idx.set_option(vx.VX_OPT_MAXSIM, vx.VX_MAXSIM_TC)
+
+
+@pytest.mark.parametrize("nq,nd,td", [(5, 64, 64), (32, 100, 128), (17, 128, 96)])
+def test_fp32_store_partial_tiles(vx, oracle, nq, nd, td):
+    """Query-token counts that are not a multiple of the 4-token register tile, doc blocks
+    shorter than the 128-row tile, other token dims: still bit-identical."""
+    from paper_2511_02062_b200 import synth
+    N2, T2, B = 20_000, 37, 6
+    table = oracle.synth_rows(45, 0, T2 * nd, td).reshape(T2, nd, td)
+    qt = synth.query_tokens(B, nq, td, seed=81)
+    rng = np.random.default_rng(nq)
+    cand = np.stack([rng.choice(N2, 40, replace=False) for _ in range(B)]).astype(np.int64)
+    with vx.Index(N2, 256, tok_per_doc=nd, tok_dim=td, tok_blocks=T2, max_batch=B, max_k=64,
+                  max_qtok=32, flags=vx.VX_FLAG_TOKENS_F32) as idx:
+        idx.synth(42)
+        idx.tokens_synth(45)
+        assert np.array_equal(idx.tokens_download(0, T2), table)
+        ms = idx.maxsim(qt, cand)
+    want = oracle.maxsim(qt, cand, table, mode=oracle.F32)
+    assert np.array_equal(ms.astype(np.float64), want.astype(np.float32).astype(np.float64))
