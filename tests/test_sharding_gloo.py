@@ -183,7 +183,7 @@ def _tau_worker(rank: int, world: int, port: int, q) -> None:
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_gloo_sharded_threshold_prunes_and_stays_exact(oracle, world):
     import multiprocessing as mp
     ctx = mp.get_context("spawn")
