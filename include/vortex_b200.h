@@ -151,6 +151,8 @@ typedef struct vx_stats {
   double kt_last_us[10];       /* [scan, sample, f32, maxsim, re-rank] x [start, end] of each
                                   kind's LAST launch, us after the earliest of those starts
                                   (both 0: no launch) — the gaps between a stage's kernels */
+  uint64_t kt_origin_ns;       /* %globaltimer (ns) of that earliest start: the origin of
+                                  kt_last_us, to place the kernels against other device stamps */
 } vx_stats;
 
 int32_t vx_abi_version(void);

@@ -53,7 +53,8 @@ class Stats(C.Structure):
                 ("cert_level2", C.c_uint64), ("host_staged_bytes", C.c_uint64),
                 ("kt_launches", C.c_uint64 * 4), ("kt_ms", C.c_double * 4), ("kt_sm_mhz", C.c_double * 4),
                 ("phase_detail_ms", C.c_float * 6), ("kt_rerank_launches", C.c_uint64),
-                ("kt_rerank_ms", C.c_double), ("kt_last_us", C.c_double * 10)]
+                ("kt_rerank_ms", C.c_double), ("kt_last_us", C.c_double * 10),
+                ("kt_origin_ns", C.c_uint64)]
 
 
 P = C.c_void_p

@@ -609,16 +609,35 @@ __global__ void __launch_bounds__(256, 2)
     return;
   }
   if (trc && threadIdx.x == 0) trc[4] = gtimer_ns();
-  // L = the head's minimum exact score (a bound on the exact k-th once k heads exist)
+  // L = the head's minimum exact score (a bound on the exact k-th once k heads exist); also
+  // its smallest key, for the final selection
   float m = INFINITY;
-  for (int i = threadIdx.x; i < kh; i += blockDim.x)
+  uint64_t mk = ~0ull;
+  for (int i = threadIdx.x; i < kh; i += blockDim.x) {
     m = fminf(m, keys[i] ? vx_key_score(keys[i]) : -INFINITY);
-  for (int o = 16; o > 0; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) s_min[threadIdx.x >> 5] = m;
+    mk = keys[i] < mk ? keys[i] : mk;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const uint64_t y = shfl_xor_u64(mk, o);
+    mk = y < mk ? y : mk;
+  }
+  __shared__ uint64_t s_mk[8];
+  if ((threadIdx.x & 31) == 0) {
+    s_min[threadIdx.x >> 5] = m;
+    s_mk[threadIdx.x >> 5] = mk;
+  }
   __syncthreads();
   float L = s_min[0];
-  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) L = fminf(L, s_min[w]);
+  mk = s_mk[0];
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+    L = fminf(L, s_min[w]);
+    mk = s_mk[w] < mk ? s_mk[w] : mk;
+  }
   if (kh < k) L = -INFINITY;
+  // the final top-k are all >= the smallest head key when the head holds k real keys (k keys
+  // are >= it); otherwise every real key stays in the running
+  const uint64_t sel_floor = (kh >= k && mk != 0ull) ? mk : 1ull;
   const float tb = tau ? tau[b] : -INFINITY;
   const float lim = fmaxf(L, tb) - E;
   int kpe = kp;  // candidates re-ranked: the prefix with cscale c >= lim
@@ -644,10 +663,34 @@ __global__ void __launch_bounds__(256, 2)
       s_fail = 1;
   }
   __syncthreads();
-  // sort the exact keys (kp is a power of two <= 1024; registers + shuffles, vx_sort.cuh).
-  // (A radix top-k of the exact keys instead was ~2 us faster per CTA at k' = 1024 but, as a
-  // second call site of the merge, took the kernel from 80 to 173 registers: one CTA per SM.)
-  block_sort_desc(keys, kp);
+  // the exact top-k: the keys >= sel_floor (the k head keys and the few tail keys that beat
+  // the head's worst: ~k + a few) compacted and ranked into keys[0, k) — a bitonic sort of all
+  // k' keys took 8.8 us per CTA at k' = 1024 (VX_DEBUG_RERANK_TRACE); the sort remains the
+  // fallback when more than 2 x 256 survive.  (A radix top-k instead, as a second call site of
+  // the merge, took the kernel from 80 to 173 registers: one CTA per SM.)
+  {
+    __shared__ int s_cnt;
+    uint64_t* surv = reinterpret_cast<uint64_t*>(rowbuf);  // the staging is drained
+    constexpr int kSurvCap = 512;
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < kp; i += blockDim.x) {
+      const uint64_t key = keys[i];
+      if (key >= sel_floor) {
+        const int slot = atomicAdd(&s_cnt, 1);
+        if (slot < kSurvCap) surv[slot] = key;
+      }
+    }
+    __syncthreads();
+    const int C = s_cnt;
+    if (C <= kSurvCap && C <= 2 * (int)blockDim.x) {
+      rank_topk_block(surv, C, k, [&](int r, uint64_t key) { keys[r] = key; });
+      for (int i = C + (int)threadIdx.x; i < k; i += blockDim.x) keys[i] = 0ull;
+      __syncthreads();
+    } else {
+      block_sort_desc(keys, kp);
+    }
+  }
   if (trc && threadIdx.x == 0) trc[6] = gtimer_ns();
   // seeded scan (ScanTcArgs::seed): the lists also dropped every document whose coarse score
   // is below the seed, so a document outside the candidates has coarse score
@@ -1041,6 +1084,7 @@ cudaError_t launch_rerank(const float* docs, const float* q, int D, uint64_t* ca
   }
   // L2 prefetch distance in items beyond the staging window (packed into nbuf's high bits)
   const int PF = head_all ? 0 : std::min(env_pf >= 0 ? env_pf : 0, 15);
+  smem = std::max(smem, base + (size_t)512 * 8);  // the final selection's survivors
   // the fused merge stages the lists and its selection in the row buffers
   if (fz.mlists)
     smem = std::max(smem, base + (size_t)(((fz.mM + 1) & ~1) + kRerankMergeSel + kRerankMergeFilter) * 8);

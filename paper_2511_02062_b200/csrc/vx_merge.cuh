@@ -42,10 +42,11 @@ constexpr int kMergeFilterKeys = 512;  // standalone merge: the sorted-list filt
 // the shards' top-k lists): a filter first.  With S = the (j+1)-th key of every list and
 // m (j+1) >= k, the m-th largest of S, T0, has at least m (j+1) >= k keys at or above it, so
 // the k best keys are all >= T0; binary searches count each list's keys >= T0 and, when those
-// (C) fit fbuf (fcap keys, a power of two), one register sort of them gives the answer — no
-// radix passes (each pass is a chain of barriers and atomics: 2 passes + collection + sort took
-// ~17 K cycles for 2368 keys -> 64, profiles/microbench/merge_bench.cu).  Otherwise (C > fcap,
-// or T0 = 0: short lists) the radix select below runs as before.
+// (C) fit fbuf (fcap keys) and two keys per thread, ranking them gives the answer in order —
+// no radix passes (each pass is a chain of barriers and atomics: 2 passes + collection + sort
+// took ~17 K cycles for 2368 keys -> 64) and no sort (T0 and the C keys were two bitonic sorts:
+// 5 K + 3.7 K of the filter's 13.6 K cycles; profiles/microbench/merge_bench.cu).  Otherwise
+// (C too large, or T0 = 0: short lists) the radix select below runs as before.
 static __device__ __noinline__ void merge_topk_block(const uint64_t* __restrict__ L, int M, int k, int64_t id_base,
                                  uint64_t* __restrict__ out_keys, int64_t* __restrict__ out_ids,
                                  float* __restrict__ out_scores, size_t row, int64_t ldout,
@@ -74,14 +75,20 @@ static __device__ __noinline__ void merge_topk_block(const uint64_t* __restrict_
     const int j1 = (k + P - 1) / P;  // j + 1
     if (j1 <= KC) {
       const int m = (k + j1 - 1) / j1;  // <= P
-      int n2 = 16;
-      while (n2 < P) n2 <<= 1;
-      for (int i = threadIdx.x; i < n2; i += blockDim.x)
-        fbuf[i] = i < P ? L[(size_t)i * KC + (j1 - 1)] : 0ull;
+      // t0 = the m-th largest of the lists' (j+1)-th keys, by rank (distinct documents:
+      // distinct keys; 0 when fewer than m lists reach j + 1 keys)
+      __shared__ uint64_t s_t0;
+      if (threadIdx.x == 0) s_t0 = 0ull;
+      for (int i = threadIdx.x; i < P; i += blockDim.x) fbuf[i] = L[(size_t)i * KC + (j1 - 1)];
       __syncthreads();
-      block_sort_desc(fbuf, n2);
-      const uint64_t t0 = fbuf[m - 1];
+      MERGE_STAMP();
+      if ((int)threadIdx.x < P) {
+        const uint64_t v = fbuf[threadIdx.x];
+        if (v != 0ull && rank_desc(fbuf, P, v) == m - 1) s_t0 = v;
+      }
       __syncthreads();
+      const uint64_t t0 = s_t0;
+      MERGE_STAMP();
       if (t0 != 0ull) {
         // keys >= t0 in list p (descending: a prefix), by binary search; block prefix sum
         int c = 0;
@@ -103,27 +110,24 @@ static __device__ __noinline__ void merge_topk_block(const uint64_t* __restrict_
         }
         if (lane == 31) s_wsum[warp] = x;
         __syncthreads();
+        MERGE_STAMP();
         int base = 0, C = 0;
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
           const int v = s_wsum[w];
           if (w < warp) base += v;
           C += v;
         }
-        int n3 = 16;
-        while (n3 < C || n3 < k) n3 <<= 1;
-        if (n3 <= fcap) {
+        // the C (>= k) survivors, all nonzero and distinct: ranked straight into the outputs
+        if (C <= fcap && C <= 2 * (int)blockDim.x) {
           const int off = base + x - c;  // exclusive prefix of this list
           if (c) {
             const uint64_t* lp = L + (size_t)threadIdx.x * KC;
             for (int i = 0; i < c; ++i) fbuf[off + i] = lp[i];
           }
-          for (int i = C + (int)threadIdx.x; i < n3; i += blockDim.x) fbuf[i] = 0ull;
           __syncthreads();
-          block_sort_desc(fbuf, n3);
           MERGE_STAMP();
-          for (int i = threadIdx.x; i < k; i += blockDim.x) {
-            const uint64_t key = fbuf[i];
-            const size_t o = row * ldout + i;
+          auto emit = [&](int r, uint64_t key) {
+            const size_t o = row * ldout + r;
             if (key == 0ull) {
               if (out_keys) out_keys[o] = 0ull;
               if (out_ids) out_ids[o] = -1;
@@ -135,7 +139,10 @@ static __device__ __noinline__ void merge_topk_block(const uint64_t* __restrict_
               if (out_ids) out_ids[o] = gid;
               if (out_scores) out_scores[o] = vx_key_score(key);
             }
-          }
+          };
+          rank_topk_block(fbuf, C, k, emit);
+          for (int i = C + (int)threadIdx.x; i < k; i += blockDim.x) emit(i, 0ull);
+          MERGE_STAMP();
           __syncthreads();
           MERGE_STAMP();
           return;

@@ -128,4 +128,36 @@ __device__ __forceinline__ void block_sort_desc(uint64_t* keys, int n) {
   else sort_shared_e<8>(keys, n);
 }
 
+// Rank of v among the n keys src[0, n) (shared memory): how many are strictly larger.  One
+// broadcast load per key, no barrier — a bitonic sort of a few hundred keys is a chain of
+// ~40 dependent shuffle/compare stages (5 K cycles for 256 keys, 3.7 K for ~150:
+// profiles/microbench/merge_bench.cu), while ranking them all is ~n independent compares per
+// thread.
+__device__ __forceinline__ int rank_desc(const uint64_t* __restrict__ src, int n, uint64_t v) {
+  int r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+  int j = 0;
+  for (; j + 4 <= n; j += 4) {
+    r0 += src[j] > v;
+    r1 += src[j + 1] > v;
+    r2 += src[j + 2] > v;
+    r3 += src[j + 3] > v;
+  }
+  for (; j < n; ++j) r0 += src[j] > v;
+  return r0 + r1 + r2 + r3;
+}
+
+// Rank selection: src[0, n) holds n DISTINCT nonzero keys (shared memory, n <= 2 * blockDim.x);
+// emit(r, key) is called for each of the min(n, k) largest with its descending position r.
+// Whole block or any subset of it (no barrier inside: the caller orders src's writes before
+// and emit's results after).
+template <typename Emit>
+__device__ __forceinline__ void rank_topk_block(const uint64_t* __restrict__ src, int n, int k,
+                                                Emit&& emit) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint64_t v = src[i];
+    const int r = rank_desc(src, n, v);
+    if (r < k) emit(r, v);
+  }
+}
+
 }  // namespace vx

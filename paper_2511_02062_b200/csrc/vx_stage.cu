@@ -1075,6 +1075,7 @@ extern "C" vx_status vx_sync(vx_index* h) {
     h->st.kt_last_us[2 * i] = on ? (double)(kt[i].last_start - t0) * 1e-3 : 0.0;
     h->st.kt_last_us[2 * i + 1] = on ? (double)(kt[i].last_end - t0) * 1e-3 : 0.0;
   }
+  h->st.kt_origin_ns = t0 != ~0ull ? t0 : 0ull;
   cudaGetLastError();
   return VX_OK;
 }
