@@ -49,6 +49,9 @@ cudaError_t launch_synth_rows(float* out, uint64_t seed, int64_t row0, int64_t n
 // fp32 -> bf16 (RNE on the bit pattern, vx_synth.h): the coarse-scan shadow of the index
 // and the per-batch query copy.  8 elements per thread (two 16-byte loads, one 16-byte store).
 __global__ void to_bf16_kernel(const float4* __restrict__ in, uint4* __restrict__ out, int64_t n8) {
+  // the scan behind a query conversion is its programmatic dependent (ScanTcArgs::pdl): let it
+  // launch now — it waits for this grid's completion before reading anything
+  asm volatile("griddepcontrol.launch_dependents;" :::);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8;
        i += (int64_t)gridDim.x * blockDim.x) {
     const float4 a = in[2 * i], b = in[2 * i + 1];
@@ -168,6 +171,7 @@ cudaError_t launch_to_i8_shadow(const float* in, int64_t n, int D, int8_t* out,
 __global__ void rows_to_i8_kernel(const float* __restrict__ in, int D,
                                   const float* __restrict__ colscale, int8_t* __restrict__ out,
                                   float* __restrict__ scales) {
+  asm volatile("griddepcontrol.launch_dependents;" :::);  // as to_bf16_kernel
   __shared__ float s_m[32];
   const float* x = in + (size_t)blockIdx.x * D;
   float m = 0.0f;

@@ -66,6 +66,8 @@ struct ScanTcArgs {
   uint64_t* trace = nullptr;  // timing experiments only (VX_DEBUG_SCAN_TRACE): per CTA 8
                              // %globaltimer stamps (entry, setup done, first stage landed, last
                              // MMA issued, epilogue done, lists written)
+  int32_t pdl = 0;   // launched as a programmatic dependent of the query conversion (single-CTA
+                     // kernel): the prologue overlaps it; every thread waits before its roles
   int32_t rep = 1;   // single-CTA kernel, TD = 256, B <= 64: each query occupies rep = 128 /
                      // a_rows rows of the A tile, replica r selects over columns
                      // [r TD/rep, (r+1) TD/rep) — rep x the epilogue lanes on a small batch

@@ -244,6 +244,9 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
       a.part = sample ? sample_lists + (size_t)g0 * grid * vx::kSampleKC : h->d_part + (size_t)g0 * ldp;
       a.seed = (seeded && !sample) ? h->d_seedk + (size_t)g0 * kSeedLd + (kSeedM - 1) : nullptr;
       a.seed_ld = kSeedLd;
+      // the first pass after the query conversion launches as its programmatic dependent
+      static const bool no_scan_pdl = getenv("VX_DEBUG_NO_SCAN_PDL") != nullptr;  // A/B only
+      a.pdl = (!no_scan_pdl && !on_pairs && g0 == 0 && (sample || !seeded) && (bf16 || i8)) ? 1 : 0;
       // 128-document pair tiles (QG = 2) load 64-row document boxes per CTA
       const CUtensorMap* tx;
       if (QG == 2)

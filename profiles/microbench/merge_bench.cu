@@ -11,6 +11,10 @@
 #include "../../paper_2511_02062_b200/csrc/topk.cu"
 
 __global__ void empty_kernel() {}
+__global__ void flush_kernel(int4* p, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    p[i] = make_int4((int)i, 0, 0, 0);
+}
 
 int main() {
   struct Case { int B, P, KC, k; };
@@ -56,6 +60,24 @@ int main() {
     cudaEventSynchronize(z);
     float ms = 0;
     cudaEventElapsedTime(&ms, a, z);
+    {  // one launch on COLD lists (L2 flushed: the re-rank reads lists the scan just wrote,
+       // partly evicted by its document stream)
+      static int4* fl = nullptr;
+      const size_t nfl = (256u << 20) / 16;
+      if (!fl) cudaMalloc(&fl, nfl * 16);
+      float best = 1e9f;
+      for (int r = 0; r < 5; ++r) {
+        flush_kernel<<<1184, 256, 0, st>>>(fl, nfl);
+        cudaEventRecord(a, st);
+        vx::launch_merge_topk(din, c.B, M, c.k, 0, dout, nullptr, nullptr, st, nullptr, 0, 0, fP, fKC);
+        cudaEventRecord(z, st);
+        cudaEventSynchronize(z);
+        float m1 = 0;
+        cudaEventElapsedTime(&m1, a, z);
+        best = m1 < best ? m1 : best;
+      }
+      printf("   cold (L2 flushed) single launch: %.2f us\n", best * 1e3);
+    }
     {  // the outputs against a host sort of each query's keys
       std::vector<uint64_t> got((size_t)c.B * c.k);
       cudaMemcpy(got.data(), dout, got.size() * 8, cudaMemcpyDeviceToHost);
