@@ -402,13 +402,17 @@ VX_DEV uint64_t gtimer_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// every CTA's start; the launch's is their minimum (a reduction, no return)
 VX_DEV void ktimer_begin(KTimer* t, uint64_t& c0, uint64_t& g0) {
   if (!t || threadIdx.x != 0) return;
   g0 = gtimer_ns();
   c0 = clock64();
   atomicMin(&t->start, (unsigned long long)g0);
 }
-// after the CTA's last work (its final barrier)
+// after the CTA's last work (its final barrier).  The end stamp is a reduction (no return);
+// the arrival is ONE acquire-release atomic (it publishes this CTA's stamp and, for the last
+// CTA, acquires everyone's); the last CTA's fold issues its two loads together and only
+// reductions / relaxed stores after them.
 VX_DEV void ktimer_end(KTimer* t, uint64_t c0, uint64_t g0) {
   if (!t || threadIdx.x != 0) return;
   const uint64_t g1 = gtimer_ns(), c1 = clock64();
@@ -417,18 +421,21 @@ VX_DEV void ktimer_end(KTimer* t, uint64_t c0, uint64_t g0) {
     atomicAdd(&t->clk_cycles, (unsigned long long)(c1 - c0));
     atomicAdd(&t->clk_ns, (unsigned long long)(g1 - g0));
   }
-  __threadfence();
   const unsigned long long n = (unsigned long long)gridDim.x * gridDim.y * gridDim.z;
-  if (atomicAdd(&t->done, 1ull) == n - 1) {  // last CTA: fold this launch, re-arm the slot
-    __threadfence();
-    const unsigned long long s = atomicAdd(&t->start, 0ull), e = atomicAdd(&t->end, 0ull);
+  unsigned long long prev;
+  asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(prev) : "l"(&t->done) : "memory");
+  if (prev == n - 1) {  // last CTA: fold this launch, re-arm the slot
+    unsigned long long s, e;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%2];\n\tld.relaxed.gpu.global.u64 %1, [%3];"
+                 : "=l"(s), "=l"(e) : "l"(&t->start), "l"(&t->end) : "memory");
     atomicAdd(&t->total_ns, e - s);
     atomicAdd(&t->launches, 1ull);
-    atomicExch(&t->last_start, s);
-    atomicExch(&t->last_end, e);
-    atomicExch(&t->start, ~0ull);
-    atomicExch(&t->end, 0ull);
-    atomicExch(&t->done, 0ull);
+    asm volatile(
+        "st.relaxed.gpu.global.u64 [%0], %1;\n\tst.relaxed.gpu.global.u64 [%2], %3;\n\t"
+        "st.relaxed.gpu.global.u64 [%4], %5;\n\tst.relaxed.gpu.global.u64 [%6], %7;\n\t"
+        "st.relaxed.gpu.global.u64 [%8], %9;"
+        :: "l"(&t->last_start), "l"(s), "l"(&t->last_end), "l"(e), "l"(&t->start), "l"(~0ull),
+           "l"(&t->end), "l"(0ull), "l"(&t->done), "l"(0ull) : "memory");
   }
 }
 

@@ -21,6 +21,13 @@
 #include "vx_handle.cuh"
 
 // Exact path: K1 scan + merge: d_q [B][D] -> keys (global ids) / ids / scores [B][k]
+// the device-side launch timer of kind i (VX_DEBUG_NO_KTIMER: none — A/B timing of the
+// timers' own cost only)
+static vx::KTimer* ktimer_of(vx_index* h, int i) {
+  static const bool off = getenv("VX_DEBUG_NO_KTIMER") != nullptr;
+  return off ? nullptr : h->d_ktimer + i;
+}
+
 static vx_status local_topk_f32(vx_index* h, const float* d_q, int B, int k, uint64_t* keys,
                                 int64_t* ids, float* scores, cudaStream_t st,
                                 const int* d_count = nullptr) {
@@ -50,7 +57,7 @@ static vx_status local_topk_f32(vx_index* h, const float* d_q, int B, int k, uin
     a.part = h->d_part + (size_t)g0 * grid * kcap;
     a.d_count = d_count;
     a.g0 = g0;
-    a.ktimer = d_count ? nullptr : h->d_ktimer + vx::KT_F32;
+    a.ktimer = d_count ? nullptr : ktimer_of(h, vx::KT_F32);
     if (g0 == 0 && !d_count) CU_TRY(record_scan_ev(h, h->tev[0], st));
     CU_TRY(vx::launch_scan_f32(bucket, &h->tmap_docs, a, grid, smem, st));
     count_launch(h);
@@ -240,7 +247,7 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
       a.dbg_no_select = h->dbg_tc_bits;  // timing experiments only (VX_DEBUG_TC_NOSELECT)
       a.kc = sample ? vx::kSampleKC : 0;
       a.rep = rep;
-      a.ktimer = h->d_ktimer + (sample ? vx::KT_SAMPLE : vx::KT_SCAN);
+      a.ktimer = ktimer_of(h, sample ? vx::KT_SAMPLE : vx::KT_SCAN);
       a.part = sample ? sample_lists + (size_t)g0 * grid * vx::kSampleKC : h->d_part + (size_t)g0 * ldp;
       a.seed = (seeded && !sample) ? h->d_seedk + (size_t)g0 * kSeedLd + (kSeedM - 1) : nullptr;
       a.seed_ld = kSeedLd;
@@ -389,7 +396,7 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
       while (r1 < B && lists_per_query(r1) == P) r1 += GS;
       r1 = std::min(r1, B);
       vx::RerankFuse fz;
-      fz.ktimer = h->d_ktimer + vx::KT_RERANK;
+      fz.ktimer = ktimer_of(h, vx::KT_RERANK);
       // G > 2 shards: each re-scores 2k/G head rows before the tau exchange instead of k (the
       // union of G x 2k/G head scores still holds k distinct exact scores, so tau stays a lower
       // bound of the global k-th; the local bound L is dropped and tau alone prunes the tail)
@@ -549,7 +556,7 @@ vx_status run_maxsim(vx_index* h, const float* d_qtok, int B, int nq, const int6
   a.id_hi = id_hi;
   if (h->nranks > 1 && id_hi - id_lo < h->desc.n_docs)
     a.own_frac = (float)((double)(id_hi - id_lo) / (double)h->desc.n_docs);
-  a.ktimer = h->d_ktimer + vx::KT_MAXSIM;
+  a.ktimer = ktimer_of(h, vx::KT_MAXSIM);
   const bool tc = !h->tokens32 && h->maxsim_algo != VX_MAXSIM_CC &&
                   vx::maxsim_tc_supported(nq, a.Nd, a.d);
   if ((h->maxsim_algo == VX_MAXSIM_TC || h->maxsim_algo == VX_MAXSIM_TC_BF16Q) && !tc)

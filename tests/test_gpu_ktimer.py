@@ -1,0 +1,46 @@
+"""The device-side launch timers behind the bench's kernel times (vx_stats.kt_*: every launch,
+inside CUDA graphs, folded by each launch's last CTA): launch counts, plausible durations and
+clocks, and the last step's kernel order.  Runs on a B200."""
+from __future__ import annotations
+
+import time
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("graphs", [0, 1])
+def test_ktimers_count_and_order(vxlib, graphs):
+    import paper_2511_02062_b200 as vx
+    from paper_2511_02062_b200 import synth
+    N, D, B, k, steps = 100_000, 768, 16, 10, 7
+    Q = synth.queries(B, D)
+    with vx.Index(N, D, max_batch=B, max_k=k) as idx:
+        idx.synth(42)
+        idx.set_option(vx.VX_OPT_GRAPHS, graphs)
+        for _ in range(3):
+            idx.search(Q, k)
+        idx.sync()
+        idx.reset_stats()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            idx.search(Q, k)
+        idx.sync()
+        wall_ms = (time.perf_counter() - t0) * 1e3
+        s = idx.stats()
+    # one tensor-core scan and one re-rank per batch, no sample pass (100K rows), no MaxSim
+    assert s["kt_launches"][0] == steps
+    assert s["kt_launches"][3] == 0
+    assert s["kt_rerank_launches"] == steps
+    scan_ms, rr_ms = s["kt_ms"][0], s["kt_rerank_ms"]
+    assert 0 < scan_ms / steps < 1.0 and 0 < rr_ms / steps < 1.0
+    assert scan_ms + rr_ms < wall_ms
+    assert 300 < s["kt_sm_mhz"][0] < 2500
+    tl = s["kt_last_us"]  # [kind][start, end], us after the earliest start
+    scan, rerank = (tl[0], tl[1]), (tl[8], tl[9])
+    assert scan[0] == 0.0 and scan[1] > 0
+    assert scan[1] <= rerank[0] < rerank[1]
+    assert s["kt_origin_ns"] > 0
+    assert np.isfinite(scan_ms)
