@@ -223,6 +223,10 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
     return cleanup(fail(VX_ERR_OOM, "pinned header"));
   if (cudaMallocHost((void**)&h->h_flags, B * 4) != cudaSuccess)
     return cleanup(fail(VX_ERR_OOM, "pinned flags"));
+  if (cudaMallocHost(&h->h_sync, 16 + sizeof(vx::KTimer) * vx::KT_N) != cudaSuccess)
+    return cleanup(fail(VX_ERR_OOM, "pinned sync mirror"));
+  if (cudaEventCreateWithFlags(&h->ev_done, cudaEventDisableTiming) != cudaSuccess)
+    return cleanup(fail(VX_ERR_CUDA, "event create"));
   if (cudaMemset(h->d_xnorm, 0, (8 + D) * 4) != cudaSuccess || cudaMemset(h->d_fcount, 0, 16) != cudaSuccess || cudaMemset(h->d_ctr, 0, 16) != cudaSuccess ||
       ktimer_reset(h) != VX_OK)
     return cleanup(fail(VX_ERR_CUDA, "memset"));
@@ -274,6 +278,8 @@ extern "C" vx_status vx_index_destroy(vx_index* h) {
   if (h->h_stage) cudaFreeHost(h->h_stage);
   if (h->h_hdr) cudaFreeHost(h->h_hdr);
   if (h->h_flags) cudaFreeHost(h->h_flags);
+  if (h->h_sync) cudaFreeHost(h->h_sync);
+  if (h->ev_done) cudaEventDestroy(h->ev_done);
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : h->gev)
@@ -581,8 +587,22 @@ static PFN_ptrAttr get_ptr_attr() {
   return fn;
 }
 
+// Ranges already verified (a few per thread: the callers' long-lived I/O buffers) skip the
+// three driver queries per buffer (~2 us each call, three buffers a batch).  A stale entry
+// (the allocation freed, the range reused as pageable memory) is harmless: cudaMemcpyAsync
+// stages pageable memory itself, and every host-API call synchronizes before returning.
+struct PinnedRange {
+  uintptr_t start = 0;
+  size_t size = 0;
+};
+static thread_local PinnedRange t_pinned[8];
+static thread_local int t_pinned_next = 0;
+
 static bool is_pinned(const void* p, size_t bytes) {
   if (!p || !bytes) return false;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  for (const PinnedRange& r : t_pinned)
+    if (r.size && a >= r.start && a + bytes <= r.start + r.size) return true;
   cudaPointerAttributes at;
   if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
     cudaGetLastError();
@@ -599,7 +619,12 @@ static bool is_pinned(const void* p, size_t bytes) {
     return false;
   // the range is reported in the allocation's device address space; p's offset into it is
   // the same in host and device views
-  return (uint64_t)dp >= (uint64_t)start && (uint64_t)dp + bytes <= (uint64_t)start + size;
+  if (!((uint64_t)dp >= (uint64_t)start && (uint64_t)dp + bytes <= (uint64_t)start + size))
+    return false;
+  PinnedRange& r = t_pinned[t_pinned_next++ & 7];
+  r.start = a - (uintptr_t)((uint64_t)dp - (uint64_t)start);  // the allocation, host view
+  r.size = size;
+  return true;
 }
 
 // source of a batch upload: the caller's contiguous pinned buffer itself, else the rows

@@ -153,6 +153,10 @@ struct vx_index {
   cudaEvent_t* ev_start = ev;    // last batch: the array holding scan begin/end + stage begin
   cudaEvent_t* ev_end = ev;      //   ... and the one holding the stage end (read by vx_sync)
   cudaStream_t stream_last = nullptr;  // stream of the last batch's final part
+  cudaEvent_t ev_done = nullptr;       // recorded there when it is not `stream` (vx_sync waits)
+  bool done_pending = false;
+  void* h_sync = nullptr;              // pinned: vx_sync's copies of the certificate counters
+                                       // and the device timers (one async copy + one sync)
   cudaStream_t stream2 = nullptr;      // host API: query-token upload overlapping part 1
   cudaStream_t stream_cond = nullptr;  // captures the body of the certificate IF node
   cudaEvent_t tok_ev = nullptr;
