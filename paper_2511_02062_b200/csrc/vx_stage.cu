@@ -1038,9 +1038,8 @@ extern "C" vx_status vx_sync(vx_index* h) {
     h->done_pending = false;
   }
   uint8_t* hs = static_cast<uint8_t*>(h->h_sync);
-  CU_TRY(cudaMemcpyAsync(hs, h->d_fcount, 16, cudaMemcpyDeviceToHost, h->stream));
-  CU_TRY(cudaMemcpyAsync(hs + 16, h->d_ktimer, sizeof(vx::KTimer) * vx::KT_N,
-                         cudaMemcpyDeviceToHost, h->stream));
+  CU_TRY(cudaMemcpyAsync(hs, h->d_fcount, 16 + sizeof(vx::KTimer) * vx::KT_N,
+                         cudaMemcpyDeviceToHost, h->stream));  // counters + timers: adjacent
   CU_TRY(cudaStreamSynchronize(h->stream));
   if (h->timing_pending) {
     cudaEvent_t* E = h->ev_start;
