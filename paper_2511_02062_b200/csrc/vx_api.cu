@@ -141,6 +141,7 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
   if (const char* e = getenv("VX_DEBUG_TC_STAGES")) h->dbg_tc_stages = atoi(e);
   if (const char* e = getenv("VX_DEBUG_NO_REP")) h->dbg_no_rep = atoi(e);
   if (const char* e = getenv("VX_DEBUG_SEED_M")) h->dbg_seed_m = std::min(32, std::max(1, atoi(e)));
+  if (const char* e = getenv("VX_DEBUG_SEED_STRIDE")) h->dbg_seed_stride = std::min(1024, std::max(8, atoi(e)));
   if (cudaSetDevice(h->device) != cudaSuccess) return cleanup(fail(VX_ERR_CUDA, "cudaSetDevice"));
   if (h->n_local < 1) return cleanup(fail(VX_ERR_INVALID, "empty shard"));
 #define ALLOC(ptr, bytes)                                                              \

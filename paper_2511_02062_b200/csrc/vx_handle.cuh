@@ -95,6 +95,7 @@ struct vx_index {
   int kprime = 0;                // TC candidate set size k' (0 = auto; VX_OPT_KPRIME)
   int dbg_tc_bits = 0;           // timing-experiment knobs, read once from the environment at
   int dbg_tc_stages = 0;         //   create: VX_DEBUG_TC_NOSELECT (bit mask), VX_DEBUG_TC_STAGES,
+  int dbg_seed_stride = 0;       //   VX_DEBUG_SEED_STRIDE (sample row stride, timing only)
   int dbg_seed_m = 0;            //   VX_DEBUG_SEED_M (sample rank of the scan seed, <= 32),
   int dbg_no_rep = 0;            //   VX_DEBUG_NO_REP (no small-batch query replication)
   int scan_seed = 1;             // seed the TC scan's admission thresholds (VX_OPT_SCAN_SEED)

@@ -210,7 +210,8 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
   // seed never enter a list; the re-rank certificate bounds them by the seed (rerank_kernel,
   // wide_select_kernel), so results are unchanged.  10M x 768 s8 B = 1024: scan 5.95 ->
   // 5.24 ms; one shard of 4 / 8: 1.89 -> 1.49, 1.18 -> 0.84 ms (seed_stage2.jsonl).
-  constexpr int kSeedStride = 64, kSeedLd = 32;
+  constexpr int kSeedLd = 32;
+  const int kSeedStride = h->dbg_seed_stride ? h->dbg_seed_stride : 64;
   const int kSeedM = h->dbg_seed_m ? h->dbg_seed_m : 32;
   const int64_t n_sample = h->n_local / kSeedStride;
   const bool seeded = h->scan_seed && n_sample >= 8192;
