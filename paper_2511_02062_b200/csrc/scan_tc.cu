@@ -816,13 +816,15 @@ __global__ void __launch_bounds__(256)
         const float4* x = reinterpret_cast<const float4*>(docs + (size_t)vx_key_id(ck) * D);
         float acc = 0.0f;
         const int nv = D >> 2;
-        for (int c0 = 0; c0 < nv; c0 += 8) {  // 8 loads in flight, then the in-order chain
-          float4 v[8];
+        // 24 loads in flight, then the in-order chain (8 left every row a chain of 24
+        // dependent gathers: 28-49 us for the 2-3 queries of a 10M-row batch)
+        for (int c0 = 0; c0 < nv; c0 += 24) {
+          float4 v[24];
 #pragma unroll
-          for (int u = 0; u < 8; ++u)
+          for (int u = 0; u < 24; ++u)
             if (c0 + u < nv) v[u] = __ldg(x + c0 + u);
 #pragma unroll
-          for (int u = 0; u < 8; ++u)
+          for (int u = 0; u < 24; ++u)
             if (c0 + u < nv) {
               const int c = c0 + u;
               acc = fmaf(v[u].x, qs[4 * c + 0], acc);
@@ -848,12 +850,13 @@ __global__ void __launch_bounds__(256)
                        uint64_t* __restrict__ out_keys, int64_t* __restrict__ out_ids,
                        float* __restrict__ out_scores, int* __restrict__ flags,
                        const uint64_t* __restrict__ seed, int seed_ld) {
-  extern __shared__ __align__(16) uint64_t keys[];  // [np2]
+  extern __shared__ __align__(16) uint64_t keys[];  // [Mmax (even)] staged keys + [kp2] top-k
   __shared__ float s_red[96];
   __shared__ unsigned long long s_t2;
   __shared__ int s_fail;
   const int n = *fcount;
   const int Mmax = P_single * kc;
+  uint64_t* sel = keys + ((Mmax + 1) & ~1);
   for (int i = blockIdx.x; i < n; i += gridDim.x) {
     const int b = fidx[i];
     const uint64_t* lists;
@@ -861,27 +864,14 @@ __global__ void __launch_bounds__(256)
     wide_lists(part_all, b, B, GS, P_pairs, P_single, kc, &lists, &P);
     const uint64_t t2 = wide_t2(lists, P, kc, &s_t2);
     const int M = P * kc;
-    int np2 = 16;
-    while (np2 < M) np2 <<= 1;
     const float sq = fmt == FMT_I8 ? qscale[b] : 1.0f;
     const float cscale = fmt == FMT_I8 ? sq * xstats[5] : 1.0f;
     query_norms(fq + (size_t)i * D, D, fmt, sq, nullptr, s_red, xstats);
-    for (int j = threadIdx.x; j < np2; j += blockDim.x)
-      keys[j] = j < M ? wkeys[(size_t)i * Mmax + j] : 0ull;
-    __syncthreads();
-    for (int size = 2; size <= np2; size <<= 1)
-      for (int stride = size >> 1; stride > 0; stride >>= 1) {
-        for (int t = threadIdx.x; t < (np2 >> 1); t += blockDim.x) {
-          int lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
-          bool desc = (lo & size) == 0;
-          uint64_t x0 = keys[lo], x1 = keys[hi];
-          if ((x0 < x1) == desc) {
-            keys[lo] = x1;
-            keys[hi] = x0;
-          }
-        }
-        __syncthreads();
-      }
+    // the k best exact keys, descending, into sel[0, k) (K3's radix select over the staged
+    // keys: a shared-memory bitonic sort of all next_pow2(M) keys took 52 us per launch at
+    // 10M x 768, profiles/r02/ncu_final/launches_bench.csv)
+    merge_topk_block(wkeys + (size_t)i * Mmax, M, k, 0, sel, nullptr, nullptr, 0, k,
+                     (M & 1) == 0 && M <= kMergeSmemKeys ? keys : nullptr, sel);
     if (threadIdx.x == 0) {
       int fail = 0;
       // documents outside every list: coarse <= max(s(T''), seed) (seeded scan)
@@ -890,7 +880,7 @@ __global__ void __launch_bounds__(256)
         float qn, qh, qr;
         query_norms_final(s_red, fmt, &qn, &qh, &qr);
         const float E = cert_err_bound(fmt, D, qn, qh, qr, xstats);
-        const uint64_t ek = k <= np2 ? keys[k - 1] : 0ull;
+        const uint64_t ek = sel[k - 1];
         fail = (ek == 0ull || !(vx_key_score(ek) > cb * cscale + E)) ? 1 : 0;
       }
       s_fail = fail;
@@ -899,7 +889,7 @@ __global__ void __launch_bounds__(256)
     __syncthreads();
     if (!s_fail) {  // else the exact re-scan writes this query
       for (int j = threadIdx.x; j < k; j += blockDim.x) {
-        const uint64_t key = j < np2 ? keys[j] : 0ull;
+        const uint64_t key = sel[j];
         const size_t o = (size_t)b * k + j;
         if (key == 0ull) {
           out_keys[o] = 0ull;
@@ -977,9 +967,9 @@ cudaError_t launch_rerank_wide(const float* docs, const float* fq, int D, const 
                                float* out_scores, int* flags, cudaStream_t st,
                                const uint64_t* seed, int seed_ld) {
   const int M = P_single * kc;
-  int np2 = 16;
-  while (np2 < M) np2 <<= 1;
-  const size_t smem = (size_t)np2 * 8;
+  int kp2 = 16;
+  while (kp2 < k) kp2 <<= 1;
+  const size_t smem = ((size_t)((M + 1) & ~1) + kp2) * 8;  // staged keys + the top-k
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(wide_select_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
