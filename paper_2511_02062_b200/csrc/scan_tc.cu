@@ -450,7 +450,10 @@ __device__ __forceinline__ void query_norms_final(const float* red, int fmt, flo
 //   phase 0: head + tail in one launch (one shard);
 //   phase 1: head only — exact head keys to hkeys[b][k], their scores to lb[b][k];
 //   phase 2: tail, from hkeys and tau.
-// two CTAs per SM (the staging stream is sized for it): at most 128 registers
+// two CTAs per SM (the staging stream is sized for it): at most 128 registers.  (Three per
+// SM — launch bounds 256 x 3 fit in 80 registers without spills — with the staging cut to
+// 72 KB per CTA was slower at every split: 0.70-0.86 vs 0.62 ms per 1024-query launch,
+// profiles/r02/rerank/three_per_sm.txt.)
 __global__ void __launch_bounds__(256, 2)
     rerank_kernel(const float* __restrict__ docs, const float* __restrict__ qv, int D,
                   uint64_t* __restrict__ cand, int kp, const uint64_t* __restrict__ part,
