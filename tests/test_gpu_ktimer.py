@@ -44,3 +44,37 @@ def test_ktimers_count_and_order(vxlib, graphs):
     assert scan[1] <= rerank[0] < rerank[1]
     assert s["kt_origin_ns"] > 0
     assert np.isfinite(scan_ms)
+
+
+def test_sync_waits_for_the_callers_stream(vxlib):
+    """vx_sync after a *_dev call on a caller's stream (no caller-side synchronize): it waits
+    for that stream's work (an event recorded there) and the stats it returns count every
+    launch; the direct-I/O graph's outputs are final when it returns."""
+    import torch
+    import paper_2511_02062_b200 as vx
+    from paper_2511_02062_b200 import synth
+    N, D, B, k, steps = 100_000, 768, 16, 10, 5
+    dev = torch.device("cuda", 0)
+    Q = synth.queries(B, D)
+    q = torch.from_numpy(Q).to(dev)
+    ids = torch.empty((B, k), dtype=torch.int64, device=dev)
+    ip = torch.empty((B, k), dtype=torch.float32, device=dev)
+    st = torch.cuda.Stream(dev)
+    with vx.Index(N, D, max_batch=B, max_k=k) as idx:
+        idx.synth(42)
+        idx.set_option(vx.VX_OPT_GRAPHS, 1)
+        want_ids, want_ip = idx.search(Q, k)
+        for _ in range(3):  # first sighting eager, then the captured direct-I/O graph
+            idx.search_dev(q, ids, ip, k, stream=st.cuda_stream)
+        idx.sync()
+        idx.reset_stats()
+        for _ in range(steps):
+            with torch.cuda.stream(st):
+                ids.fill_(-7)
+            idx.search_dev(q, ids, ip, k, stream=st.cuda_stream)
+        idx.sync()  # no torch synchronize before it
+        got_ids, got_ip = ids.cpu().numpy(), ip.cpu().numpy()
+        s = idx.stats()
+    assert s["kt_launches"][0] == steps and s["kt_rerank_launches"] == steps
+    assert s["graph_replays"] == steps
+    assert np.array_equal(got_ids, want_ids) and np.array_equal(got_ip, want_ip)
