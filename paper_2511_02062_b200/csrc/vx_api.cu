@@ -141,6 +141,7 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
   if (const char* e = getenv("VX_DEBUG_TC_STAGES")) h->dbg_tc_stages = atoi(e);
   if (const char* e = getenv("VX_DEBUG_NO_REP")) h->dbg_no_rep = atoi(e);
   if (const char* e = getenv("VX_DEBUG_SEED_M")) h->dbg_seed_m = std::min(32, std::max(1, atoi(e)));
+  if (getenv("VX_DEBUG_NO_SEED")) h->scan_seed = 0;  // timing experiments only
   if (const char* e = getenv("VX_DEBUG_SEED_STRIDE")) h->dbg_seed_stride = std::min(1024, std::max(8, atoi(e)));
   if (cudaSetDevice(h->device) != cudaSuccess) return cleanup(fail(VX_ERR_CUDA, "cudaSetDevice"));
   if (h->n_local < 1) return cleanup(fail(VX_ERR_INVALID, "empty shard"));
@@ -198,12 +199,15 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
   // D % 64 == 0; otherwise the coarse scan reads the fp32 rows as TF32 (32-wide chunks)
   if (!(d->flags & VX_FLAG_NO_BF16_SHADOW) && D % 64 == 0) {
     ALLOC(h->docs16, (size_t)h->n_local * D * 2);
-    ALLOC(h->d_q16, B * D * 2);
+    // + kQueryPadRows rows: the scan's query tensor map always spans whole A tiles (rows past
+    // the batch are real memory, not TMA out-of-bounds fills — those made a 1-query 10M-row
+    // scan 1.58 ms against 1.10 ms at 16 queries; profiles/r02/small_batch/)
+    ALLOC(h->d_q16, (B + kQueryPadRows) * D * 2);
   }
   // s8 shadow: K-chunks of 128 s8, and |s32 dot| < 2^24 (exact fp32 keys) needs D <= 1024
   if (!(d->flags & VX_FLAG_NO_I8_SHADOW) && D % 128 == 0 && D <= 1024) {
     ALLOC(h->docs8, (size_t)h->n_local * D);
-    ALLOC(h->d_q8, B * D);
+    ALLOC(h->d_q8, (B + kQueryPadRows) * D);
     ALLOC(h->d_qs8, B * 4);
   }
 #undef ALLOC
@@ -230,6 +234,9 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
     return cleanup(fail(VX_ERR_OOM, "pinned sync mirror"));
   if (cudaEventCreateWithFlags(&h->ev_done, cudaEventDisableTiming) != cudaSuccess)
     return cleanup(fail(VX_ERR_CUDA, "event create"));
+  if ((h->d_q16 && cudaMemset(h->d_q16, 0, (size_t)(B + kQueryPadRows) * D * 2) != cudaSuccess) ||
+      (h->d_q8 && cudaMemset(h->d_q8, 0, (size_t)(B + kQueryPadRows) * D) != cudaSuccess))
+    return cleanup(fail(VX_ERR_CUDA, "memset"));
   if (cudaMemset(h->d_xnorm, 0, (8 + D) * 4) != cudaSuccess || cudaMemset(h->d_fcount, 0, 16) != cudaSuccess || cudaMemset(h->d_ctr, 0, 16) != cudaSuccess ||
       ktimer_reset(h) != VX_OK)
     return cleanup(fail(VX_ERR_CUDA, "memset"));

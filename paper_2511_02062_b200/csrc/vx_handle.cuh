@@ -199,6 +199,10 @@ struct vx_index {
   std::map<uint64_t, int> io_per_shape;
 };
 
+// rows allocated past max_batch in the coarse query buffers (d_q16 / d_q8): the scan's query
+// tensor maps span whole A tiles (<= 4 x 128 rows per pass)
+constexpr int kQueryPadRows = 512;
+
 static inline void count_launch(vx_index* h, int n = 1) { h->st.kernel_launches += n; }
 static inline bool has_tokens(const vx_index* h) { return h->tokens || h->tokens32; }
 
