@@ -1071,16 +1071,28 @@ cudaError_t launch_rerank(const float* docs, const float* q, int D, uint64_t* ca
     return e ? atoi(e) : -1;
   }();
   const int head_all = phase == 0 && B <= 64 ? 1 : 0;
+  // one wave with an SM per CTA (B <= the SM count): each CTA may take the whole shared
+  // memory, and twice the chain threads — a single query's 1024 rows were bound by 64 serial
+  // fmaf chains and 64 small bulk copies per item (B = 1: 121 -> 67 us, B = 16: 172 -> 125 us
+  // at 10M x 768 s8, profiles/r02/rerank/small_batch.txt)
+  static const int num_sms = [] {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+  }();
+  const bool sm_each = B <= num_sms;
   int NB = env_bufs >= 2 ? std::min(env_bufs, kRerankMaxBufs) : 2;
   int DC = env_dc > 0 && env_dc % 32 == 0 && D % env_dc == 0 ? env_dc : 192;
   while (DC > 32 && D % DC) DC -= 32;
-  int R = env_rows > 0 ? std::min(env_rows, 256) : 64;
+  int R = env_rows > 0 ? std::min(env_rows, 256) : (sm_each ? 128 : 64);
   static const int env_smem_kb = [] {
     const char* e = getenv("VX_DEBUG_RERANK_SMEM_KB");
     return e ? atoi(e) : 0;
   }();
   auto smem_of = [&](int r) { return base + (size_t)NB * r * (DC + 4) * 4; };
-  const size_t smem_cap = (size_t)(env_smem_kb > 0 ? std::min(env_smem_kb, 220) : 110) * 1024;
+  const size_t smem_cap =
+      (size_t)(env_smem_kb > 0 ? std::min(env_smem_kb, 220) : (sm_each ? 220 : 110)) * 1024;
   while (R > 16 && smem_of(R) > smem_cap) R -= 16;  // default: two CTAs per SM
   size_t smem = smem_of(R);
   // small batch, latency-bound: ALL k' whole rows in one burst of bulk copies and one wait
