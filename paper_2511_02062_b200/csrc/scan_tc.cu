@@ -621,9 +621,13 @@ __global__ void __launch_bounds__(256, 2)
   if (trc && threadIdx.x == 0) trc[4] = gtimer_ns();
   // L = the head's minimum exact score (a bound on the exact k-th once k heads exist); also
   // its smallest key, for the final selection
+  // (over the first k candidates only — the k best coarse ones, cand is descending — so that
+  // with the whole candidate set as the head (small batch) the selection below still sees
+  // ~k + a few survivors, not all k')
+  const int kl = kh < k ? kh : k;
   float m = INFINITY;
   uint64_t mk = ~0ull;
-  for (int i = threadIdx.x; i < kh; i += blockDim.x) {
+  for (int i = threadIdx.x; i < kl; i += blockDim.x) {
     m = fminf(m, keys[i] ? vx_key_score(keys[i]) : -INFINITY);
     mk = keys[i] < mk ? keys[i] : mk;
   }
@@ -647,7 +651,7 @@ __global__ void __launch_bounds__(256, 2)
   if (kh < k) L = -INFINITY;
   // the final top-k are all >= the smallest head key when the head holds k real keys (k keys
   // are >= it); otherwise every real key stays in the running
-  const uint64_t sel_floor = (kh >= k && mk != 0ull) ? mk : 1ull;
+  const uint64_t sel_floor = (kl >= k && mk != 0ull) ? mk : 1ull;
   const float tb = tau ? tau[b] : -INFINITY;
   const float lim = fmaxf(L, tb) - E;
   int kpe = kp;  // candidates re-ranked: the prefix with cscale c >= lim
