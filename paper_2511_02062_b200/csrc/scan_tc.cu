@@ -476,7 +476,8 @@ __global__ void __launch_bounds__(256, 2)
   __shared__ float s_min[8];
   __shared__ int s_fail;
   __shared__ __align__(8) uint64_t s_bar[kRerankMaxBufs];
-  const int b = blockIdx.x;
+  const int S = fz.split;  // CTAs per query (RerankFuse::split)
+  const int b = blockIdx.x / S, sidx = blockIdx.x - b * S;
   const float* q = qv + (size_t)b * D;
   // coarse keys are in the coarse pass's units: the s8 pass scores sq * sx * (s32 dot)
   const float sq = fmt == FMT_I8 ? qscale[b] : 1.0f;
@@ -606,6 +607,27 @@ __global__ void __launch_bounds__(256, 2)
   };
   if (phase == 2) {
     for (int i = threadIdx.x; i < kh; i += blockDim.x) keys[i] = hkeys[(size_t)b * k + i];
+    __syncthreads();
+  } else if (S > 1) {
+    // split head: this CTA's slice to ekeys; the query's last CTA continues with all of them
+    const int j0 = (int)((int64_t)kh * sidx / S), j1 = (int)((int64_t)kh * (sidx + 1) / S);
+    rescore(j0, j1);
+    uint64_t* ek = fz.ekeys + (size_t)b * kp;
+    for (int i = j0 + threadIdx.x; i < j1; i += blockDim.x) ek[i] = keys[i];
+    __shared__ int s_lastq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();  // this slice before the ticket
+      s_lastq = atomicAdd(fz.qctr + b, 1u) == (unsigned)(S - 1);
+    }
+    __syncthreads();
+    if (!s_lastq) {
+      ktimer_end(fz.ktimer, kt_c0, kt_g0);
+      return;
+    }
+    __threadfence();  // every slice (each fenced before its ticket)
+    for (int i = threadIdx.x; i < kh; i += blockDim.x) keys[i] = ek[i];
+    if (threadIdx.x == 0) fz.qctr[b] = 0u;  // re-armed for the next launch (graph replays)
     __syncthreads();
   } else {
     rescore(0, kh);
@@ -749,7 +771,7 @@ __global__ void __launch_bounds__(256, 2)
     __shared__ int s_last;
     if (threadIdx.x == 0) {
       __threadfence();  // this CTA's flag before its ticket
-      s_last = atomicAdd(fz.ctr, 1u) == gridDim.x - 1;
+      s_last = atomicAdd(fz.ctr, 1u) == gridDim.x / S - 1;  // one finishing CTA per query
     }
     __syncthreads();
     if (s_last) {
@@ -877,7 +899,7 @@ __global__ void __launch_bounds__(256)
     // the k best exact keys, descending, into sel[0, k) (K3's radix select over the staged
     // keys: a shared-memory bitonic sort of all next_pow2(M) keys took 52 us per launch at
     // 10M x 768, profiles/r02/ncu_final/launches_bench.csv)
-    merge_topk_block(wkeys + (size_t)i * Mmax, M, k, 0, sel, nullptr, nullptr, 0, k,
+    merge_topk_block<1>(wkeys + (size_t)i * Mmax, M, k, 0, sel, nullptr, nullptr, 0, k,
                      (M & 1) == 0 && M <= kMergeSmemKeys ? keys : nullptr, sel);
     if (threadIdx.x == 0) {
       int fail = 0;
@@ -1075,6 +1097,9 @@ cudaError_t launch_rerank(const float* docs, const float* q, int D, uint64_t* ca
     return e ? atoi(e) : -1;
   }();
   const int head_all = phase == 0 && B <= 64 ? 1 : 0;
+  const int S = fz.split > 1 && head_all && !fz.mlists ? fz.split : 1;
+  if (fz.split > 1 && S == 1) return cudaErrorInvalidValue;  // split needs the standalone merge
+  const int kslice = (kp + S - 1) / S;  // candidates one CTA re-scores (whole-set head)
   // one wave with an SM per CTA (B <= the SM count): each CTA may take the whole shared
   // memory, and twice the chain threads — a single query's 1024 rows were bound by 64 serial
   // fmaf chains and 64 small bulk copies per item (B = 1: 121 -> 67 us, B = 16: 172 -> 125 us
@@ -1085,7 +1110,7 @@ cudaError_t launch_rerank(const float* docs, const float* q, int D, uint64_t* ca
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     return n > 0 ? n : 148;
   }();
-  const bool sm_each = B <= num_sms;
+  const bool sm_each = B * S <= num_sms;
   int NB = env_bufs >= 2 ? std::min(env_bufs, kRerankMaxBufs) : 2;
   int DC = env_dc > 0 && env_dc % 32 == 0 && D % env_dc == 0 ? env_dc : 192;
   while (DC > 32 && D % DC) DC -= 32;
@@ -1103,11 +1128,11 @@ cudaError_t launch_rerank(const float* docs, const float* q, int D, uint64_t* ca
   // (one round, one chunk), instead of the chunk stream
   // (Four 192-float chunks on four barriers instead, so the chains could start on the first
   // quarter, took the 100K-row B = 16 head from 4.0 to 7.9 us: four times the bulk copies.)
-  if (head_all && env_dc == 0 && base + (size_t)kp * (D + 4) * 4 <= 220 * 1024) {
+  if (head_all && env_dc == 0 && base + (size_t)kslice * (D + 4) * 4 <= 220 * 1024) {
     DC = D;
-    R = kp;
+    R = kslice;
     NB = 2;  // one item: only buffer 0
-    smem = base + (size_t)kp * (D + 4) * 4;
+    smem = base + (size_t)kslice * (D + 4) * 4;
   }
   // L2 prefetch distance in items beyond the staging window (packed into nbuf's high bits)
   const int PF = head_all ? 0 : std::min(env_pf >= 0 ? env_pf : 0, 15);
@@ -1123,7 +1148,7 @@ cudaError_t launch_rerank(const float* docs, const float* q, int D, uint64_t* ca
   // more than the launch latency they hide), and within noise on the 10M-row stage.
   static const bool no_pdl = getenv("VX_PDL") == nullptr || getenv("VX_DEBUG_NO_PDL") != nullptr;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(B);
+  cfg.gridDim = dim3(B * S);
   cfg.blockDim = dim3(256);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;

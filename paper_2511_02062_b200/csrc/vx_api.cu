@@ -195,6 +195,7 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
   ALLOC(h->d_fcount, 16 + sizeof(vx::KTimer) * vx::KT_N);
   h->d_ktimer = reinterpret_cast<vx::KTimer*>(reinterpret_cast<uint8_t*>(h->d_fcount) + 16);
   ALLOC(h->d_ctr, 16);
+  ALLOC(h->d_qctr, (size_t)B * 4);
   // bf16 shadow for the coarse scan: K-chunks of 64 bf16 (one 128-byte swizzle atom), so
   // D % 64 == 0; otherwise the coarse scan reads the fp32 rows as TF32 (32-wide chunks)
   if (!(d->flags & VX_FLAG_NO_BF16_SHADOW) && D % 64 == 0) {
@@ -237,7 +238,7 @@ extern "C" vx_status vx_index_create(const vx_index_desc* d, vx_index** out) {
   if ((h->d_q16 && cudaMemset(h->d_q16, 0, (size_t)(B + kQueryPadRows) * D * 2) != cudaSuccess) ||
       (h->d_q8 && cudaMemset(h->d_q8, 0, (size_t)(B + kQueryPadRows) * D) != cudaSuccess))
     return cleanup(fail(VX_ERR_CUDA, "memset"));
-  if (cudaMemset(h->d_xnorm, 0, (8 + D) * 4) != cudaSuccess || cudaMemset(h->d_fcount, 0, 16) != cudaSuccess || cudaMemset(h->d_ctr, 0, 16) != cudaSuccess ||
+  if (cudaMemset(h->d_xnorm, 0, (8 + D) * 4) != cudaSuccess || cudaMemset(h->d_fcount, 0, 16) != cudaSuccess || cudaMemset(h->d_ctr, 0, 16) != cudaSuccess || cudaMemset(h->d_qctr, 0, (size_t)B * 4) != cudaSuccess ||
       ktimer_reset(h) != VX_OK)
     return cleanup(fail(VX_ERR_CUDA, "memset"));
   if (h->tokens) {
@@ -282,7 +283,7 @@ extern "C" vx_status vx_index_destroy(vx_index* h) {
                   h->d_out_ms, h->d_send, h->d_recv, h->d_hdr, h->d_ckeys, h->d_seedk, h->d_flags,
                   h->d_xnorm, h->d_fq, h->docs16, h->d_q16, h->d_fidx, h->d_fcount,
                   h->d_qtok16, h->docs8, h->d_q8, h->d_qs8, h->d_lball, h->d_tau, h->d_hkeys,
-                  h->d_colmax, h->d_ctr};  // (d_ktimer lives in d_fcount's allocation)
+                  h->d_colmax, h->d_ctr, h->d_qctr};  // (d_ktimer lives in d_fcount's allocation)
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->h_stage) cudaFreeHost(h->h_stage);

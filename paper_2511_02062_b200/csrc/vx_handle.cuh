@@ -127,6 +127,7 @@ struct vx_index {
   uint64_t* d_hkeys = nullptr;   // [maxB][maxK] exact keys of the re-rank head (G > 1)
   int32_t* d_hdr = nullptr;      // [4]
   uint64_t* d_ckeys = nullptr;   // [maxB][1024] merged coarse keys (TC path)
+  unsigned* d_qctr = nullptr;     // [maxB] split re-rank: per-query CTA tickets (kept at 0)
   uint64_t* d_seedk = nullptr;   // [maxB][32] best sample keys per query (TC scan seeds)
   int* d_flags = nullptr;        // [maxB] certificate failures (TC path)
   unsigned int* d_xnorm = nullptr;  // [8] shard maxima (float bits, row_stats): |x|, |bf16 x|,

@@ -150,6 +150,13 @@ struct RerankFuse {
   unsigned long long cond = 0;
   int use_cond = 0;
   KTimer* ktimer = nullptr;
+  // small batch, whole candidate set as the head (phase 0): S CTAs per query, CTA s re-scores
+  // candidates [s k'/S, (s+1) k'/S) into ekeys[b][k'] (global); the query's last CTA to
+  // finish (qctr[b] ticket, re-armed to 0) loads them and selects / certifies / writes.
+  // The merge is then a launch of its own (every CTA reads the sorted candidates).
+  int split = 1;
+  uint64_t* ekeys = nullptr;
+  unsigned* qctr = nullptr;
   uint64_t* trace = nullptr;  // timing experiments only (VX_DEBUG_RERANK_TRACE): per CTA 8
                               // %globaltimer stamps (entry, norms, dependency, merge, head,
                               // tail, sort, end)

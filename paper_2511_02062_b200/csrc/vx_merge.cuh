@@ -47,6 +47,10 @@ constexpr int kMergeFilterKeys = 512;  // standalone merge: the sorted-list filt
 // took ~17 K cycles for 2368 keys -> 64) and no sort (T0 and the C keys were two bitonic sorts:
 // 5 K + 3.7 K of the filter's 13.6 K cycles; profiles/microbench/merge_bench.cu).  Otherwise
 // (C too large, or T0 = 0: short lists) the radix select below runs as before.
+// Inst: a separate instantiation per call site family (the fused re-rank keeps its own copy:
+// one non-inlined body shared with a kernel of a larger register budget raised the re-rank
+// from 80 to 116 registers)
+template <int Inst = 0>
 static __device__ __noinline__ void merge_topk_block(const uint64_t* __restrict__ L, int M, int k, int64_t id_base,
                                  uint64_t* __restrict__ out_keys, int64_t* __restrict__ out_ids,
                                  float* __restrict__ out_scores, size_t row, int64_t ldout,

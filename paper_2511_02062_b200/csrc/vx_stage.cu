@@ -393,7 +393,16 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
   // still reach the GLOBAL top-k
   const bool sharded = h->nranks > 1;
   static const bool no_fuse = getenv("VX_DEBUG_NO_FUSE_MERGE") != nullptr;  // A/B timing only
-  const bool fuse_merge = !no_fuse && (int64_t)h->grid * KC <= vx::kMergeSmemKeys;
+  // small batch (the whole candidate set is the head, launch_rerank: B <= 64) with a large
+  // k': S CTAs per query, one wave — a single CTA per query was bound by its serial chains
+  // and small bulk copies (B = 1: 1024 rows in one CTA, 69 us of a 97 us re-rank).  The merge
+  // then runs as its own launch (every CTA of a query reads the sorted candidates).
+  static const bool no_split = getenv("VX_DEBUG_NO_RERANK_SPLIT") != nullptr;  // A/B only
+  int split = 1;
+  if (!sharded && !no_split && B <= 64 && kp >= 256 &&
+      (int64_t)h->desc.max_batch * h->grid * 224 >= (int64_t)B * kp)
+    split = std::max(1, std::min(16, h->num_sms / B));
+  const bool fuse_merge = !no_fuse && split == 1 && (int64_t)h->grid * KC <= vx::kMergeSmemKeys;
   if (!fuse_merge) VX_TRY(merge_lists(h->d_part, KC, kp, h->d_ckeys, kp));
   float* lb = reinterpret_cast<float*>(h->d_send);
   for (int pass = sharded ? 1 : 0; pass <= (sharded ? 2 : 0); ++pass) {
@@ -405,6 +414,11 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
       r1 = std::min(r1, B);
       vx::RerankFuse fz;
       fz.ktimer = ktimer_of(h, vx::KT_RERANK);
+      if (split > 1) {
+        fz.split = split;
+        fz.ekeys = h->d_part + (size_t)h->desc.max_batch * grid * 32;  // the level-2 scratch
+        fz.qctr = h->d_qctr;
+      }
       // G > 2 shards: each re-scores 2k/G head rows before the tau exchange instead of k (the
       // union of G x 2k/G head scores still holds k distinct exact scores, so tau stays a lower
       // bound of the global k-th; the local bound L is dropped and tau alone prunes the tail)
