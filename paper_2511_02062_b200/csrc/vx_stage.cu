@@ -402,7 +402,11 @@ static vx_status local_topk_tc(vx_index* h, const float* d_q, int B, int k, uint
   if (!sharded && !no_split && B <= 64 && kp >= 256 &&
       (int64_t)h->desc.max_batch * h->grid * 224 >= (int64_t)B * kp)
     split = std::max(1, std::min(16, h->num_sms / B));
-  const bool fuse_merge = !no_fuse && split == 1 && (int64_t)h->grid * KC <= vx::kMergeSmemKeys;
+  // (small batches take the merge as its own launch too: fused into the re-rank CTA, whose
+  // shared memory holds the whole candidate set, it took ~11 us of a 100K-row B = 16 step
+  // against ~5 us + a launch standalone — profiles/r02/rank/fuse_small_batch.txt)
+  const bool fuse_merge = !no_fuse && split == 1 && B > 64 &&
+                          (int64_t)h->grid * KC <= vx::kMergeSmemKeys;
   if (!fuse_merge) VX_TRY(merge_lists(h->d_part, KC, kp, h->d_ckeys, kp));
   float* lb = reinterpret_cast<float*>(h->d_send);
   for (int pass = sharded ? 1 : 0; pass <= (sharded ? 2 : 0); ++pass) {
